@@ -1,0 +1,139 @@
+/*
+ * hexfem_b200.h -- C ABI of the B200-native hexfem hot path (libhexfem_b200.so).
+ *
+ * Drop-in boundary for the reference package `hexfem` (/root/reference/pkg/src/hexfem).
+ * Every entry point is extern "C", takes plain pointers + sizes, is asynchronous on the
+ * given CUDA stream (`void *stream`, a cudaStream_t; NULL = legacy default stream) and
+ * returns an int status (HX_OK = 0).  Device-side failures (degenerate elements, index
+ * validation, fast-path limits) are reported through small caller-owned DEVICE words that
+ * the caller reads after synchronising, so no call here blocks the host.
+ *
+ * All device buffers are caller-owned (the reference's `out=` convention,
+ * integrate.py:93-99); scratch is a caller-provided workspace sized by the *_workspace_bytes
+ * queries.  The library allocates nothing.
+ *
+ * Reference interfaces replaced (file:line under /root/reference/pkg/src/hexfem/):
+ *   hx_stiffness_batch             element.py:213-245 stiffness_batch / integrate.py:84-131
+ *                                  ComputeBackend.run
+ *   hx_integrate_mesh              integrate.py:146-149 + 152-212 (gather + per-group run) fused
+ *                                  with assemble.py:86-93 connectivity_index_arrays
+ *   hx_connectivity_index_arrays   assemble.py:86-93
+ *   hx_mesh_csc_*                  assemble.py:152-239 DirectAssembler / assemble_direct, and
+ *                                  triplet_to_csc (assemble.py:110-140) on mesh triplets
+ *   hx_triplet_csc_*               assemble.py:110-149 triplet_to_csc + _check_indices
+ *   hx_partition_*                 (new) element-halo exchange plan for the multi-GPU path
+ */
+#ifndef HEXFEM_B200_H
+#define HEXFEM_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HX_ABI_VERSION 1
+
+/* Status codes (host return values).  The Python layer maps them onto the reference
+ * exception hierarchy (errors.py:4-59). */
+#define HX_OK 0
+#define HX_ERR_VALUE 1         /* ValueError: bad sizes / pointers (element.py:228-233)    */
+#define HX_ERR_CONFIG 2        /* ConfigurationError (errors.py:46-47)                     */
+#define HX_ERR_CUDA 3          /* CUDA runtime error; see hx_last_error()                  */
+#define HX_ERR_WORKSPACE 4     /* workspace smaller than the *_workspace_bytes query       */
+
+/* Bits of the device status word written by the assembly entry points. */
+#define HX_ST_DEG_OVERFLOW 1u  /* a node has more than HX_MAX_NODE_DEGREE incident elements */
+#define HX_ST_ROW_OVERFLOW 2u  /* a column has more than HX_MAX_COL_ROWS distinct rows      */
+#define HX_ST_REPEATED_NODE 4u /* an element lists the same node twice                     */
+#define HX_ST_BAD_INDEX 8u     /* index outside [0, dim) (MeshValidationError, assemble.py:146) */
+#define HX_ST_UPPER 16u        /* triplet above the diagonal (MeshValidationError, assemble.py:148) */
+/* DEG/ROW/REPEATED mean "mesh fast path not applicable": the caller re-runs the generic
+ * triplet path (hx_triplet_csc_*), which has no such limits. */
+
+#define HX_MAX_NODE_DEGREE 8
+#define HX_MAX_COL_ROWS 16
+
+/* Integration modes. */
+#define HX_MODE_EXACT 0 /* reference operation order, no FMA: bitwise equal to the reference */
+#define HX_MODE_FAST 1  /* FMA + restructured algebra: |d| <= 1e-12 * max|row| (documented)  */
+
+/* Lowest failing element of an integration call (DegenerateElementError fields,
+ * errors.py:21-40).  element = -1 when every element is valid.  Device memory. */
+typedef struct hx_fail_info {
+    int64_t element;     /* global element id (element_offset applied, element.py:237-244) */
+    int32_t gauss_point; /* 0..7, r slowest (element.py:116-121)                           */
+    int32_t reserved;
+    double det;          /* det(J) at that point (element.py:276-279)                      */
+} hx_fail_info;
+
+/* One contiguous run of elements (connectivity + packed values).  Segments passed to the
+ * hx_mesh_csc_* calls are concatenated in order and MUST be in ascending global element
+ * order: duplicate positions are summed in that order (assemble.py:115-117, 179-184). */
+typedef struct hx_elem_segment {
+    const int32_t *conn; /* (n_el, 8) global node ids, device */
+    const double *ke;    /* (n_el, 36) packed lower values, device (may be NULL for symbolic) */
+    int64_t n_el;
+} hx_elem_segment;
+
+/* ---- introspection (host only, no GPU needed) ------------------------------------------ */
+int hx_abi_version(void);
+const char *hx_last_error(void);
+/* _DN_AT_GP (element.py:126-130) as compiled into the kernels: out[gp*24 + d*8 + a]. */
+void hx_dn_table(double *out192);
+/* PACK_ROWS / PACK_COLS (element.py:59-62) as compiled into the kernels. */
+void hx_pack_tables(int32_t *rows36, int32_t *cols36);
+/* Number of streaming multiprocessors of the current device (0 when no device). */
+int hx_device_sm_count(void);
+
+/* ---- numerical integration (Alg. 2) ----------------------------------------------------- */
+/* element.py:213-245: coords (n,8,3) f64 pre-gathered, coeff (n,) f64 -> out (n,36) f64.
+ * fail->element is batch-local (0-based); the caller adds element_offset. */
+int hx_stiffness_batch(const double *coords, const double *coeff, int64_t n, double *out,
+                       int32_t mode, hx_fail_info *fail, void *stream);
+
+/* integrate_all for elements [lo, hi) straight from the device-resident mesh: no host
+ * gather (integrate.py:146-149 disappears).  coords (n_nodes,3) f64, conn (n_el,8) i32,
+ * coeff (n_el,) f64.  Writes ke (hi-lo, 36) and, when rows/cols are non-NULL, the fused
+ * iK/jK triplet indices (36*(hi-lo),) i32 each (assemble.py:86-93).  fail->element is a
+ * global element id. */
+int hx_integrate_mesh(const double *coords, int64_t n_nodes, const int32_t *conn,
+                      const double *coeff, int64_t lo, int64_t hi, double *ke, int32_t *rows,
+                      int32_t *cols, int32_t mode, hx_fail_info *fail, void *stream);
+
+/* assemble.py:86-93 alone: rows/cols (36*(hi-lo),) i32 for elements [lo, hi). */
+int hx_connectivity_index_arrays(const int32_t *conn, int64_t lo, int64_t hi, int32_t *rows,
+                                 int32_t *cols, void *stream);
+
+/* ---- mesh-path assembly (node-adjacency symbolic + deterministic column numeric) ---------
+ * Builds the lower-triangular CSC block for columns [col_lo, col_hi) of a mesh with
+ * n_nodes nodes, from element segments in ascending global element order.
+ *   symbolic: writes col_ptr (col_hi-col_lo+1) i64, col_ptr[0] = 0; nnz = col_ptr[last].
+ *   numeric:  writes row_idx (nnz) i64 and vals (nnz) f64, summing duplicates in element
+ *             order with numpy add.reduceat's rule (bitwise equal to assemble.py:135).
+ * The workspace written by symbolic must be passed unchanged to numeric. */
+int64_t hx_mesh_csc_workspace_bytes(int64_t n_el_total, int64_t n_cols);
+int hx_mesh_csc_symbolic(const hx_elem_segment *segs, int32_t n_segs, int64_t n_nodes,
+                         int64_t col_lo, int64_t col_hi, int64_t *col_ptr, void *workspace,
+                         int64_t workspace_bytes, uint32_t *status, void *stream);
+int hx_mesh_csc_numeric(const hx_elem_segment *segs, int32_t n_segs, int64_t col_lo,
+                        int64_t col_hi, const int64_t *col_ptr, int64_t *row_idx, double *vals,
+                        const void *workspace, uint32_t *status, void *stream);
+
+/* ---- generic triplet -> CSC (assemble.py:110-149) ----------------------------------------
+ * symbolic: validates (status bits BAD_INDEX / UPPER), stable-sorts by (col,row), finds the
+ *           duplicate runs and writes col_ptr (dim+1) i64 and row_idx (nnz) i64 where
+ *           nnz = col_ptr[dim] (row_idx must hold n entries: nnz <= n).
+ * numeric:  vals (n,) f64 -> out_vals (nnz,) f64 with numpy add.reduceat's summation rule
+ *           (v0 + pairwise(v[1:]), any run length). */
+int64_t hx_triplet_csc_workspace_bytes(int64_t n, int64_t dim);
+int hx_triplet_csc_symbolic(const int32_t *rows, const int32_t *cols, int64_t n, int64_t dim,
+                            int64_t *col_ptr, int64_t *row_idx, void *workspace,
+                            int64_t workspace_bytes, uint32_t *status, void *stream);
+int hx_triplet_csc_numeric(const double *vals, int64_t n, int64_t dim, const int64_t *col_ptr,
+                           double *out_vals, const void *workspace, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HEXFEM_B200_H */

@@ -1,0 +1,102 @@
+"""ctypes binding of libhexfem_b200.so (include/hexfem_b200.h).
+
+The library is loaded from the package tree (built in place by build.py / __graft_entry__.build).
+There is no fallback: if the library is missing or the device is unavailable, every compute
+entry point raises NativeLibraryError.  ctypes releases the GIL during foreign calls, so the
+overlapped integration mode can call the ABI from two host threads.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from pathlib import Path
+
+from .errors import ConfigurationError, NativeLibraryError
+
+LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libhexfem_b200.so"
+
+HX_OK, HX_ERR_VALUE, HX_ERR_CONFIG, HX_ERR_CUDA, HX_ERR_WORKSPACE = 0, 1, 2, 3, 4
+ST_DEG_OVERFLOW, ST_ROW_OVERFLOW, ST_REPEATED_NODE, ST_BAD_INDEX, ST_UPPER = 1, 2, 4, 8, 16
+ST_FASTPATH_LIMITS = ST_DEG_OVERFLOW | ST_ROW_OVERFLOW | ST_REPEATED_NODE
+MODE_EXACT, MODE_FAST = 0, 1
+MAX_SEGMENTS = 4
+
+# Every symbol declared in include/hexfem_b200.h (checked by tests/test_abi_cpu.py).
+EXPORTED = (
+    "hx_abi_version", "hx_last_error", "hx_dn_table", "hx_pack_tables", "hx_device_sm_count",
+    "hx_stiffness_batch", "hx_integrate_mesh", "hx_connectivity_index_arrays",
+    "hx_mesh_csc_workspace_bytes", "hx_mesh_csc_symbolic", "hx_mesh_csc_numeric",
+    "hx_triplet_csc_workspace_bytes", "hx_triplet_csc_symbolic", "hx_triplet_csc_numeric",
+)
+
+
+class HxFailInfo(ctypes.Structure):
+    _fields_ = [("element", ctypes.c_int64), ("gauss_point", ctypes.c_int32),
+                ("reserved", ctypes.c_int32), ("det", ctypes.c_double)]
+
+
+class HxElemSegment(ctypes.Structure):
+    _fields_ = [("conn", ctypes.c_void_p), ("ke", ctypes.c_void_p), ("n_el", ctypes.c_int64)]
+
+
+_lib = None
+
+
+def lib():
+    """Load (once) and return the native library; raises NativeLibraryError if absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not LIB_PATH.exists():
+        raise NativeLibraryError(
+            f"{LIB_PATH} not found: build it with `python -m paper_1501_04784_b200.build` "
+            "(there is no CPU fallback)")
+    try:
+        L = ctypes.CDLL(str(LIB_PATH))
+    except OSError as exc:  # pragma: no cover - broken build
+        raise NativeLibraryError(f"cannot load {LIB_PATH}: {exc}") from exc
+    P, I32, I64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64
+    sig = {
+        "hx_abi_version": ([], ctypes.c_int),
+        "hx_last_error": ([], ctypes.c_char_p),
+        "hx_dn_table": ([P], None),
+        "hx_pack_tables": ([P, P], None),
+        "hx_device_sm_count": ([], ctypes.c_int),
+        "hx_stiffness_batch": ([P, P, I64, P, I32, P, P], ctypes.c_int),
+        "hx_integrate_mesh": ([P, I64, P, P, I64, I64, P, P, P, I32, P, P], ctypes.c_int),
+        "hx_connectivity_index_arrays": ([P, I64, I64, P, P, P], ctypes.c_int),
+        "hx_mesh_csc_workspace_bytes": ([I64, I64], I64),
+        "hx_mesh_csc_symbolic": ([P, I32, I64, I64, I64, P, P, I64, P, P], ctypes.c_int),
+        "hx_mesh_csc_numeric": ([P, I32, I64, I64, P, P, P, P, P, P], ctypes.c_int),
+        "hx_triplet_csc_workspace_bytes": ([I64, I64], I64),
+        "hx_triplet_csc_symbolic": ([P, P, I64, I64, P, P, P, I64, P, P], ctypes.c_int),
+        "hx_triplet_csc_numeric": ([P, I64, I64, P, P, P, P], ctypes.c_int),
+    }
+    for name, (args, res) in sig.items():
+        fn = getattr(L, name)
+        fn.argtypes = args
+        fn.restype = res
+    _lib = L
+    return L
+
+
+def check(rc: int, what: str) -> None:
+    """Map an ABI status onto the reference exception hierarchy."""
+    if rc == HX_OK:
+        return
+    msg = (lib().hx_last_error() or b"").decode(errors="replace")
+    if rc == HX_ERR_VALUE:
+        raise ValueError(f"{what}: {msg}")
+    if rc == HX_ERR_CONFIG:
+        raise ConfigurationError(f"{what}: {msg}")
+    raise NativeLibraryError(f"{what} failed ({rc}): {msg}")
+
+
+def segments(parts) -> ctypes.Array:
+    """Build an hx_elem_segment[] from (conn_ptr, ke_ptr, n_el) triples."""
+    arr = (HxElemSegment * len(parts))()
+    for i, (conn, ke, n) in enumerate(parts):
+        arr[i].conn = conn
+        arr[i].ke = ke
+        arr[i].n_el = n
+    return arr

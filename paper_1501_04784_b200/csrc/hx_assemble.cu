@@ -1,0 +1,401 @@
+// hx_assemble.cu -- on-GPU lower-triangular CSC assembly for hex8 meshes (the paper's CPU
+// sparse()/sparse_create step, assemble.py:110-239), node-adjacency based:
+//
+//   symbolic  1. degree count   deg[c]   = #incident (element, local node) pairs     (atomics)
+//             2. adj_ptr        = exclusive scan(deg)                                 (CUB)
+//             3. adjacency fill adj[adj_ptr[c] + slot] = (e << 3) | a                 (atomics)
+//             4. column count   cnt[c]   = #distinct rows r >= c over incident elements
+//             5. col_ptr        = exclusive scan(cnt) (int64)                         (CUB)
+//   numeric   6. column fill    per column: incident elements in ascending element order,
+//                               rows sorted ascending, duplicates summed in element order
+//                               with numpy add.reduceat's rule v0 + (((v1+v2)+v3)+...)
+//
+// Column c of the lower triangle holds rows {g_b : e incident to c, g_b >= c}; its triplet
+// contributions are exactly the packed entries p = tri(max(a,b), min(a,b)) of the incident
+// elements (a = local index of c).  Each thread owns one column; the incident list is sorted in
+// registers (ascending element id = the stable-sort order of assemble.py:125), the distinct
+// rows are kept as a sorted list in shared memory, and each row keeps (v0, running tail sum)
+// so the float result is bitwise equal to np.add.reduceat over the lexsorted triplets.
+//
+// Fast-path limits (reported through the status word, the caller then uses the generic
+// triplet path which has none): node degree <= HX_MAX_NODE_DEGREE (8: hex meshes with
+// regular vertices), distinct rows per column <= HX_MAX_COL_ROWS, no repeated node in an
+// element.  With degree <= 8 every duplicate run has <= 8 terms, where numpy's pairwise sum
+// degenerates to the sequential sum implemented here.
+#include <cub/device/device_scan.cuh>
+#include <cub/iterator/transform_input_iterator.cuh>
+
+#include <algorithm>
+
+#include "hx_common.cuh"
+
+namespace hx {
+
+constexpr int COL_BLOCK = 128;
+constexpr int MAXDEG = HX_MAX_NODE_DEGREE;
+constexpr int MAXR = HX_MAX_COL_ROWS;
+constexpr int MAX_SEGS = 4;
+
+struct SegTable {
+    const int32_t *conn[MAX_SEGS];
+    const double *ke[MAX_SEGS];
+    int64_t start[MAX_SEGS + 1];  // combined element index where segment s starts
+    int n;
+};
+
+__device__ __forceinline__ int seg_of(const SegTable &T, int64_t e) {
+    int s = 0;
+#pragma unroll
+    for (int q = 1; q < MAX_SEGS; ++q) s += (q < T.n && e >= T.start[q]) ? 1 : 0;
+    return s;
+}
+
+__device__ __forceinline__ void load_conn8(const int32_t *__restrict__ conn, int64_t e, int32_t (&g)[8]) {
+    const int4 *c4 = reinterpret_cast<const int4 *>(conn) + 2 * e;
+    const int4 lo = __ldg(c4), hi = __ldg(c4 + 1);
+    g[0] = lo.x; g[1] = lo.y; g[2] = lo.z; g[3] = lo.w;
+    g[4] = hi.x; g[5] = hi.y; g[6] = hi.z; g[7] = hi.w;
+}
+
+// 1. degree count over columns [col_lo, col_hi); also validates node ids against [0, n_nodes).
+__global__ void degree_kernel(SegTable T, int64_t n_total, int64_t n_nodes, int64_t col_lo, int64_t col_hi,
+                              int32_t *__restrict__ deg, uint32_t *__restrict__ status) {
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n_total;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int s = seg_of(T, e);
+        int32_t g[8];
+        load_conn8(T.conn[s], e - T.start[s], g);
+        bool bad = false;
+#pragma unroll
+        for (int a = 0; a < 8; ++a) {
+            const int32_t v = g[a];
+            bad |= (v < 0) | ((int64_t)v >= n_nodes);
+            if (v >= col_lo && v < col_hi) atomicAdd(deg + (v - col_lo), 1);
+        }
+        if (bad) atomicOr(status, HX_ST_BAD_INDEX);
+    }
+}
+
+// 3. adjacency fill; entry = (combined element index << 3) | local node.
+__global__ void adjacency_fill_kernel(SegTable T, int64_t n_total, int64_t col_lo, int64_t col_hi,
+                                      const int32_t *__restrict__ adj_ptr, int32_t *__restrict__ cursor,
+                                      int32_t *__restrict__ adj) {
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n_total;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int s = seg_of(T, e);
+        int32_t g[8];
+        load_conn8(T.conn[s], e - T.start[s], g);
+#pragma unroll
+        for (int a = 0; a < 8; ++a) {
+            const int32_t v = g[a];
+            if (v >= col_lo && v < col_hi) {
+                const int64_t c = v - col_lo;
+                const int32_t pos = adj_ptr[c] + atomicAdd(cursor + c, 1);
+                adj[pos] = (int32_t)((e << 3) | a);
+            }
+        }
+    }
+}
+
+// Sorting network for 8 keys (19 compare-exchanges), padded with INT_MAX.
+__device__ __forceinline__ void cswap(int32_t &a, int32_t &b) {
+    const int32_t lo = min(a, b), hi = max(a, b);
+    a = lo;
+    b = hi;
+}
+__device__ __forceinline__ void sort8(int32_t (&v)[8]) {
+    cswap(v[0], v[1]); cswap(v[2], v[3]); cswap(v[4], v[5]); cswap(v[6], v[7]);
+    cswap(v[0], v[2]); cswap(v[1], v[3]); cswap(v[4], v[6]); cswap(v[5], v[7]);
+    cswap(v[1], v[2]); cswap(v[5], v[6]); cswap(v[0], v[4]); cswap(v[3], v[7]);
+    cswap(v[1], v[5]); cswap(v[2], v[6]);
+    cswap(v[1], v[4]); cswap(v[3], v[6]);
+    cswap(v[2], v[4]); cswap(v[3], v[5]);
+    cswap(v[3], v[4]);
+}
+
+// Sorted-unique insert into a per-thread list R[0..m) laid out [slot][COL_BLOCK] in smem
+// (thread-fastest: conflict-free for any per-thread slot).  Returns false on overflow.
+__device__ __forceinline__ bool insert_row(int32_t *R, int &m, int32_t v) {
+    int pos = 0;
+    while (pos < m && R[pos * COL_BLOCK] < v) ++pos;
+    if (pos < m && R[pos * COL_BLOCK] == v) return true;
+    if (m == MAXR) return false;
+    for (int q = m; q > pos; --q) R[q * COL_BLOCK] = R[(q - 1) * COL_BLOCK];
+    R[pos * COL_BLOCK] = v;
+    ++m;
+    return true;
+}
+
+__device__ __forceinline__ int find_row(const int32_t *R, int m, int32_t v) {
+    int lo = 0, hi = m;  // lower_bound; v is known to be present
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (R[mid * COL_BLOCK] < v) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
+
+// 4./6. per-column pass.  VALUES=false: write counts.  VALUES=true: write rows and sums.
+template <bool VALUES>
+__global__ void __launch_bounds__(COL_BLOCK)
+column_kernel(SegTable T, int64_t col_lo, int64_t ncols, const int32_t *__restrict__ adj_ptr,
+              const int32_t *__restrict__ adj, int32_t *__restrict__ counts,
+              const int64_t *__restrict__ col_ptr, int64_t *__restrict__ row_idx,
+              double *__restrict__ vals, uint32_t *__restrict__ status) {
+    __shared__ int32_t sR[MAXR * COL_BLOCK];
+    __shared__ double sV0[VALUES ? MAXR * COL_BLOCK : 1];
+    __shared__ double sS[VALUES ? MAXR * COL_BLOCK : 1];
+    const int t = threadIdx.x;
+    const int64_t cl = (int64_t)blockIdx.x * COL_BLOCK + t;
+    if (cl >= ncols) return;
+    const int32_t c = (int32_t)(col_lo + cl);
+    const int32_t beg = __ldg(adj_ptr + cl), end = __ldg(adj_ptr + cl + 1);
+    const int deg = end - beg;
+    if (deg > MAXDEG) {
+        atomicOr(status, HX_ST_DEG_OVERFLOW);
+        if (!VALUES) counts[cl] = 0;
+        return;
+    }
+    int32_t ent[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) ent[k] = k < deg ? __ldg(adj + beg + k) : INT32_MAX;
+    sort8(ent);
+#pragma unroll
+    for (int k = 1; k < 8; ++k) {
+        if (k < deg && (ent[k] >> 3) == (ent[k - 1] >> 3)) {
+            atomicOr(status, HX_ST_REPEATED_NODE);
+            if (!VALUES) counts[cl] = 0;
+            return;
+        }
+    }
+
+    int32_t *R = sR + t;
+    int m = 0;
+    bool ok = true;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        if (k < deg) {
+            const int64_t e = ent[k] >> 3;
+            const int s = seg_of(T, e);
+            int32_t g[8];
+            load_conn8(T.conn[s], e - T.start[s], g);
+#pragma unroll
+            for (int b = 0; b < 8; ++b)
+                if (g[b] >= c) ok &= insert_row(R, m, g[b]);
+        }
+    }
+    if (!ok) {
+        atomicOr(status, HX_ST_ROW_OVERFLOW);
+        if (!VALUES) counts[cl] = 0;
+        return;
+    }
+    if (!VALUES) {
+        counts[cl] = m;
+        return;
+    }
+
+    double *V0 = sV0 + t;
+    double *S = sS + t;
+    uint32_t has0 = 0, has1 = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        if (k < deg) {
+            const int64_t e = ent[k] >> 3;
+            const int a = ent[k] & 7;
+            const int s = seg_of(T, e);
+            const int64_t el = e - T.start[s];
+            int32_t g[8];
+            load_conn8(T.conn[s], el, g);
+            const double *kr = T.ke[s] + 36 * el;
+            double x[8];
+#pragma unroll
+            for (int b = 0; b < 8; ++b) {
+                const int hi_ = max(a, b), lo_ = min(a, b);
+                x[b] = g[b] >= c ? __ldg(kr + pack_index(hi_, lo_)) : 0.0;
+            }
+#pragma unroll
+            for (int b = 0; b < 8; ++b) {
+                if (g[b] >= c) {
+                    const int j = find_row(R, m, g[b]);
+                    const uint32_t bit = 1u << j;
+                    if (!(has0 & bit)) {
+                        V0[j * COL_BLOCK] = x[b];
+                        has0 |= bit;
+                    } else if (!(has1 & bit)) {
+                        S[j * COL_BLOCK] = x[b];
+                        has1 |= bit;
+                    } else {
+                        S[j * COL_BLOCK] = __dadd_rn(S[j * COL_BLOCK], x[b]);
+                    }
+                }
+            }
+        }
+    }
+    const int64_t base = col_ptr[cl];
+    for (int j = 0; j < m; ++j) {
+        const uint32_t bit = 1u << j;
+        const double v0 = V0[j * COL_BLOCK];
+        row_idx[base + j] = R[j * COL_BLOCK];
+        vals[base + j] = (has1 & bit) ? __dadd_rn(v0, S[j * COL_BLOCK]) : v0;
+    }
+}
+
+struct CastI64 {
+    __host__ __device__ int64_t operator()(int32_t v) const { return (int64_t)v; }
+};
+
+// Workspace layout (all offsets 256-B aligned):
+//   adj_ptr  (ncols+1) i32 | cursor/deg (ncols+1) i32 | counts (ncols+1) i32 |
+//   adj (8*n_total) i32 | cub temp
+struct MeshWs {
+    int32_t *adj_ptr, *deg, *counts, *adj;
+    void *cub_tmp;
+    size_t cub_bytes;
+    size_t total;
+};
+
+static size_t cub_scan_bytes(int64_t ncols) {
+    size_t b1 = 0, b2 = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, b1, (int32_t *)nullptr, (int32_t *)nullptr, (int)(ncols + 1));
+    auto it = cub::TransformInputIterator<int64_t, CastI64, const int32_t *>((const int32_t *)nullptr, CastI64());
+    cub::DeviceScan::ExclusiveSum(nullptr, b2, it, (int64_t *)nullptr, (int)(ncols + 1));
+    return std::max(b1, b2);
+}
+
+static MeshWs mesh_ws_layout(void *base, int64_t n_total, int64_t ncols) {
+    MeshWs w{};
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        const size_t o = off;
+        off = align_up(off + bytes, 256);
+        return o;
+    };
+    const size_t o_ptr = take(sizeof(int32_t) * (ncols + 1));
+    const size_t o_deg = take(sizeof(int32_t) * (ncols + 1));
+    const size_t o_cnt = take(sizeof(int32_t) * (ncols + 1));
+    const size_t o_adj = take(sizeof(int32_t) * 8 * std::max<int64_t>(n_total, 1));
+    w.cub_bytes = cub_scan_bytes(ncols);
+    const size_t o_cub = take(w.cub_bytes);
+    w.total = off;
+    char *b = (char *)base;
+    if (b) {
+        w.adj_ptr = (int32_t *)(b + o_ptr);
+        w.deg = (int32_t *)(b + o_deg);
+        w.counts = (int32_t *)(b + o_cnt);
+        w.adj = (int32_t *)(b + o_adj);
+        w.cub_tmp = b + o_cub;
+    }
+    return w;
+}
+
+static int make_segtable(const hx_elem_segment *segs, int32_t n_segs, SegTable &T, int64_t &n_total,
+                         bool need_ke) {
+    if (n_segs < 1 || n_segs > MAX_SEGS || segs == nullptr) {
+        set_last_error("mesh csc: need 1..%d element segments, got %d", MAX_SEGS, n_segs);
+        return HX_ERR_VALUE;
+    }
+    T = SegTable{};
+    T.n = n_segs;
+    int64_t acc = 0;
+    for (int s = 0; s < n_segs; ++s) {
+        if (segs[s].n_el < 0 || (segs[s].n_el > 0 && segs[s].conn == nullptr) ||
+            (need_ke && segs[s].n_el > 0 && segs[s].ke == nullptr)) {
+            set_last_error("mesh csc: bad element segment %d", s);
+            return HX_ERR_VALUE;
+        }
+        T.conn[s] = segs[s].conn;
+        T.ke[s] = segs[s].ke;
+        T.start[s] = acc;
+        acc += segs[s].n_el;
+    }
+    for (int s = n_segs; s <= MAX_SEGS; ++s) T.start[s] = acc;
+    n_total = acc;
+    if (8 * n_total >= (int64_t)INT32_MAX) {
+        set_last_error("mesh csc: %lld elements exceed the int32 adjacency of one plan; shard the mesh",
+                       (long long)n_total);
+        return HX_ERR_CONFIG;
+    }
+    return HX_OK;
+}
+
+static unsigned grid_for(int64_t n, int threads) {
+    return (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, threads), 148 * 32));
+}
+
+}  // namespace hx
+
+using namespace hx;
+
+extern "C" int64_t hx_mesh_csc_workspace_bytes(int64_t n_el_total, int64_t n_cols) {
+    if (n_el_total < 0 || n_cols < 0) return -1;
+    return (int64_t)mesh_ws_layout(nullptr, n_el_total, n_cols).total;
+}
+
+extern "C" int hx_mesh_csc_symbolic(const hx_elem_segment *segs, int32_t n_segs, int64_t n_nodes,
+                                    int64_t col_lo, int64_t col_hi, int64_t *col_ptr, void *workspace,
+                                    int64_t workspace_bytes, uint32_t *status, void *stream) {
+    SegTable T;
+    int64_t n_total = 0;
+    int rc = make_segtable(segs, n_segs, T, n_total, false);
+    if (rc) return rc;
+    if (col_lo < 0 || col_hi < col_lo || col_hi > n_nodes || n_nodes >= INT32_MAX || col_ptr == nullptr ||
+        status == nullptr) {
+        set_last_error("hx_mesh_csc_symbolic: bad column range [%lld, %lld) for %lld nodes", (long long)col_lo,
+                       (long long)col_hi, (long long)n_nodes);
+        return HX_ERR_VALUE;
+    }
+    const int64_t ncols = col_hi - col_lo;
+    MeshWs w = mesh_ws_layout(workspace, n_total, ncols);
+    if (workspace == nullptr || workspace_bytes < (int64_t)w.total) {
+        set_last_error("hx_mesh_csc_symbolic: workspace %lld < %lld bytes", (long long)workspace_bytes,
+                       (long long)w.total);
+        return HX_ERR_WORKSPACE;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    HX_TRY_CUDA(cudaMemsetAsync(status, 0, sizeof(uint32_t), s));
+    HX_TRY_CUDA(cudaMemsetAsync(w.deg, 0, sizeof(int32_t) * (ncols + 1), s));
+    if (n_total > 0) {
+        degree_kernel<<<grid_for(n_total, 256), 256, 0, s>>>(T, n_total, n_nodes, col_lo, col_hi, w.deg, status);
+        HX_CHECK_LAUNCH("degree_kernel");
+    }
+    size_t cb = w.cub_bytes;
+    HX_TRY_CUDA(cub::DeviceScan::ExclusiveSum(w.cub_tmp, cb, w.deg, w.adj_ptr, (int)(ncols + 1), s));
+    HX_TRY_CUDA(cudaMemsetAsync(w.deg, 0, sizeof(int32_t) * (ncols + 1), s));
+    if (n_total > 0) {
+        adjacency_fill_kernel<<<grid_for(n_total, 256), 256, 0, s>>>(T, n_total, col_lo, col_hi, w.adj_ptr,
+                                                                      w.deg, w.adj);
+        HX_CHECK_LAUNCH("adjacency_fill_kernel");
+    }
+    HX_TRY_CUDA(cudaMemsetAsync(w.counts + ncols, 0, sizeof(int32_t), s));
+    if (ncols > 0) {
+        column_kernel<false><<<(unsigned)ceil_div(ncols, COL_BLOCK), COL_BLOCK, 0, s>>>(
+            T, col_lo, ncols, w.adj_ptr, w.adj, w.counts, nullptr, nullptr, nullptr, status);
+        HX_CHECK_LAUNCH("column_kernel<count>");
+    }
+    auto it = cub::TransformInputIterator<int64_t, CastI64, const int32_t *>(w.counts, CastI64());
+    cb = w.cub_bytes;
+    HX_TRY_CUDA(cub::DeviceScan::ExclusiveSum(w.cub_tmp, cb, it, col_ptr, (int)(ncols + 1), s));
+    return HX_OK;
+}
+
+extern "C" int hx_mesh_csc_numeric(const hx_elem_segment *segs, int32_t n_segs, int64_t col_lo, int64_t col_hi,
+                                   const int64_t *col_ptr, int64_t *row_idx, double *vals, const void *workspace,
+                                   uint32_t *status, void *stream) {
+    SegTable T;
+    int64_t n_total = 0;
+    int rc = make_segtable(segs, n_segs, T, n_total, true);
+    if (rc) return rc;
+    if (col_lo < 0 || col_hi < col_lo || col_ptr == nullptr || workspace == nullptr || status == nullptr) {
+        set_last_error("hx_mesh_csc_numeric: bad arguments");
+        return HX_ERR_VALUE;
+    }
+    const int64_t ncols = col_hi - col_lo;
+    MeshWs w = mesh_ws_layout(const_cast<void *>(workspace), n_total, ncols);
+    cudaStream_t s = (cudaStream_t)stream;
+    if (ncols > 0) {
+        column_kernel<true><<<(unsigned)ceil_div(ncols, COL_BLOCK), COL_BLOCK, 0, s>>>(
+            T, col_lo, ncols, w.adj_ptr, w.adj, nullptr, col_ptr, row_idx, vals, status);
+        HX_CHECK_LAUNCH("column_kernel<values>");
+    }
+    return HX_OK;
+}

@@ -1,0 +1,270 @@
+"""Device-resident hot path: torch CUDA tensors in, torch CUDA tensors out.
+
+Torch is plumbing here (device memory from its caching allocator, the current stream); every
+compute step is a call into libhexfem_b200.so.  The host-facing API in element.py /
+integrate.py / assemble.py / pipeline.py is built on these functions.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .errors import ConfigurationError, DegenerateElementError, MeshValidationError, NativeLibraryError
+
+__all__ = [
+    "DeviceMesh", "DeviceCsc", "require_device", "stream_handle", "integrate_mesh", "stiffness_batch",
+    "connectivity_index_arrays", "raise_if_failed", "mesh_csc", "triplet_csc",
+]
+
+_FAIL_WORDS = 3  # hx_fail_info = {int64 element, int32 gp, int32 pad, double det} = 24 bytes
+
+
+def require_device(device=None) -> torch.device:
+    """The CUDA device to run on; raises (no CPU fallback) when there is none."""
+    N.lib()
+    if not torch.cuda.is_available():
+        raise NativeLibraryError("hexfem_b200 needs a CUDA device (B200, sm_100a); none is available")
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+    if dev.type != "cuda":
+        raise ConfigurationError(f"hexfem_b200 runs on CUDA devices only, got {dev}")
+    return dev
+
+
+def stream_handle(stream=None) -> ctypes.c_void_p:
+    s = torch.cuda.current_stream() if stream is None else stream
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _ptr(t) -> ctypes.c_void_p:
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else ctypes.c_void_p(0)
+
+
+def _check_tensor(t, dtype, shape, name):
+    if not isinstance(t, torch.Tensor) or t.device.type != "cuda":
+        raise ValueError(f"{name} must be a CUDA tensor")
+    if t.dtype != dtype:
+        raise ValueError(f"{name} must be {dtype}, got {t.dtype}")
+    if shape is not None and tuple(t.shape) != tuple(shape):
+        raise ValueError(f"{name} must have shape {tuple(shape)}, got {tuple(t.shape)}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+
+
+@dataclass
+class DeviceMesh:
+    """Mesh arrays resident in HBM: coords (n_nodes,3) f64, conn (n_el,8) i32, coeff (n_el,) f64."""
+
+    coords: torch.Tensor
+    conn: torch.Tensor
+    coeff: torch.Tensor
+
+    @property
+    def n_nodes(self) -> int:
+        return self.coords.shape[0]
+
+    @property
+    def n_el(self) -> int:
+        return self.conn.shape[0]
+
+    @classmethod
+    def from_host(cls, mesh, device=None, non_blocking: bool = False) -> "DeviceMesh":
+        dev = require_device(device)
+
+        def up(a, dt):
+            t = a if isinstance(a, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(a, dtype=dt))
+            return t.to(dev, non_blocking=non_blocking)
+
+        return cls(up(mesh.coords, np.float64), up(mesh.connectivity, np.int32), up(mesh.coefficient, np.float64))
+
+    def h2d_bytes(self) -> int:
+        return sum(t.numel() * t.element_size() for t in (self.coords, self.conn, self.coeff))
+
+
+def new_fail_record(device) -> torch.Tensor:
+    return torch.empty(_FAIL_WORDS, dtype=torch.int64, device=device)
+
+
+def raise_if_failed(fail: torch.Tensor, element_offset: int = 0) -> None:
+    """Synchronising read of an hx_fail_info record; raises DegenerateElementError
+    (element.py:237-244) for the lowest failing element."""
+    host = fail.cpu().numpy()
+    element = int(host[0])
+    if element < 0:
+        return
+    gp = int(np.int32(host[1] & 0xFFFFFFFF))
+    det = float(host[2:3].view(np.float64)[0])
+    raise DegenerateElementError(element_id=element_offset + element, gauss_point=gp, det=det)
+
+
+def _mode_id(mode: str) -> int:
+    if mode == "exact":
+        return N.MODE_EXACT
+    if mode == "fast":
+        return N.MODE_FAST
+    raise ConfigurationError(f"integration mode must be 'exact' or 'fast', got {mode!r}")
+
+
+def integrate_mesh(dm: DeviceMesh, lo: int = 0, hi: int | None = None, *, ke=None, rows=None, cols=None,
+                   with_index: bool = True, mode: str = "exact", fail=None, stream=None):
+    """KE (+ fused iK/jK) for elements [lo, hi) of a device mesh.  Asynchronous: returns
+    ``(ke, rows, cols, fail)``; call raise_if_failed(fail) after the stream is done."""
+    hi = dm.n_el if hi is None else hi
+    if not 0 <= lo <= hi <= dm.n_el:
+        raise ValueError(f"element range [{lo}, {hi}) outside [0, {dm.n_el})")
+    n = hi - lo
+    dev = dm.conn.device
+    if ke is None:
+        ke = torch.empty((n, 36), dtype=torch.float64, device=dev)
+    _check_tensor(ke, torch.float64, (n, 36), "ke")
+    if with_index:
+        if rows is None:
+            rows = torch.empty(36 * n, dtype=torch.int32, device=dev)
+        if cols is None:
+            cols = torch.empty(36 * n, dtype=torch.int32, device=dev)
+        _check_tensor(rows, torch.int32, (36 * n,), "rows")
+        _check_tensor(cols, torch.int32, (36 * n,), "cols")
+    else:
+        rows = cols = None
+    if fail is None:
+        fail = new_fail_record(dev)
+    N.check(N.lib().hx_integrate_mesh(_ptr(dm.coords), dm.n_nodes, _ptr(dm.conn), _ptr(dm.coeff), lo, hi,
+                                      _ptr(ke), _ptr(rows), _ptr(cols), _mode_id(mode), _ptr(fail),
+                                      stream_handle(stream)), "hx_integrate_mesh")
+    return ke, rows, cols, fail
+
+
+def stiffness_batch(coords: torch.Tensor, coeff: torch.Tensor, out=None, mode: str = "exact", fail=None,
+                    stream=None):
+    """element.py:213-245 on device: coords (n,8,3) f64, coeff (n,) f64 -> (out (n,36), fail)."""
+    n = coords.shape[0]
+    _check_tensor(coords, torch.float64, (n, 8, 3), "coords")
+    _check_tensor(coeff, torch.float64, (n,), "coeff")
+    if out is None:
+        out = torch.empty((n, 36), dtype=torch.float64, device=coords.device)
+    _check_tensor(out, torch.float64, (n, 36), "out")
+    if fail is None:
+        fail = new_fail_record(coords.device)
+    N.check(N.lib().hx_stiffness_batch(_ptr(coords), _ptr(coeff), n, _ptr(out), _mode_id(mode), _ptr(fail),
+                                       stream_handle(stream)), "hx_stiffness_batch")
+    return out, fail
+
+
+def connectivity_index_arrays(conn: torch.Tensor, lo: int = 0, hi: int | None = None, stream=None):
+    """assemble.py:86-93 on device -> (rows, cols) int32 (36*(hi-lo),)."""
+    hi = conn.shape[0] if hi is None else hi
+    _check_tensor(conn, torch.int32, (conn.shape[0], 8), "conn")
+    n = hi - lo
+    rows = torch.empty(36 * n, dtype=torch.int32, device=conn.device)
+    cols = torch.empty(36 * n, dtype=torch.int32, device=conn.device)
+    N.check(N.lib().hx_connectivity_index_arrays(_ptr(conn), lo, hi, _ptr(rows), _ptr(cols),
+                                                 stream_handle(stream)), "hx_connectivity_index_arrays")
+    return rows, cols
+
+
+@dataclass
+class DeviceCsc:
+    """Lower-triangular CSC block in HBM: col_ptr (ncols+1) i64, row_idx (nnz) i64, vals (nnz) f64."""
+
+    col_ptr: torch.Tensor
+    row_idx: torch.Tensor
+    vals: torch.Tensor
+    dim: int
+    col_lo: int = 0
+    path: str = "mesh"
+
+    @property
+    def nnz(self) -> int:
+        return self.row_idx.shape[0]
+
+
+def _status_error(st: int):
+    if st & N.ST_BAD_INDEX:
+        raise MeshValidationError("triplet index outside [0, dim)")
+    if st & N.ST_UPPER:
+        raise MeshValidationError("triplet entry above the diagonal")
+
+
+def mesh_csc(parts, n_nodes: int, col_lo: int = 0, col_hi: int | None = None, stream=None) -> DeviceCsc:
+    """Assemble columns [col_lo, col_hi) of the lower CSC from element segments.
+
+    ``parts`` is a list of (conn (n,8) i32, ke (n,36) f64) CUDA tensor pairs in ascending global
+    element order (one pair for a single GPU; halo segments for the multi-GPU path).  Meshes
+    outside the node-adjacency fast path's limits fall through to the generic triplet path
+    with identical results.
+    """
+    col_hi = n_nodes if col_hi is None else col_hi
+    if len(parts) > N.MAX_SEGMENTS:
+        raise ValueError(f"at most {N.MAX_SEGMENTS} element segments")
+    dev = parts[0][0].device
+    for conn, ke in parts:
+        _check_tensor(conn, torch.int32, (conn.shape[0], 8), "conn")
+        _check_tensor(ke, torch.float64, (conn.shape[0], 36), "ke")
+    n_total = sum(int(c.shape[0]) for c, _ in parts)
+    ncols = col_hi - col_lo
+    segs = N.segments([(c.data_ptr(), k.data_ptr(), int(c.shape[0])) for c, k in parts])
+    ws_bytes = N.lib().hx_mesh_csc_workspace_bytes(n_total, ncols)
+    if ws_bytes < 0:
+        raise ValueError("bad mesh size")
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
+    status = torch.zeros(1, dtype=torch.int32, device=dev)
+    col_ptr = torch.empty(ncols + 1, dtype=torch.int64, device=dev)
+    sh = stream_handle(stream)
+    N.check(N.lib().hx_mesh_csc_symbolic(segs, len(parts), n_nodes, col_lo, col_hi, _ptr(col_ptr), _ptr(ws),
+                                         ws_bytes, _ptr(status), sh), "hx_mesh_csc_symbolic")
+    head = torch.stack([status.to(torch.int64)[0], col_ptr[-1]]).cpu()  # one sync: status + nnz
+    st, nnz = int(head[0]), int(head[1])
+    _status_error(st)
+    if st & N.ST_FASTPATH_LIMITS:
+        return _mesh_csc_generic(parts, n_nodes, col_lo, col_hi, stream)
+    row_idx = torch.empty(nnz, dtype=torch.int64, device=dev)
+    vals = torch.empty(nnz, dtype=torch.float64, device=dev)
+    N.check(N.lib().hx_mesh_csc_numeric(segs, len(parts), col_lo, col_hi, _ptr(col_ptr), _ptr(row_idx),
+                                        _ptr(vals), _ptr(ws), _ptr(status), sh), "hx_mesh_csc_numeric")
+    return DeviceCsc(col_ptr, row_idx, vals, n_nodes, col_lo, "mesh")
+
+
+def _mesh_csc_generic(parts, n_nodes, col_lo, col_hi, stream) -> DeviceCsc:
+    rows_l, cols_l, vals_l = [], [], []
+    for conn, ke in parts:
+        r, c = connectivity_index_arrays(conn, stream=stream)
+        rows_l.append(r)
+        cols_l.append(c)
+        vals_l.append(ke.reshape(-1))
+    rows, cols, vals = torch.cat(rows_l), torch.cat(cols_l), torch.cat(vals_l)
+    if col_lo != 0 or col_hi != n_nodes:
+        keep = (cols >= col_lo) & (cols < col_hi)
+        rows, cols, vals = rows[keep], cols[keep], vals[keep]
+    full = triplet_csc(rows, cols, vals, n_nodes, stream=stream)
+    cp = full.col_ptr[col_lo:col_hi + 1]
+    return DeviceCsc(cp - cp[0], full.row_idx, full.vals, n_nodes, col_lo, "triplet")
+
+
+def triplet_csc(rows: torch.Tensor, cols: torch.Tensor, vals: torch.Tensor, dim: int, stream=None) -> DeviceCsc:
+    """Generic triplet -> lower CSC (assemble.py:110-149) on device."""
+    n = rows.shape[0]
+    _check_tensor(rows, torch.int32, (n,), "rows")
+    _check_tensor(cols, torch.int32, (n,), "cols")
+    _check_tensor(vals, torch.float64, (n,), "vals")
+    dev = rows.device
+    ws_bytes = N.lib().hx_triplet_csc_workspace_bytes(n, dim)
+    if ws_bytes < 0:
+        raise ConfigurationError(f"{n} triplets exceed one device sort")
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
+    status = torch.zeros(1, dtype=torch.int32, device=dev)
+    col_ptr = torch.empty(dim + 1, dtype=torch.int64, device=dev)
+    row_buf = torch.empty(max(n, 1), dtype=torch.int64, device=dev)
+    sh = stream_handle(stream)
+    N.check(N.lib().hx_triplet_csc_symbolic(_ptr(rows), _ptr(cols), n, dim, _ptr(col_ptr), _ptr(row_buf),
+                                            _ptr(ws), ws_bytes, _ptr(status), sh), "hx_triplet_csc_symbolic")
+    head = torch.stack([status.to(torch.int64)[0], col_ptr[-1]]).cpu()
+    st, nnz = int(head[0]), int(head[1])
+    _status_error(st)
+    out = torch.empty(nnz, dtype=torch.float64, device=dev)
+    N.check(N.lib().hx_triplet_csc_numeric(_ptr(vals), n, dim, _ptr(col_ptr), _ptr(out), _ptr(ws), sh),
+            "hx_triplet_csc_numeric")
+    return DeviceCsc(col_ptr, row_buf[:nnz], out, dim, 0, "triplet")

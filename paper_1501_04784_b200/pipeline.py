@@ -1,0 +1,172 @@
+"""Global matrix construction pipeline (mesh -> KE + iK/jK -> lower CSC) on the GPU.
+
+``run_build`` mirrors reference cli.py:38-149 (same signature plus ``integration`` and
+``device``, same BuildReport fields); stage times come from CUDA events on the launch stream
+instead of perf_counter.  ``build_device`` is the device-resident step the benchmark times:
+inputs already in HBM, outputs left in HBM.
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import asdict, dataclass
+
+import numpy as np
+import torch
+
+from . import device as D
+from .assemble import LowerCscMatrix, csc_to_host
+from .errors import ConfigurationError
+from .integrate import plan_batches, required_bytes
+
+__all__ = ["BuildReport", "DeviceBuild", "build_device", "run_build", "triplet_memory", "csc_memory",
+           "memory_saving", "format_mb", "format_percent"]
+
+# sparseio.py:26-38 memory model: 16 B per triplet, 16 B per CSC entry + 8 B per column pointer.
+_MB = 10**6
+
+
+def triplet_memory(nnz_triplet: int) -> float:
+    if nnz_triplet < 0:
+        raise ValueError("nnz must be non-negative")
+    return nnz_triplet * 16 / _MB
+
+
+def csc_memory(nnz_csc: int, dim: int) -> float:
+    if nnz_csc < 0 or dim < 0:
+        raise ValueError("nnz and dim must be non-negative")
+    return (nnz_csc * 16 + (dim + 1) * 8) / _MB
+
+
+def memory_saving(triplet_mb: float, csc_mb: float) -> float:
+    if not triplet_mb > 0:
+        raise ValueError(f"triplet memory must be positive, got {triplet_mb!r}")
+    return 1.0 - csc_mb / triplet_mb
+
+
+def format_mb(mb: float) -> str:
+    return f"{mb:.2f}" if mb < 10 else f"{mb:.1f}"
+
+
+def format_percent(fraction: float) -> str:
+    return f"{fraction * 100:.1f}%"
+
+
+@dataclass(frozen=True)
+class BuildReport:
+    n_el: int
+    n_nodes: int
+    nnz_triplet: int
+    nnz_csc: int
+    nnz_compression: float
+    triplet_mb: float
+    csc_mb: float
+    memory_saving: float
+    time_integration_s: float
+    time_index_s: float | None
+    time_assembly_s: float
+    time_total_s: float
+    pct_integration: float
+    pct_assembly: float
+    group_count: int
+    workers: int
+    mode: str
+    assembler: str
+
+    def as_dict(self) -> dict:
+        return asdict(self)
+
+
+@dataclass
+class DeviceBuild:
+    ke: torch.Tensor          # (n_el, 36) f64
+    rows: torch.Tensor | None  # (36 n_el,) i32
+    cols: torch.Tensor | None  # (36 n_el,) i32
+    csc: D.DeviceCsc
+
+
+def build_device(dm: D.DeviceMesh, mode: str = "exact", with_index: bool = True, ranges=None,
+                 ke=None, rows=None, cols=None, stream=None) -> DeviceBuild:
+    """KE (+ fused iK/jK) for every element, then the lower CSC, all in HBM.
+
+    ``ranges`` is an optional BatchPlan-style list of element groups (each one kernel launch
+    into the same output buffers); results are bitwise independent of it.
+    """
+    dev = dm.conn.device
+    n = dm.n_el
+    if ke is None:
+        ke = torch.empty((n, 36), dtype=torch.float64, device=dev)
+    if with_index:
+        rows = torch.empty(36 * n, dtype=torch.int32, device=dev) if rows is None else rows
+        cols = torch.empty(36 * n, dtype=torch.int32, device=dev) if cols is None else cols
+    fails = []
+    for lo, hi in (ranges or [(0, n)]):
+        _, _, _, fail = D.integrate_mesh(dm, lo, hi, ke=ke[lo:hi],
+                                         rows=rows[36 * lo:36 * hi] if with_index else None,
+                                         cols=cols[36 * lo:36 * hi] if with_index else None,
+                                         with_index=with_index, mode=mode, stream=stream)
+        fails.append(fail)
+    csc = D.mesh_csc([(dm.conn, ke)], dm.n_nodes, stream=stream)
+    for f in fails:
+        D.raise_if_failed(f)
+    return DeviceBuild(ke, rows if with_index else None, cols if with_index else None, csc)
+
+
+def run_build(mesh, budget_bytes: int, workers: int = 1, mode: str = "sequential", assembler: str = "direct",
+              integration: str = "exact", device=None):
+    """Integrate and assemble one mesh on the GPU; returns (LowerCscMatrix, BuildReport)."""
+    if assembler not in ("direct", "triplet"):
+        raise ConfigurationError(f"assembler must be 'direct' or 'triplet', got {assembler!r}")
+    if mode not in ("sequential", "overlapped"):
+        raise ConfigurationError(f"mode must be 'sequential' or 'overlapped', got {mode!r}")
+    if workers < 1:
+        raise ConfigurationError(f"worker count must be at least 1, got {workers}")
+    plan = plan_batches(required_bytes(mesh.n_el), budget_bytes, mesh.n_el)
+    dev = D.require_device(device)
+    wall0 = time.perf_counter()
+    with torch.cuda.device(dev):
+        dm = D.DeviceMesh.from_host(mesh, dev)
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        ev[0].record()
+        n = mesh.n_el
+        with_index = assembler == "triplet"
+        ke = torch.empty((n, 36), dtype=torch.float64, device=dev)
+        rows = torch.empty(36 * n, dtype=torch.int32, device=dev) if with_index else None
+        cols = torch.empty(36 * n, dtype=torch.int32, device=dev) if with_index else None
+        fails = []
+        for lo, hi in plan.ranges:
+            _, _, _, fail = D.integrate_mesh(dm, lo, hi, ke=ke[lo:hi],
+                                             rows=rows[36 * lo:36 * hi] if with_index else None,
+                                             cols=cols[36 * lo:36 * hi] if with_index else None,
+                                             with_index=with_index, mode=integration)
+            fails.append(fail)
+        ev[1].record()
+        for f in fails:
+            D.raise_if_failed(f)
+        csc = D.mesh_csc([(dm.conn, ke)], dm.n_nodes)
+        ev[2].record()
+        matrix: LowerCscMatrix = csc_to_host(csc)
+        torch.cuda.synchronize(dev)
+        time_integration = ev[0].elapsed_time(ev[1]) / 1e3
+        time_assembly = ev[1].elapsed_time(ev[2]) / 1e3
+    time_total = time.perf_counter() - wall0
+    nnz_triplet = 36 * mesh.n_el
+    trip_mb = triplet_memory(nnz_triplet)
+    matrix_mb = csc_memory(matrix.nnz, matrix.dim)
+    stage_sum = time_integration + time_assembly
+    pct_integration = 100.0 * time_integration / stage_sum if stage_sum > 0 else 100.0
+    report = BuildReport(
+        n_el=mesh.n_el, n_nodes=mesh.n_nodes, nnz_triplet=nnz_triplet, nnz_csc=matrix.nnz,
+        nnz_compression=1.0 - matrix.nnz / nnz_triplet, triplet_mb=trip_mb, csc_mb=matrix_mb,
+        memory_saving=memory_saving(trip_mb, matrix_mb), time_integration_s=time_integration,
+        # iK/jK are produced inside the integration kernel (fused), so no separate index stage.
+        time_index_s=0.0 if assembler == "triplet" else None,
+        time_assembly_s=time_assembly, time_total_s=time_total, pct_integration=pct_integration,
+        pct_assembly=100.0 - pct_integration, group_count=plan.group_count, workers=workers, mode=mode,
+        assembler=assembler)
+    return matrix, report
+
+
+def host_csc_equal(a: LowerCscMatrix, b: LowerCscMatrix) -> bool:
+    return (a.dim == b.dim and np.array_equal(a.col_ptr, b.col_ptr) and np.array_equal(a.row_idx, b.row_idx)
+            and np.array_equal(a.vals.view(np.uint64), b.vals.view(np.uint64)))

@@ -1,0 +1,275 @@
+"""GPU parity: the CUDA path through the C ABI vs the oracle / the reference's golden outputs.
+
+Bar: bit-exact for indices and (exact mode) values.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from common import SMALL_MESHES, bits_equal, golden_mesh, sha
+from paper_1501_04784_b200 import device as D
+from paper_1501_04784_b200 import (
+    CudaBackend,
+    DegenerateElementError,
+    DirectAssembler,
+    LocalValuesBatch,
+    Mesh,
+    MeshValidationError,
+    StagingError,
+    TripletMatrix,
+    assemble_direct,
+    build_triplet,
+    connectivity_index_arrays,
+    integrate_all,
+    plan_batches,
+    required_bytes,
+    run_build,
+    stiffness_batch,
+    triplet_to_csc,
+)
+from paper_1501_04784_b200.pipeline import build_device, host_csc_equal
+from paper_1501_04784_b200.workloads import make_workload, perturbed_mesh, permuted_mesh
+
+pytestmark = pytest.mark.gpu
+
+
+def one_group(mesh):
+    return plan_batches(required_bytes(mesh.n_el), 10**13, mesh.n_el)
+
+
+def test_stiffness_batch_bitwise(golden):
+    out = stiffness_batch(golden["batch_coords"], golden["batch_coeff"])
+    assert bits_equal(out, golden["batch_ke"])
+
+
+def test_stiffness_batch_block_boundaries(golden):
+    coords, coeff = golden["batch_coords"], golden["batch_coeff"]
+    full = stiffness_batch(coords, coeff)
+    pieces = np.vstack([stiffness_batch(coords[lo:lo + 13], coeff[lo:lo + 13]) for lo in range(0, len(coeff), 13)])
+    assert bits_equal(full, pieces)
+
+
+@pytest.mark.parametrize("name", SMALL_MESHES)
+def test_integrate_mesh_fused_index_bitwise(golden, name):
+    dm = D.DeviceMesh.from_host(golden_mesh(golden, name))
+    ke, rows, cols, fail = D.integrate_mesh(dm)
+    D.raise_if_failed(fail)
+    assert bits_equal(ke.cpu().numpy(), golden[f"{name}_ke"])
+    assert bits_equal(rows.cpu().numpy(), golden[f"{name}_rows"])
+    assert bits_equal(cols.cpu().numpy(), golden[f"{name}_cols"])
+
+
+@pytest.mark.parametrize("name", SMALL_MESHES)
+def test_mesh_csc_bitwise(golden, name):
+    mesh = golden_mesh(golden, name)
+    build = build_device(D.DeviceMesh.from_host(mesh))
+    assert build.csc.path == "mesh"
+    assert bits_equal(build.csc.col_ptr.cpu().numpy(), golden[f"{name}_col_ptr"])
+    assert bits_equal(build.csc.row_idx.cpu().numpy(), golden[f"{name}_row_idx"])
+    assert bits_equal(build.csc.vals.cpu().numpy(), golden[f"{name}_vals"])
+
+
+@pytest.mark.parametrize("name", SMALL_MESHES)
+def test_triplet_to_csc_generic_bitwise(golden, name):
+    t = TripletMatrix(rows=golden[f"{name}_rows"], cols=golden[f"{name}_cols"],
+                      vals=golden[f"{name}_ke"].reshape(-1), dim=golden[f"{name}_coords"].shape[0])
+    m = triplet_to_csc(t)
+    assert bits_equal(m.col_ptr, golden[f"{name}_col_ptr"])
+    assert bits_equal(m.row_idx, golden[f"{name}_row_idx"])
+    assert bits_equal(m.vals, golden[f"{name}_vals"])
+
+
+def test_generic_triplets_long_runs_pairwise_rule(golden):
+    dim = int(golden["trip_dim"][0])
+    m = triplet_to_csc(TripletMatrix(golden["trip_rows"], golden["trip_cols"], golden["trip_vals"], dim))
+    assert bits_equal(m.col_ptr, golden["trip_col_ptr"])
+    assert bits_equal(m.row_idx, golden["trip_row_idx"])
+    assert bits_equal(m.vals, golden["trip_out"])
+
+
+def test_random_triplets_against_oracle():
+    rng = np.random.default_rng(7)
+    for n, dim in [(1, 1), (50, 3), (5000, 40), (20000, 7)]:
+        r = rng.integers(0, dim, size=n).astype(np.int32)
+        c = rng.integers(0, dim, size=n).astype(np.int32)
+        rows, cols = np.maximum(r, c), np.minimum(r, c)
+        vals = rng.standard_normal(n) * np.exp(rng.uniform(-10, 10, size=n))
+        m = triplet_to_csc(TripletMatrix(rows, cols, vals, dim))
+        cp, ri, vv = oracle.triplet_to_csc(rows, cols, vals, dim)
+        assert bits_equal(m.col_ptr, cp) and bits_equal(m.row_idx, ri) and bits_equal(m.vals, vv)
+
+
+def test_triplet_edge_cases():
+    m = triplet_to_csc(TripletMatrix(np.array([2, 2, 1], np.int32), np.array([0, 0, 1], np.int32),
+                                     np.array([1.5, -1.5, 3.0]), 3))
+    assert np.array_equal(m.row_idx, [2, 1]) and np.array_equal(m.vals, [0.0, 3.0])
+    empty = triplet_to_csc(TripletMatrix(np.empty(0, np.int32), np.empty(0, np.int32), np.empty(0), 3))
+    assert empty.nnz == 0 and np.array_equal(empty.col_ptr, np.zeros(4, np.int64))
+    with pytest.raises(MeshValidationError):
+        triplet_to_csc(TripletMatrix(np.array([5], np.int32), np.array([0], np.int32), np.array([1.0]), 4))
+    with pytest.raises(MeshValidationError):
+        triplet_to_csc(TripletMatrix(np.array([0], np.int32), np.array([2], np.int32), np.array([1.0]), 4))
+
+
+def test_connectivity_index_arrays_ranges(golden):
+    mesh = golden_mesh(golden, "perm5")
+    for lo, hi in [(0, None), (3, 17), (0, 1), (124, 125)]:
+        r, c = connectivity_index_arrays(mesh, lo, hi)
+        r2, c2 = oracle.connectivity_index_arrays(mesh.connectivity, lo, hi)
+        assert bits_equal(r, r2) and bits_equal(c, c2)
+
+
+def test_degenerate_reports_first_element(golden):
+    mesh = Mesh(golden["degen_coords"], golden["degen_conn"], np.ones(golden["degen_conn"].shape[0]))
+    exp_el, exp_gp = golden["degen_expect"]
+    with CudaBackend() as backend, pytest.raises(DegenerateElementError) as info:
+        integrate_all(mesh, backend, one_group(mesh))
+    assert info.value.element_id == exp_el and info.value.gauss_point == exp_gp
+    assert info.value.det == golden["degen_det"][0]
+    with pytest.raises(DegenerateElementError) as info:
+        stiffness_batch(mesh.coords[mesh.connectivity], mesh.coefficient, element_offset=100)
+    assert info.value.element_id == 100 + exp_el
+
+
+def test_integrate_all_plans_modes_bitwise(golden):
+    mesh = golden_mesh(golden, "m345")
+    ref = golden["m345_ke"]
+    with CudaBackend() as backend:
+        for budget in (10**13, required_bytes(7), 520):
+            plan = plan_batches(required_bytes(mesh.n_el), budget, mesh.n_el)
+            seen = []
+            for mode in ("sequential", "overlapped"):
+                seen.clear()
+                batch = integrate_all(mesh, backend, plan, mode=mode, consumer=lambda r, v: seen.append((r, v.copy())))
+                assert bits_equal(batch.values, ref)
+                assert [r for r, _ in seen] == list(plan.ranges)
+                assert bits_equal(np.vstack([v for _, v in seen]), ref)
+
+
+def test_integrate_all_host_staged_run(golden):
+    """ComputeBackend.run drop-in (host staged coords) gives the same bits."""
+    mesh = golden_mesh(golden, "perm5")
+    with CudaBackend() as backend:
+        out = np.empty((mesh.n_el, 36))
+        backend.run(mesh.coords[mesh.connectivity], mesh.coefficient, out=out)
+    assert bits_equal(out, golden["perm5_ke"])
+
+
+def test_staging_error_and_consumer_errors(golden):
+    mesh = golden_mesh(golden, "m345")
+    with CudaBackend(capacity_bytes=required_bytes(3)) as backend, pytest.raises(StagingError) as info:
+        integrate_all(mesh, backend, one_group(mesh))
+    assert info.value.group_index == 0
+
+    def bad(rng, values):
+        raise RuntimeError("downstream failed")
+
+    with CudaBackend() as backend, pytest.raises(RuntimeError, match="downstream"):
+        integrate_all(mesh, backend, plan_batches(required_bytes(27), required_bytes(5), 27), mode="overlapped",
+                      consumer=bad)
+
+
+def test_direct_assembler_streaming_and_order(golden):
+    mesh = golden_mesh(golden, "perm5")
+    values = golden["perm5_ke"]
+    one = assemble_direct(mesh, LocalValuesBatch(values))
+    streamed = DirectAssembler(mesh)
+    for lo, hi in plan_batches(required_bytes(mesh.n_el), required_bytes(37), mesh.n_el).ranges:
+        streamed.consume((lo, hi), values[lo:hi])
+    two = streamed.finish()
+    assert host_csc_equal(one, two)
+    assert bits_equal(one.vals, golden["perm5_vals"])
+    a = DirectAssembler(mesh)
+    with pytest.raises(ValueError, match="order"):
+        a.consume((4, 8), values[4:8])
+    a.consume((0, 4), values[:4])
+    with pytest.raises(ValueError, match="consumed"):
+        a.finish()
+
+
+def test_run_build_both_assemblers(golden):
+    mesh = golden_mesh(golden, "m345")
+    for assembler in ("direct", "triplet"):
+        m, report = run_build(mesh, budget_bytes=required_bytes(10), assembler=assembler)
+        assert bits_equal(m.vals, golden["m345_vals"]) and bits_equal(m.row_idx, golden["m345_row_idx"])
+        assert report.group_count == 3 and report.nnz_csc == m.nnz
+        assert abs(report.pct_integration + report.pct_assembly - 100.0) < 1e-9
+
+
+def _high_valence_mesh(rng):
+    """A mesh whose node 0 touches 11 elements (beyond the fast path's degree limit)."""
+    base = perturbed_mesh(2, seed=1)
+    extra = []
+    for _ in range(4):
+        others = rng.choice(np.arange(1, base.n_nodes), size=7, replace=False)
+        extra.append(np.concatenate([[0], others]).astype(np.int32))
+    conn = np.vstack([base.connectivity, np.array(extra)])
+    return Mesh(base.coords, conn, np.ones(conn.shape[0]))
+
+
+def test_fast_path_limits_fall_back_bitwise():
+    rng = np.random.default_rng(3)
+    mesh = _high_valence_mesh(rng)
+    values = rng.standard_normal((mesh.n_el, 36))
+    m = assemble_direct(mesh, LocalValuesBatch(values))
+    rows, cols = oracle.connectivity_index_arrays(mesh.connectivity)
+    cp, ri, vv = oracle.triplet_to_csc(rows, cols, values.reshape(-1), mesh.n_nodes)
+    assert bits_equal(m.col_ptr, cp) and bits_equal(m.row_idx, ri) and bits_equal(m.vals, vv)
+    # repeated node inside an element
+    conn = mesh.connectivity.copy()
+    conn[0, 5] = conn[0, 4]
+    m2 = assemble_direct(Mesh(mesh.coords, conn, mesh.coefficient), LocalValuesBatch(values))
+    rows, cols = oracle.connectivity_index_arrays(conn)
+    cp, ri, vv = oracle.triplet_to_csc(rows, cols, values.reshape(-1), mesh.n_nodes)
+    assert bits_equal(m2.col_ptr, cp) and bits_equal(m2.row_idx, ri) and bits_equal(m2.vals, vv)
+
+
+def test_mesh_assembly_random_values_random_numbering():
+    """Assembly is value-agnostic: random KE values + permuted numbering vs the oracle."""
+    rng = np.random.default_rng(11)
+    for n in (1, 2, 7):
+        mesh = permuted_mesh(perturbed_mesh(n, seed=n), seed=n + 1)
+        values = rng.standard_normal((mesh.n_el, 36)) * np.exp(rng.uniform(-5, 5, size=(mesh.n_el, 36)))
+        m = assemble_direct(mesh, LocalValuesBatch(values))
+        rows, cols = oracle.connectivity_index_arrays(mesh.connectivity)
+        cp, ri, vv = oracle.triplet_to_csc(rows, cols, values.reshape(-1), mesh.n_nodes)
+        assert bits_equal(m.col_ptr, cp) and bits_equal(m.row_idx, ri) and bits_equal(m.vals, vv)
+
+
+@pytest.mark.parametrize("config", ["C1", "C2", "P64", "C3"])
+def test_full_pipeline_matches_reference_digests(digests, config):
+    d = digests["configs"][config]
+    if config == "P64":
+        mesh = permuted_mesh(perturbed_mesh(64, seed=0), seed=5)
+    else:
+        mesh = make_workload(config)
+    dm = D.DeviceMesh.from_host(mesh)
+    b = build_device(dm)
+    assert b.csc.path == "mesh" and b.csc.nnz == d["nnz"]
+    assert sha(b.ke.cpu().numpy()) == d["ke"]
+    assert sha(b.rows.cpu().numpy()) == d["rows"] and sha(b.cols.cpu().numpy()) == d["cols"]
+    assert sha(b.csc.col_ptr.cpu().numpy()) == d["col_ptr"]
+    assert sha(b.csc.row_idx.cpu().numpy()) == d["row_idx"]
+    assert sha(b.csc.vals.cpu().numpy()) == d["vals"]
+    del b, dm
+    torch.cuda.empty_cache()
+
+
+def test_operator_properties_full_size():
+    """Size-independent properties at BASELINE scale (C2): K 1 = 0, symmetric pattern invariants."""
+    mesh = make_workload("C2")
+    b = build_device(D.DeviceMesh.from_host(mesh))
+    cp, ri, vv = b.csc.col_ptr, b.csc.row_idx, b.csc.vals
+    ncol = mesh.n_nodes
+    col_of = torch.repeat_interleave(torch.arange(ncol, device=cp.device), cp[1:] - cp[:-1])
+    assert bool((ri >= col_of).all())
+    same = col_of[1:] == col_of[:-1]
+    assert bool((ri[1:][same] > ri[:-1][same]).all())
+    # K 1 = 0: row sums of the full symmetric matrix
+    rs = torch.zeros(ncol, dtype=torch.float64, device=cp.device)
+    rs.index_add_(0, ri, vv)
+    off = ri != col_of
+    rs.index_add_(0, col_of[off], vv[off])
+    assert float(rs.abs().max()) <= 1e-10 * float(vv.abs().max()) * 27
