@@ -21,7 +21,7 @@
  *   hx_mesh_csc_*                  assemble.py:152-239 DirectAssembler / assemble_direct, and
  *                                  triplet_to_csc (assemble.py:110-140) on mesh triplets
  *   hx_triplet_csc_*               assemble.py:110-149 triplet_to_csc + _check_indices
- *   hx_partition_*                 (new) element-halo exchange plan for the multi-GPU path
+ *   hx_halo_*                      (new) element-halo exchange of the multi-GPU path
  */
 #ifndef HEXFEM_B200_H
 #define HEXFEM_B200_H
@@ -71,9 +71,11 @@ typedef struct hx_fail_info {
  * hx_mesh_csc_* calls are concatenated in order and MUST be in ascending global element
  * order: duplicate positions are summed in that order (assemble.py:115-117, 179-184). */
 typedef struct hx_elem_segment {
-    const int32_t *conn; /* (n_el, 8) global node ids, device */
-    const double *ke;    /* (n_el, 36) packed lower values, device (may be NULL for symbolic) */
+    const int32_t *conn; /* element e's 8 global node ids at conn + e*conn_stride, device      */
+    const double *ke;    /* element e's 36 packed values at ke + e*ke_stride (NULL: symbolic) */
     int64_t n_el;
+    int64_t conn_stride; /* in int32 units, multiple of 4; 0 means dense (8)                 */
+    int64_t ke_stride;   /* in doubles; 0 means dense (36)                                   */
 } hx_elem_segment;
 
 /* ---- introspection (host only, no GPU needed) ------------------------------------------ */
@@ -132,6 +134,20 @@ int hx_triplet_csc_symbolic(const int32_t *rows, const int32_t *cols, int64_t n,
                             int64_t workspace_bytes, uint32_t *status, void *stream);
 int hx_triplet_csc_numeric(const double *vals, int64_t n, int64_t dim, const int64_t *col_ptr,
                            double *out_vals, const void *workspace, void *stream);
+
+/* ---- multi-GPU element-halo exchange (element-range shards, column blocks) -----------------
+ * col_bounds: (world+1) int64 device array, rank r owns columns [col_bounds[r], col_bounds[r+1]).
+ * count: per_dest (world) int64 device = number of local elements each rank must receive
+ *        (elements with a node in that rank's block; per_dest[self] = 0).
+ * pack:  records (sum(per_dest), 40) f64 device, destination-major, ascending element order
+ *        within a destination; record = 36 packed KE values + 8 int32 node ids (bit-copied), i.e.
+ *        directly consumable as an hx_elem_segment with conn_stride 80, ke_stride 40.
+ * pack must follow count with the same workspace. */
+int64_t hx_halo_workspace_bytes(int64_t n_el, int32_t world);
+int hx_halo_count(const int32_t *conn, int64_t n_el, const int64_t *col_bounds, int32_t world, int32_t self,
+                  int64_t *per_dest, void *workspace, int64_t workspace_bytes, void *stream);
+int hx_halo_pack(const int32_t *conn, const double *ke, int64_t n_el, const int64_t *col_bounds, int32_t world,
+                 int32_t self, double *records, const void *workspace, void *stream);
 
 #ifdef __cplusplus
 }

@@ -27,6 +27,7 @@ EXPORTED = (
     "hx_stiffness_batch", "hx_integrate_mesh", "hx_connectivity_index_arrays",
     "hx_mesh_csc_workspace_bytes", "hx_mesh_csc_symbolic", "hx_mesh_csc_numeric",
     "hx_triplet_csc_workspace_bytes", "hx_triplet_csc_symbolic", "hx_triplet_csc_numeric",
+    "hx_halo_workspace_bytes", "hx_halo_count", "hx_halo_pack",
 )
 
 
@@ -36,7 +37,8 @@ class HxFailInfo(ctypes.Structure):
 
 
 class HxElemSegment(ctypes.Structure):
-    _fields_ = [("conn", ctypes.c_void_p), ("ke", ctypes.c_void_p), ("n_el", ctypes.c_int64)]
+    _fields_ = [("conn", ctypes.c_void_p), ("ke", ctypes.c_void_p), ("n_el", ctypes.c_int64),
+                ("conn_stride", ctypes.c_int64), ("ke_stride", ctypes.c_int64)]
 
 
 _lib = None
@@ -71,6 +73,9 @@ def lib():
         "hx_triplet_csc_workspace_bytes": ([I64, I64], I64),
         "hx_triplet_csc_symbolic": ([P, P, I64, I64, P, P, P, I64, P, P], ctypes.c_int),
         "hx_triplet_csc_numeric": ([P, I64, I64, P, P, P, P], ctypes.c_int),
+        "hx_halo_workspace_bytes": ([I64, I32], I64),
+        "hx_halo_count": ([P, I64, P, I32, I32, P, P, I64, P], ctypes.c_int),
+        "hx_halo_pack": ([P, P, I64, P, I32, I32, P, P, P], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -93,10 +98,13 @@ def check(rc: int, what: str) -> None:
 
 
 def segments(parts) -> ctypes.Array:
-    """Build an hx_elem_segment[] from (conn_ptr, ke_ptr, n_el) triples."""
+    """Build an hx_elem_segment[] from (conn_ptr, ke_ptr, n_el[, conn_stride, ke_stride]) tuples."""
     arr = (HxElemSegment * len(parts))()
-    for i, (conn, ke, n) in enumerate(parts):
+    for i, part in enumerate(parts):
+        conn, ke, n = part[:3]
         arr[i].conn = conn
         arr[i].ke = ke
         arr[i].n_el = n
+        arr[i].conn_stride = part[3] if len(part) > 3 else 0
+        arr[i].ke_stride = part[4] if len(part) > 4 else 0
     return arr

@@ -35,10 +35,14 @@ constexpr int COL_BLOCK = 128;
 constexpr int MAXDEG = HX_MAX_NODE_DEGREE;
 constexpr int MAXR = HX_MAX_COL_ROWS;
 constexpr int MAX_SEGS = 4;
+constexpr int WIDE_MAXR = 32;
+constexpr int WIDE_BLOCK = 64;
 
 struct SegTable {
     const int32_t *conn[MAX_SEGS];
     const double *ke[MAX_SEGS];
+    int64_t conn_stride[MAX_SEGS];  // int32 units
+    int64_t ke_stride[MAX_SEGS];    // doubles
     int64_t start[MAX_SEGS + 1];  // combined element index where segment s starts
     int n;
 };
@@ -50,8 +54,9 @@ __device__ __forceinline__ int seg_of(const SegTable &T, int64_t e) {
     return s;
 }
 
-__device__ __forceinline__ void load_conn8(const int32_t *__restrict__ conn, int64_t e, int32_t (&g)[8]) {
-    const int4 *c4 = reinterpret_cast<const int4 *>(conn) + 2 * e;
+__device__ __forceinline__ void load_conn8(const int32_t *__restrict__ conn, int64_t e, int64_t stride,
+                                           int32_t (&g)[8]) {
+    const int4 *c4 = reinterpret_cast<const int4 *>(conn + e * stride);
     const int4 lo = __ldg(c4), hi = __ldg(c4 + 1);
     g[0] = lo.x; g[1] = lo.y; g[2] = lo.z; g[3] = lo.w;
     g[4] = hi.x; g[5] = hi.y; g[6] = hi.z; g[7] = hi.w;
@@ -64,7 +69,7 @@ __global__ void degree_kernel(SegTable T, int64_t n_total, int64_t n_nodes, int6
          e += (int64_t)gridDim.x * blockDim.x) {
         const int s = seg_of(T, e);
         int32_t g[8];
-        load_conn8(T.conn[s], e - T.start[s], g);
+        load_conn8(T.conn[s], e - T.start[s], T.conn_stride[s], g);
         bool bad = false;
 #pragma unroll
         for (int a = 0; a < 8; ++a) {
@@ -84,7 +89,7 @@ __global__ void adjacency_fill_kernel(SegTable T, int64_t n_total, int64_t col_l
          e += (int64_t)gridDim.x * blockDim.x) {
         const int s = seg_of(T, e);
         int32_t g[8];
-        load_conn8(T.conn[s], e - T.start[s], g);
+        load_conn8(T.conn[s], e - T.start[s], T.conn_stride[s], g);
 #pragma unroll
         for (int a = 0; a < 8; ++a) {
             const int32_t v = g[a];
@@ -113,48 +118,46 @@ __device__ __forceinline__ void sort8(int32_t (&v)[8]) {
     cswap(v[3], v[4]);
 }
 
-// Sorted-unique insert into a per-thread list R[0..m) laid out [slot][COL_BLOCK] in smem
+// Sorted-unique insert into a per-thread list R[0..m) laid out [slot][BLOCK] in smem
 // (thread-fastest: conflict-free for any per-thread slot).  Returns false on overflow.
+template <int MAXR_, int BLOCK>
 __device__ __forceinline__ bool insert_row(int32_t *R, int &m, int32_t v) {
     int pos = 0;
-    while (pos < m && R[pos * COL_BLOCK] < v) ++pos;
-    if (pos < m && R[pos * COL_BLOCK] == v) return true;
-    if (m == MAXR) return false;
-    for (int q = m; q > pos; --q) R[q * COL_BLOCK] = R[(q - 1) * COL_BLOCK];
-    R[pos * COL_BLOCK] = v;
+    while (pos < m && R[pos * BLOCK] < v) ++pos;
+    if (pos < m && R[pos * BLOCK] == v) return true;
+    if (m == MAXR_) return false;
+    for (int q = m; q > pos; --q) R[q * BLOCK] = R[(q - 1) * BLOCK];
+    R[pos * BLOCK] = v;
     ++m;
     return true;
 }
 
+template <int BLOCK>
 __device__ __forceinline__ int find_row(const int32_t *R, int m, int32_t v) {
     int lo = 0, hi = m;  // lower_bound; v is known to be present
     while (lo < hi) {
         const int mid = (lo + hi) >> 1;
-        if (R[mid * COL_BLOCK] < v) lo = mid + 1; else hi = mid;
+        if (R[mid * BLOCK] < v) lo = mid + 1; else hi = mid;
     }
     return lo;
 }
 
-// 4./6. per-column pass.  VALUES=false: write counts.  VALUES=true: write rows and sums.
-template <bool VALUES>
-__global__ void __launch_bounds__(COL_BLOCK)
-column_kernel(SegTable T, int64_t col_lo, int64_t ncols, const int32_t *__restrict__ adj_ptr,
-              const int32_t *__restrict__ adj, int32_t *__restrict__ counts,
-              const int64_t *__restrict__ col_ptr, int64_t *__restrict__ row_idx,
-              double *__restrict__ vals, uint32_t *__restrict__ status) {
-    __shared__ int32_t sR[MAXR * COL_BLOCK];
-    __shared__ double sV0[VALUES ? MAXR * COL_BLOCK : 1];
-    __shared__ double sS[VALUES ? MAXR * COL_BLOCK : 1];
-    const int t = threadIdx.x;
-    const int64_t cl = (int64_t)blockIdx.x * COL_BLOCK + t;
-    if (cl >= ncols) return;
+enum ColResult { COL_OK = 0, COL_ROWS_OVERFLOW = 1, COL_FATAL = 2 };
+
+// One column: incident elements sorted by id, distinct rows >= c (sorted), and (VALUES) the
+// duplicate sums in element order with numpy reduceat's rule v0 + (((v1+v2)+v3)+...).
+template <bool VALUES, int MAXR_, int BLOCK>
+__device__ __forceinline__ int process_column(const SegTable &T, int64_t col_lo, int64_t cl,
+                                              const int32_t *__restrict__ adj_ptr, const int32_t *__restrict__ adj,
+                                              int32_t *R, double *V0, double *S, int &m_out,
+                                              const int64_t *__restrict__ col_ptr, int64_t *__restrict__ row_idx,
+                                              double *__restrict__ vals, uint32_t *__restrict__ status) {
     const int32_t c = (int32_t)(col_lo + cl);
     const int32_t beg = __ldg(adj_ptr + cl), end = __ldg(adj_ptr + cl + 1);
     const int deg = end - beg;
     if (deg > MAXDEG) {
         atomicOr(status, HX_ST_DEG_OVERFLOW);
-        if (!VALUES) counts[cl] = 0;
-        return;
+        return COL_FATAL;
     }
     int32_t ent[8];
 #pragma unroll
@@ -164,12 +167,9 @@ column_kernel(SegTable T, int64_t col_lo, int64_t ncols, const int32_t *__restri
     for (int k = 1; k < 8; ++k) {
         if (k < deg && (ent[k] >> 3) == (ent[k - 1] >> 3)) {
             atomicOr(status, HX_ST_REPEATED_NODE);
-            if (!VALUES) counts[cl] = 0;
-            return;
+            return COL_FATAL;
         }
     }
-
-    int32_t *R = sR + t;
     int m = 0;
     bool ok = true;
 #pragma unroll
@@ -178,24 +178,16 @@ column_kernel(SegTable T, int64_t col_lo, int64_t ncols, const int32_t *__restri
             const int64_t e = ent[k] >> 3;
             const int s = seg_of(T, e);
             int32_t g[8];
-            load_conn8(T.conn[s], e - T.start[s], g);
+            load_conn8(T.conn[s], e - T.start[s], T.conn_stride[s], g);
 #pragma unroll
             for (int b = 0; b < 8; ++b)
-                if (g[b] >= c) ok &= insert_row(R, m, g[b]);
+                if (g[b] >= c) ok &= insert_row<MAXR_, BLOCK>(R, m, g[b]);
         }
     }
-    if (!ok) {
-        atomicOr(status, HX_ST_ROW_OVERFLOW);
-        if (!VALUES) counts[cl] = 0;
-        return;
-    }
-    if (!VALUES) {
-        counts[cl] = m;
-        return;
-    }
+    m_out = m;
+    if (!ok) return COL_ROWS_OVERFLOW;
+    if (!VALUES) return COL_OK;
 
-    double *V0 = sV0 + t;
-    double *S = sS + t;
     uint32_t has0 = 0, has1 = 0;
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
@@ -205,8 +197,8 @@ column_kernel(SegTable T, int64_t col_lo, int64_t ncols, const int32_t *__restri
             const int s = seg_of(T, e);
             const int64_t el = e - T.start[s];
             int32_t g[8];
-            load_conn8(T.conn[s], el, g);
-            const double *kr = T.ke[s] + 36 * el;
+            load_conn8(T.conn[s], el, T.conn_stride[s], g);
+            const double *kr = T.ke[s] + T.ke_stride[s] * el;
             double x[8];
 #pragma unroll
             for (int b = 0; b < 8; ++b) {
@@ -216,16 +208,16 @@ column_kernel(SegTable T, int64_t col_lo, int64_t ncols, const int32_t *__restri
 #pragma unroll
             for (int b = 0; b < 8; ++b) {
                 if (g[b] >= c) {
-                    const int j = find_row(R, m, g[b]);
+                    const int j = find_row<BLOCK>(R, m, g[b]);
                     const uint32_t bit = 1u << j;
                     if (!(has0 & bit)) {
-                        V0[j * COL_BLOCK] = x[b];
+                        V0[j * BLOCK] = x[b];
                         has0 |= bit;
                     } else if (!(has1 & bit)) {
-                        S[j * COL_BLOCK] = x[b];
+                        S[j * BLOCK] = x[b];
                         has1 |= bit;
                     } else {
-                        S[j * COL_BLOCK] = __dadd_rn(S[j * COL_BLOCK], x[b]);
+                        S[j * BLOCK] = __dadd_rn(S[j * BLOCK], x[b]);
                     }
                 }
             }
@@ -234,9 +226,57 @@ column_kernel(SegTable T, int64_t col_lo, int64_t ncols, const int32_t *__restri
     const int64_t base = col_ptr[cl];
     for (int j = 0; j < m; ++j) {
         const uint32_t bit = 1u << j;
-        const double v0 = V0[j * COL_BLOCK];
-        row_idx[base + j] = R[j * COL_BLOCK];
-        vals[base + j] = (has1 & bit) ? __dadd_rn(v0, S[j * COL_BLOCK]) : v0;
+        const double v0 = V0[j * BLOCK];
+        row_idx[base + j] = R[j * BLOCK];
+        vals[base + j] = (has1 & bit) ? __dadd_rn(v0, S[j * BLOCK]) : v0;
+    }
+    return COL_OK;
+}
+
+// 4./6. per-column pass, narrow tier: every column with <= MAXR rows.  Wider columns are
+// appended to `wide_list` (count mode) / skipped (values mode) and handled by the wide tier.
+template <bool VALUES>
+__global__ void __launch_bounds__(COL_BLOCK)
+column_kernel(SegTable T, int64_t col_lo, int64_t ncols, const int32_t *__restrict__ adj_ptr,
+              const int32_t *__restrict__ adj, int32_t *__restrict__ counts, int32_t *__restrict__ wide_list,
+              int32_t *__restrict__ wide_count, const int64_t *__restrict__ col_ptr,
+              int64_t *__restrict__ row_idx, double *__restrict__ vals, uint32_t *__restrict__ status) {
+    __shared__ int32_t sR[MAXR * COL_BLOCK];
+    __shared__ double sV0[VALUES ? MAXR * COL_BLOCK : 1];
+    __shared__ double sS[VALUES ? MAXR * COL_BLOCK : 1];
+    const int t = threadIdx.x;
+    const int64_t cl = (int64_t)blockIdx.x * COL_BLOCK + t;
+    if (cl >= ncols) return;
+    if (VALUES && col_ptr[cl + 1] - col_ptr[cl] > MAXR) return;  // wide tier's column
+    int m = 0;
+    const int r = process_column<VALUES, MAXR, COL_BLOCK>(T, col_lo, cl, adj_ptr, adj, sR + t, sV0 + t, sS + t, m,
+                                                          col_ptr, row_idx, vals, status);
+    if (!VALUES) {
+        counts[cl] = r == COL_OK ? m : 0;
+        if (r == COL_ROWS_OVERFLOW) wide_list[atomicAdd(wide_count, 1)] = (int32_t)cl;
+    }
+}
+
+// Wide tier: columns listed by the narrow count pass (up to WIDE_MAXR rows; e.g. randomly
+// numbered meshes, where the smallest id of a 27-node neighbourhood owns 27 rows).
+template <bool VALUES>
+__global__ void __launch_bounds__(WIDE_BLOCK)
+column_wide_kernel(SegTable T, int64_t col_lo, const int32_t *__restrict__ adj_ptr, const int32_t *__restrict__ adj,
+                   int32_t *__restrict__ counts, const int32_t *__restrict__ wide_list,
+                   const int32_t *__restrict__ wide_count, const int64_t *__restrict__ col_ptr,
+                   int64_t *__restrict__ row_idx, double *__restrict__ vals, uint32_t *__restrict__ status) {
+    __shared__ int32_t sR[WIDE_MAXR * WIDE_BLOCK];
+    __shared__ double sV0[VALUES ? WIDE_MAXR * WIDE_BLOCK : 1];
+    __shared__ double sS[VALUES ? WIDE_MAXR * WIDE_BLOCK : 1];
+    const int t = threadIdx.x;
+    const int n = *wide_count;
+    for (int i = blockIdx.x * WIDE_BLOCK + t; i < n; i += gridDim.x * WIDE_BLOCK) {
+        const int64_t cl = wide_list[i];
+        int m = 0;
+        const int r = process_column<VALUES, WIDE_MAXR, WIDE_BLOCK>(T, col_lo, cl, adj_ptr, adj, sR + t, sV0 + t,
+                                                                    sS + t, m, col_ptr, row_idx, vals, status);
+        if (r == COL_ROWS_OVERFLOW) atomicOr(status, HX_ST_ROW_OVERFLOW);
+        if (!VALUES) counts[cl] = r == COL_OK ? m : 0;
     }
 }
 
@@ -246,9 +286,9 @@ struct CastI64 {
 
 // Workspace layout (all offsets 256-B aligned):
 //   adj_ptr  (ncols+1) i32 | cursor/deg (ncols+1) i32 | counts (ncols+1) i32 |
-//   adj (8*n_total) i32 | cub temp
+//   adj (8*n_total) i32 | wide_list (ncols) i32 | wide_count i32 | cub temp
 struct MeshWs {
-    int32_t *adj_ptr, *deg, *counts, *adj;
+    int32_t *adj_ptr, *deg, *counts, *adj, *wide_list, *wide_count;
     void *cub_tmp;
     size_t cub_bytes;
     size_t total;
@@ -274,6 +314,8 @@ static MeshWs mesh_ws_layout(void *base, int64_t n_total, int64_t ncols) {
     const size_t o_deg = take(sizeof(int32_t) * (ncols + 1));
     const size_t o_cnt = take(sizeof(int32_t) * (ncols + 1));
     const size_t o_adj = take(sizeof(int32_t) * 8 * std::max<int64_t>(n_total, 1));
+    const size_t o_wl = take(sizeof(int32_t) * std::max<int64_t>(ncols, 1));
+    const size_t o_wc = take(sizeof(int32_t));
     w.cub_bytes = cub_scan_bytes(ncols);
     const size_t o_cub = take(w.cub_bytes);
     w.total = off;
@@ -283,6 +325,8 @@ static MeshWs mesh_ws_layout(void *base, int64_t n_total, int64_t ncols) {
         w.deg = (int32_t *)(b + o_deg);
         w.counts = (int32_t *)(b + o_cnt);
         w.adj = (int32_t *)(b + o_adj);
+        w.wide_list = (int32_t *)(b + o_wl);
+        w.wide_count = (int32_t *)(b + o_wc);
         w.cub_tmp = b + o_cub;
     }
     return w;
@@ -305,6 +349,12 @@ static int make_segtable(const hx_elem_segment *segs, int32_t n_segs, SegTable &
         }
         T.conn[s] = segs[s].conn;
         T.ke[s] = segs[s].ke;
+        T.conn_stride[s] = segs[s].conn_stride ? segs[s].conn_stride : 8;
+        T.ke_stride[s] = segs[s].ke_stride ? segs[s].ke_stride : 36;
+        if (T.conn_stride[s] < 8 || T.conn_stride[s] % 4 != 0 || T.ke_stride[s] < 36) {
+            set_last_error("mesh csc: bad strides in segment %d", s);
+            return HX_ERR_VALUE;
+        }
         T.start[s] = acc;
         acc += segs[s].n_el;
     }
@@ -316,6 +366,10 @@ static int make_segtable(const hx_elem_segment *segs, int32_t n_segs, SegTable &
         return HX_ERR_CONFIG;
     }
     return HX_OK;
+}
+
+static unsigned wide_grid(int64_t ncols) {
+    return (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(ncols, WIDE_BLOCK), 148 * 8));
 }
 
 static unsigned grid_for(int64_t n, int threads) {
@@ -367,10 +421,15 @@ extern "C" int hx_mesh_csc_symbolic(const hx_elem_segment *segs, int32_t n_segs,
         HX_CHECK_LAUNCH("adjacency_fill_kernel");
     }
     HX_TRY_CUDA(cudaMemsetAsync(w.counts + ncols, 0, sizeof(int32_t), s));
+    HX_TRY_CUDA(cudaMemsetAsync(w.wide_count, 0, sizeof(int32_t), s));
     if (ncols > 0) {
         column_kernel<false><<<(unsigned)ceil_div(ncols, COL_BLOCK), COL_BLOCK, 0, s>>>(
-            T, col_lo, ncols, w.adj_ptr, w.adj, w.counts, nullptr, nullptr, nullptr, status);
+            T, col_lo, ncols, w.adj_ptr, w.adj, w.counts, w.wide_list, w.wide_count, nullptr, nullptr, nullptr,
+            status);
         HX_CHECK_LAUNCH("column_kernel<count>");
+        column_wide_kernel<false><<<wide_grid(ncols), WIDE_BLOCK, 0, s>>>(
+            T, col_lo, w.adj_ptr, w.adj, w.counts, w.wide_list, w.wide_count, nullptr, nullptr, nullptr, status);
+        HX_CHECK_LAUNCH("column_wide_kernel<count>");
     }
     auto it = cub::TransformInputIterator<int64_t, CastI64, const int32_t *>(w.counts, CastI64());
     cb = w.cub_bytes;
@@ -394,8 +453,11 @@ extern "C" int hx_mesh_csc_numeric(const hx_elem_segment *segs, int32_t n_segs, 
     cudaStream_t s = (cudaStream_t)stream;
     if (ncols > 0) {
         column_kernel<true><<<(unsigned)ceil_div(ncols, COL_BLOCK), COL_BLOCK, 0, s>>>(
-            T, col_lo, ncols, w.adj_ptr, w.adj, nullptr, col_ptr, row_idx, vals, status);
+            T, col_lo, ncols, w.adj_ptr, w.adj, nullptr, nullptr, nullptr, col_ptr, row_idx, vals, status);
         HX_CHECK_LAUNCH("column_kernel<values>");
+        column_wide_kernel<true><<<wide_grid(ncols), WIDE_BLOCK, 0, s>>>(
+            T, col_lo, w.adj_ptr, w.adj, nullptr, w.wide_list, w.wide_count, col_ptr, row_idx, vals, status);
+        HX_CHECK_LAUNCH("column_wide_kernel<values>");
     }
     return HX_OK;
 }

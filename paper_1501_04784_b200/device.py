@@ -189,24 +189,35 @@ def _status_error(st: int):
         raise MeshValidationError("triplet entry above the diagonal")
 
 
+def _check_segment(conn, ke):
+    n = conn.shape[0]
+    if conn.dtype != torch.int32 or tuple(conn.shape) != (n, 8) or conn.device.type != "cuda":
+        raise ValueError("segment conn must be a CUDA int32 (n, 8) tensor")
+    if ke.dtype != torch.float64 or tuple(ke.shape) != (n, 36) or ke.device.type != conn.device.type:
+        raise ValueError("segment ke must be a CUDA float64 (n, 36) tensor")
+    if n and (conn.stride(1) != 1 or conn.stride(0) % 4 or conn.stride(0) < 8 or conn.data_ptr() % 16):
+        raise ValueError("segment conn rows must be 16-byte aligned with unit inner stride")
+    if n and (ke.stride(1) != 1 or ke.stride(0) < 36):
+        raise ValueError("segment ke rows must have unit inner stride")
+
+
 def mesh_csc(parts, n_nodes: int, col_lo: int = 0, col_hi: int | None = None, stream=None) -> DeviceCsc:
     """Assemble columns [col_lo, col_hi) of the lower CSC from element segments.
 
-    ``parts`` is a list of (conn (n,8) i32, ke (n,36) f64) CUDA tensor pairs in ascending global
-    element order (one pair for a single GPU; halo segments for the multi-GPU path).  Meshes
-    outside the node-adjacency fast path's limits fall through to the generic triplet path
-    with identical results.
+    ``parts`` is a list of (conn (n,8) i32, ke (n,36) f64) CUDA tensor views in ascending global
+    element order (one pair for a single GPU; halo record views for the multi-GPU path -- rows
+    may be strided).  Meshes outside the node-adjacency fast path's limits fall through to the
+    generic triplet path with identical results.
     """
     col_hi = n_nodes if col_hi is None else col_hi
-    if len(parts) > N.MAX_SEGMENTS:
-        raise ValueError(f"at most {N.MAX_SEGMENTS} element segments")
+    if not 1 <= len(parts) <= N.MAX_SEGMENTS:
+        raise ValueError(f"1..{N.MAX_SEGMENTS} element segments required")
     dev = parts[0][0].device
     for conn, ke in parts:
-        _check_tensor(conn, torch.int32, (conn.shape[0], 8), "conn")
-        _check_tensor(ke, torch.float64, (conn.shape[0], 36), "ke")
+        _check_segment(conn, ke)
     n_total = sum(int(c.shape[0]) for c, _ in parts)
     ncols = col_hi - col_lo
-    segs = N.segments([(c.data_ptr(), k.data_ptr(), int(c.shape[0])) for c, k in parts])
+    segs = N.segments([(c.data_ptr(), k.data_ptr(), int(c.shape[0]), c.stride(0), k.stride(0)) for c, k in parts])
     ws_bytes = N.lib().hx_mesh_csc_workspace_bytes(n_total, ncols)
     if ws_bytes < 0:
         raise ValueError("bad mesh size")
@@ -231,10 +242,10 @@ def mesh_csc(parts, n_nodes: int, col_lo: int = 0, col_hi: int | None = None, st
 def _mesh_csc_generic(parts, n_nodes, col_lo, col_hi, stream) -> DeviceCsc:
     rows_l, cols_l, vals_l = [], [], []
     for conn, ke in parts:
-        r, c = connectivity_index_arrays(conn, stream=stream)
+        r, c = connectivity_index_arrays(conn.contiguous(), stream=stream)
         rows_l.append(r)
         cols_l.append(c)
-        vals_l.append(ke.reshape(-1))
+        vals_l.append(ke.contiguous().reshape(-1))
     rows, cols, vals = torch.cat(rows_l), torch.cat(cols_l), torch.cat(vals_l)
     if col_lo != 0 or col_hi != n_nodes:
         keep = (cols >= col_lo) & (cols < col_hi)

@@ -1,0 +1,297 @@
+"""Multi-GPU construction: element-range shards, column blocks, one all-to-all of element halos.
+
+Rank r of G (one process per GPU, torch.distributed over NCCL):
+
+1. integrates its contiguous element range E_r = [n_el*r/G, n_el*(r+1)/G) -- KE + fused iK/jK,
+   exactly the single-GPU kernel on a slice of the mesh;
+2. owns the lower-CSC column block C_r = [n_nodes*r/G, n_nodes*(r+1)/G) (a column block of the
+   lower triangle is a row block of K by symmetry).  Column nnz is <= 27 and near-uniform on
+   conforming hex meshes, so an equal node split is an equal nnz split;
+3. sends every owned element that has a node in another rank's block to that rank -- one
+   all-to-all of 320-byte records (36 KE values + 8 node ids), packed destination-major in
+   ascending element order by hx_halo_pack;
+4. assembles its block from the segments [received from lower ranks | own | received from
+   higher ranks], which are in ascending global element order, so every duplicate position is
+   summed in the single-GPU order: the concatenated blocks are bitwise equal to G = 1.
+
+The global K is the concatenation of the blocks; global col_ptr = block col_ptr + exclusive
+scan of the block nnz (one all-gather of G int64).
+
+The collective is behind a small ``Exchange`` interface (torch.distributed for NCCL/gloo, a
+loopback for simulating G ranks in one process) and the per-rank compute behind ``Ops`` (the
+CUDA ops by default), so the host logic is tested with gloo on CPU and the CUDA path with the
+loopback on one GPU.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+__all__ = ["element_ranges", "column_bounds", "ShardedBuild", "TorchExchange", "LoopbackExchange", "CudaOps",
+           "run_loopback", "RECORD_DOUBLES"]
+
+RECORD_DOUBLES = 40  # 36 packed KE values + 8 int32 node ids
+
+
+def element_ranges(n_el: int, world: int):
+    return [(n_el * r // world, n_el * (r + 1) // world) for r in range(world)]
+
+
+def column_bounds(n_nodes: int, world: int) -> np.ndarray:
+    return np.array([n_nodes * r // world for r in range(world + 1)], dtype=np.int64)
+
+
+# ------------------------------------------------------------------------------------------
+# collectives
+# ------------------------------------------------------------------------------------------
+class TorchExchange:
+    """torch.distributed all-to-all (NCCL on GPUs, gloo on CPU)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.group = group
+
+    def counts(self, send_counts: torch.Tensor) -> torch.Tensor:
+        recv = torch.empty_like(send_counts)
+        self.dist.all_to_all_single(recv, send_counts, group=self.group)
+        return recv
+
+    def records(self, send: torch.Tensor, send_splits, recv_splits) -> torch.Tensor:
+        recv = torch.empty((sum(recv_splits), RECORD_DOUBLES), dtype=send.dtype, device=send.device)
+        self.dist.all_to_all_single(recv, send, output_split_sizes=list(recv_splits),
+                                    input_split_sizes=list(send_splits), group=self.group)
+        return recv
+
+    def allgather_int(self, value: int, device) -> list:
+        t = torch.tensor([value], dtype=torch.int64, device=device)
+        out = [torch.empty_like(t) for _ in range(self.dist.get_world_size(self.group))]
+        self.dist.all_gather(out, t, group=self.group)
+        return [int(x.item()) for x in out]
+
+
+# ------------------------------------------------------------------------------------------
+# per-rank compute (CUDA)
+# ------------------------------------------------------------------------------------------
+class CudaOps:
+    """The device kernels of libhexfem_b200.so."""
+
+    def __init__(self, device=None, mode="exact"):
+        from . import device as D
+
+        self.D = D
+        self.device = D.require_device(device)
+        self.mode = mode
+
+    def upload(self, coords, conn, coeff):
+        def up(a, dt):
+            return torch.from_numpy(np.ascontiguousarray(a, dtype=dt)).to(self.device)
+
+        return self.D.DeviceMesh(up(coords, np.float64), up(conn, np.int32), up(coeff, np.float64))
+
+    def integrate(self, dm):
+        ke, rows, cols, fail = self.D.integrate_mesh(dm, mode=self.mode)
+        return ke, rows, cols, fail
+
+    def check_fail(self, fail, offset):
+        self.D.raise_if_failed(fail, offset)
+
+    def halo(self, dm, ke, bounds_dev, world, rank):
+        """-> (records (S, 40) f64, per_dest (world,) int64 host list)"""
+        from . import _native as N
+
+        n = dm.n_el
+        ws_bytes = N.lib().hx_halo_workspace_bytes(n, world)
+        ws = torch.empty(ws_bytes, dtype=torch.uint8, device=self.device)
+        per_dest = torch.empty(world, dtype=torch.int64, device=self.device)
+        sh = self.D.stream_handle()
+        N.check(N.lib().hx_halo_count(self.D._ptr(dm.conn), n, self.D._ptr(bounds_dev), world, rank,
+                                      self.D._ptr(per_dest), self.D._ptr(ws), ws_bytes, sh), "hx_halo_count")
+        counts = per_dest.cpu().tolist()
+        records = torch.empty((max(sum(counts), 0), RECORD_DOUBLES), dtype=torch.float64, device=self.device)
+        N.check(N.lib().hx_halo_pack(self.D._ptr(dm.conn), self.D._ptr(ke), n, self.D._ptr(bounds_dev), world, rank,
+                                     self.D._ptr(records), self.D._ptr(ws), sh), "hx_halo_pack")
+        return records, counts
+
+    def bounds(self, bounds_np):
+        return torch.from_numpy(bounds_np).to(self.device)
+
+    def assemble(self, segments, n_nodes, c_lo, c_hi):
+        return self.D.mesh_csc(segments, n_nodes, c_lo, c_hi)
+
+
+def record_segment(records: torch.Tensor):
+    """(n, 40) f64 records -> (conn (n, 8) int32 view, ke (n, 36) f64 view), no copy."""
+    as_i32 = records.view(torch.int32)
+    return as_i32[:, 72:80], records[:, :36]
+
+
+@dataclass
+class ShardResult:
+    col_ptr: torch.Tensor  # local, starts at 0
+    row_idx: torch.Tensor
+    vals: torch.Tensor
+    col_lo: int
+    col_hi: int
+    nnz_offset: int = 0
+
+
+class ShardedBuild:
+    """One rank's share of the global build (see module docstring)."""
+
+    def __init__(self, mesh, rank: int, world: int, mode: str = "exact", ops=None, exchange=None):
+        self.rank, self.world = rank, world
+        self.ops = ops if ops is not None else CudaOps(mode=mode)
+        self.exchange = exchange if exchange is not None else TorchExchange()
+        self.n_el, self.n_nodes = mesh.n_el, mesh.n_nodes
+        self.e_lo, self.e_hi = element_ranges(mesh.n_el, world)[rank]
+        self.bounds_np = column_bounds(mesh.n_nodes, world)
+        self.c_lo, self.c_hi = int(self.bounds_np[rank]), int(self.bounds_np[rank + 1])
+        self.dm = self.ops.upload(mesh.coords, mesh.connectivity[self.e_lo:self.e_hi],
+                                  mesh.coefficient[self.e_lo:self.e_hi])
+        self.bounds = self.ops.bounds(self.bounds_np)
+        self.last = None
+        self.last_index = None
+
+    # -- phases (so a loopback driver can interleave G ranks in one process) --
+    def phase_local(self):
+        ke, rows, cols, fail = self.ops.integrate(self.dm)
+        records, send_counts = self.ops.halo(self.dm, ke, self.bounds, self.world, self.rank)
+        self._pending = (ke, rows, cols, fail)
+        return records, send_counts
+
+    def phase_assemble(self, recv: torch.Tensor, recv_counts):
+        ke, rows, cols, fail = self._pending
+        self._pending = None
+        n_lower = int(sum(recv_counts[:self.rank]))
+        segments = []
+        if n_lower:
+            segments.append(record_segment(recv[:n_lower]))
+        segments.append((self.dm.conn, ke))
+        if recv.shape[0] > n_lower:
+            segments.append(record_segment(recv[n_lower:]))
+        self.ops.check_fail(fail, self.e_lo)
+        csc = self.ops.assemble(segments, self.n_nodes, self.c_lo, self.c_hi)
+        self.last = ShardResult(csc.col_ptr, csc.row_idx, csc.vals, self.c_lo, self.c_hi)
+        self.last_index = (ke, rows, cols)
+        return self.last
+
+    def step(self):
+        records, send_counts = self.phase_local()
+        dev = records.device
+        recv_counts = self.exchange.counts(torch.tensor(send_counts, dtype=torch.int64, device=dev)).cpu().tolist()
+        recv = self.exchange.records(records, send_counts, recv_counts)
+        return self.phase_assemble(recv, recv_counts)
+
+    def global_nnz(self) -> int:
+        nnzs = self.exchange.allgather_int(int(self.last.row_idx.shape[0]), self.last.row_idx.device)
+        self.last.nnz_offset = int(sum(nnzs[:self.rank]))
+        return int(sum(nnzs))
+
+    # -- benchmark helpers --
+    def stage_times(self, repeats=3):
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        acc = {"ke_ms": 0.0, "halo_exchange_ms": 0.0, "assembly_ms": 0.0}
+        for _ in range(repeats):
+            ev[0].record()
+            ke, rows, cols, fail = self.ops.integrate(self.dm)
+            ev[1].record()
+            records, send_counts = self.ops.halo(self.dm, ke, self.bounds, self.world, self.rank)
+            dev = records.device
+            recv_counts = self.exchange.counts(torch.tensor(send_counts, dtype=torch.int64, device=dev)).cpu().tolist()
+            recv = self.exchange.records(records, send_counts, recv_counts)
+            ev[2].record()
+            self._pending = (ke, rows, cols, fail)
+            self.phase_assemble(recv, recv_counts)
+            ev[3].record()
+            torch.cuda.synchronize()
+            acc["ke_ms"] += ev[0].elapsed_time(ev[1]) / repeats
+            acc["halo_exchange_ms"] += ev[1].elapsed_time(ev[2]) / repeats
+            acc["assembly_ms"] += ev[2].elapsed_time(ev[3]) / repeats
+        acc["launches_per_step"] = 10 + 5  # single-GPU set + halo count/scan(2)/totals/pack
+        return acc
+
+    def measure_e2e(self, steps, barrier):
+        """Host shard in (pinned) -> build -> CSC block out (pinned), max over ranks."""
+        import torch.distributed as dist
+
+        D = self.ops.D
+        h = [t.cpu().pin_memory() for t in (self.dm.coords, self.dm.conn, self.dm.coeff)]
+        self.step()
+        nnz = int(self.last.row_idx.shape[0])
+        o = [torch.empty(self.c_hi - self.c_lo + 1, dtype=torch.int64, pin_memory=True),
+             torch.empty(nnz, dtype=torch.int64, pin_memory=True), torch.empty(nnz, dtype=torch.float64, pin_memory=True)]
+        dev = self.ops.device
+        keep = self.dm
+
+        def one():
+            self.dm = D.DeviceMesh(*(t.to(dev, non_blocking=True) for t in h))
+            r = self.step()
+            o[0].copy_(r.col_ptr, non_blocking=True)
+            o[1].copy_(r.row_idx, non_blocking=True)
+            o[2].copy_(r.vals, non_blocking=True)
+
+        one()
+        torch.cuda.synchronize()
+        barrier()
+        start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        start.record()
+        for _ in range(steps):
+            one()
+        stop.record()
+        torch.cuda.synchronize()
+        ms = torch.tensor([start.elapsed_time(stop) / steps], dtype=torch.float64, device=dev)
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+        self.dm = keep
+        h2d = sum(t.numel() * t.element_size() for t in h)
+        d2h = sum(t.numel() * t.element_size() for t in o)
+        tot = torch.tensor([h2d, d2h], dtype=torch.int64, device=dev)
+        dist.all_reduce(tot)
+        return {"value": self.n_el / (float(ms.item()) / 1e3), "unit": "elements/s",
+                "h2d_bytes_per_step": int(tot[0]), "d2h_bytes_per_step": int(tot[1]),
+                "ms_per_step": float(ms.item()), "steps": steps,
+                "api": "per-rank shard (pinned host -> HBM) + ShardedBuild.step + CSC block -> pinned host"}
+
+
+# ------------------------------------------------------------------------------------------
+# loopback: G virtual ranks in one process (tests the CUDA sharded path on one GPU)
+# ------------------------------------------------------------------------------------------
+class LoopbackExchange:
+    def allgather_int(self, value, device):
+        raise NotImplementedError("use run_loopback")
+
+
+def run_loopback(mesh, world: int, ops_factory):
+    """Run all G ranks' phases in one process; returns the list of ShardResult (rank order)."""
+    ranks = [ShardedBuild(mesh, r, world, ops=ops_factory(), exchange=LoopbackExchange()) for r in range(world)]
+    sends = [rk.phase_local() for rk in ranks]
+    results = []
+    for r, rk in enumerate(ranks):
+        parts, recv_counts = [], []
+        for s, (records, counts) in enumerate(sends):
+            off = int(sum(counts[:r]))
+            parts.append(records[off:off + counts[r]])
+            recv_counts.append(int(counts[r]))
+        recv = torch.cat(parts) if parts else sends[r][0][:0]
+        results.append(rk.phase_assemble(recv, recv_counts))
+    off = 0
+    for res in results:
+        res.nnz_offset = off
+        off += int(res.row_idx.shape[0])
+    return results
+
+
+def concat_blocks(results):
+    """Global (col_ptr, row_idx, vals) from the rank blocks (host numpy)."""
+    col_ptr = [np.zeros(1, dtype=np.int64)]
+    rows, vals = [], []
+    for res in results:
+        cp = res.col_ptr.cpu().numpy()
+        col_ptr.append(cp[1:] + res.nnz_offset)
+        rows.append(res.row_idx.cpu().numpy())
+        vals.append(res.vals.cpu().numpy())
+    return np.concatenate(col_ptr), np.concatenate(rows), np.concatenate(vals)
