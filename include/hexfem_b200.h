@@ -52,7 +52,7 @@ extern "C" {
  * triplet path (hx_triplet_csc_*), which has no such limits. */
 
 #define HX_MAX_NODE_DEGREE 8
-#define HX_MAX_COL_ROWS 16
+#define HX_MAX_COL_ROWS 32
 
 /* Integration modes. */
 #define HX_MODE_EXACT 0 /* reference operation order, no FMA: bitwise equal to the reference */
@@ -87,6 +87,9 @@ void hx_dn_table(double *out192);
 void hx_pack_tables(int32_t *rows36, int32_t *cols36);
 /* Number of streaming multiprocessors of the current device (0 when no device). */
 int hx_device_sm_count(void);
+/* Self-test of the exact-mode quotient (reciprocal + two Markstein corrections) against IEEE
+ * division on n generated operand pairs; result2 (device, 2 x u64) = {mismatches, tested}. */
+int hx_selftest_division(uint64_t n, uint64_t seed, unsigned long long *result2, void *stream);
 
 /* ---- numerical integration (Alg. 2) ----------------------------------------------------- */
 /* element.py:213-245: coords (n,8,3) f64 pre-gathered, coeff (n,) f64 -> out (n,36) f64.
@@ -110,17 +113,25 @@ int hx_connectivity_index_arrays(const int32_t *conn, int64_t lo, int64_t hi, in
 /* ---- mesh-path assembly (node-adjacency symbolic + deterministic column numeric) ---------
  * Builds the lower-triangular CSC block for columns [col_lo, col_hi) of a mesh with
  * n_nodes nodes, from element segments in ascending global element order.
- *   symbolic: writes col_ptr (col_hi-col_lo+1) i64, col_ptr[0] = 0; nnz = col_ptr[last].
- *   numeric:  writes row_idx (nnz) i64 and vals (nnz) f64, summing duplicates in element
- *             order with numpy add.reduceat's rule (bitwise equal to assemble.py:135).
+ *   symbolic: writes col_ptr (col_hi-col_lo+1) i64 (col_ptr[0] = 0, nnz = col_ptr[last]) and
+ *             row_idx i64 (ascending within each column) for the first row_capacity entries;
+ *             when nnz > row_capacity the caller re-runs symbolic with row_capacity >= nnz.
+ *   numeric:  writes vals (nnz) f64, summing duplicates in element order with numpy
+ *             add.reduceat's rule (bitwise equal to assemble.py:135).
  * The workspace written by symbolic must be passed unchanged to numeric. */
 int64_t hx_mesh_csc_workspace_bytes(int64_t n_el_total, int64_t n_cols);
 int hx_mesh_csc_symbolic(const hx_elem_segment *segs, int32_t n_segs, int64_t n_nodes,
-                         int64_t col_lo, int64_t col_hi, int64_t *col_ptr, void *workspace,
-                         int64_t workspace_bytes, uint32_t *status, void *stream);
+                         int64_t col_lo, int64_t col_hi, int64_t *col_ptr, int64_t *row_idx,
+                         int64_t row_capacity, void *workspace, int64_t workspace_bytes,
+                         uint32_t *status, void *stream);
+/* symbolic + numeric in one pass (the cold build): col_ptr, row_idx and vals, the latter two for
+ * the first `capacity` entries (re-run with capacity >= nnz when short). */
+int hx_mesh_csc_build(const hx_elem_segment *segs, int32_t n_segs, int64_t n_nodes, int64_t col_lo,
+                      int64_t col_hi, int64_t *col_ptr, int64_t *row_idx, double *vals, int64_t capacity,
+                      void *workspace, int64_t workspace_bytes, uint32_t *status, void *stream);
 int hx_mesh_csc_numeric(const hx_elem_segment *segs, int32_t n_segs, int64_t col_lo,
-                        int64_t col_hi, const int64_t *col_ptr, int64_t *row_idx, double *vals,
-                        const void *workspace, uint32_t *status, void *stream);
+                        int64_t col_hi, const int64_t *col_ptr, const int64_t *row_idx,
+                        double *vals, const void *workspace, uint32_t *status, void *stream);
 
 /* ---- generic triplet -> CSC (assemble.py:110-149) ----------------------------------------
  * symbolic: validates (status bits BAD_INDEX / UPPER), stable-sorts by (col,row), finds the

@@ -24,8 +24,9 @@ MAX_SEGMENTS = 4
 # Every symbol declared in include/hexfem_b200.h (checked by tests/test_abi_cpu.py).
 EXPORTED = (
     "hx_abi_version", "hx_last_error", "hx_dn_table", "hx_pack_tables", "hx_device_sm_count",
+    "hx_selftest_division",
     "hx_stiffness_batch", "hx_integrate_mesh", "hx_connectivity_index_arrays",
-    "hx_mesh_csc_workspace_bytes", "hx_mesh_csc_symbolic", "hx_mesh_csc_numeric",
+    "hx_mesh_csc_workspace_bytes", "hx_mesh_csc_symbolic", "hx_mesh_csc_build", "hx_mesh_csc_numeric",
     "hx_triplet_csc_workspace_bytes", "hx_triplet_csc_symbolic", "hx_triplet_csc_numeric",
     "hx_halo_workspace_bytes", "hx_halo_count", "hx_halo_pack",
 )
@@ -64,11 +65,13 @@ def lib():
         "hx_dn_table": ([P], None),
         "hx_pack_tables": ([P, P], None),
         "hx_device_sm_count": ([], ctypes.c_int),
+        "hx_selftest_division": ([ctypes.c_uint64, ctypes.c_uint64, P, P], ctypes.c_int),
         "hx_stiffness_batch": ([P, P, I64, P, I32, P, P], ctypes.c_int),
         "hx_integrate_mesh": ([P, I64, P, P, I64, I64, P, P, P, I32, P, P], ctypes.c_int),
         "hx_connectivity_index_arrays": ([P, I64, I64, P, P, P], ctypes.c_int),
         "hx_mesh_csc_workspace_bytes": ([I64, I64], I64),
-        "hx_mesh_csc_symbolic": ([P, I32, I64, I64, I64, P, P, I64, P, P], ctypes.c_int),
+        "hx_mesh_csc_symbolic": ([P, I32, I64, I64, I64, P, P, I64, P, I64, P, P], ctypes.c_int),
+        "hx_mesh_csc_build": ([P, I32, I64, I64, I64, P, P, P, I64, P, I64, P, P], ctypes.c_int),
         "hx_mesh_csc_numeric": ([P, I32, I64, I64, P, P, P, P, P, P], ctypes.c_int),
         "hx_triplet_csc_workspace_bytes": ([I64, I64], I64),
         "hx_triplet_csc_symbolic": ([P, P, I64, I64, P, P, P, I64, P, P], ctypes.c_int),

@@ -22,8 +22,8 @@
 // regular vertices), distinct rows per column <= HX_MAX_COL_ROWS, no repeated node in an
 // element.  With degree <= 8 every duplicate run has <= 8 terms, where numpy's pairwise sum
 // degenerates to the sequential sum implemented here.
+#include <cub/block/block_scan.cuh>
 #include <cub/device/device_scan.cuh>
-#include <cub/iterator/transform_input_iterator.cuh>
 
 #include <algorithm>
 
@@ -31,12 +31,10 @@
 
 namespace hx {
 
-constexpr int COL_BLOCK = 128;
+constexpr int COL_BLOCK = 64;  // columns per tile (one thread per column in phase A)
 constexpr int MAXDEG = HX_MAX_NODE_DEGREE;
 constexpr int MAXR = HX_MAX_COL_ROWS;
 constexpr int MAX_SEGS = 4;
-constexpr int WIDE_MAXR = 32;
-constexpr int WIDE_BLOCK = 64;
 
 struct SegTable {
     const int32_t *conn[MAX_SEGS];
@@ -120,46 +118,29 @@ __device__ __forceinline__ void sort8(int32_t (&v)[8]) {
 
 // Sorted-unique insert into a per-thread list R[0..m) laid out [slot][BLOCK] in smem
 // (thread-fastest: conflict-free for any per-thread slot).  Returns false on overflow.
-template <int MAXR_, int BLOCK>
+template <int BLOCK>
 __device__ __forceinline__ bool insert_row(int32_t *R, int &m, int32_t v) {
     int pos = 0;
     while (pos < m && R[pos * BLOCK] < v) ++pos;
     if (pos < m && R[pos * BLOCK] == v) return true;
-    if (m == MAXR_) return false;
+    if (m == MAXR) return false;
     for (int q = m; q > pos; --q) R[q * BLOCK] = R[(q - 1) * BLOCK];
     R[pos * BLOCK] = v;
     ++m;
     return true;
 }
 
-template <int BLOCK>
-__device__ __forceinline__ int find_row(const int32_t *R, int m, int32_t v) {
-    int lo = 0, hi = m;  // lower_bound; v is known to be present
-    while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (R[mid * BLOCK] < v) lo = mid + 1; else hi = mid;
-    }
-    return lo;
-}
-
-enum ColResult { COL_OK = 0, COL_ROWS_OVERFLOW = 1, COL_FATAL = 2 };
-
-// One column: incident elements sorted by id, distinct rows >= c (sorted), and (VALUES) the
-// duplicate sums in element order with numpy reduceat's rule v0 + (((v1+v2)+v3)+...).
-template <bool VALUES, int MAXR_, int BLOCK>
-__device__ __forceinline__ int process_column(const SegTable &T, int64_t col_lo, int64_t cl,
-                                              const int32_t *__restrict__ adj_ptr, const int32_t *__restrict__ adj,
-                                              int32_t *R, double *V0, double *S, int &m_out,
-                                              const int64_t *__restrict__ col_ptr, int64_t *__restrict__ row_idx,
-                                              double *__restrict__ vals, uint32_t *__restrict__ status) {
-    const int32_t c = (int32_t)(col_lo + cl);
+// Incident elements of column cl, sorted by element id (= the stable triplet order).
+// Returns deg, or -1 with a status bit when the column is outside the fast path.
+__device__ __forceinline__ int incident_sorted(int64_t cl, const int32_t *__restrict__ adj_ptr,
+                                               const int32_t *__restrict__ adj, int32_t (&ent)[8],
+                                               uint32_t *__restrict__ status) {
     const int32_t beg = __ldg(adj_ptr + cl), end = __ldg(adj_ptr + cl + 1);
     const int deg = end - beg;
     if (deg > MAXDEG) {
         atomicOr(status, HX_ST_DEG_OVERFLOW);
-        return COL_FATAL;
+        return -1;
     }
-    int32_t ent[8];
 #pragma unroll
     for (int k = 0; k < 8; ++k) ent[k] = k < deg ? __ldg(adj + beg + k) : INT32_MAX;
     sort8(ent);
@@ -167,139 +148,331 @@ __device__ __forceinline__ int process_column(const SegTable &T, int64_t col_lo,
     for (int k = 1; k < 8; ++k) {
         if (k < deg && (ent[k] >> 3) == (ent[k - 1] >> 3)) {
             atomicOr(status, HX_ST_REPEATED_NODE);
-            return COL_FATAL;
+            return -1;
         }
     }
-    int m = 0;
-    bool ok = true;
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-        if (k < deg) {
-            const int64_t e = ent[k] >> 3;
-            const int s = seg_of(T, e);
-            int32_t g[8];
-            load_conn8(T.conn[s], e - T.start[s], T.conn_stride[s], g);
-#pragma unroll
-            for (int b = 0; b < 8; ++b)
-                if (g[b] >= c) ok &= insert_row<MAXR_, BLOCK>(R, m, g[b]);
-        }
-    }
-    m_out = m;
-    if (!ok) return COL_ROWS_OVERFLOW;
-    if (!VALUES) return COL_OK;
+    return deg;
+}
 
-    uint32_t has0 = 0, has1 = 0;
+// Decoupled look-back tile state: one 64-bit word, flag in the top 2 bits, value below.
+constexpr unsigned long long TILE_AGG = 1ull << 62, TILE_INC = 2ull << 62, TILE_VAL = (1ull << 62) - 1;
+
+__device__ __forceinline__ void tile_publish(unsigned long long *state, int64_t tile, unsigned long long word) {
+    atomicExch(state + tile, word);
+}
+__device__ __forceinline__ unsigned long long tile_read(const unsigned long long *state, int64_t tile) {
+    return *reinterpret_cast<const volatile unsigned long long *>(state + tile);
+}
+
+// Bitonic sorting network on 32 register-resident keys (ascending).
+__device__ __forceinline__ void sort32(int32_t (&v)[32]) {
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-        if (k < deg) {
+    for (int k = 2; k <= 32; k <<= 1)
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1)
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+                const int l = i ^ j;
+                if (l > i) {
+                    const int32_t a = v[i], b = v[l];
+                    const bool up = (i & k) == 0;
+                    v[i] = up ? min(a, b) : max(a, b);
+                    v[l] = up ? max(a, b) : min(a, b);
+                }
+            }
+}
+
+constexpr int32_t HASH_EMPTY = -1;
+constexpr int MAX_OFFDIAG_CONTRIB = 4;  // hex meshes: an edge is shared by at most 4 elements
+
+// Contribution word of an off-diagonal row: bits 0-2 count, then up to 4 entries of 9 bits
+// (incident-element slot k: 3 bits, packed KE index p: 6 bits), in ascending element order.
+__device__ __forceinline__ uint64_t contrib_push(uint64_t w, int k, int p) {
+    const uint64_t n = w & 7u;
+    return (w + 1u) | ((uint64_t)(k << 6 | p) << (3 + 9 * n));
+}
+
+// 4-6. The column pass.  One tile = COL_BLOCK consecutive columns (one thread per column in
+// phase A); the tile's output entries are spread over all threads in phase B.
+//   A1 incident elements sorted by id (= the stable triplet order) -> sE, their KE row
+//      pointers -> sP; distinct rows >= c via a 32-slot hash set, sorted by a register bitonic
+//      network -> sR (LOOKBACK), or read from row_idx (numeric-only mode);
+//   -  block scan of the row counts; the tile's aggregate is published right away;
+//   A2 (VALS) for every off-diagonal row the ordered list of contributing (element, packed
+//      index) pairs -> sM -- built while thread 0 looks back over the predecessor tiles
+//      (decoupled look-back; tiles are taken in scheduling order via a ticket);
+//   B  the tile's output entries in output order (coalesced row_idx / vals stores): diagonals
+//      (one per column, contributions from every incident element at its own local node), then
+//      off-diagonals; 1..8 gathered values reduced with numpy add.reduceat's rule
+//      v0 + (((v1 + v2) + v3) + ...).
+// ROWS: write row_idx.  VALS: compute vals.  LOOKBACK: compute the rows and col_ptr (else both
+// are inputs: the numeric-only pass of a symbolic/numeric split).
+template <bool ROWS, bool VALS, bool LOOKBACK>
+__global__ void __launch_bounds__(COL_BLOCK)
+column_pass_kernel(SegTable T, int64_t col_lo, int64_t ncols, const int32_t *__restrict__ adj_ptr,
+                   const int32_t *__restrict__ adj, int64_t *__restrict__ col_ptr, int64_t *__restrict__ row_idx,
+                   int64_t capacity, double *__restrict__ vals, unsigned long long *__restrict__ tile_state,
+                   int32_t *__restrict__ tile_ticket, uint32_t *__restrict__ status) {
+    __shared__ int32_t sR[MAXR * COL_BLOCK];            // hash set, then sorted rows: [slot][t]
+    __shared__ uint64_t sM[VALS ? MAXR * COL_BLOCK : 1];  // contribution words: [slot][t]
+    __shared__ const double *sP[VALS ? 8 * COL_BLOCK : 1];  // KE row of incident element k: [k][t]
+    __shared__ uint8_t sA[8 * COL_BLOCK];                 // local index of the column node in element k
+    __shared__ int32_t s_deg[COL_BLOCK];
+    __shared__ int32_t s_excl[COL_BLOCK + 1];
+    __shared__ int32_t s_dexcl[COL_BLOCK + 1];            // exclusive scan of (m - 1): off-diagonals
+    __shared__ int64_t s_base;
+    __shared__ int64_t s_tile;
+    using BlockScan = cub::BlockScan<int32_t, COL_BLOCK>;
+    __shared__ typename BlockScan::TempStorage scan_tmp;
+    const int t = threadIdx.x;
+    if (LOOKBACK) {
+        if (t == 0) s_tile = atomicAdd(tile_ticket, 1);
+        __syncthreads();
+    }
+    const int64_t tile = LOOKBACK ? s_tile : (int64_t)blockIdx.x;
+    const int64_t first = tile * COL_BLOCK;
+    const int64_t cl = first + t;
+    const int32_t c = (int32_t)(col_lo + cl);
+    int32_t *R = sR + t;
+
+    // ---- phase A1 ----
+    int m = 0, deg = 0;
+    bool ok = true;
+    int32_t ent[8];
+    if (cl < ncols) {
+        deg = incident_sorted(cl, adj_ptr, adj, ent, status);
+        if (deg < 0) {
+            deg = 0;
+            ok = false;
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            sA[k * COL_BLOCK + t] = (uint8_t)(ent[k] & 7);
+            if (VALS && k < deg) {
+                const int64_t e = ent[k] >> 3;
+                const int sg = seg_of(T, e);
+                sP[k * COL_BLOCK + t] = T.ke[sg] + T.ke_stride[sg] * (e - T.start[sg]);
+            }
+        }
+        if (LOOKBACK && ok) {
+#pragma unroll
+            for (int q = 0; q < MAXR; ++q) R[q * COL_BLOCK] = HASH_EMPTY;
+#pragma unroll 1
+            for (int k = 0; k < deg; ++k) {
+                int32_t g[8];
+                const int64_t e = ent[k] >> 3;
+                const int sg = seg_of(T, e);
+                load_conn8(T.conn[sg], e - T.start[sg], T.conn_stride[sg], g);
+#pragma unroll
+                for (int b = 0; b < 8; ++b) {
+                    const int32_t v = g[b];
+                    if (v < c) continue;
+                    uint32_t h = ((uint32_t)v * 0x9E3779B1u) >> 27;
+                    bool placed = false;
+#pragma unroll 1
+                    for (int probe = 0; probe < MAXR; ++probe) {
+                        const int32_t cur = R[h * COL_BLOCK];
+                        if (cur == v) {
+                            placed = true;
+                            break;
+                        }
+                        if (cur == HASH_EMPTY) {
+                            R[h * COL_BLOCK] = v;
+                            ++m;
+                            placed = true;
+                            break;
+                        }
+                        h = (h + 1) & (MAXR - 1);
+                    }
+                    ok &= placed;  // a full table: more than MAXR distinct rows
+                }
+            }
+            int32_t r[MAXR];
+#pragma unroll
+            for (int q = 0; q < MAXR; ++q) {
+                const int32_t v = R[q * COL_BLOCK];
+                r[q] = v == HASH_EMPTY ? INT32_MAX : v;
+            }
+            sort32(r);
+#pragma unroll
+            for (int q = 0; q < MAXR; ++q) R[q * COL_BLOCK] = r[q];
+            if (!ok) {
+                atomicOr(status, HX_ST_ROW_OVERFLOW);
+                m = 0;
+                deg = 0;
+            }
+        }
+    }
+
+    // ---- block scan of row counts (or read them back) ----
+    int64_t base = 0;
+    int total, excl;
+    if (LOOKBACK) {
+        BlockScan(scan_tmp).ExclusiveSum(m, excl, total);
+        if (t == 0 && tile == 0) tile_publish(tile_state, 0, TILE_INC | (unsigned long long)total);
+        if (t == 0 && tile > 0) tile_publish(tile_state, tile, TILE_AGG | (unsigned long long)total);
+    } else {
+        base = col_ptr[first];
+        const int64_t last = first + COL_BLOCK < ncols ? first + COL_BLOCK : ncols;
+        excl = cl <= ncols ? (int)(col_ptr[cl < last ? cl : last] - base) : 0;
+        total = (int)(col_ptr[last] - base);
+        if (cl < ncols) m = (int)(col_ptr[cl + 1] - col_ptr[cl]);
+        if (m > MAXR) {
+            ok = false;
+            m = 0;
+        }
+        if (cl < ncols && ok) {
+            for (int q = 0; q < m; ++q) R[q * COL_BLOCK] = (int32_t)row_idx[base + excl + q];
+        }
+    }
+    s_excl[t] = cl < ncols ? excl : total;
+    s_deg[t] = deg;
+    if (t == 0) s_excl[COL_BLOCK] = total;
+    {
+        int dex, dtot;
+        BlockScan(scan_tmp).ExclusiveSum(m > 0 ? m - 1 : 0, dex, dtot);
+        s_dexcl[t] = cl < ncols ? dex : dtot;
+        if (t == 0) s_dexcl[COL_BLOCK] = dtot;
+    }
+
+    // ---- phase A2: contribution lists of the off-diagonal rows ----
+    if (VALS && cl < ncols && deg > 0 && m > 1) {
+        uint64_t *M = sM + t;
+#pragma unroll
+        for (int q = 0; q < MAXR; ++q) M[q * COL_BLOCK] = 0u;
+#pragma unroll 1
+        for (int k = 0; k < deg; ++k) {
+            int32_t g[8];
             const int64_t e = ent[k] >> 3;
             const int a = ent[k] & 7;
-            const int s = seg_of(T, e);
-            const int64_t el = e - T.start[s];
-            int32_t g[8];
-            load_conn8(T.conn[s], el, T.conn_stride[s], g);
-            const double *kr = T.ke[s] + T.ke_stride[s] * el;
-            double x[8];
+            const int sg = seg_of(T, e);
+            load_conn8(T.conn[sg], e - T.start[sg], T.conn_stride[sg], g);
 #pragma unroll
             for (int b = 0; b < 8; ++b) {
-                const int hi_ = max(a, b), lo_ = min(a, b);
-                x[b] = g[b] >= c ? __ldg(kr + pack_index(hi_, lo_)) : 0.0;
-            }
-#pragma unroll
-            for (int b = 0; b < 8; ++b) {
-                if (g[b] >= c) {
-                    const int j = find_row<BLOCK>(R, m, g[b]);
-                    const uint32_t bit = 1u << j;
-                    if (!(has0 & bit)) {
-                        V0[j * BLOCK] = x[b];
-                        has0 |= bit;
-                    } else if (!(has1 & bit)) {
-                        S[j * BLOCK] = x[b];
-                        has1 |= bit;
-                    } else {
-                        S[j * BLOCK] = __dadd_rn(S[j * BLOCK], x[b]);
-                    }
+                const int32_t v = g[b];
+                if (v <= c) continue;
+                int lo = 1, hi = m;  // lower_bound over rows 1..m-1
+                while (lo < hi) {
+                    const int mid = (lo + hi) >> 1;
+                    if (R[mid * COL_BLOCK] < v) lo = mid + 1; else hi = mid;
+                }
+                const uint64_t w = M[lo * COL_BLOCK];
+                if ((w & 7u) == MAX_OFFDIAG_CONTRIB) {
+                    ok = false;
+                } else {
+                    M[lo * COL_BLOCK] = contrib_push(w, k, pack_index(max(a, b), min(a, b)));
                 }
             }
         }
+        if (!ok) atomicOr(status, HX_ST_ROW_OVERFLOW);
     }
-    const int64_t base = col_ptr[cl];
-    for (int j = 0; j < m; ++j) {
-        const uint32_t bit = 1u << j;
-        const double v0 = V0[j * BLOCK];
-        row_idx[base + j] = R[j * BLOCK];
-        vals[base + j] = (has1 & bit) ? __dadd_rn(v0, S[j * BLOCK]) : v0;
-    }
-    return COL_OK;
-}
 
-// 4./6. per-column pass, narrow tier: every column with <= MAXR rows.  Wider columns are
-// appended to `wide_list` (count mode) / skipped (values mode) and handled by the wide tier.
-template <bool VALUES>
-__global__ void __launch_bounds__(COL_BLOCK)
-column_kernel(SegTable T, int64_t col_lo, int64_t ncols, const int32_t *__restrict__ adj_ptr,
-              const int32_t *__restrict__ adj, int32_t *__restrict__ counts, int32_t *__restrict__ wide_list,
-              int32_t *__restrict__ wide_count, const int64_t *__restrict__ col_ptr,
-              int64_t *__restrict__ row_idx, double *__restrict__ vals, uint32_t *__restrict__ status) {
-    __shared__ int32_t sR[MAXR * COL_BLOCK];
-    __shared__ double sV0[VALUES ? MAXR * COL_BLOCK : 1];
-    __shared__ double sS[VALUES ? MAXR * COL_BLOCK : 1];
-    const int t = threadIdx.x;
-    const int64_t cl = (int64_t)blockIdx.x * COL_BLOCK + t;
-    if (cl >= ncols) return;
-    if (VALUES && col_ptr[cl + 1] - col_ptr[cl] > MAXR) return;  // wide tier's column
-    int m = 0;
-    const int r = process_column<VALUES, MAXR, COL_BLOCK>(T, col_lo, cl, adj_ptr, adj, sR + t, sV0 + t, sS + t, m,
-                                                          col_ptr, row_idx, vals, status);
-    if (!VALUES) {
-        counts[cl] = r == COL_OK ? m : 0;
-        if (r == COL_ROWS_OVERFLOW) wide_list[atomicAdd(wide_count, 1)] = (int32_t)cl;
+    // ---- tile offset (decoupled look-back) ----
+    if (LOOKBACK) {
+        if (t == 0) {
+            int64_t prefix = 0;
+            if (tile > 0) {
+                for (int64_t p = tile - 1; p >= 0;) {
+                    const unsigned long long w = tile_read(tile_state, p);
+                    if ((w & ~TILE_VAL) == 0) continue;  // predecessor still in phase A1
+                    prefix += (int64_t)(w & TILE_VAL);
+                    if ((w & ~TILE_VAL) == TILE_INC) break;
+                    --p;
+                }
+                tile_publish(tile_state, tile, TILE_INC | (unsigned long long)(prefix + total));
+            }
+            s_base = prefix;
+        }
+        __syncthreads();
+        base = s_base;
+        if (cl < ncols) col_ptr[cl] = base + excl;
+        if (cl == ncols - 1) col_ptr[ncols] = base + excl + m;
+    } else {
+        __syncthreads();
+    }
+
+    // ---- phase B ----
+    const int64_t room = capacity - base;
+    const int limit = room <= 0 ? 0 : (room < total ? (int)room : total);  // beyond capacity: caller retries
+    // diagonals: entry s_excl[u] of column u
+    if (cl < ncols && s_deg[t] > 0 && excl < limit) {
+        const int64_t o = base + excl;
+        if (ROWS) row_idx[o] = c;
+        if (VALS) {
+            const int dg = s_deg[t];
+            double x[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                x[k] = 0.0;
+                if (k < dg) {
+                    const int a = sA[k * COL_BLOCK + t];
+                    x[k] = __ldg(sP[k * COL_BLOCK + t] + pack_index(a, a));
+                }
+            }
+            double v = x[0];
+            if (dg >= 2) {
+                double sum = x[1];
+#pragma unroll
+                for (int k = 2; k < 8; ++k)
+                    if (k < dg) sum = __dadd_rn(sum, x[k]);
+                v = __dadd_rn(x[0], sum);
+            }
+            vals[o] = v;
+        }
+    }
+    // off-diagonals: q-th off-diagonal entry of the tile
+    const int dtotal = s_dexcl[COL_BLOCK];
+    for (int q = t; q < dtotal; q += COL_BLOCK) {
+        int lo = 0, hi = COL_BLOCK;  // column of off-diagonal q: largest u with s_dexcl[u] <= q
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (s_dexcl[mid] <= q) lo = mid; else hi = mid;
+        }
+        const int u = lo;
+        const int j = q - s_dexcl[u] + 1;
+        const int o = s_excl[u] + j;
+        if (o >= limit) continue;
+        if (ROWS) row_idx[base + o] = sR[j * COL_BLOCK + u];
+        if (VALS) {
+            const uint64_t w = sM[j * COL_BLOCK + u];
+            const int n = (int)(w & 7u);
+            double x[MAX_OFFDIAG_CONTRIB];
+#pragma unroll
+            for (int i = 0; i < MAX_OFFDIAG_CONTRIB; ++i) {
+                x[i] = 0.0;
+                if (i < n) {
+                    const uint32_t kp = (uint32_t)(w >> (3 + 9 * i)) & 511u;
+                    x[i] = __ldg(sP[(kp >> 6) * COL_BLOCK + u] + (kp & 63u));
+                }
+            }
+            double v = x[0];
+            if (n >= 2) {
+                double sum = x[1];
+#pragma unroll
+                for (int i = 2; i < MAX_OFFDIAG_CONTRIB; ++i)
+                    if (i < n) sum = __dadd_rn(sum, x[i]);
+                v = __dadd_rn(x[0], sum);
+            }
+            vals[base + o] = v;
+        }
     }
 }
-
-// Wide tier: columns listed by the narrow count pass (up to WIDE_MAXR rows; e.g. randomly
-// numbered meshes, where the smallest id of a 27-node neighbourhood owns 27 rows).
-template <bool VALUES>
-__global__ void __launch_bounds__(WIDE_BLOCK)
-column_wide_kernel(SegTable T, int64_t col_lo, const int32_t *__restrict__ adj_ptr, const int32_t *__restrict__ adj,
-                   int32_t *__restrict__ counts, const int32_t *__restrict__ wide_list,
-                   const int32_t *__restrict__ wide_count, const int64_t *__restrict__ col_ptr,
-                   int64_t *__restrict__ row_idx, double *__restrict__ vals, uint32_t *__restrict__ status) {
-    __shared__ int32_t sR[WIDE_MAXR * WIDE_BLOCK];
-    __shared__ double sV0[VALUES ? WIDE_MAXR * WIDE_BLOCK : 1];
-    __shared__ double sS[VALUES ? WIDE_MAXR * WIDE_BLOCK : 1];
-    const int t = threadIdx.x;
-    const int n = *wide_count;
-    for (int i = blockIdx.x * WIDE_BLOCK + t; i < n; i += gridDim.x * WIDE_BLOCK) {
-        const int64_t cl = wide_list[i];
-        int m = 0;
-        const int r = process_column<VALUES, WIDE_MAXR, WIDE_BLOCK>(T, col_lo, cl, adj_ptr, adj, sR + t, sV0 + t,
-                                                                    sS + t, m, col_ptr, row_idx, vals, status);
-        if (r == COL_ROWS_OVERFLOW) atomicOr(status, HX_ST_ROW_OVERFLOW);
-        if (!VALUES) counts[cl] = r == COL_OK ? m : 0;
-    }
-}
-
-struct CastI64 {
-    __host__ __device__ int64_t operator()(int32_t v) const { return (int64_t)v; }
-};
 
 // Workspace layout (all offsets 256-B aligned):
-//   adj_ptr  (ncols+1) i32 | cursor/deg (ncols+1) i32 | counts (ncols+1) i32 |
-//   adj (8*n_total) i32 | wide_list (ncols) i32 | wide_count i32 | cub temp
+//   adj_ptr (ncols+1) i32 | cursor/deg (ncols+1) i32 | adj (8*n_total) i32 |
+//   tile_state (tiles) u64 | tile_ticket i32 | cub temp
 struct MeshWs {
-    int32_t *adj_ptr, *deg, *counts, *adj, *wide_list, *wide_count;
+    int32_t *adj_ptr, *deg, *adj, *tile_ticket;
+    unsigned long long *tile_state;
     void *cub_tmp;
     size_t cub_bytes;
     size_t total;
 };
 
 static size_t cub_scan_bytes(int64_t ncols) {
-    size_t b1 = 0, b2 = 0;
+    size_t b1 = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, b1, (int32_t *)nullptr, (int32_t *)nullptr, (int)(ncols + 1));
-    auto it = cub::TransformInputIterator<int64_t, CastI64, const int32_t *>((const int32_t *)nullptr, CastI64());
-    cub::DeviceScan::ExclusiveSum(nullptr, b2, it, (int64_t *)nullptr, (int)(ncols + 1));
-    return std::max(b1, b2);
+    return b1;
 }
 
 static MeshWs mesh_ws_layout(void *base, int64_t n_total, int64_t ncols) {
@@ -312,10 +485,9 @@ static MeshWs mesh_ws_layout(void *base, int64_t n_total, int64_t ncols) {
     };
     const size_t o_ptr = take(sizeof(int32_t) * (ncols + 1));
     const size_t o_deg = take(sizeof(int32_t) * (ncols + 1));
-    const size_t o_cnt = take(sizeof(int32_t) * (ncols + 1));
     const size_t o_adj = take(sizeof(int32_t) * 8 * std::max<int64_t>(n_total, 1));
-    const size_t o_wl = take(sizeof(int32_t) * std::max<int64_t>(ncols, 1));
-    const size_t o_wc = take(sizeof(int32_t));
+    const size_t o_ts = take(sizeof(unsigned long long) * std::max<int64_t>(1, ceil_div(ncols, COL_BLOCK)));
+    const size_t o_tt = take(sizeof(int32_t));
     w.cub_bytes = cub_scan_bytes(ncols);
     const size_t o_cub = take(w.cub_bytes);
     w.total = off;
@@ -323,10 +495,9 @@ static MeshWs mesh_ws_layout(void *base, int64_t n_total, int64_t ncols) {
     if (b) {
         w.adj_ptr = (int32_t *)(b + o_ptr);
         w.deg = (int32_t *)(b + o_deg);
-        w.counts = (int32_t *)(b + o_cnt);
         w.adj = (int32_t *)(b + o_adj);
-        w.wide_list = (int32_t *)(b + o_wl);
-        w.wide_count = (int32_t *)(b + o_wc);
+        w.tile_state = (unsigned long long *)(b + o_ts);
+        w.tile_ticket = (int32_t *)(b + o_tt);
         w.cub_tmp = b + o_cub;
     }
     return w;
@@ -368,12 +539,9 @@ static int make_segtable(const hx_elem_segment *segs, int32_t n_segs, SegTable &
     return HX_OK;
 }
 
-static unsigned wide_grid(int64_t ncols) {
-    return (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(ncols, WIDE_BLOCK), 148 * 8));
-}
 
 static unsigned grid_for(int64_t n, int threads) {
-    return (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, threads), 148 * 32));
+    return (unsigned)std::max<int64_t>(1, ceil_div(n, threads));
 }
 
 }  // namespace hx
@@ -385,15 +553,15 @@ extern "C" int64_t hx_mesh_csc_workspace_bytes(int64_t n_el_total, int64_t n_col
     return (int64_t)mesh_ws_layout(nullptr, n_el_total, n_cols).total;
 }
 
-extern "C" int hx_mesh_csc_symbolic(const hx_elem_segment *segs, int32_t n_segs, int64_t n_nodes,
-                                    int64_t col_lo, int64_t col_hi, int64_t *col_ptr, void *workspace,
-                                    int64_t workspace_bytes, uint32_t *status, void *stream) {
+static int mesh_csc_build(const hx_elem_segment *segs, int32_t n_segs, int64_t n_nodes, int64_t col_lo,
+                          int64_t col_hi, int64_t *col_ptr, int64_t *row_idx, double *vals, int64_t row_capacity,
+                          void *workspace, int64_t workspace_bytes, uint32_t *status, void *stream) {
     SegTable T;
     int64_t n_total = 0;
-    int rc = make_segtable(segs, n_segs, T, n_total, false);
+    int rc = make_segtable(segs, n_segs, T, n_total, vals != nullptr);
     if (rc) return rc;
     if (col_lo < 0 || col_hi < col_lo || col_hi > n_nodes || n_nodes >= INT32_MAX || col_ptr == nullptr ||
-        status == nullptr) {
+        status == nullptr || row_capacity < 0 || (row_capacity > 0 && row_idx == nullptr)) {
         set_last_error("hx_mesh_csc_symbolic: bad column range [%lld, %lld) for %lld nodes", (long long)col_lo,
                        (long long)col_hi, (long long)n_nodes);
         return HX_ERR_VALUE;
@@ -420,26 +588,49 @@ extern "C" int hx_mesh_csc_symbolic(const hx_elem_segment *segs, int32_t n_segs,
                                                                       w.deg, w.adj);
         HX_CHECK_LAUNCH("adjacency_fill_kernel");
     }
-    HX_TRY_CUDA(cudaMemsetAsync(w.counts + ncols, 0, sizeof(int32_t), s));
-    HX_TRY_CUDA(cudaMemsetAsync(w.wide_count, 0, sizeof(int32_t), s));
+    const int64_t tiles = ceil_div(ncols, COL_BLOCK);
+    HX_TRY_CUDA(cudaMemsetAsync(w.tile_state, 0, sizeof(unsigned long long) * std::max<int64_t>(tiles, 1), s));
+    HX_TRY_CUDA(cudaMemsetAsync(w.tile_ticket, 0, sizeof(int32_t), s));
     if (ncols > 0) {
-        column_kernel<false><<<(unsigned)ceil_div(ncols, COL_BLOCK), COL_BLOCK, 0, s>>>(
-            T, col_lo, ncols, w.adj_ptr, w.adj, w.counts, w.wide_list, w.wide_count, nullptr, nullptr, nullptr,
-            status);
-        HX_CHECK_LAUNCH("column_kernel<count>");
-        column_wide_kernel<false><<<wide_grid(ncols), WIDE_BLOCK, 0, s>>>(
-            T, col_lo, w.adj_ptr, w.adj, w.counts, w.wide_list, w.wide_count, nullptr, nullptr, nullptr, status);
-        HX_CHECK_LAUNCH("column_wide_kernel<count>");
+        if (vals != nullptr) {
+            column_pass_kernel<true, true, true><<<(unsigned)tiles, COL_BLOCK, 0, s>>>(
+                T, col_lo, ncols, w.adj_ptr, w.adj, col_ptr, row_idx, row_capacity, vals, w.tile_state,
+                w.tile_ticket, status);
+        } else {
+            column_pass_kernel<true, false, true><<<(unsigned)tiles, COL_BLOCK, 0, s>>>(
+                T, col_lo, ncols, w.adj_ptr, w.adj, col_ptr, row_idx, row_capacity, nullptr, w.tile_state,
+                w.tile_ticket, status);
+        }
+        HX_CHECK_LAUNCH("column_pass_kernel");
+    } else {
+        HX_TRY_CUDA(cudaMemsetAsync(col_ptr, 0, sizeof(int64_t), s));
     }
-    auto it = cub::TransformInputIterator<int64_t, CastI64, const int32_t *>(w.counts, CastI64());
-    cb = w.cub_bytes;
-    HX_TRY_CUDA(cub::DeviceScan::ExclusiveSum(w.cub_tmp, cb, it, col_ptr, (int)(ncols + 1), s));
     return HX_OK;
 }
 
+extern "C" int hx_mesh_csc_symbolic(const hx_elem_segment *segs, int32_t n_segs, int64_t n_nodes,
+                                    int64_t col_lo, int64_t col_hi, int64_t *col_ptr, int64_t *row_idx,
+                                    int64_t row_capacity, void *workspace, int64_t workspace_bytes,
+                                    uint32_t *status, void *stream) {
+    return mesh_csc_build(segs, n_segs, n_nodes, col_lo, col_hi, col_ptr, row_idx, nullptr, row_capacity, workspace,
+                          workspace_bytes, status, stream);
+}
+
+extern "C" int hx_mesh_csc_build(const hx_elem_segment *segs, int32_t n_segs, int64_t n_nodes, int64_t col_lo,
+                                 int64_t col_hi, int64_t *col_ptr, int64_t *row_idx, double *vals,
+                                 int64_t capacity, void *workspace, int64_t workspace_bytes, uint32_t *status,
+                                 void *stream) {
+    if (vals == nullptr && capacity > 0) {
+        set_last_error("hx_mesh_csc_build: vals is NULL");
+        return HX_ERR_VALUE;
+    }
+    return mesh_csc_build(segs, n_segs, n_nodes, col_lo, col_hi, col_ptr, row_idx, vals, capacity, workspace,
+                          workspace_bytes, status, stream);
+}
+
 extern "C" int hx_mesh_csc_numeric(const hx_elem_segment *segs, int32_t n_segs, int64_t col_lo, int64_t col_hi,
-                                   const int64_t *col_ptr, int64_t *row_idx, double *vals, const void *workspace,
-                                   uint32_t *status, void *stream) {
+                                   const int64_t *col_ptr, const int64_t *row_idx, double *vals,
+                                   const void *workspace, uint32_t *status, void *stream) {
     SegTable T;
     int64_t n_total = 0;
     int rc = make_segtable(segs, n_segs, T, n_total, true);
@@ -452,12 +643,10 @@ extern "C" int hx_mesh_csc_numeric(const hx_elem_segment *segs, int32_t n_segs, 
     MeshWs w = mesh_ws_layout(const_cast<void *>(workspace), n_total, ncols);
     cudaStream_t s = (cudaStream_t)stream;
     if (ncols > 0) {
-        column_kernel<true><<<(unsigned)ceil_div(ncols, COL_BLOCK), COL_BLOCK, 0, s>>>(
-            T, col_lo, ncols, w.adj_ptr, w.adj, nullptr, nullptr, nullptr, col_ptr, row_idx, vals, status);
-        HX_CHECK_LAUNCH("column_kernel<values>");
-        column_wide_kernel<true><<<wide_grid(ncols), WIDE_BLOCK, 0, s>>>(
-            T, col_lo, w.adj_ptr, w.adj, nullptr, w.wide_list, w.wide_count, col_ptr, row_idx, vals, status);
-        HX_CHECK_LAUNCH("column_wide_kernel<values>");
+        column_pass_kernel<false, true, false><<<(unsigned)ceil_div(ncols, COL_BLOCK), COL_BLOCK, 0, s>>>(
+            T, col_lo, ncols, w.adj_ptr, w.adj, const_cast<int64_t *>(col_ptr), const_cast<int64_t *>(row_idx),
+            INT64_MAX, vals, nullptr, nullptr, status);
+        HX_CHECK_LAUNCH("column_pass_kernel<numeric>");
     }
     return HX_OK;
 }

@@ -32,8 +32,31 @@ __device__ __forceinline__ double acc_signed(double acc, int sign, double prod) 
     return sign > 0 ? dadd(acc, prod) : dsub(acc, prod);
 }
 
-// element.py:255-297 for one element, bitwise.  Returns failing gauss point or -1.
-__device__ __forceinline__ int ke_exact(const double (&x)[8][3], double coeff, double (&ke)[36],
+// IEEE round-to-nearest a/b from y = RN(1/b): q0 = RN(a*y) is within 2 ulp of a/b; one
+// correction q1 = RN(q0 + (a - b q0) y) lands within 1 ulp (the residual is exact via FMA and
+// the correction error is ~2^-52 ulp); Markstein's theorem (y = RN(1/b), q within 1 ulp, exact
+// residual) then makes q2 = RN(q1 + (a - b q1) y) the correctly rounded quotient, i.e. bitwise
+// __ddiv_rn(a, b).  Valid while nothing over/underflows: the caller guards exponents and zero.
+__device__ __forceinline__ double div_markstein(double a, double b, double y) {
+    const double q0 = __dmul_rn(a, y);
+    const double r0 = __fma_rn(-q0, b, a);
+    const double q1 = __fma_rn(r0, y, q0);
+    const double r1 = __fma_rn(-q1, b, a);
+    const double q2 = __fma_rn(r1, y, q1);
+    return a == 0.0 ? q0 : q2;  // signed zero: 0*y keeps the sign of a (b > 0)
+}
+
+// |x| in [2^-800, 2^800] (or x == 0): Markstein path safe for these operands.
+__device__ __forceinline__ bool div_safe(double x) {
+    const int e = (__double2hiint(x) >> 20) & 0x7ff;
+    return (e >= 1023 - 800 && e <= 1023 + 800) || x == 0.0;
+}
+
+// element.py:255-297 for one element, bitwise.  Coordinates are read from shared memory with
+// volatile loads (xs[(3a+k)*stride]) once per Gauss point: products M_k*x are recomputed per
+// point instead of being kept live across all eight (register pressure -> occupancy).
+// Returns the failing gauss point or -1.
+__device__ __forceinline__ int ke_exact(const volatile double *xs, int stride, double coeff, double (&ke)[36],
                                         double &fail_det) {
 #pragma unroll
     for (int p = 0; p < 36; ++p) ke[p] = 0.0;
@@ -47,13 +70,16 @@ __device__ __forceinline__ int ke_exact(const double (&x)[8][3], double coeff, d
 #pragma unroll
             for (int k = 0; k < 3; ++k) j[d][k] = 0.0;
 #pragma unroll
-        for (int a = 0; a < 8; ++a)
+        for (int a = 0; a < 8; ++a) {
+            double xa[3];
+#pragma unroll
+            for (int k = 0; k < 3; ++k) xa[k] = xs[(3 * a + k) * stride];
 #pragma unroll
             for (int d = 0; d < 3; ++d)
 #pragma unroll
                 for (int k = 0; k < 3; ++k)
-                    j[d][k] = acc_signed(j[d][k], dn_sign(gp, d, a),
-                                         dmul(dn_magnitude(dn_mag(gp, d, a)), x[a][k]));
+                    j[d][k] = acc_signed(j[d][k], dn_sign(gp, d, a), dmul(dn_magnitude(dn_mag(gp, d, a)), xa[k]));
+        }
         // cofactors of the first row and det (element.py:271-275)
         const double c00 = dsub(dmul(j[1][1], j[2][2]), dmul(j[1][2], j[2][1]));
         const double c01 = dsub(dmul(j[1][2], j[2][0]), dmul(j[1][0], j[2][2]));
@@ -64,17 +90,29 @@ __device__ __forceinline__ int ke_exact(const double (&x)[8][3], double coeff, d
             fail_det = det;
             break;
         }
-        // adjugate / det (element.py:281-284), true IEEE division
+        // adjugate / det (element.py:281-284): IEEE-exact quotients
+        double num[9];
+        num[0] = c00;
+        num[1] = dsub(dmul(j[0][2], j[2][1]), dmul(j[0][1], j[2][2]));
+        num[2] = dsub(dmul(j[0][1], j[1][2]), dmul(j[0][2], j[1][1]));
+        num[3] = c01;
+        num[4] = dsub(dmul(j[0][0], j[2][2]), dmul(j[0][2], j[2][0]));
+        num[5] = dsub(dmul(j[0][2], j[1][0]), dmul(j[0][0], j[1][2]));
+        num[6] = c02;
+        num[7] = dsub(dmul(j[0][1], j[2][0]), dmul(j[0][0], j[2][1]));
+        num[8] = dsub(dmul(j[0][0], j[1][1]), dmul(j[0][1], j[1][0]));
+        bool safe = div_safe(det) && det != 0.0;
+#pragma unroll
+        for (int i = 0; i < 9; ++i) safe &= div_safe(num[i]);
         double inv[3][3];
-        inv[0][0] = __ddiv_rn(c00, det);
-        inv[0][1] = __ddiv_rn(dsub(dmul(j[0][2], j[2][1]), dmul(j[0][1], j[2][2])), det);
-        inv[0][2] = __ddiv_rn(dsub(dmul(j[0][1], j[1][2]), dmul(j[0][2], j[1][1])), det);
-        inv[1][0] = __ddiv_rn(c01, det);
-        inv[1][1] = __ddiv_rn(dsub(dmul(j[0][0], j[2][2]), dmul(j[0][2], j[2][0])), det);
-        inv[1][2] = __ddiv_rn(dsub(dmul(j[0][2], j[1][0]), dmul(j[0][0], j[1][2])), det);
-        inv[2][0] = __ddiv_rn(c02, det);
-        inv[2][1] = __ddiv_rn(dsub(dmul(j[0][1], j[2][0]), dmul(j[0][0], j[2][1])), det);
-        inv[2][2] = __ddiv_rn(dsub(dmul(j[0][0], j[1][1]), dmul(j[0][1], j[1][0])), det);
+        if (safe) {
+            const double y = __drcp_rn(det);
+#pragma unroll
+            for (int i = 0; i < 9; ++i) inv[i / 3][i % 3] = div_markstein(num[i], det, y);
+        } else {
+#pragma unroll
+            for (int i = 0; i < 9; ++i) inv[i / 3][i % 3] = __ddiv_rn(num[i], det);
+        }
         // B = J^-1 dn (element.py:286-290): (i_r0*dn0a + i_r1*dn1a) + i_r2*dn2a
         double B[3][8];
 #pragma unroll
@@ -108,7 +146,7 @@ __device__ __forceinline__ int ke_exact(const double (&x)[8][3], double coeff, d
 __device__ void fail_detail(const double (&x)[8][3], double coeff, int64_t element, hx_fail_info *fail) {
     double ke[36];
     double det = 0.0;
-    const int gp = ke_exact(x, coeff, ke, det);
+    const int gp = ke_exact(&x[0][0], 1, coeff, ke, det);
     fail->element = element;
     fail->gauss_point = gp;
     fail->det = det;
@@ -146,7 +184,7 @@ integrate_mesh_kernel(const double *__restrict__ coords, const int32_t *__restri
                       const double *__restrict__ coeff, int64_t lo, int64_t n,
                       double *__restrict__ ke_out, int32_t *__restrict__ rows_out,
                       int32_t *__restrict__ cols_out, unsigned long long *__restrict__ fail_min) {
-    __shared__ double s_ke[KE_BLOCK * KE_PAD];
+    __shared__ double s_ke[KE_BLOCK * KE_PAD];  // also holds the staged coordinates (24 x KE_BLOCK)
     __shared__ int32_t s_conn[KE_BLOCK * 8];
     __shared__ uint8_t s_pi[36], s_pj[36];
     init_pack_smem(s_pi, s_pj);
@@ -154,19 +192,26 @@ integrate_mesh_kernel(const double *__restrict__ coords, const int32_t *__restri
     const int64_t first = (int64_t)blockIdx.x * KE_BLOCK;
     const int t = threadIdx.x;
     const int64_t k = first + t;
+    double ke[36];
     if (k < n) {
         const int64_t e = lo + k;
         int32_t g[8];
         load_conn(conn, e, g);
 #pragma unroll
         for (int a = 0; a < 8; ++a) s_conn[t * 8 + a] = g[a];
-        double x[8][3];
 #pragma unroll
-        for (int a = 0; a < 8; ++a) load_node(coords, g[a], x[a]);
-        double ke[36];
+        for (int a = 0; a < 8; ++a) {
+            double xa[3];
+            load_node(coords, g[a], xa);
+#pragma unroll
+            for (int d = 0; d < 3; ++d) s_ke[(3 * a + d) * KE_BLOCK + t] = xa[d];
+        }
         double det = 0.0;
-        const int gp = ke_exact(x, __ldg(coeff + e), ke, det);
+        const int gp = ke_exact(s_ke + t, KE_BLOCK, __ldg(coeff + e), ke, det);
         if (gp >= 0) atomicMin(fail_min, (unsigned long long)e);
+    }
+    __syncthreads();  // every thread is done with its staged coordinates
+    if (k < n) {
 #pragma unroll
         for (int p = 0; p < 36; ++p) s_ke[t * KE_PAD + p] = ke[p];
     }
@@ -199,17 +244,17 @@ stiffness_batch_kernel(const double *__restrict__ coords, const double *__restri
     const int64_t first = (int64_t)blockIdx.x * KE_BLOCK;
     const int t = threadIdx.x;
     const int64_t e = first + t;
+    double ke[36];
     if (e < n) {
-        double x[8][3];
         const double *src = coords + 24 * e;
 #pragma unroll
-        for (int a = 0; a < 8; ++a)
-#pragma unroll
-            for (int d = 0; d < 3; ++d) x[a][d] = __ldg(src + 3 * a + d);
-        double ke[36];
+        for (int i = 0; i < 24; ++i) s_ke[i * KE_BLOCK + t] = __ldg(src + i);
         double det = 0.0;
-        const int gp = ke_exact(x, __ldg(coeff + e), ke, det);
+        const int gp = ke_exact(s_ke + t, KE_BLOCK, __ldg(coeff + e), ke, det);
         if (gp >= 0) atomicMin(fail_min, (unsigned long long)e);
+    }
+    __syncthreads();
+    if (e < n) {
 #pragma unroll
         for (int p = 0; p < 36; ++p) s_ke[t * KE_PAD + p] = ke[p];
     }
@@ -277,9 +322,62 @@ __global__ void index_kernel(const int32_t *__restrict__ conn, int64_t lo, int64
     }
 }
 
+__device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+    x += 0x9e3779b97f4a7c15ull;
+    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+    x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+    return x ^ (x >> 31);
+}
+
+// Self-test of div_markstein against __ddiv_rn: random mantissas, exponents spread over the
+// guarded range, cancellation-like numerators, exact multiples and neighbours of exact
+// quotients (the hardest rounding cases).  Counts mismatching bit patterns.
+__global__ void division_selftest_kernel(uint64_t n, uint64_t seed, unsigned long long *mismatches,
+                                         unsigned long long *tested) {
+    unsigned long long bad = 0, cnt = 0;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t r1 = splitmix64(seed ^ (2 * i)), r2 = splitmix64(seed ^ (2 * i + 1));
+        const int kind = (int)(r1 & 3);
+        const int ea = (int)((r1 >> 2) & 1023) - 512, eb = (int)((r2 >> 2) & 1023) - 512;
+        double b = __hiloint2double(0x3ff00000 | (int)((r2 >> 12) & 0xfffff), (int)(r2 >> 32));
+        b = ldexp(b, kind == 0 ? eb : (eb & 63) - 32);
+        double a = __hiloint2double(0x3ff00000 | (int)((r1 >> 12) & 0xfffff), (int)(r1 >> 32));
+        a = ldexp(a, kind == 0 ? ea : (ea & 63) - 32);
+        if (r1 & (1ull << 62)) a = -a;
+        if (kind == 2) {  // a = exact-ish multiple of b, nudged by a few ulps
+            const double q = __hiloint2double(0x3ff00000 | (int)((r2 >> 40) & 0xfffff), (int)r1);
+            a = __dmul_rn(q, b);
+            const long long bits = __double_as_longlong(a) + (long long)((r2 >> 60) & 7) - 3;
+            a = __longlong_as_double(bits);
+        } else if (kind == 3) {  // small-integer ratios (cancellation zeros and halves)
+            a = (double)((long long)(r1 >> 40) % 97 - 48);
+            b = (double)((r2 >> 40) % 13 + 1);
+        }
+        if (!(b > 0.0) || !div_safe(a) || !div_safe(b)) continue;
+        const double y = __drcp_rn(b);
+        const double q = div_markstein(a, b, y), ref = __ddiv_rn(a, b);
+        bad += __double_as_longlong(q) != __double_as_longlong(ref);
+        ++cnt;
+    }
+    atomicAdd(mismatches, bad);
+    atomicAdd(tested, cnt);
+}
+
 }  // namespace hx
 
 using namespace hx;
+
+extern "C" int hx_selftest_division(uint64_t n, uint64_t seed, unsigned long long *result2, void *stream) {
+    if (result2 == nullptr) {
+        set_last_error("hx_selftest_division: null result");
+        return HX_ERR_VALUE;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    HX_TRY_CUDA(cudaMemsetAsync(result2, 0, 2 * sizeof(unsigned long long), s));
+    division_selftest_kernel<<<148 * 8, 256, 0, s>>>(n, seed, result2, result2 + 1);
+    HX_CHECK_LAUNCH("division_selftest_kernel");
+    return HX_OK;
+}
 
 extern "C" int hx_integrate_mesh(const double *coords, int64_t n_nodes, const int32_t *conn,
                                  const double *coeff, int64_t lo, int64_t hi, double *ke,

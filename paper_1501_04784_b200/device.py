@@ -201,7 +201,13 @@ def _check_segment(conn, ke):
         raise ValueError("segment ke rows must have unit inner stride")
 
 
-def mesh_csc(parts, n_nodes: int, col_lo: int = 0, col_hi: int | None = None, stream=None) -> DeviceCsc:
+# Conforming hex meshes have <= 14 lower rows per column on average (27-point stencil); the
+# symbolic pass writes rows into a buffer of this many per column and retries exactly if short.
+ROWS_PER_COLUMN_ESTIMATE = 16
+
+
+def mesh_csc(parts, n_nodes: int, col_lo: int = 0, col_hi: int | None = None, stream=None,
+             row_capacity: int | None = None) -> DeviceCsc:
     """Assemble columns [col_lo, col_hi) of the lower CSC from element segments.
 
     ``parts`` is a list of (conn (n,8) i32, ke (n,36) f64) CUDA tensor views in ascending global
@@ -225,17 +231,23 @@ def mesh_csc(parts, n_nodes: int, col_lo: int = 0, col_hi: int | None = None, st
     status = torch.zeros(1, dtype=torch.int32, device=dev)
     col_ptr = torch.empty(ncols + 1, dtype=torch.int64, device=dev)
     sh = stream_handle(stream)
-    N.check(N.lib().hx_mesh_csc_symbolic(segs, len(parts), n_nodes, col_lo, col_hi, _ptr(col_ptr), _ptr(ws),
-                                         ws_bytes, _ptr(status), sh), "hx_mesh_csc_symbolic")
-    head = torch.stack([status.to(torch.int64)[0], col_ptr[-1]]).cpu()  # one sync: status + nnz
-    st, nnz = int(head[0]), int(head[1])
-    _status_error(st)
-    if st & N.ST_FASTPATH_LIMITS:
-        return _mesh_csc_generic(parts, n_nodes, col_lo, col_hi, stream)
-    row_idx = torch.empty(nnz, dtype=torch.int64, device=dev)
-    vals = torch.empty(nnz, dtype=torch.float64, device=dev)
-    N.check(N.lib().hx_mesh_csc_numeric(segs, len(parts), col_lo, col_hi, _ptr(col_ptr), _ptr(row_idx),
-                                        _ptr(vals), _ptr(ws), _ptr(status), sh), "hx_mesh_csc_numeric")
+    capacity = ROWS_PER_COLUMN_ESTIMATE * ncols if row_capacity is None else row_capacity
+    while True:
+        row_buf = torch.empty(max(capacity, 1), dtype=torch.int64, device=dev)
+        val_buf = torch.empty(max(capacity, 1), dtype=torch.float64, device=dev)
+        N.check(N.lib().hx_mesh_csc_build(segs, len(parts), n_nodes, col_lo, col_hi, _ptr(col_ptr), _ptr(row_buf),
+                                          _ptr(val_buf), capacity, _ptr(ws), ws_bytes, _ptr(status), sh),
+                "hx_mesh_csc_build")
+        head = torch.stack([status.to(torch.int64)[0], col_ptr[-1]]).cpu()  # one sync: status + nnz
+        st, nnz = int(head[0]), int(head[1])
+        _status_error(st)
+        if st & N.ST_FASTPATH_LIMITS:
+            return _mesh_csc_generic(parts, n_nodes, col_lo, col_hi, stream)
+        if nnz <= capacity:
+            break
+        capacity = nnz  # rare: more rows than the estimate -> exact-size retry
+    row_idx = row_buf[:nnz]
+    vals = val_buf[:nnz]
     return DeviceCsc(col_ptr, row_idx, vals, n_nodes, col_lo, "mesh")
 
 

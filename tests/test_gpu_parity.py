@@ -273,3 +273,29 @@ def test_operator_properties_full_size():
     off = ri != col_of
     rs.index_add_(0, col_of[off], vv[off])
     assert float(rs.abs().max()) <= 1e-10 * float(vv.abs().max()) * 27
+
+
+def test_exact_division_selftest():
+    """Reciprocal + Markstein quotient == IEEE division, bit for bit, on 2^30 operand pairs."""
+    from paper_1501_04784_b200 import _native as N
+
+    res = torch.zeros(2, dtype=torch.int64, device="cuda")
+    N.check(N.lib().hx_selftest_division(1 << 30, 12345, D._ptr(res), D.stream_handle()), "selftest")
+    mismatches, tested = res.cpu().tolist()
+    assert tested > (1 << 29)
+    assert mismatches == 0
+
+
+def test_random_elements_bitwise_against_oracle():
+    """1M random valid hexahedra (distortion up to 0.3, wide coefficient/scale range) vs the oracle."""
+    rng = np.random.default_rng(2024)
+    n = 1 << 20
+    corners = (np.array([(-1, -1, -1), (1, -1, -1), (1, 1, -1), (-1, 1, -1), (-1, -1, 1), (1, -1, 1), (1, 1, 1),
+                         (-1, 1, 1)], dtype=float) + 1.0) / 2.0
+    scale = np.exp(rng.uniform(-20, 20, size=(n, 1, 1)))
+    coords = (corners[None] + rng.uniform(-0.2, 0.2, size=(n, 8, 3)) + rng.uniform(-10, 10, size=(n, 1, 3))) * scale
+    coeff = np.exp(rng.uniform(-10, 10, size=n))
+    ref, first, _, _ = oracle.stiffness_batch(coords, coeff)
+    assert first == -1
+    got = stiffness_batch(coords, coeff)
+    assert bits_equal(got, ref)
