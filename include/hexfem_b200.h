@@ -48,7 +48,8 @@ extern "C" {
 #define HX_ST_REPEATED_NODE 4u /* an element lists the same node twice                     */
 #define HX_ST_BAD_INDEX 8u     /* index outside [0, dim) (MeshValidationError, assemble.py:146) */
 #define HX_ST_UPPER 16u        /* triplet above the diagonal (MeshValidationError, assemble.py:148) */
-/* DEG/ROW/REPEATED mean "mesh fast path not applicable": the caller re-runs the generic
+#define HX_ST_SCRATCH_OVERFLOW 32u /* pattern scratch too small (> 15 off-diagonals per column on average) */
+/* DEG/ROW/REPEATED/SCRATCH mean "mesh fast path not applicable": the caller re-runs the generic
  * triplet path (hx_triplet_csc_*), which has no such limits. */
 
 #define HX_MAX_NODE_DEGREE 8

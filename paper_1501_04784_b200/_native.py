@@ -16,8 +16,8 @@ from .errors import ConfigurationError, NativeLibraryError
 LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libhexfem_b200.so"
 
 HX_OK, HX_ERR_VALUE, HX_ERR_CONFIG, HX_ERR_CUDA, HX_ERR_WORKSPACE = 0, 1, 2, 3, 4
-ST_DEG_OVERFLOW, ST_ROW_OVERFLOW, ST_REPEATED_NODE, ST_BAD_INDEX, ST_UPPER = 1, 2, 4, 8, 16
-ST_FASTPATH_LIMITS = ST_DEG_OVERFLOW | ST_ROW_OVERFLOW | ST_REPEATED_NODE
+ST_DEG_OVERFLOW, ST_ROW_OVERFLOW, ST_REPEATED_NODE, ST_BAD_INDEX, ST_UPPER, ST_SCRATCH = 1, 2, 4, 8, 16, 32
+ST_FASTPATH_LIMITS = ST_DEG_OVERFLOW | ST_ROW_OVERFLOW | ST_REPEATED_NODE | ST_SCRATCH
 MODE_EXACT, MODE_FAST = 0, 1
 MAX_SEGMENTS = 4
 

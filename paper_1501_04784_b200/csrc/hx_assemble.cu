@@ -31,7 +31,6 @@
 
 namespace hx {
 
-constexpr int COL_BLOCK = 64;  // columns per tile (one thread per column in phase A)
 constexpr int MAXDEG = HX_MAX_NODE_DEGREE;
 constexpr int MAXR = HX_MAX_COL_ROWS;
 constexpr int MAX_SEGS = 4;
@@ -154,17 +153,12 @@ __device__ __forceinline__ int incident_sorted(int64_t cl, const int32_t *__rest
     return deg;
 }
 
-// Decoupled look-back tile state: one 64-bit word, flag in the top 2 bits, value below.
-constexpr unsigned long long TILE_AGG = 1ull << 62, TILE_INC = 2ull << 62, TILE_VAL = (1ull << 62) - 1;
+constexpr int32_t HASH_EMPTY = INT32_MAX;  // sorts last
+constexpr int MAX_OFFDIAG_CONTRIB = 4;     // hex meshes: an edge is shared by at most 4 elements
+constexpr int COL_BLOCK = 64;              // columns per block (pattern: one thread per column)
+constexpr int EMIT_BLOCK = 128;            // emit: threads per COL_BLOCK columns
 
-__device__ __forceinline__ void tile_publish(unsigned long long *state, int64_t tile, unsigned long long word) {
-    atomicExch(state + tile, word);
-}
-__device__ __forceinline__ unsigned long long tile_read(const unsigned long long *state, int64_t tile) {
-    return *reinterpret_cast<const volatile unsigned long long *>(state + tile);
-}
-
-// Bitonic sorting network on 32 register-resident keys (ascending).
+// Bitonic sorting network on 32 register-resident keys, ascending.
 __device__ __forceinline__ void sort32(int32_t (&v)[32]) {
 #pragma unroll
     for (int k = 2; k <= 32; k <<= 1)
@@ -182,297 +176,279 @@ __device__ __forceinline__ void sort32(int32_t (&v)[32]) {
             }
 }
 
-constexpr int32_t HASH_EMPTY = -1;
-constexpr int MAX_OFFDIAG_CONTRIB = 4;  // hex meshes: an edge is shared by at most 4 elements
+__device__ __forceinline__ uint32_t hash_slot(int32_t v) { return ((uint32_t)v * 0x9E3779B1u) >> 27; }
 
-// Contribution word of an off-diagonal row: bits 0-2 count, then up to 4 entries of 9 bits
-// (incident-element slot k: 3 bits, packed KE index p: 6 bits), in ascending element order.
-__device__ __forceinline__ uint64_t contrib_push(uint64_t w, int k, int p) {
-    const uint64_t n = w & 7u;
-    return (w + 1u) | ((uint64_t)(k << 6 | p) << (3 + 9 * n));
-}
-
-// 4-6. The column pass.  One tile = COL_BLOCK consecutive columns (one thread per column in
-// phase A); the tile's output entries are spread over all threads in phase B.
-//   A1 incident elements sorted by id (= the stable triplet order) -> sE, their KE row
-//      pointers -> sP; distinct rows >= c via a 32-slot hash set, sorted by a register bitonic
-//      network -> sR (LOOKBACK), or read from row_idx (numeric-only mode);
-//   -  block scan of the row counts; the tile's aggregate is published right away;
-//   A2 (VALS) for every off-diagonal row the ordered list of contributing (element, packed
-//      index) pairs -> sM -- built while thread 0 looks back over the predecessor tiles
-//      (decoupled look-back; tiles are taken in scheduling order via a ticket);
-//   B  the tile's output entries in output order (coalesced row_idx / vals stores): diagonals
-//      (one per column, contributions from every incident element at its own local node), then
-//      off-diagonals; 1..8 gathered values reduced with numpy add.reduceat's rule
-//      v0 + (((v1 + v2) + v3) + ...).
-// ROWS: write row_idx.  VALS: compute vals.  LOOKBACK: compute the rows and col_ptr (else both
-// are inputs: the numeric-only pass of a symbolic/numeric split).
-template <bool ROWS, bool VALS, bool LOOKBACK>
+// 4. Pattern pass: one thread per column, COL_BLOCK columns per block.
+//   - incident elements sorted by id (= the stable triplet order of assemble.py:125) and
+//     written back to the adjacency, so the emit pass reads them in order;
+//   - distinct rows > c in a 32-slot open-addressing hash set (smem); every slot carries its
+//     contribution word: (incident element k, local node b) pairs appended in ascending element
+//     order (<= 4 per off-diagonal: an edge is shared by <= 4 hexes);
+//   - keys sorted by a register bitonic network; m = 1 + distinct rows -> col_ptr[cl] (the
+//     exclusive scan turns the counts into offsets);
+//   - the column's sorted off-diagonal records (row, word) -> a compact scratch region reserved
+//     per block with one atomic (block order in the scratch is irrelevant: every block records
+//     where its records start).
 __global__ void __launch_bounds__(COL_BLOCK)
-column_pass_kernel(SegTable T, int64_t col_lo, int64_t ncols, const int32_t *__restrict__ adj_ptr,
-                   const int32_t *__restrict__ adj, int64_t *__restrict__ col_ptr, int64_t *__restrict__ row_idx,
-                   int64_t capacity, double *__restrict__ vals, unsigned long long *__restrict__ tile_state,
-                   int32_t *__restrict__ tile_ticket, uint32_t *__restrict__ status) {
-    __shared__ int32_t sR[MAXR * COL_BLOCK];            // hash set, then sorted rows: [slot][t]
-    __shared__ uint64_t sM[VALS ? MAXR * COL_BLOCK : 1];  // contribution words: [slot][t]
-    __shared__ const double *sP[VALS ? 8 * COL_BLOCK : 1];  // KE row of incident element k: [k][t]
-    __shared__ uint8_t sA[8 * COL_BLOCK];                 // local index of the column node in element k
-    __shared__ int32_t s_deg[COL_BLOCK];
-    __shared__ int32_t s_excl[COL_BLOCK + 1];
-    __shared__ int32_t s_dexcl[COL_BLOCK + 1];            // exclusive scan of (m - 1): off-diagonals
-    __shared__ int64_t s_base;
-    __shared__ int64_t s_tile;
+pattern_kernel(SegTable T, int64_t col_lo, int64_t ncols, const int32_t *__restrict__ adj_ptr,
+               int32_t *__restrict__ adj, int64_t *__restrict__ col_ptr, int2 *__restrict__ scratch,
+               int64_t scratch_capacity, unsigned long long *__restrict__ scratch_top,
+               int64_t *__restrict__ block_scratch, uint32_t *__restrict__ status) {
+    __shared__ int32_t sH[MAXR * COL_BLOCK];   // hash keys, then sorted rows: [slot][t]
+    __shared__ uint32_t sW[MAXR * COL_BLOCK];  // contribution words: [slot][t]
+    __shared__ unsigned long long s_base;
     using BlockScan = cub::BlockScan<int32_t, COL_BLOCK>;
     __shared__ typename BlockScan::TempStorage scan_tmp;
     const int t = threadIdx.x;
-    if (LOOKBACK) {
-        if (t == 0) s_tile = atomicAdd(tile_ticket, 1);
-        __syncthreads();
-    }
-    const int64_t tile = LOOKBACK ? s_tile : (int64_t)blockIdx.x;
-    const int64_t first = tile * COL_BLOCK;
-    const int64_t cl = first + t;
+    const int64_t cl = (int64_t)blockIdx.x * COL_BLOCK + t;
     const int32_t c = (int32_t)(col_lo + cl);
-    int32_t *R = sR + t;
+    int32_t *H = sH + t;
+    uint32_t *W = sW + t;
 
-    // ---- phase A1 ----
     int m = 0, deg = 0;
-    bool ok = true;
     int32_t ent[8];
     if (cl < ncols) {
         deg = incident_sorted(cl, adj_ptr, adj, ent, status);
-        if (deg < 0) {
-            deg = 0;
-            ok = false;
-        }
+        if (deg < 0) deg = 0;
+        const int32_t beg = __ldg(adj_ptr + cl);
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+            if (k < deg) adj[beg + k] = ent[k];
+    }
+    if (deg > 0) {
+        int32_t g[8][8];
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
-            sA[k * COL_BLOCK + t] = (uint8_t)(ent[k] & 7);
-            if (VALS && k < deg) {
+            if (k < deg) {
                 const int64_t e = ent[k] >> 3;
                 const int sg = seg_of(T, e);
-                sP[k * COL_BLOCK + t] = T.ke[sg] + T.ke_stride[sg] * (e - T.start[sg]);
+                load_conn8(T.conn[sg], e - T.start[sg], T.conn_stride[sg], g[k]);
             }
         }
-        if (LOOKBACK && ok) {
 #pragma unroll
-            for (int q = 0; q < MAXR; ++q) R[q * COL_BLOCK] = HASH_EMPTY;
-#pragma unroll 1
-            for (int k = 0; k < deg; ++k) {
-                int32_t g[8];
-                const int64_t e = ent[k] >> 3;
-                const int sg = seg_of(T, e);
-                load_conn8(T.conn[sg], e - T.start[sg], T.conn_stride[sg], g);
-#pragma unroll
-                for (int b = 0; b < 8; ++b) {
-                    const int32_t v = g[b];
-                    if (v < c) continue;
-                    uint32_t h = ((uint32_t)v * 0x9E3779B1u) >> 27;
-                    bool placed = false;
-#pragma unroll 1
-                    for (int probe = 0; probe < MAXR; ++probe) {
-                        const int32_t cur = R[h * COL_BLOCK];
-                        if (cur == v) {
-                            placed = true;
-                            break;
-                        }
-                        if (cur == HASH_EMPTY) {
-                            R[h * COL_BLOCK] = v;
-                            ++m;
-                            placed = true;
-                            break;
-                        }
-                        h = (h + 1) & (MAXR - 1);
-                    }
-                    ok &= placed;  // a full table: more than MAXR distinct rows
-                }
-            }
-            int32_t r[MAXR];
-#pragma unroll
-            for (int q = 0; q < MAXR; ++q) {
-                const int32_t v = R[q * COL_BLOCK];
-                r[q] = v == HASH_EMPTY ? INT32_MAX : v;
-            }
-            sort32(r);
-#pragma unroll
-            for (int q = 0; q < MAXR; ++q) R[q * COL_BLOCK] = r[q];
-            if (!ok) {
-                atomicOr(status, HX_ST_ROW_OVERFLOW);
-                m = 0;
-                deg = 0;
-            }
+        for (int q = 0; q < MAXR; ++q) {
+            H[q * COL_BLOCK] = HASH_EMPTY;
+            W[q * COL_BLOCK] = 0u;
         }
-    }
-
-    // ---- block scan of row counts (or read them back) ----
-    int64_t base = 0;
-    int total, excl;
-    if (LOOKBACK) {
-        BlockScan(scan_tmp).ExclusiveSum(m, excl, total);
-        if (t == 0 && tile == 0) tile_publish(tile_state, 0, TILE_INC | (unsigned long long)total);
-        if (t == 0 && tile > 0) tile_publish(tile_state, tile, TILE_AGG | (unsigned long long)total);
-    } else {
-        base = col_ptr[first];
-        const int64_t last = first + COL_BLOCK < ncols ? first + COL_BLOCK : ncols;
-        excl = cl <= ncols ? (int)(col_ptr[cl < last ? cl : last] - base) : 0;
-        total = (int)(col_ptr[last] - base);
-        if (cl < ncols) m = (int)(col_ptr[cl + 1] - col_ptr[cl]);
-        if (m > MAXR) {
-            ok = false;
-            m = 0;
-        }
-        if (cl < ncols && ok) {
-            for (int q = 0; q < m; ++q) R[q * COL_BLOCK] = (int32_t)row_idx[base + excl + q];
-        }
-    }
-    s_excl[t] = cl < ncols ? excl : total;
-    s_deg[t] = deg;
-    if (t == 0) s_excl[COL_BLOCK] = total;
-    {
-        int dex, dtot;
-        BlockScan(scan_tmp).ExclusiveSum(m > 0 ? m - 1 : 0, dex, dtot);
-        s_dexcl[t] = cl < ncols ? dex : dtot;
-        if (t == 0) s_dexcl[COL_BLOCK] = dtot;
-    }
-
-    // ---- phase A2: contribution lists of the off-diagonal rows ----
-    if (VALS && cl < ncols && deg > 0 && m > 1) {
-        uint64_t *M = sM + t;
+        bool ok = true;
 #pragma unroll
-        for (int q = 0; q < MAXR; ++q) M[q * COL_BLOCK] = 0u;
-#pragma unroll 1
-        for (int k = 0; k < deg; ++k) {
-            int32_t g[8];
-            const int64_t e = ent[k] >> 3;
-            const int a = ent[k] & 7;
-            const int sg = seg_of(T, e);
-            load_conn8(T.conn[sg], e - T.start[sg], T.conn_stride[sg], g);
+        for (int k = 0; k < 8; ++k) {
+            if (k >= deg) continue;
 #pragma unroll
             for (int b = 0; b < 8; ++b) {
-                const int32_t v = g[b];
-                if (v <= c) continue;
-                int lo = 1, hi = m;  // lower_bound over rows 1..m-1
-                while (lo < hi) {
-                    const int mid = (lo + hi) >> 1;
-                    if (R[mid * COL_BLOCK] < v) lo = mid + 1; else hi = mid;
+                const int32_t v = g[k][b];
+                if (v <= c) continue;  // the diagonal (v == c) is implicit
+                uint32_t h = hash_slot(v);
+                int probe = 0;
+#pragma unroll 1
+                for (; probe < MAXR; ++probe) {
+                    const int32_t cur = H[h * COL_BLOCK];
+                    if (cur == v || cur == HASH_EMPTY) break;
+                    h = (h + 1) & (MAXR - 1);
                 }
-                const uint64_t w = M[lo * COL_BLOCK];
-                if ((w & 7u) == MAX_OFFDIAG_CONTRIB) {
-                    ok = false;
-                } else {
-                    M[lo * COL_BLOCK] = contrib_push(w, k, pack_index(max(a, b), min(a, b)));
+                if (probe == MAXR) {
+                    ok = false;  // more than MAXR distinct rows
+                    continue;
                 }
+                H[h * COL_BLOCK] = v;
+                const uint32_t w = W[h * COL_BLOCK];
+                const uint32_t n = w & 7u;
+                if (n == MAX_OFFDIAG_CONTRIB) ok = false;
+                else W[h * COL_BLOCK] = (w + 1u) | ((uint32_t)(k << 3 | b) << (3 + 6 * n));
             }
         }
-        if (!ok) atomicOr(status, HX_ST_ROW_OVERFLOW);
-    }
-
-    // ---- tile offset (decoupled look-back) ----
-    if (LOOKBACK) {
-        if (t == 0) {
-            int64_t prefix = 0;
-            if (tile > 0) {
-                for (int64_t p = tile - 1; p >= 0;) {
-                    const unsigned long long w = tile_read(tile_state, p);
-                    if ((w & ~TILE_VAL) == 0) continue;  // predecessor still in phase A1
-                    prefix += (int64_t)(w & TILE_VAL);
-                    if ((w & ~TILE_VAL) == TILE_INC) break;
-                    --p;
+        if (!ok) {
+            atomicOr(status, HX_ST_ROW_OVERFLOW);
+            deg = 0;
+        } else {
+            int32_t key[MAXR];
+#pragma unroll
+            for (int q = 0; q < MAXR; ++q) key[q] = H[q * COL_BLOCK];
+            sort32(key);
+            m = 1;
+#pragma unroll
+            for (int q = 0; q < MAXR; ++q) m += key[q] != HASH_EMPTY;
+            uint32_t ws[MAXR];
+#pragma unroll
+            for (int q = 0; q < MAXR; ++q) {
+                ws[q] = 0u;
+                if (q + 1 < m) {
+                    uint32_t h = hash_slot(key[q]);
+#pragma unroll 1
+                    while (H[h * COL_BLOCK] != key[q]) h = (h + 1) & (MAXR - 1);
+                    ws[q] = W[h * COL_BLOCK];
                 }
-                tile_publish(tile_state, tile, TILE_INC | (unsigned long long)(prefix + total));
             }
-            s_base = prefix;
+#pragma unroll
+            for (int q = 0; q < MAXR; ++q) {
+                H[q * COL_BLOCK] = key[q];
+                W[q * COL_BLOCK] = ws[q];
+            }
         }
-        __syncthreads();
-        base = s_base;
-        if (cl < ncols) col_ptr[cl] = base + excl;
-        if (cl == ncols - 1) col_ptr[ncols] = base + excl + m;
-    } else {
-        __syncthreads();
     }
+    if (cl < ncols) col_ptr[cl] = m;
 
-    // ---- phase B ----
+    // compact scratch: this block's off-diagonal records
+    int excl, total;
+    const int off = m > 0 ? m - 1 : 0;
+    BlockScan(scan_tmp).ExclusiveSum(off, excl, total);
+    if (t == 0) {
+        s_base = atomicAdd(scratch_top, (unsigned long long)total);
+        block_scratch[blockIdx.x] = (int64_t)s_base;
+    }
+    __syncthreads();
+    const int64_t sb = (int64_t)s_base + excl;
+    if (sb + off > scratch_capacity) {
+        if (off > 0) atomicOr(status, HX_ST_SCRATCH_OVERFLOW);
+        return;
+    }
+#pragma unroll 1
+    for (int j = 0; j < off; ++j) scratch[sb + j] = make_int2(H[j * COL_BLOCK], (int)W[j * COL_BLOCK]);
+}
+
+// Rows only (symbolic without values).
+__global__ void __launch_bounds__(EMIT_BLOCK)
+emit_rows_kernel(int64_t col_lo, int64_t ncols, const int64_t *__restrict__ col_ptr, const int2 *__restrict__ scratch,
+                 const int64_t *__restrict__ block_scratch, int64_t *__restrict__ row_idx, int64_t capacity) {
+    __shared__ int64_t s_cp[COL_BLOCK + 1];
+    const int64_t first = (int64_t)blockIdx.x * COL_BLOCK;
+    const int ncol = (int)(ncols - first < COL_BLOCK ? ncols - first : COL_BLOCK);
+    for (int i = threadIdx.x; i <= ncol; i += EMIT_BLOCK) s_cp[i] = col_ptr[first + i];
+    __syncthreads();
+    const int64_t base = s_cp[0];
+    const int total = (int)(s_cp[ncol] - base);
+    const int64_t sb = block_scratch[blockIdx.x];
     const int64_t room = capacity - base;
-    const int limit = room <= 0 ? 0 : (room < total ? (int)room : total);  // beyond capacity: caller retries
-    // diagonals: entry s_excl[u] of column u
-    if (cl < ncols && s_deg[t] > 0 && excl < limit) {
-        const int64_t o = base + excl;
-        if (ROWS) row_idx[o] = c;
-        if (VALS) {
-            const int dg = s_deg[t];
-            double x[8];
-#pragma unroll
-            for (int k = 0; k < 8; ++k) {
-                x[k] = 0.0;
-                if (k < dg) {
-                    const int a = sA[k * COL_BLOCK + t];
-                    x[k] = __ldg(sP[k * COL_BLOCK + t] + pack_index(a, a));
-                }
-            }
-            double v = x[0];
-            if (dg >= 2) {
-                double sum = x[1];
-#pragma unroll
-                for (int k = 2; k < 8; ++k)
-                    if (k < dg) sum = __dadd_rn(sum, x[k]);
-                v = __dadd_rn(x[0], sum);
-            }
-            vals[o] = v;
-        }
-    }
-    // off-diagonals: q-th off-diagonal entry of the tile
-    const int dtotal = s_dexcl[COL_BLOCK];
-    for (int q = t; q < dtotal; q += COL_BLOCK) {
-        int lo = 0, hi = COL_BLOCK;  // column of off-diagonal q: largest u with s_dexcl[u] <= q
+    const int limit = room <= 0 ? 0 : (room < total ? (int)room : total);
+    for (int o = threadIdx.x; o < limit; o += EMIT_BLOCK) {
+        int lo = 0, hi = ncol;
+#pragma unroll 1
         while (hi - lo > 1) {
             const int mid = (lo + hi) >> 1;
-            if (s_dexcl[mid] <= q) lo = mid; else hi = mid;
+            if (s_cp[mid] - base <= o) lo = mid; else hi = mid;
         }
-        const int u = lo;
-        const int j = q - s_dexcl[u] + 1;
-        const int o = s_excl[u] + j;
-        if (o >= limit) continue;
-        if (ROWS) row_idx[base + o] = sR[j * COL_BLOCK + u];
-        if (VALS) {
-            const uint64_t w = sM[j * COL_BLOCK + u];
-            const int n = (int)(w & 7u);
-            double x[MAX_OFFDIAG_CONTRIB];
+        const int j = (int)(o - (s_cp[lo] - base));
+        row_idx[base + o] = j == 0 ? (int64_t)(col_lo + first + lo) : (int64_t)scratch[sb + o - lo - 1].x;
+    }
+}
+
+// 6. Emit pass: block b re-walks the output entries of the same COL_BLOCK columns (coalesced
+// scratch reads, row_idx / vals stores).  Diagonals first (one per column: every incident element
+// at its own local node), then the off-diagonal scratch records in output order.  Values are
+// gathered from the KE rows and reduced with numpy add.reduceat's rule v0 + (((v1 + v2) + v3) + ...).
+// SINGLE: one dense element segment (the single-GPU build) -> KE row = ke + 36 e.
+template <bool SINGLE>
+__device__ __forceinline__ const double *ke_row(const SegTable &T, int64_t e) {
+    if (SINGLE) return T.ke[0] + 36 * e;
+    const int sg = seg_of(T, e);
+    return T.ke[sg] + T.ke_stride[sg] * (e - T.start[sg]);
+}
+
+template <bool ROWS, bool SINGLE>
+__global__ void __launch_bounds__(EMIT_BLOCK)
+emit_kernel(SegTable T, int64_t col_lo, int64_t ncols, const int32_t *__restrict__ adj_ptr,
+            const int32_t *__restrict__ adj, const int64_t *__restrict__ col_ptr, const int2 *__restrict__ scratch,
+            const int64_t *__restrict__ block_scratch, int64_t *__restrict__ row_idx, double *__restrict__ vals,
+            int64_t capacity) {
+    __shared__ int64_t s_cp[COL_BLOCK + 1];
+    __shared__ int32_t s_aptr[COL_BLOCK + 1];
+    __shared__ uint8_t s_col[COL_BLOCK * MAXR];  // column of each off-diagonal record of the block
+    const int64_t first = (int64_t)blockIdx.x * COL_BLOCK;
+    const int ncol = (int)(ncols - first < COL_BLOCK ? ncols - first : COL_BLOCK);
+    for (int i = threadIdx.x; i <= ncol; i += EMIT_BLOCK) {
+        s_cp[i] = col_ptr[first + i];
+        s_aptr[i] = adj_ptr[first + i];
+    }
+    __syncthreads();
+    const int64_t base = s_cp[0];
+    const int64_t room = capacity - base;
+    const int64_t sb = block_scratch[blockIdx.x];
+    for (int u = threadIdx.x; u < ncol; u += EMIT_BLOCK) {
+        const int o0 = (int)(s_cp[u] - base), o1 = (int)(s_cp[u + 1] - base);
+        for (int q = o0 - u; q < o1 - u - 1; ++q) s_col[q] = (uint8_t)u;
+    }
+    __syncthreads();
+    // diagonals
+    for (int u = threadIdx.x; u < ncol; u += EMIT_BLOCK) {
+        const int o = (int)(s_cp[u] - base);
+        if (s_cp[u + 1] == s_cp[u] || o >= room) continue;
+        const int deg = s_aptr[u + 1] - s_aptr[u];
+        const int32_t *ent = adj + s_aptr[u];
+        if (ROWS) row_idx[base + o] = col_lo + first + u;
+        double x[8];
 #pragma unroll
-            for (int i = 0; i < MAX_OFFDIAG_CONTRIB; ++i) {
-                x[i] = 0.0;
-                if (i < n) {
-                    const uint32_t kp = (uint32_t)(w >> (3 + 9 * i)) & 511u;
-                    x[i] = __ldg(sP[(kp >> 6) * COL_BLOCK + u] + (kp & 63u));
-                }
+        for (int k = 0; k < 8; ++k) {
+            x[k] = 0.0;
+            if (k < deg) {
+                const int32_t en = __ldg(ent + k);
+                const int a = en & 7;
+                x[k] = __ldg(ke_row<SINGLE>(T, en >> 3) + pack_index(a, a));
             }
-            double v = x[0];
-            if (n >= 2) {
-                double sum = x[1];
-#pragma unroll
-                for (int i = 2; i < MAX_OFFDIAG_CONTRIB; ++i)
-                    if (i < n) sum = __dadd_rn(sum, x[i]);
-                v = __dadd_rn(x[0], sum);
-            }
-            vals[base + o] = v;
         }
+        double v = x[0];
+        if (deg >= 2) {
+            double sum = x[1];
+#pragma unroll
+            for (int k = 2; k < 8; ++k)
+                if (k < deg) sum = __dadd_rn(sum, x[k]);
+            v = __dadd_rn(x[0], sum);
+        }
+        vals[base + o] = v;
+    }
+    // off-diagonals
+    const int n_off = (int)(s_cp[ncol] - base) - ncol;
+    for (int q = threadIdx.x; q < n_off; q += EMIT_BLOCK) {
+        const int u = s_col[q];
+        const int o = q + u + 1;
+        if (o >= room) continue;  // beyond capacity: the caller retries
+        const int2 rec = scratch[sb + q];
+        if (ROWS) row_idx[base + o] = rec.x;
+        const uint32_t w = (uint32_t)rec.y;
+        const int n = (int)(w & 7u);
+        const int32_t *ent = adj + s_aptr[u];
+        double x[MAX_OFFDIAG_CONTRIB];
+#pragma unroll
+        for (int r = 0; r < MAX_OFFDIAG_CONTRIB; ++r) {
+            x[r] = 0.0;
+            if (r < n) {
+                const uint32_t kb = (w >> (3 + 6 * r)) & 63u;
+                const int32_t en = __ldg(ent + (kb >> 3));
+                const int a = en & 7, b = (int)(kb & 7u);
+                x[r] = __ldg(ke_row<SINGLE>(T, en >> 3) + pack_index(max(a, b), min(a, b)));
+            }
+        }
+        double v = x[0];
+        if (n >= 2) {
+            double sum = x[1];
+#pragma unroll
+            for (int r = 2; r < MAX_OFFDIAG_CONTRIB; ++r)
+                if (r < n) sum = __dadd_rn(sum, x[r]);
+            v = __dadd_rn(x[0], sum);
+        }
+        vals[base + o] = v;
     }
 }
 
 // Workspace layout (all offsets 256-B aligned):
 //   adj_ptr (ncols+1) i32 | cursor/deg (ncols+1) i32 | adj (8*n_total) i32 |
-//   tile_state (tiles) u64 | tile_ticket i32 | cub temp
+//   block_scratch (blocks) i64 | scratch_top u64 | scratch (SCRATCH_PER_COL*ncols) int2 | cub temp
+constexpr int64_t SCRATCH_PER_COL = 15;  // off-diagonal records per column reserved (hex: 13 avg)
 struct MeshWs {
-    int32_t *adj_ptr, *deg, *adj, *tile_ticket;
-    unsigned long long *tile_state;
+    int32_t *adj_ptr, *deg, *adj;
+    int64_t *block_scratch;
+    unsigned long long *scratch_top;
+    int2 *scratch;
+    int64_t scratch_capacity;
     void *cub_tmp;
     size_t cub_bytes;
     size_t total;
 };
 
 static size_t cub_scan_bytes(int64_t ncols) {
-    size_t b1 = 0;
+    size_t b1 = 0, b2 = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, b1, (int32_t *)nullptr, (int32_t *)nullptr, (int)(ncols + 1));
-    return b1;
+    cub::DeviceScan::ExclusiveSum(nullptr, b2, (int64_t *)nullptr, (int64_t *)nullptr, (int)(ncols + 1));
+    return std::max(b1, b2);
 }
 
 static MeshWs mesh_ws_layout(void *base, int64_t n_total, int64_t ncols) {
@@ -486,8 +462,10 @@ static MeshWs mesh_ws_layout(void *base, int64_t n_total, int64_t ncols) {
     const size_t o_ptr = take(sizeof(int32_t) * (ncols + 1));
     const size_t o_deg = take(sizeof(int32_t) * (ncols + 1));
     const size_t o_adj = take(sizeof(int32_t) * 8 * std::max<int64_t>(n_total, 1));
-    const size_t o_ts = take(sizeof(unsigned long long) * std::max<int64_t>(1, ceil_div(ncols, COL_BLOCK)));
-    const size_t o_tt = take(sizeof(int32_t));
+    const size_t o_bs = take(sizeof(int64_t) * std::max<int64_t>(1, ceil_div(ncols, COL_BLOCK)));
+    const size_t o_st = take(sizeof(unsigned long long));
+    w.scratch_capacity = std::max<int64_t>(1, SCRATCH_PER_COL * ncols);
+    const size_t o_sc = take(sizeof(int2) * w.scratch_capacity);
     w.cub_bytes = cub_scan_bytes(ncols);
     const size_t o_cub = take(w.cub_bytes);
     w.total = off;
@@ -496,8 +474,9 @@ static MeshWs mesh_ws_layout(void *base, int64_t n_total, int64_t ncols) {
         w.adj_ptr = (int32_t *)(b + o_ptr);
         w.deg = (int32_t *)(b + o_deg);
         w.adj = (int32_t *)(b + o_adj);
-        w.tile_state = (unsigned long long *)(b + o_ts);
-        w.tile_ticket = (int32_t *)(b + o_tt);
+        w.block_scratch = (int64_t *)(b + o_bs);
+        w.scratch_top = (unsigned long long *)(b + o_st);
+        w.scratch = (int2 *)(b + o_sc);
         w.cub_tmp = b + o_cub;
     }
     return w;
@@ -539,6 +518,8 @@ static int make_segtable(const hx_elem_segment *segs, int32_t n_segs, SegTable &
     return HX_OK;
 }
 
+
+static bool single_dense(const SegTable &T) { return T.n == 1 && T.ke_stride[0] == 36; }
 
 static unsigned grid_for(int64_t n, int threads) {
     return (unsigned)std::max<int64_t>(1, ceil_div(n, threads));
@@ -588,20 +569,30 @@ static int mesh_csc_build(const hx_elem_segment *segs, int32_t n_segs, int64_t n
                                                                       w.deg, w.adj);
         HX_CHECK_LAUNCH("adjacency_fill_kernel");
     }
-    const int64_t tiles = ceil_div(ncols, COL_BLOCK);
-    HX_TRY_CUDA(cudaMemsetAsync(w.tile_state, 0, sizeof(unsigned long long) * std::max<int64_t>(tiles, 1), s));
-    HX_TRY_CUDA(cudaMemsetAsync(w.tile_ticket, 0, sizeof(int32_t), s));
     if (ncols > 0) {
+        const unsigned tiles = (unsigned)ceil_div(ncols, COL_BLOCK);
+        HX_TRY_CUDA(cudaMemsetAsync(w.scratch_top, 0, sizeof(unsigned long long), s));
+        pattern_kernel<<<tiles, COL_BLOCK, 0, s>>>(T, col_lo, ncols, w.adj_ptr, w.adj, col_ptr, w.scratch,
+                                                   w.scratch_capacity, w.scratch_top, w.block_scratch, status);
+        HX_CHECK_LAUNCH("pattern_kernel");
+        HX_TRY_CUDA(cudaMemsetAsync(col_ptr + ncols, 0, sizeof(int64_t), s));
+        size_t cb2 = w.cub_bytes;
+        HX_TRY_CUDA(cub::DeviceScan::ExclusiveSum(w.cub_tmp, cb2, col_ptr, col_ptr, (int)(ncols + 1), s));
         if (vals != nullptr) {
-            column_pass_kernel<true, true, true><<<(unsigned)tiles, COL_BLOCK, 0, s>>>(
-                T, col_lo, ncols, w.adj_ptr, w.adj, col_ptr, row_idx, row_capacity, vals, w.tile_state,
-                w.tile_ticket, status);
+            if (single_dense(T))
+                emit_kernel<true, true><<<tiles, EMIT_BLOCK, 0, s>>>(T, col_lo, ncols, w.adj_ptr, w.adj, col_ptr,
+                                                                    w.scratch, w.block_scratch, row_idx, vals,
+                                                                    row_capacity);
+            else
+                emit_kernel<true, false><<<tiles, EMIT_BLOCK, 0, s>>>(T, col_lo, ncols, w.adj_ptr, w.adj, col_ptr,
+                                                                     w.scratch, w.block_scratch, row_idx, vals,
+                                                                     row_capacity);
+            HX_CHECK_LAUNCH("emit_kernel");
         } else {
-            column_pass_kernel<true, false, true><<<(unsigned)tiles, COL_BLOCK, 0, s>>>(
-                T, col_lo, ncols, w.adj_ptr, w.adj, col_ptr, row_idx, row_capacity, nullptr, w.tile_state,
-                w.tile_ticket, status);
+            emit_rows_kernel<<<tiles, EMIT_BLOCK, 0, s>>>(col_lo, ncols, col_ptr, w.scratch, w.block_scratch, row_idx,
+                                                         row_capacity);
+            HX_CHECK_LAUNCH("emit_rows_kernel");
         }
-        HX_CHECK_LAUNCH("column_pass_kernel");
     } else {
         HX_TRY_CUDA(cudaMemsetAsync(col_ptr, 0, sizeof(int64_t), s));
     }
@@ -643,10 +634,13 @@ extern "C" int hx_mesh_csc_numeric(const hx_elem_segment *segs, int32_t n_segs, 
     MeshWs w = mesh_ws_layout(const_cast<void *>(workspace), n_total, ncols);
     cudaStream_t s = (cudaStream_t)stream;
     if (ncols > 0) {
-        column_pass_kernel<false, true, false><<<(unsigned)ceil_div(ncols, COL_BLOCK), COL_BLOCK, 0, s>>>(
-            T, col_lo, ncols, w.adj_ptr, w.adj, const_cast<int64_t *>(col_ptr), const_cast<int64_t *>(row_idx),
-            INT64_MAX, vals, nullptr, nullptr, status);
-        HX_CHECK_LAUNCH("column_pass_kernel<numeric>");
+        if (single_dense(T))
+            emit_kernel<false, true><<<(unsigned)ceil_div(ncols, COL_BLOCK), EMIT_BLOCK, 0, s>>>(
+                T, col_lo, ncols, w.adj_ptr, w.adj, col_ptr, w.scratch, w.block_scratch, nullptr, vals, INT64_MAX);
+        else
+            emit_kernel<false, false><<<(unsigned)ceil_div(ncols, COL_BLOCK), EMIT_BLOCK, 0, s>>>(
+                T, col_lo, ncols, w.adj_ptr, w.adj, col_ptr, w.scratch, w.block_scratch, nullptr, vals, INT64_MAX);
+        HX_CHECK_LAUNCH("emit_kernel<numeric>");
     }
     return HX_OK;
 }
