@@ -31,6 +31,7 @@ sys.path.insert(0, str(ROOT))
 METRIC = "hex8 elements/s (KE+index+CSR assembly), % HBM roofline, 1/2/4/8 GPUs"
 UNIT = "elements/s"
 # algorithmic bytes: each API array touched once
+KE_KERNEL = "integrate_mesh_kernel"  # KE + fused iK/jK
 KE_INDEX_BYTES_PER_EL = 32 + 8 + 288 + 288  # conn + coeff + KE f64 + iK/jK i32 (+ 24 B/node coords)
 
 
@@ -53,6 +54,16 @@ def algorithmic_bytes(n_el, n_nodes, nnz):
     ke_index = KE_INDEX_BYTES_PER_EL * n_el + 24 * n_nodes
     full = ke_index + 16 * nnz + 8 * (n_nodes + 1)
     return ke_index, full
+
+
+def load_traffic(workload, kernel):
+    """DRAM bytes (read + write) per launch of `kernel` at `workload`, from the committed ncu
+    --set full capture summary (profiles/traffic.json), or None when there is none."""
+    try:
+        t = json.loads((ROOT / "profiles" / "traffic.json").read_text())
+        return float(t[workload][kernel]["dram_bytes_per_launch"])
+    except Exception:
+        return None
 
 
 def load_peaks():
@@ -295,7 +306,7 @@ def run_ours(args):
                        "parallelism": f"element-range shards + column blocks x{world}" if world > 1 else "single GPU",
                        "mesh_gen_s": round(t_mesh, 2)},
             "roofline": {"bound": "hbm", "achieved": achieved_ke, "peak": peak, "unit": "GB/s",
-                         "frac": achieved_ke / peak, "traffic": None, "kernel": "integrate_mesh_kernel (KE + iK/jK)",
+                         "frac": achieved_ke / peak, "traffic": load_traffic(wl, KE_KERNEL) if world == 1 else None, "kernel": KE_KERNEL,
                          "algorithmic_bytes_per_el": ke_bytes / n_el_total, "peak_kind": peak_kind,
                          "kernel_ms": kernel["ke_ms"], "kernel_share_of_step": kernel["ke_ms"] / ms,
                          "note": "exact mode is FP64-ALU bound (~3.8k DP instr/element), see DESIGN.md"},
@@ -326,17 +337,24 @@ def measure_kernels(args, rank, world, runner, dm):
 
     reps = 3
     acc = {"ke_ms": 0.0, "assembly_ms": 0.0}
-    for _ in range(reps):
+    n = dm.n_el
+    # outputs allocated outside the timed region (a cudaMalloc inside it would stall the stream)
+    ke = torch.empty((n, 36), dtype=torch.float64, device=dm.conn.device)
+    rows = torch.empty(36 * n, dtype=torch.int32, device=dm.conn.device)
+    cols = torch.empty(36 * n, dtype=torch.int32, device=dm.conn.device)
+    for it in range(reps + 1):
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
         ev[0].record()
-        ke, rows, cols, fail = D.integrate_mesh(dm, mode=args.mode)
+        D.integrate_mesh(dm, ke=ke, rows=rows, cols=cols, mode=args.mode)
         ev[1].record()
         csc = D.mesh_csc([(dm.conn, ke)], dm.n_nodes)
         ev[2].record()
         torch.cuda.synchronize()
-        acc["ke_ms"] += ev[0].elapsed_time(ev[1]) / reps
-        acc["assembly_ms"] += ev[1].elapsed_time(ev[2]) / reps
-        del ke, rows, cols, csc
+        if it:  # first pass warms the allocator
+            acc["ke_ms"] += ev[0].elapsed_time(ev[1]) / reps
+            acc["assembly_ms"] += ev[1].elapsed_time(ev[2]) / reps
+        del csc
+    del ke, rows, cols
     # integrate_mesh_kernel, fail_resolve, degree, adjacency_fill, column<count>, column<values>,
     # 2 CUB scans (2 kernels each)
     acc["launches_per_step"] = 10
