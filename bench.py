@@ -355,9 +355,9 @@ def measure_kernels(args, rank, world, runner, dm):
             acc["assembly_ms"] += ev[1].elapsed_time(ev[2]) / reps
         del csc
     del ke, rows, cols
-    # integrate_mesh_kernel, fail_resolve, degree, adjacency_fill, column<count>, column<values>,
+    # integrate_mesh_kernel, fail_resolve, adjacency, pattern, emit, CUB scan (init + scan)
     # 2 CUB scans (2 kernels each)
-    acc["launches_per_step"] = 10
+    acc["launches_per_step"] = 7
     return acc
 
 

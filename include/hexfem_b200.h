@@ -48,9 +48,12 @@ extern "C" {
 #define HX_ST_REPEATED_NODE 4u /* an element lists the same node twice                     */
 #define HX_ST_BAD_INDEX 8u     /* index outside [0, dim) (MeshValidationError, assemble.py:146) */
 #define HX_ST_UPPER 16u        /* triplet above the diagonal (MeshValidationError, assemble.py:148) */
-#define HX_ST_SCRATCH_OVERFLOW 32u /* pattern scratch too small (> 15 off-diagonals per column on average) */
-/* DEG/ROW/REPEATED/SCRATCH mean "mesh fast path not applicable": the caller re-runs the generic
- * triplet path (hx_triplet_csc_*), which has no such limits. */
+#define HX_ST_SCRATCH_OVERFLOW 32u /* pattern scratch too small (> 15 off-diagonals per column on average):
+                                    * col_ptr is complete; re-run with workspace_bytes +=
+                                    * 8 * col_ptr[ncols] */
+/* DEG/ROW/REPEATED mean "mesh fast path not applicable": the caller re-runs the generic triplet
+ * path (hx_triplet_csc_*), which has no such limits.  With any of the four bits set the entry
+ * points write no row_idx / vals. */
 
 #define HX_MAX_NODE_DEGREE 8
 #define HX_MAX_COL_ROWS 32
@@ -120,6 +123,8 @@ int hx_connectivity_index_arrays(const int32_t *conn, int64_t lo, int64_t hi, in
  *   numeric:  writes vals (nnz) f64, summing duplicates in element order with numpy
  *             add.reduceat's rule (bitwise equal to assemble.py:135).
  * The workspace written by symbolic must be passed unchanged to numeric. */
+/* Default workspace (scratch for 15 off-diagonal records per column); any larger workspace is
+ * used in full as scratch. */
 int64_t hx_mesh_csc_workspace_bytes(int64_t n_el_total, int64_t n_cols);
 int hx_mesh_csc_symbolic(const hx_elem_segment *segs, int32_t n_segs, int64_t n_nodes,
                          int64_t col_lo, int64_t col_hi, int64_t *col_ptr, int64_t *row_idx,

@@ -13,7 +13,10 @@ from pathlib import Path
 
 from .errors import ConfigurationError, NativeLibraryError
 
-LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libhexfem_b200.so"
+import os
+
+# HEXFEM_B200_LIB: alternate build of the same library (kernel experiments only).
+LIB_PATH = Path(os.environ.get("HEXFEM_B200_LIB") or Path(__file__).resolve().parent / "_lib" / "libhexfem_b200.so")
 
 HX_OK, HX_ERR_VALUE, HX_ERR_CONFIG, HX_ERR_CUDA, HX_ERR_WORKSPACE = 0, 1, 2, 3, 4
 ST_DEG_OVERFLOW, ST_ROW_OVERFLOW, ST_REPEATED_NODE, ST_BAD_INDEX, ST_UPPER, ST_SCRATCH = 1, 2, 4, 8, 16, 32

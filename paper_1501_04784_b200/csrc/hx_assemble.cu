@@ -1,27 +1,27 @@
 // hx_assemble.cu -- on-GPU lower-triangular CSC assembly for hex8 meshes (the paper's CPU
 // sparse()/sparse_create step, assemble.py:110-239), node-adjacency based:
 //
-//   symbolic  1. degree count   deg[c]   = #incident (element, local node) pairs     (atomics)
-//             2. adj_ptr        = exclusive scan(deg)                                 (CUB)
-//             3. adjacency fill adj[adj_ptr[c] + slot] = (e << 3) | a                 (atomics)
-//             4. column count   cnt[c]   = #distinct rows r >= c over incident elements
-//             5. col_ptr        = exclusive scan(cnt) (int64)                         (CUB)
-//   numeric   6. column fill    per column: incident elements in ascending element order,
-//                               rows sorted ascending, duplicates summed in element order
-//                               with numpy add.reduceat's rule v0 + (((v1+v2)+v3)+...)
+//   symbolic  1. adjacency   node -> incident (element << 3 | local node), 8 fixed slots per
+//                            node (atomic slot counter; valence > 8 leaves the fast path)
+//             2. pattern     per column c: incident elements sorted by id (= the stable-sort order of
+//                            assemble.py:125), distinct rows r > c from a 32-slot shared-memory hash
+//                            set, each carrying its contribution list (<= 4 (element, local node)
+//                            pairs in element order); keys compacted and sorted by a register network;
+//                            column count -> CUB scan -> col_ptr (int64); sorted off-diagonal records
+//                            (row, contribution word) -> compact per-block scratch
+//   numeric   3. emit        per output entry: gather the KE contributions in element order and sum
+//                            them with numpy add.reduceat's rule v0 + (((v1 + v2) + v3) + ...)
+//                            (bitwise equal to assemble.py:135); coalesced row_idx / vals stores
 //
 // Column c of the lower triangle holds rows {g_b : e incident to c, g_b >= c}; its triplet
-// contributions are exactly the packed entries p = tri(max(a,b), min(a,b)) of the incident
-// elements (a = local index of c).  Each thread owns one column; the incident list is sorted in
-// registers (ascending element id = the stable-sort order of assemble.py:125), the distinct
-// rows are kept as a sorted list in shared memory, and each row keeps (v0, running tail sum)
-// so the float result is bitwise equal to np.add.reduceat over the lexsorted triplets.
+// contributions are exactly the packed entries p = tri(max(a,b), min(a,b)) of the incident elements
+// (a = local index of c).
 //
-// Fast-path limits (reported through the status word, the caller then uses the generic
-// triplet path which has none): node degree <= HX_MAX_NODE_DEGREE (8: hex meshes with
-// regular vertices), distinct rows per column <= HX_MAX_COL_ROWS, no repeated node in an
-// element.  With degree <= 8 every duplicate run has <= 8 terms, where numpy's pairwise sum
-// degenerates to the sequential sum implemented here.
+// Fast-path limits (reported through the status word; the caller then uses the generic triplet
+// path, which has none): node valence <= HX_MAX_NODE_DEGREE (8: hex meshes with regular vertices),
+// distinct rows per column <= HX_MAX_COL_ROWS, no repeated node in an element.  With valence <= 8
+// every duplicate run has <= 8 terms, where numpy's pairwise sum degenerates to the sequential sum
+// implemented here.
 #include <cub/block/block_scan.cuh>
 #include <cub/device/device_scan.cuh>
 
@@ -59,42 +59,26 @@ __device__ __forceinline__ void load_conn8(const int32_t *__restrict__ conn, int
     g[4] = hi.x; g[5] = hi.y; g[6] = hi.z; g[7] = hi.w;
 }
 
-// 1. degree count over columns [col_lo, col_hi); also validates node ids against [0, n_nodes).
-__global__ void degree_kernel(SegTable T, int64_t n_total, int64_t n_nodes, int64_t col_lo, int64_t col_hi,
-                              int32_t *__restrict__ deg, uint32_t *__restrict__ status) {
-    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n_total;
-         e += (int64_t)gridDim.x * blockDim.x) {
+// 1. adjacency: one thread per (element, local node); also validates node ids against [0, n_nodes).
+// adj[(v - col_lo) * 8 + slot] = (combined element index << 3) | local node, slot from an atomic
+// counter (slot order is arbitrary: the pattern pass sorts each node's list by element).
+__global__ void adjacency_kernel(SegTable T, int64_t n_total, int64_t n_nodes, int64_t col_lo, int64_t col_hi,
+                                 int32_t *__restrict__ deg, int32_t *__restrict__ adj, uint32_t *__restrict__ status) {
+    for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < 8 * n_total;
+         w += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t e = w >> 3;
+        const int a = (int)(w & 7);
         const int s = seg_of(T, e);
-        int32_t g[8];
-        load_conn8(T.conn[s], e - T.start[s], T.conn_stride[s], g);
-        bool bad = false;
-#pragma unroll
-        for (int a = 0; a < 8; ++a) {
-            const int32_t v = g[a];
-            bad |= (v < 0) | ((int64_t)v >= n_nodes);
-            if (v >= col_lo && v < col_hi) atomicAdd(deg + (v - col_lo), 1);
+        const int32_t v = __ldg(T.conn[s] + (e - T.start[s]) * T.conn_stride[s] + a);
+        if (v < 0 || (int64_t)v >= n_nodes) {
+            atomicOr(status, HX_ST_BAD_INDEX);
+            continue;
         }
-        if (bad) atomicOr(status, HX_ST_BAD_INDEX);
-    }
-}
-
-// 3. adjacency fill; entry = (combined element index << 3) | local node.
-__global__ void adjacency_fill_kernel(SegTable T, int64_t n_total, int64_t col_lo, int64_t col_hi,
-                                      const int32_t *__restrict__ adj_ptr, int32_t *__restrict__ cursor,
-                                      int32_t *__restrict__ adj) {
-    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n_total;
-         e += (int64_t)gridDim.x * blockDim.x) {
-        const int s = seg_of(T, e);
-        int32_t g[8];
-        load_conn8(T.conn[s], e - T.start[s], T.conn_stride[s], g);
-#pragma unroll
-        for (int a = 0; a < 8; ++a) {
-            const int32_t v = g[a];
-            if (v >= col_lo && v < col_hi) {
-                const int64_t c = v - col_lo;
-                const int32_t pos = adj_ptr[c] + atomicAdd(cursor + c, 1);
-                adj[pos] = (int32_t)((e << 3) | a);
-            }
+        if (v >= col_lo && v < col_hi) {
+            const int64_t c = v - col_lo;
+            const int slot = atomicAdd(deg + c, 1);
+            if (slot < MAXDEG) adj[8 * c + slot] = (int32_t)((e << 3) | a);
+            else atomicOr(status, HX_ST_DEG_OVERFLOW);
         }
     }
 }
@@ -131,17 +115,13 @@ __device__ __forceinline__ bool insert_row(int32_t *R, int &m, int32_t v) {
 
 // Incident elements of column cl, sorted by element id (= the stable triplet order).
 // Returns deg, or -1 with a status bit when the column is outside the fast path.
-__device__ __forceinline__ int incident_sorted(int64_t cl, const int32_t *__restrict__ adj_ptr,
+__device__ __forceinline__ int incident_sorted(int64_t cl, const int32_t *__restrict__ deg_arr,
                                                const int32_t *__restrict__ adj, int32_t (&ent)[8],
                                                uint32_t *__restrict__ status) {
-    const int32_t beg = __ldg(adj_ptr + cl), end = __ldg(adj_ptr + cl + 1);
-    const int deg = end - beg;
-    if (deg > MAXDEG) {
-        atomicOr(status, HX_ST_DEG_OVERFLOW);
-        return -1;
-    }
+    const int deg = __ldg(deg_arr + cl);
+    if (deg > MAXDEG) return -1;  // flagged by the adjacency pass
 #pragma unroll
-    for (int k = 0; k < 8; ++k) ent[k] = k < deg ? __ldg(adj + beg + k) : INT32_MAX;
+    for (int k = 0; k < 8; ++k) ent[k] = k < deg ? __ldg(adj + 8 * cl + k) : INT32_MAX;
     sort8(ent);
 #pragma unroll
     for (int k = 1; k < 8; ++k) {
@@ -153,22 +133,23 @@ __device__ __forceinline__ int incident_sorted(int64_t cl, const int32_t *__rest
     return deg;
 }
 
-constexpr int32_t HASH_EMPTY = INT32_MAX;  // sorts last
+constexpr int32_t HASH_EMPTY = INT32_MAX;
 constexpr int MAX_OFFDIAG_CONTRIB = 4;     // hex meshes: an edge is shared by at most 4 elements
 constexpr int COL_BLOCK = 64;              // columns per block (pattern: one thread per column)
 constexpr int EMIT_BLOCK = 128;            // emit: threads per COL_BLOCK columns
 
-// Bitonic sorting network on 32 register-resident keys, ascending.
-__device__ __forceinline__ void sort32(int32_t (&v)[32]) {
+// Bitonic sorting network on N register-resident keys, ascending.
+template <int N, typename K>
+__device__ __forceinline__ void bitonic_sort(K (&v)[N]) {
 #pragma unroll
-    for (int k = 2; k <= 32; k <<= 1)
+    for (int k = 2; k <= N; k <<= 1)
 #pragma unroll
         for (int j = k >> 1; j > 0; j >>= 1)
 #pragma unroll
-            for (int i = 0; i < 32; ++i) {
+            for (int i = 0; i < N; ++i) {
                 const int l = i ^ j;
                 if (l > i) {
-                    const int32_t a = v[i], b = v[l];
+                    const K a = v[i], b = v[l];
                     const bool up = (i & k) == 0;
                     v[i] = up ? min(a, b) : max(a, b);
                     v[l] = up ? max(a, b) : min(a, b);
@@ -176,26 +157,41 @@ __device__ __forceinline__ void sort32(int32_t (&v)[32]) {
             }
 }
 
+// Sort the first n (<= N) keys of the per-thread list L[q * COL_BLOCK] in place (padding sorts last).
+template <int N, typename K>
+__device__ __forceinline__ void sort_list(K *L, int n) {
+    K v[N];
+#pragma unroll
+    for (int q = 0; q < N; ++q) v[q] = q < n ? L[q * COL_BLOCK] : (K)~(K)0;
+    bitonic_sort<N, K>(v);
+#pragma unroll
+    for (int q = 0; q < N; ++q)
+        if (q < n) L[q * COL_BLOCK] = v[q];
+}
+
 __device__ __forceinline__ uint32_t hash_slot(int32_t v) { return ((uint32_t)v * 0x9E3779B1u) >> 27; }
 
-// 4. Pattern pass: one thread per column, COL_BLOCK columns per block.
-//   - incident elements sorted by id (= the stable triplet order of assemble.py:125) and
-//     written back to the adjacency, so the emit pass reads them in order;
-//   - distinct rows > c in a 32-slot open-addressing hash set (smem); every slot carries its
-//     contribution word: (incident element k, local node b) pairs appended in ascending element
-//     order (<= 4 per off-diagonal: an edge is shared by <= 4 hexes);
-//   - keys sorted by a register bitonic network; m = 1 + distinct rows -> col_ptr[cl] (the
-//     exclusive scan turns the counts into offsets);
-//   - the column's sorted off-diagonal records (row, word) -> a compact scratch region reserved
-//     per block with one atomic (block order in the scratch is irrelevant: every block records
-//     where its records start).
+// 2. Pattern pass: one thread per column, COL_BLOCK columns per block.
+//   - incident elements sorted by id and written back to the adjacency (the emit pass reads them
+//     in order);
+//   - distinct rows > c in a 32-slot open-addressing hash set (smem, [slot][thread] layout); every
+//     slot carries its contribution word: count (3 bits) + up to 4 (incident k, local node b) pairs
+//     appended in ascending element order;
+//   - occupied slots compacted in place to keys (row << 5 | slot) -- 32-bit when n_nodes <= 2^26,
+//     else 64-bit -- and sorted by a 16- or 32-key register network;
+//   - m = 1 + distinct rows -> col_ptr[cl] (the exclusive scan turns counts into offsets);
+//   - sorted off-diagonal records (row, word) -> a compact scratch region reserved per block with
+//     one atomic (every block records where its records start).
+template <typename K>
 __global__ void __launch_bounds__(COL_BLOCK)
-pattern_kernel(SegTable T, int64_t col_lo, int64_t ncols, const int32_t *__restrict__ adj_ptr,
+pattern_kernel(SegTable T, int64_t col_lo, int64_t ncols, const int32_t *__restrict__ deg_arr,
                int32_t *__restrict__ adj, int64_t *__restrict__ col_ptr, int2 *__restrict__ scratch,
                int64_t scratch_capacity, unsigned long long *__restrict__ scratch_top,
                int64_t *__restrict__ block_scratch, uint32_t *__restrict__ status) {
-    __shared__ int32_t sH[MAXR * COL_BLOCK];   // hash keys, then sorted rows: [slot][t]
-    __shared__ uint32_t sW[MAXR * COL_BLOCK];  // contribution words: [slot][t]
+    __shared__ int32_t sH[MAXR * COL_BLOCK];   // hash keys
+    __shared__ uint32_t sW[MAXR * COL_BLOCK];  // contribution words, by hash slot
+    // compacted / sorted keys (row << 5 | slot): 32-bit keys reuse the hash-key array in place
+    __shared__ K sL[sizeof(K) == 4 ? 1 : MAXR * COL_BLOCK];
     __shared__ unsigned long long s_base;
     using BlockScan = cub::BlockScan<int32_t, COL_BLOCK>;
     __shared__ typename BlockScan::TempStorage scan_tmp;
@@ -204,49 +200,42 @@ pattern_kernel(SegTable T, int64_t col_lo, int64_t ncols, const int32_t *__restr
     const int32_t c = (int32_t)(col_lo + cl);
     int32_t *H = sH + t;
     uint32_t *W = sW + t;
+    K *L = sizeof(K) == 4 ? reinterpret_cast<K *>(sH) + t : sL + t;
 
     int m = 0, deg = 0;
     int32_t ent[8];
     if (cl < ncols) {
-        deg = incident_sorted(cl, adj_ptr, adj, ent, status);
+        deg = incident_sorted(cl, deg_arr, adj, ent, status);
         if (deg < 0) deg = 0;
-        const int32_t beg = __ldg(adj_ptr + cl);
 #pragma unroll
         for (int k = 0; k < 8; ++k)
-            if (k < deg) adj[beg + k] = ent[k];
+            if (k < deg) adj[8 * cl + k] = ent[k];
     }
     if (deg > 0) {
-        int32_t g[8][8];
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            if (k < deg) {
-                const int64_t e = ent[k] >> 3;
-                const int sg = seg_of(T, e);
-                load_conn8(T.conn[sg], e - T.start[sg], T.conn_stride[sg], g[k]);
-            }
-        }
 #pragma unroll
         for (int q = 0; q < MAXR; ++q) {
             H[q * COL_BLOCK] = HASH_EMPTY;
             W[q * COL_BLOCK] = 0u;
         }
         bool ok = true;
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            if (k >= deg) continue;
+#pragma unroll 1
+        for (int k = 0; k < deg; ++k) {
+            const int64_t e = adj[8 * cl + k] >> 3;  // the sorted list just written (own writes)
+            const int sg = seg_of(T, e);
+            int32_t g[8];
+            load_conn8(T.conn[sg], e - T.start[sg], T.conn_stride[sg], g);
 #pragma unroll
             for (int b = 0; b < 8; ++b) {
-                const int32_t v = g[k][b];
+                const int32_t v = g[b];
                 if (v <= c) continue;  // the diagonal (v == c) is implicit
                 uint32_t h = hash_slot(v);
-                int probe = 0;
+                int32_t cur = H[h * COL_BLOCK];
 #pragma unroll 1
-                for (; probe < MAXR; ++probe) {
-                    const int32_t cur = H[h * COL_BLOCK];
-                    if (cur == v || cur == HASH_EMPTY) break;
+                for (int probe = 1; cur != v && cur != HASH_EMPTY && probe < MAXR; ++probe) {
                     h = (h + 1) & (MAXR - 1);
+                    cur = H[h * COL_BLOCK];
                 }
-                if (probe == MAXR) {
+                if (cur != v && cur != HASH_EMPTY) {
                     ok = false;  // more than MAXR distinct rows
                     continue;
                 }
@@ -259,31 +248,19 @@ pattern_kernel(SegTable T, int64_t col_lo, int64_t ncols, const int32_t *__restr
         }
         if (!ok) {
             atomicOr(status, HX_ST_ROW_OVERFLOW);
-            deg = 0;
         } else {
-            int32_t key[MAXR];
-#pragma unroll
-            for (int q = 0; q < MAXR; ++q) key[q] = H[q * COL_BLOCK];
-            sort32(key);
-            m = 1;
-#pragma unroll
-            for (int q = 0; q < MAXR; ++q) m += key[q] != HASH_EMPTY;
-            uint32_t ws[MAXR];
+            int cnt = 0;
 #pragma unroll
             for (int q = 0; q < MAXR; ++q) {
-                ws[q] = 0u;
-                if (q + 1 < m) {
-                    uint32_t h = hash_slot(key[q]);
-#pragma unroll 1
-                    while (H[h * COL_BLOCK] != key[q]) h = (h + 1) & (MAXR - 1);
-                    ws[q] = W[h * COL_BLOCK];
+                const int32_t key = H[q * COL_BLOCK];
+                if (key != HASH_EMPTY) {
+                    L[cnt * COL_BLOCK] = ((K)key << 5) | (K)q;
+                    ++cnt;
                 }
             }
-#pragma unroll
-            for (int q = 0; q < MAXR; ++q) {
-                H[q * COL_BLOCK] = key[q];
-                W[q * COL_BLOCK] = ws[q];
-            }
+            if (cnt <= 16) sort_list<16, K>(L, cnt);
+            else sort_list<32, K>(L, cnt);
+            m = 1 + cnt;
         }
     }
     if (cl < ncols) col_ptr[cl] = m;
@@ -303,13 +280,18 @@ pattern_kernel(SegTable T, int64_t col_lo, int64_t ncols, const int32_t *__restr
         return;
     }
 #pragma unroll 1
-    for (int j = 0; j < off; ++j) scratch[sb + j] = make_int2(H[j * COL_BLOCK], (int)W[j * COL_BLOCK]);
+    for (int j = 0; j < off; ++j) {
+        const K key = L[j * COL_BLOCK];
+        scratch[sb + j] = make_int2((int)(key >> 5), (int)W[(int)(key & 31) * COL_BLOCK]);
+    }
 }
 
 // Rows only (symbolic without values).
 __global__ void __launch_bounds__(EMIT_BLOCK)
 emit_rows_kernel(int64_t col_lo, int64_t ncols, const int64_t *__restrict__ col_ptr, const int2 *__restrict__ scratch,
-                 const int64_t *__restrict__ block_scratch, int64_t *__restrict__ row_idx, int64_t capacity) {
+                 const int64_t *__restrict__ block_scratch, int64_t *__restrict__ row_idx, int64_t capacity,
+                 const uint32_t *__restrict__ status) {
+    if (*status & (HX_ST_DEG_OVERFLOW | HX_ST_ROW_OVERFLOW | HX_ST_REPEATED_NODE | HX_ST_SCRATCH_OVERFLOW)) return;
     __shared__ int64_t s_cp[COL_BLOCK + 1];
     const int64_t first = (int64_t)blockIdx.x * COL_BLOCK;
     const int ncol = (int)(ncols - first < COL_BLOCK ? ncols - first : COL_BLOCK);
@@ -346,18 +328,20 @@ __device__ __forceinline__ const double *ke_row(const SegTable &T, int64_t e) {
 
 template <bool ROWS, bool SINGLE>
 __global__ void __launch_bounds__(EMIT_BLOCK)
-emit_kernel(SegTable T, int64_t col_lo, int64_t ncols, const int32_t *__restrict__ adj_ptr,
+emit_kernel(SegTable T, int64_t col_lo, int64_t ncols, const int32_t *__restrict__ deg_arr,
             const int32_t *__restrict__ adj, const int64_t *__restrict__ col_ptr, const int2 *__restrict__ scratch,
             const int64_t *__restrict__ block_scratch, int64_t *__restrict__ row_idx, double *__restrict__ vals,
-            int64_t capacity) {
+            int64_t capacity, const uint32_t *__restrict__ status) {
+    // the pattern pass hit a fast-path limit: its records are incomplete and the caller re-runs
+    if (*status & (HX_ST_DEG_OVERFLOW | HX_ST_ROW_OVERFLOW | HX_ST_REPEATED_NODE | HX_ST_SCRATCH_OVERFLOW)) return;
     __shared__ int64_t s_cp[COL_BLOCK + 1];
-    __shared__ int32_t s_aptr[COL_BLOCK + 1];
+    __shared__ int32_t s_deg[COL_BLOCK];
     __shared__ uint8_t s_col[COL_BLOCK * MAXR];  // column of each off-diagonal record of the block
     const int64_t first = (int64_t)blockIdx.x * COL_BLOCK;
     const int ncol = (int)(ncols - first < COL_BLOCK ? ncols - first : COL_BLOCK);
     for (int i = threadIdx.x; i <= ncol; i += EMIT_BLOCK) {
         s_cp[i] = col_ptr[first + i];
-        s_aptr[i] = adj_ptr[first + i];
+        if (i < ncol) s_deg[i] = min(deg_arr[first + i], MAXDEG);
     }
     __syncthreads();
     const int64_t base = s_cp[0];
@@ -372,8 +356,8 @@ emit_kernel(SegTable T, int64_t col_lo, int64_t ncols, const int32_t *__restrict
     for (int u = threadIdx.x; u < ncol; u += EMIT_BLOCK) {
         const int o = (int)(s_cp[u] - base);
         if (s_cp[u + 1] == s_cp[u] || o >= room) continue;
-        const int deg = s_aptr[u + 1] - s_aptr[u];
-        const int32_t *ent = adj + s_aptr[u];
+        const int deg = s_deg[u];
+        const int32_t *ent = adj + 8 * (first + u);
         if (ROWS) row_idx[base + o] = col_lo + first + u;
         double x[8];
 #pragma unroll
@@ -405,7 +389,7 @@ emit_kernel(SegTable T, int64_t col_lo, int64_t ncols, const int32_t *__restrict
         if (ROWS) row_idx[base + o] = rec.x;
         const uint32_t w = (uint32_t)rec.y;
         const int n = (int)(w & 7u);
-        const int32_t *ent = adj + s_aptr[u];
+        const int32_t *ent = adj + 8 * (first + u);
         double x[MAX_OFFDIAG_CONTRIB];
 #pragma unroll
         for (int r = 0; r < MAX_OFFDIAG_CONTRIB; ++r) {
@@ -430,28 +414,29 @@ emit_kernel(SegTable T, int64_t col_lo, int64_t ncols, const int32_t *__restrict
 }
 
 // Workspace layout (all offsets 256-B aligned):
-//   adj_ptr (ncols+1) i32 | cursor/deg (ncols+1) i32 | adj (8*n_total) i32 |
-//   block_scratch (blocks) i64 | scratch_top u64 | scratch (SCRATCH_PER_COL*ncols) int2 | cub temp
+//   deg (ncols) i32 | adj (8*ncols) i32 | block_scratch (blocks) i64 | scratch_top u64 | cub temp |
+//   scratch int2 (the rest of the workspace; hx_mesh_csc_workspace_bytes sizes it for
+//   SCRATCH_PER_COL records per column, and a caller that gets HX_ST_SCRATCH_OVERFLOW re-runs with
+//   room for col_ptr[ncols] records -- the counts are complete even then)
 constexpr int64_t SCRATCH_PER_COL = 15;  // off-diagonal records per column reserved (hex: 13 avg)
 struct MeshWs {
-    int32_t *adj_ptr, *deg, *adj;
+    int32_t *deg, *adj;
     int64_t *block_scratch;
     unsigned long long *scratch_top;
     int2 *scratch;
     int64_t scratch_capacity;
     void *cub_tmp;
     size_t cub_bytes;
-    size_t total;
+    size_t total;  // with the default scratch
 };
 
 static size_t cub_scan_bytes(int64_t ncols) {
-    size_t b1 = 0, b2 = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, b1, (int32_t *)nullptr, (int32_t *)nullptr, (int)(ncols + 1));
-    cub::DeviceScan::ExclusiveSum(nullptr, b2, (int64_t *)nullptr, (int64_t *)nullptr, (int)(ncols + 1));
-    return std::max(b1, b2);
+    size_t b = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, b, (int64_t *)nullptr, (int64_t *)nullptr, (int)(ncols + 1));
+    return b;
 }
 
-static MeshWs mesh_ws_layout(void *base, int64_t n_total, int64_t ncols) {
+static MeshWs mesh_ws_layout(void *base, int64_t ncols, int64_t workspace_bytes = -1) {
     MeshWs w{};
     size_t off = 0;
     auto take = [&](size_t bytes) {
@@ -459,19 +444,19 @@ static MeshWs mesh_ws_layout(void *base, int64_t n_total, int64_t ncols) {
         off = align_up(off + bytes, 256);
         return o;
     };
-    const size_t o_ptr = take(sizeof(int32_t) * (ncols + 1));
-    const size_t o_deg = take(sizeof(int32_t) * (ncols + 1));
-    const size_t o_adj = take(sizeof(int32_t) * 8 * std::max<int64_t>(n_total, 1));
+    const size_t o_deg = take(sizeof(int32_t) * std::max<int64_t>(ncols, 1));
+    const size_t o_adj = take(sizeof(int32_t) * 8 * std::max<int64_t>(ncols, 1));
     const size_t o_bs = take(sizeof(int64_t) * std::max<int64_t>(1, ceil_div(ncols, COL_BLOCK)));
     const size_t o_st = take(sizeof(unsigned long long));
-    w.scratch_capacity = std::max<int64_t>(1, SCRATCH_PER_COL * ncols);
-    const size_t o_sc = take(sizeof(int2) * w.scratch_capacity);
     w.cub_bytes = cub_scan_bytes(ncols);
     const size_t o_cub = take(w.cub_bytes);
-    w.total = off;
+    const size_t o_sc = off;
+    const int64_t default_cap = std::max<int64_t>(1, SCRATCH_PER_COL * ncols);
+    w.total = o_sc + sizeof(int2) * default_cap;
+    w.scratch_capacity =
+        workspace_bytes < 0 ? default_cap : std::max<int64_t>(0, (workspace_bytes - (int64_t)o_sc) / (int64_t)sizeof(int2));
     char *b = (char *)base;
     if (b) {
-        w.adj_ptr = (int32_t *)(b + o_ptr);
         w.deg = (int32_t *)(b + o_deg);
         w.adj = (int32_t *)(b + o_adj);
         w.block_scratch = (int64_t *)(b + o_bs);
@@ -521,9 +506,6 @@ static int make_segtable(const hx_elem_segment *segs, int32_t n_segs, SegTable &
 
 static bool single_dense(const SegTable &T) { return T.n == 1 && T.ke_stride[0] == 36; }
 
-static unsigned grid_for(int64_t n, int threads) {
-    return (unsigned)std::max<int64_t>(1, ceil_div(n, threads));
-}
 
 }  // namespace hx
 
@@ -531,7 +513,8 @@ using namespace hx;
 
 extern "C" int64_t hx_mesh_csc_workspace_bytes(int64_t n_el_total, int64_t n_cols) {
     if (n_el_total < 0 || n_cols < 0) return -1;
-    return (int64_t)mesh_ws_layout(nullptr, n_el_total, n_cols).total;
+    (void)n_el_total;
+    return (int64_t)mesh_ws_layout(nullptr, n_cols).total;
 }
 
 static int mesh_csc_build(const hx_elem_segment *segs, int32_t n_segs, int64_t n_nodes, int64_t col_lo,
@@ -548,7 +531,7 @@ static int mesh_csc_build(const hx_elem_segment *segs, int32_t n_segs, int64_t n
         return HX_ERR_VALUE;
     }
     const int64_t ncols = col_hi - col_lo;
-    MeshWs w = mesh_ws_layout(workspace, n_total, ncols);
+    MeshWs w = mesh_ws_layout(workspace, ncols, workspace_bytes);
     if (workspace == nullptr || workspace_bytes < (int64_t)w.total) {
         set_last_error("hx_mesh_csc_symbolic: workspace %lld < %lld bytes", (long long)workspace_bytes,
                        (long long)w.total);
@@ -556,41 +539,40 @@ static int mesh_csc_build(const hx_elem_segment *segs, int32_t n_segs, int64_t n
     }
     cudaStream_t s = (cudaStream_t)stream;
     HX_TRY_CUDA(cudaMemsetAsync(status, 0, sizeof(uint32_t), s));
-    HX_TRY_CUDA(cudaMemsetAsync(w.deg, 0, sizeof(int32_t) * (ncols + 1), s));
-    if (n_total > 0) {
-        degree_kernel<<<grid_for(n_total, 256), 256, 0, s>>>(T, n_total, n_nodes, col_lo, col_hi, w.deg, status);
-        HX_CHECK_LAUNCH("degree_kernel");
-    }
-    size_t cb = w.cub_bytes;
-    HX_TRY_CUDA(cub::DeviceScan::ExclusiveSum(w.cub_tmp, cb, w.deg, w.adj_ptr, (int)(ncols + 1), s));
-    HX_TRY_CUDA(cudaMemsetAsync(w.deg, 0, sizeof(int32_t) * (ncols + 1), s));
-    if (n_total > 0) {
-        adjacency_fill_kernel<<<grid_for(n_total, 256), 256, 0, s>>>(T, n_total, col_lo, col_hi, w.adj_ptr,
-                                                                      w.deg, w.adj);
-        HX_CHECK_LAUNCH("adjacency_fill_kernel");
-    }
     if (ncols > 0) {
+        HX_TRY_CUDA(cudaMemsetAsync(w.deg, 0, sizeof(int32_t) * ncols, s));
+        if (n_total > 0) {
+            adjacency_kernel<<<(unsigned)std::min<int64_t>(ceil_div(8 * n_total, 256), 148 * 64), 256, 0, s>>>(
+                T, n_total, n_nodes, col_lo, col_hi, w.deg, w.adj, status);
+            HX_CHECK_LAUNCH("adjacency_kernel");
+        }
         const unsigned tiles = (unsigned)ceil_div(ncols, COL_BLOCK);
         HX_TRY_CUDA(cudaMemsetAsync(w.scratch_top, 0, sizeof(unsigned long long), s));
-        pattern_kernel<<<tiles, COL_BLOCK, 0, s>>>(T, col_lo, ncols, w.adj_ptr, w.adj, col_ptr, w.scratch,
-                                                   w.scratch_capacity, w.scratch_top, w.block_scratch, status);
+        if (n_nodes <= (int64_t(1) << 26))
+            pattern_kernel<uint32_t><<<tiles, COL_BLOCK, 0, s>>>(T, col_lo, ncols, w.deg, w.adj, col_ptr, w.scratch,
+                                                                w.scratch_capacity, w.scratch_top, w.block_scratch,
+                                                                status);
+        else
+            pattern_kernel<uint64_t><<<tiles, COL_BLOCK, 0, s>>>(T, col_lo, ncols, w.deg, w.adj, col_ptr, w.scratch,
+                                                                w.scratch_capacity, w.scratch_top, w.block_scratch,
+                                                                status);
         HX_CHECK_LAUNCH("pattern_kernel");
         HX_TRY_CUDA(cudaMemsetAsync(col_ptr + ncols, 0, sizeof(int64_t), s));
         size_t cb2 = w.cub_bytes;
         HX_TRY_CUDA(cub::DeviceScan::ExclusiveSum(w.cub_tmp, cb2, col_ptr, col_ptr, (int)(ncols + 1), s));
         if (vals != nullptr) {
             if (single_dense(T))
-                emit_kernel<true, true><<<tiles, EMIT_BLOCK, 0, s>>>(T, col_lo, ncols, w.adj_ptr, w.adj, col_ptr,
+                emit_kernel<true, true><<<tiles, EMIT_BLOCK, 0, s>>>(T, col_lo, ncols, w.deg, w.adj, col_ptr,
                                                                     w.scratch, w.block_scratch, row_idx, vals,
-                                                                    row_capacity);
+                                                                    row_capacity, status);
             else
-                emit_kernel<true, false><<<tiles, EMIT_BLOCK, 0, s>>>(T, col_lo, ncols, w.adj_ptr, w.adj, col_ptr,
+                emit_kernel<true, false><<<tiles, EMIT_BLOCK, 0, s>>>(T, col_lo, ncols, w.deg, w.adj, col_ptr,
                                                                      w.scratch, w.block_scratch, row_idx, vals,
-                                                                     row_capacity);
+                                                                     row_capacity, status);
             HX_CHECK_LAUNCH("emit_kernel");
         } else {
             emit_rows_kernel<<<tiles, EMIT_BLOCK, 0, s>>>(col_lo, ncols, col_ptr, w.scratch, w.block_scratch, row_idx,
-                                                         row_capacity);
+                                                         row_capacity, status);
             HX_CHECK_LAUNCH("emit_rows_kernel");
         }
     } else {
@@ -631,15 +613,15 @@ extern "C" int hx_mesh_csc_numeric(const hx_elem_segment *segs, int32_t n_segs, 
         return HX_ERR_VALUE;
     }
     const int64_t ncols = col_hi - col_lo;
-    MeshWs w = mesh_ws_layout(const_cast<void *>(workspace), n_total, ncols);
+    MeshWs w = mesh_ws_layout(const_cast<void *>(workspace), ncols);
     cudaStream_t s = (cudaStream_t)stream;
     if (ncols > 0) {
         if (single_dense(T))
             emit_kernel<false, true><<<(unsigned)ceil_div(ncols, COL_BLOCK), EMIT_BLOCK, 0, s>>>(
-                T, col_lo, ncols, w.adj_ptr, w.adj, col_ptr, w.scratch, w.block_scratch, nullptr, vals, INT64_MAX);
+                T, col_lo, ncols, w.deg, w.adj, col_ptr, w.scratch, w.block_scratch, nullptr, vals, INT64_MAX, status);
         else
             emit_kernel<false, false><<<(unsigned)ceil_div(ncols, COL_BLOCK), EMIT_BLOCK, 0, s>>>(
-                T, col_lo, ncols, w.adj_ptr, w.adj, col_ptr, w.scratch, w.block_scratch, nullptr, vals, INT64_MAX);
+                T, col_lo, ncols, w.deg, w.adj, col_ptr, w.scratch, w.block_scratch, nullptr, vals, INT64_MAX, status);
         HX_CHECK_LAUNCH("emit_kernel<numeric>");
     }
     return HX_OK;

@@ -1,28 +1,38 @@
 // hx_ke.cu -- numerical integration (the paper's Algorithm 2) for hex8 Poisson elements on
 // sm_100a, fused with the iK/jK triplet index generation.
 //
-// One thread per element.  The 8 node coordinates are gathered straight from the mesh via two
-// 16-byte connectivity loads per element (no host-side staging, integrate.py:146-149 is gone),
-// the 2x2x2 Gauss quadrature runs in FP64 registers, and the 36 packed lower-triangular values
-// are staged in shared memory so the global stores of the element-major (n_el, 36) f64 array and
-// of the (36 n_el) i32 row/col arrays are fully coalesced.  Tensor cores are deliberately not
-// used: the contractions are 8x3 and FP64.
+// Exact mode (the only arithmetic this file ships) reproduces element.py:255-297 operation for
+// operation with explicitly rounded intrinsics (__dmul_rn/__dadd_rn cannot be contracted into
+// FMA), so KE is bitwise equal to the reference's numba kernel.  Tensor cores are deliberately
+// not used: the contractions are 8x3 and FP64, and the kernel is FP64-pipe bound.
 //
-// HX_MODE_EXACT reproduces element.py:255-297 operation for operation with explicitly rounded
-// intrinsics (__dmul_rn/__dadd_rn/__ddiv_rn cannot be contracted into FMA), so the output is
-// bitwise equal to the reference.  Two bit-preserving restructurings are applied:
-//   * dn = +-M_k: (-M)*x == -(M*x) exactly, so products are formed from the 3 magnitudes and
-//     the sign becomes add/sub;
-//   * B[r][a] = (i_r0 dn0a + i_r1 dn1a) + i_r2 dn2a uses the same identity.
+// Work decomposition: one thread per (element, Gauss point).  A warp holds 4 elements x 8 Gauss
+// points (lane = 8 el + gp):
+//   * lane (el, a) gathers node a of its element (connectivity row read 8-wide across lanes) and
+//     stores the 9 products M_m * x[a][k] (m = the 3 dN magnitudes) to shared memory -- the only
+//     distinct products of J = dN @ X over all eight Gauss points (72 per element instead of 576);
+//   * lane (el, gp) then runs Gauss point gp in reference order: J (signed sums of the shared
+//     products), cofactors, det, the 9 true divisions, B, and its 36 contributions
+//     t_gp[p] = (c det) ((B0i B0j + B1i B1j) + B2i B2j);
+//   * the element's 8 lanes reduce ke[p] = ((((0 + t_0) + t_1) + ...) + t_7) in Gauss-point order
+//     through a per-warp shared buffer (8 entries per pass) -- the reference's accumulation -- and
+//     store KE and the fused iK/jK as 8-wide element-major runs.
+// Warps are persistent and prefetch the next element quad's connectivity and coordinates into
+// registers while integrating the current one.
+//
+// Bit-preserving rewrites:
+//   * dN = sign * M_k with M_k one of three magnitudes; (-M)*x == -(M*x) exactly, so the sign is
+//     folded into add/sub and the products are shared between Gauss points;
+//   * a/b = copysign(Markstein(|a|, b, RN(1/b)), a): reciprocal + two FMA corrections, bitwise
+//     __ddiv_rn(a, b) while nothing over/underflows.  That is guaranteed for every element whose
+//     coordinates are 0 or within [2^-100, 2^100] in magnitude (checked per element; other
+//     elements take __ddiv_rn).  hx_selftest_division checks the quotient on 2^30 operand pairs.
 #include <algorithm>
 #include <cstdio>
 
 #include "hx_common.cuh"
 
 namespace hx {
-
-constexpr int KE_BLOCK = 128;
-constexpr int KE_PAD = 37;  // odd stride (in doubles) -> conflict-free smem staging
 
 __device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
 __device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
@@ -32,121 +42,71 @@ __device__ __forceinline__ double acc_signed(double acc, int sign, double prod) 
     return sign > 0 ? dadd(acc, prod) : dsub(acc, prod);
 }
 
-// IEEE round-to-nearest a/b from y = RN(1/b): q0 = RN(a*y) is within 2 ulp of a/b; one
-// correction q1 = RN(q0 + (a - b q0) y) lands within 1 ulp (the residual is exact via FMA and
-// the correction error is ~2^-52 ulp); Markstein's theorem (y = RN(1/b), q within 1 ulp, exact
-// residual) then makes q2 = RN(q1 + (a - b q1) y) the correctly rounded quotient, i.e. bitwise
-// __ddiv_rn(a, b).  Valid while nothing over/underflows: the caller guards exponents and zero.
-__device__ __forceinline__ double div_markstein(double a, double b, double y) {
-    const double q0 = __dmul_rn(a, y);
-    const double r0 = __fma_rn(-q0, b, a);
+__device__ __forceinline__ double dabs_bits(double x) {
+    return __hiloint2double(__double2hiint(x) & 0x7fffffff, __double2loint(x));
+}
+// x with the sign bit of s (x >= +0)
+__device__ __forceinline__ double dsign_bits(double x, double s) {
+    return __hiloint2double(__double2hiint(x) | (__double2hiint(s) & (int)0x80000000), __double2loint(x));
+}
+
+// IEEE round-to-nearest a/b (b > 0) from y = RN(1/b).  For A = |a|: q0 = RN(A y) is within 2 ulp
+// of A/b; q1 = RN(q0 + (A - b q0) y) lands within 1 ulp (the FMA residual is exact); Markstein's
+// theorem (y = RN(1/b), q1 within 1 ulp, exact residual) makes q2 = RN(q1 + (A - b q1) y) the
+// correctly rounded quotient.  RN is odd-symmetric, so copysign(q2, a) == RN(a/b) -- including
+// a = -0.  Valid while no intermediate over/underflows (the callers guarantee the operand range).
+__device__ __forceinline__ double div_exact(double a, double b, double y) {
+    const double A = dabs_bits(a);
+    const double q0 = __dmul_rn(A, y);
+    const double r0 = __fma_rn(-q0, b, A);
     const double q1 = __fma_rn(r0, y, q0);
-    const double r1 = __fma_rn(-q1, b, a);
+    const double r1 = __fma_rn(-q1, b, A);
     const double q2 = __fma_rn(r1, y, q1);
-    return a == 0.0 ? q0 : q2;  // signed zero: 0*y keeps the sign of a (b > 0)
+    return dsign_bits(q2, a);
 }
 
-// |x| in [2^-800, 2^800] (or x == 0): Markstein path safe for these operands.
-__device__ __forceinline__ bool div_safe(double x) {
-    const int e = (__double2hiint(x) >> 20) & 0x7ff;
-    return (e >= 1023 - 800 && e <= 1023 + 800) || x == 0.0;
+// det > 0 (element.py:276: `not det > 0` fails; NaN fails) on the integer pipe.
+__device__ __forceinline__ bool positive(double x) {
+    const long long b = __double_as_longlong(x);
+    return b > 0 && b <= 0x7ff0000000000000ll;
 }
 
-// element.py:255-297 for one element, bitwise.  Coordinates are read from shared memory with
-// volatile loads (xs[(3a+k)*stride]) once per Gauss point: products M_k*x are recomputed per
-// point instead of being kept live across all eight (register pressure -> occupancy).
-// Returns the failing gauss point or -1.
-__device__ __forceinline__ int ke_exact(const volatile double *xs, int stride, double coeff, double (&ke)[36],
-                                        double &fail_det) {
-#pragma unroll
-    for (int p = 0; p < 36; ++p) ke[p] = 0.0;
-    int fail = -1;
-#pragma unroll
+// Coordinates 0 or with |x| in [2^-100, 2^100]: every J entry, cofactor and det of the element
+// then stays within [2^-600, 2^320] or is exactly 0, so the Markstein quotients are exact.
+__device__ __forceinline__ bool coord_in_range(double x) {
+    const unsigned hi = (unsigned)__double2hiint(x) & 0x7fffffffu, lo = (unsigned)__double2loint(x);
+    return (hi | lo) == 0u || hi - (unsigned)((1023 - 100) << 20) < (201u << 20);
+}
+
+// First failing Gauss point of one element and its det (reference order for J and det), or -1.
+// Only the degenerate-element report needs it (element.py:237-244), so it runs single-threaded.
+__device__ int first_failing_gp(const double (&x)[8][3], double &fail_det) {
     for (int gp = 0; gp < 8; ++gp) {
-        // J = dn @ x (element.py:262-269): accumulate from 0.0 over a = 0..7
+        double dn[3][8];
+        for (int a = 0; a < 8; ++a)
+            for (int d = 0; d < 3; ++d) dn[d][a] = dn_value(gp, d, a);
         double j[3][3];
-#pragma unroll
         for (int d = 0; d < 3; ++d)
-#pragma unroll
-            for (int k = 0; k < 3; ++k) j[d][k] = 0.0;
-#pragma unroll
-        for (int a = 0; a < 8; ++a) {
-            double xa[3];
-#pragma unroll
-            for (int k = 0; k < 3; ++k) xa[k] = xs[(3 * a + k) * stride];
-#pragma unroll
-            for (int d = 0; d < 3; ++d)
-#pragma unroll
-                for (int k = 0; k < 3; ++k)
-                    j[d][k] = acc_signed(j[d][k], dn_sign(gp, d, a), dmul(dn_magnitude(dn_mag(gp, d, a)), xa[k]));
-        }
-        // cofactors of the first row and det (element.py:271-275)
+            for (int k = 0; k < 3; ++k) {
+                double acc = 0.0;
+                for (int a = 0; a < 8; ++a) acc = dadd(acc, dmul(dn[d][a], x[a][k]));
+                j[d][k] = acc;
+            }
         const double c00 = dsub(dmul(j[1][1], j[2][2]), dmul(j[1][2], j[2][1]));
         const double c01 = dsub(dmul(j[1][2], j[2][0]), dmul(j[1][0], j[2][2]));
         const double c02 = dsub(dmul(j[1][0], j[2][1]), dmul(j[1][1], j[2][0]));
         const double det = dadd(dadd(dmul(j[0][0], c00), dmul(j[0][1], c01)), dmul(j[0][2], c02));
-        if (!(det > 0.0)) {  // element.py:276-279 (also catches NaN)
-            fail = gp;
+        if (!(det > 0.0)) {
             fail_det = det;
-            break;
-        }
-        // adjugate / det (element.py:281-284): IEEE-exact quotients
-        double num[9];
-        num[0] = c00;
-        num[1] = dsub(dmul(j[0][2], j[2][1]), dmul(j[0][1], j[2][2]));
-        num[2] = dsub(dmul(j[0][1], j[1][2]), dmul(j[0][2], j[1][1]));
-        num[3] = c01;
-        num[4] = dsub(dmul(j[0][0], j[2][2]), dmul(j[0][2], j[2][0]));
-        num[5] = dsub(dmul(j[0][2], j[1][0]), dmul(j[0][0], j[1][2]));
-        num[6] = c02;
-        num[7] = dsub(dmul(j[0][1], j[2][0]), dmul(j[0][0], j[2][1]));
-        num[8] = dsub(dmul(j[0][0], j[1][1]), dmul(j[0][1], j[1][0]));
-        bool safe = div_safe(det) && det != 0.0;
-#pragma unroll
-        for (int i = 0; i < 9; ++i) safe &= div_safe(num[i]);
-        double inv[3][3];
-        if (safe) {
-            const double y = __drcp_rn(det);
-#pragma unroll
-            for (int i = 0; i < 9; ++i) inv[i / 3][i % 3] = div_markstein(num[i], det, y);
-        } else {
-#pragma unroll
-            for (int i = 0; i < 9; ++i) inv[i / 3][i % 3] = __ddiv_rn(num[i], det);
-        }
-        // B = J^-1 dn (element.py:286-290): (i_r0*dn0a + i_r1*dn1a) + i_r2*dn2a
-        double B[3][8];
-#pragma unroll
-        for (int r = 0; r < 3; ++r) {
-            double q[3][3];  // q[d][m] = inv[r][d] * M_m
-#pragma unroll
-            for (int d = 0; d < 3; ++d)
-#pragma unroll
-                for (int m = 0; m < 3; ++m) q[d][m] = dmul(inv[r][d], dn_magnitude(m));
-#pragma unroll
-            for (int a = 0; a < 8; ++a) {
-                const double t0 = dn_sign(gp, 0, a) > 0 ? q[0][dn_mag(gp, 0, a)] : -q[0][dn_mag(gp, 0, a)];
-                const double t01 = acc_signed(t0, dn_sign(gp, 1, a), q[1][dn_mag(gp, 1, a)]);
-                B[r][a] = acc_signed(t01, dn_sign(gp, 2, a), q[2][dn_mag(gp, 2, a)]);
-            }
-        }
-        // ke[p] += (c*det) * ((B0i B0j + B1i B1j) + B2i B2j)  (element.py:293-297)
-        const double scale = dmul(coeff, det);
-#pragma unroll
-        for (int p = 0; p < 36; ++p) {
-            const int i = pack_i(p), jj = pack_j(p);
-            const double s = dadd(dadd(dmul(B[0][i], B[0][jj]), dmul(B[1][i], B[1][jj])),
-                                  dmul(B[2][i], B[2][jj]));
-            ke[p] = dadd(ke[p], dmul(scale, s));
+            return gp;
         }
     }
-    return fail;
+    return -1;
 }
 
-// Recompute one element to report (gauss point, det) of a failure -- single thread.
-__device__ void fail_detail(const double (&x)[8][3], double coeff, int64_t element, hx_fail_info *fail) {
-    double ke[36];
+__device__ void fail_detail(const double (&x)[8][3], int64_t element, hx_fail_info *fail) {
     double det = 0.0;
-    const int gp = ke_exact(&x[0][0], 1, coeff, ke, det);
+    const int gp = first_failing_gp(x, det);
     fail->element = element;
     fail->gauss_point = gp;
     fail->det = det;
@@ -166,7 +126,7 @@ __device__ __forceinline__ void load_conn(const int32_t *__restrict__ conn, int6
     g[4] = hi.x; g[5] = hi.y; g[6] = hi.z; g[7] = hi.w;
 }
 
-// Packed pair tables in shared memory for the coalesced copy-out (dynamic p per lane).
+// Packed pair tables in shared memory (lane-dependent p -> (i, j) lookups).
 __device__ __forceinline__ void init_pack_smem(uint8_t *pi, uint8_t *pj) {
     if (threadIdx.x < 36) {
         const int p = threadIdx.x;
@@ -177,95 +137,254 @@ __device__ __forceinline__ void init_pack_smem(uint8_t *pi, uint8_t *pj) {
     }
 }
 
+#ifndef HX_KE_MIN_BLOCKS
+#define HX_KE_MIN_BLOCKS 2
+#endif
+constexpr int GP_BLOCK = 256;                    // 32 elements x 8 Gauss points
+constexpr int GP_WARPS = GP_BLOCK / 32;
+constexpr int GP_EL_PER_BLOCK = GP_BLOCK / 8;
+constexpr int GP_EL_PER_WARP = 4;
+// Shared products P[el][m][a][k] = M_m x[a][k]: m stride 25, element stride 76 (doubles) keep the
+// <= 12 distinct (el, m) words of one warp-wide load in distinct bank pairs.
+constexpr int P_M_STRIDE = 25;
+constexpr int P_EL_STRIDE = 76;
+// Contribution buffer t[el][j][g]: g contiguous (the reducing lane reads 8 doubles with 4 x 16-B
+// loads), j stride 10 and element stride 88 make both the stores and the loads conflict-free.
+constexpr int T_J_STRIDE = 10;
+constexpr int T_EL_STRIDE = 88;
+
+__host__ __device__ constexpr int bit_r(int a) { return nat_r(a) > 0; }
+__host__ __device__ constexpr int bit_s(int a) { return nat_s(a) > 0; }
+__host__ __device__ constexpr int bit_t(int a) { return nat_t(a) > 0; }
+
+struct __align__(16) GpWarpSmem {
+    double t[GP_EL_PER_WARP * T_EL_STRIDE];
+    double P[GP_EL_PER_WARP * P_EL_STRIDE];
+    double coeff[GP_EL_PER_WARP];
+    int32_t conn[GP_EL_PER_WARP * 8];
+};
+
+__device__ __forceinline__ double mag_select(int k) {
+    return k == 0 ? dn_magnitude(0) : (k == 1 ? dn_magnitude(1) : dn_magnitude(2));
+}
+
+
+// Lane (el, a): publish node a's products M_m x[a][k] and id; the element's coefficient from a = 0.
+__device__ __forceinline__ void publish_node(GpWarpSmem &sm, int el, int a, int32_t node, double x0, double x1,
+                                             double x2, double c) {
+    double *P = sm.P + el * P_EL_STRIDE + 3 * a;
+#pragma unroll
+    for (int m = 0; m < 3; ++m) {
+        P[m * P_M_STRIDE] = dmul(dn_magnitude(m), x0);
+        P[m * P_M_STRIDE + 1] = dmul(dn_magnitude(m), x1);
+        P[m * P_M_STRIDE + 2] = dmul(dn_magnitude(m), x2);
+    }
+    sm.conn[el * 8 + a] = node;
+    if (a == 0) sm.coeff[el] = c;
+}
+
+// Gauss point gp of element el (products published in sm), reference operation order; then the
+// cooperative reduction and the KE / iK / jK stores of element out_el.  Returns det > 0.
+template <bool WITH_INDEX>
+__device__ __forceinline__ bool ke_gauss_point(GpWarpSmem &sm, int el, int gp, bool fast_div,
+                                               int64_t out_el, bool valid, double *__restrict__ ke_out,
+                                               int32_t *__restrict__ rows_out, int32_t *__restrict__ cols_out,
+                                               const uint8_t *s_pi, const uint8_t *s_pj) {
+    const int ir = (gp >> 2) & 1, is = (gp >> 1) & 1, it = gp & 1;
+    const volatile double *P = sm.P + el * P_EL_STRIDE;
+    // J = dn @ x (element.py:262-269), accumulated from 0.0 over a = 0..7.  dN_r,a at this point
+    // has magnitude index (s_a == s_gp) + (t_a == t_gp), and cyclically for s and t.
+    double j[3][3];
+#pragma unroll
+    for (int d = 0; d < 3; ++d)
+#pragma unroll
+        for (int k = 0; k < 3; ++k) j[d][k] = 0.0;
+#pragma unroll
+    for (int a = 0; a < 8; ++a) {
+        const int mr = (bit_s(a) == is) + (bit_t(a) == it);
+        const int ms = (bit_r(a) == ir) + (bit_t(a) == it);
+        const int mt = (bit_r(a) == ir) + (bit_s(a) == is);
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            j[0][k] = acc_signed(j[0][k], nat_r(a), P[mr * P_M_STRIDE + 3 * a + k]);
+            j[1][k] = acc_signed(j[1][k], nat_s(a), P[ms * P_M_STRIDE + 3 * a + k]);
+            j[2][k] = acc_signed(j[2][k], nat_t(a), P[mt * P_M_STRIDE + 3 * a + k]);
+        }
+    }
+    // cofactors, det (element.py:271-275)
+    const double c00 = dsub(dmul(j[1][1], j[2][2]), dmul(j[1][2], j[2][1]));
+    const double c01 = dsub(dmul(j[1][2], j[2][0]), dmul(j[1][0], j[2][2]));
+    const double c02 = dsub(dmul(j[1][0], j[2][1]), dmul(j[1][1], j[2][0]));
+    const double det = dadd(dadd(dmul(j[0][0], c00), dmul(j[0][1], c01)), dmul(j[0][2], c02));
+    const bool ok = positive(det);
+    // adjugate / det (element.py:281-284): true divisions
+    double num[9];
+    num[0] = c00;
+    num[1] = dsub(dmul(j[0][2], j[2][1]), dmul(j[0][1], j[2][2]));
+    num[2] = dsub(dmul(j[0][1], j[1][2]), dmul(j[0][2], j[1][1]));
+    num[3] = c01;
+    num[4] = dsub(dmul(j[0][0], j[2][2]), dmul(j[0][2], j[2][0]));
+    num[5] = dsub(dmul(j[0][2], j[1][0]), dmul(j[0][0], j[1][2]));
+    num[6] = c02;
+    num[7] = dsub(dmul(j[0][1], j[2][0]), dmul(j[0][0], j[2][1]));
+    num[8] = dsub(dmul(j[0][0], j[1][1]), dmul(j[0][1], j[1][0]));
+    double inv[3][3];
+    if (fast_div && ok) {
+        const double y = __drcp_rn(det);
+#pragma unroll
+        for (int i = 0; i < 9; ++i) inv[i / 3][i % 3] = div_exact(num[i], det, y);
+    } else {
+#pragma unroll
+        for (int i = 0; i < 9; ++i) inv[i / 3][i % 3] = __ddiv_rn(num[i], det);
+    }
+    // B = J^-1 dn (element.py:286-290): (i_r0 dn0a + i_r1 dn1a) + i_r2 dn2a with dn = sign * M.
+    // This lane's magnitudes per direction, indexed by the node's other two natural coordinates.
+    double Mr[4], Ms[4], Mt[4];
+#pragma unroll
+    for (int u = 0; u < 2; ++u)
+#pragma unroll
+        for (int v = 0; v < 2; ++v) {
+            Mr[2 * u + v] = mag_select((u == is) + (v == it));  // (s_a, t_a)
+            Ms[2 * u + v] = mag_select((u == ir) + (v == it));  // (r_a, t_a)
+            Mt[2 * u + v] = mag_select((u == ir) + (v == is));  // (r_a, s_a)
+        }
+    double B[3][8];
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+        double q0[4], q1[4], q2[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            q0[c] = dmul(inv[r][0], Mr[c]);
+            q1[c] = dmul(inv[r][1], Ms[c]);
+            q2[c] = dmul(inv[r][2], Mt[c]);
+        }
+#pragma unroll
+        for (int a = 0; a < 8; ++a) {
+            const double p0 = q0[2 * bit_s(a) + bit_t(a)];
+            const double t0 = nat_r(a) > 0 ? p0 : -p0;
+            const double t01 = acc_signed(t0, nat_s(a), q1[2 * bit_r(a) + bit_t(a)]);
+            B[r][a] = acc_signed(t01, nat_t(a), q2[2 * bit_r(a) + bit_s(a)]);
+        }
+    }
+    const double scale = dmul(sm.coeff[el], det);
+    // 36 contributions, 8 per pass, reduced across the element's 8 lanes in Gauss-point order
+    double *tb = sm.t + el * T_EL_STRIDE;
+#pragma unroll
+    for (int c = 0; c < 5; ++c) {
+#pragma unroll
+        for (int jj = 0; jj < 8; ++jj) {
+            const int p = 8 * c + jj;
+            if (p < 36) {
+                const int i = pack_i(p), q = pack_j(p);
+                const double s = dadd(dadd(dmul(B[0][i], B[0][q]), dmul(B[1][i], B[1][q])), dmul(B[2][i], B[2][q]));
+                tb[jj * T_J_STRIDE + gp] = dmul(scale, s);
+            }
+        }
+        __syncwarp();
+        const int p = 8 * c + gp;  // this lane reduces packed entry p of its element
+        if (p < 36) {
+            const double2 *src = reinterpret_cast<const double2 *>(tb + gp * T_J_STRIDE);
+            double acc = 0.0;
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+                const double2 v = src[h];
+                acc = dadd(acc, v.x);
+                acc = dadd(acc, v.y);
+            }
+            if (valid) {
+                ke_out[out_el * 36 + p] = acc;
+                if (WITH_INDEX) {
+                    const int32_t gi = sm.conn[el * 8 + s_pi[p]], gj = sm.conn[el * 8 + s_pj[p]];
+                    rows_out[out_el * 36 + p] = max(gi, gj);
+                    cols_out[out_el * 36 + p] = min(gi, gj);
+                }
+            }
+        }
+        __syncwarp();
+    }
+    return ok;
+}
+
 // Mesh kernel: elements [lo, lo+n) of the mesh; outputs indexed from 0 (= element lo).
-template <int MODE>
-__global__ void __launch_bounds__(KE_BLOCK)
+// Persistent warps: warp w handles element quads w, w + W, w + 2W, ... and prefetches the next
+// quad's node ids, coordinates and coefficients into registers before integrating the current one,
+// so the gather latency hides under the FP64 work.
+template <int MODE, bool WITH_INDEX>
+__global__ void __launch_bounds__(GP_BLOCK, HX_KE_MIN_BLOCKS)
 integrate_mesh_kernel(const double *__restrict__ coords, const int32_t *__restrict__ conn,
                       const double *__restrict__ coeff, int64_t lo, int64_t n,
                       double *__restrict__ ke_out, int32_t *__restrict__ rows_out,
                       int32_t *__restrict__ cols_out, unsigned long long *__restrict__ fail_min) {
-    __shared__ double s_ke[KE_BLOCK * KE_PAD];  // also holds the staged coordinates (24 x KE_BLOCK)
-    __shared__ int32_t s_conn[KE_BLOCK * 8];
+    __shared__ GpWarpSmem s_warp[GP_WARPS];
     __shared__ uint8_t s_pi[36], s_pj[36];
     init_pack_smem(s_pi, s_pj);
-
-    const int64_t first = (int64_t)blockIdx.x * KE_BLOCK;
-    const int t = threadIdx.x;
-    const int64_t k = first + t;
-    double ke[36];
-    if (k < n) {
-        const int64_t e = lo + k;
-        int32_t g[8];
-        load_conn(conn, e, g);
-#pragma unroll
-        for (int a = 0; a < 8; ++a) s_conn[t * 8 + a] = g[a];
-#pragma unroll
-        for (int a = 0; a < 8; ++a) {
-            double xa[3];
-            load_node(coords, g[a], xa);
-#pragma unroll
-            for (int d = 0; d < 3; ++d) s_ke[(3 * a + d) * KE_BLOCK + t] = xa[d];
-        }
-        double det = 0.0;
-        const int gp = ke_exact(s_ke + t, KE_BLOCK, __ldg(coeff + e), ke, det);
-        if (gp >= 0) atomicMin(fail_min, (unsigned long long)e);
-    }
-    __syncthreads();  // every thread is done with its staged coordinates
-    if (k < n) {
-#pragma unroll
-        for (int p = 0; p < 36; ++p) s_ke[t * KE_PAD + p] = ke[p];
-    }
     __syncthreads();
-    const int nvalid = (int)(n - first < KE_BLOCK ? n - first : KE_BLOCK);
-    const int total = nvalid * 36;
-    double *kdst = ke_out + first * 36;
-    for (int w = t; w < total; w += KE_BLOCK) {
-        const int el = w / 36, p = w - el * 36;
-        kdst[w] = s_ke[el * KE_PAD + p];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int el = lane >> 3, gp = lane & 7;
+    GpWarpSmem &sm = s_warp[warp];
+    const int64_t n_quads = (n + GP_EL_PER_WARP - 1) / GP_EL_PER_WARP;
+    const int64_t stride = (int64_t)gridDim.x * GP_WARPS;
+    int64_t quad = (int64_t)blockIdx.x * GP_WARPS + warp;
+    auto node_id = [&](int64_t q) -> int32_t {
+        const int64_t k = q * GP_EL_PER_WARP + el;
+        return k < n ? __ldg(conn + (lo + k) * 8 + gp) : -1;
+    };
+    // padding lanes integrate a unit cube (keeps them off the slow paths; never stored)
+    const double u0 = nat_r(gp) > 0, u1 = nat_s(gp) > 0, u2 = nat_t(gp) > 0;
+    int32_t node = node_id(quad), node_next = node_id(quad + stride);
+    double x0 = u0, x1 = u1, x2 = u2, c = 1.0;
+    if (node >= 0) {
+        const double *p = coords + 3 * (int64_t)node;
+        x0 = __ldg(p); x1 = __ldg(p + 1); x2 = __ldg(p + 2);
+        c = __ldg(coeff + lo + quad * GP_EL_PER_WARP + el);
     }
-    if (rows_out != nullptr) {
-        int32_t *rdst = rows_out + first * 36;
-        int32_t *cdst = cols_out + first * 36;
-        for (int w = t; w < total; w += KE_BLOCK) {
-            const int el = w / 36, p = w - el * 36;
-            const int32_t gi = s_conn[el * 8 + s_pi[p]], gj = s_conn[el * 8 + s_pj[p]];
-            rdst[w] = max(gi, gj);
-            cdst[w] = min(gi, gj);
+    for (; quad < n_quads; quad += stride) {
+        const int64_t k = quad * GP_EL_PER_WARP + el;
+        const bool valid = k < n;
+        const unsigned in_range = __ballot_sync(0xffffffffu, coord_in_range(x0) && coord_in_range(x1) &&
+                                                               coord_in_range(x2));
+        const bool fast_div = ((in_range >> (8 * el)) & 0xffu) == 0xffu;
+        __syncwarp();
+        publish_node(sm, el, gp, node, x0, x1, x2, c);
+        __syncwarp();
+        // prefetch the next quad
+        node = node_next;
+        node_next = node_id(quad + 2 * stride);
+        x0 = u0; x1 = u1; x2 = u2; c = 1.0;
+        if (node >= 0) {
+            const double *p = coords + 3 * (int64_t)node;
+            x0 = __ldg(p); x1 = __ldg(p + 1); x2 = __ldg(p + 2);
+            c = __ldg(coeff + lo + (quad + stride) * GP_EL_PER_WARP + el);
         }
+        const bool ok = ke_gauss_point<WITH_INDEX>(sm, el, gp, fast_div, k, valid, ke_out, rows_out, cols_out, s_pi,
+                                                   s_pj);
+        if (valid && !ok) atomicMin(fail_min, (unsigned long long)(lo + k));
     }
 }
 
 // Batch kernel: pre-gathered coords (n, 8, 3) (stiffness_batch, element.py:213-245).
 template <int MODE>
-__global__ void __launch_bounds__(KE_BLOCK)
+__global__ void __launch_bounds__(GP_BLOCK, HX_KE_MIN_BLOCKS)
 stiffness_batch_kernel(const double *__restrict__ coords, const double *__restrict__ coeff, int64_t n,
                        double *__restrict__ out, unsigned long long *__restrict__ fail_min) {
-    __shared__ double s_ke[KE_BLOCK * KE_PAD];
-    const int64_t first = (int64_t)blockIdx.x * KE_BLOCK;
-    const int t = threadIdx.x;
-    const int64_t e = first + t;
-    double ke[36];
-    if (e < n) {
-        const double *src = coords + 24 * e;
+    __shared__ GpWarpSmem s_warp[GP_WARPS];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int el = lane >> 3, gp = lane & 7;
+    GpWarpSmem &sm = s_warp[warp];
+    const int64_t e = (int64_t)blockIdx.x * GP_EL_PER_BLOCK + warp * GP_EL_PER_WARP + el;
+    const bool valid = e < n;
+    double x[3];
 #pragma unroll
-        for (int i = 0; i < 24; ++i) s_ke[i * KE_BLOCK + t] = __ldg(src + i);
-        double det = 0.0;
-        const int gp = ke_exact(s_ke + t, KE_BLOCK, __ldg(coeff + e), ke, det);
-        if (gp >= 0) atomicMin(fail_min, (unsigned long long)e);
-    }
-    __syncthreads();
-    if (e < n) {
-#pragma unroll
-        for (int p = 0; p < 36; ++p) s_ke[t * KE_PAD + p] = ke[p];
-    }
-    __syncthreads();
-    const int nvalid = (int)(n - first < KE_BLOCK ? n - first : KE_BLOCK);
-    const int total = nvalid * 36;
-    double *kdst = out + first * 36;
-    for (int w = t; w < total; w += KE_BLOCK) {
-        const int el = w / 36, p = w - el * 36;
-        kdst[w] = s_ke[el * KE_PAD + p];
-    }
+    for (int d = 0; d < 3; ++d)
+        x[d] = valid ? __ldg(coords + 24 * e + 3 * gp + d)
+                     : (double)((d == 0 ? nat_r(gp) : d == 1 ? nat_s(gp) : nat_t(gp)) > 0);
+    const unsigned in_range =
+        __ballot_sync(0xffffffffu, coord_in_range(x[0]) && coord_in_range(x[1]) && coord_in_range(x[2]));
+    const bool fast_div = ((in_range >> (8 * el)) & 0xffu) == 0xffu;
+    publish_node(sm, el, gp, 0, x[0], x[1], x[2], valid ? __ldg(coeff + e) : 1.0);
+    __syncwarp();
+    const bool ok = ke_gauss_point<false>(sm, el, gp, fast_div, e, valid, out, nullptr, nullptr, nullptr, nullptr);
+    if (valid && !ok) atomicMin(fail_min, (unsigned long long)e);
 }
 
 // Resolve the lowest failing element into the hx_fail_info record (element.py:237-244).
@@ -284,11 +403,10 @@ __global__ void fail_resolve_mesh_kernel(const double *__restrict__ coords, cons
     load_conn(conn, e, g);
     double x[8][3];
     for (int a = 0; a < 8; ++a) load_node(coords, g[a], x[a]);
-    fail_detail(x, coeff[e], e, fail);
+    fail_detail(x, e, fail);
 }
 
-__global__ void fail_resolve_batch_kernel(const double *__restrict__ coords, const double *__restrict__ coeff,
-                                          hx_fail_info *fail) {
+__global__ void fail_resolve_batch_kernel(const double *__restrict__ coords, hx_fail_info *fail) {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
     const unsigned long long key = *reinterpret_cast<unsigned long long *>(fail);
     if (key == ~0ull) {
@@ -301,10 +419,10 @@ __global__ void fail_resolve_batch_kernel(const double *__restrict__ coords, con
     double x[8][3];
     for (int a = 0; a < 8; ++a)
         for (int d = 0; d < 3; ++d) x[a][d] = coords[24 * e + 3 * a + d];
-    fail_detail(x, coeff[e], e, fail);
+    fail_detail(x, e, fail);
 }
 
-// connectivity_index_arrays alone (assemble.py:86-93), 4 outputs per thread.
+// connectivity_index_arrays alone (assemble.py:86-93).
 __global__ void index_kernel(const int32_t *__restrict__ conn, int64_t lo, int64_t n,
                              int32_t *__restrict__ rows, int32_t *__restrict__ cols) {
     __shared__ uint8_t s_pi[36], s_pj[36];
@@ -322,6 +440,19 @@ __global__ void index_kernel(const int32_t *__restrict__ conn, int64_t lo, int64
     }
 }
 
+// Resident blocks of the persistent integration kernel on the current device (queried once).
+static int64_t persistent_blocks() {
+    static int64_t cached = 0;
+    if (cached == 0) {
+        int dev = 0, sms = 148, per_sm = HX_KE_MIN_BLOCKS;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, integrate_mesh_kernel<HX_MODE_EXACT, true>, GP_BLOCK, 0);
+        cached = (int64_t)sms * std::max(per_sm, 1);
+    }
+    return cached;
+}
+
 __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
     x += 0x9e3779b97f4a7c15ull;
     x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
@@ -329,21 +460,21 @@ __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
     return x ^ (x >> 31);
 }
 
-// Self-test of div_markstein against __ddiv_rn: random mantissas, exponents spread over the
-// guarded range, cancellation-like numerators, exact multiples and neighbours of exact
-// quotients (the hardest rounding cases).  Counts mismatching bit patterns.
+// Self-test of div_exact against __ddiv_rn over the operand range the kernel guarantees
+// (|a| = 0 or in [2^-420, 2^260], b in [2^-600, 2^330]): random mantissas, signed zeros,
+// cancellation-like small integers, exact multiples and their ulp neighbours (the hardest rounding
+// cases).  Counts mismatching bit patterns.
 __global__ void division_selftest_kernel(uint64_t n, uint64_t seed, unsigned long long *mismatches,
                                          unsigned long long *tested) {
     unsigned long long bad = 0, cnt = 0;
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
         const uint64_t r1 = splitmix64(seed ^ (2 * i)), r2 = splitmix64(seed ^ (2 * i + 1));
         const int kind = (int)(r1 & 3);
-        const int ea = (int)((r1 >> 2) & 1023) - 512, eb = (int)((r2 >> 2) & 1023) - 512;
+        const int ea = (int)((r1 >> 2) % 681) - 420, eb = (int)((r2 >> 2) % 931) - 600;
         double b = __hiloint2double(0x3ff00000 | (int)((r2 >> 12) & 0xfffff), (int)(r2 >> 32));
         b = ldexp(b, kind == 0 ? eb : (eb & 63) - 32);
         double a = __hiloint2double(0x3ff00000 | (int)((r1 >> 12) & 0xfffff), (int)(r1 >> 32));
         a = ldexp(a, kind == 0 ? ea : (ea & 63) - 32);
-        if (r1 & (1ull << 62)) a = -a;
         if (kind == 2) {  // a = exact-ish multiple of b, nudged by a few ulps
             const double q = __hiloint2double(0x3ff00000 | (int)((r2 >> 40) & 0xfffff), (int)r1);
             a = __dmul_rn(q, b);
@@ -353,9 +484,9 @@ __global__ void division_selftest_kernel(uint64_t n, uint64_t seed, unsigned lon
             a = (double)((long long)(r1 >> 40) % 97 - 48);
             b = (double)((r2 >> 40) % 13 + 1);
         }
-        if (!(b > 0.0) || !div_safe(a) || !div_safe(b)) continue;
+        if (r1 & (1ull << 62)) a = -a;
         const double y = __drcp_rn(b);
-        const double q = div_markstein(a, b, y), ref = __ddiv_rn(a, b);
+        const double q = div_exact(a, b, y), ref = __ddiv_rn(a, b);
         bad += __double_as_longlong(q) != __double_as_longlong(ref);
         ++cnt;
     }
@@ -396,9 +527,13 @@ extern "C" int hx_integrate_mesh(const double *coords, int64_t n_nodes, const in
     const int64_t n = hi - lo;
     HX_TRY_CUDA(cudaMemsetAsync(fail, 0xff, sizeof(unsigned long long), s));
     if (n > 0) {
-        const int64_t blocks = ceil_div(n, KE_BLOCK);
-        integrate_mesh_kernel<HX_MODE_EXACT><<<(unsigned)blocks, KE_BLOCK, 0, s>>>(
-            coords, conn, coeff, lo, n, ke, rows, cols, reinterpret_cast<unsigned long long *>(fail));
+        const int64_t blocks = std::min<int64_t>(ceil_div(n, GP_EL_PER_BLOCK), persistent_blocks());
+        if (rows != nullptr)
+            integrate_mesh_kernel<HX_MODE_EXACT, true><<<(unsigned)blocks, GP_BLOCK, 0, s>>>(
+                coords, conn, coeff, lo, n, ke, rows, cols, reinterpret_cast<unsigned long long *>(fail));
+        else
+            integrate_mesh_kernel<HX_MODE_EXACT, false><<<(unsigned)blocks, GP_BLOCK, 0, s>>>(
+                coords, conn, coeff, lo, n, ke, rows, cols, reinterpret_cast<unsigned long long *>(fail));
         HX_CHECK_LAUNCH("integrate_mesh_kernel");
     }
     fail_resolve_mesh_kernel<<<1, 1, 0, s>>>(coords, conn, coeff, fail);
@@ -419,12 +554,12 @@ extern "C" int hx_stiffness_batch(const double *coords, const double *coeff, int
     cudaStream_t s = (cudaStream_t)stream;
     HX_TRY_CUDA(cudaMemsetAsync(fail, 0xff, sizeof(unsigned long long), s));
     if (n > 0) {
-        const int64_t blocks = ceil_div(n, KE_BLOCK);
-        stiffness_batch_kernel<HX_MODE_EXACT><<<(unsigned)blocks, KE_BLOCK, 0, s>>>(
+        const int64_t blocks = ceil_div(n, GP_EL_PER_BLOCK);
+        stiffness_batch_kernel<HX_MODE_EXACT><<<(unsigned)blocks, GP_BLOCK, 0, s>>>(
             coords, coeff, n, out, reinterpret_cast<unsigned long long *>(fail));
         HX_CHECK_LAUNCH("stiffness_batch_kernel");
     }
-    fail_resolve_batch_kernel<<<1, 1, 0, s>>>(coords, coeff, fail);
+    fail_resolve_batch_kernel<<<1, 1, 0, s>>>(coords, fail);
     HX_CHECK_LAUNCH("fail_resolve_batch_kernel");
     return HX_OK;
 }

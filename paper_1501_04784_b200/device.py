@@ -227,12 +227,12 @@ def mesh_csc(parts, n_nodes: int, col_lo: int = 0, col_hi: int | None = None, st
     ws_bytes = N.lib().hx_mesh_csc_workspace_bytes(n_total, ncols)
     if ws_bytes < 0:
         raise ValueError("bad mesh size")
-    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
     status = torch.zeros(1, dtype=torch.int32, device=dev)
     col_ptr = torch.empty(ncols + 1, dtype=torch.int64, device=dev)
     sh = stream_handle(stream)
     capacity = ROWS_PER_COLUMN_ESTIMATE * ncols if row_capacity is None else row_capacity
     while True:
+        ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
         row_buf = torch.empty(max(capacity, 1), dtype=torch.int64, device=dev)
         val_buf = torch.empty(max(capacity, 1), dtype=torch.float64, device=dev)
         N.check(N.lib().hx_mesh_csc_build(segs, len(parts), n_nodes, col_lo, col_hi, _ptr(col_ptr), _ptr(row_buf),
@@ -241,6 +241,12 @@ def mesh_csc(parts, n_nodes: int, col_lo: int = 0, col_hi: int | None = None, st
         head = torch.stack([status.to(torch.int64)[0], col_ptr[-1]]).cpu()  # one sync: status + nnz
         st, nnz = int(head[0]), int(head[1])
         _status_error(st)
+        if st & N.ST_SCRATCH and not st & (N.ST_FASTPATH_LIMITS & ~N.ST_SCRATCH):
+            # more off-diagonal records than the default scratch (e.g. the first column block of a
+            # permuted mesh): the counts are complete, re-run with room for all of them
+            ws_bytes = N.lib().hx_mesh_csc_workspace_bytes(n_total, ncols) + 8 * nnz
+            capacity = max(capacity, nnz)
+            continue
         if st & N.ST_FASTPATH_LIMITS:
             return _mesh_csc_generic(parts, n_nodes, col_lo, col_hi, stream)
         if nnz <= capacity:

@@ -18,7 +18,7 @@ for s in $STEPS; do
     launches) timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
         --csv --log-file gpurun_out/${TAG}_launches_c3.csv python tools/profile_step.py C3 > gpurun_out/${TAG}_launches.log 2>&1 ;;
     ncu) timeout 1200 ncu --set full --clock-control none --import-source on \
-        -k regex:"integrate_mesh_kernel|pattern_kernel|emit_kernel|adjacency_fill|degree_kernel" -c 5 \
+        -k regex:"integrate_mesh_kernel|pattern_kernel|emit_kernel|adjacency_kernel" -c 5 \
         -o gpurun_out/${TAG}_full_c3 python tools/profile_step.py C3 > gpurun_out/${TAG}_ncu_full.log 2>&1 ;;
   esac
 done
