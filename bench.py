@@ -356,7 +356,6 @@ def measure_kernels(args, rank, world, runner, dm):
         del csc
     del ke, rows, cols
     # integrate_mesh_kernel, fail_resolve, adjacency, pattern, emit, CUB scan (init + scan)
-    # 2 CUB scans (2 kernels each)
     acc["launches_per_step"] = 7
     return acc
 

@@ -67,7 +67,7 @@ extern "C" {
 typedef struct hx_fail_info {
     int64_t element;     /* global element id (element_offset applied, element.py:237-244) */
     int32_t gauss_point; /* 0..7, r slowest (element.py:116-121)                           */
-    int32_t reserved;
+    int32_t reserved;    /* scratch of the integration call (work counter), zeroed by it        */
     double det;          /* det(J) at that point (element.py:276-279)                      */
 } hx_fail_info;
 
@@ -135,6 +135,12 @@ int hx_mesh_csc_symbolic(const hx_elem_segment *segs, int32_t n_segs, int64_t n_
 int hx_mesh_csc_build(const hx_elem_segment *segs, int32_t n_segs, int64_t n_nodes, int64_t col_lo,
                       int64_t col_hi, int64_t *col_ptr, int64_t *row_idx, double *vals, int64_t capacity,
                       void *workspace, int64_t workspace_bytes, uint32_t *status, void *stream);
+/* Symbolic with row_capacity = 0 only plans (col_ptr + workspace, no row_idx); hx_mesh_csc_emit
+ * then writes row_idx and vals (first `capacity` entries) in one pass -- the split lets the plan run
+ * on a second stream concurrently with the integration kernel. */
+int hx_mesh_csc_emit(const hx_elem_segment *segs, int32_t n_segs, int64_t col_lo, int64_t col_hi,
+                     const int64_t *col_ptr, int64_t *row_idx, double *vals, int64_t capacity,
+                     const void *workspace, uint32_t *status, void *stream);
 int hx_mesh_csc_numeric(const hx_elem_segment *segs, int32_t n_segs, int64_t col_lo,
                         int64_t col_hi, const int64_t *col_ptr, const int64_t *row_idx,
                         double *vals, const void *workspace, uint32_t *status, void *stream);

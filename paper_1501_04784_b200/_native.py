@@ -30,6 +30,7 @@ EXPORTED = (
     "hx_selftest_division",
     "hx_stiffness_batch", "hx_integrate_mesh", "hx_connectivity_index_arrays",
     "hx_mesh_csc_workspace_bytes", "hx_mesh_csc_symbolic", "hx_mesh_csc_build", "hx_mesh_csc_numeric",
+    "hx_mesh_csc_emit",
     "hx_triplet_csc_workspace_bytes", "hx_triplet_csc_symbolic", "hx_triplet_csc_numeric",
     "hx_halo_workspace_bytes", "hx_halo_count", "hx_halo_pack",
 )
@@ -76,6 +77,7 @@ def lib():
         "hx_mesh_csc_symbolic": ([P, I32, I64, I64, I64, P, P, I64, P, I64, P, P], ctypes.c_int),
         "hx_mesh_csc_build": ([P, I32, I64, I64, I64, P, P, P, I64, P, I64, P, P], ctypes.c_int),
         "hx_mesh_csc_numeric": ([P, I32, I64, I64, P, P, P, P, P, P], ctypes.c_int),
+        "hx_mesh_csc_emit": ([P, I32, I64, I64, P, P, P, I64, P, P, P], ctypes.c_int),
         "hx_triplet_csc_workspace_bytes": ([I64, I64], I64),
         "hx_triplet_csc_symbolic": ([P, P, I64, I64, P, P, P, I64, P, P], ctypes.c_int),
         "hx_triplet_csc_numeric": ([P, I64, I64, P, P, P, P], ctypes.c_int),

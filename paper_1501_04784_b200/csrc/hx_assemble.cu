@@ -570,7 +570,7 @@ static int mesh_csc_build(const hx_elem_segment *segs, int32_t n_segs, int64_t n
                                                                      w.scratch, w.block_scratch, row_idx, vals,
                                                                      row_capacity, status);
             HX_CHECK_LAUNCH("emit_kernel");
-        } else {
+        } else if (row_capacity > 0) {
             emit_rows_kernel<<<tiles, EMIT_BLOCK, 0, s>>>(col_lo, ncols, col_ptr, w.scratch, w.block_scratch, row_idx,
                                                          row_capacity, status);
             HX_CHECK_LAUNCH("emit_rows_kernel");
@@ -623,6 +623,34 @@ extern "C" int hx_mesh_csc_numeric(const hx_elem_segment *segs, int32_t n_segs, 
             emit_kernel<false, false><<<(unsigned)ceil_div(ncols, COL_BLOCK), EMIT_BLOCK, 0, s>>>(
                 T, col_lo, ncols, w.deg, w.adj, col_ptr, w.scratch, w.block_scratch, nullptr, vals, INT64_MAX, status);
         HX_CHECK_LAUNCH("emit_kernel<numeric>");
+    }
+    return HX_OK;
+}
+
+extern "C" int hx_mesh_csc_emit(const hx_elem_segment *segs, int32_t n_segs, int64_t col_lo, int64_t col_hi,
+                                const int64_t *col_ptr, int64_t *row_idx, double *vals, int64_t capacity,
+                                const void *workspace, uint32_t *status, void *stream) {
+    SegTable T;
+    int64_t n_total = 0;
+    int rc = make_segtable(segs, n_segs, T, n_total, true);
+    if (rc) return rc;
+    if (col_lo < 0 || col_hi < col_lo || col_ptr == nullptr || workspace == nullptr || status == nullptr ||
+        capacity < 0 || (capacity > 0 && (row_idx == nullptr || vals == nullptr))) {
+        set_last_error("hx_mesh_csc_emit: bad arguments");
+        return HX_ERR_VALUE;
+    }
+    const int64_t ncols = col_hi - col_lo;
+    MeshWs w = mesh_ws_layout(const_cast<void *>(workspace), ncols);
+    cudaStream_t s = (cudaStream_t)stream;
+    if (ncols > 0) {
+        const unsigned tiles = (unsigned)ceil_div(ncols, COL_BLOCK);
+        if (single_dense(T))
+            emit_kernel<true, true><<<tiles, EMIT_BLOCK, 0, s>>>(T, col_lo, ncols, w.deg, w.adj, col_ptr, w.scratch,
+                                                                w.block_scratch, row_idx, vals, capacity, status);
+        else
+            emit_kernel<true, false><<<tiles, EMIT_BLOCK, 0, s>>>(T, col_lo, ncols, w.deg, w.adj, col_ptr, w.scratch,
+                                                                 w.block_scratch, row_idx, vals, capacity, status);
+        HX_CHECK_LAUNCH("emit_kernel<emit>");
     }
     return HX_OK;
 }

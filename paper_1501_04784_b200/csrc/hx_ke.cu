@@ -29,6 +29,7 @@
 //     elements take __ddiv_rn).  hx_selftest_division checks the quotient on 2^30 operand pairs.
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 
 #include "hx_common.cuh"
 
@@ -306,16 +307,19 @@ __device__ __forceinline__ bool ke_gauss_point(GpWarpSmem &sm, int el, int gp, b
 }
 
 // Mesh kernel: elements [lo, lo+n) of the mesh; outputs indexed from 0 (= element lo).
-// Persistent warps: warp w handles element quads w, w + W, w + 2W, ... and prefetches the next
-// quad's node ids, coordinates and coefficients into registers before integrating the current one,
-// so the gather latency hides under the FP64 work.
+// Persistent warps with dynamic work distribution: each warp takes element quads from a global
+// counter (so the kernel balances itself when it shares the GPU with the concurrently running
+// symbolic assembly) and prefetches the next quad's node ids, coordinates and coefficients into
+// registers before integrating the current one, so the gather latency hides under the FP64 work.
 template <int MODE, bool WITH_INDEX>
 __global__ void __launch_bounds__(GP_BLOCK, HX_KE_MIN_BLOCKS)
 integrate_mesh_kernel(const double *__restrict__ coords, const int32_t *__restrict__ conn,
                       const double *__restrict__ coeff, int64_t lo, int64_t n,
                       double *__restrict__ ke_out, int32_t *__restrict__ rows_out,
-                      int32_t *__restrict__ cols_out, unsigned long long *__restrict__ fail_min) {
-    __shared__ GpWarpSmem s_warp[GP_WARPS];
+                      int32_t *__restrict__ cols_out, unsigned long long *__restrict__ fail_min,
+                      unsigned *__restrict__ quad_counter) {
+    extern __shared__ __align__(16) unsigned char s_dyn[];
+    GpWarpSmem *s_warp = reinterpret_cast<GpWarpSmem *>(s_dyn);
     __shared__ uint8_t s_pi[36], s_pj[36];
     init_pack_smem(s_pi, s_pj);
     __syncthreads();
@@ -323,22 +327,29 @@ integrate_mesh_kernel(const double *__restrict__ coords, const int32_t *__restri
     const int el = lane >> 3, gp = lane & 7;
     GpWarpSmem &sm = s_warp[warp];
     const int64_t n_quads = (n + GP_EL_PER_WARP - 1) / GP_EL_PER_WARP;
-    const int64_t stride = (int64_t)gridDim.x * GP_WARPS;
-    int64_t quad = (int64_t)blockIdx.x * GP_WARPS + warp;
+    const int64_t first_dynamic = (int64_t)gridDim.x * GP_WARPS;
+    auto grab = [&]() -> int64_t {
+        unsigned q = 0;
+        if (lane == 0) q = atomicAdd(quad_counter, 1u);
+        return first_dynamic + (int64_t)__shfl_sync(0xffffffffu, q, 0);
+    };
     auto node_id = [&](int64_t q) -> int32_t {
         const int64_t k = q * GP_EL_PER_WARP + el;
         return k < n ? __ldg(conn + (lo + k) * 8 + gp) : -1;
     };
     // padding lanes integrate a unit cube (keeps them off the slow paths; never stored)
     const double u0 = nat_r(gp) > 0, u1 = nat_s(gp) > 0, u2 = nat_t(gp) > 0;
-    int32_t node = node_id(quad), node_next = node_id(quad + stride);
+    int64_t quad = (int64_t)blockIdx.x * GP_WARPS + warp;  // being published / integrated
+    int64_t quad1 = quad < n_quads ? grab() : n_quads;      // coordinates in flight
+    int64_t quad2 = quad1 < n_quads ? grab() : n_quads;     // node ids in flight
+    int32_t node = node_id(quad), node_next = node_id(quad1);
     double x0 = u0, x1 = u1, x2 = u2, c = 1.0;
     if (node >= 0) {
         const double *p = coords + 3 * (int64_t)node;
         x0 = __ldg(p); x1 = __ldg(p + 1); x2 = __ldg(p + 2);
         c = __ldg(coeff + lo + quad * GP_EL_PER_WARP + el);
     }
-    for (; quad < n_quads; quad += stride) {
+    while (quad < n_quads) {
         const int64_t k = quad * GP_EL_PER_WARP + el;
         const bool valid = k < n;
         const unsigned in_range = __ballot_sync(0xffffffffu, coord_in_range(x0) && coord_in_range(x1) &&
@@ -347,18 +358,22 @@ integrate_mesh_kernel(const double *__restrict__ coords, const int32_t *__restri
         __syncwarp();
         publish_node(sm, el, gp, node, x0, x1, x2, c);
         __syncwarp();
-        // prefetch the next quad
+        // prefetch: coordinates of quad1, node ids of quad2, claim the quad after
         node = node_next;
-        node_next = node_id(quad + 2 * stride);
+        node_next = node_id(quad2);
         x0 = u0; x1 = u1; x2 = u2; c = 1.0;
         if (node >= 0) {
             const double *p = coords + 3 * (int64_t)node;
             x0 = __ldg(p); x1 = __ldg(p + 1); x2 = __ldg(p + 2);
-            c = __ldg(coeff + lo + (quad + stride) * GP_EL_PER_WARP + el);
+            c = __ldg(coeff + lo + quad1 * GP_EL_PER_WARP + el);
         }
+        const int64_t quad3 = quad2 < n_quads ? grab() : n_quads;
         const bool ok = ke_gauss_point<WITH_INDEX>(sm, el, gp, fast_div, k, valid, ke_out, rows_out, cols_out, s_pi,
                                                    s_pj);
         if (valid && !ok) atomicMin(fail_min, (unsigned long long)(lo + k));
+        quad = quad1;
+        quad1 = quad2;
+        quad2 = quad3;
     }
 }
 
@@ -367,7 +382,8 @@ template <int MODE>
 __global__ void __launch_bounds__(GP_BLOCK, HX_KE_MIN_BLOCKS)
 stiffness_batch_kernel(const double *__restrict__ coords, const double *__restrict__ coeff, int64_t n,
                        double *__restrict__ out, unsigned long long *__restrict__ fail_min) {
-    __shared__ GpWarpSmem s_warp[GP_WARPS];
+    extern __shared__ __align__(16) unsigned char s_dyn[];
+    GpWarpSmem *s_warp = reinterpret_cast<GpWarpSmem *>(s_dyn);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int el = lane >> 3, gp = lane & 7;
     GpWarpSmem &sm = s_warp[warp];
@@ -440,14 +456,34 @@ __global__ void index_kernel(const int32_t *__restrict__ conn, int64_t lo, int64
     }
 }
 
+constexpr size_t GP_SMEM = GP_WARPS * sizeof(GpWarpSmem);  // dynamic shared memory per block
+
+// Opt the integration kernels into > 48 KB of dynamic shared memory (once per device).
+static void configure_ke_kernels() {
+    static bool done[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 64 && done[dev]) return;
+    cudaFuncSetAttribute(integrate_mesh_kernel<HX_MODE_EXACT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)GP_SMEM);
+    cudaFuncSetAttribute(integrate_mesh_kernel<HX_MODE_EXACT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)GP_SMEM);
+    cudaFuncSetAttribute(stiffness_batch_kernel<HX_MODE_EXACT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)GP_SMEM);
+    if (dev < 64) done[dev] = true;
+}
+
 // Resident blocks of the persistent integration kernel on the current device (queried once).
 static int64_t persistent_blocks() {
     static int64_t cached = 0;
+    configure_ke_kernels();
     if (cached == 0) {
         int dev = 0, sms = 148, per_sm = HX_KE_MIN_BLOCKS;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, integrate_mesh_kernel<HX_MODE_EXACT, true>, GP_BLOCK, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, integrate_mesh_kernel<HX_MODE_EXACT, true>, GP_BLOCK,
+                                                      GP_SMEM);
+        if (const char *env = getenv("HX_KE_BLOCKS_PER_SM")) per_sm = std::min(per_sm, atoi(env));  // experiments
         cached = (int64_t)sms * std::max(per_sm, 1);
     }
     return cached;
@@ -526,14 +562,20 @@ extern "C" int hx_integrate_mesh(const double *coords, int64_t n_nodes, const in
     cudaStream_t s = (cudaStream_t)stream;
     const int64_t n = hi - lo;
     HX_TRY_CUDA(cudaMemsetAsync(fail, 0xff, sizeof(unsigned long long), s));
+    HX_TRY_CUDA(cudaMemsetAsync(&fail->reserved, 0, sizeof(int32_t), s));  // quad counter
     if (n > 0) {
+        if (n > (int64_t)UINT32_MAX * GP_EL_PER_WARP / 2) {
+            set_last_error("hx_integrate_mesh: %lld elements exceed one launch", (long long)n);
+            return HX_ERR_CONFIG;
+        }
         const int64_t blocks = std::min<int64_t>(ceil_div(n, GP_EL_PER_BLOCK), persistent_blocks());
+        unsigned *counter = reinterpret_cast<unsigned *>(&fail->reserved);
         if (rows != nullptr)
-            integrate_mesh_kernel<HX_MODE_EXACT, true><<<(unsigned)blocks, GP_BLOCK, 0, s>>>(
-                coords, conn, coeff, lo, n, ke, rows, cols, reinterpret_cast<unsigned long long *>(fail));
+            integrate_mesh_kernel<HX_MODE_EXACT, true><<<(unsigned)blocks, GP_BLOCK, GP_SMEM, s>>>(
+                coords, conn, coeff, lo, n, ke, rows, cols, reinterpret_cast<unsigned long long *>(fail), counter);
         else
-            integrate_mesh_kernel<HX_MODE_EXACT, false><<<(unsigned)blocks, GP_BLOCK, 0, s>>>(
-                coords, conn, coeff, lo, n, ke, rows, cols, reinterpret_cast<unsigned long long *>(fail));
+            integrate_mesh_kernel<HX_MODE_EXACT, false><<<(unsigned)blocks, GP_BLOCK, GP_SMEM, s>>>(
+                coords, conn, coeff, lo, n, ke, rows, cols, reinterpret_cast<unsigned long long *>(fail), counter);
         HX_CHECK_LAUNCH("integrate_mesh_kernel");
     }
     fail_resolve_mesh_kernel<<<1, 1, 0, s>>>(coords, conn, coeff, fail);
@@ -555,7 +597,8 @@ extern "C" int hx_stiffness_batch(const double *coords, const double *coeff, int
     HX_TRY_CUDA(cudaMemsetAsync(fail, 0xff, sizeof(unsigned long long), s));
     if (n > 0) {
         const int64_t blocks = ceil_div(n, GP_EL_PER_BLOCK);
-        stiffness_batch_kernel<HX_MODE_EXACT><<<(unsigned)blocks, GP_BLOCK, 0, s>>>(
+        configure_ke_kernels();
+        stiffness_batch_kernel<HX_MODE_EXACT><<<(unsigned)blocks, GP_BLOCK, GP_SMEM, s>>>(
             coords, coeff, n, out, reinterpret_cast<unsigned long long *>(fail));
         HX_CHECK_LAUNCH("stiffness_batch_kernel");
     }

@@ -18,7 +18,8 @@ from .errors import ConfigurationError, DegenerateElementError, MeshValidationEr
 
 __all__ = [
     "DeviceMesh", "DeviceCsc", "require_device", "stream_handle", "integrate_mesh", "stiffness_batch",
-    "connectivity_index_arrays", "raise_if_failed", "mesh_csc", "triplet_csc",
+    "connectivity_index_arrays", "raise_if_failed", "mesh_csc", "triplet_csc", "MeshPlan", "mesh_plan_async",
+    "mesh_emit",
 ]
 
 _FAIL_WORDS = 3  # hx_fail_info = {int64 element, int32 gp, int32 pad, double det} = 24 bytes
@@ -255,6 +256,61 @@ def mesh_csc(parts, n_nodes: int, col_lo: int = 0, col_hi: int | None = None, st
     row_idx = row_buf[:nnz]
     vals = val_buf[:nnz]
     return DeviceCsc(col_ptr, row_idx, vals, n_nodes, col_lo, "mesh")
+
+
+@dataclass
+class MeshPlan:
+    """Symbolic assembly launched asynchronously (hx_mesh_csc_symbolic without row emission):
+    col_ptr, the workspace holding the sorted adjacency and the off-diagonal records, the status
+    word and the output buffers sized by the rows-per-column estimate."""
+
+    conn: torch.Tensor
+    n_nodes: int
+    col_ptr: torch.Tensor
+    ws: torch.Tensor
+    status: torch.Tensor
+    row_buf: torch.Tensor
+    val_buf: torch.Tensor
+    capacity: int
+
+
+def mesh_plan_async(conn: torch.Tensor, n_nodes: int, stream=None) -> MeshPlan:
+    """Launch the symbolic phase of a single-segment mesh assembly on ``stream`` (no host sync).
+    It reads only the connectivity, so it can run concurrently with the integration kernel."""
+    n = conn.shape[0]
+    if conn.dtype != torch.int32 or tuple(conn.shape) != (n, 8) or not conn.is_contiguous():
+        raise ValueError("conn must be a contiguous CUDA int32 (n, 8) tensor")
+    dev = conn.device
+    ws_bytes = N.lib().hx_mesh_csc_workspace_bytes(n, n_nodes)
+    if ws_bytes < 0:
+        raise ValueError("bad mesh size")
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
+    status = torch.zeros(1, dtype=torch.int32, device=dev)
+    col_ptr = torch.empty(n_nodes + 1, dtype=torch.int64, device=dev)
+    capacity = ROWS_PER_COLUMN_ESTIMATE * n_nodes
+    row_buf = torch.empty(max(capacity, 1), dtype=torch.int64, device=dev)
+    val_buf = torch.empty(max(capacity, 1), dtype=torch.float64, device=dev)
+    segs = N.segments([(conn.data_ptr(), 0, n)])
+    N.check(N.lib().hx_mesh_csc_symbolic(segs, 1, n_nodes, 0, n_nodes, _ptr(col_ptr), ctypes.c_void_p(0), 0,
+                                         _ptr(ws), ws_bytes, _ptr(status), stream_handle(stream)),
+            "hx_mesh_csc_symbolic")
+    return MeshPlan(conn, n_nodes, col_ptr, ws, status, row_buf, val_buf, capacity)
+
+
+def mesh_emit(plan: MeshPlan, ke: torch.Tensor, stream=None) -> DeviceCsc:
+    """Row indices and values of a planned assembly (one pass over the KE rows), then one host
+    sync for the status word and nnz.  Falls back to mesh_csc when the plan hit a limit."""
+    _check_segment(plan.conn, ke)
+    segs = N.segments([(plan.conn.data_ptr(), ke.data_ptr(), plan.conn.shape[0])])
+    N.check(N.lib().hx_mesh_csc_emit(segs, 1, 0, plan.n_nodes, _ptr(plan.col_ptr), _ptr(plan.row_buf),
+                                     _ptr(plan.val_buf), plan.capacity, _ptr(plan.ws), _ptr(plan.status),
+                                     stream_handle(stream)), "hx_mesh_csc_emit")
+    head = torch.stack([plan.status.to(torch.int64)[0], plan.col_ptr[-1]]).cpu()
+    st, nnz = int(head[0]), int(head[1])
+    _status_error(st)
+    if st & N.ST_FASTPATH_LIMITS or nnz > plan.capacity:
+        return mesh_csc([(plan.conn, ke)], plan.n_nodes, stream=stream)
+    return DeviceCsc(plan.col_ptr, plan.row_buf[:nnz], plan.val_buf[:nnz], plan.n_nodes, 0, "mesh")
 
 
 def _mesh_csc_generic(parts, n_nodes, col_lo, col_hi, stream) -> DeviceCsc:

@@ -212,7 +212,7 @@ class ShardedBuild:
             acc["ke_ms"] += ev[0].elapsed_time(ev[1]) / repeats
             acc["halo_exchange_ms"] += ev[1].elapsed_time(ev[2]) / repeats
             acc["assembly_ms"] += ev[2].elapsed_time(ev[3]) / repeats
-        acc["launches_per_step"] = 10 + 5  # single-GPU set + halo count/scan(2)/totals/pack
+        acc["launches_per_step"] = 7 + 5  # single-GPU set + halo count/scan(2)/totals/pack
         return acc
 
     def measure_e2e(self, steps, barrier):

@@ -85,28 +85,52 @@ class DeviceBuild:
     csc: D.DeviceCsc
 
 
+_SIDE_STREAMS: dict = {}
+
+
+def _side_stream(dev) -> torch.cuda.Stream:
+    key = torch.device(dev).index
+    if key not in _SIDE_STREAMS:
+        _SIDE_STREAMS[key] = torch.cuda.Stream(device=dev)
+    return _SIDE_STREAMS[key]
+
+
 def build_device(dm: D.DeviceMesh, mode: str = "exact", with_index: bool = True, ranges=None,
-                 ke=None, rows=None, cols=None, stream=None) -> DeviceBuild:
+                 ke=None, rows=None, cols=None, stream=None, overlap: bool = True) -> DeviceBuild:
     """KE (+ fused iK/jK) for every element, then the lower CSC, all in HBM.
 
-    ``ranges`` is an optional BatchPlan-style list of element groups (each one kernel launch
-    into the same output buffers); results are bitwise independent of it.
+    The symbolic assembly reads only the connectivity, so with ``overlap`` it runs on a side
+    stream concurrently with the FP64-bound integration kernel; the emit pass (row indices +
+    values, which needs KE) follows on the main stream.  ``ranges`` is an optional BatchPlan-style
+    list of element groups (each one kernel launch into the same output buffers); results are
+    bitwise independent of both.
     """
     dev = dm.conn.device
     n = dm.n_el
+    main = torch.cuda.current_stream(dev) if stream is None else stream
     if ke is None:
         ke = torch.empty((n, 36), dtype=torch.float64, device=dev)
     if with_index:
         rows = torch.empty(36 * n, dtype=torch.int32, device=dev) if rows is None else rows
         cols = torch.empty(36 * n, dtype=torch.int32, device=dev) if cols is None else cols
+    plan = None
+    if overlap and n > 0:
+        side = _side_stream(dev)
+        side.wait_stream(main)  # inputs and the buffers below are ordered before the plan
+        plan = D.mesh_plan_async(dm.conn, dm.n_nodes, stream=side)
+        plan_done = side.record_event()
     fails = []
     for lo, hi in (ranges or [(0, n)]):
         _, _, _, fail = D.integrate_mesh(dm, lo, hi, ke=ke[lo:hi],
                                          rows=rows[36 * lo:36 * hi] if with_index else None,
                                          cols=cols[36 * lo:36 * hi] if with_index else None,
-                                         with_index=with_index, mode=mode, stream=stream)
+                                         with_index=with_index, mode=mode, stream=main)
         fails.append(fail)
-    csc = D.mesh_csc([(dm.conn, ke)], dm.n_nodes, stream=stream)
+    if plan is not None:
+        main.wait_event(plan_done)
+        csc = D.mesh_emit(plan, ke, stream=main)
+    else:
+        csc = D.mesh_csc([(dm.conn, ke)], dm.n_nodes, stream=main)
     for f in fails:
         D.raise_if_failed(f)
     return DeviceBuild(ke, rows if with_index else None, cols if with_index else None, csc)
