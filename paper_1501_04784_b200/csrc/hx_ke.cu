@@ -170,18 +170,147 @@ __device__ __forceinline__ double mag_select(int k) {
 }
 
 
-// Lane (el, a): publish node a's products M_m x[a][k] and id; the element's coefficient from a = 0.
+// Lane (el, a): publish node a's id and, in exact mode, its products M_m x[a][k] (fast mode: the
+// raw coordinates); the element's coefficient from a = 0.
+template <int MODE>
 __device__ __forceinline__ void publish_node(GpWarpSmem &sm, int el, int a, int32_t node, double x0, double x1,
                                              double x2, double c) {
     double *P = sm.P + el * P_EL_STRIDE + 3 * a;
+    if (MODE == HX_MODE_EXACT) {
 #pragma unroll
-    for (int m = 0; m < 3; ++m) {
-        P[m * P_M_STRIDE] = dmul(dn_magnitude(m), x0);
-        P[m * P_M_STRIDE + 1] = dmul(dn_magnitude(m), x1);
-        P[m * P_M_STRIDE + 2] = dmul(dn_magnitude(m), x2);
+        for (int m = 0; m < 3; ++m) {
+            P[m * P_M_STRIDE] = dmul(dn_magnitude(m), x0);
+            P[m * P_M_STRIDE + 1] = dmul(dn_magnitude(m), x1);
+            P[m * P_M_STRIDE + 2] = dmul(dn_magnitude(m), x2);
+        }
+    } else {
+        P[0] = x0;
+        P[1] = x1;
+        P[2] = x2;
     }
     sm.conn[el * 8 + a] = node;
     if (a == 0) sm.coeff[el] = c;
+}
+
+// Reduce the element's 8 lanes' contributions of pass c and store KE / iK / jK (shared by both
+// modes; exact mode sums in Gauss-point order, fast mode as a fixed depth-3 tree).
+template <int MODE, bool WITH_INDEX>
+__device__ __forceinline__ void reduce_store(const GpWarpSmem &sm, const double *tb, int el, int gp, int c,
+                                             int64_t out_el, bool valid, double *__restrict__ ke_out,
+                                             int32_t *__restrict__ rows_out, int32_t *__restrict__ cols_out,
+                                             const uint8_t *s_pi, const uint8_t *s_pj) {
+    const int p = 8 * c + gp;  // this lane reduces packed entry p of its element
+    if (p >= 36) return;
+    const double2 *src = reinterpret_cast<const double2 *>(tb + gp * T_J_STRIDE);
+    const double2 v0 = src[0], v1 = src[1], v2 = src[2], v3 = src[3];
+    double acc;
+    if (MODE == HX_MODE_EXACT) {
+        acc = dadd(0.0, v0.x);
+        acc = dadd(acc, v0.y);
+        acc = dadd(acc, v1.x);
+        acc = dadd(acc, v1.y);
+        acc = dadd(acc, v2.x);
+        acc = dadd(acc, v2.y);
+        acc = dadd(acc, v3.x);
+        acc = dadd(acc, v3.y);
+    } else {
+        acc = ((v0.x + v0.y) + (v1.x + v1.y)) + ((v2.x + v2.y) + (v3.x + v3.y));
+    }
+    if (valid) {
+        ke_out[out_el * 36 + p] = acc;
+        if (WITH_INDEX) {
+            const int32_t gi = sm.conn[el * 8 + s_pi[p]], gj = sm.conn[el * 8 + s_pj[p]];
+            rows_out[out_el * 36 + p] = max(gi, gj);
+            cols_out[out_el * 36 + p] = min(gi, gj);
+        }
+    }
+}
+
+// Fast mode (HX_MODE_FAST): the same quadrature restructured for FMA,
+//   ke_ij += dN_i^T G dN_j,  G = (c / det) adj(J)^T adj(J)  (= c det J^-1 J^-T),
+// about 300 FP64 operations per Gauss point instead of ~500 in reference order.  Not bitwise:
+// |KE - KE_ref| <= 1e-12 max_j |KE_ref[e, j]| per element (tests/test_gpu_fast_mode.py), and the
+// degenerate-element test uses this det (differs from the reference only for |det| at rounding
+// level of 0).
+template <bool WITH_INDEX>
+__device__ __forceinline__ bool ke_gauss_point_fast(GpWarpSmem &sm, int el, int gp, int64_t out_el, bool valid,
+                                                    double *__restrict__ ke_out, int32_t *__restrict__ rows_out,
+                                                    int32_t *__restrict__ cols_out, const uint8_t *s_pi,
+                                                    const uint8_t *s_pj) {
+    const int ir = (gp >> 2) & 1, is = (gp >> 1) & 1, it = gp & 1;
+    const double *X = sm.P + el * P_EL_STRIDE;
+    double Mr[4], Ms[4], Mt[4];
+#pragma unroll
+    for (int u = 0; u < 2; ++u)
+#pragma unroll
+        for (int v = 0; v < 2; ++v) {
+            Mr[2 * u + v] = mag_select((u == is) + (v == it));
+            Ms[2 * u + v] = mag_select((u == ir) + (v == it));
+            Mt[2 * u + v] = mag_select((u == ir) + (v == is));
+        }
+    // dN[d][a] = sign(d, a) * M (register-resident for this lane's Gauss point)
+    auto dn = [&](int d, int a) -> double {
+        const double m = d == 0 ? Mr[2 * bit_s(a) + bit_t(a)] : d == 1 ? Ms[2 * bit_r(a) + bit_t(a)]
+                                                               : Mt[2 * bit_r(a) + bit_s(a)];
+        const int sg = d == 0 ? nat_r(a) : d == 1 ? nat_s(a) : nat_t(a);
+        return sg > 0 ? m : -m;
+    };
+    double j[3][3];
+#pragma unroll
+    for (int d = 0; d < 3; ++d)
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            double acc = dn(d, 0) * X[k];
+#pragma unroll
+            for (int a = 1; a < 8; ++a) acc = fma(dn(d, a), X[3 * a + k], acc);
+            j[d][k] = acc;
+        }
+    // adjugate: a[r][d] = det * inv[r][d]
+    double ad[3][3];
+    ad[0][0] = fma(j[1][1], j[2][2], -j[1][2] * j[2][1]);
+    ad[0][1] = fma(j[0][2], j[2][1], -j[0][1] * j[2][2]);
+    ad[0][2] = fma(j[0][1], j[1][2], -j[0][2] * j[1][1]);
+    ad[1][0] = fma(j[1][2], j[2][0], -j[1][0] * j[2][2]);
+    ad[1][1] = fma(j[0][0], j[2][2], -j[0][2] * j[2][0]);
+    ad[1][2] = fma(j[0][2], j[1][0], -j[0][0] * j[1][2]);
+    ad[2][0] = fma(j[1][0], j[2][1], -j[1][1] * j[2][0]);
+    ad[2][1] = fma(j[0][1], j[2][0], -j[0][0] * j[2][1]);
+    ad[2][2] = fma(j[0][0], j[1][1], -j[0][1] * j[1][0]);
+    const double det = fma(j[0][0], ad[0][0], fma(j[0][1], ad[1][0], j[0][2] * ad[2][0]));
+    const bool ok = positive(det);
+    const double f = sm.coeff[el] * __drcp_rn(det);
+    // G = f adj^T adj (symmetric)
+    double G[3][3];
+#pragma unroll
+    for (int d = 0; d < 3; ++d)
+#pragma unroll
+        for (int e = d; e < 3; ++e) {
+            G[d][e] = f * fma(ad[0][d], ad[0][e], fma(ad[1][d], ad[1][e], ad[2][d] * ad[2][e]));
+            G[e][d] = G[d][e];
+        }
+    // H = G dN (3 x 8)
+    double H[3][8];
+#pragma unroll
+    for (int d = 0; d < 3; ++d)
+#pragma unroll
+        for (int a = 0; a < 8; ++a) H[d][a] = fma(G[d][0], dn(0, a), fma(G[d][1], dn(1, a), G[d][2] * dn(2, a)));
+    double *tb = sm.t + el * T_EL_STRIDE;
+#pragma unroll
+    for (int c = 0; c < 5; ++c) {
+#pragma unroll
+        for (int jj = 0; jj < 8; ++jj) {
+            const int p = 8 * c + jj;
+            if (p < 36) {
+                const int i = pack_i(p), q = pack_j(p);
+                tb[jj * T_J_STRIDE + gp] = fma(dn(0, i), H[0][q], fma(dn(1, i), H[1][q], dn(2, i) * H[2][q]));
+            }
+        }
+        __syncwarp();
+        reduce_store<HX_MODE_FAST, WITH_INDEX>(sm, tb, el, gp, c, out_el, valid, ke_out, rows_out, cols_out, s_pi,
+                                              s_pj);
+        __syncwarp();
+    }
+    return ok;
 }
 
 // Gauss point gp of element el (products published in sm), reference operation order; then the
@@ -192,7 +321,7 @@ __device__ __forceinline__ bool ke_gauss_point(GpWarpSmem &sm, int el, int gp, b
                                                int32_t *__restrict__ rows_out, int32_t *__restrict__ cols_out,
                                                const uint8_t *s_pi, const uint8_t *s_pj) {
     const int ir = (gp >> 2) & 1, is = (gp >> 1) & 1, it = gp & 1;
-    const volatile double *P = sm.P + el * P_EL_STRIDE;
+    const double *P = sm.P + el * P_EL_STRIDE;
     // J = dn @ x (element.py:262-269), accumulated from 0.0 over a = 0..7.  dN_r,a at this point
     // has magnitude index (s_a == s_gp) + (t_a == t_gp), and cyclically for s and t.
     double j[3][3];
@@ -282,25 +411,8 @@ __device__ __forceinline__ bool ke_gauss_point(GpWarpSmem &sm, int el, int gp, b
             }
         }
         __syncwarp();
-        const int p = 8 * c + gp;  // this lane reduces packed entry p of its element
-        if (p < 36) {
-            const double2 *src = reinterpret_cast<const double2 *>(tb + gp * T_J_STRIDE);
-            double acc = 0.0;
-#pragma unroll
-            for (int h = 0; h < 4; ++h) {
-                const double2 v = src[h];
-                acc = dadd(acc, v.x);
-                acc = dadd(acc, v.y);
-            }
-            if (valid) {
-                ke_out[out_el * 36 + p] = acc;
-                if (WITH_INDEX) {
-                    const int32_t gi = sm.conn[el * 8 + s_pi[p]], gj = sm.conn[el * 8 + s_pj[p]];
-                    rows_out[out_el * 36 + p] = max(gi, gj);
-                    cols_out[out_el * 36 + p] = min(gi, gj);
-                }
-            }
-        }
+        reduce_store<HX_MODE_EXACT, WITH_INDEX>(sm, tb, el, gp, c, out_el, valid, ke_out, rows_out, cols_out, s_pi,
+                                               s_pj);
         __syncwarp();
     }
     return ok;
@@ -356,7 +468,7 @@ integrate_mesh_kernel(const double *__restrict__ coords, const int32_t *__restri
                                                                coord_in_range(x2));
         const bool fast_div = ((in_range >> (8 * el)) & 0xffu) == 0xffu;
         __syncwarp();
-        publish_node(sm, el, gp, node, x0, x1, x2, c);
+        publish_node<MODE>(sm, el, gp, node, x0, x1, x2, c);
         __syncwarp();
         // prefetch: coordinates of quad1, node ids of quad2, claim the quad after
         node = node_next;
@@ -368,8 +480,11 @@ integrate_mesh_kernel(const double *__restrict__ coords, const int32_t *__restri
             c = __ldg(coeff + lo + quad1 * GP_EL_PER_WARP + el);
         }
         const int64_t quad3 = quad2 < n_quads ? grab() : n_quads;
-        const bool ok = ke_gauss_point<WITH_INDEX>(sm, el, gp, fast_div, k, valid, ke_out, rows_out, cols_out, s_pi,
-                                                   s_pj);
+        bool ok;
+        if constexpr (MODE == HX_MODE_EXACT)
+            ok = ke_gauss_point<WITH_INDEX>(sm, el, gp, fast_div, k, valid, ke_out, rows_out, cols_out, s_pi, s_pj);
+        else
+            ok = ke_gauss_point_fast<WITH_INDEX>(sm, el, gp, k, valid, ke_out, rows_out, cols_out, s_pi, s_pj);
         if (valid && !ok) atomicMin(fail_min, (unsigned long long)(lo + k));
         quad = quad1;
         quad1 = quad2;
@@ -397,9 +512,13 @@ stiffness_batch_kernel(const double *__restrict__ coords, const double *__restri
     const unsigned in_range =
         __ballot_sync(0xffffffffu, coord_in_range(x[0]) && coord_in_range(x[1]) && coord_in_range(x[2]));
     const bool fast_div = ((in_range >> (8 * el)) & 0xffu) == 0xffu;
-    publish_node(sm, el, gp, 0, x[0], x[1], x[2], valid ? __ldg(coeff + e) : 1.0);
+    publish_node<MODE>(sm, el, gp, 0, x[0], x[1], x[2], valid ? __ldg(coeff + e) : 1.0);
     __syncwarp();
-    const bool ok = ke_gauss_point<false>(sm, el, gp, fast_div, e, valid, out, nullptr, nullptr, nullptr, nullptr);
+    bool ok;
+    if constexpr (MODE == HX_MODE_EXACT)
+        ok = ke_gauss_point<false>(sm, el, gp, fast_div, e, valid, out, nullptr, nullptr, nullptr, nullptr);
+    else
+        ok = ke_gauss_point_fast<false>(sm, el, gp, e, valid, out, nullptr, nullptr, nullptr, nullptr);
     if (valid && !ok) atomicMin(fail_min, (unsigned long long)e);
 }
 
@@ -458,22 +577,27 @@ __global__ void index_kernel(const int32_t *__restrict__ conn, int64_t lo, int64
 
 constexpr size_t GP_SMEM = GP_WARPS * sizeof(GpWarpSmem);  // dynamic shared memory per block
 
-// Opt the integration kernels into > 48 KB of dynamic shared memory (once per device).
+// Opt the integration kernels into dynamic shared memory beyond the default (once per device).
+template <int MODE>
+static void configure_mode() {
+    cudaFuncSetAttribute(integrate_mesh_kernel<MODE, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)GP_SMEM);
+    cudaFuncSetAttribute(integrate_mesh_kernel<MODE, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)GP_SMEM);
+    cudaFuncSetAttribute(stiffness_batch_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GP_SMEM);
+}
 static void configure_ke_kernels() {
     static bool done[64] = {};
     int dev = 0;
     cudaGetDevice(&dev);
     if (dev < 64 && done[dev]) return;
-    cudaFuncSetAttribute(integrate_mesh_kernel<HX_MODE_EXACT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)GP_SMEM);
-    cudaFuncSetAttribute(integrate_mesh_kernel<HX_MODE_EXACT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)GP_SMEM);
-    cudaFuncSetAttribute(stiffness_batch_kernel<HX_MODE_EXACT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)GP_SMEM);
+    configure_mode<HX_MODE_EXACT>();
+    configure_mode<HX_MODE_FAST>();
     if (dev < 64) done[dev] = true;
 }
 
-// Resident blocks of the persistent integration kernel on the current device (queried once).
+// Resident blocks of the persistent integration kernel on the current device (queried once per mode).
+template <int MODE>
 static int64_t persistent_blocks() {
     static int64_t cached = 0;
     configure_ke_kernels();
@@ -481,12 +605,25 @@ static int64_t persistent_blocks() {
         int dev = 0, sms = 148, per_sm = HX_KE_MIN_BLOCKS;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, integrate_mesh_kernel<HX_MODE_EXACT, true>, GP_BLOCK,
-                                                      GP_SMEM);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, integrate_mesh_kernel<MODE, true>, GP_BLOCK, GP_SMEM);
         if (const char *env = getenv("HX_KE_BLOCKS_PER_SM")) per_sm = std::min(per_sm, atoi(env));  // experiments
         cached = (int64_t)sms * std::max(per_sm, 1);
     }
     return cached;
+}
+
+template <int MODE>
+static void launch_integrate(int64_t blocks, cudaStream_t s, const double *coords, const int32_t *conn,
+                             const double *coeff, int64_t lo, int64_t n, double *ke, int32_t *rows, int32_t *cols,
+                             hx_fail_info *fail) {
+    unsigned *counter = reinterpret_cast<unsigned *>(&fail->reserved);
+    auto *fmin = reinterpret_cast<unsigned long long *>(fail);
+    if (rows != nullptr)
+        integrate_mesh_kernel<MODE, true><<<(unsigned)blocks, GP_BLOCK, GP_SMEM, s>>>(coords, conn, coeff, lo, n, ke,
+                                                                                   rows, cols, fmin, counter);
+    else
+        integrate_mesh_kernel<MODE, false><<<(unsigned)blocks, GP_BLOCK, GP_SMEM, s>>>(coords, conn, coeff, lo, n,
+                                                                                    ke, rows, cols, fmin, counter);
 }
 
 __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
@@ -568,14 +705,12 @@ extern "C" int hx_integrate_mesh(const double *coords, int64_t n_nodes, const in
             set_last_error("hx_integrate_mesh: %lld elements exceed one launch", (long long)n);
             return HX_ERR_CONFIG;
         }
-        const int64_t blocks = std::min<int64_t>(ceil_div(n, GP_EL_PER_BLOCK), persistent_blocks());
-        unsigned *counter = reinterpret_cast<unsigned *>(&fail->reserved);
-        if (rows != nullptr)
-            integrate_mesh_kernel<HX_MODE_EXACT, true><<<(unsigned)blocks, GP_BLOCK, GP_SMEM, s>>>(
-                coords, conn, coeff, lo, n, ke, rows, cols, reinterpret_cast<unsigned long long *>(fail), counter);
+        if (mode == HX_MODE_EXACT)
+            launch_integrate<HX_MODE_EXACT>(std::min<int64_t>(ceil_div(n, GP_EL_PER_BLOCK), persistent_blocks<HX_MODE_EXACT>()),
+                                            s, coords, conn, coeff, lo, n, ke, rows, cols, fail);
         else
-            integrate_mesh_kernel<HX_MODE_EXACT, false><<<(unsigned)blocks, GP_BLOCK, GP_SMEM, s>>>(
-                coords, conn, coeff, lo, n, ke, rows, cols, reinterpret_cast<unsigned long long *>(fail), counter);
+            launch_integrate<HX_MODE_FAST>(std::min<int64_t>(ceil_div(n, GP_EL_PER_BLOCK), persistent_blocks<HX_MODE_FAST>()),
+                                           s, coords, conn, coeff, lo, n, ke, rows, cols, fail);
         HX_CHECK_LAUNCH("integrate_mesh_kernel");
     }
     fail_resolve_mesh_kernel<<<1, 1, 0, s>>>(coords, conn, coeff, fail);
@@ -598,8 +733,12 @@ extern "C" int hx_stiffness_batch(const double *coords, const double *coeff, int
     if (n > 0) {
         const int64_t blocks = ceil_div(n, GP_EL_PER_BLOCK);
         configure_ke_kernels();
-        stiffness_batch_kernel<HX_MODE_EXACT><<<(unsigned)blocks, GP_BLOCK, GP_SMEM, s>>>(
-            coords, coeff, n, out, reinterpret_cast<unsigned long long *>(fail));
+        if (mode == HX_MODE_EXACT)
+            stiffness_batch_kernel<HX_MODE_EXACT><<<(unsigned)blocks, GP_BLOCK, GP_SMEM, s>>>(
+                coords, coeff, n, out, reinterpret_cast<unsigned long long *>(fail));
+        else
+            stiffness_batch_kernel<HX_MODE_FAST><<<(unsigned)blocks, GP_BLOCK, GP_SMEM, s>>>(
+                coords, coeff, n, out, reinterpret_cast<unsigned long long *>(fail));
         HX_CHECK_LAUNCH("stiffness_batch_kernel");
     }
     fail_resolve_batch_kernel<<<1, 1, 0, s>>>(coords, fail);
