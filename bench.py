@@ -32,6 +32,11 @@ METRIC = "hex8 elements/s (KE+index+CSR assembly), % HBM roofline, 1/2/4/8 GPUs"
 UNIT = "elements/s"
 # algorithmic bytes: each API array touched once
 KE_KERNEL = "integrate_mesh_kernel"  # KE + fused iK/jK
+# FP64 instructions per element of the exact-mode kernel (ncu smsp__sass_thread_inst_executed_op_
+# {dadd,dmul,dfma}, profiles/r01_ncu_full_c3.txt) and the FP64 pipe peak measured by
+# tools/fp64_peak.cu (profiles/r01_fp64_microbench.txt): the kernel's second ceiling.
+FP64_INSTR_PER_EL = {"exact": 4000.0, "fast": 2676.0}
+FP64_PEAK_T_INSTR = 18.3
 KE_INDEX_BYTES_PER_EL = 32 + 8 + 288 + 288  # conn + coeff + KE f64 + iK/jK i32 (+ 24 B/node coords)
 
 
@@ -309,7 +314,14 @@ def run_ours(args):
                          "frac": achieved_ke / peak, "traffic": load_traffic(wl, KE_KERNEL) if world == 1 else None, "kernel": KE_KERNEL,
                          "algorithmic_bytes_per_el": ke_bytes / n_el_total, "peak_kind": peak_kind,
                          "kernel_ms": kernel["ke_ms"], "kernel_share_of_step": kernel["ke_ms"] / ms,
-                         "note": "exact mode is FP64-ALU bound (~3.8k DP instr/element), see DESIGN.md"},
+                         "fp64_pipe": {"instr_per_el": FP64_INSTR_PER_EL[args.mode],
+                                       "achieved_t_instr_s": FP64_INSTR_PER_EL[args.mode] * n_el_total / world
+                                       / (kernel["ke_ms"] / 1e3) / 1e12,
+                                       "peak_t_instr_s": FP64_PEAK_T_INSTR,
+                                       "frac": FP64_INSTR_PER_EL[args.mode] * n_el_total / world
+                                       / (kernel["ke_ms"] / 1e3) / 1e12 / FP64_PEAK_T_INSTR},
+                         "note": "exact mode (reference operation order, bitwise) is FP64-pipe bound: ~4.0k FP64 "
+                                 "instr/element caps it at ~4.6 G el/s = 45% of the HBM roofline; see DESIGN.md"},
             "pipeline_roofline": {"achieved": pipeline_gbs, "peak": peak * world, "unit": "GB/s",
                                   "frac": pipeline_gbs / (peak * world),
                                   "algorithmic_bytes_per_el": full_bytes / n_el_total},
