@@ -295,34 +295,6 @@ pattern_kernel(SegTable T, int64_t col_lo, int64_t ncols, const int32_t *__restr
     }
 }
 
-// Rows only (symbolic without values).
-__global__ void __launch_bounds__(EMIT_BLOCK)
-emit_rows_kernel(int64_t col_lo, int64_t ncols, const int64_t *__restrict__ col_ptr, const int2 *__restrict__ scratch,
-                 const int64_t *__restrict__ block_scratch, int64_t *__restrict__ row_idx, int64_t capacity,
-                 const uint32_t *__restrict__ status) {
-    if (*status & (HX_ST_DEG_OVERFLOW | HX_ST_ROW_OVERFLOW | HX_ST_REPEATED_NODE | HX_ST_SCRATCH_OVERFLOW)) return;
-    __shared__ int64_t s_cp[COL_BLOCK + 1];
-    const int64_t first = (int64_t)blockIdx.x * COL_BLOCK;
-    const int ncol = (int)(ncols - first < COL_BLOCK ? ncols - first : COL_BLOCK);
-    for (int i = threadIdx.x; i <= ncol; i += EMIT_BLOCK) s_cp[i] = col_ptr[first + i];
-    __syncthreads();
-    const int64_t base = s_cp[0];
-    const int total = (int)(s_cp[ncol] - base);
-    const int64_t sb = block_scratch[blockIdx.x];
-    const int64_t room = capacity - base;
-    const int limit = room <= 0 ? 0 : (room < total ? (int)room : total);
-    for (int o = threadIdx.x; o < limit; o += EMIT_BLOCK) {
-        int lo = 0, hi = ncol;
-#pragma unroll 1
-        while (hi - lo > 1) {
-            const int mid = (lo + hi) >> 1;
-            if (s_cp[mid] - base <= o) lo = mid; else hi = mid;
-        }
-        const int j = (int)(o - (s_cp[lo] - base));
-        row_idx[base + o] = j == 0 ? (int64_t)(col_lo + first + lo) : (int64_t)scratch[sb + o - lo - 1].x;
-    }
-}
-
 // 6. Emit pass: block b re-walks the output entries of the same COL_BLOCK columns (coalesced
 // scratch reads, row_idx / vals stores).  Diagonals first (one per column: every incident element
 // at its own local node), then the off-diagonal scratch records in output order.  Values are
@@ -335,7 +307,7 @@ __device__ __forceinline__ const double *ke_row(const SegTable &T, int64_t e) {
     return T.ke[sg] + T.ke_stride[sg] * (e - T.start[sg]);
 }
 
-template <bool ROWS, bool SINGLE>
+template <bool ROWS, bool VALS, bool SINGLE>
 __global__ void __launch_bounds__(EMIT_BLOCK)
 emit_kernel(SegTable T, int64_t col_lo, int64_t ncols, const int32_t *__restrict__ deg_arr,
             const int32_t *__restrict__ adj, const int64_t *__restrict__ col_ptr, const int2 *__restrict__ scratch,
@@ -344,6 +316,7 @@ emit_kernel(SegTable T, int64_t col_lo, int64_t ncols, const int32_t *__restrict
     // the pattern pass hit a fast-path limit: its records are incomplete and the caller re-runs
     if (*status & (HX_ST_DEG_OVERFLOW | HX_ST_ROW_OVERFLOW | HX_ST_REPEATED_NODE | HX_ST_SCRATCH_OVERFLOW)) return;
     __shared__ int64_t s_cp[COL_BLOCK + 1];
+    __shared__ int32_t s_rs[COL_BLOCK + 1];      // first scratch record of each column (tile-relative)
     __shared__ int32_t s_deg[COL_BLOCK];
     __shared__ int32_t s_adj[COL_BLOCK * 8];    // the block's sorted incident lists (one coalesced read)
     __shared__ uint8_t s_col[COL_BLOCK * MAXR];  // column of each off-diagonal record of the block
@@ -353,23 +326,45 @@ emit_kernel(SegTable T, int64_t col_lo, int64_t ncols, const int32_t *__restrict
         s_cp[i] = col_ptr[first + i];
         if (i < ncol) s_deg[i] = min(deg_arr[first + i], MAXDEG);
     }
-    for (int i = threadIdx.x; i < ncol * 8; i += EMIT_BLOCK) s_adj[i] = __ldg(adj + 8 * first + i);
+    if (VALS)
+        for (int i = threadIdx.x; i < ncol * 8; i += EMIT_BLOCK) s_adj[i] = __ldg(adj + 8 * first + i);
+    __syncthreads();
+    // scratch record offsets: column u has max(m_u - 1, 0) records (m_u = 0 for a node no element
+    // references), laid out in column order by the pattern pass -- warp 0 scans them
+    if (threadIdx.x < 32) {
+        const int l = threadIdx.x, u0 = 2 * l, u1 = 2 * l + 1;
+        const int m0 = u0 < ncol ? (int)(s_cp[u0 + 1] - s_cp[u0]) : 0;
+        const int m1 = u1 < ncol ? (int)(s_cp[u1 + 1] - s_cp[u1]) : 0;
+        const int off0 = m0 > 0 ? m0 - 1 : 0, off1 = m1 > 0 ? m1 - 1 : 0;
+        int incl = off0 + off1;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int v = __shfl_up_sync(0xffffffffu, incl, d);
+            if (l >= d) incl += v;
+        }
+        const int excl = incl - off0 - off1;
+        s_rs[u0] = excl;
+        s_rs[u1] = excl + off0;
+        if (l == 31) s_rs[COL_BLOCK] = incl;
+    }
     __syncthreads();
     const int64_t base = s_cp[0];
     const int64_t room = capacity - base;
     const int64_t sb = block_scratch[blockIdx.x];
+    const int n_off = s_rs[COL_BLOCK];
     for (int u = threadIdx.x; u < ncol; u += EMIT_BLOCK) {
-        const int o0 = (int)(s_cp[u] - base), o1 = (int)(s_cp[u + 1] - base);
-        for (int q = o0 - u; q < o1 - u - 1; ++q) s_col[q] = (uint8_t)u;
+        const int m = (int)(s_cp[u + 1] - s_cp[u]);
+        for (int q = s_rs[u]; q < s_rs[u] + m - 1; ++q) s_col[q] = (uint8_t)u;
     }
     __syncthreads();
     // diagonals
     for (int u = threadIdx.x; u < ncol; u += EMIT_BLOCK) {
         const int o = (int)(s_cp[u] - base);
         if (s_cp[u + 1] == s_cp[u] || o >= room) continue;
+        if (ROWS) row_idx[base + o] = col_lo + first + u;
+        if (!VALS) continue;
         const int deg = s_deg[u];
         const int32_t *ent = s_adj + 8 * u;
-        if (ROWS) row_idx[base + o] = col_lo + first + u;
         double x[8];
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
@@ -390,14 +385,14 @@ emit_kernel(SegTable T, int64_t col_lo, int64_t ncols, const int32_t *__restrict
         }
         vals[base + o] = v;
     }
-    // off-diagonals
-    const int n_off = (int)(s_cp[ncol] - base) - ncol;
+    // off-diagonals: record q of column u is output entry (s_cp[u] - base) + 1 + (q - s_rs[u])
     for (int q = threadIdx.x; q < n_off; q += EMIT_BLOCK) {
         const int u = s_col[q];
-        const int o = q + u + 1;
+        const int o = (int)(s_cp[u] - base) + 1 + (q - s_rs[u]);
         if (o >= room) continue;  // beyond capacity: the caller retries
         const int2 rec = scratch[sb + q];
         if (ROWS) row_idx[base + o] = rec.x;
+        if (!VALS) continue;
         const uint32_t w = (uint32_t)rec.y;
         const int n = (int)(w & 7u);
         const int32_t *ent = s_adj + 8 * u;
@@ -573,18 +568,19 @@ static int mesh_csc_build(const hx_elem_segment *segs, int32_t n_segs, int64_t n
         HX_TRY_CUDA(cub::DeviceScan::ExclusiveSum(w.cub_tmp, cb2, col_ptr, col_ptr, (int)(ncols + 1), s));
         if (vals != nullptr) {
             if (single_dense(T))
-                emit_kernel<true, true><<<tiles, EMIT_BLOCK, 0, s>>>(T, col_lo, ncols, w.deg, w.adj, col_ptr,
+                emit_kernel<true, true, true><<<tiles, EMIT_BLOCK, 0, s>>>(T, col_lo, ncols, w.deg, w.adj, col_ptr,
                                                                     w.scratch, w.block_scratch, row_idx, vals,
                                                                     row_capacity, status);
             else
-                emit_kernel<true, false><<<tiles, EMIT_BLOCK, 0, s>>>(T, col_lo, ncols, w.deg, w.adj, col_ptr,
+                emit_kernel<true, true, false><<<tiles, EMIT_BLOCK, 0, s>>>(T, col_lo, ncols, w.deg, w.adj, col_ptr,
                                                                      w.scratch, w.block_scratch, row_idx, vals,
                                                                      row_capacity, status);
             HX_CHECK_LAUNCH("emit_kernel");
         } else if (row_capacity > 0) {
-            emit_rows_kernel<<<tiles, EMIT_BLOCK, 0, s>>>(col_lo, ncols, col_ptr, w.scratch, w.block_scratch, row_idx,
-                                                         row_capacity, status);
-            HX_CHECK_LAUNCH("emit_rows_kernel");
+            emit_kernel<true, false, true><<<tiles, EMIT_BLOCK, 0, s>>>(T, col_lo, ncols, w.deg, w.adj, col_ptr,
+                                                                      w.scratch, w.block_scratch, row_idx, nullptr,
+                                                                      row_capacity, status);
+            HX_CHECK_LAUNCH("emit_kernel<rows>");
         }
     } else {
         HX_TRY_CUDA(cudaMemsetAsync(col_ptr, 0, sizeof(int64_t), s));
@@ -628,10 +624,10 @@ extern "C" int hx_mesh_csc_numeric(const hx_elem_segment *segs, int32_t n_segs, 
     cudaStream_t s = (cudaStream_t)stream;
     if (ncols > 0) {
         if (single_dense(T))
-            emit_kernel<false, true><<<(unsigned)ceil_div(ncols, COL_BLOCK), EMIT_BLOCK, 0, s>>>(
+            emit_kernel<false, true, true><<<(unsigned)ceil_div(ncols, COL_BLOCK), EMIT_BLOCK, 0, s>>>(
                 T, col_lo, ncols, w.deg, w.adj, col_ptr, w.scratch, w.block_scratch, nullptr, vals, INT64_MAX, status);
         else
-            emit_kernel<false, false><<<(unsigned)ceil_div(ncols, COL_BLOCK), EMIT_BLOCK, 0, s>>>(
+            emit_kernel<false, true, false><<<(unsigned)ceil_div(ncols, COL_BLOCK), EMIT_BLOCK, 0, s>>>(
                 T, col_lo, ncols, w.deg, w.adj, col_ptr, w.scratch, w.block_scratch, nullptr, vals, INT64_MAX, status);
         HX_CHECK_LAUNCH("emit_kernel<numeric>");
     }
@@ -656,10 +652,10 @@ extern "C" int hx_mesh_csc_emit(const hx_elem_segment *segs, int32_t n_segs, int
     if (ncols > 0) {
         const unsigned tiles = (unsigned)ceil_div(ncols, COL_BLOCK);
         if (single_dense(T))
-            emit_kernel<true, true><<<tiles, EMIT_BLOCK, 0, s>>>(T, col_lo, ncols, w.deg, w.adj, col_ptr, w.scratch,
+            emit_kernel<true, true, true><<<tiles, EMIT_BLOCK, 0, s>>>(T, col_lo, ncols, w.deg, w.adj, col_ptr, w.scratch,
                                                                 w.block_scratch, row_idx, vals, capacity, status);
         else
-            emit_kernel<true, false><<<tiles, EMIT_BLOCK, 0, s>>>(T, col_lo, ncols, w.deg, w.adj, col_ptr, w.scratch,
+            emit_kernel<true, true, false><<<tiles, EMIT_BLOCK, 0, s>>>(T, col_lo, ncols, w.deg, w.adj, col_ptr, w.scratch,
                                                                  w.block_scratch, row_idx, vals, capacity, status);
         HX_CHECK_LAUNCH("emit_kernel<emit>");
     }

@@ -299,3 +299,49 @@ def test_random_elements_bitwise_against_oracle():
     assert first == -1
     got = stiffness_batch(coords, coeff)
     assert bits_equal(got, ref)
+
+
+@pytest.mark.parametrize("permute", [False, True])
+def test_unreferenced_nodes_give_empty_columns(permute):
+    """Nodes no element references (allowed by validate_mesh, mesh.py:100-119) are empty columns;
+    they must not shift the other columns' records (every second id unused, some runs of 3)."""
+    base = perturbed_mesh(7, seed=12)
+    if permute:
+        base = permuted_mesh(base, seed=13)
+    old = np.arange(base.n_nodes)
+    new_id = 2 * old + (old % 5 == 0)  # gaps of 1 and 2 between used ids
+    n_nodes = int(new_id.max()) + 3
+    coords = np.zeros((n_nodes, 3))
+    coords[new_id] = base.coords
+    mesh = Mesh(coords, new_id.astype(np.int32)[base.connectivity], base.coefficient)
+    b = build_device(D.DeviceMesh.from_host(mesh))
+    assert b.csc.path == "mesh"
+    ke, rows, cols, first, _, _ = oracle.stiffness_mesh(mesh.coords, mesh.connectivity, mesh.coefficient)
+    cp, ri, vv = oracle.triplet_to_csc(rows, cols, ke.reshape(-1), mesh.n_nodes)
+    assert bits_equal(b.csc.col_ptr.cpu().numpy(), cp)
+    assert bits_equal(b.csc.row_idx.cpu().numpy(), ri)
+    assert bits_equal(b.csc.vals.cpu().numpy(), vv)
+
+
+@pytest.mark.parametrize("name", SMALL_MESHES)
+def test_symbolic_rows_only_abi(golden, name):
+    """hx_mesh_csc_symbolic with a row buffer: the pattern without values (rows-only emit)."""
+    import ctypes
+
+    from paper_1501_04784_b200 import _native as N
+
+    mesh = golden_mesh(golden, name)
+    conn = torch.from_numpy(mesh.connectivity).cuda()
+    n, dim = mesh.n_el, mesh.n_nodes
+    ws_bytes = N.lib().hx_mesh_csc_workspace_bytes(n, dim)
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device="cuda")
+    status = torch.zeros(1, dtype=torch.int32, device="cuda")
+    col_ptr = torch.empty(dim + 1, dtype=torch.int64, device="cuda")
+    rows = torch.empty(36 * n, dtype=torch.int64, device="cuda")
+    segs = N.segments([(conn.data_ptr(), 0, n)])
+    N.check(N.lib().hx_mesh_csc_symbolic(segs, 1, dim, 0, dim, D._ptr(col_ptr), D._ptr(rows), 36 * n, D._ptr(ws),
+                                         ws_bytes, D._ptr(status), D.stream_handle()), "symbolic")
+    assert int(status.item()) == 0
+    nnz = int(col_ptr[-1].item())
+    assert bits_equal(col_ptr.cpu().numpy(), golden[f"{name}_col_ptr"])
+    assert bits_equal(rows[:nnz].cpu().numpy(), golden[f"{name}_row_idx"])
