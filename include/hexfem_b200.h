@@ -58,6 +58,12 @@ extern "C" {
 #define HX_MAX_NODE_DEGREE 8
 #define HX_MAX_COL_ROWS 32
 
+/* Flags of the mesh-path assembly (hx_mesh_csc_symbolic / hx_mesh_csc_build). */
+#define HX_CSC_ORDER_BY_ELEMENT 1 /* process columns in order of their lowest incident element (one pair
+                                   * sort): for numberings without locality (e.g. randomly permuted
+                                   * node ids) the pattern and emit passes then gather nearby
+                                   * elements; results are identical either way */
+
 /* Integration modes. */
 #define HX_MODE_EXACT 0 /* reference operation order, no FMA: bitwise equal to the reference */
 #define HX_MODE_FAST 1  /* FMA + restructured algebra: |d| <= 1e-12 * max|row| (documented)  */
@@ -129,12 +135,12 @@ int64_t hx_mesh_csc_workspace_bytes(int64_t n_el_total, int64_t n_cols);
 int hx_mesh_csc_symbolic(const hx_elem_segment *segs, int32_t n_segs, int64_t n_nodes,
                          int64_t col_lo, int64_t col_hi, int64_t *col_ptr, int64_t *row_idx,
                          int64_t row_capacity, void *workspace, int64_t workspace_bytes,
-                         uint32_t *status, void *stream);
+                         uint32_t *status, int32_t flags, void *stream);
 /* symbolic + numeric in one pass (the cold build): col_ptr, row_idx and vals, the latter two for
  * the first `capacity` entries (re-run with capacity >= nnz when short). */
 int hx_mesh_csc_build(const hx_elem_segment *segs, int32_t n_segs, int64_t n_nodes, int64_t col_lo,
                       int64_t col_hi, int64_t *col_ptr, int64_t *row_idx, double *vals, int64_t capacity,
-                      void *workspace, int64_t workspace_bytes, uint32_t *status, void *stream);
+                      void *workspace, int64_t workspace_bytes, uint32_t *status, int32_t flags, void *stream);
 /* Symbolic with row_capacity = 0 only plans (col_ptr + workspace, no row_idx); hx_mesh_csc_emit
  * then writes row_idx and vals (first `capacity` entries) in one pass -- the split lets the plan run
  * on a second stream concurrently with the integration kernel. */

@@ -22,6 +22,7 @@ HX_OK, HX_ERR_VALUE, HX_ERR_CONFIG, HX_ERR_CUDA, HX_ERR_WORKSPACE = 0, 1, 2, 3, 
 ST_DEG_OVERFLOW, ST_ROW_OVERFLOW, ST_REPEATED_NODE, ST_BAD_INDEX, ST_UPPER, ST_SCRATCH = 1, 2, 4, 8, 16, 32
 ST_FASTPATH_LIMITS = ST_DEG_OVERFLOW | ST_ROW_OVERFLOW | ST_REPEATED_NODE | ST_SCRATCH
 MODE_EXACT, MODE_FAST = 0, 1
+CSC_ORDER_BY_ELEMENT = 1
 MAX_SEGMENTS = 4
 
 # Every symbol declared in include/hexfem_b200.h (checked by tests/test_abi_cpu.py).
@@ -74,8 +75,8 @@ def lib():
         "hx_integrate_mesh": ([P, I64, P, P, I64, I64, P, P, P, I32, P, P], ctypes.c_int),
         "hx_connectivity_index_arrays": ([P, I64, I64, P, P, P], ctypes.c_int),
         "hx_mesh_csc_workspace_bytes": ([I64, I64], I64),
-        "hx_mesh_csc_symbolic": ([P, I32, I64, I64, I64, P, P, I64, P, I64, P, P], ctypes.c_int),
-        "hx_mesh_csc_build": ([P, I32, I64, I64, I64, P, P, P, I64, P, I64, P, P], ctypes.c_int),
+        "hx_mesh_csc_symbolic": ([P, I32, I64, I64, I64, P, P, I64, P, I64, P, I32, P], ctypes.c_int),
+        "hx_mesh_csc_build": ([P, I32, I64, I64, I64, P, P, P, I64, P, I64, P, I32, P], ctypes.c_int),
         "hx_mesh_csc_numeric": ([P, I32, I64, I64, P, P, P, P, P, P], ctypes.c_int),
         "hx_mesh_csc_emit": ([P, I32, I64, I64, P, P, P, I64, P, P, P], ctypes.c_int),
         "hx_triplet_csc_workspace_bytes": ([I64, I64], I64),

@@ -23,9 +23,11 @@
 // every duplicate run has <= 8 terms, where numpy's pairwise sum degenerates to the sequential sum
 // implemented here.
 #include <cub/block/block_scan.cuh>
+#include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
 #include <algorithm>
+#include <type_traits>
 
 #include "hx_common.cuh"
 
@@ -51,6 +53,14 @@ __device__ __forceinline__ int seg_of(const SegTable &T, int64_t e) {
     return s;
 }
 
+// Element e's connectivity row; SINGLE: one dense segment (the single-GPU build).
+template <bool SINGLE>
+__device__ __forceinline__ const int32_t *conn_row(const SegTable &T, int64_t e) {
+    if (SINGLE) return T.conn[0] + 8 * e;
+    const int sg = seg_of(T, e);
+    return T.conn[sg] + (e - T.start[sg]) * T.conn_stride[sg];
+}
+
 __device__ __forceinline__ void load_conn8(const int32_t *__restrict__ conn, int64_t e, int64_t stride,
                                            int32_t (&g)[8]) {
     const int4 *c4 = reinterpret_cast<const int4 *>(conn + e * stride);
@@ -62,14 +72,14 @@ __device__ __forceinline__ void load_conn8(const int32_t *__restrict__ conn, int
 // 1. adjacency: one thread per (element, local node); also validates node ids against [0, n_nodes).
 // adj[(v - col_lo) * 8 + slot] = (combined element index << 3) | local node, slot from an atomic
 // counter (slot order is arbitrary: the pattern pass sorts each node's list by element).
+template <bool SINGLE>
 __global__ void adjacency_kernel(SegTable T, int64_t n_total, int64_t n_nodes, int64_t col_lo, int64_t col_hi,
                                  int32_t *__restrict__ deg, int32_t *__restrict__ adj, uint32_t *__restrict__ status) {
     for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < 8 * n_total;
          w += (int64_t)gridDim.x * blockDim.x) {
         const int64_t e = w >> 3;
         const int a = (int)(w & 7);
-        const int s = seg_of(T, e);
-        const int32_t v = __ldg(T.conn[s] + (e - T.start[s]) * T.conn_stride[s] + a);
+        const int32_t v = __ldg(conn_row<SINGLE>(T, e) + a);
         if (v < 0 || (int64_t)v >= n_nodes) {
             atomicOr(status, HX_ST_BAD_INDEX);
             continue;
@@ -80,6 +90,21 @@ __global__ void adjacency_kernel(SegTable T, int64_t n_total, int64_t n_nodes, i
             if (slot < MAXDEG) adj[8 * c + slot] = (int32_t)((e << 3) | a);
             else atomicOr(status, HX_ST_DEG_OVERFLOW);
         }
+    }
+}
+
+// Column processing order for non-local numberings (HX_CSC_ORDER_BY_ELEMENT): key = the column's
+// lowest incident element (its adjacency slots), value = the column; sorting the pairs makes
+// consecutive pattern/emit threads work on nearby elements (connectivity rows and KE values stay in
+// L1/L2 instead of being gathered from random elements).
+__global__ void first_element_kernel(int64_t ncols, const int32_t *__restrict__ deg, const int32_t *__restrict__ adj,
+                                     uint32_t empty_key, uint32_t *__restrict__ keys, uint32_t *__restrict__ cols) {
+    for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < ncols; c += (int64_t)gridDim.x * blockDim.x) {
+        const int d = min(__ldg(deg + c), MAXDEG);
+        uint32_t k = empty_key;
+        for (int j = 0; j < d; ++j) k = min(k, (uint32_t)(__ldg(adj + 8 * c + j) >> 3));
+        keys[c] = k;
+        cols[c] = (uint32_t)c;
     }
 }
 
@@ -182,12 +207,13 @@ __device__ __forceinline__ uint32_t hash_slot(int32_t v) { return ((uint32_t)v *
 //   - m = 1 + distinct rows -> col_ptr[cl] (the exclusive scan turns counts into offsets);
 //   - sorted off-diagonal records (row, word) -> a compact scratch region reserved per block with
 //     one atomic (every block records where its records start).
-template <typename K>
+template <typename K, bool SINGLE>
 __global__ void __launch_bounds__(COL_BLOCK)
 pattern_kernel(SegTable T, int64_t col_lo, int64_t ncols, const int32_t *__restrict__ deg_arr,
                int32_t *__restrict__ adj, int64_t *__restrict__ col_ptr, int2 *__restrict__ scratch,
                int64_t scratch_capacity, unsigned long long *__restrict__ scratch_top,
-               int64_t *__restrict__ block_scratch, uint32_t *__restrict__ status) {
+               int64_t *__restrict__ block_scratch, uint32_t *__restrict__ status,
+               const uint32_t *__restrict__ order) {
     __shared__ int32_t sH[MAXR * COL_BLOCK];   // hash keys
     __shared__ uint32_t sW[MAXR * COL_BLOCK];  // contribution words, by hash slot
     // compacted / sorted keys (row << 5 | slot): 32-bit keys reuse the hash-key array in place
@@ -196,7 +222,8 @@ pattern_kernel(SegTable T, int64_t col_lo, int64_t ncols, const int32_t *__restr
     using BlockScan = cub::BlockScan<int32_t, COL_BLOCK>;
     __shared__ typename BlockScan::TempStorage scan_tmp;
     const int t = threadIdx.x;
-    const int64_t cl = (int64_t)blockIdx.x * COL_BLOCK + t;
+    const int64_t idx = (int64_t)blockIdx.x * COL_BLOCK + t;  // position in the processing order
+    const int64_t cl = order != nullptr && idx < ncols ? (int64_t)__ldg(order + idx) : idx;
     const int32_t c = (int32_t)(col_lo + cl);
     int32_t *H = sH + t;
     uint32_t *W = sW + t;
@@ -213,18 +240,16 @@ pattern_kernel(SegTable T, int64_t col_lo, int64_t ncols, const int32_t *__restr
     }
     if (deg > 0) {
 #pragma unroll
-        for (int q = 0; q < MAXR; ++q) {
-            H[q * COL_BLOCK] = HASH_EMPTY;
-            W[q * COL_BLOCK] = 0u;
-        }
+        for (int q = 0; q < MAXR; ++q) H[q * COL_BLOCK] = HASH_EMPTY;  // W[slot] is written on first insert
         // all incident connectivity rows in flight at once (memory-level parallelism)
         int32_t g[8][8];
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
             if (k < deg) {
-                const int64_t e = ent[k] >> 3;
-                const int sg = seg_of(T, e);
-                load_conn8(T.conn[sg], e - T.start[sg], T.conn_stride[sg], g[k]);
+                const int4 *c4 = reinterpret_cast<const int4 *>(conn_row<SINGLE>(T, ent[k] >> 3));
+                const int4 lo = __ldg(c4), hi = __ldg(c4 + 1);
+                g[k][0] = lo.x; g[k][1] = lo.y; g[k][2] = lo.z; g[k][3] = lo.w;
+                g[k][4] = hi.x; g[k][5] = hi.y; g[k][6] = hi.z; g[k][7] = hi.w;
             } else {
 #pragma unroll
                 for (int b = 0; b < 8; ++b) g[k][b] = INT32_MIN;  // never a row (< c)
@@ -249,7 +274,7 @@ pattern_kernel(SegTable T, int64_t col_lo, int64_t ncols, const int32_t *__restr
                     continue;
                 }
                 H[h * COL_BLOCK] = v;
-                const uint32_t w = W[h * COL_BLOCK];
+                const uint32_t w = cur == HASH_EMPTY ? 0u : W[h * COL_BLOCK];
                 const uint32_t n = w & 7u;
                 if (n == MAX_OFFDIAG_CONTRIB) ok = false;
                 else W[h * COL_BLOCK] = (w + 1u) | ((uint32_t)(k << 3 | b) << (3 + 6 * n));
@@ -312,29 +337,37 @@ __global__ void __launch_bounds__(EMIT_BLOCK)
 emit_kernel(SegTable T, int64_t col_lo, int64_t ncols, const int32_t *__restrict__ deg_arr,
             const int32_t *__restrict__ adj, const int64_t *__restrict__ col_ptr, const int2 *__restrict__ scratch,
             const int64_t *__restrict__ block_scratch, int64_t *__restrict__ row_idx, double *__restrict__ vals,
-            int64_t capacity, const uint32_t *__restrict__ status) {
+            int64_t capacity, const uint32_t *__restrict__ status, const uint32_t *__restrict__ order_flag,
+            const uint32_t *__restrict__ order) {
     // the pattern pass hit a fast-path limit: its records are incomplete and the caller re-runs
     if (*status & (HX_ST_DEG_OVERFLOW | HX_ST_ROW_OVERFLOW | HX_ST_REPEATED_NODE | HX_ST_SCRATCH_OVERFLOW)) return;
-    __shared__ int64_t s_cp[COL_BLOCK + 1];
+    const bool ordered = *order_flag != 0u;
+    __shared__ int64_t s_start[COL_BLOCK];       // first output entry of each column of the tile
+    __shared__ int32_t s_m[COL_BLOCK + 1];       // entries per column
+    __shared__ int32_t s_cl[COL_BLOCK];          // column (block-local index) of each tile position
     __shared__ int32_t s_rs[COL_BLOCK + 1];      // first scratch record of each column (tile-relative)
     __shared__ int32_t s_deg[COL_BLOCK];
-    __shared__ int32_t s_adj[COL_BLOCK * 8];    // the block's sorted incident lists (one coalesced read)
-    __shared__ uint8_t s_col[COL_BLOCK * MAXR];  // column of each off-diagonal record of the block
+    __shared__ int32_t s_adj[COL_BLOCK * 8];     // the tile's sorted incident lists
+    __shared__ uint8_t s_col[COL_BLOCK * MAXR];  // tile position of each off-diagonal record
     const int64_t first = (int64_t)blockIdx.x * COL_BLOCK;
     const int ncol = (int)(ncols - first < COL_BLOCK ? ncols - first : COL_BLOCK);
-    for (int i = threadIdx.x; i <= ncol; i += EMIT_BLOCK) {
-        s_cp[i] = col_ptr[first + i];
-        if (i < ncol) s_deg[i] = min(deg_arr[first + i], MAXDEG);
+    for (int u = threadIdx.x; u < ncol; u += EMIT_BLOCK) {
+        const int64_t cl = ordered ? (int64_t)__ldg(order + first + u) : first + u;
+        s_cl[u] = (int32_t)cl;
+        const int64_t a = col_ptr[cl], b = col_ptr[cl + 1];
+        s_start[u] = a;
+        s_m[u] = (int)(b - a);
+        s_deg[u] = min(deg_arr[cl], MAXDEG);
     }
-    if (VALS)
-        for (int i = threadIdx.x; i < ncol * 8; i += EMIT_BLOCK) s_adj[i] = __ldg(adj + 8 * first + i);
     __syncthreads();
+    if (VALS)
+        for (int i = threadIdx.x; i < ncol * 8; i += EMIT_BLOCK)
+            s_adj[i] = __ldg(adj + 8 * (int64_t)s_cl[i >> 3] + (i & 7));
     // scratch record offsets: column u has max(m_u - 1, 0) records (m_u = 0 for a node no element
-    // references), laid out in column order by the pattern pass -- warp 0 scans them
+    // references), laid out in tile order by the pattern pass -- warp 0 scans them
     if (threadIdx.x < 32) {
         const int l = threadIdx.x, u0 = 2 * l, u1 = 2 * l + 1;
-        const int m0 = u0 < ncol ? (int)(s_cp[u0 + 1] - s_cp[u0]) : 0;
-        const int m1 = u1 < ncol ? (int)(s_cp[u1 + 1] - s_cp[u1]) : 0;
+        const int m0 = u0 < ncol ? s_m[u0] : 0, m1 = u1 < ncol ? s_m[u1] : 0;
         const int off0 = m0 > 0 ? m0 - 1 : 0, off1 = m1 > 0 ? m1 - 1 : 0;
         int incl = off0 + off1;
 #pragma unroll
@@ -348,20 +381,16 @@ emit_kernel(SegTable T, int64_t col_lo, int64_t ncols, const int32_t *__restrict
         if (l == 31) s_rs[COL_BLOCK] = incl;
     }
     __syncthreads();
-    const int64_t base = s_cp[0];
-    const int64_t room = capacity - base;
     const int64_t sb = block_scratch[blockIdx.x];
     const int n_off = s_rs[COL_BLOCK];
-    for (int u = threadIdx.x; u < ncol; u += EMIT_BLOCK) {
-        const int m = (int)(s_cp[u + 1] - s_cp[u]);
-        for (int q = s_rs[u]; q < s_rs[u] + m - 1; ++q) s_col[q] = (uint8_t)u;
-    }
+    for (int u = threadIdx.x; u < ncol; u += EMIT_BLOCK)
+        for (int q = s_rs[u]; q < s_rs[u] + s_m[u] - 1; ++q) s_col[q] = (uint8_t)u;
     __syncthreads();
     // diagonals
     for (int u = threadIdx.x; u < ncol; u += EMIT_BLOCK) {
-        const int o = (int)(s_cp[u] - base);
-        if (s_cp[u + 1] == s_cp[u] || o >= room) continue;
-        if (ROWS) row_idx[base + o] = col_lo + first + u;
+        const int64_t o = s_start[u];
+        if (s_m[u] == 0 || o >= capacity) continue;
+        if (ROWS) row_idx[o] = col_lo + s_cl[u];
         if (!VALS) continue;
         const int deg = s_deg[u];
         const int32_t *ent = s_adj + 8 * u;
@@ -383,15 +412,15 @@ emit_kernel(SegTable T, int64_t col_lo, int64_t ncols, const int32_t *__restrict
                 if (k < deg) sum = __dadd_rn(sum, x[k]);
             v = __dadd_rn(x[0], sum);
         }
-        vals[base + o] = v;
+        vals[o] = v;
     }
-    // off-diagonals: record q of column u is output entry (s_cp[u] - base) + 1 + (q - s_rs[u])
+    // off-diagonals: record q of tile position u is output entry s_start[u] + 1 + (q - s_rs[u])
     for (int q = threadIdx.x; q < n_off; q += EMIT_BLOCK) {
         const int u = s_col[q];
-        const int o = (int)(s_cp[u] - base) + 1 + (q - s_rs[u]);
-        if (o >= room) continue;  // beyond capacity: the caller retries
+        const int64_t o = s_start[u] + 1 + (q - s_rs[u]);
+        if (o >= capacity) continue;  // beyond capacity: the caller retries
         const int2 rec = scratch[sb + q];
-        if (ROWS) row_idx[base + o] = rec.x;
+        if (ROWS) row_idx[o] = rec.x;
         if (!VALS) continue;
         const uint32_t w = (uint32_t)rec.y;
         const int n = (int)(w & 7u);
@@ -415,20 +444,23 @@ emit_kernel(SegTable T, int64_t col_lo, int64_t ncols, const int32_t *__restrict
                 if (r < n) sum = __dadd_rn(sum, x[r]);
             v = __dadd_rn(x[0], sum);
         }
-        vals[base + o] = v;
+        vals[o] = v;
     }
 }
 
 // Workspace layout (all offsets 256-B aligned):
-//   deg (ncols) i32 | adj (8*ncols) i32 | block_scratch (blocks) i64 | scratch_top u64 | cub temp |
+//   order_flag u32 | deg (ncols) i32 | adj (8*ncols) i32 | block_scratch (blocks) i64 |
+//   scratch_top u64 | order keys/cols (2 x 2 x ncols) u32 | cub temp (scan / pair sort) |
 //   scratch int2 (the rest of the workspace; hx_mesh_csc_workspace_bytes sizes it for
 //   SCRATCH_PER_COL records per column, and a caller that gets HX_ST_SCRATCH_OVERFLOW re-runs with
 //   room for col_ptr[ncols] records -- the counts are complete even then)
 constexpr int64_t SCRATCH_PER_COL = 15;  // off-diagonal records per column reserved (hex: 13 avg)
 struct MeshWs {
+    uint32_t *order_flag;
     int32_t *deg, *adj;
     int64_t *block_scratch;
     unsigned long long *scratch_top;
+    uint32_t *keys_in, *keys_out, *cols_in, *order;
     int2 *scratch;
     int64_t scratch_capacity;
     void *cub_tmp;
@@ -436,10 +468,12 @@ struct MeshWs {
     size_t total;  // with the default scratch
 };
 
-static size_t cub_scan_bytes(int64_t ncols) {
-    size_t b = 0;
+static size_t cub_temp_bytes(int64_t ncols) {
+    size_t b = 0, c = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, b, (int64_t *)nullptr, (int64_t *)nullptr, (int)(ncols + 1));
-    return b;
+    cub::DeviceRadixSort::SortPairs(nullptr, c, (uint32_t *)nullptr, (uint32_t *)nullptr, (uint32_t *)nullptr,
+                                    (uint32_t *)nullptr, (int)std::max<int64_t>(ncols, 1));
+    return std::max(b, c);
 }
 
 static MeshWs mesh_ws_layout(void *base, int64_t ncols, int64_t workspace_bytes = -1) {
@@ -450,11 +484,15 @@ static MeshWs mesh_ws_layout(void *base, int64_t ncols, int64_t workspace_bytes 
         off = align_up(off + bytes, 256);
         return o;
     };
-    const size_t o_deg = take(sizeof(int32_t) * std::max<int64_t>(ncols, 1));
-    const size_t o_adj = take(sizeof(int32_t) * 8 * std::max<int64_t>(ncols, 1));
+    const int64_t nc = std::max<int64_t>(ncols, 1);
+    const size_t o_flag = take(sizeof(uint32_t));
+    const size_t o_deg = take(sizeof(int32_t) * nc);
+    const size_t o_adj = take(sizeof(int32_t) * 8 * nc);
     const size_t o_bs = take(sizeof(int64_t) * std::max<int64_t>(1, ceil_div(ncols, COL_BLOCK)));
     const size_t o_st = take(sizeof(unsigned long long));
-    w.cub_bytes = cub_scan_bytes(ncols);
+    const size_t o_ki = take(sizeof(uint32_t) * nc), o_ko = take(sizeof(uint32_t) * nc);
+    const size_t o_ci = take(sizeof(uint32_t) * nc), o_or = take(sizeof(uint32_t) * nc);
+    w.cub_bytes = cub_temp_bytes(ncols);
     const size_t o_cub = take(w.cub_bytes);
     const size_t o_sc = off;
     const int64_t default_cap = std::max<int64_t>(1, SCRATCH_PER_COL * ncols);
@@ -463,10 +501,15 @@ static MeshWs mesh_ws_layout(void *base, int64_t ncols, int64_t workspace_bytes 
         workspace_bytes < 0 ? default_cap : std::max<int64_t>(0, (workspace_bytes - (int64_t)o_sc) / (int64_t)sizeof(int2));
     char *b = (char *)base;
     if (b) {
+        w.order_flag = (uint32_t *)(b + o_flag);
         w.deg = (int32_t *)(b + o_deg);
         w.adj = (int32_t *)(b + o_adj);
         w.block_scratch = (int64_t *)(b + o_bs);
         w.scratch_top = (unsigned long long *)(b + o_st);
+        w.keys_in = (uint32_t *)(b + o_ki);
+        w.keys_out = (uint32_t *)(b + o_ko);
+        w.cols_in = (uint32_t *)(b + o_ci);
+        w.order = (uint32_t *)(b + o_or);
         w.scratch = (int2 *)(b + o_sc);
         w.cub_tmp = b + o_cub;
     }
@@ -510,7 +553,8 @@ static int make_segtable(const hx_elem_segment *segs, int32_t n_segs, SegTable &
 }
 
 
-static bool single_dense(const SegTable &T) { return T.n == 1 && T.ke_stride[0] == 36; }
+static bool single_dense(const SegTable &T) { return T.n == 1 && T.ke_stride[0] == 36 && T.conn_stride[0] == 8; }
+static bool single_conn(const SegTable &T) { return T.n == 1 && T.conn_stride[0] == 8; }
 
 
 }  // namespace hx
@@ -525,7 +569,7 @@ extern "C" int64_t hx_mesh_csc_workspace_bytes(int64_t n_el_total, int64_t n_col
 
 static int mesh_csc_build(const hx_elem_segment *segs, int32_t n_segs, int64_t n_nodes, int64_t col_lo,
                           int64_t col_hi, int64_t *col_ptr, int64_t *row_idx, double *vals, int64_t row_capacity,
-                          void *workspace, int64_t workspace_bytes, uint32_t *status, void *stream) {
+                          void *workspace, int64_t workspace_bytes, uint32_t *status, int32_t flags, void *stream) {
     SegTable T;
     int64_t n_total = 0;
     int rc = make_segtable(segs, n_segs, T, n_total, vals != nullptr);
@@ -544,24 +588,46 @@ static int mesh_csc_build(const hx_elem_segment *segs, int32_t n_segs, int64_t n
         return HX_ERR_WORKSPACE;
     }
     cudaStream_t s = (cudaStream_t)stream;
+    const bool ordered = (flags & HX_CSC_ORDER_BY_ELEMENT) != 0 && ncols > 0 && n_total > 0;
     HX_TRY_CUDA(cudaMemsetAsync(status, 0, sizeof(uint32_t), s));
+    HX_TRY_CUDA(cudaMemsetAsync(w.order_flag, ordered ? 1 : 0, sizeof(uint32_t), s));
     if (ncols > 0) {
         HX_TRY_CUDA(cudaMemsetAsync(w.deg, 0, sizeof(int32_t) * ncols, s));
         if (n_total > 0) {
-            adjacency_kernel<<<(unsigned)std::min<int64_t>(ceil_div(8 * n_total, 256), 148 * 64), 256, 0, s>>>(
-                T, n_total, n_nodes, col_lo, col_hi, w.deg, w.adj, status);
+            const unsigned grid = (unsigned)std::min<int64_t>(ceil_div(8 * n_total, 256), 148 * 64);
+            if (single_conn(T))
+                adjacency_kernel<true><<<grid, 256, 0, s>>>(T, n_total, n_nodes, col_lo, col_hi, w.deg, w.adj, status);
+            else
+                adjacency_kernel<false><<<grid, 256, 0, s>>>(T, n_total, n_nodes, col_lo, col_hi, w.deg, w.adj, status);
             HX_CHECK_LAUNCH("adjacency_kernel");
         }
         const unsigned tiles = (unsigned)ceil_div(ncols, COL_BLOCK);
+        if (ordered) {
+            first_element_kernel<<<(unsigned)std::min<int64_t>(ceil_div(ncols, 256), 148 * 32), 256, 0, s>>>(
+                ncols, w.deg, w.adj, (uint32_t)n_total, w.keys_in, w.cols_in);
+            HX_CHECK_LAUNCH("first_element_kernel");
+            int end_bit = 1;
+            while (end_bit < 32 && ((uint64_t)n_total >> end_bit) != 0) ++end_bit;
+            size_t cb = w.cub_bytes;
+            HX_TRY_CUDA(cub::DeviceRadixSort::SortPairs(w.cub_tmp, cb, w.keys_in, w.keys_out, w.cols_in, w.order,
+                                                        (int)ncols, 0, end_bit, s));
+        }
+        const uint32_t *order = ordered ? w.order : nullptr;
         HX_TRY_CUDA(cudaMemsetAsync(w.scratch_top, 0, sizeof(unsigned long long), s));
-        if (n_nodes <= (int64_t(1) << 26))
-            pattern_kernel<uint32_t><<<tiles, COL_BLOCK, 0, s>>>(T, col_lo, ncols, w.deg, w.adj, col_ptr, w.scratch,
-                                                                w.scratch_capacity, w.scratch_top, w.block_scratch,
-                                                                status);
-        else
-            pattern_kernel<uint64_t><<<tiles, COL_BLOCK, 0, s>>>(T, col_lo, ncols, w.deg, w.adj, col_ptr, w.scratch,
-                                                                w.scratch_capacity, w.scratch_top, w.block_scratch,
-                                                                status);
+        auto pattern = [&](auto key_tag, auto single_tag) {
+            using K = decltype(key_tag);
+            pattern_kernel<K, decltype(single_tag)::value><<<tiles, COL_BLOCK, 0, s>>>(
+                T, col_lo, ncols, w.deg, w.adj, col_ptr, w.scratch, w.scratch_capacity, w.scratch_top, w.block_scratch,
+                status, order);
+        };
+        const bool packed = n_nodes <= (int64_t(1) << 26);
+        if (single_conn(T)) {
+            if (packed) pattern(uint32_t{}, std::true_type{});
+            else pattern(uint64_t{}, std::true_type{});
+        } else {
+            if (packed) pattern(uint32_t{}, std::false_type{});
+            else pattern(uint64_t{}, std::false_type{});
+        }
         HX_CHECK_LAUNCH("pattern_kernel");
         HX_TRY_CUDA(cudaMemsetAsync(col_ptr + ncols, 0, sizeof(int64_t), s));
         size_t cb2 = w.cub_bytes;
@@ -570,16 +636,16 @@ static int mesh_csc_build(const hx_elem_segment *segs, int32_t n_segs, int64_t n
             if (single_dense(T))
                 emit_kernel<true, true, true><<<tiles, EMIT_BLOCK, 0, s>>>(T, col_lo, ncols, w.deg, w.adj, col_ptr,
                                                                     w.scratch, w.block_scratch, row_idx, vals,
-                                                                    row_capacity, status);
+                                                                    row_capacity, status, w.order_flag, w.order);
             else
                 emit_kernel<true, true, false><<<tiles, EMIT_BLOCK, 0, s>>>(T, col_lo, ncols, w.deg, w.adj, col_ptr,
                                                                      w.scratch, w.block_scratch, row_idx, vals,
-                                                                     row_capacity, status);
+                                                                     row_capacity, status, w.order_flag, w.order);
             HX_CHECK_LAUNCH("emit_kernel");
         } else if (row_capacity > 0) {
             emit_kernel<true, false, true><<<tiles, EMIT_BLOCK, 0, s>>>(T, col_lo, ncols, w.deg, w.adj, col_ptr,
                                                                       w.scratch, w.block_scratch, row_idx, nullptr,
-                                                                      row_capacity, status);
+                                                                      row_capacity, status, w.order_flag, w.order);
             HX_CHECK_LAUNCH("emit_kernel<rows>");
         }
     } else {
@@ -591,21 +657,21 @@ static int mesh_csc_build(const hx_elem_segment *segs, int32_t n_segs, int64_t n
 extern "C" int hx_mesh_csc_symbolic(const hx_elem_segment *segs, int32_t n_segs, int64_t n_nodes,
                                     int64_t col_lo, int64_t col_hi, int64_t *col_ptr, int64_t *row_idx,
                                     int64_t row_capacity, void *workspace, int64_t workspace_bytes,
-                                    uint32_t *status, void *stream) {
+                                    uint32_t *status, int32_t flags, void *stream) {
     return mesh_csc_build(segs, n_segs, n_nodes, col_lo, col_hi, col_ptr, row_idx, nullptr, row_capacity, workspace,
-                          workspace_bytes, status, stream);
+                          workspace_bytes, status, flags, stream);
 }
 
 extern "C" int hx_mesh_csc_build(const hx_elem_segment *segs, int32_t n_segs, int64_t n_nodes, int64_t col_lo,
                                  int64_t col_hi, int64_t *col_ptr, int64_t *row_idx, double *vals,
                                  int64_t capacity, void *workspace, int64_t workspace_bytes, uint32_t *status,
-                                 void *stream) {
+                                 int32_t flags, void *stream) {
     if (vals == nullptr && capacity > 0) {
         set_last_error("hx_mesh_csc_build: vals is NULL");
         return HX_ERR_VALUE;
     }
     return mesh_csc_build(segs, n_segs, n_nodes, col_lo, col_hi, col_ptr, row_idx, vals, capacity, workspace,
-                          workspace_bytes, status, stream);
+                          workspace_bytes, status, flags, stream);
 }
 
 extern "C" int hx_mesh_csc_numeric(const hx_elem_segment *segs, int32_t n_segs, int64_t col_lo, int64_t col_hi,
@@ -625,10 +691,10 @@ extern "C" int hx_mesh_csc_numeric(const hx_elem_segment *segs, int32_t n_segs, 
     if (ncols > 0) {
         if (single_dense(T))
             emit_kernel<false, true, true><<<(unsigned)ceil_div(ncols, COL_BLOCK), EMIT_BLOCK, 0, s>>>(
-                T, col_lo, ncols, w.deg, w.adj, col_ptr, w.scratch, w.block_scratch, nullptr, vals, INT64_MAX, status);
+                T, col_lo, ncols, w.deg, w.adj, col_ptr, w.scratch, w.block_scratch, nullptr, vals, INT64_MAX, status, w.order_flag, w.order);
         else
             emit_kernel<false, true, false><<<(unsigned)ceil_div(ncols, COL_BLOCK), EMIT_BLOCK, 0, s>>>(
-                T, col_lo, ncols, w.deg, w.adj, col_ptr, w.scratch, w.block_scratch, nullptr, vals, INT64_MAX, status);
+                T, col_lo, ncols, w.deg, w.adj, col_ptr, w.scratch, w.block_scratch, nullptr, vals, INT64_MAX, status, w.order_flag, w.order);
         HX_CHECK_LAUNCH("emit_kernel<numeric>");
     }
     return HX_OK;
@@ -653,10 +719,12 @@ extern "C" int hx_mesh_csc_emit(const hx_elem_segment *segs, int32_t n_segs, int
         const unsigned tiles = (unsigned)ceil_div(ncols, COL_BLOCK);
         if (single_dense(T))
             emit_kernel<true, true, true><<<tiles, EMIT_BLOCK, 0, s>>>(T, col_lo, ncols, w.deg, w.adj, col_ptr, w.scratch,
-                                                                w.block_scratch, row_idx, vals, capacity, status);
+                                                                w.block_scratch, row_idx, vals, capacity, status,
+                                                                w.order_flag, w.order);
         else
             emit_kernel<true, true, false><<<tiles, EMIT_BLOCK, 0, s>>>(T, col_lo, ncols, w.deg, w.adj, col_ptr, w.scratch,
-                                                                 w.block_scratch, row_idx, vals, capacity, status);
+                                                                 w.block_scratch, row_idx, vals, capacity, status,
+                                                                w.order_flag, w.order);
         HX_CHECK_LAUNCH("emit_kernel<emit>");
     }
     return HX_OK;

@@ -85,6 +85,13 @@ class DeviceMesh:
     def h2d_bytes(self) -> int:
         return sum(t.numel() * t.element_size() for t in (self.coords, self.conn, self.coeff))
 
+    def assembly_order(self) -> str:
+        """Column processing order for this mesh's assembly ("column" or "element"), decided once
+        per mesh by numbering_is_local (one small device reduction + host read)."""
+        if getattr(self, "_order", None) is None:
+            self._order = "column" if numbering_is_local(self.conn, self.n_nodes) else "element"
+        return self._order
+
 
 def new_fail_record(device) -> torch.Tensor:
     return torch.empty(_FAIL_WORDS, dtype=torch.int64, device=device)
@@ -207,14 +214,38 @@ def _check_segment(conn, ke):
 ROWS_PER_COLUMN_ESTIMATE = 16
 
 
+def numbering_is_local(conn: torch.Tensor, n_nodes: int, sample: int = 4096) -> bool:
+    """Heuristic for the assembly processing order: on meshes numbered with locality (structured
+    generators, RCM-ordered inputs) an element's node ids span a small fraction of the id range;
+    on randomly numbered meshes they span most of it.  One small device reduction + host read."""
+    n = conn.shape[0]
+    if n == 0 or n_nodes < 1 << 16:
+        return True
+    idx = torch.linspace(0, n - 1, min(sample, n), device=conn.device).long()
+    rows = conn[idx]
+    span = (rows.max(dim=1).values - rows.min(dim=1).values).double().mean()
+    return bool(span.item() < n_nodes / 64)
+
+
+def _order_flags(order, conn, n_nodes) -> int:
+    if order == "element":
+        return N.CSC_ORDER_BY_ELEMENT
+    if order == "column":
+        return 0
+    if order != "auto":
+        raise ConfigurationError(f"assembly order must be 'auto', 'element' or 'column', got {order!r}")
+    return 0 if numbering_is_local(conn, n_nodes) else N.CSC_ORDER_BY_ELEMENT
+
+
 def mesh_csc(parts, n_nodes: int, col_lo: int = 0, col_hi: int | None = None, stream=None,
-             row_capacity: int | None = None) -> DeviceCsc:
+             row_capacity: int | None = None, order: str = "auto") -> DeviceCsc:
     """Assemble columns [col_lo, col_hi) of the lower CSC from element segments.
 
     ``parts`` is a list of (conn (n,8) i32, ke (n,36) f64) CUDA tensor views in ascending global
     element order (one pair for a single GPU; halo record views for the multi-GPU path -- rows
     may be strided).  Meshes outside the node-adjacency fast path's limits fall through to the
-    generic triplet path with identical results.
+    generic triplet path with identical results.  ``order`` picks the column processing order
+    (results are identical; "auto" uses element order for numberings without locality).
     """
     col_hi = n_nodes if col_hi is None else col_hi
     if not 1 <= len(parts) <= N.MAX_SEGMENTS:
@@ -225,6 +256,7 @@ def mesh_csc(parts, n_nodes: int, col_lo: int = 0, col_hi: int | None = None, st
     n_total = sum(int(c.shape[0]) for c, _ in parts)
     ncols = col_hi - col_lo
     segs = N.segments([(c.data_ptr(), k.data_ptr(), int(c.shape[0]), c.stride(0), k.stride(0)) for c, k in parts])
+    flags = _order_flags(order, parts[0][0], n_nodes)
     ws_bytes = N.lib().hx_mesh_csc_workspace_bytes(n_total, ncols)
     if ws_bytes < 0:
         raise ValueError("bad mesh size")
@@ -237,7 +269,7 @@ def mesh_csc(parts, n_nodes: int, col_lo: int = 0, col_hi: int | None = None, st
         row_buf = torch.empty(max(capacity, 1), dtype=torch.int64, device=dev)
         val_buf = torch.empty(max(capacity, 1), dtype=torch.float64, device=dev)
         N.check(N.lib().hx_mesh_csc_build(segs, len(parts), n_nodes, col_lo, col_hi, _ptr(col_ptr), _ptr(row_buf),
-                                          _ptr(val_buf), capacity, _ptr(ws), ws_bytes, _ptr(status), sh),
+                                          _ptr(val_buf), capacity, _ptr(ws), ws_bytes, _ptr(status), flags, sh),
                 "hx_mesh_csc_build")
         head = torch.stack([status.to(torch.int64)[0], col_ptr[-1]]).cpu()  # one sync: status + nnz
         st, nnz = int(head[0]), int(head[1])
@@ -272,9 +304,10 @@ class MeshPlan:
     row_buf: torch.Tensor
     val_buf: torch.Tensor
     capacity: int
+    flags: int = 0
 
 
-def mesh_plan_async(conn: torch.Tensor, n_nodes: int, stream=None) -> MeshPlan:
+def mesh_plan_async(conn: torch.Tensor, n_nodes: int, stream=None, order: str = "auto") -> MeshPlan:
     """Launch the symbolic phase of a single-segment mesh assembly on ``stream`` (no host sync).
     It reads only the connectivity, so it can run concurrently with the integration kernel."""
     n = conn.shape[0]
@@ -291,10 +324,11 @@ def mesh_plan_async(conn: torch.Tensor, n_nodes: int, stream=None) -> MeshPlan:
     row_buf = torch.empty(max(capacity, 1), dtype=torch.int64, device=dev)
     val_buf = torch.empty(max(capacity, 1), dtype=torch.float64, device=dev)
     segs = N.segments([(conn.data_ptr(), 0, n)])
+    flags = _order_flags(order, conn, n_nodes)
     N.check(N.lib().hx_mesh_csc_symbolic(segs, 1, n_nodes, 0, n_nodes, _ptr(col_ptr), ctypes.c_void_p(0), 0,
-                                         _ptr(ws), ws_bytes, _ptr(status), stream_handle(stream)),
+                                         _ptr(ws), ws_bytes, _ptr(status), flags, stream_handle(stream)),
             "hx_mesh_csc_symbolic")
-    return MeshPlan(conn, n_nodes, col_ptr, ws, status, row_buf, val_buf, capacity)
+    return MeshPlan(conn, n_nodes, col_ptr, ws, status, row_buf, val_buf, capacity, flags)
 
 
 def mesh_emit(plan: MeshPlan, ke: torch.Tensor, stream=None) -> DeviceCsc:
@@ -309,7 +343,8 @@ def mesh_emit(plan: MeshPlan, ke: torch.Tensor, stream=None) -> DeviceCsc:
     st, nnz = int(head[0]), int(head[1])
     _status_error(st)
     if st & N.ST_FASTPATH_LIMITS or nnz > plan.capacity:
-        return mesh_csc([(plan.conn, ke)], plan.n_nodes, stream=stream)
+        order = "element" if plan.flags & N.CSC_ORDER_BY_ELEMENT else "column"
+        return mesh_csc([(plan.conn, ke)], plan.n_nodes, stream=stream, order=order)
     return DeviceCsc(plan.col_ptr, plan.row_buf[:nnz], plan.val_buf[:nnz], plan.n_nodes, 0, "mesh")
 
 

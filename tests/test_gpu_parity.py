@@ -323,8 +323,9 @@ def test_unreferenced_nodes_give_empty_columns(permute):
     assert bits_equal(b.csc.vals.cpu().numpy(), vv)
 
 
+@pytest.mark.parametrize("flags", [0, 1])
 @pytest.mark.parametrize("name", SMALL_MESHES)
-def test_symbolic_rows_only_abi(golden, name):
+def test_symbolic_rows_only_abi(golden, name, flags):
     """hx_mesh_csc_symbolic with a row buffer: the pattern without values (rows-only emit)."""
     import ctypes
 
@@ -340,8 +341,36 @@ def test_symbolic_rows_only_abi(golden, name):
     rows = torch.empty(36 * n, dtype=torch.int64, device="cuda")
     segs = N.segments([(conn.data_ptr(), 0, n)])
     N.check(N.lib().hx_mesh_csc_symbolic(segs, 1, dim, 0, dim, D._ptr(col_ptr), D._ptr(rows), 36 * n, D._ptr(ws),
-                                         ws_bytes, D._ptr(status), D.stream_handle()), "symbolic")
+                                         ws_bytes, D._ptr(status), flags, D.stream_handle()), "symbolic")
     assert int(status.item()) == 0
     nnz = int(col_ptr[-1].item())
     assert bits_equal(col_ptr.cpu().numpy(), golden[f"{name}_col_ptr"])
     assert bits_equal(rows[:nnz].cpu().numpy(), golden[f"{name}_row_idx"])
+
+
+@pytest.mark.parametrize("order", ["column", "element"])
+@pytest.mark.parametrize("kind", ["structured", "permuted", "gaps"])
+def test_assembly_orders_bitwise(order, kind):
+    """Both column processing orders give the reference's bits (structured, permuted numbering,
+    unreferenced nodes)."""
+    mesh = perturbed_mesh(11, seed=21)
+    if kind == "permuted":
+        mesh = permuted_mesh(mesh, seed=22)
+    elif kind == "gaps":
+        new_id = 3 * np.arange(mesh.n_nodes)
+        coords = np.zeros((3 * mesh.n_nodes, 3))
+        coords[new_id] = mesh.coords
+        mesh = Mesh(coords, new_id.astype(np.int32)[mesh.connectivity], mesh.coefficient)
+    dm = D.DeviceMesh.from_host(mesh)
+    ke, _, _, fail = D.integrate_mesh(dm)
+    D.raise_if_failed(fail)
+    csc = D.mesh_csc([(dm.conn, ke)], mesh.n_nodes, order=order)
+    plan = D.mesh_plan_async(dm.conn, mesh.n_nodes, order=order)
+    csc2 = D.mesh_emit(plan, ke)
+    rows, cols = oracle.connectivity_index_arrays(mesh.connectivity)
+    cp, ri, vv = oracle.triplet_to_csc(rows, cols, ke.cpu().numpy().reshape(-1), mesh.n_nodes)
+    for c in (csc, csc2):
+        assert c.path == "mesh"
+        assert bits_equal(c.col_ptr.cpu().numpy(), cp)
+        assert bits_equal(c.row_idx.cpu().numpy(), ri)
+        assert bits_equal(c.vals.cpu().numpy(), vv)
