@@ -22,6 +22,8 @@
  *                                  triplet_to_csc (assemble.py:110-140) on mesh triplets
  *   hx_triplet_csc_*               assemble.py:110-149 triplet_to_csc + _check_indices
  *   hx_halo_*                      (new) element-halo exchange of the multi-GPU path
+ *   hx_block_*                     (new) column blocks of the out-of-core build (Eq. 10 batching,
+ *                                  integrate.py:55-81 / PAPER.md:192-199, beyond one GPU's HBM)
  */
 #ifndef HEXFEM_B200_H
 #define HEXFEM_B200_H
@@ -177,6 +179,18 @@ int hx_halo_count(const int32_t *conn, int64_t n_el, const int64_t *col_bounds, 
                   int64_t *per_dest, void *workspace, int64_t workspace_bytes, void *stream);
 int hx_halo_pack(const int32_t *conn, const double *ke, int64_t n_el, const int64_t *col_bounds, int32_t world,
                  int32_t self, double *records, const void *workspace, void *stream);
+
+/* ---- column blocks of one GPU (out-of-core build, Eq. 10 beyond HBM) ---------------------------
+ * select: ids (n_el capacity) i64 device <- ascending ids of the elements with a node in
+ *         [col_lo, col_hi); *count (device) = their number.  Stable: the block's elements keep the
+ *         global element order, so duplicates are summed exactly as in the one-shot build.
+ * gather: conn_out (count, 8) i32 / coeff_out (count,) f64 <- those elements' rows; capacity bounds
+ *         the launch (>= count). */
+int64_t hx_block_select_workspace_bytes(int64_t n_el);
+int hx_block_select(const int32_t *conn, int64_t n_el, int64_t col_lo, int64_t col_hi, int64_t *ids,
+                    int64_t *count, void *workspace, int64_t workspace_bytes, void *stream);
+int hx_block_gather(const int32_t *conn, const double *coeff, const int64_t *ids, const int64_t *count,
+                    int64_t capacity, int32_t *conn_out, double *coeff_out, void *stream);
 
 #ifdef __cplusplus
 }

@@ -13,6 +13,8 @@
 //   scan    exclusive scan over the destination-major (d, tile) table (CUB)
 //   pass 2  each tile writes its records at offset(d, tile) + intra-tile rank (ballots again)
 #include <cub/device/device_scan.cuh>
+#include <cub/device/device_select.cuh>
+#include <thrust/iterator/counting_iterator.h>
 
 #include <algorithm>
 
@@ -132,9 +134,85 @@ static ShardWs shard_ws_layout(void *base, int64_t n_el, int world) {
     return w;
 }
 
+// ---- column-block element selection (out-of-core build: one column block at a time) ----------
+// Element e belongs to block [col_lo, col_hi) when one of its nodes does; the selection keeps
+// ascending element order (a stable compaction), so the block's single segment sums duplicates in
+// the global element order.
+struct TouchesBlock {
+    const int32_t *conn;
+    int64_t lo, hi;
+    __device__ __forceinline__ bool operator()(const int64_t &e) const {
+        const int4 *c4 = reinterpret_cast<const int4 *>(conn) + 2 * e;
+        const int4 a = __ldg(c4), b = __ldg(c4 + 1);
+        const int32_t g[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+        bool in = false;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) in |= g[k] >= lo && g[k] < hi;
+        return in;
+    }
+};
+
+__global__ void block_gather_kernel(const int32_t *__restrict__ conn, const double *__restrict__ coeff,
+                                    const int64_t *__restrict__ ids, const int64_t *__restrict__ count,
+                                    int32_t *__restrict__ conn_out, double *__restrict__ coeff_out) {
+    const int64_t n = *count;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t e = ids[i];
+        const int4 *src = reinterpret_cast<const int4 *>(conn) + 2 * e;
+        int4 *dst = reinterpret_cast<int4 *>(conn_out) + 2 * i;
+        dst[0] = __ldg(src);
+        dst[1] = __ldg(src + 1);
+        coeff_out[i] = __ldg(coeff + e);
+    }
+}
+
 }  // namespace hx
 
 using namespace hx;
+
+extern "C" int64_t hx_block_select_workspace_bytes(int64_t n_el) {
+    if (n_el < 0 || n_el > INT32_MAX) return -1;
+    size_t b = 0;
+    cub::DeviceSelect::If(nullptr, b, thrust::counting_iterator<int64_t>(0), (int64_t *)nullptr, (int64_t *)nullptr,
+                          (int)std::max<int64_t>(n_el, 1), TouchesBlock{nullptr, 0, 0});
+    return (int64_t)b;
+}
+
+extern "C" int hx_block_select(const int32_t *conn, int64_t n_el, int64_t col_lo, int64_t col_hi, int64_t *ids,
+                               int64_t *count, void *workspace, int64_t workspace_bytes, void *stream) {
+    if (n_el < 0 || n_el > INT32_MAX || col_lo < 0 || col_hi < col_lo || ids == nullptr || count == nullptr ||
+        (n_el > 0 && conn == nullptr)) {
+        set_last_error("hx_block_select: bad arguments");
+        return HX_ERR_VALUE;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    if (n_el == 0) {
+        HX_TRY_CUDA(cudaMemsetAsync(count, 0, sizeof(int64_t), s));
+        return HX_OK;
+    }
+    size_t b = (size_t)workspace_bytes;
+    if (workspace == nullptr || workspace_bytes < hx_block_select_workspace_bytes(n_el)) {
+        set_last_error("hx_block_select: workspace too small");
+        return HX_ERR_WORKSPACE;
+    }
+    HX_TRY_CUDA(cub::DeviceSelect::If(workspace, b, thrust::counting_iterator<int64_t>(0), ids, count, (int)n_el,
+                                      TouchesBlock{conn, col_lo, col_hi}, s));
+    return HX_OK;
+}
+
+extern "C" int hx_block_gather(const int32_t *conn, const double *coeff, const int64_t *ids, const int64_t *count,
+                               int64_t capacity, int32_t *conn_out, double *coeff_out, void *stream) {
+    if (conn == nullptr || coeff == nullptr || ids == nullptr || count == nullptr || capacity < 0 ||
+        (capacity > 0 && (conn_out == nullptr || coeff_out == nullptr))) {
+        set_last_error("hx_block_gather: bad arguments");
+        return HX_ERR_VALUE;
+    }
+    if (capacity == 0) return HX_OK;
+    block_gather_kernel<<<(unsigned)std::min<int64_t>(ceil_div(capacity, 256), 148 * 16), 256, 0,
+                          (cudaStream_t)stream>>>(conn, coeff, ids, count, conn_out, coeff_out);
+    HX_CHECK_LAUNCH("block_gather_kernel");
+    return HX_OK;
+}
 
 extern "C" int64_t hx_halo_workspace_bytes(int64_t n_el, int32_t world) {
     if (n_el < 0 || world < 1 || world > MAX_WORLD) return -1;

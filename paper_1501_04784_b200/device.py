@@ -19,7 +19,7 @@ from .errors import ConfigurationError, DegenerateElementError, MeshValidationEr
 __all__ = [
     "DeviceMesh", "DeviceCsc", "require_device", "stream_handle", "integrate_mesh", "stiffness_batch",
     "connectivity_index_arrays", "raise_if_failed", "mesh_csc", "triplet_csc", "MeshPlan", "mesh_plan_async",
-    "mesh_emit",
+    "mesh_emit", "block_elements",
 ]
 
 _FAIL_WORDS = 3  # hx_fail_info = {int64 element, int32 gp, int32 pad, double det} = 24 bytes
@@ -346,6 +346,27 @@ def mesh_emit(plan: MeshPlan, ke: torch.Tensor, stream=None) -> DeviceCsc:
         order = "element" if plan.flags & N.CSC_ORDER_BY_ELEMENT else "column"
         return mesh_csc([(plan.conn, ke)], plan.n_nodes, stream=stream, order=order)
     return DeviceCsc(plan.col_ptr, plan.row_buf[:nnz], plan.val_buf[:nnz], plan.n_nodes, 0, "mesh")
+
+
+def block_elements(dm: DeviceMesh, col_lo: int, col_hi: int, ids=None, ws=None, stream=None):
+    """Elements with a node in columns [col_lo, col_hi), ascending (hx_block_select + gather):
+    returns (global ids (m,) i64, conn (m, 8) i32, coeff (m,) f64) on the device."""
+    n = dm.n_el
+    dev = dm.conn.device
+    if ids is None:
+        ids = torch.empty(max(n, 1), dtype=torch.int64, device=dev)
+    if ws is None:
+        ws = torch.empty(max(N.lib().hx_block_select_workspace_bytes(n), 1), dtype=torch.uint8, device=dev)
+    count = torch.empty(1, dtype=torch.int64, device=dev)
+    sh = stream_handle(stream)
+    N.check(N.lib().hx_block_select(_ptr(dm.conn), n, col_lo, col_hi, _ptr(ids), _ptr(count), _ptr(ws),
+                                    ws.numel(), sh), "hx_block_select")
+    m = int(count.item())
+    conn = torch.empty((m, 8), dtype=torch.int32, device=dev)
+    coeff = torch.empty(m, dtype=torch.float64, device=dev)
+    N.check(N.lib().hx_block_gather(_ptr(dm.conn), _ptr(dm.coeff), _ptr(ids), _ptr(count), m, _ptr(conn),
+                                    _ptr(coeff), sh), "hx_block_gather")
+    return ids[:m], conn, coeff
 
 
 def _mesh_csc_generic(parts, n_nodes, col_lo, col_hi, stream) -> DeviceCsc:

@@ -19,7 +19,7 @@ from .assemble import LowerCscMatrix, csc_to_host
 from .errors import ConfigurationError
 from .integrate import plan_batches, required_bytes
 
-__all__ = ["BuildReport", "DeviceBuild", "build_device", "run_build", "triplet_memory", "csc_memory",
+__all__ = ["BuildReport", "DeviceBuild", "build_device", "run_build", "build_out_of_core", "device_bytes", "triplet_memory", "csc_memory",
            "memory_saving", "format_mb", "format_percent"]
 
 # sparseio.py:26-38 memory model: 16 B per triplet, 16 B per CSC entry + 8 B per column pointer.
@@ -137,9 +137,95 @@ def build_device(dm: D.DeviceMesh, mode: str = "exact", with_index: bool = True,
     return DeviceBuild(ke, rows if with_index else None, cols if with_index else None, csc)
 
 
+def device_bytes(n_el: int, n_nodes: int, with_index: bool = True) -> int:
+    """HBM footprint of an in-core build_device: inputs, KE (+ iK/jK), the CSC output buffers at the
+    rows-per-column estimate and the symbolic workspace."""
+    inputs = 40 * n_el + 24 * n_nodes
+    ke = 288 * n_el + (288 * n_el if with_index else 0)
+    csc = 16 * D.ROWS_PER_COLUMN_ESTIMATE * n_nodes + 8 * (n_nodes + 1)
+    workspace = 156 * n_nodes
+    return inputs + ke + csc + workspace
+
+
+def build_out_of_core(mesh, n_blocks: int, mode: str = "exact", device=None, return_values: bool = False):
+    """Global matrix of a mesh whose build does not fit in HBM (Eq. 10 batching, integrate.py:55-81 /
+    PAPER.md:192-199): the lower CSC is built one column block at a time on one GPU.
+
+    Block r = columns [N r / B, N (r+1) / B): its elements (those with a node in the block, selected
+    in ascending order on the device) are integrated and assembled, the block is copied to the host
+    and its device memory released.  Elements on a block boundary are integrated once per block they
+    touch (a halo recompute instead of a halo store).  Duplicates are summed in global element order,
+    so the result is bitwise equal to the one-shot build.  Returns (LowerCscMatrix, values or None,
+    stage times); values (n_el, 36) come from each element's first block.
+    """
+    from .distributed import column_bounds
+
+    if n_blocks < 1:
+        raise ConfigurationError(f"block count must be at least 1, got {n_blocks}")
+    dev = D.require_device(device)
+    n_el, n_nodes = mesh.n_el, mesh.n_nodes
+    with torch.cuda.device(dev):
+        dm = D.DeviceMesh.from_host(mesh, dev)
+        bounds = column_bounds(n_nodes, n_blocks)
+        ids_buf = torch.empty(max(n_el, 1), dtype=torch.int64, device=dev)
+        sel_ws = torch.empty(max(D.N.lib().hx_block_select_workspace_bytes(n_el), 1), dtype=torch.uint8, device=dev)
+        col_ptr = np.zeros(n_nodes + 1, dtype=np.int64)
+        rows, vals = [], []
+        values = np.empty((n_el, 36)) if return_values else None
+        done = np.zeros(n_el, dtype=bool) if return_values else None
+        order = dm.assembly_order()
+        worst = None  # (global element id, gauss point, det) of the lowest failing element
+        nnz = 0
+        t_int = t_asm = 0.0
+        for r in range(n_blocks):
+            lo, hi = int(bounds[r]), int(bounds[r + 1])
+            ids, conn, coeff = D.block_elements(dm, lo, hi, ids=ids_buf, ws=sel_ws)
+            if conn.shape[0] == 0:
+                continue
+            sub = D.DeviceMesh(dm.coords, conn, coeff)
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+            ev[0].record()
+            ke, _, _, fail = D.integrate_mesh(sub, with_index=False, mode=mode)
+            ev[1].record()
+            f = fail.cpu().numpy()
+            if f[0] >= 0:
+                gid = int(ids[int(f[0])].item())
+                if worst is None or gid < worst[0]:
+                    worst = (gid, int(np.int32(f[1] & 0xFFFFFFFF)), float(f[2:3].view(np.float64)[0]))
+                continue
+            csc = D.mesh_csc([(conn, ke)], n_nodes, lo, hi, order=order)
+            ev[2].record()
+            torch.cuda.synchronize(dev)
+            t_int += ev[0].elapsed_time(ev[1]) / 1e3
+            t_asm += ev[1].elapsed_time(ev[2]) / 1e3
+            col_ptr[lo + 1:hi + 1] = csc.col_ptr[1:].cpu().numpy() + nnz
+            nnz += csc.nnz
+            rows.append(csc.row_idx.cpu().numpy())
+            vals.append(csc.vals.cpu().numpy())
+            if return_values:
+                ids_h = ids.cpu().numpy()
+                new = ~done[ids_h]
+                values[ids_h[new]] = ke.cpu().numpy()[new]
+                done[ids_h] = True
+            del ids, conn, coeff, sub, ke, csc
+        if worst is not None:
+            from .errors import DegenerateElementError
+
+            raise DegenerateElementError(element_id=worst[0], gauss_point=worst[1], det=worst[2])
+        # columns of nodes no element references keep col_ptr flat
+        np.maximum.accumulate(col_ptr, out=col_ptr)
+    matrix = LowerCscMatrix(col_ptr=col_ptr, row_idx=np.concatenate(rows) if rows else np.empty(0, np.int64),
+                            vals=np.concatenate(vals) if vals else np.empty(0), dim=n_nodes)
+    return matrix, values, {"time_integration_s": t_int, "time_assembly_s": t_asm, "blocks": n_blocks}
+
+
 def run_build(mesh, budget_bytes: int, workers: int = 1, mode: str = "sequential", assembler: str = "direct",
-              integration: str = "exact", device=None):
-    """Integrate and assemble one mesh on the GPU; returns (LowerCscMatrix, BuildReport)."""
+              integration: str = "exact", device=None, device_budget_bytes: int | None = None):
+    """Integrate and assemble one mesh on the GPU; returns (LowerCscMatrix, BuildReport).
+
+    ``device_budget_bytes``: HBM the build may use.  When the in-core footprint (device_bytes)
+    exceeds it, the matrix is built in ceil(footprint / budget) column blocks (build_out_of_core).
+    """
     if assembler not in ("direct", "triplet"):
         raise ConfigurationError(f"assembler must be 'direct' or 'triplet', got {assembler!r}")
     if mode not in ("sequential", "overlapped"):
@@ -148,6 +234,10 @@ def run_build(mesh, budget_bytes: int, workers: int = 1, mode: str = "sequential
         raise ConfigurationError(f"worker count must be at least 1, got {workers}")
     plan = plan_batches(required_bytes(mesh.n_el), budget_bytes, mesh.n_el)
     dev = D.require_device(device)
+    need = device_bytes(mesh.n_el, mesh.n_nodes, with_index=assembler == "triplet")
+    if device_budget_bytes is not None and need > device_budget_bytes:
+        return _run_build_blocks(mesh, plan, -(-need // device_budget_bytes), workers, mode, assembler, integration,
+                                 dev)
     wall0 = time.perf_counter()
     with torch.cuda.device(dev):
         dm = D.DeviceMesh.from_host(mesh, dev)
@@ -189,6 +279,24 @@ def run_build(mesh, budget_bytes: int, workers: int = 1, mode: str = "sequential
         time_assembly_s=time_assembly, time_total_s=time_total, pct_integration=pct_integration,
         pct_assembly=100.0 - pct_integration, group_count=plan.group_count, workers=workers, mode=mode,
         assembler=assembler)
+    return matrix, report
+
+
+def _run_build_blocks(mesh, plan, n_blocks, workers, mode, assembler, integration, dev):
+    wall0 = time.perf_counter()
+    matrix, _, st = build_out_of_core(mesh, int(min(n_blocks, max(mesh.n_nodes, 1))), mode=integration, device=dev)
+    total = time.perf_counter() - wall0
+    t_int, t_asm = st["time_integration_s"], st["time_assembly_s"]
+    pct = 100.0 * t_int / (t_int + t_asm) if t_int + t_asm > 0 else 100.0
+    nnz_triplet = 36 * mesh.n_el
+    trip_mb = triplet_memory(nnz_triplet)
+    matrix_mb = csc_memory(matrix.nnz, matrix.dim)
+    report = BuildReport(
+        n_el=mesh.n_el, n_nodes=mesh.n_nodes, nnz_triplet=nnz_triplet, nnz_csc=matrix.nnz,
+        nnz_compression=1.0 - matrix.nnz / nnz_triplet, triplet_mb=trip_mb, csc_mb=matrix_mb,
+        memory_saving=memory_saving(trip_mb, matrix_mb), time_integration_s=t_int, time_index_s=None,
+        time_assembly_s=t_asm, time_total_s=total, pct_integration=pct, pct_assembly=100.0 - pct,
+        group_count=plan.group_count, workers=workers, mode=mode, assembler=assembler)
     return matrix, report
 
 

@@ -374,3 +374,35 @@ def test_assembly_orders_bitwise(order, kind):
         assert bits_equal(c.col_ptr.cpu().numpy(), cp)
         assert bits_equal(c.row_idx.cpu().numpy(), ri)
         assert bits_equal(c.vals.cpu().numpy(), vv)
+
+
+@pytest.mark.parametrize("blocks", [1, 2, 5, 13])
+@pytest.mark.parametrize("kind", ["structured", "permuted"])
+def test_out_of_core_blocks_bitwise(blocks, kind):
+    """Column blocks built one at a time (halo elements recomputed) == the one-shot build, bit for bit."""
+    from paper_1501_04784_b200.pipeline import build_out_of_core
+
+    mesh = perturbed_mesh(10, seed=31)
+    if kind == "permuted":
+        mesh = permuted_mesh(mesh, seed=32)
+    m, values, stats = build_out_of_core(mesh, blocks, return_values=True)
+    ke, rows, cols, first, _, _ = oracle.stiffness_mesh(mesh.coords, mesh.connectivity, mesh.coefficient)
+    cp, ri, vv = oracle.triplet_to_csc(rows, cols, ke.reshape(-1), mesh.n_nodes)
+    assert bits_equal(m.col_ptr, cp) and bits_equal(m.row_idx, ri) and bits_equal(m.vals, vv)
+    assert bits_equal(values, ke)
+    assert stats["blocks"] == blocks
+
+
+def test_out_of_core_degenerate_and_budget(golden):
+    from paper_1501_04784_b200.pipeline import build_out_of_core, device_bytes
+
+    mesh = Mesh(golden["degen_coords"], golden["degen_conn"], np.ones(golden["degen_conn"].shape[0]))
+    exp_el, exp_gp = golden["degen_expect"]
+    with pytest.raises(DegenerateElementError) as info:
+        build_out_of_core(mesh, 3)
+    assert info.value.element_id == exp_el and info.value.gauss_point == exp_gp
+    good = golden_mesh(golden, "m345")
+    budget = device_bytes(good.n_el, good.n_nodes) // 4
+    m, report = run_build(good, budget_bytes=10**12, device_budget_bytes=budget)
+    assert bits_equal(m.vals, golden["m345_vals"]) and bits_equal(m.row_idx, golden["m345_row_idx"])
+    assert abs(report.pct_integration + report.pct_assembly - 100.0) < 1e-9
