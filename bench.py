@@ -219,9 +219,16 @@ def run_ours(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    # HX_DIST_BACKEND=gloo runs N ranks on however many GPUs exist (host-staged exchange): a
+    # functional test of the N>1 path on a 1-GPU box.  Production runs use NCCL, one GPU per rank.
+    backend = os.environ.get("HX_DIST_BACKEND", "nccl")
+    local = local % max(torch.cuda.device_count(), 1) if backend == "gloo" else local
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     wl = args.workload.upper()
     side = args.side or WORKLOADS[wl]["n"]
     t_mesh = time.perf_counter()
@@ -247,7 +254,9 @@ def run_ours(args):
 
     def barrier():
         if world > 1:
-            dist.barrier(device_ids=[local])
+            from paper_1501_04784_b200.distributed import barrier as dist_barrier
+
+            dist_barrier(device_index=local)
 
     for _ in range(args.warmup):
         step()
@@ -266,8 +275,10 @@ def run_ours(args):
         barrier()
     ms_local = start.elapsed_time(stop) / args.steps
     if world > 1:
+        from paper_1501_04784_b200.distributed import all_reduce
+
         t = torch.tensor([ms_local], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     else:
         ms = ms_local
@@ -340,7 +351,7 @@ def run_ours(args):
             line["cpu_baseline"] = cpu
         print(json.dumps(line), flush=True)
     if world > 1:
-        dist.barrier(device_ids=[local])
+        barrier()
         dist.destroy_process_group()
 
 

@@ -31,7 +31,7 @@ import numpy as np
 import torch
 
 __all__ = ["element_ranges", "column_bounds", "ShardedBuild", "TorchExchange", "LoopbackExchange", "CudaOps",
-           "run_loopback", "RECORD_DOUBLES"]
+           "run_loopback", "RECORD_DOUBLES", "all_reduce", "barrier"]
 
 RECORD_DOUBLES = 40  # 36 packed KE values + 8 int32 node ids
 
@@ -47,8 +47,40 @@ def column_bounds(n_nodes: int, world: int) -> np.ndarray:
 # ------------------------------------------------------------------------------------------
 # collectives
 # ------------------------------------------------------------------------------------------
+def _host_staged(group=None) -> bool:
+    """gloo collectives take host tensors: CUDA buffers are staged through host memory (the
+    single-GPU multi-rank test mode); NCCL moves device buffers directly over NVLink."""
+    import torch.distributed as dist
+
+    return dist.get_backend(group) == "gloo"
+
+
+def all_reduce(t: torch.Tensor, op=None, group=None) -> torch.Tensor:
+    """In-place all-reduce of ``t`` (any device) over the group's backend; returns ``t``."""
+    import torch.distributed as dist
+
+    op = dist.ReduceOp.SUM if op is None else op
+    if t.is_cuda and _host_staged(group):
+        h = t.cpu()
+        dist.all_reduce(h, op=op, group=group)
+        t.copy_(h)
+    else:
+        dist.all_reduce(t, op=op, group=group)
+    return t
+
+
+def barrier(group=None, device_index=None) -> None:
+    import torch.distributed as dist
+
+    if dist.get_backend(group) == "nccl" and device_index is not None:
+        dist.barrier(group=group, device_ids=[device_index])
+    else:
+        dist.barrier(group=group)
+
+
 class TorchExchange:
-    """torch.distributed all-to-all (NCCL on GPUs, gloo on CPU)."""
+    """torch.distributed all-to-all: NCCL over NVLink on GPUs (device buffers), gloo on CPU (and
+    host-staged CUDA buffers when several ranks share one GPU for testing)."""
 
     def __init__(self, group=None):
         import torch.distributed as dist
@@ -56,19 +88,24 @@ class TorchExchange:
         self.dist = dist
         self.group = group
 
-    def counts(self, send_counts: torch.Tensor) -> torch.Tensor:
-        recv = torch.empty_like(send_counts)
-        self.dist.all_to_all_single(recv, send_counts, group=self.group)
+    def _a2a(self, recv, send, **kw):
+        if send.is_cuda and _host_staged(self.group):
+            r = torch.empty(recv.shape, dtype=recv.dtype)
+            self.dist.all_to_all_single(r, send.cpu(), group=self.group, **kw)
+            recv.copy_(r)
+        else:
+            self.dist.all_to_all_single(recv, send, group=self.group, **kw)
         return recv
+
+    def counts(self, send_counts: torch.Tensor) -> torch.Tensor:
+        return self._a2a(torch.empty_like(send_counts), send_counts)
 
     def records(self, send: torch.Tensor, send_splits, recv_splits) -> torch.Tensor:
         recv = torch.empty((sum(recv_splits), RECORD_DOUBLES), dtype=send.dtype, device=send.device)
-        self.dist.all_to_all_single(recv, send, output_split_sizes=list(recv_splits),
-                                    input_split_sizes=list(send_splits), group=self.group)
-        return recv
+        return self._a2a(recv, send, output_split_sizes=list(recv_splits), input_split_sizes=list(send_splits))
 
     def allgather_int(self, value: int, device) -> list:
-        t = torch.tensor([value], dtype=torch.int64, device=device)
+        t = torch.tensor([value], dtype=torch.int64, device="cpu" if _host_staged(self.group) else device)
         out = [torch.empty_like(t) for _ in range(self.dist.get_world_size(self.group))]
         self.dist.all_gather(out, t, group=self.group)
         return [int(x.item()) for x in out]
@@ -245,12 +282,12 @@ class ShardedBuild:
         stop.record()
         torch.cuda.synchronize()
         ms = torch.tensor([start.elapsed_time(stop) / steps], dtype=torch.float64, device=dev)
-        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+        all_reduce(ms, op=dist.ReduceOp.MAX)
         self.dm = keep
         h2d = sum(t.numel() * t.element_size() for t in h)
         d2h = sum(t.numel() * t.element_size() for t in o)
         tot = torch.tensor([h2d, d2h], dtype=torch.int64, device=dev)
-        dist.all_reduce(tot)
+        all_reduce(tot)
         return {"value": self.n_el / (float(ms.item()) / 1e3), "unit": "elements/s",
                 "h2d_bytes_per_step": int(tot[0]), "d2h_bytes_per_step": int(tot[1]),
                 "ms_per_step": float(ms.item()), "steps": steps,
