@@ -160,8 +160,15 @@ __device__ __forceinline__ int incident_sorted(int64_t cl, const int32_t *__rest
 
 constexpr int32_t HASH_EMPTY = INT32_MAX;
 constexpr int MAX_OFFDIAG_CONTRIB = 4;     // hex meshes: an edge is shared by at most 4 elements
-constexpr int COL_BLOCK = 64;              // columns per block (pattern: one thread per column)
-constexpr int EMIT_BLOCK = 128;            // emit: threads per COL_BLOCK columns
+#ifndef HX_COL_BLOCK
+#define HX_COL_BLOCK 64
+#endif
+#ifndef HX_EMIT_BLOCK
+#define HX_EMIT_BLOCK 128
+#endif
+constexpr int COL_BLOCK = HX_COL_BLOCK;    // columns per tile (pattern: one thread per column)
+constexpr int EMIT_BLOCK = HX_EMIT_BLOCK;  // emit: threads per tile
+static_assert(COL_BLOCK % 32 == 0 && COL_BLOCK <= 256, "tile = 1..8 warps of columns");
 
 // Bitonic sorting network on N register-resident keys, ascending.
 template <int N, typename K>
@@ -366,18 +373,28 @@ emit_kernel(SegTable T, int64_t col_lo, int64_t ncols, const int32_t *__restrict
     // scratch record offsets: column u has max(m_u - 1, 0) records (m_u = 0 for a node no element
     // references), laid out in tile order by the pattern pass -- warp 0 scans them
     if (threadIdx.x < 32) {
-        const int l = threadIdx.x, u0 = 2 * l, u1 = 2 * l + 1;
-        const int m0 = u0 < ncol ? s_m[u0] : 0, m1 = u1 < ncol ? s_m[u1] : 0;
-        const int off0 = m0 > 0 ? m0 - 1 : 0, off1 = m1 > 0 ? m1 - 1 : 0;
-        int incl = off0 + off1;
+        constexpr int PER = COL_BLOCK / 32;  // columns per lane, consecutive
+        const int l = threadIdx.x;
+        int off[PER], sum = 0;
+#pragma unroll
+        for (int i = 0; i < PER; ++i) {
+            const int u = PER * l + i;
+            const int m = u < ncol ? s_m[u] : 0;
+            off[i] = m > 0 ? m - 1 : 0;
+            sum += off[i];
+        }
+        int incl = sum;
 #pragma unroll
         for (int d = 1; d < 32; d <<= 1) {
             const int v = __shfl_up_sync(0xffffffffu, incl, d);
             if (l >= d) incl += v;
         }
-        const int excl = incl - off0 - off1;
-        s_rs[u0] = excl;
-        s_rs[u1] = excl + off0;
+        int run = incl - sum;
+#pragma unroll
+        for (int i = 0; i < PER; ++i) {
+            s_rs[PER * l + i] = run;
+            run += off[i];
+        }
         if (l == 31) s_rs[COL_BLOCK] = incl;
     }
     __syncthreads();

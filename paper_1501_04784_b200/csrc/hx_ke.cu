@@ -139,9 +139,12 @@ __device__ __forceinline__ void init_pack_smem(uint8_t *pi, uint8_t *pj) {
 }
 
 #ifndef HX_KE_MIN_BLOCKS
-#define HX_KE_MIN_BLOCKS 2
+#define HX_KE_MIN_BLOCKS 4
 #endif
-constexpr int GP_BLOCK = 256;                    // 32 elements x 8 Gauss points
+#ifndef HX_KE_BLOCK
+#define HX_KE_BLOCK 128
+#endif
+constexpr int GP_BLOCK = HX_KE_BLOCK;  // 16 elements x 8 Gauss points; 4 blocks x 128 regs/SM measured best
 constexpr int GP_WARPS = GP_BLOCK / 32;
 constexpr int GP_EL_PER_BLOCK = GP_BLOCK / 8;
 constexpr int GP_EL_PER_WARP = 4;
