@@ -431,15 +431,9 @@ emit_kernel(SegTable T, int64_t col_lo, int64_t ncols, const int32_t *__restrict
         }
         vals[o] = v;
     }
-    // off-diagonals: record q of tile position u is output entry s_start[u] + 1 + (q - s_rs[u])
-    for (int q = threadIdx.x; q < n_off; q += EMIT_BLOCK) {
-        const int u = s_col[q];
-        const int64_t o = s_start[u] + 1 + (q - s_rs[u]);
-        if (o >= capacity) continue;  // beyond capacity: the caller retries
-        const int2 rec = scratch[sb + q];
-        if (ROWS) row_idx[o] = rec.x;
-        if (!VALS) continue;
-        const uint32_t w = (uint32_t)rec.y;
+    // off-diagonals: record q of tile position u is output entry s_start[u] + 1 + (q - s_rs[u]).
+    // Two records per thread per iteration: their KE gathers are independent and overlap.
+    auto offdiag_value = [&](int u, uint32_t w) -> double {
         const int n = (int)(w & 7u);
         const int32_t *ent = s_adj + 8 * u;
         double x[MAX_OFFDIAG_CONTRIB];
@@ -461,7 +455,25 @@ emit_kernel(SegTable T, int64_t col_lo, int64_t ncols, const int32_t *__restrict
                 if (r < n) sum = __dadd_rn(sum, x[r]);
             v = __dadd_rn(x[0], sum);
         }
-        vals[o] = v;
+        return v;
+    };
+    for (int q0 = threadIdx.x; q0 < n_off; q0 += 2 * EMIT_BLOCK) {
+        const int q1 = q0 + EMIT_BLOCK;
+        const bool has1 = q1 < n_off;
+        const int u0 = s_col[q0], u1 = has1 ? s_col[q1] : 0;
+        const int64_t o0 = s_start[u0] + 1 + (q0 - s_rs[u0]);
+        const int64_t o1 = has1 ? s_start[u1] + 1 + (q1 - s_rs[u1]) : capacity;
+        const int2 rec0 = scratch[sb + q0];
+        const int2 rec1 = has1 ? scratch[sb + q1] : make_int2(0, 0);
+        if (ROWS) {
+            if (o0 < capacity) row_idx[o0] = rec0.x;
+            if (o1 < capacity) row_idx[o1] = rec1.x;
+        }
+        if (!VALS) continue;
+        const double v0 = offdiag_value(u0, (uint32_t)rec0.y);
+        const double v1 = has1 ? offdiag_value(u1, (uint32_t)rec1.y) : 0.0;
+        if (o0 < capacity) vals[o0] = v0;  // beyond capacity: the caller retries
+        if (o1 < capacity) vals[o1] = v1;
     }
 }
 
