@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define HX_ABI_VERSION 1
+#define HX_ABI_VERSION 2  /* 2: flags argument of hx_mesh_csc_symbolic/build, hx_mesh_csc_emit, hx_block_* */
 
 /* Status codes (host return values).  The Python layer maps them onto the reference
  * exception hierarchy (errors.py:4-59). */
