@@ -299,7 +299,9 @@ pattern_kernel(SegTable T, int64_t col_lo, int64_t ncols, const int32_t *__restr
                     ++cnt;
                 }
             }
-            if (cnt <= 16) sort_list<16, K>(L, cnt);
+            // one network per warp: a warp with any column above 16 rows sorts all with 32 keys
+            // (a divergent warp would otherwise run both networks)
+            if (!__any_sync(__activemask(), cnt > 16)) sort_list<16, K>(L, cnt);
             else sort_list<32, K>(L, cnt);
             m = 1 + cnt;
         }
