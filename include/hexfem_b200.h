@@ -180,6 +180,16 @@ int hx_halo_count(const int32_t *conn, int64_t n_el, const int64_t *col_bounds, 
 int hx_halo_pack(const int32_t *conn, const double *ke, int64_t n_el, const int64_t *col_bounds, int32_t world,
                  int32_t self, double *records, const void *workspace, void *stream);
 
+/* send: the fused pack-and-send -- the same records as hx_halo_pack, written straight into each
+ *       destination d's receive buffer dest_ptrs[d] (device array of world pointers: peer memory
+ *       mapped through CUDA IPC, or local buffers) starting at record dest_offsets[d] (device array)
+ *       = the number of records lower ranks send to d.  Requires hx_halo_count's workspace.
+ *       The caller orders the receivers' reads after every sender's kernel (a stream-ordered
+ *       barrier). */
+int hx_halo_send(const int32_t *conn, const double *ke, int64_t n_el, const int64_t *col_bounds, int32_t world,
+                 int32_t self, double *const *dest_ptrs, const int64_t *dest_offsets, const void *workspace,
+                 void *stream);
+
 /* ---- column blocks of one GPU (out-of-core build, Eq. 10 beyond HBM) ---------------------------
  * select: ids (n_el capacity) i64 device <- ascending ids of the elements with a node in
  *         [col_lo, col_hi); *count (device) = their number.  Stable: the block's elements keep the

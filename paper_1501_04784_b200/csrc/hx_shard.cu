@@ -17,6 +17,7 @@
 #include <thrust/iterator/counting_iterator.h>
 
 #include <algorithm>
+#include <cstring>
 
 #include "hx_common.cuh"
 
@@ -102,6 +103,52 @@ __global__ void halo_totals_kernel(const int64_t *__restrict__ offsets, const in
         const int64_t first = offsets[(int64_t)d * n_tiles];
         const int64_t last = offsets[(int64_t)d * n_tiles + n_tiles - 1] + counts[(int64_t)d * n_tiles + n_tiles - 1];
         per_dest[d] = last - first;
+    }
+}
+
+// Fused pack-and-send (the dispatch of the all-to-all done by the producer over NVLink): each warp
+// takes its 32 elements one destination at a time, and the warp's records for that destination --
+// contiguous at the receiver -- are written cooperatively with coalesced 8-byte stores straight into
+// the destination rank's receive buffer (a peer pointer opened from its IPC handle, or a local
+// buffer in the loopback).  The receiver's buffer layout is the one the NCCL all-to-all produces:
+// source ranks in ascending order, ascending element order within each source.
+__global__ void __launch_bounds__(SHARD_TILE)
+halo_send_kernel(const int32_t *__restrict__ conn, const double *__restrict__ ke, int64_t n_el,
+                 const int64_t *__restrict__ bounds, int world, int self, int64_t n_tiles,
+                 const int64_t *__restrict__ offsets, double *const *__restrict__ dest_ptrs,
+                 const int64_t *__restrict__ dest_offsets) {
+    __shared__ int32_t s_warp[MAX_WORLD][SHARD_TILE / 32];
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const int64_t e = (int64_t)blockIdx.x * SHARD_TILE + t;
+    const uint32_t m = e < n_el ? dest_mask(conn, e, bounds, world, self) : 0u;
+    uint32_t ballots[MAX_WORLD];
+    for (int d = 0; d < world; ++d) {
+        ballots[d] = __ballot_sync(0xffffffffu, (m >> d) & 1u);
+        if (lane == 0) s_warp[d][warp] = __popc(ballots[d]);
+    }
+    __syncthreads();
+    const int64_t e0 = (int64_t)blockIdx.x * SHARD_TILE + warp * 32;
+    for (int d = 0; d < world; ++d) {
+        const uint32_t b = ballots[d];
+        const int k = __popc(b);
+        if (k == 0) continue;
+        int before = 0;
+        for (int w = 0; w < warp; ++w) before += s_warp[d][w];
+        // record slot of this warp's first record for d, in d's receive buffer
+        const int64_t slot0 = dest_offsets[d] + (offsets[(int64_t)d * n_tiles + blockIdx.x] - offsets[(int64_t)d * n_tiles]) + before;
+        double *dst = dest_ptrs[d] + 40 * slot0;
+        for (int f = lane; f < 40 * k; f += 32) {
+            const int i = f / 40, word = f - 40 * i;
+            const int64_t el = e0 + __fns(b, 0, i + 1);  // the warp's i-th record: (i+1)-th set bit
+            double v;
+            if (word < 36) {
+                v = __ldg(ke + 36 * el + word);
+            } else {
+                const int2 ids = __ldg(reinterpret_cast<const int2 *>(conn + 8 * el) + (word - 36));
+                v = __hiloint2double(ids.y, ids.x);  // bit copy of two int32 node ids
+            }
+            dst[f] = v;
+        }
     }
 }
 
@@ -244,6 +291,23 @@ extern "C" int hx_halo_count(const int32_t *conn, int64_t n_el, const int64_t *c
     HX_TRY_CUDA(cub::DeviceScan::ExclusiveSum(w.cub_tmp, cb, w.counts, w.offsets, (int)(n_tiles * world), s));
     halo_totals_kernel<<<1, MAX_WORLD, 0, s>>>(w.offsets, w.counts, world, n_tiles, per_dest);
     HX_CHECK_LAUNCH("halo_totals_kernel");
+    return HX_OK;
+}
+
+extern "C" int hx_halo_send(const int32_t *conn, const double *ke, int64_t n_el, const int64_t *col_bounds,
+                            int32_t world, int32_t self, double *const *dest_ptrs, const int64_t *dest_offsets,
+                            const void *workspace, void *stream) {
+    if (n_el < 0 || world < 1 || world > MAX_WORLD || workspace == nullptr || dest_ptrs == nullptr ||
+        dest_offsets == nullptr) {
+        set_last_error("hx_halo_send: bad arguments");
+        return HX_ERR_VALUE;
+    }
+    if (n_el == 0) return HX_OK;
+    ShardWs w = shard_ws_layout(const_cast<void *>(workspace), n_el, world);
+    const int64_t n_tiles = ceil_div(n_el, SHARD_TILE);
+    halo_send_kernel<<<(unsigned)n_tiles, SHARD_TILE, 0, (cudaStream_t)stream>>>(
+        conn, ke, n_el, col_bounds, world, self, n_tiles, w.offsets, dest_ptrs, dest_offsets);
+    HX_CHECK_LAUNCH("halo_send_kernel");
     return HX_OK;
 }
 

@@ -31,7 +31,7 @@ import numpy as np
 import torch
 
 __all__ = ["element_ranges", "column_bounds", "ShardedBuild", "TorchExchange", "LoopbackExchange", "CudaOps",
-           "run_loopback", "RECORD_DOUBLES", "all_reduce", "barrier"]
+           "run_loopback", "run_loopback_p2p", "P2PExchange", "RECORD_DOUBLES", "all_reduce", "barrier"]
 
 RECORD_DOUBLES = 40  # 36 packed KE values + 8 int32 node ids
 
@@ -111,6 +111,87 @@ class TorchExchange:
         return [int(x.item()) for x in out]
 
 
+class P2PExchange:
+    """The all-to-all done by the producer: every rank maps every other rank's receive buffer
+    (CUDA IPC through torch's storage sharing -- NVLink peer memory between GPUs, the same memory
+    between processes sharing a GPU) and hx_halo_send writes the records straight into them.  Only
+    the G x G count matrix goes through the process group (one all-gather); a stream-ordered
+    barrier (an NCCL all-reduce of one word; a host barrier under gloo) orders the receivers'
+    reads after every sender's kernel."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.buf = None        # own receive buffer (records, 40 doubles each)
+        self.peers = None      # tensors mapping every rank's buffer (own included)
+        self.ptrs = None       # device int64 array of the peer base pointers
+
+    def _ensure_capacity(self, need: int, device):
+        """Grow the receive buffer when needed; whenever any rank grows, all ranks re-map."""
+        grow = self.buf is None or self.buf.shape[0] < need
+        flag = torch.tensor([1 if grow else 0], dtype=torch.int64)
+        if self.dist.get_backend(self.group) != "gloo":
+            flag = flag.to(device)
+        self.dist.all_reduce(flag, op=self.dist.ReduceOp.MAX, group=self.group)
+        if int(flag.item()) == 0:
+            return
+        if grow:
+            self.buf = torch.empty((max(need + need // 4, 1024), RECORD_DOUBLES), dtype=torch.float64, device=device)
+        meta = self.buf.untyped_storage()._share_cuda_()
+        metas = [None] * self.world
+        self.dist.all_gather_object(metas, meta, group=self.group)
+        self.peers = []
+        for r, m in enumerate(metas):
+            if r == self.rank:
+                self.peers.append(self.buf)
+            else:
+                st = torch.UntypedStorage._new_shared_cuda(*m)
+                self.peers.append(torch.empty(0, dtype=torch.float64, device=device).set_(st))
+        self.ptrs = torch.tensor([p.data_ptr() for p in self.peers], dtype=torch.int64, device=device)
+
+    def prepare(self, send_counts, device):
+        """-> (dest_ptrs, dest_offsets (device int64), recv_counts host list, receive view)"""
+        mine = torch.tensor(send_counts, dtype=torch.int64)
+        rows = [torch.empty_like(mine) for _ in range(self.world)]
+        if self.dist.get_backend(self.group) == "gloo":
+            self.dist.all_gather(rows, mine, group=self.group)
+        else:
+            dev_rows = [torch.empty(self.world, dtype=torch.int64, device=device) for _ in range(self.world)]
+            self.dist.all_gather(dev_rows, mine.to(device), group=self.group)
+            rows = [r.cpu() for r in dev_rows]
+        C = torch.stack(rows).numpy()  # C[s][d] records s -> d
+        recv_counts = [int(C[s][self.rank]) for s in range(self.world)]
+        self._ensure_capacity(int(sum(recv_counts)), device)
+        offsets = torch.tensor([int(C[:self.rank, d].sum()) for d in range(self.world)], dtype=torch.int64,
+                               device=device)
+        return self.ptrs, offsets, recv_counts, self.buf[:sum(recv_counts)]
+
+    def barrier(self, device):
+        if self.dist.get_backend(self.group) == "gloo":
+            torch.cuda.synchronize(device)
+            self.dist.barrier(group=self.group)
+        else:
+            t = torch.zeros(1, dtype=torch.int32, device=device)
+            self.dist.all_reduce(t, group=self.group)  # stream-ordered: after every rank's send kernel
+
+    def counts(self, send_counts):  # the ShardedBuild e2e helpers use the process group directly
+        raise NotImplementedError
+
+    def allgather_int(self, value: int, device) -> list:
+        t = torch.tensor([value], dtype=torch.int64)
+        out = [torch.empty_like(t) for _ in range(self.world)]
+        if self.dist.get_backend(self.group) == "gloo":
+            self.dist.all_gather(out, t, group=self.group)
+            return [int(x.item()) for x in out]
+        dev_out = [torch.empty(1, dtype=torch.int64, device=device) for _ in range(self.world)]
+        self.dist.all_gather(dev_out, t.to(device), group=self.group)
+        return [int(x.item()) for x in dev_out]
+
+
 # ------------------------------------------------------------------------------------------
 # per-rank compute (CUDA)
 # ------------------------------------------------------------------------------------------
@@ -137,22 +218,37 @@ class CudaOps:
     def check_fail(self, fail, offset):
         self.D.raise_if_failed(fail, offset)
 
-    def halo(self, dm, ke, bounds_dev, world, rank):
-        """-> (records (S, 40) f64, per_dest (world,) int64 host list)"""
+    def halo_count(self, dm, bounds_dev, world, rank):
+        """-> (per_dest (world,) int64 host list, workspace) -- hx_halo_count."""
         from . import _native as N
 
         n = dm.n_el
         ws_bytes = N.lib().hx_halo_workspace_bytes(n, world)
         ws = torch.empty(ws_bytes, dtype=torch.uint8, device=self.device)
         per_dest = torch.empty(world, dtype=torch.int64, device=self.device)
-        sh = self.D.stream_handle()
         N.check(N.lib().hx_halo_count(self.D._ptr(dm.conn), n, self.D._ptr(bounds_dev), world, rank,
-                                      self.D._ptr(per_dest), self.D._ptr(ws), ws_bytes, sh), "hx_halo_count")
-        counts = per_dest.cpu().tolist()
+                                      self.D._ptr(per_dest), self.D._ptr(ws), ws_bytes, self.D.stream_handle()),
+                "hx_halo_count")
+        return per_dest.cpu().tolist(), ws
+
+    def halo(self, dm, ke, bounds_dev, world, rank):
+        """-> (records (S, 40) f64 destination-major send buffer, per_dest host list)"""
+        from . import _native as N
+
+        counts, ws = self.halo_count(dm, bounds_dev, world, rank)
         records = torch.empty((max(sum(counts), 0), RECORD_DOUBLES), dtype=torch.float64, device=self.device)
-        N.check(N.lib().hx_halo_pack(self.D._ptr(dm.conn), self.D._ptr(ke), n, self.D._ptr(bounds_dev), world, rank,
-                                     self.D._ptr(records), self.D._ptr(ws), sh), "hx_halo_pack")
+        N.check(N.lib().hx_halo_pack(self.D._ptr(dm.conn), self.D._ptr(ke), dm.n_el, self.D._ptr(bounds_dev), world,
+                                     rank, self.D._ptr(records), self.D._ptr(ws), self.D.stream_handle()),
+                "hx_halo_pack")
         return records, counts
+
+    def halo_send(self, dm, ke, bounds_dev, world, rank, dest_ptrs, dest_offsets, ws):
+        """Fused pack-and-send: records straight into the destinations' receive buffers."""
+        from . import _native as N
+
+        N.check(N.lib().hx_halo_send(self.D._ptr(dm.conn), self.D._ptr(ke), dm.n_el, self.D._ptr(bounds_dev), world,
+                                     rank, self.D._ptr(dest_ptrs), self.D._ptr(dest_offsets), self.D._ptr(ws),
+                                     self.D.stream_handle()), "hx_halo_send")
 
     def bounds(self, bounds_np):
         return torch.from_numpy(bounds_np).to(self.device)
@@ -218,10 +314,23 @@ class ShardedBuild:
         return self.last
 
     def step(self):
+        if isinstance(self.exchange, P2PExchange):
+            return self.step_p2p()
         records, send_counts = self.phase_local()
         dev = records.device
         recv_counts = self.exchange.counts(torch.tensor(send_counts, dtype=torch.int64, device=dev)).cpu().tolist()
         recv = self.exchange.records(records, send_counts, recv_counts)
+        return self.phase_assemble(recv, recv_counts)
+
+    def step_p2p(self):
+        """Integrate, count, map the destinations, fused pack-and-send, barrier, assemble."""
+        dev = self.ops.device
+        ke, rows, cols, fail = self.ops.integrate(self.dm)
+        send_counts, ws = self.ops.halo_count(self.dm, self.bounds, self.world, self.rank)
+        ptrs, offsets, recv_counts, recv = self.exchange.prepare(send_counts, dev)
+        self.ops.halo_send(self.dm, ke, self.bounds, self.world, self.rank, ptrs, offsets, ws)
+        self.exchange.barrier(dev)
+        self._pending = (ke, rows, cols, fail)
         return self.phase_assemble(recv, recv_counts)
 
     def global_nnz(self) -> int:
@@ -237,10 +346,18 @@ class ShardedBuild:
             ev[0].record()
             ke, rows, cols, fail = self.ops.integrate(self.dm)
             ev[1].record()
-            records, send_counts = self.ops.halo(self.dm, ke, self.bounds, self.world, self.rank)
-            dev = records.device
-            recv_counts = self.exchange.counts(torch.tensor(send_counts, dtype=torch.int64, device=dev)).cpu().tolist()
-            recv = self.exchange.records(records, send_counts, recv_counts)
+            if isinstance(self.exchange, P2PExchange):
+                dev = self.ops.device
+                send_counts, ws = self.ops.halo_count(self.dm, self.bounds, self.world, self.rank)
+                ptrs, offsets, recv_counts, recv = self.exchange.prepare(send_counts, dev)
+                self.ops.halo_send(self.dm, ke, self.bounds, self.world, self.rank, ptrs, offsets, ws)
+                self.exchange.barrier(dev)
+            else:
+                records, send_counts = self.ops.halo(self.dm, ke, self.bounds, self.world, self.rank)
+                dev = records.device
+                recv_counts = self.exchange.counts(torch.tensor(send_counts, dtype=torch.int64,
+                                                                device=dev)).cpu().tolist()
+                recv = self.exchange.records(records, send_counts, recv_counts)
             ev[2].record()
             self._pending = (ke, rows, cols, fail)
             self.phase_assemble(recv, recv_counts)
@@ -315,6 +432,38 @@ def run_loopback(mesh, world: int, ops_factory):
             recv_counts.append(int(counts[r]))
         recv = torch.cat(parts) if parts else sends[r][0][:0]
         results.append(rk.phase_assemble(recv, recv_counts))
+    off = 0
+    for res in results:
+        res.nnz_offset = off
+        off += int(res.row_idx.shape[0])
+    return results
+
+
+def run_loopback_p2p(mesh, world: int, ops_factory):
+    """G virtual ranks in one process with the fused pack-and-send: each rank's hx_halo_send writes
+    into the other ranks' receive buffers (local memory here, peer memory across GPUs)."""
+    ranks = [ShardedBuild(mesh, r, world, ops=ops_factory(), exchange=LoopbackExchange()) for r in range(world)]
+    local = []
+    C = np.zeros((world, world), dtype=np.int64)
+    for r, rk in enumerate(ranks):
+        ke, rows, cols, fail = rk.ops.integrate(rk.dm)
+        counts, ws = rk.ops.halo_count(rk.dm, rk.bounds, world, r)
+        C[r] = counts
+        local.append((ke, rows, cols, fail, ws))
+    dev = ranks[0].ops.device
+    bufs = [torch.full((max(int(C[:, d].sum()), 1), RECORD_DOUBLES), float("nan"), dtype=torch.float64, device=dev)
+            for d in range(world)]
+    ptrs = torch.tensor([b.data_ptr() for b in bufs], dtype=torch.int64, device=dev)
+    for r, rk in enumerate(ranks):
+        offsets = torch.tensor([int(C[:r, d].sum()) for d in range(world)], dtype=torch.int64, device=dev)
+        ke, _, _, _, ws = local[r]
+        rk.ops.halo_send(rk.dm, ke, rk.bounds, world, r, ptrs, offsets, ws)
+    results = []
+    for r, rk in enumerate(ranks):
+        ke, rows, cols, fail, _ = local[r]
+        rk._pending = (ke, rows, cols, fail)
+        recv_counts = [int(C[s][r]) for s in range(world)]
+        results.append(rk.phase_assemble(bufs[r][:sum(recv_counts)], recv_counts))
     off = 0
     for res in results:
         res.nnz_offset = off

@@ -7,7 +7,7 @@ import torch
 
 from common import bits_equal, golden_mesh
 from paper_1501_04784_b200 import device as D
-from paper_1501_04784_b200.distributed import CudaOps, concat_blocks, run_loopback
+from paper_1501_04784_b200.distributed import CudaOps, concat_blocks, run_loopback, run_loopback_p2p
 from paper_1501_04784_b200.pipeline import build_device
 from paper_1501_04784_b200.workloads import make_workload, permuted_mesh, perturbed_mesh
 
@@ -45,3 +45,15 @@ def test_loopback_c2_scale():
     cp1, ri1, vv1 = single(mesh)
     assert bits_equal(cp, cp1) and bits_equal(ri, ri1) and bits_equal(vv, vv1)
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("world", [2, 3, 8])
+@pytest.mark.parametrize("kind", ["structured", "permuted"])
+def test_loopback_fused_send_bitwise(world, kind):
+    """hx_halo_send (pack-and-send into the destinations' buffers) == the NCCL-path layout, bitwise."""
+    mesh = perturbed_mesh(9, seed=world + 40)
+    if kind == "permuted":
+        mesh = permuted_mesh(mesh, seed=world + 50)
+    cp, ri, vv = concat_blocks(run_loopback_p2p(mesh, world, lambda: CudaOps()))
+    cp1, ri1, vv1 = single(mesh)
+    assert bits_equal(cp, cp1) and bits_equal(ri, ri1) and bits_equal(vv, vv1)
