@@ -221,7 +221,8 @@ def numbering_is_local(conn: torch.Tensor, n_nodes: int, sample: int = 4096) -> 
     n = conn.shape[0]
     if n == 0 or n_nodes < 1 << 16:
         return True
-    idx = torch.linspace(0, n - 1, min(sample, n), device=conn.device).long()
+    k = min(sample, n)
+    idx = torch.arange(k, dtype=torch.int64, device=conn.device) * (n - 1) // max(k - 1, 1)
     rows = conn[idx]
     span = (rows.max(dim=1).values - rows.min(dim=1).values).double().mean()
     return bool(span.item() < n_nodes / 64)

@@ -406,3 +406,14 @@ def test_out_of_core_degenerate_and_budget(golden):
     m, report = run_build(good, budget_bytes=10**12, device_budget_bytes=budget)
     assert bits_equal(m.vals, golden["m345_vals"]) and bits_equal(m.row_idx, golden["m345_row_idx"])
     assert abs(report.pct_integration + report.pct_assembly - 100.0) < 1e-9
+
+
+def test_numbering_heuristic_large_index_range():
+    """The locality probe samples element rows by index: exact at 64M elements (no float rounding)."""
+    n = 64_000_000
+    conn = torch.zeros((n, 8), dtype=torch.int32, device="cuda")
+    conn[-1] = torch.arange(8, dtype=torch.int32, device="cuda") * 1_000_000
+    assert D.numbering_is_local(conn, 64_481_201) in (True, False)
+    torch.cuda.synchronize()
+    del conn
+    torch.cuda.empty_cache()
