@@ -202,6 +202,13 @@ int hx_block_select(const int32_t *conn, int64_t n_el, int64_t col_lo, int64_t c
 int hx_block_gather(const int32_t *conn, const double *coeff, const int64_t *ids, const int64_t *count,
                     int64_t capacity, int32_t *conn_out, double *coeff_out, void *stream);
 
+/* ---- Matrix Market export (sparseio.py:73-87), host code -----------------------------------------
+ * Host arrays of a lower CSC -> "%%MatrixMarket matrix coordinate real symmetric" file, 1-based,
+ * column-major, "%.17g" values: byte-identical to the reference's writer, formatted by `threads`
+ * worker threads (<= 0: all hardware threads). */
+int hx_mm_write(const int64_t *col_ptr, const int64_t *row_idx, const double *vals, int64_t dim, const char *path,
+                int32_t threads);
+
 #ifdef __cplusplus
 }
 #endif

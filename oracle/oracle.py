@@ -170,3 +170,12 @@ def reduceat_model(run):
     if len(run) == 1:
         return float(run[0])
     return float(run[0]) + pairwise_sum(run[1:])
+
+
+def export_matrix_market_text(col_ptr, row_idx, vals, dim) -> str:
+    """sparseio.py:73-87 restated: the reference writer's exact text."""
+    out = ["%%MatrixMarket matrix coordinate real symmetric", f"{dim} {dim} {len(row_idx)}"]
+    for col in range(dim):
+        for k in range(col_ptr[col], col_ptr[col + 1]):
+            out.append(f"{row_idx[k] + 1} {col + 1} {vals[k]:.17g}")
+    return "\n".join(out) + "\n"

@@ -51,6 +51,7 @@ from .integrate import (
     required_bytes,
 )
 from .mesh import Mesh, StructuredGridSpec, generate_cube_mesh, validate_mesh
+from .sparseio import export_matrix_market, import_matrix_market
 from .pipeline import (
     BuildReport,
     build_device,

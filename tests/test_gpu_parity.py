@@ -417,3 +417,18 @@ def test_numbering_heuristic_large_index_range():
     torch.cuda.synchronize()
     del conn
     torch.cuda.empty_cache()
+
+
+def test_matrix_market_round_trip(tmp_path, golden):
+    """export (native writer) -> import (reference line rules, GPU triplet_to_csc) reproduces K."""
+    from paper_1501_04784_b200 import LowerCscMatrix, MeshFormatError, export_matrix_market, import_matrix_market
+
+    m = LowerCscMatrix(golden["perm5_col_ptr"], golden["perm5_row_idx"], golden["perm5_vals"],
+                       golden["perm5_coords"].shape[0])
+    path = tmp_path / "k.mtx"
+    export_matrix_market(m, path)
+    back = import_matrix_market(path)
+    assert host_csc_equal(back, m)
+    path.write_text("%%MatrixMarket matrix coordinate real symmetric\n3 3 1\n1 2 4.0\n")
+    with pytest.raises(MeshFormatError, match="above the diagonal"):
+        import_matrix_market(path)
