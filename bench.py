@@ -379,7 +379,7 @@ def measure_kernels(args, rank, world, runner, dm):
         ev[0].record()
         D.integrate_mesh(dm, ke=ke, rows=rows, cols=cols, mode=args.mode)
         ev[1].record()
-        csc = D.mesh_csc([(dm.conn, ke)], dm.n_nodes)
+        csc = D.mesh_csc([(dm.conn, ke)], dm.n_nodes, order=dm.assembly_order())
         ev[2].record()
         torch.cuda.synchronize()
         if it:  # first pass warms the allocator
