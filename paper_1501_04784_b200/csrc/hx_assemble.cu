@@ -409,7 +409,7 @@ emit_kernel(SegTable T, int64_t col_lo, int64_t ncols, const int32_t *__restrict
     for (int u = threadIdx.x; u < ncol; u += EMIT_BLOCK) {
         const int64_t o = s_start[u];
         if (s_m[u] == 0 || o >= capacity) continue;
-        if (ROWS) row_idx[o] = col_lo + s_cl[u];
+        if (ROWS) __stcs(reinterpret_cast<long long *>(row_idx) + o, (long long)(col_lo + s_cl[u]));
         if (!VALS) continue;
         const int deg = s_deg[u];
         const int32_t *ent = s_adj + 8 * u;
@@ -431,7 +431,7 @@ emit_kernel(SegTable T, int64_t col_lo, int64_t ncols, const int32_t *__restrict
                 if (k < deg) sum = __dadd_rn(sum, x[k]);
             v = __dadd_rn(x[0], sum);
         }
-        vals[o] = v;
+        __stcs(vals + o, v);
     }
     // off-diagonals: record q of tile position u is output entry s_start[u] + 1 + (q - s_rs[u]).
     // Two records per thread per iteration: their KE gathers are independent and overlap.
@@ -465,17 +465,17 @@ emit_kernel(SegTable T, int64_t col_lo, int64_t ncols, const int32_t *__restrict
         const int u0 = s_col[q0], u1 = has1 ? s_col[q1] : 0;
         const int64_t o0 = s_start[u0] + 1 + (q0 - s_rs[u0]);
         const int64_t o1 = has1 ? s_start[u1] + 1 + (q1 - s_rs[u1]) : capacity;
-        const int2 rec0 = scratch[sb + q0];
-        const int2 rec1 = has1 ? scratch[sb + q1] : make_int2(0, 0);
+        const int2 rec0 = __ldcs(scratch + sb + q0);  // streamed once: evict first, keep KE in L2
+        const int2 rec1 = has1 ? __ldcs(scratch + sb + q1) : make_int2(0, 0);
         if (ROWS) {
-            if (o0 < capacity) row_idx[o0] = rec0.x;
-            if (o1 < capacity) row_idx[o1] = rec1.x;
+            if (o0 < capacity) __stcs(reinterpret_cast<long long *>(row_idx) + o0, (long long)rec0.x);
+            if (o1 < capacity) __stcs(reinterpret_cast<long long *>(row_idx) + o1, (long long)rec1.x);
         }
         if (!VALS) continue;
         const double v0 = offdiag_value(u0, (uint32_t)rec0.y);
         const double v1 = has1 ? offdiag_value(u1, (uint32_t)rec1.y) : 0.0;
-        if (o0 < capacity) vals[o0] = v0;  // beyond capacity: the caller retries
-        if (o1 < capacity) vals[o1] = v1;
+        if (o0 < capacity) __stcs(vals + o0, v0);  // beyond capacity: the caller retries
+        if (o1 < capacity) __stcs(vals + o1, v1);
     }
 }
 
