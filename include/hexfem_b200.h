@@ -202,6 +202,13 @@ int hx_block_select(const int32_t *conn, int64_t n_el, int64_t col_lo, int64_t c
 int hx_block_gather(const int32_t *conn, const double *coeff, const int64_t *ids, const int64_t *count,
                     int64_t capacity, int32_t *conn_out, double *coeff_out, void *stream);
 
+/* ---- structured box in device memory (mesh.py:73-98 generate_cube_mesh) --------------------------
+ * coords (n_nodes, 3) f64, conn (n_el, 8) i32, coeff (n_el,) f64: node (i,j,k) at (i h, j h, k h)
+ * with id i + j (nx+1) + k (nx+1)(ny+1), x-fastest elements, local order
+ * [0, 1, 1+sx, sx, L, 1+L, 1+sx+L, sx+L] -- bitwise the reference generator's arrays. */
+int hx_generate_cube_mesh(int64_t nx, int64_t ny, int64_t nz, double h, double c0, double *coords, int32_t *conn,
+                          double *coeff, void *stream);
+
 /* ---- Matrix Market export (sparseio.py:73-87), host code -----------------------------------------
  * Host arrays of a lower CSC -> "%%MatrixMarket matrix coordinate real symmetric" file, 1-based,
  * column-major, "%.17g" values: byte-identical to the reference's writer, formatted by `threads`

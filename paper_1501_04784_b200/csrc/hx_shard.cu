@@ -325,3 +325,52 @@ extern "C" int hx_halo_pack(const int32_t *conn, const double *ke, int64_t n_el,
     HX_CHECK_LAUNCH("halo_pack_kernel");
     return HX_OK;
 }
+
+// ---- structured box on the device (mesh.py:73-98: the mesh producer before the path) ------------
+namespace hx {
+__global__ void cube_nodes_kernel(int64_t sx, int64_t sy, int64_t n_nodes, double h, double *__restrict__ coords) {
+    for (int64_t id = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; id < n_nodes;
+         id += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = id % sx, j = (id / sx) % sy, k = id / (sx * sy);
+        coords[3 * id] = __dmul_rn((double)i, h);  // node (i, j, k) at (i h, j h, k h)
+        coords[3 * id + 1] = __dmul_rn((double)j, h);
+        coords[3 * id + 2] = __dmul_rn((double)k, h);
+    }
+}
+
+__global__ void cube_elements_kernel(int64_t nx, int64_t ny, int64_t n_el, double c0, int32_t *__restrict__ conn,
+                                     double *__restrict__ coeff) {
+    const int64_t sx = nx + 1, layer = sx * (ny + 1);
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n_el; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t ex = e % nx, ey = (e / nx) % ny, ez = e / (nx * ny);  // x-fastest element numbering
+        const int32_t o = (int32_t)(ex + ey * sx + ez * layer);
+        const int32_t s = (int32_t)sx, l = (int32_t)layer;
+        int4 *dst = reinterpret_cast<int4 *>(conn) + 2 * e;
+        dst[0] = make_int4(o, o + 1, o + 1 + s, o + s);               // ccw bottom face
+        dst[1] = make_int4(o + l, o + 1 + l, o + 1 + s + l, o + s + l);  // ccw top face
+        coeff[e] = c0;
+    }
+}
+}  // namespace hx
+
+extern "C" int hx_generate_cube_mesh(int64_t nx, int64_t ny, int64_t nz, double h, double c0, double *coords,
+                                     int32_t *conn, double *coeff, void *stream) {
+    if (nx < 1 || ny < 1 || nz < 1 || !(h > 0.0) || !(c0 > 0.0) || coords == nullptr || conn == nullptr ||
+        coeff == nullptr) {
+        set_last_error("hx_generate_cube_mesh: bad arguments");
+        return HX_ERR_VALUE;
+    }
+    const int64_t n_nodes = (nx + 1) * (ny + 1) * (nz + 1), n_el = nx * ny * nz;
+    if (n_nodes >= INT32_MAX) {
+        set_last_error("hx_generate_cube_mesh: %lld nodes exceed int32 ids", (long long)n_nodes);
+        return HX_ERR_CONFIG;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    cube_nodes_kernel<<<(unsigned)std::min<int64_t>(ceil_div(n_nodes, 256), 148 * 32), 256, 0, s>>>(nx + 1, ny + 1,
+                                                                                                  n_nodes, h, coords);
+    HX_CHECK_LAUNCH("cube_nodes_kernel");
+    cube_elements_kernel<<<(unsigned)std::min<int64_t>(ceil_div(n_el, 256), 148 * 32), 256, 0, s>>>(nx, ny, n_el, c0,
+                                                                                                  conn, coeff);
+    HX_CHECK_LAUNCH("cube_elements_kernel");
+    return HX_OK;
+}

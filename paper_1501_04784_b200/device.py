@@ -19,7 +19,7 @@ from .errors import ConfigurationError, DegenerateElementError, MeshValidationEr
 __all__ = [
     "DeviceMesh", "DeviceCsc", "require_device", "stream_handle", "integrate_mesh", "stiffness_batch",
     "connectivity_index_arrays", "raise_if_failed", "mesh_csc", "triplet_csc", "MeshPlan", "mesh_plan_async",
-    "mesh_emit", "block_elements",
+    "mesh_emit", "block_elements", "generate_cube_mesh",
 ]
 
 _FAIL_WORDS = 3  # hx_fail_info = {int64 element, int32 gp, int32 pad, double det} = 24 bytes
@@ -91,6 +91,20 @@ class DeviceMesh:
         if getattr(self, "_order", None) is None:
             self._order = "column" if numbering_is_local(self.conn, self.n_nodes) else "element"
         return self._order
+
+
+def generate_cube_mesh(spec, device=None, stream=None) -> DeviceMesh:
+    """mesh.py:73-98 generate_cube_mesh straight into HBM (hx_generate_cube_mesh): bitwise the
+    reference generator's coords / connectivity / coefficient, without the host arrays or the copy."""
+    dev = require_device(device)
+    nx, ny, nz = int(spec.nx), int(spec.ny), int(spec.nz)
+    n_nodes, n_el = (nx + 1) * (ny + 1) * (nz + 1), nx * ny * nz
+    coords = torch.empty((n_nodes, 3), dtype=torch.float64, device=dev)
+    conn = torch.empty((n_el, 8), dtype=torch.int32, device=dev)
+    coeff = torch.empty(n_el, dtype=torch.float64, device=dev)
+    N.check(N.lib().hx_generate_cube_mesh(nx, ny, nz, float(spec.h), float(spec.c0), _ptr(coords), _ptr(conn),
+                                          _ptr(coeff), stream_handle(stream)), "hx_generate_cube_mesh")
+    return DeviceMesh(coords, conn, coeff)
 
 
 def new_fail_record(device) -> torch.Tensor:

@@ -432,3 +432,16 @@ def test_matrix_market_round_trip(tmp_path, golden):
     path.write_text("%%MatrixMarket matrix coordinate real symmetric\n3 3 1\n1 2 4.0\n")
     with pytest.raises(MeshFormatError, match="above the diagonal"):
         import_matrix_market(path)
+
+
+@pytest.mark.parametrize("dims", [(1, 1, 1), (4, 3, 5), (37, 2, 9), (100, 100, 100)])
+def test_device_cube_generator_bitwise(dims):
+    """hx_generate_cube_mesh == generate_cube_mesh (mesh.py:73-98 numbering and coordinates)."""
+    from paper_1501_04784_b200 import StructuredGridSpec, generate_cube_mesh
+
+    spec = StructuredGridSpec(*dims, h=0.37, c0=1.7)
+    host = generate_cube_mesh(spec)
+    dm = D.generate_cube_mesh(spec)
+    assert bits_equal(dm.coords.cpu().numpy(), host.coords)
+    assert bits_equal(dm.conn.cpu().numpy(), host.connectivity)
+    assert bits_equal(dm.coeff.cpu().numpy(), host.coefficient)
