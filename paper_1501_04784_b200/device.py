@@ -19,7 +19,7 @@ from .errors import ConfigurationError, DegenerateElementError, MeshValidationEr
 __all__ = [
     "DeviceMesh", "DeviceCsc", "require_device", "stream_handle", "integrate_mesh", "stiffness_batch",
     "connectivity_index_arrays", "raise_if_failed", "mesh_csc", "triplet_csc", "MeshPlan", "mesh_plan_async",
-    "mesh_emit", "block_elements", "generate_cube_mesh",
+    "mesh_emit", "plan_assembly", "block_elements", "generate_cube_mesh",
 ]
 
 _FAIL_WORDS = 3  # hx_fail_info = {int64 element, int32 gp, int32 pad, double det} = 24 bytes
@@ -320,22 +320,25 @@ class MeshPlan:
     val_buf: torch.Tensor
     capacity: int
     flags: int = 0
+    nnz: int = -1  # known once the plan is verified (plan_assembly): emits then need no host sync
 
 
-def mesh_plan_async(conn: torch.Tensor, n_nodes: int, stream=None, order: str = "auto") -> MeshPlan:
+def mesh_plan_async(conn: torch.Tensor, n_nodes: int, stream=None, order: str = "auto", ws_bytes: int | None = None,
+                    capacity: int | None = None) -> MeshPlan:
     """Launch the symbolic phase of a single-segment mesh assembly on ``stream`` (no host sync).
     It reads only the connectivity, so it can run concurrently with the integration kernel."""
     n = conn.shape[0]
     if conn.dtype != torch.int32 or tuple(conn.shape) != (n, 8) or not conn.is_contiguous():
         raise ValueError("conn must be a contiguous CUDA int32 (n, 8) tensor")
     dev = conn.device
-    ws_bytes = N.lib().hx_mesh_csc_workspace_bytes(n, n_nodes)
+    if ws_bytes is None:
+        ws_bytes = N.lib().hx_mesh_csc_workspace_bytes(n, n_nodes)
     if ws_bytes < 0:
         raise ValueError("bad mesh size")
     ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
     status = torch.zeros(1, dtype=torch.int32, device=dev)
     col_ptr = torch.empty(n_nodes + 1, dtype=torch.int64, device=dev)
-    capacity = ROWS_PER_COLUMN_ESTIMATE * n_nodes
+    capacity = ROWS_PER_COLUMN_ESTIMATE * n_nodes if capacity is None else capacity
     row_buf = torch.empty(max(capacity, 1), dtype=torch.int64, device=dev)
     val_buf = torch.empty(max(capacity, 1), dtype=torch.float64, device=dev)
     segs = N.segments([(conn.data_ptr(), 0, n)])
@@ -346,14 +349,42 @@ def mesh_plan_async(conn: torch.Tensor, n_nodes: int, stream=None, order: str = 
     return MeshPlan(conn, n_nodes, col_ptr, ws, status, row_buf, val_buf, capacity, flags)
 
 
+def plan_assembly(dm: "DeviceMesh", order: str | None = None, stream=None):
+    """Verified symbolic plan of a mesh's assembly (pattern, sorted adjacency, contribution records),
+    reusable for rebuilds while the connectivity is unchanged -- new coordinates or coefficients
+    only need the integration kernel and one emit pass (``build_device(dm, plan=...)``).  Returns
+    None when the mesh is outside the node-adjacency fast path (rebuilds then use mesh_csc)."""
+    order = dm.assembly_order() if order is None else order
+    ws_bytes, capacity = None, None
+    while True:
+        plan = mesh_plan_async(dm.conn, dm.n_nodes, stream=stream, order=order, ws_bytes=ws_bytes, capacity=capacity)
+        head = torch.stack([plan.status.to(torch.int64)[0], plan.col_ptr[-1]]).cpu()
+        st, nnz = int(head[0]), int(head[1])
+        _status_error(st)
+        if st & N.ST_SCRATCH and not st & (N.ST_FASTPATH_LIMITS & ~N.ST_SCRATCH):
+            ws_bytes = N.lib().hx_mesh_csc_workspace_bytes(dm.n_el, dm.n_nodes) + 8 * nnz
+            continue
+        if st & N.ST_FASTPATH_LIMITS:
+            return None
+        if nnz > plan.capacity:
+            capacity = nnz
+            continue
+        plan.nnz = nnz
+        return plan
+
+
 def mesh_emit(plan: MeshPlan, ke: torch.Tensor, stream=None) -> DeviceCsc:
-    """Row indices and values of a planned assembly (one pass over the KE rows), then one host
-    sync for the status word and nnz.  Falls back to mesh_csc when the plan hit a limit."""
+    """Row indices and values of a planned assembly (one pass over the KE rows).  A verified plan
+    (plan_assembly) returns without a host sync -- the outputs live in the plan's buffers and are
+    overwritten by the next emit; otherwise one sync checks the status word and nnz and falls back
+    to mesh_csc when the plan hit a limit."""
     _check_segment(plan.conn, ke)
     segs = N.segments([(plan.conn.data_ptr(), ke.data_ptr(), plan.conn.shape[0])])
     N.check(N.lib().hx_mesh_csc_emit(segs, 1, 0, plan.n_nodes, _ptr(plan.col_ptr), _ptr(plan.row_buf),
                                      _ptr(plan.val_buf), plan.capacity, _ptr(plan.ws), _ptr(plan.status),
                                      stream_handle(stream)), "hx_mesh_csc_emit")
+    if plan.nnz >= 0:
+        return DeviceCsc(plan.col_ptr, plan.row_buf[:plan.nnz], plan.val_buf[:plan.nnz], plan.n_nodes, 0, "mesh")
     head = torch.stack([plan.status.to(torch.int64)[0], plan.col_ptr[-1]]).cpu()
     st, nnz = int(head[0]), int(head[1])
     _status_error(st)

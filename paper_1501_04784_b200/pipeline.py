@@ -83,6 +83,13 @@ class DeviceBuild:
     rows: torch.Tensor | None  # (36 n_el,) i32
     cols: torch.Tensor | None  # (36 n_el,) i32
     csc: D.DeviceCsc
+    fails: list | None = None  # hx_fail_info records of the integration launches
+
+    def check(self) -> "DeviceBuild":
+        """Raise DegenerateElementError for the lowest failing element (synchronises)."""
+        for f in self.fails or []:
+            D.raise_if_failed(f)
+        return self
 
 
 _SIDE_STREAMS: dict = {}
@@ -96,7 +103,8 @@ def _side_stream(dev) -> torch.cuda.Stream:
 
 
 def build_device(dm: D.DeviceMesh, mode: str = "exact", with_index: bool = True, ranges=None,
-                 ke=None, rows=None, cols=None, stream=None, overlap: bool = False) -> DeviceBuild:
+                 ke=None, rows=None, cols=None, stream=None, overlap: bool = False,
+                 plan: D.MeshPlan | None = None) -> DeviceBuild:
     """KE (+ fused iK/jK) for every element, then the lower CSC, all in HBM.
 
     The symbolic assembly reads only the connectivity, so with ``overlap`` it runs on a side
@@ -104,7 +112,8 @@ def build_device(dm: D.DeviceMesh, mode: str = "exact", with_index: bool = True,
     values, which needs KE) follows on the main stream.  Measured neutral to -1% on B200 (the
     integration kernel occupies the whole register file), so the default is one stream.  ``ranges`` is an optional BatchPlan-style
     list of element groups (each one kernel launch into the same output buffers); results are
-    bitwise independent of both.
+    bitwise independent of both.  ``plan`` (device.plan_assembly) reuses a verified symbolic plan of
+    the same connectivity: the rebuild is the integration kernel plus one emit pass, no host sync.
     """
     dev = dm.conn.device
     n = dm.n_el
@@ -114,8 +123,9 @@ def build_device(dm: D.DeviceMesh, mode: str = "exact", with_index: bool = True,
     if with_index:
         rows = torch.empty(36 * n, dtype=torch.int32, device=dev) if rows is None else rows
         cols = torch.empty(36 * n, dtype=torch.int32, device=dev) if cols is None else cols
+    cached = plan
     plan = None
-    if overlap and n > 0:
+    if cached is None and overlap and n > 0:
         side = _side_stream(dev)
         side.wait_stream(main)  # inputs and the buffers below are ordered before the plan
         plan = D.mesh_plan_async(dm.conn, dm.n_nodes, stream=side, order=dm.assembly_order())
@@ -127,14 +137,19 @@ def build_device(dm: D.DeviceMesh, mode: str = "exact", with_index: bool = True,
                                          cols=cols[36 * lo:36 * hi] if with_index else None,
                                          with_index=with_index, mode=mode, stream=main)
         fails.append(fail)
-    if plan is not None:
+    if cached is not None:
+        if cached.conn is not dm.conn:
+            raise ConfigurationError("the assembly plan belongs to another mesh")
+        csc = D.mesh_emit(cached, ke, stream=main)
+    elif plan is not None:
         main.wait_event(plan_done)
         csc = D.mesh_emit(plan, ke, stream=main)
     else:
         csc = D.mesh_csc([(dm.conn, ke)], dm.n_nodes, stream=main, order=dm.assembly_order())
-    for f in fails:
-        D.raise_if_failed(f)
-    return DeviceBuild(ke, rows if with_index else None, cols if with_index else None, csc)
+    if cached is None:  # a planned rebuild stays asynchronous: check the fail records later
+        for f in fails:
+            D.raise_if_failed(f)
+    return DeviceBuild(ke, rows if with_index else None, cols if with_index else None, csc, fails)
 
 
 def device_bytes(n_el: int, n_nodes: int, with_index: bool = True) -> int:

@@ -445,3 +445,26 @@ def test_device_cube_generator_bitwise(dims):
     assert bits_equal(dm.coords.cpu().numpy(), host.coords)
     assert bits_equal(dm.conn.cpu().numpy(), host.connectivity)
     assert bits_equal(dm.coeff.cpu().numpy(), host.coefficient)
+
+
+def test_planned_rebuild_new_coefficients():
+    """A verified plan (connectivity only) reused for a rebuild with new coordinates/coefficients
+    gives the one-shot build's bits; degenerate elements are still reported (DeviceBuild.check)."""
+    from paper_1501_04784_b200.pipeline import build_device
+
+    mesh = permuted_mesh(perturbed_mesh(12, seed=61), seed=62)
+    dm = D.DeviceMesh.from_host(mesh)
+    plan = D.plan_assembly(dm)
+    assert plan is not None and plan.nnz > 0
+    for seed in (1, 2):
+        rng = np.random.default_rng(seed)
+        dm.coeff.copy_(torch.from_numpy(rng.uniform(0.5, 2.0, size=mesh.n_el)))
+        warm = build_device(dm, plan=plan).check()
+        cold = build_device(D.DeviceMesh(dm.coords, dm.conn, dm.coeff.clone()))
+        assert bits_equal(warm.csc.vals.cpu().numpy(), cold.csc.vals.cpu().numpy())
+        assert bits_equal(warm.csc.row_idx.cpu().numpy(), cold.csc.row_idx.cpu().numpy())
+    flipped = dm.coords.clone()
+    dm2 = D.DeviceMesh(flipped, dm.conn, dm.coeff)
+    dm2.coords[:, 2] *= -1.0  # mirror: every det < 0
+    with pytest.raises(DegenerateElementError):
+        build_device(dm2, plan=plan).check()
