@@ -459,23 +459,34 @@ emit_kernel(SegTable T, int64_t col_lo, int64_t ncols, const int32_t *__restrict
         }
         return v;
     };
-    for (int q0 = threadIdx.x; q0 < n_off; q0 += 2 * EMIT_BLOCK) {
-        const int q1 = q0 + EMIT_BLOCK;
-        const bool has1 = q1 < n_off;
-        const int u0 = s_col[q0], u1 = has1 ? s_col[q1] : 0;
-        const int64_t o0 = s_start[u0] + 1 + (q0 - s_rs[u0]);
-        const int64_t o1 = has1 ? s_start[u1] + 1 + (q1 - s_rs[u1]) : capacity;
-        const int2 rec0 = __ldcs(scratch + sb + q0);  // streamed once: evict first, keep KE in L2
-        const int2 rec1 = has1 ? __ldcs(scratch + sb + q1) : make_int2(0, 0);
+#ifndef HX_EMIT_UNROLL
+#define HX_EMIT_UNROLL 4
+#endif
+    constexpr int R = HX_EMIT_UNROLL;  // records in flight per thread: their loads/gathers overlap
+    for (int q0 = threadIdx.x; q0 < n_off; q0 += R * EMIT_BLOCK) {
+        int u[R];
+        int64_t o[R];
+        int2 rec[R];
+#pragma unroll
+        for (int i = 0; i < R; ++i) {
+            const int q = q0 + i * EMIT_BLOCK;
+            const bool has = q < n_off;
+            u[i] = has ? s_col[q] : 0;
+            o[i] = has ? s_start[u[i]] + 1 + (q - s_rs[u[i]]) : capacity;
+            rec[i] = has ? __ldcs(scratch + sb + q) : make_int2(0, 0);  // streamed once: evict first
+        }
         if (ROWS) {
-            if (o0 < capacity) __stcs(reinterpret_cast<long long *>(row_idx) + o0, (long long)rec0.x);
-            if (o1 < capacity) __stcs(reinterpret_cast<long long *>(row_idx) + o1, (long long)rec1.x);
+#pragma unroll
+            for (int i = 0; i < R; ++i)
+                if (o[i] < capacity) __stcs(reinterpret_cast<long long *>(row_idx) + o[i], (long long)rec[i].x);
         }
         if (!VALS) continue;
-        const double v0 = offdiag_value(u0, (uint32_t)rec0.y);
-        const double v1 = has1 ? offdiag_value(u1, (uint32_t)rec1.y) : 0.0;
-        if (o0 < capacity) __stcs(vals + o0, v0);  // beyond capacity: the caller retries
-        if (o1 < capacity) __stcs(vals + o1, v1);
+        double v[R];
+#pragma unroll
+        for (int i = 0; i < R; ++i) v[i] = o[i] < capacity ? offdiag_value(u[i], (uint32_t)rec[i].y) : 0.0;
+#pragma unroll
+        for (int i = 0; i < R; ++i)
+            if (o[i] < capacity) __stcs(vals + o[i], v[i]);  // beyond capacity: the caller retries
     }
 }
 
