@@ -632,7 +632,8 @@ static int mesh_csc_build(const hx_elem_segment *segs, int32_t n_segs, int64_t n
     cudaStream_t s = (cudaStream_t)stream;
     const bool ordered = (flags & HX_CSC_ORDER_BY_ELEMENT) != 0 && ncols > 0 && n_total > 0;
     HX_TRY_CUDA(cudaMemsetAsync(status, 0, sizeof(uint32_t), s));
-    HX_TRY_CUDA(cudaMemsetAsync(w.order_flag, ordered ? 1 : 0, sizeof(uint32_t), s));
+    HX_TRY_CUDA(cudaMemsetAsync(w.order_flag, 0, sizeof(uint32_t), s));
+    if (ordered) HX_TRY_CUDA(cudaMemsetAsync(w.order_flag, 1, 1, s));  // little-endian u32 == 1
     if (ncols > 0) {
         HX_TRY_CUDA(cudaMemsetAsync(w.deg, 0, sizeof(int32_t) * ncols, s));
         if (n_total > 0) {
