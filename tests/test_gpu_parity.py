@@ -468,3 +468,31 @@ def test_planned_rebuild_new_coefficients():
     dm2.coords[:, 2] *= -1.0  # mirror: every det < 0
     with pytest.raises(DegenerateElementError):
         build_device(dm2, plan=plan).check()
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2, 3])
+def test_random_mesh_variants_full_pipeline_bitwise(seed):
+    """Shuffled element order, deleted elements (holes -> boundary columns and unreferenced nodes),
+    permuted node ids and random distortion/coefficients: the full pipeline (KE, iK/jK, CSC) stays
+    bitwise equal to the oracle."""
+    rng = np.random.default_rng(1000 + seed)
+    n = int(rng.integers(3, 11))
+    mesh = perturbed_mesh(n, seed=seed, distortion=0.2)
+    keep = rng.random(mesh.n_el) > 0.25
+    keep[0] = True
+    conn = mesh.connectivity[keep]
+    coeff = mesh.coefficient[keep] * np.exp(rng.uniform(-3, 3, size=keep.sum()))
+    order = rng.permutation(conn.shape[0])
+    conn, coeff = conn[order], coeff[order]
+    mesh = Mesh(mesh.coords, np.ascontiguousarray(conn), np.ascontiguousarray(coeff))
+    if seed % 2:
+        mesh = permuted_mesh(mesh, seed=seed + 7)
+    b = build_device(D.DeviceMesh.from_host(mesh))
+    ke, rows, cols, first, _, _ = oracle.stiffness_mesh(mesh.coords, mesh.connectivity, mesh.coefficient)
+    assert first == -1
+    cp, ri, vv = oracle.triplet_to_csc(rows, cols, ke.reshape(-1), mesh.n_nodes)
+    assert bits_equal(b.ke.cpu().numpy(), ke)
+    assert bits_equal(b.rows.cpu().numpy(), rows) and bits_equal(b.cols.cpu().numpy(), cols)
+    assert bits_equal(b.csc.col_ptr.cpu().numpy(), cp)
+    assert bits_equal(b.csc.row_idx.cpu().numpy(), ri)
+    assert bits_equal(b.csc.vals.cpu().numpy(), vv)
