@@ -496,3 +496,31 @@ def test_random_mesh_variants_full_pipeline_bitwise(seed):
     assert bits_equal(b.csc.col_ptr.cpu().numpy(), cp)
     assert bits_equal(b.csc.row_idx.cpu().numpy(), ri)
     assert bits_equal(b.csc.vals.cpu().numpy(), vv)
+
+
+@pytest.mark.parametrize("name", SMALL_MESHES)
+def test_symbolic_then_numeric_abi(golden, name):
+    """hx_mesh_csc_symbolic (pattern + rows) followed by hx_mesh_csc_numeric (values only) on the same
+    workspace: the reference's CSC."""
+    from paper_1501_04784_b200 import _native as N
+
+    mesh = golden_mesh(golden, name)
+    dm = D.DeviceMesh.from_host(mesh)
+    ke, _, _, fail = D.integrate_mesh(dm, with_index=False)
+    n, dim = mesh.n_el, mesh.n_nodes
+    ws_bytes = N.lib().hx_mesh_csc_workspace_bytes(n, dim)
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device="cuda")
+    status = torch.zeros(1, dtype=torch.int32, device="cuda")
+    col_ptr = torch.empty(dim + 1, dtype=torch.int64, device="cuda")
+    rows = torch.empty(36 * n, dtype=torch.int64, device="cuda")
+    segs = N.segments([(dm.conn.data_ptr(), ke.data_ptr(), n)])
+    sh = D.stream_handle()
+    N.check(N.lib().hx_mesh_csc_symbolic(segs, 1, dim, 0, dim, D._ptr(col_ptr), D._ptr(rows), 36 * n, D._ptr(ws),
+                                         ws_bytes, D._ptr(status), 0, sh), "symbolic")
+    nnz = int(col_ptr[-1].item())
+    vals = torch.empty(nnz, dtype=torch.float64, device="cuda")
+    N.check(N.lib().hx_mesh_csc_numeric(segs, 1, 0, dim, D._ptr(col_ptr), D._ptr(rows), D._ptr(vals), D._ptr(ws),
+                                        D._ptr(status), sh), "numeric")
+    assert int(status.item()) == 0
+    assert bits_equal(rows[:nnz].cpu().numpy(), golden[f"{name}_row_idx"])
+    assert bits_equal(vals.cpu().numpy(), golden[f"{name}_vals"])
