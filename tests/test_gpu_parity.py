@@ -524,3 +524,31 @@ def test_symbolic_then_numeric_abi(golden, name):
     assert int(status.item()) == 0
     assert bits_equal(rows[:nnz].cpu().numpy(), golden[f"{name}_row_idx"])
     assert bits_equal(vals.cpu().numpy(), golden[f"{name}_vals"])
+
+
+def _star_mesh(shared):
+    """8 elements around node 0; with shared=False they share only node 0 (56 distinct rows in
+    column 0 > the 32-slot fast path), with shared=True all 8 also share node 1 (edge (0, 1) carried
+    by 8 elements > 4 contributions)."""
+    rng = np.random.default_rng(5 if shared else 6)
+    conn = []
+    nxt = 2 if shared else 1
+    for e in range(8):
+        others = list(range(nxt, nxt + (6 if shared else 7)))
+        nxt += 6 if shared else 7
+        nodes = [0, 1] + others if shared else [0] + others
+        conn.append(nodes)
+    conn = np.array(conn, dtype=np.int32)
+    n_nodes = int(conn.max()) + 1
+    # geometry irrelevant for assembly: random values through the assembly-only entry point
+    return conn, n_nodes, rng.standard_normal((8, 36))
+
+
+@pytest.mark.parametrize("shared", [False, True])
+def test_fast_path_row_limits_fall_back_bitwise(shared):
+    conn, n_nodes, values = _star_mesh(shared)
+    mesh = Mesh(np.zeros((n_nodes, 3)), conn, np.ones(conn.shape[0]))
+    m = assemble_direct(mesh, LocalValuesBatch(values))
+    rows, cols = oracle.connectivity_index_arrays(conn)
+    cp, ri, vv = oracle.triplet_to_csc(rows, cols, values.reshape(-1), n_nodes)
+    assert bits_equal(m.col_ptr, cp) and bits_equal(m.row_idx, ri) and bits_equal(m.vals, vv)
