@@ -215,6 +215,11 @@ int hx_generate_cube_mesh(int64_t nx, int64_t ny, int64_t nz, double h, double c
  * worker threads (<= 0: all hardware threads). */
 int hx_mm_write(const int64_t *col_ptr, const int64_t *row_idx, const double *vals, int64_t dim, const char *path,
                 int32_t threads);
+/* Import (sparseio.py:90-138), host code: rows == NULL queries (n_rows, nnz); then fills rows/cols
+ * (0-based int32) and vals.  Returns 0 ok, 1 = outside the strict fast path (the caller re-reads with
+ * the reference's own rules), 2 = format error at *err_line (message in hx_last_error). */
+int hx_mm_read(const char *path, int64_t *n_rows, int64_t *nnz, int32_t *rows, int32_t *cols, double *vals,
+               int64_t *err_line);
 
 #ifdef __cplusplus
 }

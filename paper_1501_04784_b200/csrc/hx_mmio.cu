@@ -22,8 +22,12 @@ static void format_columns(const int64_t *col_ptr, const int64_t *row_idx, const
     out.reserve((size_t)(col_ptr[c1] - col_ptr[c0]) * 36);
     for (int64_t c = c0; c < c1; ++c)
         for (int64_t k = col_ptr[c]; k < col_ptr[c + 1]; ++k) {
-            const int n = snprintf(line, sizeof(line), "%lld %lld %.17g\n", (long long)(row_idx[k] + 1),
-                                   (long long)(c + 1), vals[k]);
+            // Python formats every NaN as "nan"; glibc prints a negative NaN as "-nan"
+            const double v = vals[k];
+            const int n = v != v ? snprintf(line, sizeof(line), "%lld %lld nan\n", (long long)(row_idx[k] + 1),
+                                             (long long)(c + 1))
+                                 : snprintf(line, sizeof(line), "%lld %lld %.17g\n", (long long)(row_idx[k] + 1),
+                                             (long long)(c + 1), v);
             out.append(line, (size_t)n);
         }
 }
@@ -79,4 +83,146 @@ extern "C" int hx_mm_write(const int64_t *col_ptr, const int64_t *row_idx, const
         rc = HX_ERR_VALUE;
     }
     return rc;
+}
+
+// ---- Matrix Market import (sparseio.py:90-138), strict fast path ------------------------------------
+// The reference splits the text with str.splitlines()/str.split() and converts with int()/float().
+// This parser accepts the strict subset those produce identically for files like the writer's: '\n'
+// line ends, ' ' / '\t' separators, decimal integers, and decimal/exponent floats or inf/nan (strtod
+// is correctly rounded, as float() is).  Anything else -- other whitespace or line breaks, signs on
+// indices, underscores, hex floats, ... -- returns HX_MM_FALLBACK and the caller re-reads the file
+// with the reference's own rules, so semantics (and error messages) never differ.
+#include <cerrno>
+#include <cmath>
+#include <cstdlib>
+
+namespace hx {
+enum { MM_OK = 0, MM_FALLBACK = 1, MM_ERROR = 2 };
+
+static bool is_sep(char c) { return c == ' ' || c == '\t'; }
+
+// next token of [p, end) (within one line); returns false at the end of the line
+static bool next_token(const char *&p, const char *end, const char *&tb, const char *&te) {
+    while (p < end && is_sep(*p)) ++p;
+    if (p >= end) return false;
+    tb = p;
+    while (p < end && !is_sep(*p)) ++p;
+    te = p;
+    return true;
+}
+
+static bool strict_int(const char *b, const char *e, long long &v) {
+    if (b >= e || e - b > 18) return false;
+    long long x = 0;
+    for (const char *q = b; q < e; ++q) {
+        if (*q < '0' || *q > '9') return false;
+        x = 10 * x + (*q - '0');
+    }
+    v = x;
+    return true;
+}
+
+static bool strict_double(const char *b, const char *e, double &v) {
+    char buf[64];
+    const size_t n = (size_t)(e - b);
+    if (n == 0 || n >= sizeof(buf)) return false;
+    memcpy(buf, b, n);
+    buf[n] = '\0';
+    // accepted alphabet: digits . e E + - and the words inf / nan (as the writer emits them)
+    const char *s = buf + ((buf[0] == '-' || buf[0] == '+') ? 1 : 0);
+    if (strcmp(s, "inf") != 0 && strcmp(s, "nan") != 0) {
+        for (const char *q = s; *q; ++q)
+            if (!((*q >= '0' && *q <= '9') || *q == '.' || *q == 'e' || *q == 'E' || *q == '+' || *q == '-'))
+                return false;
+        if (!((s[0] >= '0' && s[0] <= '9') || s[0] == '.')) return false;
+    }
+    char *endp = nullptr;
+    errno = 0;
+    v = strtod(buf, &endp);
+    return endp == buf + n;
+}
+}  // namespace hx
+
+// Parse `path`.  First call with rows == NULL to get the sizes (n_rows, nnz); then with buffers of
+// nnz entries.  Returns 0 (ok), 1 (fall back to the reference parser), 2 (format error at *err_line,
+// message in hx_last_error, mirroring sparseio.py's MeshFormatError).
+extern "C" int hx_mm_read(const char *path, int64_t *n_rows, int64_t *nnz, int32_t *rows, int32_t *cols, double *vals,
+                          int64_t *err_line) {
+    if (path == nullptr || n_rows == nullptr || nnz == nullptr || err_line == nullptr) return MM_FALLBACK;
+    FILE *f = fopen(path, "rb");
+    if (f == nullptr) return MM_FALLBACK;
+    std::string text;
+    {
+        char chunk[1 << 16];
+        size_t got;
+        while ((got = fread(chunk, 1, sizeof(chunk), f)) > 0) text.append(chunk, got);
+        fclose(f);
+    }
+    for (char c : text)
+        if (c == '\r' || c == '\v' || c == '\f' || (unsigned char)c >= 0x1c && (unsigned char)c <= 0x1e ||
+            (unsigned char)c >= 0x80)
+            return MM_FALLBACK;  // other line breaks / non-ASCII: the reference's splitlines rules
+    const char *p = text.data(), *end = p + text.size();
+    int64_t line_no = 0;
+    auto next_line = [&](const char *&lb, const char *&le) -> bool {
+        if (p >= end) return false;
+        lb = p;
+        const char *nl = (const char *)memchr(p, '\n', (size_t)(end - p));
+        le = nl ? nl : end;
+        p = nl ? nl + 1 : end;
+        ++line_no;
+        return true;
+    };
+    const char *lb, *le, *tb, *te;
+    if (!next_line(lb, le)) return MM_FALLBACK;  // empty file: the reference's error path
+    {  // banner, case-insensitive tokens
+        static const char *want[5] = {"%%matrixmarket", "matrix", "coordinate", "real", "symmetric"};
+        const char *q = lb;
+        for (int k = 0; k < 5; ++k) {
+            if (!next_token(q, le, tb, te) || (size_t)(te - tb) != strlen(want[k])) return MM_FALLBACK;
+            for (size_t i = 0; i < strlen(want[k]); ++i)
+                if (tolower((unsigned char)tb[i]) != want[k][i]) return MM_FALLBACK;
+        }
+        if (next_token(q, le, tb, te)) return MM_FALLBACK;
+    }
+    // comments, then the size line
+    do {
+        if (!next_line(lb, le)) return MM_FALLBACK;
+    } while (le > lb && lb[0] == '%');
+    long long nr, nc, nz;
+    {
+        const char *q = lb;
+        if (!next_token(q, le, tb, te) || !strict_int(tb, te, nr)) return MM_FALLBACK;
+        if (!next_token(q, le, tb, te) || !strict_int(tb, te, nc)) return MM_FALLBACK;
+        if (!next_token(q, le, tb, te) || !strict_int(tb, te, nz)) return MM_FALLBACK;
+        if (next_token(q, le, tb, te)) return MM_FALLBACK;
+    }
+    if (nr != nc || nr > INT32_MAX) return MM_FALLBACK;
+    *n_rows = nr;
+    *nnz = nz;
+    if (rows == nullptr) return MM_OK;  // size query
+    for (long long k = 0; k < nz; ++k) {
+        if (!next_line(lb, le)) return MM_FALLBACK;  // too few entries: reference error path
+        const char *q = lb;
+        long long r, c;
+        double v;
+        if (!next_token(q, le, tb, te) || !strict_int(tb, te, r)) return MM_FALLBACK;
+        if (!next_token(q, le, tb, te) || !strict_int(tb, te, c)) return MM_FALLBACK;
+        if (!next_token(q, le, tb, te) || !strict_double(tb, te, v)) return MM_FALLBACK;
+        if (next_token(q, le, tb, te)) return MM_FALLBACK;
+        if (!(1 <= r && r <= nr && 1 <= c && c <= nc)) {
+            *err_line = line_no;
+            set_last_error("entry (%lld, %lld) outside the matrix", r, c);
+            return MM_ERROR;
+        }
+        if (r < c) {
+            *err_line = line_no;
+            set_last_error("entry (%lld, %lld) lies above the diagonal; symmetric storage is lower-triangular", r, c);
+            return MM_ERROR;
+        }
+        rows[k] = (int32_t)(r - 1);
+        cols[k] = (int32_t)(c - 1);
+        vals[k] = v;
+    }
+    return MM_OK;
 }

@@ -429,6 +429,9 @@ def test_matrix_market_round_trip(tmp_path, golden):
     export_matrix_market(m, path)
     back = import_matrix_market(path)
     assert host_csc_equal(back, m)
+    crlf = tmp_path / "crlf.mtx"  # outside the native reader's strict subset: the reference's rules
+    crlf.write_bytes(path.read_bytes().replace(b"\n", b"\r\n"))
+    assert host_csc_equal(import_matrix_market(crlf), m)
     path.write_text("%%MatrixMarket matrix coordinate real symmetric\n3 3 1\n1 2 4.0\n")
     with pytest.raises(MeshFormatError, match="above the diagonal"):
         import_matrix_market(path)
