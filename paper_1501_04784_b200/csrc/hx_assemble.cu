@@ -27,6 +27,7 @@
 #include <cub/device/device_scan.cuh>
 
 #include <algorithm>
+#include <cstdlib>
 #include <type_traits>
 
 #include "hx_common.cuh"
@@ -203,47 +204,24 @@ __device__ __forceinline__ void sort_list(K *L, int n) {
 
 __device__ __forceinline__ uint32_t hash_slot(int32_t v) { return ((uint32_t)v * 0x9E3779B1u) >> 27; }
 
-// 2. Pattern pass: one thread per column, COL_BLOCK columns per block.
-//   - incident elements sorted by id and written back to the adjacency (the emit pass reads them
-//     in order);
-//   - distinct rows > c in a 32-slot open-addressing hash set (smem, [slot][thread] layout); every
-//     slot carries its contribution word: count (3 bits) + up to 4 (incident k, local node b) pairs
-//     appended in ascending element order;
-//   - occupied slots compacted in place to keys (row << 5 | slot) -- 32-bit when n_nodes <= 2^26,
-//     else 64-bit -- and sorted by a 16- or 32-key register network;
-//   - m = 1 + distinct rows -> col_ptr[cl] (the exclusive scan turns counts into offsets);
-//   - sorted off-diagonal records (row, word) -> a compact scratch region reserved per block with
-//     one atomic (every block records where its records start).
-template <typename K, bool SINGLE>
-__global__ void __launch_bounds__(COL_BLOCK)
-pattern_kernel(SegTable T, int64_t col_lo, int64_t ncols, const int32_t *__restrict__ deg_arr,
-               int32_t *__restrict__ adj, int64_t *__restrict__ col_ptr, int2 *__restrict__ scratch,
-               int64_t scratch_capacity, unsigned long long *__restrict__ scratch_top,
-               int64_t *__restrict__ block_scratch, uint32_t *__restrict__ status,
-               const uint32_t *__restrict__ order) {
-    __shared__ int32_t sH[MAXR * COL_BLOCK];   // hash keys
-    __shared__ uint32_t sW[MAXR * COL_BLOCK];  // contribution words, by hash slot
-    // compacted / sorted keys (row << 5 | slot): 32-bit keys reuse the hash-key array in place
-    __shared__ K sL[sizeof(K) == 4 ? 1 : MAXR * COL_BLOCK];
-    __shared__ unsigned long long s_base;
-    using BlockScan = cub::BlockScan<int32_t, COL_BLOCK>;
-    __shared__ typename BlockScan::TempStorage scan_tmp;
-    const int t = threadIdx.x;
-    const int64_t idx = (int64_t)blockIdx.x * COL_BLOCK + t;  // position in the processing order
-    const int64_t cl = order != nullptr && idx < ncols ? (int64_t)__ldg(order + idx) : idx;
-    const int32_t c = (int32_t)(col_lo + cl);
-    int32_t *H = sH + t;
-    uint32_t *W = sW + t;
-    K *L = sizeof(K) == 4 ? reinterpret_cast<K *>(sH) + t : sL + t;
-
-    int m = 0, deg = 0;
-    int32_t ent[8];
-    if (cl < ncols) {
+// Pattern of one column (the calling thread's): sorted incident list (written back to the adjacency
+// when WRITE_ADJ), distinct rows r > c in the hash set H with contribution words W[slot], then the
+// occupied keys compacted into L as (row << 5 | slot) and sorted.  Returns m = 1 + rows (0 for an
+// empty column or one outside the fast path, with a status bit).  H, W, L: this thread's slices of
+// the [slot][thread] shared arrays.
+template <typename K, bool SINGLE, bool WRITE_ADJ>
+__device__ __forceinline__ int column_pattern(const SegTable &T, bool active, int64_t cl, int32_t c,
+                                              const int32_t *__restrict__ deg_arr, int32_t *__restrict__ adj,
+                                              int32_t *H, uint32_t *W, K *L, int32_t (&ent)[8], int &deg,
+                                              uint32_t *__restrict__ status) {
+    int m = 0;
+    deg = 0;
+    if (active) {
         deg = incident_sorted(cl, deg_arr, adj, ent, status);
         if (deg < 0) deg = 0;
 #pragma unroll
         for (int k = 0; k < 8; ++k)
-            if (k < deg) adj[8 * cl + k] = ent[k];
+            if (WRITE_ADJ && k < deg) adj[8 * cl + k] = ent[k];
     }
     if (deg > 0) {
 #pragma unroll
@@ -306,6 +284,45 @@ pattern_kernel(SegTable T, int64_t col_lo, int64_t ncols, const int32_t *__restr
             m = 1 + cnt;
         }
     }
+    return m;
+}
+
+// 2. Pattern pass: one thread per column, COL_BLOCK columns per block.
+//   - incident elements sorted by id and written back to the adjacency (the emit pass reads them
+//     in order);
+//   - distinct rows > c in a 32-slot open-addressing hash set (smem, [slot][thread] layout); every
+//     slot carries its contribution word: count (3 bits) + up to 4 (incident k, local node b) pairs
+//     appended in ascending element order;
+//   - occupied slots compacted in place to keys (row << 5 | slot) -- 32-bit when n_nodes <= 2^26,
+//     else 64-bit -- and sorted by a 16- or 32-key register network;
+//   - m = 1 + distinct rows -> col_ptr[cl] (the exclusive scan turns counts into offsets);
+//   - sorted off-diagonal records (row, word) -> a compact scratch region reserved per block with
+//     one atomic (every block records where its records start).
+template <typename K, bool SINGLE>
+__global__ void __launch_bounds__(COL_BLOCK)
+pattern_kernel(SegTable T, int64_t col_lo, int64_t ncols, const int32_t *__restrict__ deg_arr,
+               int32_t *__restrict__ adj, int64_t *__restrict__ col_ptr, int2 *__restrict__ scratch,
+               int64_t scratch_capacity, unsigned long long *__restrict__ scratch_top,
+               int64_t *__restrict__ block_scratch, uint32_t *__restrict__ status,
+               const uint32_t *__restrict__ order) {
+    __shared__ int32_t sH[MAXR * COL_BLOCK];   // hash keys
+    __shared__ uint32_t sW[MAXR * COL_BLOCK];  // contribution words, by hash slot
+    // compacted / sorted keys (row << 5 | slot): 32-bit keys reuse the hash-key array in place
+    __shared__ K sL[sizeof(K) == 4 ? 1 : MAXR * COL_BLOCK];
+    __shared__ unsigned long long s_base;
+    using BlockScan = cub::BlockScan<int32_t, COL_BLOCK>;
+    __shared__ typename BlockScan::TempStorage scan_tmp;
+    const int t = threadIdx.x;
+    const int64_t idx = (int64_t)blockIdx.x * COL_BLOCK + t;  // position in the processing order
+    const int64_t cl = order != nullptr && idx < ncols ? (int64_t)__ldg(order + idx) : idx;
+    const int32_t c = (int32_t)(col_lo + cl);
+    int32_t *H = sH + t;
+    uint32_t *W = sW + t;
+    K *L = sizeof(K) == 4 ? reinterpret_cast<K *>(sH) + t : sL + t;
+
+    int32_t ent[8];
+    int deg = 0;
+    const int m = column_pattern<K, SINGLE, true>(T, cl < ncols, cl, c, deg_arr, adj, H, W, L, ent, deg, status);
     if (cl < ncols) col_ptr[cl] = m;
 
     // compact scratch: this block's off-diagonal records
@@ -489,6 +506,7 @@ emit_kernel(SegTable T, int64_t col_lo, int64_t ncols, const int32_t *__restrict
             if (o[i] < capacity) __stcs(vals + o[i], v[i]);  // beyond capacity: the caller retries
     }
 }
+
 
 // Workspace layout (all offsets 256-B aligned):
 //   order_flag u32 | deg (ncols) i32 | adj (8*ncols) i32 | block_scratch (blocks) i64 |
