@@ -10,7 +10,9 @@
  *
  * All device buffers are caller-owned (the reference's `out=` convention,
  * integrate.py:93-99); scratch is a caller-provided workspace sized by the *_workspace_bytes
- * queries.  The library allocates nothing.
+ * queries.  The library allocates nothing.  Arrays of length zero may be passed as NULL
+ * (what allocators hand out for empty tensors); zero-size calls are valid no-ops that still
+ * write their status / fail words.
  *
  * Reference interfaces replaced (file:line under /root/reference/pkg/src/hexfem/):
  *   hx_stiffness_batch             element.py:213-245 stiffness_batch / integrate.py:84-131

@@ -691,7 +691,7 @@ extern "C" int hx_integrate_mesh(const double *coords, int64_t n_nodes, const in
                                  int32_t *rows, int32_t *cols, int32_t mode, hx_fail_info *fail,
                                  void *stream) {
     (void)n_nodes;
-    if (lo < 0 || hi < lo || ke == nullptr || fail == nullptr || (rows == nullptr) != (cols == nullptr)) {
+    if (lo < 0 || hi < lo || (hi > lo && ke == nullptr) || fail == nullptr || (rows == nullptr) != (cols == nullptr)) {
         set_last_error("hx_integrate_mesh: bad arguments (lo=%lld hi=%lld)", (long long)lo, (long long)hi);
         return HX_ERR_VALUE;
     }
@@ -723,7 +723,7 @@ extern "C" int hx_integrate_mesh(const double *coords, int64_t n_nodes, const in
 
 extern "C" int hx_stiffness_batch(const double *coords, const double *coeff, int64_t n, double *out,
                                   int32_t mode, hx_fail_info *fail, void *stream) {
-    if (n < 0 || out == nullptr || fail == nullptr) {
+    if (n < 0 || (n > 0 && out == nullptr) || fail == nullptr) {
         set_last_error("hx_stiffness_batch: bad arguments (n=%lld)", (long long)n);
         return HX_ERR_VALUE;
     }
@@ -751,7 +751,7 @@ extern "C" int hx_stiffness_batch(const double *coords, const double *coeff, int
 
 extern "C" int hx_connectivity_index_arrays(const int32_t *conn, int64_t lo, int64_t hi, int32_t *rows,
                                             int32_t *cols, void *stream) {
-    if (lo < 0 || hi < lo || rows == nullptr || cols == nullptr) {
+    if (lo < 0 || hi < lo || (hi > lo && (rows == nullptr || cols == nullptr))) {
         set_last_error("hx_connectivity_index_arrays: bad arguments");
         return HX_ERR_VALUE;
     }

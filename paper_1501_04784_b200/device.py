@@ -211,15 +211,21 @@ def _status_error(st: int):
         raise MeshValidationError("triplet entry above the diagonal")
 
 
+def _row_stride(t: torch.Tensor, width: int) -> int:
+    """Row stride of an (n, width) tensor; a single row's stride is meaningless (numpy's [None]
+    gives it 0), so it is the dense width there."""
+    return t.stride(0) if t.shape[0] > 1 else width
+
+
 def _check_segment(conn, ke):
     n = conn.shape[0]
     if conn.dtype != torch.int32 or tuple(conn.shape) != (n, 8) or conn.device.type != "cuda":
         raise ValueError("segment conn must be a CUDA int32 (n, 8) tensor")
     if ke.dtype != torch.float64 or tuple(ke.shape) != (n, 36) or ke.device.type != conn.device.type:
         raise ValueError("segment ke must be a CUDA float64 (n, 36) tensor")
-    if n and (conn.stride(1) != 1 or conn.stride(0) % 4 or conn.stride(0) < 8 or conn.data_ptr() % 16):
+    if n and (conn.stride(1) != 1 or _row_stride(conn, 8) % 4 or _row_stride(conn, 8) < 8 or conn.data_ptr() % 16):
         raise ValueError("segment conn rows must be 16-byte aligned with unit inner stride")
-    if n and (ke.stride(1) != 1 or ke.stride(0) < 36):
+    if n and (ke.stride(1) != 1 or _row_stride(ke, 36) < 36):
         raise ValueError("segment ke rows must have unit inner stride")
 
 
@@ -270,7 +276,8 @@ def mesh_csc(parts, n_nodes: int, col_lo: int = 0, col_hi: int | None = None, st
         _check_segment(conn, ke)
     n_total = sum(int(c.shape[0]) for c, _ in parts)
     ncols = col_hi - col_lo
-    segs = N.segments([(c.data_ptr(), k.data_ptr(), int(c.shape[0]), c.stride(0), k.stride(0)) for c, k in parts])
+    segs = N.segments([(c.data_ptr(), k.data_ptr(), int(c.shape[0]), _row_stride(c, 8), _row_stride(k, 36))
+                       for c, k in parts])
     flags = _order_flags(order, parts[0][0], n_nodes)
     ws_bytes = N.lib().hx_mesh_csc_workspace_bytes(n_total, ncols)
     if ws_bytes < 0:

@@ -586,3 +586,54 @@ def test_full_size_column_windows_bitwise(config):
         assert bits_equal(b.csc.vals[a:z].cpu().numpy(), vv)
     del b, dm
     torch.cuda.empty_cache()
+
+
+def test_empty_and_single_element_meshes():
+    """Edge sizes the reference accepts: zero elements (test_assemble.py:212-222 empty-triplet rule,
+    stiffness_batch -> (0, 36), assemble_direct -> all-zero col_ptr; run_build rejects it through
+    plan_batches, integrate.py:70-71) and a single unit-cube element (test_element.py:133-136)."""
+    empty = Mesh(np.zeros((5, 3)), np.empty((0, 8), np.int32), np.empty(0))
+    assert stiffness_batch(np.empty((0, 8, 3)), np.empty(0)).shape == (0, 36)
+    r, c = connectivity_index_arrays(empty)
+    assert r.dtype == np.int32 and r.size == 0 and c.size == 0
+    for m in (assemble_direct(empty, LocalValuesBatch(np.empty((0, 36)))),
+              triplet_to_csc(build_triplet(empty, LocalValuesBatch(np.empty((0, 36)))))):
+        assert m.dim == 5 and np.array_equal(m.col_ptr, np.zeros(6, np.int64)) and m.nnz == 0
+        assert m.row_idx.dtype == np.int64 and m.vals.dtype == np.float64
+    dm = D.DeviceMesh.from_host(empty)
+    ke, _, _, fail = D.integrate_mesh(dm)
+    D.raise_if_failed(fail)
+    assert tuple(ke.shape) == (0, 36)
+    assert np.array_equal(D.mesh_csc([(dm.conn, ke)], dm.n_nodes).col_ptr.cpu().numpy(), np.zeros(6, np.int64))
+    with pytest.raises(ValueError):
+        run_build(empty, 1 << 20)
+
+    corners = np.array([(0, 0, 0), (1, 0, 0), (1, 1, 0), (0, 1, 0), (0, 0, 1), (1, 0, 1), (1, 1, 1), (0, 1, 1)],
+                       float)
+    one = Mesh(corners, np.arange(8, dtype=np.int32)[None], np.ones(1))
+    ke_ref, rows, cols, first, _, _ = oracle.stiffness_mesh(one.coords, one.connectivity, one.coefficient)
+    cp, ri, vv = oracle.triplet_to_csc(rows, cols, ke_ref.reshape(-1), 8)
+    for assembler in ("direct", "triplet"):
+        m, rep = run_build(one, 1 << 20, assembler=assembler)
+        assert rep.nnz_csc == 36 and rep.n_el == 1
+        assert bits_equal(m.col_ptr, cp) and bits_equal(m.row_idx, ri) and bits_equal(m.vals, vv)
+
+
+def test_generic_triplet_path_beyond_int32_triplets():
+    """C4 through the triplet assembler: 36 * 64M = 2.30e9 triplets (> 2^31, 64-bit offsets in the
+    sort, run detection and pairwise gather) must give the same CSC, bit for bit, as the fused
+    direct path (itself checked against the oracle by test_full_size_column_windows_bitwise)."""
+    mesh = make_workload("C4")
+    dm = D.DeviceMesh.from_host(mesh)
+    del mesh
+    ke, rows, cols, fail = D.integrate_mesh(dm, with_index=True)
+    D.raise_if_failed(fail)
+    assert rows.shape[0] > 2**31
+    direct = D.mesh_csc([(dm.conn, ke)], dm.n_nodes)
+    d_ptr, d_rows, d_vals = direct.col_ptr, direct.row_idx.to(torch.int32), direct.vals
+    del direct
+    torch.cuda.empty_cache()
+    trip = D.triplet_csc(rows, cols, ke.view(-1), dm.n_nodes)
+    assert torch.equal(trip.col_ptr, d_ptr)
+    assert torch.equal(trip.row_idx.to(torch.int32), d_rows)
+    assert torch.equal(trip.vals.view(torch.int64), d_vals.view(torch.int64))
