@@ -36,7 +36,8 @@
 extern "C" {
 #endif
 
-#define HX_ABI_VERSION 2  /* 2: flags argument of hx_mesh_csc_symbolic/build, hx_mesh_csc_emit, hx_block_* */
+#define HX_ABI_VERSION 3  /* 2: flags argument of hx_mesh_csc_symbolic/build, hx_mesh_csc_emit, hx_block_*
+                           * 3: hx_integrate_mesh_adjacency + HX_CSC_ADJACENCY_READY (fused first pass) */
 
 /* Status codes (host return values).  The Python layer maps them onto the reference
  * exception hierarchy (errors.py:4-59). */
@@ -55,6 +56,9 @@ extern "C" {
 #define HX_ST_SCRATCH_OVERFLOW 32u /* pattern scratch too small (> 15 off-diagonals per column on average):
                                     * col_ptr is complete; re-run with workspace_bytes +=
                                     * 8 * col_ptr[ncols] */
+#define HX_ST_SLOT_COLLISION 64u /* HX_CSC_ADJACENCY_READY build: two elements hold one node at the same
+                                   * local index, so the fixed-slot adjacency lost an entry: re-run the
+                                   * build without the flag (the atomic adjacency pass) */
 /* DEG/ROW/REPEATED mean "mesh fast path not applicable": the caller re-runs the generic triplet
  * path (hx_triplet_csc_*), which has no such limits.  With any of the four bits set the entry
  * points write no row_idx / vals. */
@@ -67,6 +71,9 @@ extern "C" {
                                    * sort): for numberings without locality (e.g. randomly permuted
                                    * node ids) the pattern and emit passes then gather nearby
                                    * elements; results are identical either way */
+#define HX_CSC_ADJACENCY_READY 2  /* hx_mesh_csc_build only: the workspace's node adjacency and the status
+                                   * word were filled by hx_integrate_mesh_adjacency over every element
+                                   * (one segment, columns [0, n_nodes)); the build skips its first pass */
 
 /* Integration modes. */
 #define HX_MODE_EXACT 0 /* reference operation order, no FMA: bitwise equal to the reference */
@@ -119,6 +126,19 @@ int hx_stiffness_batch(const double *coords, const double *coeff, int64_t n, dou
 int hx_integrate_mesh(const double *coords, int64_t n_nodes, const int32_t *conn,
                       const double *coeff, int64_t lo, int64_t hi, double *ke, int32_t *rows,
                       int32_t *cols, int32_t mode, hx_fail_info *fail, void *stream);
+
+/* hx_integrate_mesh fused with the first pass of the mesh-path assembly: the kernel also records
+ * each node's incident (element << 3 | local node) slots in the adjacency section of a mesh-CSC
+ * workspace (hx_mesh_csc_workspace_bytes(n_el, n_nodes) bytes) -- element e puts (e << 3 | a) in
+ * slot a of its local node a, no atomics -- and validates node ids into csc_status
+ * (HX_ST_BAD_INDEX).  reset != 0 empties the slots and zeroes the status first (the first element
+ * range of a build).  Follow with hx_mesh_csc_build(...,
+ * flags | HX_CSC_ADJACENCY_READY) on the same workspace and status.  Element ids must fit the
+ * int32 adjacency: 8 * hi < 2^31. */
+int hx_integrate_mesh_adjacency(const double *coords, int64_t n_nodes, const int32_t *conn,
+                                const double *coeff, int64_t lo, int64_t hi, double *ke, int32_t *rows,
+                                int32_t *cols, int32_t mode, hx_fail_info *fail, void *csc_workspace,
+                                int64_t workspace_bytes, uint32_t *csc_status, int32_t reset, void *stream);
 
 /* assemble.py:86-93 alone: rows/cols (36*(hi-lo),) i32 for elements [lo, hi). */
 int hx_connectivity_index_arrays(const int32_t *conn, int64_t lo, int64_t hi, int32_t *rows,

@@ -20,16 +20,18 @@ LIB_PATH = Path(os.environ.get("HEXFEM_B200_LIB") or Path(__file__).resolve().pa
 
 HX_OK, HX_ERR_VALUE, HX_ERR_CONFIG, HX_ERR_CUDA, HX_ERR_WORKSPACE = 0, 1, 2, 3, 4
 ST_DEG_OVERFLOW, ST_ROW_OVERFLOW, ST_REPEATED_NODE, ST_BAD_INDEX, ST_UPPER, ST_SCRATCH = 1, 2, 4, 8, 16, 32
+ST_SLOT_COLLISION = 64
 ST_FASTPATH_LIMITS = ST_DEG_OVERFLOW | ST_ROW_OVERFLOW | ST_REPEATED_NODE | ST_SCRATCH
 MODE_EXACT, MODE_FAST = 0, 1
 CSC_ORDER_BY_ELEMENT = 1
+CSC_ADJACENCY_READY = 2
 MAX_SEGMENTS = 4
 
 # Every symbol declared in include/hexfem_b200.h (checked by tests/test_abi_cpu.py).
 EXPORTED = (
     "hx_abi_version", "hx_last_error", "hx_dn_table", "hx_pack_tables", "hx_device_sm_count",
     "hx_selftest_division",
-    "hx_stiffness_batch", "hx_integrate_mesh", "hx_connectivity_index_arrays",
+    "hx_stiffness_batch", "hx_integrate_mesh", "hx_integrate_mesh_adjacency", "hx_connectivity_index_arrays",
     "hx_mesh_csc_workspace_bytes", "hx_mesh_csc_symbolic", "hx_mesh_csc_build", "hx_mesh_csc_numeric",
     "hx_mesh_csc_emit",
     "hx_triplet_csc_workspace_bytes", "hx_triplet_csc_symbolic", "hx_triplet_csc_numeric",
@@ -75,6 +77,7 @@ def lib():
         "hx_selftest_division": ([ctypes.c_uint64, ctypes.c_uint64, P, P], ctypes.c_int),
         "hx_stiffness_batch": ([P, P, I64, P, I32, P, P], ctypes.c_int),
         "hx_integrate_mesh": ([P, I64, P, P, I64, I64, P, P, P, I32, P, P], ctypes.c_int),
+        "hx_integrate_mesh_adjacency": ([P, I64, P, P, I64, I64, P, P, P, I32, P, P, I64, P, I32, P], ctypes.c_int),
         "hx_connectivity_index_arrays": ([P, I64, I64, P, P, P], ctypes.c_int),
         "hx_mesh_csc_workspace_bytes": ([I64, I64], I64),
         "hx_mesh_csc_symbolic": ([P, I32, I64, I64, I64, P, P, I64, P, I64, P, I32, P], ctypes.c_int),

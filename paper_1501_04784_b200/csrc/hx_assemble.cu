@@ -98,12 +98,17 @@ __global__ void adjacency_kernel(SegTable T, int64_t n_total, int64_t n_nodes, i
 // lowest incident element (its adjacency slots), value = the column; sorting the pairs makes
 // consecutive pattern/emit threads work on nearby elements (connectivity rows and KE values stay in
 // L1/L2 instead of being gathered from random elements).
+// FIXED: fixed-slot adjacency (slot = local node, empty = -1; see incident_sorted).
+template <bool FIXED>
 __global__ void first_element_kernel(int64_t ncols, const int32_t *__restrict__ deg, const int32_t *__restrict__ adj,
                                      uint32_t empty_key, uint32_t *__restrict__ keys, uint32_t *__restrict__ cols) {
     for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < ncols; c += (int64_t)gridDim.x * blockDim.x) {
-        const int d = min(__ldg(deg + c), MAXDEG);
+        const int d = FIXED ? MAXDEG : min(__ldg(deg + c), MAXDEG);
         uint32_t k = empty_key;
-        for (int j = 0; j < d; ++j) k = min(k, (uint32_t)(__ldg(adj + 8 * c + j) >> 3));
+        for (int j = 0; j < d; ++j) {
+            const int32_t v = __ldg(adj + 8 * c + j);
+            if (!FIXED || v >= 0) k = min(k, (uint32_t)(v >> 3));
+        }
         keys[c] = k;
         cols[c] = (uint32_t)c;
     }
@@ -141,13 +146,31 @@ __device__ __forceinline__ bool insert_row(int32_t *R, int &m, int32_t v) {
 
 // Incident elements of column cl, sorted by element id (= the stable triplet order).
 // Returns deg, or -1 with a status bit when the column is outside the fast path.
-__device__ __forceinline__ int incident_sorted(int64_t cl, const int32_t *__restrict__ deg_arr,
+// FIXED: the adjacency was recorded by the integration kernel in fixed slots -- element e stores
+// (e << 3 | a) in slot a of its local node a, empty slots hold -1 -- so deg is the number of
+// filled slots; it is written to deg_arr (the emit pass reads it) and summed into *slot_total
+// (two elements claiming one slot lose an entry; the build detects that from the total).
+template <bool FIXED>
+__device__ __forceinline__ int incident_sorted(int64_t cl, int32_t *__restrict__ deg_arr,
                                                const int32_t *__restrict__ adj, int32_t (&ent)[8],
                                                uint32_t *__restrict__ status) {
-    const int deg = __ldg(deg_arr + cl);
-    if (deg > MAXDEG) return -1;  // flagged by the adjacency pass
+    int deg = 0;
+    if (FIXED) {
+        const int4 *a4 = reinterpret_cast<const int4 *>(adj + 8 * cl);
+        const int4 lo = a4[0], hi = a4[1];
+        const int32_t v[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
 #pragma unroll
-    for (int k = 0; k < 8; ++k) ent[k] = k < deg ? __ldg(adj + 8 * cl + k) : INT32_MAX;
+        for (int k = 0; k < 8; ++k) {
+            ent[k] = v[k] >= 0 ? v[k] : INT32_MAX;
+            deg += v[k] >= 0;
+        }
+        deg_arr[cl] = deg;
+    } else {
+        deg = __ldg(deg_arr + cl);
+        if (deg > MAXDEG) return -1;  // flagged by the adjacency pass
+#pragma unroll
+        for (int k = 0; k < 8; ++k) ent[k] = k < deg ? __ldg(adj + 8 * cl + k) : INT32_MAX;
+    }
     sort8(ent);
 #pragma unroll
     for (int k = 1; k < 8; ++k) {
@@ -209,15 +232,15 @@ __device__ __forceinline__ uint32_t hash_slot(int32_t v) { return ((uint32_t)v *
 // occupied keys compacted into L as (row << 5 | slot) and sorted.  Returns m = 1 + rows (0 for an
 // empty column or one outside the fast path, with a status bit).  H, W, L: this thread's slices of
 // the [slot][thread] shared arrays.
-template <typename K, bool SINGLE, bool WRITE_ADJ>
+template <typename K, bool SINGLE, bool WRITE_ADJ, bool FIXED>
 __device__ __forceinline__ int column_pattern(const SegTable &T, bool active, int64_t cl, int32_t c,
-                                              const int32_t *__restrict__ deg_arr, int32_t *__restrict__ adj,
+                                              int32_t *__restrict__ deg_arr, int32_t *__restrict__ adj,
                                               int32_t *H, uint32_t *W, K *L, int32_t (&ent)[8], int &deg,
                                               uint32_t *__restrict__ status) {
     int m = 0;
     deg = 0;
     if (active) {
-        deg = incident_sorted(cl, deg_arr, adj, ent, status);
+        deg = incident_sorted<FIXED>(cl, deg_arr, adj, ent, status);
         if (deg < 0) deg = 0;
 #pragma unroll
         for (int k = 0; k < 8; ++k)
@@ -298,13 +321,13 @@ __device__ __forceinline__ int column_pattern(const SegTable &T, bool active, in
 //   - m = 1 + distinct rows -> col_ptr[cl] (the exclusive scan turns counts into offsets);
 //   - sorted off-diagonal records (row, word) -> a compact scratch region reserved per block with
 //     one atomic (every block records where its records start).
-template <typename K, bool SINGLE>
+template <typename K, bool SINGLE, bool FIXED>
 __global__ void __launch_bounds__(COL_BLOCK)
-pattern_kernel(SegTable T, int64_t col_lo, int64_t ncols, const int32_t *__restrict__ deg_arr,
+pattern_kernel(SegTable T, int64_t col_lo, int64_t ncols, int32_t *__restrict__ deg_arr,
                int32_t *__restrict__ adj, int64_t *__restrict__ col_ptr, int2 *__restrict__ scratch,
                int64_t scratch_capacity, unsigned long long *__restrict__ scratch_top,
                int64_t *__restrict__ block_scratch, uint32_t *__restrict__ status,
-               const uint32_t *__restrict__ order) {
+               const uint32_t *__restrict__ order, unsigned long long *__restrict__ slot_total) {
     __shared__ int32_t sH[MAXR * COL_BLOCK];   // hash keys
     __shared__ uint32_t sW[MAXR * COL_BLOCK];  // contribution words, by hash slot
     // compacted / sorted keys (row << 5 | slot): 32-bit keys reuse the hash-key array in place
@@ -322,8 +345,12 @@ pattern_kernel(SegTable T, int64_t col_lo, int64_t ncols, const int32_t *__restr
 
     int32_t ent[8];
     int deg = 0;
-    const int m = column_pattern<K, SINGLE, true>(T, cl < ncols, cl, c, deg_arr, adj, H, W, L, ent, deg, status);
+    const int m = column_pattern<K, SINGLE, true, FIXED>(T, cl < ncols, cl, c, deg_arr, adj, H, W, L, ent, deg, status);
     if (cl < ncols) col_ptr[cl] = m;
+    if (FIXED) {
+        const unsigned filled = __reduce_add_sync(0xffffffffu, (unsigned)deg);
+        if ((t & 31) == 0 && filled) atomicAdd(slot_total, (unsigned long long)filled);
+    }
 
     // compact scratch: this block's off-diagonal records
     int excl, total;
@@ -346,6 +373,13 @@ pattern_kernel(SegTable T, int64_t col_lo, int64_t ncols, const int32_t *__restr
     }
 }
 
+// Fixed-slot adjacency check: every (element, local node) pair must have landed in its own slot.
+__global__ void slot_check_kernel(const unsigned long long *__restrict__ slot_total, int64_t n_total,
+                                  uint32_t *__restrict__ status) {
+    if (threadIdx.x == 0 && blockIdx.x == 0 && *slot_total != 8ull * (unsigned long long)n_total)
+        atomicOr(status, HX_ST_SLOT_COLLISION);
+}
+
 // 6. Emit pass: block b re-walks the output entries of the same COL_BLOCK columns (coalesced
 // scratch reads, row_idx / vals stores).  Diagonals first (one per column: every incident element
 // at its own local node), then the off-diagonal scratch records in output order.  Values are
@@ -358,6 +392,34 @@ __device__ __forceinline__ const double *ke_row(const SegTable &T, int64_t e) {
     return T.ke[sg] + T.ke_stride[sg] * (e - T.start[sg]);
 }
 
+// KE gathers of the emit pass.  Each KE row is read by the columns of its element's 8 nodes, up to
+// one node layer apart; HX_EMIT_KE_HINT 1 marks those loads L2 evict_last (the streamed scratch
+// loads and CSC stores are evict-first) so the rows survive until their last column.
+#ifndef HX_EMIT_KE_HINT
+#define HX_EMIT_KE_HINT 0
+#endif
+__device__ __forceinline__ uint64_t ke_policy() {
+    uint64_t p = 0;
+#if HX_EMIT_KE_HINT >= 1
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+#endif
+    return p;
+}
+__device__ __forceinline__ double ke_load(const double *ptr, uint64_t pol) {
+#if HX_EMIT_KE_HINT == 1
+    double v;
+    asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(ptr), "l"(pol));
+    return v;
+#elif HX_EMIT_KE_HINT == 2
+    double v;
+    asm("ld.global.nc.L2::cache_hint.L2::256B.f64 %0, [%1], %2;" : "=d"(v) : "l"(ptr), "l"(pol));
+    return v;
+#else
+    (void)pol;
+    return __ldg(ptr);
+#endif
+}
+
 template <bool ROWS, bool VALS, bool SINGLE>
 __global__ void __launch_bounds__(EMIT_BLOCK)
 emit_kernel(SegTable T, int64_t col_lo, int64_t ncols, const int32_t *__restrict__ deg_arr,
@@ -366,8 +428,11 @@ emit_kernel(SegTable T, int64_t col_lo, int64_t ncols, const int32_t *__restrict
             int64_t capacity, const uint32_t *__restrict__ status, const uint32_t *__restrict__ order_flag,
             const uint32_t *__restrict__ order) {
     // the pattern pass hit a fast-path limit: its records are incomplete and the caller re-runs
-    if (*status & (HX_ST_DEG_OVERFLOW | HX_ST_ROW_OVERFLOW | HX_ST_REPEATED_NODE | HX_ST_SCRATCH_OVERFLOW)) return;
+    if (*status & (HX_ST_DEG_OVERFLOW | HX_ST_ROW_OVERFLOW | HX_ST_REPEATED_NODE | HX_ST_SCRATCH_OVERFLOW |
+                   HX_ST_SLOT_COLLISION))
+        return;
     const bool ordered = *order_flag != 0u;
+    const uint64_t pol = ke_policy();
     __shared__ int64_t s_start[COL_BLOCK];       // first output entry of each column of the tile
     __shared__ int32_t s_m[COL_BLOCK + 1];       // entries per column
     __shared__ int32_t s_cl[COL_BLOCK];          // column (block-local index) of each tile position
@@ -437,7 +502,7 @@ emit_kernel(SegTable T, int64_t col_lo, int64_t ncols, const int32_t *__restrict
             if (k < deg) {
                 const int32_t en = ent[k];
                 const int a = en & 7;
-                x[k] = __ldg(ke_row<SINGLE>(T, en >> 3) + pack_index(a, a));
+                x[k] = ke_load(ke_row<SINGLE>(T, en >> 3) + pack_index(a, a), pol);
             }
         }
         double v = x[0];
@@ -463,7 +528,7 @@ emit_kernel(SegTable T, int64_t col_lo, int64_t ncols, const int32_t *__restrict
                 const uint32_t kb = (w >> (3 + 6 * r)) & 63u;
                 const int32_t en = ent[kb >> 3];
                 const int a = en & 7, b = (int)(kb & 7u);
-                x[r] = __ldg(ke_row<SINGLE>(T, en >> 3) + pack_index(max(a, b), min(a, b)));
+                x[r] = ke_load(ke_row<SINGLE>(T, en >> 3) + pack_index(max(a, b), min(a, b)), pol);
             }
         }
         double v = x[0];
@@ -519,7 +584,7 @@ struct MeshWs {
     uint32_t *order_flag;
     int32_t *deg, *adj;
     int64_t *block_scratch;
-    unsigned long long *scratch_top;
+    unsigned long long *scratch_top, *slot_total;
     uint32_t *keys_in, *keys_out, *cols_in, *order;
     int2 *scratch;
     int64_t scratch_capacity;
@@ -549,7 +614,7 @@ static MeshWs mesh_ws_layout(void *base, int64_t ncols, int64_t workspace_bytes 
     const size_t o_deg = take(sizeof(int32_t) * nc);
     const size_t o_adj = take(sizeof(int32_t) * 8 * nc);
     const size_t o_bs = take(sizeof(int64_t) * std::max<int64_t>(1, ceil_div(ncols, COL_BLOCK)));
-    const size_t o_st = take(sizeof(unsigned long long));
+    const size_t o_st = take(2 * sizeof(unsigned long long));  // scratch_top, slot_total
     const size_t o_ki = take(sizeof(uint32_t) * nc), o_ko = take(sizeof(uint32_t) * nc);
     const size_t o_ci = take(sizeof(uint32_t) * nc), o_or = take(sizeof(uint32_t) * nc);
     w.cub_bytes = cub_temp_bytes(ncols);
@@ -566,6 +631,7 @@ static MeshWs mesh_ws_layout(void *base, int64_t ncols, int64_t workspace_bytes 
         w.adj = (int32_t *)(b + o_adj);
         w.block_scratch = (int64_t *)(b + o_bs);
         w.scratch_top = (unsigned long long *)(b + o_st);
+        w.slot_total = w.scratch_top + 1;
         w.keys_in = (uint32_t *)(b + o_ki);
         w.keys_out = (uint32_t *)(b + o_ko);
         w.cols_in = (uint32_t *)(b + o_ci);
@@ -613,6 +679,17 @@ static int make_segtable(const hx_elem_segment *segs, int32_t n_segs, SegTable &
 }
 
 
+int mesh_ws_adjacency(void *workspace, int64_t workspace_bytes, int64_t ncols, int32_t **deg, int32_t **adj) {
+    const MeshWs w = mesh_ws_layout(workspace, ncols, workspace_bytes);
+    if (workspace == nullptr || workspace_bytes < (int64_t)w.total) {
+        set_last_error("mesh csc workspace %lld < %lld bytes", (long long)workspace_bytes, (long long)w.total);
+        return HX_ERR_WORKSPACE;
+    }
+    *deg = w.deg;
+    *adj = w.adj;
+    return HX_OK;
+}
+
 static bool single_dense(const SegTable &T) { return T.n == 1 && T.ke_stride[0] == 36 && T.conn_stride[0] == 8; }
 static bool single_conn(const SegTable &T) { return T.n == 1 && T.conn_stride[0] == 8; }
 
@@ -649,12 +726,18 @@ static int mesh_csc_build(const hx_elem_segment *segs, int32_t n_segs, int64_t n
     }
     cudaStream_t s = (cudaStream_t)stream;
     const bool ordered = (flags & HX_CSC_ORDER_BY_ELEMENT) != 0 && ncols > 0 && n_total > 0;
-    HX_TRY_CUDA(cudaMemsetAsync(status, 0, sizeof(uint32_t), s));
+    // adjacency (and its status bits) already recorded by hx_integrate_mesh_adjacency
+    const bool adj_ready = (flags & HX_CSC_ADJACENCY_READY) != 0;
+    if (adj_ready && (n_segs != 1 || col_lo != 0 || col_hi != n_nodes || !single_conn(T))) {
+        set_last_error("hx_mesh_csc_build: HX_CSC_ADJACENCY_READY needs one segment and every column");
+        return HX_ERR_VALUE;
+    }
+    if (!adj_ready) HX_TRY_CUDA(cudaMemsetAsync(status, 0, sizeof(uint32_t), s));
     HX_TRY_CUDA(cudaMemsetAsync(w.order_flag, 0, sizeof(uint32_t), s));
     if (ordered) HX_TRY_CUDA(cudaMemsetAsync(w.order_flag, 1, 1, s));  // little-endian u32 == 1
     if (ncols > 0) {
-        HX_TRY_CUDA(cudaMemsetAsync(w.deg, 0, sizeof(int32_t) * ncols, s));
-        if (n_total > 0) {
+        if (!adj_ready) HX_TRY_CUDA(cudaMemsetAsync(w.deg, 0, sizeof(int32_t) * ncols, s));
+        if (n_total > 0 && !adj_ready) {
             const unsigned grid = (unsigned)std::min<int64_t>(ceil_div(8 * n_total, 256), 148 * 64);
             if (single_conn(T))
                 adjacency_kernel<true><<<grid, 256, 0, s>>>(T, n_total, n_nodes, col_lo, col_hi, w.deg, w.adj, status);
@@ -664,8 +747,11 @@ static int mesh_csc_build(const hx_elem_segment *segs, int32_t n_segs, int64_t n
         }
         const unsigned tiles = (unsigned)ceil_div(ncols, COL_BLOCK);
         if (ordered) {
-            first_element_kernel<<<(unsigned)std::min<int64_t>(ceil_div(ncols, 256), 148 * 32), 256, 0, s>>>(
-                ncols, w.deg, w.adj, (uint32_t)n_total, w.keys_in, w.cols_in);
+            const unsigned g = (unsigned)std::min<int64_t>(ceil_div(ncols, 256), 148 * 32);
+            if (adj_ready)
+                first_element_kernel<true><<<g, 256, 0, s>>>(ncols, w.deg, w.adj, (uint32_t)n_total, w.keys_in, w.cols_in);
+            else
+                first_element_kernel<false><<<g, 256, 0, s>>>(ncols, w.deg, w.adj, (uint32_t)n_total, w.keys_in, w.cols_in);
             HX_CHECK_LAUNCH("first_element_kernel");
             int end_bit = 1;
             while (end_bit < 32 && ((uint64_t)n_total >> end_bit) != 0) ++end_bit;
@@ -674,22 +760,29 @@ static int mesh_csc_build(const hx_elem_segment *segs, int32_t n_segs, int64_t n
                                                         (int)ncols, 0, end_bit, s));
         }
         const uint32_t *order = ordered ? w.order : nullptr;
-        HX_TRY_CUDA(cudaMemsetAsync(w.scratch_top, 0, sizeof(unsigned long long), s));
-        auto pattern = [&](auto key_tag, auto single_tag) {
+        HX_TRY_CUDA(cudaMemsetAsync(w.scratch_top, 0, 2 * sizeof(unsigned long long), s));  // + slot_total
+        auto pattern = [&](auto key_tag, auto single_tag, auto fixed_tag) {
             using K = decltype(key_tag);
-            pattern_kernel<K, decltype(single_tag)::value><<<tiles, COL_BLOCK, 0, s>>>(
+            pattern_kernel<K, decltype(single_tag)::value, decltype(fixed_tag)::value><<<tiles, COL_BLOCK, 0, s>>>(
                 T, col_lo, ncols, w.deg, w.adj, col_ptr, w.scratch, w.scratch_capacity, w.scratch_top, w.block_scratch,
-                status, order);
+                status, order, w.slot_total);
         };
         const bool packed = n_nodes <= (int64_t(1) << 26);
-        if (single_conn(T)) {
-            if (packed) pattern(uint32_t{}, std::true_type{});
-            else pattern(uint64_t{}, std::true_type{});
+        if (adj_ready) {  // one dense segment (checked above)
+            if (packed) pattern(uint32_t{}, std::true_type{}, std::true_type{});
+            else pattern(uint64_t{}, std::true_type{}, std::true_type{});
+        } else if (single_conn(T)) {
+            if (packed) pattern(uint32_t{}, std::true_type{}, std::false_type{});
+            else pattern(uint64_t{}, std::true_type{}, std::false_type{});
         } else {
-            if (packed) pattern(uint32_t{}, std::false_type{});
-            else pattern(uint64_t{}, std::false_type{});
+            if (packed) pattern(uint32_t{}, std::false_type{}, std::false_type{});
+            else pattern(uint64_t{}, std::false_type{}, std::false_type{});
         }
         HX_CHECK_LAUNCH("pattern_kernel");
+        if (adj_ready) {
+            slot_check_kernel<<<1, 32, 0, s>>>(w.slot_total, n_total, status);
+            HX_CHECK_LAUNCH("slot_check_kernel");
+        }
         HX_TRY_CUDA(cudaMemsetAsync(col_ptr + ncols, 0, sizeof(int64_t), s));
         size_t cb2 = w.cub_bytes;
         HX_TRY_CUDA(cub::DeviceScan::ExclusiveSum(w.cub_tmp, cb2, col_ptr, col_ptr, (int)(ncols + 1), s));

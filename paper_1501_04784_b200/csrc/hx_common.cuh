@@ -65,6 +65,10 @@ int cuda_status(cudaError_t err, const char *where);
     } while (0)
 #define HX_CHECK_LAUNCH(where) HX_TRY_CUDA(cudaGetLastError())
 
+// Adjacency section (deg (ncols) i32, adj (8 ncols) i32) of a mesh-CSC workspace (hx_assemble.cu),
+// filled by the integration kernel in the fused build (hx_integrate_mesh_adjacency).
+int mesh_ws_adjacency(void *workspace, int64_t workspace_bytes, int64_t ncols, int32_t **deg, int32_t **adj);
+
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 

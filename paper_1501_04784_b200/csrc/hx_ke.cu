@@ -19,6 +19,12 @@
 //     store KE and the fused iK/jK as 8-wide element-major runs.
 // Warps are persistent and prefetch the next element quad's connectivity and coordinates into
 // registers while integrating the current one.
+// With WITH_ADJ the kernel also records the node adjacency of the mesh-path assembly (the symbolic
+// phase's first pass): lane (el, a) already holds node a of its element and stores (element << 3 |
+// a) into slot a of that node -- a fixed slot, so no atomic and no returned value stalls the FP64
+// work; the connectivity is read once for both.  Meshes whose elements put one node at the same
+// local index twice (inconsistent orientation) lose a slot; the pattern pass counts the filled
+// slots and the build then re-runs the atomic adjacency (HX_ST_SLOT_COLLISION).
 //
 // Bit-preserving rewrites:
 //   * dN = sign * M_k with M_k one of three magnitudes; (-M)*x == -(M*x) exactly, so the sign is
@@ -426,13 +432,21 @@ __device__ __forceinline__ bool ke_gauss_point(GpWarpSmem &sm, int el, int gp, b
 // counter (so the kernel balances itself when it shares the GPU with the concurrently running
 // symbolic assembly) and prefetches the next quad's node ids, coordinates and coefficients into
 // registers before integrating the current one, so the gather latency hides under the FP64 work.
-template <int MODE, bool WITH_INDEX>
+// Adjacency outputs of the fused symbolic first pass (WITH_ADJ): deg (n_nodes) i32 zeroed by the
+// caller, adj (8 n_nodes) i32 slots, status bits HX_ST_BAD_INDEX / HX_ST_DEG_OVERFLOW.
+struct AdjOut {
+    int32_t *deg;
+    int32_t *adj;
+    uint32_t *status;
+};
+
+template <int MODE, bool WITH_INDEX, bool WITH_ADJ>
 __global__ void __launch_bounds__(GP_BLOCK, HX_KE_MIN_BLOCKS)
-integrate_mesh_kernel(const double *__restrict__ coords, const int32_t *__restrict__ conn,
+integrate_mesh_kernel(const double *__restrict__ coords, int64_t n_nodes, const int32_t *__restrict__ conn,
                       const double *__restrict__ coeff, int64_t lo, int64_t n,
                       double *__restrict__ ke_out, int32_t *__restrict__ rows_out,
                       int32_t *__restrict__ cols_out, unsigned long long *__restrict__ fail_min,
-                      unsigned *__restrict__ quad_counter) {
+                      unsigned *__restrict__ quad_counter, AdjOut adj_out) {
     extern __shared__ __align__(16) unsigned char s_dyn[];
     GpWarpSmem *s_warp = reinterpret_cast<GpWarpSmem *>(s_dyn);
     __shared__ uint8_t s_pi[36], s_pj[36];
@@ -459,7 +473,8 @@ integrate_mesh_kernel(const double *__restrict__ coords, const int32_t *__restri
     int64_t quad2 = quad1 < n_quads ? grab() : n_quads;     // node ids in flight
     int32_t node = node_id(quad), node_next = node_id(quad1);
     double x0 = u0, x1 = u1, x2 = u2, c = 1.0;
-    if (node >= 0) {
+    // out-of-range ids are never dereferenced (the assembly reports them: HX_ST_BAD_INDEX)
+    if (node >= 0 && (!WITH_ADJ || node < n_nodes)) {
         const double *p = coords + 3 * (int64_t)node;
         x0 = __ldg(p); x1 = __ldg(p + 1); x2 = __ldg(p + 2);
         c = __ldg(coeff + lo + quad * GP_EL_PER_WARP + el);
@@ -470,6 +485,11 @@ integrate_mesh_kernel(const double *__restrict__ coords, const int32_t *__restri
         const unsigned in_range = __ballot_sync(0xffffffffu, coord_in_range(x0) && coord_in_range(x1) &&
                                                                coord_in_range(x2));
         const bool fast_div = ((in_range >> (8 * el)) & 0xffu) == 0xffu;
+        // fixed-slot adjacency: (element, local node gp) -> slot gp of its node (fire and forget)
+        if (WITH_ADJ && valid) {
+            if (node < 0 || node >= n_nodes) atomicOr(adj_out.status, HX_ST_BAD_INDEX);
+            else adj_out.adj[8 * (int64_t)node + gp] = (int32_t)(((lo + k) << 3) | gp);
+        }
         __syncwarp();
         publish_node<MODE>(sm, el, gp, node, x0, x1, x2, c);
         __syncwarp();
@@ -477,7 +497,7 @@ integrate_mesh_kernel(const double *__restrict__ coords, const int32_t *__restri
         node = node_next;
         node_next = node_id(quad2);
         x0 = u0; x1 = u1; x2 = u2; c = 1.0;
-        if (node >= 0) {
+        if (node >= 0 && (!WITH_ADJ || node < n_nodes)) {
             const double *p = coords + 3 * (int64_t)node;
             x0 = __ldg(p); x1 = __ldg(p + 1); x2 = __ldg(p + 2);
             c = __ldg(coeff + lo + quad1 * GP_EL_PER_WARP + el);
@@ -583,9 +603,13 @@ constexpr size_t GP_SMEM = GP_WARPS * sizeof(GpWarpSmem);  // dynamic shared mem
 // Opt the integration kernels into dynamic shared memory beyond the default (once per device).
 template <int MODE>
 static void configure_mode() {
-    cudaFuncSetAttribute(integrate_mesh_kernel<MODE, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(integrate_mesh_kernel<MODE, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)GP_SMEM);
-    cudaFuncSetAttribute(integrate_mesh_kernel<MODE, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(integrate_mesh_kernel<MODE, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)GP_SMEM);
+    cudaFuncSetAttribute(integrate_mesh_kernel<MODE, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)GP_SMEM);
+    cudaFuncSetAttribute(integrate_mesh_kernel<MODE, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)GP_SMEM);
     cudaFuncSetAttribute(stiffness_batch_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GP_SMEM);
 }
@@ -608,7 +632,7 @@ static int64_t persistent_blocks() {
         int dev = 0, sms = 148, per_sm = HX_KE_MIN_BLOCKS;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, integrate_mesh_kernel<MODE, true>, GP_BLOCK, GP_SMEM);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, integrate_mesh_kernel<MODE, true, false>, GP_BLOCK, GP_SMEM);
         if (const char *env = getenv("HX_KE_BLOCKS_PER_SM")) per_sm = std::min(per_sm, atoi(env));  // experiments
         cached = (int64_t)sms * std::max(per_sm, 1);
     }
@@ -616,17 +640,22 @@ static int64_t persistent_blocks() {
 }
 
 template <int MODE>
-static void launch_integrate(int64_t blocks, cudaStream_t s, const double *coords, const int32_t *conn,
+static void launch_integrate(int64_t blocks, cudaStream_t s, const double *coords, int64_t n_nodes, const int32_t *conn,
                              const double *coeff, int64_t lo, int64_t n, double *ke, int32_t *rows, int32_t *cols,
-                             hx_fail_info *fail) {
+                             hx_fail_info *fail, AdjOut adj) {
     unsigned *counter = reinterpret_cast<unsigned *>(&fail->reserved);
     auto *fmin = reinterpret_cast<unsigned long long *>(fail);
-    if (rows != nullptr)
-        integrate_mesh_kernel<MODE, true><<<(unsigned)blocks, GP_BLOCK, GP_SMEM, s>>>(coords, conn, coeff, lo, n, ke,
-                                                                                   rows, cols, fmin, counter);
-    else
-        integrate_mesh_kernel<MODE, false><<<(unsigned)blocks, GP_BLOCK, GP_SMEM, s>>>(coords, conn, coeff, lo, n,
-                                                                                    ke, rows, cols, fmin, counter);
+    auto go = [&](auto kernel) {
+        kernel<<<(unsigned)blocks, GP_BLOCK, GP_SMEM, s>>>(coords, n_nodes, conn, coeff, lo, n, ke, rows, cols, fmin,
+                                                           counter, adj);
+    };
+    if (adj.deg != nullptr) {
+        if (rows != nullptr) go(integrate_mesh_kernel<MODE, true, true>);
+        else go(integrate_mesh_kernel<MODE, false, true>);
+    } else {
+        if (rows != nullptr) go(integrate_mesh_kernel<MODE, true, false>);
+        else go(integrate_mesh_kernel<MODE, false, false>);
+    }
 }
 
 __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
@@ -686,20 +715,9 @@ extern "C" int hx_selftest_division(uint64_t n, uint64_t seed, unsigned long lon
     return HX_OK;
 }
 
-extern "C" int hx_integrate_mesh(const double *coords, int64_t n_nodes, const int32_t *conn,
-                                 const double *coeff, int64_t lo, int64_t hi, double *ke,
-                                 int32_t *rows, int32_t *cols, int32_t mode, hx_fail_info *fail,
-                                 void *stream) {
-    (void)n_nodes;
-    if (lo < 0 || hi < lo || (hi > lo && ke == nullptr) || fail == nullptr || (rows == nullptr) != (cols == nullptr)) {
-        set_last_error("hx_integrate_mesh: bad arguments (lo=%lld hi=%lld)", (long long)lo, (long long)hi);
-        return HX_ERR_VALUE;
-    }
-    if (mode != HX_MODE_EXACT && mode != HX_MODE_FAST) {
-        set_last_error("hx_integrate_mesh: unknown mode %d", mode);
-        return HX_ERR_CONFIG;
-    }
-    cudaStream_t s = (cudaStream_t)stream;
+static int integrate_mesh_impl(const double *coords, int64_t n_nodes, const int32_t *conn, const double *coeff,
+                               int64_t lo, int64_t hi, double *ke, int32_t *rows, int32_t *cols, int32_t mode,
+                               hx_fail_info *fail, AdjOut adj, cudaStream_t s) {
     const int64_t n = hi - lo;
     HX_TRY_CUDA(cudaMemsetAsync(fail, 0xff, sizeof(unsigned long long), s));
     HX_TRY_CUDA(cudaMemsetAsync(&fail->reserved, 0, sizeof(int32_t), s));  // quad counter
@@ -710,15 +728,63 @@ extern "C" int hx_integrate_mesh(const double *coords, int64_t n_nodes, const in
         }
         if (mode == HX_MODE_EXACT)
             launch_integrate<HX_MODE_EXACT>(std::min<int64_t>(ceil_div(n, GP_EL_PER_BLOCK), persistent_blocks<HX_MODE_EXACT>()),
-                                            s, coords, conn, coeff, lo, n, ke, rows, cols, fail);
+                                            s, coords, n_nodes, conn, coeff, lo, n, ke, rows, cols, fail, adj);
         else
             launch_integrate<HX_MODE_FAST>(std::min<int64_t>(ceil_div(n, GP_EL_PER_BLOCK), persistent_blocks<HX_MODE_FAST>()),
-                                           s, coords, conn, coeff, lo, n, ke, rows, cols, fail);
+                                           s, coords, n_nodes, conn, coeff, lo, n, ke, rows, cols, fail, adj);
         HX_CHECK_LAUNCH("integrate_mesh_kernel");
     }
     fail_resolve_mesh_kernel<<<1, 1, 0, s>>>(coords, conn, coeff, fail);
     HX_CHECK_LAUNCH("fail_resolve_mesh_kernel");
     return HX_OK;
+}
+
+static bool integrate_args_ok(int64_t lo, int64_t hi, const double *ke, const int32_t *rows, const int32_t *cols,
+                              const hx_fail_info *fail, int32_t mode, int &rc) {
+    if (lo < 0 || hi < lo || (hi > lo && ke == nullptr) || fail == nullptr || (rows == nullptr) != (cols == nullptr)) {
+        set_last_error("hx_integrate_mesh: bad arguments (lo=%lld hi=%lld)", (long long)lo, (long long)hi);
+        rc = HX_ERR_VALUE;
+        return false;
+    }
+    if (mode != HX_MODE_EXACT && mode != HX_MODE_FAST) {
+        set_last_error("hx_integrate_mesh: unknown mode %d", mode);
+        rc = HX_ERR_CONFIG;
+        return false;
+    }
+    return true;
+}
+
+extern "C" int hx_integrate_mesh(const double *coords, int64_t n_nodes, const int32_t *conn,
+                                 const double *coeff, int64_t lo, int64_t hi, double *ke,
+                                 int32_t *rows, int32_t *cols, int32_t mode, hx_fail_info *fail,
+                                 void *stream) {
+    int rc = HX_OK;
+    if (!integrate_args_ok(lo, hi, ke, rows, cols, fail, mode, rc)) return rc;
+    return integrate_mesh_impl(coords, n_nodes, conn, coeff, lo, hi, ke, rows, cols, mode, fail,
+                               AdjOut{nullptr, nullptr, nullptr}, (cudaStream_t)stream);
+}
+
+extern "C" int hx_integrate_mesh_adjacency(const double *coords, int64_t n_nodes, const int32_t *conn,
+                                           const double *coeff, int64_t lo, int64_t hi, double *ke, int32_t *rows,
+                                           int32_t *cols, int32_t mode, hx_fail_info *fail, void *csc_workspace,
+                                           int64_t workspace_bytes, uint32_t *csc_status, int32_t reset,
+                                           void *stream) {
+    int rc = HX_OK;
+    if (!integrate_args_ok(lo, hi, ke, rows, cols, fail, mode, rc)) return rc;
+    if (csc_status == nullptr || n_nodes < 0 || n_nodes >= INT32_MAX || 8 * hi >= (int64_t)INT32_MAX) {
+        set_last_error("hx_integrate_mesh_adjacency: bad arguments (n_nodes=%lld hi=%lld)", (long long)n_nodes,
+                       (long long)hi);
+        return HX_ERR_VALUE;
+    }
+    AdjOut adj{nullptr, nullptr, csc_status};
+    rc = mesh_ws_adjacency(csc_workspace, workspace_bytes, n_nodes, &adj.deg, &adj.adj);
+    if (rc) return rc;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (reset) {  // status 0, every adjacency slot empty (-1)
+        HX_TRY_CUDA(cudaMemsetAsync(csc_status, 0, sizeof(uint32_t), s));
+        if (n_nodes > 0) HX_TRY_CUDA(cudaMemsetAsync(adj.adj, 0xff, sizeof(int32_t) * 8 * n_nodes, s));
+    }
+    return integrate_mesh_impl(coords, n_nodes, conn, coeff, lo, hi, ke, rows, cols, mode, fail, adj, s);
 }
 
 extern "C" int hx_stiffness_batch(const double *coords, const double *coeff, int64_t n, double *out,

@@ -17,7 +17,7 @@ from . import _native as N
 from .errors import ConfigurationError, DegenerateElementError, MeshValidationError, NativeLibraryError
 
 __all__ = [
-    "DeviceMesh", "DeviceCsc", "require_device", "stream_handle", "integrate_mesh", "stiffness_batch",
+    "DeviceMesh", "DeviceCsc", "AssemblyPrep", "new_assembly_prep", "require_device", "stream_handle", "integrate_mesh", "stiffness_batch",
     "connectivity_index_arrays", "raise_if_failed", "mesh_csc", "triplet_csc", "MeshPlan", "mesh_plan_async",
     "mesh_emit", "plan_assembly", "block_elements", "generate_cube_mesh",
 ]
@@ -132,9 +132,13 @@ def _mode_id(mode: str) -> int:
 
 
 def integrate_mesh(dm: DeviceMesh, lo: int = 0, hi: int | None = None, *, ke=None, rows=None, cols=None,
-                   with_index: bool = True, mode: str = "exact", fail=None, stream=None):
+                   with_index: bool = True, mode: str = "exact", fail=None, stream=None, adjacency=None):
     """KE (+ fused iK/jK) for elements [lo, hi) of a device mesh.  Asynchronous: returns
-    ``(ke, rows, cols, fail)``; call raise_if_failed(fail) after the stream is done."""
+    ``(ke, rows, cols, fail)``; call raise_if_failed(fail) after the stream is done.
+
+    ``adjacency`` = an AssemblyPrep (new_assembly_prep): the kernel also records the node adjacency
+    of the mesh-path assembly in its workspace (hx_integrate_mesh_adjacency), which mesh_csc(...,
+    prep=) then skips.  The first range of a build resets it."""
     hi = dm.n_el if hi is None else hi
     if not 0 <= lo <= hi <= dm.n_el:
         raise ValueError(f"element range [{lo}, {hi}) outside [0, {dm.n_el})")
@@ -154,10 +158,39 @@ def integrate_mesh(dm: DeviceMesh, lo: int = 0, hi: int | None = None, *, ke=Non
         rows = cols = None
     if fail is None:
         fail = new_fail_record(dev)
-    N.check(N.lib().hx_integrate_mesh(_ptr(dm.coords), dm.n_nodes, _ptr(dm.conn), _ptr(dm.coeff), lo, hi,
-                                      _ptr(ke), _ptr(rows), _ptr(cols), _mode_id(mode), _ptr(fail),
-                                      stream_handle(stream)), "hx_integrate_mesh")
+    if adjacency is None:
+        N.check(N.lib().hx_integrate_mesh(_ptr(dm.coords), dm.n_nodes, _ptr(dm.conn), _ptr(dm.coeff), lo, hi,
+                                          _ptr(ke), _ptr(rows), _ptr(cols), _mode_id(mode), _ptr(fail),
+                                          stream_handle(stream)), "hx_integrate_mesh")
+    else:
+        if adjacency.conn is not dm.conn:
+            raise ConfigurationError("the assembly workspace belongs to another mesh")
+        N.check(N.lib().hx_integrate_mesh_adjacency(
+            _ptr(dm.coords), dm.n_nodes, _ptr(dm.conn), _ptr(dm.coeff), lo, hi, _ptr(ke), _ptr(rows), _ptr(cols),
+            _mode_id(mode), _ptr(fail), _ptr(adjacency.ws), adjacency.ws.numel(), _ptr(adjacency.status),
+            0 if adjacency.started else 1, stream_handle(stream)), "hx_integrate_mesh_adjacency")
+        adjacency.started = True
     return ke, rows, cols, fail
+
+
+@dataclass
+class AssemblyPrep:
+    """Mesh-CSC workspace + status word whose node adjacency the integration kernel fills
+    (hx_integrate_mesh_adjacency) so the assembly skips its first pass."""
+
+    conn: torch.Tensor
+    ws: torch.Tensor
+    status: torch.Tensor
+    started: bool = False
+
+
+def new_assembly_prep(dm: DeviceMesh) -> AssemblyPrep:
+    ws_bytes = N.lib().hx_mesh_csc_workspace_bytes(dm.n_el, dm.n_nodes)
+    if ws_bytes < 0 or 8 * dm.n_el >= 2**31 - 1:
+        raise ValueError("mesh too large for one assembly plan")
+    dev = dm.conn.device
+    return AssemblyPrep(dm.conn, torch.empty(ws_bytes, dtype=torch.uint8, device=dev),
+                        torch.zeros(1, dtype=torch.int32, device=dev))
 
 
 def stiffness_batch(coords: torch.Tensor, coeff: torch.Tensor, out=None, mode: str = "exact", fail=None,
@@ -259,14 +292,16 @@ def _order_flags(order, conn, n_nodes) -> int:
 
 
 def mesh_csc(parts, n_nodes: int, col_lo: int = 0, col_hi: int | None = None, stream=None,
-             row_capacity: int | None = None, order: str = "auto") -> DeviceCsc:
+             row_capacity: int | None = None, order: str = "auto", prep: AssemblyPrep | None = None) -> DeviceCsc:
     """Assemble columns [col_lo, col_hi) of the lower CSC from element segments.
 
     ``parts`` is a list of (conn (n,8) i32, ke (n,36) f64) CUDA tensor views in ascending global
     element order (one pair for a single GPU; halo record views for the multi-GPU path -- rows
     may be strided).  Meshes outside the node-adjacency fast path's limits fall through to the
     generic triplet path with identical results.  ``order`` picks the column processing order
-    (results are identical; "auto" uses element order for numberings without locality).
+    (results are identical; "auto" uses element order for numberings without locality).  ``prep``:
+    the workspace whose adjacency the integration kernel already recorded (one segment, every
+    column) -- the first attempt skips the adjacency pass; retries rebuild it.
     """
     col_hi = n_nodes if col_hi is None else col_hi
     if not 1 <= len(parts) <= N.MAX_SEGMENTS:
@@ -282,12 +317,19 @@ def mesh_csc(parts, n_nodes: int, col_lo: int = 0, col_hi: int | None = None, st
     ws_bytes = N.lib().hx_mesh_csc_workspace_bytes(n_total, ncols)
     if ws_bytes < 0:
         raise ValueError("bad mesh size")
-    status = torch.zeros(1, dtype=torch.int32, device=dev)
+    if prep is not None:
+        if not prep.started or len(parts) != 1 or parts[0][0] is not prep.conn or col_lo != 0 or col_hi != n_nodes:
+            raise ConfigurationError("assembly prep must cover the whole single-segment mesh it was made for")
+        status, ws, ws_bytes = prep.status, prep.ws, prep.ws.numel()
+        flags |= N.CSC_ADJACENCY_READY
+    else:
+        status = torch.zeros(1, dtype=torch.int32, device=dev)
     col_ptr = torch.empty(ncols + 1, dtype=torch.int64, device=dev)
     sh = stream_handle(stream)
     capacity = ROWS_PER_COLUMN_ESTIMATE * ncols if row_capacity is None else row_capacity
     while True:
-        ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
+        if not flags & N.CSC_ADJACENCY_READY:
+            ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
         row_buf = torch.empty(max(capacity, 1), dtype=torch.int64, device=dev)
         val_buf = torch.empty(max(capacity, 1), dtype=torch.float64, device=dev)
         N.check(N.lib().hx_mesh_csc_build(segs, len(parts), n_nodes, col_lo, col_hi, _ptr(col_ptr), _ptr(row_buf),
@@ -296,6 +338,9 @@ def mesh_csc(parts, n_nodes: int, col_lo: int = 0, col_hi: int | None = None, st
         head = torch.stack([status.to(torch.int64)[0], col_ptr[-1]]).cpu()  # one sync: status + nnz
         st, nnz = int(head[0]), int(head[1])
         _status_error(st)
+        flags &= ~N.CSC_ADJACENCY_READY  # a retry recomputes the adjacency in a fresh workspace
+        if st & N.ST_SLOT_COLLISION:
+            continue  # fixed-slot adjacency lost an entry (inconsistent element orientation)
         if st & N.ST_SCRATCH and not st & (N.ST_FASTPATH_LIMITS & ~N.ST_SCRATCH):
             # more off-diagonal records than the default scratch (e.g. the first column block of a
             # permuted mesh): the counts are complete, re-run with room for all of them

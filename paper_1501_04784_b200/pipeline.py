@@ -8,6 +8,8 @@ inputs already in HBM, outputs left in HBM.
 
 from __future__ import annotations
 
+import os
+
 import time
 from dataclasses import asdict, dataclass
 
@@ -130,12 +132,18 @@ def build_device(dm: D.DeviceMesh, mode: str = "exact", with_index: bool = True,
         side.wait_stream(main)  # inputs and the buffers below are ordered before the plan
         plan = D.mesh_plan_async(dm.conn, dm.n_nodes, stream=side, order=dm.assembly_order())
         plan_done = side.record_event()
+    # cold single-stream build: the integration kernel also records the node adjacency (the
+    # assembly's first pass), so the connectivity is read once and the atomics hide under FP64 work
+    spans = sorted(ranges or [(0, n)])
+    covers = spans[0][0] == 0 and spans[-1][1] == n and all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
+    fuse = cached is None and plan is None and covers and 0 < n and 8 * n < 2**31 - 1
+    prep = D.new_assembly_prep(dm) if fuse and os.environ.get("HX_FUSED_ADJACENCY", "1") != "0" else None
     fails = []
     for lo, hi in (ranges or [(0, n)]):
         _, _, _, fail = D.integrate_mesh(dm, lo, hi, ke=ke[lo:hi],
                                          rows=rows[36 * lo:36 * hi] if with_index else None,
                                          cols=cols[36 * lo:36 * hi] if with_index else None,
-                                         with_index=with_index, mode=mode, stream=main)
+                                         with_index=with_index, mode=mode, stream=main, adjacency=prep)
         fails.append(fail)
     if cached is not None:
         if cached.conn is not dm.conn:
@@ -145,7 +153,7 @@ def build_device(dm: D.DeviceMesh, mode: str = "exact", with_index: bool = True,
         main.wait_event(plan_done)
         csc = D.mesh_emit(plan, ke, stream=main)
     else:
-        csc = D.mesh_csc([(dm.conn, ke)], dm.n_nodes, stream=main, order=dm.assembly_order())
+        csc = D.mesh_csc([(dm.conn, ke)], dm.n_nodes, stream=main, order=dm.assembly_order(), prep=prep)
     if cached is None:  # a planned rebuild stays asynchronous: check the fail records later
         for f in fails:
             D.raise_if_failed(f)

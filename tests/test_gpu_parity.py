@@ -637,3 +637,67 @@ def test_generic_triplet_path_beyond_int32_triplets():
     assert torch.equal(trip.col_ptr, d_ptr)
     assert torch.equal(trip.row_idx.to(torch.int32), d_rows)
     assert torch.equal(trip.vals.view(torch.int64), d_vals.view(torch.int64))
+
+
+def _oracle_build(mesh):
+    ke, rows, cols, first, _, _ = oracle.stiffness_mesh(mesh.coords, mesh.connectivity, mesh.coefficient)
+    assert first == -1
+    return ke, rows, cols, oracle.triplet_to_csc(rows, cols, ke.reshape(-1), mesh.n_nodes)
+
+
+@pytest.mark.parametrize("fused", ["0", "1"])
+@pytest.mark.parametrize("rotate", [0.0, 0.3, 1.0])
+def test_fused_adjacency_orientations_bitwise(monkeypatch, fused, rotate):
+    """The cold build records the node adjacency inside the integration kernel in fixed slots
+    (slot = local node).  Elements re-oriented by a rotation of the reference cube put shared nodes
+    at colliding local indices; the build detects the lost slots and re-runs the atomic adjacency
+    pass.  Either way the results are bitwise the oracle's (also with the fusion switched off)."""
+    monkeypatch.setenv("HX_FUSED_ADJACENCY", fused)
+    rng = np.random.default_rng(77)
+    mesh = perturbed_mesh(7, seed=5, distortion=0.15)
+    conn = mesh.connectivity.copy()
+    turn = rng.random(mesh.n_el) < rotate  # 90 degrees about t: a valid, positively oriented relabelling
+    conn[turn] = conn[turn][:, [1, 2, 3, 0, 5, 6, 7, 4]]
+    mesh = Mesh(mesh.coords, np.ascontiguousarray(conn), mesh.coefficient)
+    ke, rows, cols, (cp, ri, vv) = _oracle_build(mesh)
+    b = build_device(D.DeviceMesh.from_host(mesh))
+    assert bits_equal(b.ke.cpu().numpy(), ke)
+    assert bits_equal(b.rows.cpu().numpy(), rows) and bits_equal(b.cols.cpu().numpy(), cols)
+    assert bits_equal(b.csc.col_ptr.cpu().numpy(), cp)
+    assert bits_equal(b.csc.row_idx.cpu().numpy(), ri)
+    assert bits_equal(b.csc.vals.cpu().numpy(), vv)
+
+
+def test_fused_adjacency_slot_collision_detected():
+    """Two elements holding a node at the same local index: the fixed-slot record loses one entry
+    and the status word says so (HX_ST_SLOT_COLLISION) -- the Python layer then re-runs."""
+    from paper_1501_04784_b200 import _native as N
+
+    mesh = perturbed_mesh(3, seed=2)
+    conn = mesh.connectivity.copy()
+    conn[1] = conn[1][[1, 2, 3, 0, 5, 6, 7, 4]]
+    mesh = Mesh(mesh.coords, np.ascontiguousarray(conn), mesh.coefficient)
+    dm = D.DeviceMesh.from_host(mesh)
+    prep = D.new_assembly_prep(dm)
+    ke, _, _, fail = D.integrate_mesh(dm, adjacency=prep)
+    D.raise_if_failed(fail)
+    segs = N.segments([(dm.conn.data_ptr(), ke.data_ptr(), dm.n_el)])
+    col_ptr = torch.empty(dm.n_nodes + 1, dtype=torch.int64, device=dm.conn.device)
+    cap = 16 * dm.n_nodes
+    rbuf = torch.empty(cap, dtype=torch.int64, device=dm.conn.device)
+    vbuf = torch.empty(cap, dtype=torch.float64, device=dm.conn.device)
+    N.check(N.lib().hx_mesh_csc_build(segs, 1, dm.n_nodes, 0, dm.n_nodes, col_ptr.data_ptr(), rbuf.data_ptr(),
+                                      vbuf.data_ptr(), cap, prep.ws.data_ptr(), prep.ws.numel(),
+                                      prep.status.data_ptr(), N.CSC_ADJACENCY_READY, None), "build")
+    torch.cuda.synchronize()
+    assert int(prep.status.item()) & N.ST_SLOT_COLLISION
+
+
+def test_fused_adjacency_bad_node_id_raises():
+    """An out-of-range node id is reported (MeshValidationError, assemble.py:146-149), never
+    dereferenced by the fused integration kernel."""
+    mesh = perturbed_mesh(3, seed=2)
+    conn = mesh.connectivity.copy()
+    conn[4, 6] = mesh.n_nodes + 1000
+    with pytest.raises(MeshValidationError):
+        build_device(D.DeviceMesh.from_host(Mesh(mesh.coords, conn, mesh.coefficient)))
