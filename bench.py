@@ -472,7 +472,7 @@ def measure_e2e(args, mesh, nnz):
 
     e2e_step()
     torch.cuda.synchronize()
-    steps = max(1, min(args.steps, 5))
+    steps = max(1, min(args.steps, 10))
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     start.record(main)
     for _ in range(steps):

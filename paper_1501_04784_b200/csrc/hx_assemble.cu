@@ -310,6 +310,84 @@ __device__ __forceinline__ int column_pattern(const SegTable &T, bool active, in
     return m;
 }
 
+// Sort-based pattern of one column (HX_PATTERN_SORT, the default): every contribution (k, b) of an
+// incident element k whose node v = g[k][b] lies below the diagonal becomes one key
+// (v << 6 | k << 3 | b), appended branch-free to the thread's list L; a 16/32/64-key register
+// network (warp-uniform choice) sorts them, so equal rows form runs whose contributions are already
+// in element order.  Replaces the hash set: no data-dependent probe loops (the hash variant spent
+// half its instructions and most of its divergence there).  Returns m = 1 + distinct rows (0 for an
+// empty column or one outside the fast path) and cnt = keys left sorted in L.
+#ifndef HX_PATTERN_SORT
+#define HX_PATTERN_SORT 1
+#endif
+constexpr int SORT_SLOTS = 64;  // <= 8 elements x 7 other nodes = 56 contributions per column
+
+template <typename K, bool SINGLE, bool FIXED>
+__device__ __forceinline__ int column_pattern_sort(const SegTable &T, bool active, int64_t cl, int32_t c,
+                                                   int32_t *__restrict__ deg_arr, int32_t *__restrict__ adj, K *L,
+                                                   int &cnt, int &deg, uint32_t *__restrict__ status) {
+    int m = 0;
+    deg = 0;
+    int32_t ent[8];
+    cnt = 0;
+    if (active) {
+        deg = incident_sorted<FIXED>(cl, deg_arr, adj, ent, status);
+        if (deg < 0) deg = 0;
+        if (deg > 0) {  // the emit pass reads the sorted incident list
+            int4 *a4 = reinterpret_cast<int4 *>(adj + 8 * cl);
+            a4[0] = make_int4(ent[0], ent[1], ent[2], ent[3]);
+            a4[1] = make_int4(ent[4], ent[5], ent[6], ent[7]);
+        }
+    }
+    if (deg > 0) {
+        int32_t g[8][8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            if (k < deg) {
+                const int4 *c4 = reinterpret_cast<const int4 *>(conn_row<SINGLE>(T, ent[k] >> 3));
+                const int4 lo = __ldg(c4), hi = __ldg(c4 + 1);
+                g[k][0] = lo.x; g[k][1] = lo.y; g[k][2] = lo.z; g[k][3] = lo.w;
+                g[k][4] = hi.x; g[k][5] = hi.y; g[k][6] = hi.z; g[k][7] = hi.w;
+            } else {
+#pragma unroll
+                for (int b = 0; b < 8; ++b) g[k][b] = INT32_MIN;  // never a row (< c)
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+#pragma unroll
+            for (int b = 0; b < 8; ++b) {
+                const int32_t v = g[k][b];
+                L[cnt * COL_BLOCK] = ((K)(uint32_t)v << 6) | (K)(k * 8 + b);  // kept only when v > c
+                cnt += v > c;
+            }
+        const unsigned am = __activemask();
+        if (!__any_sync(am, cnt > 16)) sort_list<16, K>(L, cnt);
+        else if (!__any_sync(am, cnt > 32)) sort_list<32, K>(L, cnt);
+        else sort_list<64, K>(L, cnt);
+        // distinct rows; a row with more than MAX_OFFDIAG_CONTRIB contributions leaves the fast path
+        int rows = 0, run = 0;
+        K prev = ~(K)0;
+        bool ok = true;
+#pragma unroll 1
+        for (int q = 0; q < cnt; ++q) {
+            const K v = L[q * COL_BLOCK] >> 6;
+            const bool head = v != prev;
+            rows += head;
+            run = head ? 1 : run + 1;
+            ok &= run <= MAX_OFFDIAG_CONTRIB;
+            prev = v;
+        }
+        if (!ok || rows > MAXR) {
+            atomicOr(status, HX_ST_ROW_OVERFLOW);
+            cnt = 0;
+        } else {
+            m = 1 + rows;
+        }
+    }
+    return m;
+}
+
 // 2. Pattern pass: one thread per column, COL_BLOCK columns per block.
 //   - incident elements sorted by id and written back to the adjacency (the emit pass reads them
 //     in order);
@@ -321,17 +399,24 @@ __device__ __forceinline__ int column_pattern(const SegTable &T, bool active, in
 //   - m = 1 + distinct rows -> col_ptr[cl] (the exclusive scan turns counts into offsets);
 //   - sorted off-diagonal records (row, word) -> a compact scratch region reserved per block with
 //     one atomic (every block records where its records start).
+#ifndef HX_PATTERN_MIN_BLOCKS
+#define HX_PATTERN_MIN_BLOCKS 10  // 96 registers: 10 x 64-thread tiles per SM (measured best of 1, 10, 12)
+#endif
 template <typename K, bool SINGLE, bool FIXED>
-__global__ void __launch_bounds__(COL_BLOCK)
+__global__ void __launch_bounds__(COL_BLOCK, HX_PATTERN_MIN_BLOCKS)
 pattern_kernel(SegTable T, int64_t col_lo, int64_t ncols, int32_t *__restrict__ deg_arr,
                int32_t *__restrict__ adj, int64_t *__restrict__ col_ptr, int2 *__restrict__ scratch,
                int64_t scratch_capacity, unsigned long long *__restrict__ scratch_top,
                int64_t *__restrict__ block_scratch, uint32_t *__restrict__ status,
                const uint32_t *__restrict__ order, unsigned long long *__restrict__ slot_total) {
+#if HX_PATTERN_SORT
+    __shared__ K sL[SORT_SLOTS * COL_BLOCK];  // this thread's contribution keys, [slot][thread]
+#else
     __shared__ int32_t sH[MAXR * COL_BLOCK];   // hash keys
     __shared__ uint32_t sW[MAXR * COL_BLOCK];  // contribution words, by hash slot
     // compacted / sorted keys (row << 5 | slot): 32-bit keys reuse the hash-key array in place
     __shared__ K sL[sizeof(K) == 4 ? 1 : MAXR * COL_BLOCK];
+#endif
     __shared__ unsigned long long s_base;
     using BlockScan = cub::BlockScan<int32_t, COL_BLOCK>;
     __shared__ typename BlockScan::TempStorage scan_tmp;
@@ -339,13 +424,18 @@ pattern_kernel(SegTable T, int64_t col_lo, int64_t ncols, int32_t *__restrict__ 
     const int64_t idx = (int64_t)blockIdx.x * COL_BLOCK + t;  // position in the processing order
     const int64_t cl = order != nullptr && idx < ncols ? (int64_t)__ldg(order + idx) : idx;
     const int32_t c = (int32_t)(col_lo + cl);
+#if HX_PATTERN_SORT
+    K *L = sL + t;
+    int cnt = 0, deg = 0;
+    const int m = column_pattern_sort<K, SINGLE, FIXED>(T, cl < ncols, cl, c, deg_arr, adj, L, cnt, deg, status);
+#else
     int32_t *H = sH + t;
     uint32_t *W = sW + t;
     K *L = sizeof(K) == 4 ? reinterpret_cast<K *>(sH) + t : sL + t;
-
     int32_t ent[8];
     int deg = 0;
     const int m = column_pattern<K, SINGLE, true, FIXED>(T, cl < ncols, cl, c, deg_arr, adj, H, W, L, ent, deg, status);
+#endif
     if (cl < ncols) col_ptr[cl] = m;
     if (FIXED) {
         const unsigned filled = __reduce_add_sync(0xffffffffu, (unsigned)deg);
@@ -366,11 +456,35 @@ pattern_kernel(SegTable T, int64_t col_lo, int64_t ncols, int32_t *__restrict__ 
         if (off > 0) atomicOr(status, HX_ST_SCRATCH_OVERFLOW);
         return;
     }
+#if HX_PATTERN_SORT
+    // runs of equal rows -> records (row, count | (k, b) pairs in element order)
+    int j = -1, n = 0;
+    K prev = ~(K)0;
+    uint32_t word = 0;
+#pragma unroll 1
+    for (int q = 0; q < cnt; ++q) {
+        const K key = L[q * COL_BLOCK];
+        const K v = key >> 6;
+        const uint32_t kb = (uint32_t)key & 63u;
+        if (v != prev) {
+            if (j >= 0) scratch[sb + j] = make_int2((int)prev, (int)word);
+            ++j;
+            prev = v;
+            word = 1u | (kb << 3);
+            n = 1;
+        } else {
+            word = (word + 1u) | (kb << (3 + 6 * n));
+            ++n;
+        }
+    }
+    if (j >= 0) scratch[sb + j] = make_int2((int)prev, (int)word);
+#else
 #pragma unroll 1
     for (int j = 0; j < off; ++j) {
         const K key = L[j * COL_BLOCK];
         scratch[sb + j] = make_int2((int)(key >> 5), (int)W[(int)(key & 31) * COL_BLOCK]);
     }
+#endif
 }
 
 // Fixed-slot adjacency check: every (element, local node) pair must have landed in its own slot.

@@ -428,14 +428,19 @@ __device__ __forceinline__ bool ke_gauss_point(GpWarpSmem &sm, int el, int gp, b
 }
 
 // Mesh kernel: elements [lo, lo+n) of the mesh; outputs indexed from 0 (= element lo).
-// Persistent warps with dynamic work distribution: each warp takes element quads from a global
-// counter (so the kernel balances itself when it shares the GPU with the concurrently running
-// symbolic assembly) and prefetches the next quad's node ids, coordinates and coefficients into
+// Persistent warps, each prefetching the next quad's node ids, coordinates and coefficients into
 // registers before integrating the current one, so the gather latency hides under the FP64 work.
-// Adjacency outputs of the fused symbolic first pass (WITH_ADJ): deg (n_nodes) i32 zeroed by the
-// caller, adj (8 n_nodes) i32 slots, status bits HX_ST_BAD_INDEX / HX_ST_DEG_OVERFLOW.
+// HX_KE_STATIC (default): warp w takes quads w, w + W, w + 2W, ... (W = resident warps) -- every SM
+// is busy with this kernel alone, so the static split balances to within one quad and no warp waits
+// on a work-counter atomic (ncu: 15% of the kernel's stall samples sat on that atomic's result);
+// HX_KE_STATIC=0 takes quads from a global counter instead (self-balancing when the kernel shares
+// the GPU, e.g. with a concurrently running symbolic phase).
+#ifndef HX_KE_STATIC
+#define HX_KE_STATIC 1
+#endif
+// Adjacency output of the fused symbolic first pass (WITH_ADJ): adj (8 n_nodes) i32 fixed slots
+// (emptied to -1 by the caller), status bit HX_ST_BAD_INDEX.
 struct AdjOut {
-    int32_t *deg;
     int32_t *adj;
     uint32_t *status;
 };
@@ -457,7 +462,13 @@ integrate_mesh_kernel(const double *__restrict__ coords, int64_t n_nodes, const 
     GpWarpSmem &sm = s_warp[warp];
     const int64_t n_quads = (n + GP_EL_PER_WARP - 1) / GP_EL_PER_WARP;
     const int64_t first_dynamic = (int64_t)gridDim.x * GP_WARPS;
+    int64_t static_next = (int64_t)blockIdx.x * GP_WARPS + warp;
     auto grab = [&]() -> int64_t {
+        if (HX_KE_STATIC) {
+            (void)quad_counter;
+            static_next += first_dynamic;
+            return static_next;
+        }
         unsigned q = 0;
         if (lane == 0) q = atomicAdd(quad_counter, 1u);
         return first_dynamic + (int64_t)__shfl_sync(0xffffffffu, q, 0);
@@ -649,7 +660,7 @@ static void launch_integrate(int64_t blocks, cudaStream_t s, const double *coord
         kernel<<<(unsigned)blocks, GP_BLOCK, GP_SMEM, s>>>(coords, n_nodes, conn, coeff, lo, n, ke, rows, cols, fmin,
                                                            counter, adj);
     };
-    if (adj.deg != nullptr) {
+    if (adj.adj != nullptr) {
         if (rows != nullptr) go(integrate_mesh_kernel<MODE, true, true>);
         else go(integrate_mesh_kernel<MODE, false, true>);
     } else {
@@ -761,7 +772,7 @@ extern "C" int hx_integrate_mesh(const double *coords, int64_t n_nodes, const in
     int rc = HX_OK;
     if (!integrate_args_ok(lo, hi, ke, rows, cols, fail, mode, rc)) return rc;
     return integrate_mesh_impl(coords, n_nodes, conn, coeff, lo, hi, ke, rows, cols, mode, fail,
-                               AdjOut{nullptr, nullptr, nullptr}, (cudaStream_t)stream);
+                               AdjOut{nullptr, nullptr}, (cudaStream_t)stream);
 }
 
 extern "C" int hx_integrate_mesh_adjacency(const double *coords, int64_t n_nodes, const int32_t *conn,
@@ -776,8 +787,9 @@ extern "C" int hx_integrate_mesh_adjacency(const double *coords, int64_t n_nodes
                        (long long)hi);
         return HX_ERR_VALUE;
     }
-    AdjOut adj{nullptr, nullptr, csc_status};
-    rc = mesh_ws_adjacency(csc_workspace, workspace_bytes, n_nodes, &adj.deg, &adj.adj);
+    AdjOut adj{nullptr, csc_status};
+    int32_t *deg = nullptr;
+    rc = mesh_ws_adjacency(csc_workspace, workspace_bytes, n_nodes, &deg, &adj.adj);
     if (rc) return rc;
     cudaStream_t s = (cudaStream_t)stream;
     if (reset) {  // status 0, every adjacency slot empty (-1)
