@@ -430,13 +430,13 @@ __device__ __forceinline__ bool ke_gauss_point(GpWarpSmem &sm, int el, int gp, b
 // Mesh kernel: elements [lo, lo+n) of the mesh; outputs indexed from 0 (= element lo).
 // Persistent warps, each prefetching the next quad's node ids, coordinates and coefficients into
 // registers before integrating the current one, so the gather latency hides under the FP64 work.
-// HX_KE_STATIC (default): warp w takes quads w, w + W, w + 2W, ... (W = resident warps) -- every SM
-// is busy with this kernel alone, so the static split balances to within one quad and no warp waits
-// on a work-counter atomic (ncu: 15% of the kernel's stall samples sat on that atomic's result);
-// HX_KE_STATIC=0 takes quads from a global counter instead (self-balancing when the kernel shares
-// the GPU, e.g. with a concurrently running symbolic phase).
+// Work distribution: warps take element quads from a global counter (self-balancing, also when the
+// kernel shares the GPU with a concurrently running symbolic phase).  HX_KE_STATIC=1 assigns quads
+// w, w + W, w + 2W, ... instead (no counter atomic): measured 1% slower at C3/C4 although ncu
+// attributes 15% of the stall samples to waiting on the atomic's result -- other warps fill those
+// cycles, so the default stays dynamic.
 #ifndef HX_KE_STATIC
-#define HX_KE_STATIC 1
+#define HX_KE_STATIC 0
 #endif
 // Adjacency output of the fused symbolic first pass (WITH_ADJ): adj (8 n_nodes) i32 fixed slots
 // (emptied to -1 by the caller), status bit HX_ST_BAD_INDEX.
