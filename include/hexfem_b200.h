@@ -19,6 +19,7 @@
  *                                  ComputeBackend.run
  *   hx_integrate_mesh              integrate.py:146-149 + 152-212 (gather + per-group run) fused
  *                                  with assemble.py:86-93 connectivity_index_arrays
+ *   hx_integrate_mesh_adjacency    hx_integrate_mesh + the node adjacency (first pass) of hx_mesh_csc_build
  *   hx_connectivity_index_arrays   assemble.py:86-93
  *   hx_mesh_csc_*                  assemble.py:152-239 DirectAssembler / assemble_direct, and
  *                                  triplet_to_csc (assemble.py:110-140) on mesh triplets
