@@ -162,17 +162,79 @@ constexpr int P_EL_STRIDE = 76;
 // loads), j stride 10 and element stride 88 make both the stores and the loads conflict-free.
 constexpr int T_J_STRIDE = 10;
 constexpr int T_EL_STRIDE = 88;
+// HX_KE_FULL_T: all 36 contributions of a Gauss point are staged at once (t[el][p][g], p stride 10,
+// element stride 376 -- conflict-free 64-bit stores and 128-bit loads), so a lane reduces its up to
+// five entries as independent chains after a single __syncwarp instead of five store/sync/reduce
+// passes with one serial 8-add chain each.  The product table P aliases the buffer (it is dead once
+// J is formed; a __syncwarp separates the last P read from the first contribution store).
+#ifndef HX_KE_FULL_T
+#define HX_KE_FULL_T 1
+#endif
+constexpr int TF_EL_STRIDE = 376;
 
 __host__ __device__ constexpr int bit_r(int a) { return nat_r(a) > 0; }
 __host__ __device__ constexpr int bit_s(int a) { return nat_s(a) > 0; }
 __host__ __device__ constexpr int bit_t(int a) { return nat_t(a) > 0; }
 
 struct __align__(16) GpWarpSmem {
+#if HX_KE_FULL_T
+    union {
+        double t[GP_EL_PER_WARP * TF_EL_STRIDE];
+        double P[GP_EL_PER_WARP * P_EL_STRIDE];
+    };
+#else
     double t[GP_EL_PER_WARP * T_EL_STRIDE];
     double P[GP_EL_PER_WARP * P_EL_STRIDE];
+#endif
     double coeff[GP_EL_PER_WARP];
     int32_t conn[GP_EL_PER_WARP * 8];
 };
+
+// All 36 staged contributions of element el (t[el][p][g]) reduced by its 8 lanes -- lane gp takes
+// entries gp, gp + 8, ..., as independent chains -- and KE / iK / jK stored (HX_KE_FULL_T).  Exact
+// mode sums in Gauss-point order, fast mode as a fixed depth-3 tree.
+template <int MODE, bool WITH_INDEX>
+__device__ __forceinline__ void reduce_store_all(const GpWarpSmem &sm, const double *tb, int el, int gp,
+                                                 int64_t out_el, bool valid, double *__restrict__ ke_out,
+                                                 int32_t *__restrict__ rows_out, int32_t *__restrict__ cols_out,
+                                                 const uint8_t *s_pi, const uint8_t *s_pj) {
+    double acc[5];
+#pragma unroll
+    for (int c = 0; c < 5; ++c) {
+        const int p = 8 * c + gp;
+        acc[c] = 0.0;
+        if (c < 4 || gp < 4) {
+            const double2 *src = reinterpret_cast<const double2 *>(tb + p * T_J_STRIDE);
+            const double2 v0 = src[0], v1 = src[1], v2 = src[2], v3 = src[3];
+            if (MODE == HX_MODE_EXACT) {
+                double a = dadd(0.0, v0.x);
+                a = dadd(a, v0.y);
+                a = dadd(a, v1.x);
+                a = dadd(a, v1.y);
+                a = dadd(a, v2.x);
+                a = dadd(a, v2.y);
+                a = dadd(a, v3.x);
+                acc[c] = dadd(a, v3.y);
+            } else {
+                acc[c] = ((v0.x + v0.y) + (v1.x + v1.y)) + ((v2.x + v2.y) + (v3.x + v3.y));
+            }
+        }
+    }
+    if (valid) {
+#pragma unroll
+        for (int c = 0; c < 5; ++c) {
+            const int p = 8 * c + gp;
+            if (c < 4 || gp < 4) {
+                ke_out[out_el * 36 + p] = acc[c];
+                if (WITH_INDEX) {
+                    const int32_t gi = sm.conn[el * 8 + s_pi[p]], gj = sm.conn[el * 8 + s_pj[p]];
+                    rows_out[out_el * 36 + p] = max(gi, gj);
+                    cols_out[out_el * 36 + p] = min(gi, gj);
+                }
+            }
+        }
+    }
+}
 
 __device__ __forceinline__ double mag_select(int k) {
     return k == 0 ? dn_magnitude(0) : (k == 1 ? dn_magnitude(1) : dn_magnitude(2));
@@ -303,6 +365,21 @@ __device__ __forceinline__ bool ke_gauss_point_fast(GpWarpSmem &sm, int el, int 
     for (int d = 0; d < 3; ++d)
 #pragma unroll
         for (int a = 0; a < 8; ++a) H[d][a] = fma(G[d][0], dn(0, a), fma(G[d][1], dn(1, a), G[d][2] * dn(2, a)));
+#if HX_KE_FULL_T
+    __syncwarp();  // every lane has read the coordinates, which the contribution buffer overwrites
+    {
+        double *tf = sm.t + el * TF_EL_STRIDE;
+#pragma unroll
+        for (int p = 0; p < 36; ++p) {
+            const int i = pack_i(p), q = pack_j(p);
+            tf[p * T_J_STRIDE + gp] = fma(dn(0, i), H[0][q], fma(dn(1, i), H[1][q], dn(2, i) * H[2][q]));
+        }
+        __syncwarp();
+        reduce_store_all<HX_MODE_FAST, WITH_INDEX>(sm, tf, el, gp, out_el, valid, ke_out, rows_out, cols_out, s_pi,
+                                                  s_pj);
+    }
+    return ok;
+#endif
     double *tb = sm.t + el * T_EL_STRIDE;
 #pragma unroll
     for (int c = 0; c < 5; ++c) {
@@ -406,6 +483,22 @@ __device__ __forceinline__ bool ke_gauss_point(GpWarpSmem &sm, int el, int gp, b
         }
     }
     const double scale = dmul(sm.coeff[el], det);
+#if HX_KE_FULL_T
+    __syncwarp();  // every lane has read its J from P, which the contribution buffer overwrites
+    {
+        double *tf = sm.t + el * TF_EL_STRIDE;
+#pragma unroll
+        for (int p = 0; p < 36; ++p) {
+            const int i = pack_i(p), q = pack_j(p);
+            const double s = dadd(dadd(dmul(B[0][i], B[0][q]), dmul(B[1][i], B[1][q])), dmul(B[2][i], B[2][q]));
+            tf[p * T_J_STRIDE + gp] = dmul(scale, s);
+        }
+        __syncwarp();
+        reduce_store_all<HX_MODE_EXACT, WITH_INDEX>(sm, tf, el, gp, out_el, valid, ke_out, rows_out, cols_out,
+                                                   s_pi, s_pj);
+    }
+    return ok;
+#endif
     // 36 contributions, 8 per pass, reduced across the element's 8 lanes in Gauss-point order
     double *tb = sm.t + el * T_EL_STRIDE;
 #pragma unroll
