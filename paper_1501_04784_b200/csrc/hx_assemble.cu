@@ -322,6 +322,26 @@ __device__ __forceinline__ int column_pattern(const SegTable &T, bool active, in
 #endif
 constexpr int SORT_SLOTS = 64;  // <= 8 elements x 7 other nodes = 56 contributions per column
 
+// Sort the first n (<= N) contribution keys of L in place and, while they are in registers, count
+// the distinct rows (key >> 6) and check that no row has more than MAX_OFFDIAG_CONTRIB
+// contributions (sorted: a run of 5 has v[q] and v[q - 4] in the same row).
+template <int N, typename K>
+__device__ __forceinline__ void sort_count(K *L, int n, int &rows, bool &ok) {
+    K v[N];
+#pragma unroll
+    for (int q = 0; q < N; ++q) v[q] = q < n ? L[q * COL_BLOCK] : (K)~(K)0;
+    bitonic_sort<N, K>(v);
+    rows = 0;
+    ok = true;
+#pragma unroll
+    for (int q = 0; q < N; ++q) {
+        if (q < n) L[q * COL_BLOCK] = v[q];
+        const K r = v[q] >> 6;
+        rows += q < n && (q == 0 || r != (v[q > 0 ? q - 1 : 0] >> 6));
+        if (q >= MAX_OFFDIAG_CONTRIB) ok &= !(q < n && r == (v[q >= MAX_OFFDIAG_CONTRIB ? q - MAX_OFFDIAG_CONTRIB : 0] >> 6));
+    }
+}
+
 template <typename K, bool SINGLE, bool FIXED>
 __device__ __forceinline__ int column_pattern_sort(const SegTable &T, bool active, int64_t cl, int32_t c,
                                                    int32_t *__restrict__ deg_arr, int32_t *__restrict__ adj, K *L,
@@ -350,34 +370,25 @@ __device__ __forceinline__ int column_pattern_sort(const SegTable &T, bool activ
                 g[k][4] = hi.x; g[k][5] = hi.y; g[k][6] = hi.z; g[k][7] = hi.w;
             } else {
 #pragma unroll
-                for (int b = 0; b < 8; ++b) g[k][b] = INT32_MIN;  // never a row (< c)
+                for (int b = 0; b < 8; ++b) g[k][b] = -1;  // never a row (< c)
             }
         }
+        // node ids and c are in [0, 2^31): v > c <=> the sign bit of c - v (no overflow)
 #pragma unroll
         for (int k = 0; k < 8; ++k)
 #pragma unroll
             for (int b = 0; b < 8; ++b) {
                 const int32_t v = g[k][b];
                 L[cnt * COL_BLOCK] = ((K)(uint32_t)v << 6) | (K)(k * 8 + b);  // kept only when v > c
-                cnt += v > c;
+                cnt += (int)((uint32_t)(c - v) >> 31);
             }
         const unsigned am = __activemask();
-        if (!__any_sync(am, cnt > 16)) sort_list<16, K>(L, cnt);
-        else if (!__any_sync(am, cnt > 32)) sort_list<32, K>(L, cnt);
-        else sort_list<64, K>(L, cnt);
         // distinct rows; a row with more than MAX_OFFDIAG_CONTRIB contributions leaves the fast path
-        int rows = 0, run = 0;
-        K prev = ~(K)0;
+        int rows = 0;
         bool ok = true;
-#pragma unroll 1
-        for (int q = 0; q < cnt; ++q) {
-            const K v = L[q * COL_BLOCK] >> 6;
-            const bool head = v != prev;
-            rows += head;
-            run = head ? 1 : run + 1;
-            ok &= run <= MAX_OFFDIAG_CONTRIB;
-            prev = v;
-        }
+        if (!__any_sync(am, cnt > 16)) sort_count<16, K>(L, cnt, rows, ok);
+        else if (!__any_sync(am, cnt > 32)) sort_count<32, K>(L, cnt, rows, ok);
+        else sort_count<64, K>(L, cnt, rows, ok);
         if (!ok || rows > MAXR) {
             atomicOr(status, HX_ST_ROW_OVERFLOW);
             cnt = 0;
@@ -458,7 +469,8 @@ pattern_kernel(SegTable T, int64_t col_lo, int64_t ncols, int32_t *__restrict__ 
     }
 #if HX_PATTERN_SORT
     // runs of equal rows -> records (row, count | (k, b) pairs in element order)
-    int j = -1, n = 0;
+    int2 *out = scratch + sb - 1;  // record j of this column at out[j + 1]; j = -1 before the first
+    int j = -1, shift = 3;
     K prev = ~(K)0;
     uint32_t word = 0;
 #pragma unroll 1
@@ -466,18 +478,14 @@ pattern_kernel(SegTable T, int64_t col_lo, int64_t ncols, int32_t *__restrict__ 
         const K key = L[q * COL_BLOCK];
         const K v = key >> 6;
         const uint32_t kb = (uint32_t)key & 63u;
-        if (v != prev) {
-            if (j >= 0) scratch[sb + j] = make_int2((int)prev, (int)word);
-            ++j;
-            prev = v;
-            word = 1u | (kb << 3);
-            n = 1;
-        } else {
-            word = (word + 1u) | (kb << (3 + 6 * n));
-            ++n;
-        }
+        const bool head = v != prev;
+        if (head && j >= 0) out[j + 1] = make_int2((int)prev, (int)word);
+        j += head;
+        word = head ? (1u | (kb << 3)) : ((word + 1u) | (kb << shift));
+        shift = head ? 9 : shift + 6;
+        prev = v;
     }
-    if (j >= 0) scratch[sb + j] = make_int2((int)prev, (int)word);
+    if (j >= 0) out[j + 1] = make_int2((int)prev, (int)word);
 #else
 #pragma unroll 1
     for (int j = 0; j < off; ++j) {
