@@ -190,6 +190,21 @@ struct __align__(16) GpWarpSmem {
     int32_t conn[GP_EL_PER_WARP * 8];
 };
 
+// Output stores of the integration kernel.  HX_KE_STREAM_STORES: evict-first (st.global.cs) -- KE,
+// iK and jK are not re-read by this kernel, so they should not push the partially written adjacency
+// slot sectors out of L2 (each slot sector collects 8 stores from elements up to a layer apart).
+#ifndef HX_KE_STREAM_STORES
+#define HX_KE_STREAM_STORES 1
+#endif
+template <typename T>
+__device__ __forceinline__ void st_out(T *p, T v) {
+#if HX_KE_STREAM_STORES
+    __stcs(p, v);
+#else
+    *p = v;
+#endif
+}
+
 // All 36 staged contributions of element el (t[el][p][g]) reduced by its 8 lanes -- lane gp takes
 // entries gp, gp + 8, ..., as independent chains -- and KE / iK / jK stored (HX_KE_FULL_T).  Exact
 // mode sums in Gauss-point order, fast mode as a fixed depth-3 tree.
@@ -225,11 +240,11 @@ __device__ __forceinline__ void reduce_store_all(const GpWarpSmem &sm, const dou
         for (int c = 0; c < 5; ++c) {
             const int p = 8 * c + gp;
             if (c < 4 || gp < 4) {
-                ke_out[out_el * 36 + p] = acc[c];
+                st_out(ke_out + out_el * 36 + p, acc[c]);
                 if (WITH_INDEX) {
                     const int32_t gi = sm.conn[el * 8 + s_pi[p]], gj = sm.conn[el * 8 + s_pj[p]];
-                    rows_out[out_el * 36 + p] = max(gi, gj);
-                    cols_out[out_el * 36 + p] = min(gi, gj);
+                    st_out(rows_out + out_el * 36 + p, max(gi, gj));
+                    st_out(cols_out + out_el * 36 + p, min(gi, gj));
                 }
             }
         }

@@ -701,3 +701,29 @@ def test_fused_adjacency_bad_node_id_raises():
     conn[4, 6] = mesh.n_nodes + 1000
     with pytest.raises(MeshValidationError):
         build_device(D.DeviceMesh.from_host(Mesh(mesh.coords, conn, mesh.coefficient)))
+
+
+@pytest.mark.parametrize("ranges", [[(0, 100), (100, 250), (250, 343)], [(250, 343), (0, 250)], [(0, 100)]])
+def test_fused_adjacency_with_element_groups(ranges):
+    """BatchPlan-style element groups (one integration launch each, any order) share one fused
+    adjacency record; a partial cover falls back to the assembly's own pass.  Bitwise either way."""
+    mesh = permuted_mesh(perturbed_mesh(7, seed=9), seed=3)
+    ke, rows, cols, (cp, ri, vv) = _oracle_build(mesh)
+    dm = D.DeviceMesh.from_host(mesh)
+    if sum(hi - lo for lo, hi in ranges) != mesh.n_el:
+        # elements outside the groups keep their (caller-provided) values: zero KE rows
+        ke0 = torch.zeros((mesh.n_el, 36), dtype=torch.float64, device=dm.conn.device)
+        b = build_device(dm, ranges=ranges, ke=ke0)
+        part = ke.copy()
+        covered = np.zeros(mesh.n_el, bool)
+        for lo, hi in ranges:
+            covered[lo:hi] = True
+        part[~covered] = 0.0
+        cp, ri, vv = oracle.triplet_to_csc(rows, cols, part.reshape(-1), mesh.n_nodes)
+        assert bits_equal(b.ke.cpu().numpy(), part)
+    else:
+        b = build_device(dm, ranges=ranges)
+        assert bits_equal(b.ke.cpu().numpy(), ke)
+    assert bits_equal(b.csc.col_ptr.cpu().numpy(), cp)
+    assert bits_equal(b.csc.row_idx.cpu().numpy(), ri)
+    assert bits_equal(b.csc.vals.cpu().numpy(), vv)
