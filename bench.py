@@ -51,6 +51,8 @@ def parse():
     p.add_argument("--mode", default="exact", choices=["exact", "fast"])
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--e2e-rows", choices=["i32", "i64"], default="i32",
+                   help="row indices over PCIe: int32 widened on the host (default) or int64")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-sample-layers", type=int, default=6)
     return p.parse_args()
@@ -438,17 +440,20 @@ def measure_kernels(args, rank, world, runner, dm):
 
 
 def measure_e2e(args, mesh, nnz):
-    """Public host API with pinned buffers: H2D mesh -> build -> D2H lower CSC, every step.
+    """Public host API with pinned buffers: H2D mesh -> build -> host LowerCscMatrix, every step.
 
     Steps are pipelined the way a service would run back-to-back builds: step i's CSC leaves over
-    PCIe on a copy stream while step i+1's mesh arrives and is built (PCIe is full duplex; the
-    D2H of the 16 B/nnz result is the long pole).  Every step still does its own H2D, build and
-    D2H inside the timed region; the region ends when the last D2H has landed in host memory.
+    PCIe on a copy stream (transfer.CscHostTransfer: int64 col_ptr, float64 values and int32 row
+    indices, widened back to the reference's int64 on the host cores) while step i+1's mesh arrives
+    and is built.  Every step does its own H2D, build, D2H and widening inside the timed region,
+    which ends when the last step's host matrix is complete (host clock; the device work is
+    bracketed by synchronisations).  ``--e2e-rows i64`` sends the int64 row indices instead.
     """
     import torch
 
     from paper_1501_04784_b200 import device as D
     from paper_1501_04784_b200.pipeline import build_device
+    from paper_1501_04784_b200.transfer import CscHostTransfer
 
     def pinned(a):
         t = torch.empty(a.shape, dtype={np.float64: torch.float64, np.int32: torch.int32}[a.dtype.type],
@@ -457,40 +462,58 @@ def measure_e2e(args, mesh, nnz):
         return t
 
     h_coords, h_conn, h_coeff = pinned(mesh.coords), pinned(mesh.connectivity), pinned(mesh.coefficient)
-    o_cp = torch.empty(mesh.n_nodes + 1, dtype=torch.int64, pin_memory=True)
-    o_ri = torch.empty(nnz, dtype=torch.int64, pin_memory=True)
-    o_v = torch.empty(nnz, dtype=torch.float64, pin_memory=True)
     dev = torch.device("cuda", torch.cuda.current_device())
     h2d = sum(t.numel() * t.element_size() for t in (h_coords, h_conn, h_coeff))
-    d2h = sum(t.numel() * t.element_size() for t in (o_cp, o_ri, o_v))
-    main, copy = torch.cuda.Stream(), torch.cuda.Stream()
+    main = torch.cuda.Stream()
+    compact = args.e2e_rows == "i32"
+    if compact:
+        xfer = CscHostTransfer(mesh.n_nodes, nnz, depth=2, device=dev)
+        d2h = xfer.bytes_per_transfer(nnz)
+    else:
+        o_cp = torch.empty(mesh.n_nodes + 1, dtype=torch.int64, pin_memory=True)
+        o_ri = torch.empty(nnz, dtype=torch.int64, pin_memory=True)
+        o_v = torch.empty(nnz, dtype=torch.float64, pin_memory=True)
+        d2h = sum(t.numel() * t.element_size() for t in (o_cp, o_ri, o_v))
+        copy = torch.cuda.Stream()
+    futures = []
 
     def e2e_step():
         with torch.cuda.stream(main):
             dm = D.DeviceMesh(h_coords.to(dev, non_blocking=True), h_conn.to(dev, non_blocking=True),
                               h_coeff.to(dev, non_blocking=True))
             b = build_device(dm, mode=args.mode)
-            done = main.record_event()
-        copy.wait_event(done)
-        with torch.cuda.stream(copy):
-            for src, dst in ((b.csc.col_ptr, o_cp), (b.csc.row_idx, o_ri), (b.csc.vals, o_v)):
-                dst.copy_(src, non_blocking=True)
-                src.record_stream(copy)  # keep the block alive until the copy stream is done with it
+            if compact:
+                futures.append(xfer.submit(b.csc, stream=main))
+            else:
+                copy.wait_event(main.record_event())
+                with torch.cuda.stream(copy):
+                    for src, dst in ((b.csc.col_ptr, o_cp), (b.csc.row_idx, o_ri), (b.csc.vals, o_v)):
+                        dst.copy_(src, non_blocking=True)
+                        src.record_stream(copy)
         del b, dm
 
+    def drain():
+        for f in futures:
+            f.result()
+        futures.clear()
+        torch.cuda.synchronize()
+
     e2e_step()
-    torch.cuda.synchronize()
+    drain()
     steps = max(1, min(args.steps, 10))
-    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    start.record(main)
+    t0 = time.perf_counter()
     for _ in range(steps):
         e2e_step()
-    stop.record(copy)
-    torch.cuda.synchronize()
-    ms = start.elapsed_time(stop) / steps
+    drain()
+    ms = (time.perf_counter() - t0) * 1e3 / steps
+    if compact:
+        xfer.close()
     return {"value": mesh.n_el / (ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-            "ms_per_step": ms, "steps": steps, "pipelined": "step i's D2H overlaps step i+1's H2D + build",
-            "api": "DeviceMesh(pinned host -> HBM) + build_device + CSC -> pinned host"}
+            "ms_per_step": ms, "steps": steps,
+            "pipelined": "step i's D2H (+ host widening) overlaps step i+1's H2D + build",
+            "row_transfer": "int32 over PCIe, widened to int64 on the host" if compact else "int64",
+            "api": "DeviceMesh(pinned host -> HBM) + build_device + transfer.CscHostTransfer -> host LowerCscMatrix"
+                   if compact else "DeviceMesh(pinned host -> HBM) + build_device + CSC -> pinned host"}
 
 
 def main():

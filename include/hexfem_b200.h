@@ -232,6 +232,13 @@ int hx_block_gather(const int32_t *conn, const double *coeff, const int64_t *ids
 int hx_generate_cube_mesh(int64_t nx, int64_t ny, int64_t nz, double h, double c0, double *coords, int32_t *conn,
                           double *coeff, void *stream);
 
+/* ---- compact device -> host transfer of the lower CSC (12 instead of 16 bytes per entry) -------
+ * narrow: rows32[i] = (int32) row_idx[i] on the device (node ids are int32 in the reference).
+ * widen:  row_idx[i] = rows32[i] on the host with `threads` worker threads (<= 0: all), giving back
+ *         the reference's int64 row_idx (assemble.py:51-62).  Host code. */
+int hx_rows_narrow(const int64_t *row_idx, int32_t *rows32, int64_t n, void *stream);
+int hx_rows_widen(const int32_t *rows32, int64_t *row_idx, int64_t n, int32_t threads);
+
 /* ---- Matrix Market export (sparseio.py:73-87), host code -----------------------------------------
  * Host arrays of a lower CSC -> "%%MatrixMarket matrix coordinate real symmetric" file, 1-based,
  * column-major, "%.17g" values: byte-identical to the reference's writer, formatted by `threads`

@@ -17,7 +17,7 @@ from . import _native as N
 from .errors import ConfigurationError, DegenerateElementError, MeshValidationError, NativeLibraryError
 
 __all__ = [
-    "DeviceMesh", "DeviceCsc", "AssemblyPrep", "new_assembly_prep", "require_device", "stream_handle", "integrate_mesh", "stiffness_batch",
+    "DeviceMesh", "DeviceCsc", "AssemblyPrep", "new_assembly_prep", "rows_narrow", "require_device", "stream_handle", "integrate_mesh", "stiffness_batch",
     "connectivity_index_arrays", "raise_if_failed", "mesh_csc", "triplet_csc", "MeshPlan", "mesh_plan_async",
     "mesh_emit", "plan_assembly", "block_elements", "generate_cube_mesh",
 ]
@@ -444,6 +444,19 @@ def mesh_emit(plan: MeshPlan, ke: torch.Tensor, stream=None) -> DeviceCsc:
         order = "element" if plan.flags & N.CSC_ORDER_BY_ELEMENT else "column"
         return mesh_csc([(plan.conn, ke)], plan.n_nodes, stream=stream, order=order)
     return DeviceCsc(plan.col_ptr, plan.row_buf[:nnz], plan.val_buf[:nnz], plan.n_nodes, 0, "mesh")
+
+
+def rows_narrow(row_idx: torch.Tensor, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """int32 copy of an int64 row-index array on the device (hx_rows_narrow): the compact form the
+    host transfer sends over PCIe."""
+    if row_idx.dtype != torch.int64 or row_idx.dim() != 1 or not row_idx.is_contiguous():
+        raise ValueError("row_idx must be a contiguous 1-D int64 tensor")
+    if out is None:
+        out = torch.empty(row_idx.shape[0], dtype=torch.int32, device=row_idx.device)
+    _check_tensor(out, torch.int32, (row_idx.shape[0],), "out")
+    N.check(N.lib().hx_rows_narrow(_ptr(row_idx), _ptr(out), row_idx.shape[0], stream_handle(stream)),
+            "hx_rows_narrow")
+    return out
 
 
 def block_elements(dm: DeviceMesh, col_lo: int, col_hi: int, ids=None, ws=None, stream=None):

@@ -1,0 +1,105 @@
+"""Device lower CSC -> host ``LowerCscMatrix`` with the reference's dtypes (assemble.py:51-62: int64
+col_ptr / row_idx, float64 vals), pipelined for back-to-back builds.
+
+PCIe (~57 GB/s device -> host) bounds the end-to-end build of a large mesh: its 16-byte entries
+are ~14.9 GB at 400^3.  Row indices are node ids (int32 in the reference's meshes), so they cross
+as int32 (``hx_rows_narrow`` on the device) and are sign-extended back to int64 on the host by all
+host cores (``hx_rows_widen``) while the next build's transfers run: 12 bytes per entry cross the
+bus.  Values and col_ptr cross unchanged into pinned buffers.
+
+A ``CscHostTransfer`` owns ``depth`` result slots (pinned values / col_ptr / int32 rows, a host
+int64 row array); ``submit`` enqueues the copies of a device CSC on a copy stream ordered after the
+producing stream and returns a future of the host matrix, whose arrays stay valid until the slot
+is reused ``depth`` submissions later.
+"""
+
+from __future__ import annotations
+
+import os
+from concurrent.futures import Future, ThreadPoolExecutor
+
+import numpy as np
+import torch
+
+from . import _native as N
+from . import device as D
+from .assemble import LowerCscMatrix
+
+__all__ = ["CscHostTransfer", "host_threads"]
+
+
+def host_threads() -> int:
+    """Host cores this process may use (the widening pass runs one thread per core)."""
+    try:
+        return max(1, len(os.sched_getaffinity(0)))
+    except AttributeError:  # pragma: no cover - non-Linux
+        return max(1, os.cpu_count() or 1)
+
+
+class _Slot:
+    def __init__(self, n_cols: int, nnz: int):
+        self.col_ptr = torch.empty(n_cols + 1, dtype=torch.int64, pin_memory=True)
+        self.vals = torch.empty(max(nnz, 1), dtype=torch.float64, pin_memory=True)
+        self.rows32 = torch.empty(max(nnz, 1), dtype=torch.int32, pin_memory=True)
+        self.row_idx = np.empty(max(nnz, 1), dtype=np.int64)
+        self.row_idx.fill(0)  # fault the pages in now, not inside a timed transfer
+        self.pending: Future | None = None
+
+
+class CscHostTransfer:
+    """Pipelined compact transfer of device CSC blocks with a fixed shape (n_cols, nnz capacity)."""
+
+    def __init__(self, n_cols: int, nnz_capacity: int, depth: int = 2, threads: int | None = None,
+                 device=None):
+        if depth < 1:
+            raise ValueError("depth must be at least 1")
+        self.dev = D.require_device(device)
+        self.n_cols, self.capacity = int(n_cols), int(nnz_capacity)
+        self.threads = host_threads() if threads is None else int(threads)
+        self.slots = [_Slot(self.n_cols, self.capacity) for _ in range(depth)]
+        self.copy = torch.cuda.Stream(device=self.dev)
+        self.pool = ThreadPoolExecutor(max_workers=depth)
+        self.k = 0
+
+    def bytes_per_transfer(self, nnz: int) -> int:
+        """PCIe bytes of one transfer: col_ptr int64 + row indices int32 + values float64."""
+        return 8 * (self.n_cols + 1) + 12 * nnz
+
+    def submit(self, csc: D.DeviceCsc, stream=None) -> Future:
+        nnz = csc.nnz
+        if csc.col_ptr.shape[0] != self.n_cols + 1 or nnz > self.capacity:
+            raise ValueError("CSC block does not fit this transfer's buffers")
+        slot = self.slots[self.k % len(self.slots)]
+        self.k += 1
+        if slot.pending is not None:  # its previous result must be finished (widened) first
+            slot.pending.result()
+        producer = torch.cuda.current_stream(self.dev) if stream is None else stream
+        rows32 = D.rows_narrow(csc.row_idx, stream=producer)
+        ready = producer.record_event()
+        self.copy.wait_event(ready)
+        with torch.cuda.stream(self.copy):
+            slot.rows32[:nnz].copy_(rows32, non_blocking=True)
+            rows_landed = self.copy.record_event()
+            slot.vals[:nnz].copy_(csc.vals, non_blocking=True)
+            slot.col_ptr.copy_(csc.col_ptr, non_blocking=True)
+            done = self.copy.record_event()
+            for t in (rows32, csc.row_idx, csc.vals, csc.col_ptr):
+                t.record_stream(self.copy)  # keep the device blocks alive until the copies ran
+        dim, threads = csc.dim, self.threads
+
+        def finish() -> LowerCscMatrix:
+            rows_landed.synchronize()
+            N.check(N.lib().hx_rows_widen(slot.rows32.data_ptr(), slot.row_idx.ctypes.data, nnz, threads),
+                    "hx_rows_widen")
+            done.synchronize()
+            return LowerCscMatrix(col_ptr=slot.col_ptr.numpy(), row_idx=slot.row_idx[:nnz],
+                                  vals=slot.vals.numpy()[:nnz], dim=dim)
+
+        slot.pending = self.pool.submit(finish)
+        return slot.pending
+
+    def close(self) -> None:
+        for s in self.slots:
+            if s.pending is not None:
+                s.pending.result()
+        self.pool.shutdown()

@@ -73,3 +73,16 @@ def test_product_path_fails_loudly_without_a_gpu():
 
     with pytest.raises(hx.NativeLibraryError):
         hx.stiffness_batch(np.zeros((1, 8, 3)), np.ones(1))
+
+
+def test_rows_widen_host_threads():
+    """hx_rows_widen (host code): int32 -> int64 sign extension, any thread count, empty input."""
+    import numpy as np
+
+    a = np.concatenate([np.array([0, -1, 2**31 - 1, -2**31], np.int32),
+                        np.random.default_rng(0).integers(-2**31, 2**31, 3_000_001, dtype=np.int64).astype(np.int32)])
+    for threads in (1, 3, 0):
+        b = np.full(a.size, 7, np.int64)
+        N.check(N.lib().hx_rows_widen(a.ctypes.data, b.ctypes.data, a.size, threads), "widen")
+        assert np.array_equal(b, a.astype(np.int64))
+    N.check(N.lib().hx_rows_widen(None, None, 0, 0), "widen empty")
