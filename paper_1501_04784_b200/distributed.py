@@ -370,45 +370,56 @@ class ShardedBuild:
         return acc
 
     def measure_e2e(self, steps, barrier):
-        """Host shard in (pinned) -> build -> CSC block out (pinned), max over ranks."""
+        """Host shard in (pinned) -> build -> host CSC block (reference dtypes), pipelined like the
+        single-GPU e2e (transfer.CscHostTransfer: int32 rows over PCIe, widened on the host while
+        the next step builds); host clock per rank, max over ranks."""
+        import time
+
         import torch.distributed as dist
+
+        from .transfer import CscHostTransfer
 
         D = self.ops.D
         h = [t.cpu().pin_memory() for t in (self.dm.coords, self.dm.conn, self.dm.coeff)]
         self.step()
         nnz = int(self.last.row_idx.shape[0])
-        o = [torch.empty(self.c_hi - self.c_lo + 1, dtype=torch.int64, pin_memory=True),
-             torch.empty(nnz, dtype=torch.int64, pin_memory=True), torch.empty(nnz, dtype=torch.float64, pin_memory=True)]
         dev = self.ops.device
         keep = self.dm
+        ncols = self.c_hi - self.c_lo
+        xfer = CscHostTransfer(ncols, nnz, depth=2, device=dev)
+        futures = []
 
         def one():
             self.dm = D.DeviceMesh(*(t.to(dev, non_blocking=True) for t in h))
             r = self.step()
-            o[0].copy_(r.col_ptr, non_blocking=True)
-            o[1].copy_(r.row_idx, non_blocking=True)
-            o[2].copy_(r.vals, non_blocking=True)
+            futures.append(xfer.submit(D.DeviceCsc(r.col_ptr, r.row_idx, r.vals, ncols, self.c_lo)))
+
+        def drain():
+            for f in futures:
+                f.result()
+            futures.clear()
+            torch.cuda.synchronize()
 
         one()
-        torch.cuda.synchronize()
+        drain()
         barrier()
-        start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        start.record()
+        t0 = time.perf_counter()
         for _ in range(steps):
             one()
-        stop.record()
-        torch.cuda.synchronize()
-        ms = torch.tensor([start.elapsed_time(stop) / steps], dtype=torch.float64, device=dev)
+        drain()
+        ms = torch.tensor([(time.perf_counter() - t0) * 1e3 / steps], dtype=torch.float64, device=dev)
+        xfer.close()
         all_reduce(ms, op=dist.ReduceOp.MAX)
         self.dm = keep
         h2d = sum(t.numel() * t.element_size() for t in h)
-        d2h = sum(t.numel() * t.element_size() for t in o)
+        d2h = xfer.bytes_per_transfer(nnz)
         tot = torch.tensor([h2d, d2h], dtype=torch.int64, device=dev)
         all_reduce(tot)
         return {"value": self.n_el / (float(ms.item()) / 1e3), "unit": "elements/s",
                 "h2d_bytes_per_step": int(tot[0]), "d2h_bytes_per_step": int(tot[1]),
                 "ms_per_step": float(ms.item()), "steps": steps,
-                "api": "per-rank shard (pinned host -> HBM) + ShardedBuild.step + CSC block -> pinned host"}
+                "pipelined": "step i's D2H (+ host widening) overlaps step i+1's H2D + build",
+                "api": "per-rank shard (pinned host -> HBM) + ShardedBuild.step + transfer.CscHostTransfer -> host CSC block"}
 
 
 # ------------------------------------------------------------------------------------------
