@@ -322,6 +322,49 @@ __device__ __forceinline__ int column_pattern(const SegTable &T, bool active, in
 #endif
 constexpr int SORT_SLOTS = 64;  // <= 8 elements x 7 other nodes = 56 contributions per column
 
+// Batcher's odd-even merge sort on N register-resident keys, ascending (N = 16/32/64: 63/191/543
+// compare-exchanges against the bitonic network's 80/240/672).  HX_PATTERN_NET: 1 = odd-even
+// merge, 0 = bitonic.
+#ifndef HX_PATTERN_NET
+#define HX_PATTERN_NET 1
+#endif
+template <int N>
+struct OddEvenPairs {  // comparator list of the network, built at compile time
+    static constexpr int count() {
+        int c = 0;
+        for (int p = 1; p < N; p <<= 1)
+            for (int k = p; k >= 1; k >>= 1)
+                for (int j = k % p; j + k < N; j += 2 * k)
+                    for (int i = 0; i < k && i + j + k < N; ++i)
+                        if ((i + j) / (2 * p) == (i + j + k) / (2 * p)) ++c;
+        return c;
+    }
+    int lo[count()], hi[count()];
+    constexpr OddEvenPairs() : lo(), hi() {
+        int c = 0;
+        for (int p = 1; p < N; p <<= 1)
+            for (int k = p; k >= 1; k >>= 1)
+                for (int j = k % p; j + k < N; j += 2 * k)
+                    for (int i = 0; i < k && i + j + k < N; ++i)
+                        if ((i + j) / (2 * p) == (i + j + k) / (2 * p)) {
+                            lo[c] = i + j;
+                            hi[c] = i + j + k;
+                            ++c;
+                        }
+    }
+};
+
+template <int N, typename K>
+__device__ __forceinline__ void oddeven_merge_sort(K (&v)[N]) {
+    constexpr OddEvenPairs<N> P{};
+#pragma unroll
+    for (int c = 0; c < OddEvenPairs<N>::count(); ++c) {
+        const K a = v[P.lo[c]], b = v[P.hi[c]];
+        v[P.lo[c]] = min(a, b);
+        v[P.hi[c]] = max(a, b);
+    }
+}
+
 // Sort the first n (<= N) contribution keys of L in place and, while they are in registers, count
 // the distinct rows (key >> 6) and check that no row has more than MAX_OFFDIAG_CONTRIB
 // contributions (sorted: a run of 5 has v[q] and v[q - 4] in the same row).
@@ -330,7 +373,8 @@ __device__ __forceinline__ void sort_count(K *L, int n, int &rows, bool &ok) {
     K v[N];
 #pragma unroll
     for (int q = 0; q < N; ++q) v[q] = q < n ? L[q * COL_BLOCK] : (K)~(K)0;
-    bitonic_sort<N, K>(v);
+    if (HX_PATTERN_NET) oddeven_merge_sort<N, K>(v);
+    else bitonic_sort<N, K>(v);
     rows = 0;
     ok = true;
 #pragma unroll
