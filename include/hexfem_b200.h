@@ -237,6 +237,17 @@ int hx_generate_cube_mesh(int64_t nx, int64_t ny, int64_t nz, double h, double c
  * widen:  row_idx[i] = rows32[i] on the host with `threads` worker threads (<= 0: all), giving back
  *         the reference's int64 row_idx (assemble.py:51-62).  Host code. */
 int hx_rows_narrow(const int64_t *row_idx, int32_t *rows32, int64_t n, void *stream);
+/* peek: up to HX_PEEK_MAX 4- or 8-byte device words -> host_dst[i] (int64; 4-byte words sign-
+ * extended) written by a kernel into MAPPED pinned host memory (cudaHostAlloc / pinned torch
+ * tensors), so the read does not queue behind bulk copies on the copy engines; the caller
+ * synchronises the stream before reading host_dst. */
+#define HX_PEEK_MAX 8
+typedef struct hx_peek_args {
+    const void *src[HX_PEEK_MAX];
+    int32_t bytes[HX_PEEK_MAX];
+    int32_t n;
+} hx_peek_args;
+int hx_peek(const hx_peek_args *args, int64_t *host_dst, void *stream);
 int hx_rows_widen(const int32_t *rows32, int64_t *row_idx, int64_t n, int32_t threads);
 
 /* ---- Matrix Market export (sparseio.py:73-87), host code -----------------------------------------

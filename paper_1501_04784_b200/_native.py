@@ -37,8 +37,15 @@ EXPORTED = (
     "hx_triplet_csc_workspace_bytes", "hx_triplet_csc_symbolic", "hx_triplet_csc_numeric",
     "hx_halo_workspace_bytes", "hx_halo_count", "hx_halo_pack",
     "hx_block_select_workspace_bytes", "hx_block_select", "hx_block_gather",
-    "hx_halo_send", "hx_mm_write", "hx_mm_read", "hx_generate_cube_mesh", "hx_rows_narrow", "hx_rows_widen",
+    "hx_halo_send", "hx_mm_write", "hx_mm_read", "hx_generate_cube_mesh", "hx_rows_narrow", "hx_rows_widen", "hx_peek",
 )
+
+
+PEEK_MAX = 8
+
+
+class HxPeekArgs(ctypes.Structure):
+    _fields_ = [("src", ctypes.c_void_p * PEEK_MAX), ("bytes", ctypes.c_int32 * PEEK_MAX), ("n", ctypes.c_int32)]
 
 
 class HxFailInfo(ctypes.Structure):
@@ -94,6 +101,7 @@ def lib():
         "hx_mm_write": ([P, P, P, I64, ctypes.c_char_p, I32], ctypes.c_int),
         "hx_rows_narrow": ([P, P, I64, P], ctypes.c_int),
         "hx_rows_widen": ([P, P, I64, I32], ctypes.c_int),
+        "hx_peek": ([P, P, P], ctypes.c_int),
         "hx_mm_read": ([ctypes.c_char_p, P, P, P, P, P, P], ctypes.c_int),
         "hx_generate_cube_mesh": ([I64, I64, I64, ctypes.c_double, ctypes.c_double, P, P, P, P], ctypes.c_int),
         "hx_block_select_workspace_bytes": ([I64], I64),

@@ -8,6 +8,7 @@
 // while the next build's transfers run.  12 bytes per entry instead of 16; values and col_ptr cross
 // unchanged.
 #include <algorithm>
+#include <atomic>
 #include <thread>
 #include <vector>
 
@@ -30,9 +31,38 @@ __global__ void rows_narrow_kernel(const int64_t *__restrict__ src, int32_t *__r
         dst[i] = (int32_t)src[i];
 }
 
+// Small device words -> mapped pinned host memory, written by a kernel: the host's status / nnz /
+// fail-record reads of a build then do not queue behind a multi-gigabyte copy of the previous
+// build's result on the copy engine (a cudaMemcpy of 16 bytes would wait ~200 ms there).
+__global__ void peek_kernel(hx_peek_args a, int64_t *__restrict__ host) {
+    const int i = threadIdx.x;
+    if (i >= a.n) return;
+    const unsigned char *src = static_cast<const unsigned char *>(a.src[i]);
+    int64_t v = 0;
+    if (a.bytes[i] == 4) v = *reinterpret_cast<const int32_t *>(src);  // sign-extended
+    else v = *reinterpret_cast<const int64_t *>(src);                   // raw 8 bytes
+    host[i] = v;
+}
+
 }  // namespace hx
 
 using namespace hx;
+
+extern "C" int hx_peek(const hx_peek_args *args, int64_t *host_dst, void *stream) {
+    if (args == nullptr || host_dst == nullptr || args->n < 0 || args->n > HX_PEEK_MAX) {
+        set_last_error("hx_peek: bad arguments");
+        return HX_ERR_VALUE;
+    }
+    for (int i = 0; i < args->n; ++i)
+        if (args->src[i] == nullptr || (args->bytes[i] != 4 && args->bytes[i] != 8)) {
+            set_last_error("hx_peek: word %d must be a 4- or 8-byte device word", i);
+            return HX_ERR_VALUE;
+        }
+    if (args->n == 0) return HX_OK;
+    peek_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(*args, host_dst);
+    HX_CHECK_LAUNCH("peek_kernel");
+    return HX_OK;
+}
 
 extern "C" int hx_rows_narrow(const int64_t *row_idx, int32_t *rows32, int64_t n, void *stream) {
     if (n < 0 || (n > 0 && (row_idx == nullptr || rows32 == nullptr))) {
@@ -52,20 +82,23 @@ extern "C" int hx_rows_widen(const int32_t *rows32, int64_t *row_idx, int64_t n,
         set_last_error("hx_rows_widen: bad arguments");
         return HX_ERR_VALUE;
     }
+    // chunks of 2^21 entries taken from a shared counter: a core that is busy elsewhere (the
+    // caller's stream synchronisation spins on one) delays only the chunks it holds
+    constexpr int64_t CHUNK = int64_t(1) << 21;
+    const int64_t chunks = (n + CHUNK - 1) / CHUNK;
     const int nt = (int)std::max<int64_t>(1, std::min<int64_t>(threads > 0 ? threads : (int)std::thread::hardware_concurrency(),
-                                                              n / (1 << 20) + 1));
-    auto work = [&](int t) {
-        const int64_t lo = n * t / nt, hi = n * (t + 1) / nt;
-        for (int64_t i = lo; i < hi; ++i) row_idx[i] = rows32[i];
+                                                              chunks));
+    std::atomic<int64_t> next{0};
+    auto work = [&]() {
+        for (int64_t c = next.fetch_add(1); c < chunks; c = next.fetch_add(1)) {
+            const int64_t lo = c * CHUNK, hi = std::min(n, lo + CHUNK);
+            for (int64_t i = lo; i < hi; ++i) row_idx[i] = rows32[i];
+        }
     };
-    if (nt == 1) {
-        work(0);
-        return HX_OK;
-    }
     std::vector<std::thread> pool;
     pool.reserve(nt - 1);
-    for (int t = 1; t < nt; ++t) pool.emplace_back(work, t);
-    work(0);
+    for (int t = 1; t < nt; ++t) pool.emplace_back(work);
+    work();
     for (auto &th : pool) th.join();
     return HX_OK;
 }

@@ -8,6 +8,8 @@ integrate.py / assemble.py / pipeline.py is built on these functions.
 from __future__ import annotations
 
 import ctypes
+import os
+import threading
 from dataclasses import dataclass
 
 import numpy as np
@@ -111,9 +113,43 @@ def new_fail_record(device) -> torch.Tensor:
     return torch.empty(_FAIL_WORDS, dtype=torch.int64, device=device)
 
 
+_PEEK = {}
+_PEEK_LOCK = threading.Lock()
+
+
+def peek(*words: torch.Tensor, stream=None) -> list:
+    """Synchronising read of up to 8 small device words (one-element int32 / int64 tensors; int32
+    comes back sign-extended) through hx_peek: a kernel writes them into mapped pinned host memory,
+    so the read does not wait behind bulk copies queued on the copy engines (the previous build's
+    result streaming to the host).  Synchronises ``stream`` (default: the current stream)."""
+    if not 0 < len(words) <= N.PEEK_MAX:
+        raise ValueError("peek reads 1..8 words")
+    if os.environ.get("HX_PEEK", "1") == "0":  # plain copies (they queue on the copy engines)
+        return [int(w.reshape(()).to(torch.int64).item()) for w in words]
+    dev = words[0].device
+    s = torch.cuda.current_stream(dev) if stream is None else stream
+    args = N.HxPeekArgs()
+    args.n = len(words)
+    for i, w in enumerate(words):
+        if w.device != dev or w.numel() != 1 or w.element_size() not in (4, 8):
+            raise ValueError("peek words must be one-element 4- or 8-byte tensors on one device")
+        args.src[i] = w.data_ptr()
+        args.bytes[i] = w.element_size()
+    with _PEEK_LOCK:
+        buf = _PEEK.get(dev.index)
+        if buf is None:
+            buf = _PEEK[dev.index] = torch.zeros(N.PEEK_MAX, dtype=torch.int64, pin_memory=True)
+        N.check(N.lib().hx_peek(ctypes.byref(args), ctypes.c_void_p(buf.data_ptr()), ctypes.c_void_p(s.cuda_stream)),
+                "hx_peek")
+        s.synchronize()
+        return [int(v) for v in buf.numpy()[:len(words)]]
+
+
 def raise_if_failed(fail: torch.Tensor, element_offset: int = 0) -> None:
     """Synchronising read of an hx_fail_info record; raises DegenerateElementError
     (element.py:237-244) for the lowest failing element."""
+    if peek(fail[0:1])[0] < 0:
+        return
     host = fail.cpu().numpy()
     element = int(host[0])
     if element < 0:
@@ -278,7 +314,7 @@ def numbering_is_local(conn: torch.Tensor, n_nodes: int, sample: int = 4096) -> 
     idx = torch.arange(k, dtype=torch.int64, device=conn.device) * (n - 1) // max(k - 1, 1)
     rows = conn[idx]
     span = (rows.max(dim=1).values - rows.min(dim=1).values).double().mean()
-    return bool(span.item() < n_nodes / 64)
+    return bool(peek((span < n_nodes / 64).to(torch.int32).reshape(1))[0])
 
 
 def _order_flags(order, conn, n_nodes) -> int:
@@ -335,8 +371,7 @@ def mesh_csc(parts, n_nodes: int, col_lo: int = 0, col_hi: int | None = None, st
         N.check(N.lib().hx_mesh_csc_build(segs, len(parts), n_nodes, col_lo, col_hi, _ptr(col_ptr), _ptr(row_buf),
                                           _ptr(val_buf), capacity, _ptr(ws), ws_bytes, _ptr(status), flags, sh),
                 "hx_mesh_csc_build")
-        head = torch.stack([status.to(torch.int64)[0], col_ptr[-1]]).cpu()  # one sync: status + nnz
-        st, nnz = int(head[0]), int(head[1])
+        st, nnz = peek(status[0:1], col_ptr[-1:], stream=stream)  # one sync: status + nnz
         _status_error(st)
         flags &= ~N.CSC_ADJACENCY_READY  # a retry recomputes the adjacency in a fresh workspace
         if st & N.ST_SLOT_COLLISION:
@@ -410,8 +445,7 @@ def plan_assembly(dm: "DeviceMesh", order: str | None = None, stream=None):
     ws_bytes, capacity = None, None
     while True:
         plan = mesh_plan_async(dm.conn, dm.n_nodes, stream=stream, order=order, ws_bytes=ws_bytes, capacity=capacity)
-        head = torch.stack([plan.status.to(torch.int64)[0], plan.col_ptr[-1]]).cpu()
-        st, nnz = int(head[0]), int(head[1])
+        st, nnz = peek(plan.status[0:1], plan.col_ptr[-1:], stream=stream)
         _status_error(st)
         if st & N.ST_SCRATCH and not st & (N.ST_FASTPATH_LIMITS & ~N.ST_SCRATCH):
             ws_bytes = N.lib().hx_mesh_csc_workspace_bytes(dm.n_el, dm.n_nodes) + 8 * nnz
@@ -437,8 +471,7 @@ def mesh_emit(plan: MeshPlan, ke: torch.Tensor, stream=None) -> DeviceCsc:
                                      stream_handle(stream)), "hx_mesh_csc_emit")
     if plan.nnz >= 0:
         return DeviceCsc(plan.col_ptr, plan.row_buf[:plan.nnz], plan.val_buf[:plan.nnz], plan.n_nodes, 0, "mesh")
-    head = torch.stack([plan.status.to(torch.int64)[0], plan.col_ptr[-1]]).cpu()
-    st, nnz = int(head[0]), int(head[1])
+    st, nnz = peek(plan.status[0:1], plan.col_ptr[-1:], stream=stream)
     _status_error(st)
     if st & N.ST_FASTPATH_LIMITS or nnz > plan.capacity:
         order = "element" if plan.flags & N.CSC_ORDER_BY_ELEMENT else "column"
@@ -513,8 +546,7 @@ def triplet_csc(rows: torch.Tensor, cols: torch.Tensor, vals: torch.Tensor, dim:
     sh = stream_handle(stream)
     N.check(N.lib().hx_triplet_csc_symbolic(_ptr(rows), _ptr(cols), n, dim, _ptr(col_ptr), _ptr(row_buf),
                                             _ptr(ws), ws_bytes, _ptr(status), sh), "hx_triplet_csc_symbolic")
-    head = torch.stack([status.to(torch.int64)[0], col_ptr[-1]]).cpu()
-    st, nnz = int(head[0]), int(head[1])
+    st, nnz = peek(status[0:1], col_ptr[-1:], stream=stream)
     _status_error(st)
     out = torch.empty(nnz, dtype=torch.float64, device=dev)
     N.check(N.lib().hx_triplet_csc_numeric(_ptr(vals), n, dim, _ptr(col_ptr), _ptr(out), _ptr(ws), sh),

@@ -16,6 +16,7 @@ is reused ``depth`` submissions later.
 from __future__ import annotations
 
 import os
+import time
 from concurrent.futures import Future, ThreadPoolExecutor
 
 import numpy as np
@@ -55,11 +56,14 @@ class CscHostTransfer:
             raise ValueError("depth must be at least 1")
         self.dev = D.require_device(device)
         self.n_cols, self.capacity = int(n_cols), int(nnz_capacity)
-        self.threads = host_threads() if threads is None else int(threads)
+        if threads is None:  # half the cores: the widening shares host memory bandwidth with the DMA
+            threads = int(os.environ.get("HX_WIDEN_THREADS", "0")) or max(1, host_threads() // 2)
+        self.threads = int(threads)
         self.slots = [_Slot(self.n_cols, self.capacity) for _ in range(depth)]
         self.copy = torch.cuda.Stream(device=self.dev)
         self.pool = ThreadPoolExecutor(max_workers=depth)
         self.k = 0
+        self.trace = [] if os.environ.get("HX_TRACE_TRANSFER") else None
 
     def bytes_per_transfer(self, nnz: int) -> int:
         """PCIe bytes of one transfer: col_ptr int64 + row indices int32 + values float64."""
@@ -78,20 +82,28 @@ class CscHostTransfer:
         ready = producer.record_event()
         self.copy.wait_event(ready)
         with torch.cuda.stream(self.copy):
+            started = self.copy.record_event(torch.cuda.Event(enable_timing=self.trace is not None))
             slot.rows32[:nnz].copy_(rows32, non_blocking=True)
-            rows_landed = self.copy.record_event()
+            rows_landed = self.copy.record_event(torch.cuda.Event(enable_timing=self.trace is not None))
             slot.vals[:nnz].copy_(csc.vals, non_blocking=True)
             slot.col_ptr.copy_(csc.col_ptr, non_blocking=True)
-            done = self.copy.record_event()
+            done = self.copy.record_event(torch.cuda.Event(enable_timing=self.trace is not None))
             for t in (rows32, csc.row_idx, csc.vals, csc.col_ptr):
                 t.record_stream(self.copy)  # keep the device blocks alive until the copies ran
         dim, threads = csc.dim, self.threads
 
+        trace, k = self.trace, self.k - 1
+
         def finish() -> LowerCscMatrix:
             rows_landed.synchronize()
+            t0 = time.perf_counter()
             N.check(N.lib().hx_rows_widen(slot.rows32.data_ptr(), slot.row_idx.ctypes.data, nnz, threads),
                     "hx_rows_widen")
+            t1 = time.perf_counter()
             done.synchronize()
+            if trace is not None:  # (step, D2H ms, widen ms, rows-landed -> widen start ms)
+                trace.append((k, started.elapsed_time(done), (t1 - t0) * 1e3, (t0 - time.perf_counter()) * 1e3
+                              + started.elapsed_time(done) - started.elapsed_time(rows_landed)))
             return LowerCscMatrix(col_ptr=slot.col_ptr.numpy(), row_idx=slot.row_idx[:nnz],
                                   vals=slot.vals.numpy()[:nnz], dim=dim)
 
