@@ -753,3 +753,18 @@ def test_compact_host_transfer_matches_device_csc():
     ri = builds[0].csc.row_idx
     assert np.array_equal(D.rows_narrow(ri[1:].contiguous()).cpu().numpy(), ri[1:].cpu().numpy())
     assert np.array_equal(D.rows_narrow(ri[3:]).cpu().numpy(), ri[3:].cpu().numpy())
+
+
+def test_peek_reads_device_words():
+    """hx_peek: int32 words come back sign-extended, int64 words exact, from any stream."""
+    dev = torch.device("cuda")
+    a = torch.tensor([-7], dtype=torch.int32, device=dev)
+    b = torch.tensor([2**40 + 3], dtype=torch.int64, device=dev)
+    c = torch.tensor([2**31 - 1], dtype=torch.int32, device=dev)
+    assert D.peek(a, b, c) == [-7, 2**40 + 3, 2**31 - 1]
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        d = torch.full((1,), -(2**62), dtype=torch.int64, device=dev)
+        assert D.peek(d, stream=s) == [-(2**62)]
+    with pytest.raises(ValueError):
+        D.peek(torch.zeros(2, dtype=torch.int64, device=dev))
