@@ -109,6 +109,12 @@ def build_device(dm: D.DeviceMesh, mode: str = "exact", with_index: bool = True,
                  plan: D.MeshPlan | None = None) -> DeviceBuild:
     """KE (+ fused iK/jK) for every element, then the lower CSC, all in HBM.
 
+    Cold build (no ``plan``, no ``overlap``): the integration kernel also records the node adjacency
+    that the assembly's symbolic pass starts from (fixed slots, ``device.new_assembly_prep`` /
+    ``hx_integrate_mesh_adjacency``), so the assembly runs pattern + scan + emit only; meshes whose
+    elements hold a node at the same local index fall back to the atomic adjacency pass inside
+    ``mesh_csc`` (detected on the device).  ``HX_FUSED_ADJACENCY=0`` disables the fusion.
+
     The symbolic assembly reads only the connectivity, so with ``overlap`` it runs on a side
     stream concurrently with the FP64-bound integration kernel and the emit pass (row indices +
     values, which needs KE) follows on the main stream.  Measured neutral to -1% on B200 (the
