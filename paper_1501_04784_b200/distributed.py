@@ -377,7 +377,7 @@ class ShardedBuild:
 
         import torch.distributed as dist
 
-        from .transfer import CscHostTransfer
+        from .transfer import CscHostTransfer, host_threads
 
         D = self.ops.D
         h = [t.cpu().pin_memory() for t in (self.dm.coords, self.dm.conn, self.dm.coeff)]
@@ -386,7 +386,9 @@ class ShardedBuild:
         dev = self.ops.device
         keep = self.dm
         ncols = self.c_hi - self.c_lo
-        xfer = CscHostTransfer(ncols, nnz, depth=2, device=dev)
+        # the ranks of one node share its cores (and host memory bandwidth) for the widening
+        xfer = CscHostTransfer(ncols, nnz, depth=2, device=dev,
+                               threads=max(1, host_threads() // (2 * max(1, self.world))))
         futures = []
 
         def one():
