@@ -434,8 +434,9 @@ def measure_kernels(args, rank, world, runner, dm):
     acc[f"ke_{other}_mode_ms"] = sum(t_other) / len(t_other)
     del ke, rows, cols
     # integrate_mesh_kernel (+ adjacency), fail_resolve, pattern, slot check, CUB scan (init + scan),
-    # emit; element-ordered assembly adds first_element + the CUB pair sort
-    acc["launches_per_step"] = 7
+    # emit, two hx_peek reads (status/nnz, fail record); element-ordered assembly adds
+    # first_element + the CUB pair sort (profiles/r01f_launches_bench_c4.txt)
+    acc["launches_per_step"] = 9
     return acc
 
 
