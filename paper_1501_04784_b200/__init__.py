@@ -62,5 +62,6 @@ from .pipeline import (
     run_build,
     triplet_memory,
 )
+from .transfer import CscHostTransfer
 
 __version__ = "0.1.0"
