@@ -768,3 +768,16 @@ def test_peek_reads_device_words():
         assert D.peek(d, stream=s) == [-(2**62)]
     with pytest.raises(ValueError):
         D.peek(torch.zeros(2, dtype=torch.int64, device=dev))
+
+
+def test_compact_host_transfer_empty_block():
+    """A CSC block with no entries (a mesh without elements) crosses as col_ptr only."""
+    from paper_1501_04784_b200.transfer import CscHostTransfer
+
+    mesh = Mesh(np.zeros((5, 3)), np.zeros((0, 8), np.int32), np.zeros(0))
+    b = build_device(D.DeviceMesh.from_host(mesh))
+    xfer = CscHostTransfer(mesh.n_nodes, 0, depth=1)
+    got = xfer.submit(b.csc).result()
+    xfer.close()
+    assert got.row_idx.shape == (0,) and got.vals.shape == (0,) and got.row_idx.dtype == np.int64
+    assert np.array_equal(got.col_ptr, np.zeros(6, np.int64))
