@@ -167,11 +167,11 @@ constexpr int T_EL_STRIDE = 88;
 // five entries as independent chains after a single __syncwarp instead of five store/sync/reduce
 // passes with one serial 8-add chain each.  The product table P aliases the buffer (it is dead once
 // J is formed; a __syncwarp separates the last P read from the first contribution store).
-// Measured: -0.5% with 4 x 128-thread blocks per SM; with one-warp blocks x 16 (the default) the
-// five-pass form is 0.6% faster (its 5.4 KB per warp leave ~140 KB of L1 for the coordinate
-// gathers instead of ~33 KB), so the default is 0.
+// Measured: exact mode -0.5% with 4 x 128-thread blocks per SM and +0.6% with one-warp blocks x 16
+// (the 12 KB per warp take L1 space from the coordinate gathers); fast mode -7% either way -- so the
+// default is 1.
 #ifndef HX_KE_FULL_T
-#define HX_KE_FULL_T 0
+#define HX_KE_FULL_T 1
 #endif
 constexpr int TF_EL_STRIDE = 376;
 
