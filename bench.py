@@ -7,8 +7,9 @@ One step = the full hot path over the whole mesh: KE (36 packed f64 per element)
 (36+36 i32 per element), node-adjacency symbolic CSC, deterministic column numeric CSC.  `value`
 is device throughput with the mesh resident in HBM; `e2e` is the same build through the public
 host API with pinned host input/output buffers, copies inside the timed region.  N>1 ranks
-(torchrun) shard elements and column blocks and exchange element halos with one NCCL all-to-all
-(paper_1501_04784_b200.distributed).
+(torchrun) shard elements and nnz-balanced column blocks and exchange compact element records with
+one NCCL all-to-all (paper_1501_04784_b200.distributed); the line carries "parity": "bitwise" when
+the summed block digests equal the one-GPU build of the same mesh (rank 0 builds it).
 """
 
 from __future__ import annotations
@@ -209,6 +210,63 @@ def run_reference(args):
 # ------------------------------------------------------------------------------------------
 # GPU arm
 # ------------------------------------------------------------------------------------------
+def exchange_kind() -> str:
+    return os.environ.get("HX_EXCHANGE", "nccl")
+
+
+def digest_hex(d) -> str:
+    return "".join(f"{int(x) & 0xFFFFFFFFFFFFFFFF:016x}" for x in d)
+
+
+def single_gpu_digest(mesh, mode):
+    """(col_ptr, row_idx, vals) digests of the one-GPU build of ``mesh`` (hx_digest)."""
+    import torch
+
+    from paper_1501_04784_b200 import device as D
+    from paper_1501_04784_b200.distributed import CudaOps
+    from paper_1501_04784_b200.pipeline import build_device
+
+    ops = CudaOps(mode=mode)
+    b = build_device(D.DeviceMesh.from_host(mesh), mode=mode)
+    d = [ops.digest(b.csc.col_ptr, 0), ops.digest(b.csc.row_idx, 0), ops.digest(b.csc.vals, 0)]
+    out = [int(x.item()) for x in d]
+    del b
+    torch.cuda.empty_cache()
+    return out
+
+
+def sharded_parity(runner, mesh, mode, rank, world, local):
+    """Bitwise check of the sharded build inside the bench: the ranks' block digests (position-keyed,
+    additive) are summed and rank 0 compares them with the one-GPU build of the same mesh on its own
+    device.  Also reports the exchange volume and the column-block nnz balance."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1501_04784_b200.distributed import all_reduce, barrier
+
+    runner.global_nnz()
+    dig = all_reduce(runner.block_digest())
+    nnz = torch.tensor([int(runner.last.row_idx.shape[0])], dtype=torch.int64, device="cuda")
+    nnzs = runner.exchange.allgather(nnz)[:, 0]
+    xb = runner.exchange_bytes()
+    sharded = [int(x) for x in dig.cpu().tolist()]
+    out = {"exchange": {**xb, "kind": exchange_kind()},
+           "block_nnz_max_over_mean": float(nnzs.max() / nnzs.mean()),
+           "column_bounds": "nnz-balanced (hx_column_weights histogram, one all-reduce)"}
+    if rank == 0:
+        runner.dm = None
+        runner.last = runner.last_index = None
+        torch.cuda.empty_cache()
+        ref = single_gpu_digest(mesh, mode)
+        out["parity"] = "bitwise" if ref == sharded else "MISMATCH"
+        out["digest"] = digest_hex(sharded)
+        out["parity_note"] = ("sum over ranks of the position-keyed block digests (hx_digest of col_ptr, "
+                              "row_idx, vals) == digest of the one-GPU build of the same mesh on rank 0")
+    barrier(device_index=local)
+    del dist
+    return out
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -241,10 +299,12 @@ def run_ours(args):
     if world > 1:
         from paper_1501_04784_b200 import distributed as X
 
-        # fused pack-and-send into the peers' IPC-mapped receive buffers (default); HX_EXCHANGE=nccl:
-        # pack + NCCL all-to-all
-        exchange = X.P2PExchange() if os.environ.get("HX_EXCHANGE", "p2p") == "p2p" else None
+        # compact records + one NCCL all-to-all (default); HX_EXCHANGE=p2p: fused pack-and-send into
+        # the peers' IPC-mapped receive buffers (verified on one GPU with several processes only)
+        exchange = X.P2PExchange() if exchange_kind() == "p2p" else None
+        t_setup = time.perf_counter()
         runner = X.ShardedBuild(mesh, rank, world, mode=args.mode, exchange=exchange)
+        t_setup = time.perf_counter() - t_setup
         step = runner.step
         n_el_total, n_nodes = mesh.n_el, mesh.n_nodes
     else:
@@ -333,8 +393,15 @@ def run_ours(args):
         e2e = measure_e2e(args, mesh, nnz)
     elif not args.no_e2e and world > 1:
         e2e = runner.measure_e2e(args.steps, barrier)
+    shard_info = None
     if world > 1:
+        runner.step()
+        shard_info = sharded_parity(runner, mesh, args.mode, rank, world, local)
+        shard_info["setup_s"] = round(t_setup, 3)
         del runner
+        torch.cuda.empty_cache()
+    else:
+        digest = single_gpu_digest(mesh, args.mode) if os.environ.get("HX_BENCH_DIGEST", "1") != "0" else None
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -348,8 +415,8 @@ def run_ours(args):
             "config": {"workload": f"{wl}: {WORKLOADS[wl]['desc']}", "n_el": n_el_total, "n_nodes": n_nodes,
                        "nnz": nnz, "integration_mode": args.mode,
                        "l2": "no flush: inputs+outputs per step >> 126 MB L2",
-                       "parallelism": (f"element-range shards + column blocks x{world}, halo exchange: "
-                                       f"{os.environ.get('HX_EXCHANGE', 'p2p')}") if world > 1 else "single GPU",
+                       "parallelism": (f"element-range shards + nnz-balanced column blocks x{world}, compact "
+                                       f"record exchange: {exchange_kind()}") if world > 1 else "single GPU",
                        "mesh_gen_s": round(t_mesh, 2)},
             "roofline": {"bound": "hbm", "achieved": achieved_ke, "peak": peak, "unit": "GB/s",
                          "frac": achieved_ke / peak, "frac_of_spec_8000": achieved_ke / 8000.0, "traffic": load_traffic(wl, KE_KERNEL) if world == 1 else None, "kernel": KE_KERNEL,
@@ -378,6 +445,11 @@ def run_ours(args):
         }
         if warm is not None:
             line["warm_rebuild"] = warm
+        if shard_info is not None:
+            line["sharded"] = shard_info
+            line["parity"] = shard_info.get("parity")
+        elif world == 1 and digest is not None:
+            line["digest"] = digest_hex(digest)
         if e2e is not None:
             line["e2e"] = e2e
         if cpu is not None:

@@ -10,7 +10,7 @@
  *
  * All device buffers are caller-owned (the reference's `out=` convention,
  * integrate.py:93-99); scratch is a caller-provided workspace sized by the *_workspace_bytes
- * queries.  The library allocates nothing.  Arrays of length zero may be passed as NULL
+ * queries.  The library allocates nothing (except hx_ipc_alloc, which exists to allocate).  Arrays of length zero may be passed as NULL
  * (what allocators hand out for empty tensors); zero-size calls are valid no-ops that still
  * write their status / fail words.
  *
@@ -24,7 +24,8 @@
  *   hx_mesh_csc_*                  assemble.py:152-239 DirectAssembler / assemble_direct, and
  *                                  triplet_to_csc (assemble.py:110-140) on mesh triplets
  *   hx_triplet_csc_*               assemble.py:110-149 triplet_to_csc + _check_indices
- *   hx_halo_*                      (new) element-halo exchange of the multi-GPU path
+ *   hx_halo_*, hx_column_weights,  (new) exchange step of the multi-GPU path: nnz-balanced column
+ *   hx_digest, hx_ipc_*            blocks, compact element records, block checksums, IPC buffers
  *   hx_block_*                     (new) column blocks of the out-of-core build (Eq. 10 batching,
  *                                  integrate.py:55-81 / PAPER.md:192-199, beyond one GPU's HBM)
  */
@@ -37,8 +38,10 @@
 extern "C" {
 #endif
 
-#define HX_ABI_VERSION 3  /* 2: flags argument of hx_mesh_csc_symbolic/build, hx_mesh_csc_emit, hx_block_*
-                           * 3: hx_integrate_mesh_adjacency + HX_CSC_ADJACENCY_READY (fused first pass) */
+#define HX_ABI_VERSION 4  /* 2: flags argument of hx_mesh_csc_symbolic/build, hx_mesh_csc_emit, hx_block_*
+                           * 3: hx_integrate_mesh_adjacency + HX_CSC_ADJACENCY_READY (fused first pass)
+                           * 4: compact halo records (hx_halo_count/pack/unpack), hx_column_weights,
+                           *    hx_digest, hx_ipc_*; HX_FAIL_BAD_NODE */
 
 /* Status codes (host return values).  The Python layer maps them onto the reference
  * exception hierarchy (errors.py:4-59). */
@@ -81,10 +84,16 @@ extern "C" {
 #define HX_MODE_FAST 1  /* FMA + restructured algebra: |d| <= 1e-12 * max|row| (documented)  */
 
 /* Lowest failing element of an integration call (DegenerateElementError fields,
- * errors.py:21-40).  element = -1 when every element is valid.  Device memory. */
+ * errors.py:21-40).  element = -1 when every element is valid.  Device memory.
+ * gauss_point = HX_FAIL_BAD_NODE: the element references a node id outside [0, n_nodes) (the
+ * reference's staging gather raises IndexError there, integrate.py:146-149; validate_mesh raises
+ * MeshValidationError, mesh.py:106-110) -- det then holds the offending node id.  Elements with a
+ * bad node id take precedence over degenerate ones (the reference fails at staging, before
+ * computing). */
+#define HX_FAIL_BAD_NODE (-2)
 typedef struct hx_fail_info {
     int64_t element;     /* global element id (element_offset applied, element.py:237-244) */
-    int32_t gauss_point; /* 0..7, r slowest (element.py:116-121)                           */
+    int32_t gauss_point; /* 0..7, r slowest (element.py:116-121); HX_FAIL_BAD_NODE         */
     int32_t reserved;    /* scratch of the integration call (work counter), zeroed by it        */
     double det;          /* det(J) at that point (element.py:276-279)                      */
 } hx_fail_info;
@@ -189,29 +198,53 @@ int hx_triplet_csc_symbolic(const int32_t *rows, const int32_t *cols, int64_t n,
 int hx_triplet_csc_numeric(const double *vals, int64_t n, int64_t dim, const int64_t *col_ptr,
                            double *out_vals, const void *workspace, void *stream);
 
-/* ---- multi-GPU element-halo exchange (element-range shards, column blocks) -----------------
+/* ---- multi-GPU exchange (element-range shards, nnz-balanced column blocks) ---------------------
+ * The sharded build has no reference counterpart (the reference is single-process);
+ * the blocks it produces are the reference's LowerCscMatrix (assemble.py:51-62) cut into column
+ * ranges, bitwise.
+ *
+ * column_weights: hist[b] += nnz estimate (units of 1/8 entry) of the lower-CSC columns in bin
+ *        b = node * n_bins / n_nodes, over the given elements (hex8 pair (i, j) adds 1 << (number of
+ *        differing natural coordinates)).  Summed over ranks (all-reduce) and cut at equal prefix
+ *        sums, it gives nnz-balanced column bounds.  hist (n_bins) u64 device, caller-zeroed.
  * col_bounds: (world+1) int64 device array, rank r owns columns [col_bounds[r], col_bounds[r+1]).
- * count: per_dest (world) int64 device = number of local elements each rank must receive
- *        (elements with a node in that rank's block; per_dest[self] = 0).
- * pack:  records (sum(per_dest), 40) f64 device, destination-major, ascending element order
- *        within a destination; record = 36 packed KE values + 8 int32 node ids (bit-copied), i.e.
- *        directly consumable as an hx_elem_segment with conn_stride 80, ke_stride 40.
- * pack must follow count with the same workspace. */
+ * count: per_dest (world, 2) int64 device <- (records, values) each rank needs from this rank's
+ *        elements: one record per element with a node in that rank's block, carrying the KE
+ *        entries whose column (min of the pair's node ids) the rank owns; per_dest[self] = 0.
+ * pack:  writes the records into dest_ptrs[d] + dest_offsets[d] (int64 words; device arrays of
+ *        world entries -- a send buffer for an all-to-all, or receive buffers in peer memory):
+ *        [ids: 4 words per record = the 8 int32 node ids][values: the owned entries, ascending
+ *        packed index p, as f64 bit patterns], destination-major, ascending element order.  Must
+ *        follow count with the same workspace.
+ * unpack: recv = the chunks of every source in ascending source order; src_desc (world, 3) int64
+ *        device = per source (word offset of its chunk in recv, records, values).  records
+ *        (n_rec, 40) f64 <- 36 KE words (entries this rank does not own are 0) + the 8 ids, i.e.
+ *        an hx_elem_segment with conn_stride 80, ke_stride 40.
+ * digest: *out += sum_i mix(mix(pos0 + i) ^ (word_i + add)) (mod 2^64) over n_words 8-byte words --
+ *        a position-keyed checksum whose sum over the ranks' blocks equals that of the whole array. */
+int hx_column_weights(const int32_t *conn, int64_t n_el, int64_t n_nodes, int64_t n_bins, uint64_t *hist,
+                      void *stream);
 int64_t hx_halo_workspace_bytes(int64_t n_el, int32_t world);
 int hx_halo_count(const int32_t *conn, int64_t n_el, const int64_t *col_bounds, int32_t world, int32_t self,
                   int64_t *per_dest, void *workspace, int64_t workspace_bytes, void *stream);
 int hx_halo_pack(const int32_t *conn, const double *ke, int64_t n_el, const int64_t *col_bounds, int32_t world,
-                 int32_t self, double *records, const void *workspace, void *stream);
-
-/* send: the fused pack-and-send -- the same records as hx_halo_pack, written straight into each
- *       destination d's receive buffer dest_ptrs[d] (device array of world pointers: peer memory
- *       mapped through CUDA IPC, or local buffers) starting at record dest_offsets[d] (device array)
- *       = the number of records lower ranks send to d.  Requires hx_halo_count's workspace.
- *       The caller orders the receivers' reads after every sender's kernel (a stream-ordered
- *       barrier). */
-int hx_halo_send(const int32_t *conn, const double *ke, int64_t n_el, const int64_t *col_bounds, int32_t world,
-                 int32_t self, double *const *dest_ptrs, const int64_t *dest_offsets, const void *workspace,
+                 int32_t self, int64_t *const *dest_ptrs, const int64_t *dest_offsets, const void *workspace,
                  void *stream);
+int64_t hx_halo_unpack_workspace_bytes(int64_t n_rec);
+int hx_halo_unpack(const int64_t *recv, const int64_t *src_desc, int32_t world, int32_t self,
+                   const int64_t *col_bounds, int64_t n_rec, double *records, void *workspace,
+                   int64_t workspace_bytes, void *stream);
+int hx_digest(const void *data, int64_t n_words, int64_t pos0, uint64_t add, uint64_t *out, void *stream);
+
+/* CUDA IPC receive buffers of the fused pack-and-send exchange (the one allocating entry point: an
+ * IPC handle needs its own cudaMalloc base).  alloc: device buffer + its 64-byte handle; open: maps
+ * a handle of ANOTHER process into the current device's context with lazy peer access (NVLink
+ * stores from this device's kernels into the owner's GPU); close / free undo them. */
+#define HX_IPC_HANDLE_BYTES 64
+int hx_ipc_alloc(int64_t bytes, void **ptr, void *handle);
+int hx_ipc_open(const void *handle, void **ptr);
+int hx_ipc_close(void *ptr);
+int hx_ipc_free(void *ptr);
 
 /* ---- column blocks of one GPU (out-of-core build, Eq. 10 beyond HBM) ---------------------------
  * select: ids (n_el capacity) i64 device <- ascending ids of the elements with a node in

@@ -38,6 +38,7 @@ from .errors import (
     MeshFormatError,
     MeshValidationError,
     NativeLibraryError,
+    NodeIndexError,
     StagingError,
 )
 from .integrate import (

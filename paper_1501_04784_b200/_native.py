@@ -35,13 +35,16 @@ EXPORTED = (
     "hx_mesh_csc_workspace_bytes", "hx_mesh_csc_symbolic", "hx_mesh_csc_build", "hx_mesh_csc_numeric",
     "hx_mesh_csc_emit",
     "hx_triplet_csc_workspace_bytes", "hx_triplet_csc_symbolic", "hx_triplet_csc_numeric",
-    "hx_halo_workspace_bytes", "hx_halo_count", "hx_halo_pack",
+    "hx_column_weights", "hx_halo_workspace_bytes", "hx_halo_count", "hx_halo_pack",
+    "hx_halo_unpack_workspace_bytes", "hx_halo_unpack", "hx_digest",
+    "hx_ipc_alloc", "hx_ipc_open", "hx_ipc_close", "hx_ipc_free",
     "hx_block_select_workspace_bytes", "hx_block_select", "hx_block_gather",
-    "hx_halo_send", "hx_mm_write", "hx_mm_read", "hx_generate_cube_mesh", "hx_rows_narrow", "hx_rows_widen", "hx_peek",
+    "hx_mm_write", "hx_mm_read", "hx_generate_cube_mesh", "hx_rows_narrow", "hx_rows_widen", "hx_peek",
 )
 
 
 PEEK_MAX = 8
+IPC_HANDLE_BYTES = 64
 
 
 class HxPeekArgs(ctypes.Structure):
@@ -94,10 +97,17 @@ def lib():
         "hx_triplet_csc_workspace_bytes": ([I64, I64], I64),
         "hx_triplet_csc_symbolic": ([P, P, I64, I64, P, P, P, I64, P, P], ctypes.c_int),
         "hx_triplet_csc_numeric": ([P, I64, I64, P, P, P, P], ctypes.c_int),
+        "hx_column_weights": ([P, I64, I64, I64, P, P], ctypes.c_int),
         "hx_halo_workspace_bytes": ([I64, I32], I64),
         "hx_halo_count": ([P, I64, P, I32, I32, P, P, I64, P], ctypes.c_int),
-        "hx_halo_pack": ([P, P, I64, P, I32, I32, P, P, P], ctypes.c_int),
-        "hx_halo_send": ([P, P, I64, P, I32, I32, P, P, P, P], ctypes.c_int),
+        "hx_halo_pack": ([P, P, I64, P, I32, I32, P, P, P, P], ctypes.c_int),
+        "hx_halo_unpack_workspace_bytes": ([I64], I64),
+        "hx_halo_unpack": ([P, P, I32, I32, P, I64, P, P, I64, P], ctypes.c_int),
+        "hx_digest": ([P, I64, I64, ctypes.c_uint64, P, P], ctypes.c_int),
+        "hx_ipc_alloc": ([I64, ctypes.POINTER(ctypes.c_void_p), P], ctypes.c_int),
+        "hx_ipc_open": ([P, ctypes.POINTER(ctypes.c_void_p)], ctypes.c_int),
+        "hx_ipc_close": ([P], ctypes.c_int),
+        "hx_ipc_free": ([P], ctypes.c_int),
         "hx_mm_write": ([P, P, P, I64, ctypes.c_char_p, I32], ctypes.c_int),
         "hx_rows_narrow": ([P, P, I64, P], ctypes.c_int),
         "hx_rows_widen": ([P, P, I64, I32], ctypes.c_int),

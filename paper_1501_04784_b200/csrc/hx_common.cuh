@@ -10,6 +10,11 @@
 
 namespace hx {
 
+// Fail-record key of an integration call (atomicMin): a degenerate element e is
+// HX_FAIL_DEGENERATE_KEY | e, an element with an out-of-range node id is plain e, so the lowest
+// bad-node element wins over every degenerate one (see hx_fail_info).
+constexpr unsigned long long HX_FAIL_DEGENERATE_KEY = 1ull << 62;
+
 // ---------------------------------------------------------------------------------------
 // Reference element tables (element.py:43-62, 104-135).
 //

@@ -595,8 +595,9 @@ integrate_mesh_kernel(const double *__restrict__ coords, int64_t n_nodes, const 
     int64_t quad2 = quad1 < n_quads ? grab() : n_quads;     // node ids in flight
     int32_t node = node_id(quad), node_next = node_id(quad1);
     double x0 = u0, x1 = u1, x2 = u2, c = 1.0;
-    // out-of-range ids are never dereferenced (the assembly reports them: HX_ST_BAD_INDEX)
-    if (node >= 0 && (!WITH_ADJ || node < n_nodes)) {
+    // node ids outside [0, n_nodes) are never dereferenced: the element is reported through the
+    // fail record (bad-node key, below) and, fused, the assembly status (HX_ST_BAD_INDEX)
+    if (node >= 0 && node < n_nodes) {
         const double *p = coords + 3 * (int64_t)node;
         x0 = __ldg(p); x1 = __ldg(p + 1); x2 = __ldg(p + 2);
         c = __ldg(coeff + lo + quad * GP_EL_PER_WARP + el);
@@ -608,9 +609,11 @@ integrate_mesh_kernel(const double *__restrict__ coords, int64_t n_nodes, const 
                                                                coord_in_range(x2));
         const bool fast_div = ((in_range >> (8 * el)) & 0xffu) == 0xffu;
         // fixed-slot adjacency: (element, local node gp) -> slot gp of its node (fire and forget)
-        if (WITH_ADJ && valid) {
-            if (node < 0 || node >= n_nodes) atomicOr(adj_out.status, HX_ST_BAD_INDEX);
-            else adj_out.adj[8 * (int64_t)node + gp] = (int32_t)(((lo + k) << 3) | gp);
+        if (valid && (node < 0 || node >= n_nodes)) {
+            atomicMin(fail_min, (unsigned long long)(lo + k));  // bad-node key: below every degenerate key
+            if (WITH_ADJ) atomicOr(adj_out.status, HX_ST_BAD_INDEX);
+        } else if (WITH_ADJ && valid) {
+            adj_out.adj[8 * (int64_t)node + gp] = (int32_t)(((lo + k) << 3) | gp);
         }
         __syncwarp();
         publish_node<MODE>(sm, el, gp, node, x0, x1, x2, c);
@@ -619,7 +622,7 @@ integrate_mesh_kernel(const double *__restrict__ coords, int64_t n_nodes, const 
         node = node_next;
         node_next = node_id(quad2);
         x0 = u0; x1 = u1; x2 = u2; c = 1.0;
-        if (node >= 0 && (!WITH_ADJ || node < n_nodes)) {
+        if (node >= 0 && node < n_nodes) {
             const double *p = coords + 3 * (int64_t)node;
             x0 = __ldg(p); x1 = __ldg(p + 1); x2 = __ldg(p + 2);
             c = __ldg(coeff + lo + quad1 * GP_EL_PER_WARP + el);
@@ -630,7 +633,7 @@ integrate_mesh_kernel(const double *__restrict__ coords, int64_t n_nodes, const 
             ok = ke_gauss_point<WITH_INDEX>(sm, el, gp, fast_div, k, valid, ke_out, rows_out, cols_out, s_pi, s_pj);
         else
             ok = ke_gauss_point_fast<WITH_INDEX>(sm, el, gp, k, valid, ke_out, rows_out, cols_out, s_pi, s_pj);
-        if (valid && !ok) atomicMin(fail_min, (unsigned long long)(lo + k));
+        if (valid && !ok) atomicMin(fail_min, HX_FAIL_DEGENERATE_KEY | (unsigned long long)(lo + k));
         quad = quad1;
         quad1 = quad2;
         quad2 = quad3;
@@ -664,12 +667,12 @@ stiffness_batch_kernel(const double *__restrict__ coords, const double *__restri
         ok = ke_gauss_point<false>(sm, el, gp, fast_div, e, valid, out, nullptr, nullptr, nullptr, nullptr);
     else
         ok = ke_gauss_point_fast<false>(sm, el, gp, e, valid, out, nullptr, nullptr, nullptr, nullptr);
-    if (valid && !ok) atomicMin(fail_min, (unsigned long long)e);
+    if (valid && !ok) atomicMin(fail_min, HX_FAIL_DEGENERATE_KEY | (unsigned long long)e);
 }
 
 // Resolve the lowest failing element into the hx_fail_info record (element.py:237-244).
-__global__ void fail_resolve_mesh_kernel(const double *__restrict__ coords, const int32_t *__restrict__ conn,
-                                         const double *__restrict__ coeff, hx_fail_info *fail) {
+__global__ void fail_resolve_mesh_kernel(const double *__restrict__ coords, int64_t n_nodes,
+                                         const int32_t *__restrict__ conn, hx_fail_info *fail) {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
     const unsigned long long key = *reinterpret_cast<unsigned long long *>(fail);
     if (key == ~0ull) {
@@ -678,8 +681,18 @@ __global__ void fail_resolve_mesh_kernel(const double *__restrict__ coords, cons
         fail->det = 0.0;
         return;
     }
-    const int64_t e = (int64_t)key;
     int32_t g[8];
+    if (!(key & HX_FAIL_DEGENERATE_KEY)) {  // lowest element with a node id outside [0, n_nodes)
+        const int64_t e = (int64_t)key;
+        load_conn(conn, e, g);
+        int a = 0;
+        while (a < 7 && g[a] >= 0 && g[a] < n_nodes) ++a;
+        fail->element = e;
+        fail->gauss_point = HX_FAIL_BAD_NODE;
+        fail->det = (double)g[a];  // the offending node id
+        return;
+    }
+    const int64_t e = (int64_t)(key & ~HX_FAIL_DEGENERATE_KEY);
     load_conn(conn, e, g);
     double x[8][3];
     for (int a = 0; a < 8; ++a) load_node(coords, g[a], x[a]);
@@ -695,7 +708,7 @@ __global__ void fail_resolve_batch_kernel(const double *__restrict__ coords, hx_
         fail->det = 0.0;
         return;
     }
-    const int64_t e = (int64_t)key;
+    const int64_t e = (int64_t)(key & ~HX_FAIL_DEGENERATE_KEY);
     double x[8][3];
     for (int a = 0; a < 8; ++a)
         for (int d = 0; d < 3; ++d) x[a][d] = coords[24 * e + 3 * a + d];
@@ -856,7 +869,7 @@ static int integrate_mesh_impl(const double *coords, int64_t n_nodes, const int3
                                            s, coords, n_nodes, conn, coeff, lo, n, ke, rows, cols, fail, adj);
         HX_CHECK_LAUNCH("integrate_mesh_kernel");
     }
-    fail_resolve_mesh_kernel<<<1, 1, 0, s>>>(coords, conn, coeff, fail);
+    fail_resolve_mesh_kernel<<<1, 1, 0, s>>>(coords, n_nodes, conn, fail);
     HX_CHECK_LAUNCH("fail_resolve_mesh_kernel");
     return HX_OK;
 }

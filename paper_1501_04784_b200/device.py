@@ -16,7 +16,7 @@ import numpy as np
 import torch
 
 from . import _native as N
-from .errors import ConfigurationError, DegenerateElementError, MeshValidationError, NativeLibraryError
+from .errors import ConfigurationError, DegenerateElementError, MeshValidationError, NativeLibraryError, NodeIndexError
 
 __all__ = [
     "DeviceMesh", "DeviceCsc", "AssemblyPrep", "new_assembly_prep", "rows_narrow", "require_device", "stream_handle", "integrate_mesh", "stiffness_batch",
@@ -145,18 +145,30 @@ def peek(*words: torch.Tensor, stream=None) -> list:
         return [int(v) for v in buf.numpy()[:len(words)]]
 
 
-def raise_if_failed(fail: torch.Tensor, element_offset: int = 0) -> None:
-    """Synchronising read of an hx_fail_info record; raises DegenerateElementError
-    (element.py:237-244) for the lowest failing element."""
-    if peek(fail[0:1])[0] < 0:
-        return
-    host = fail.cpu().numpy()
+FAIL_BAD_NODE = -2  # hx_fail_info.gauss_point of an element with a node id outside [0, n_nodes)
+
+
+def fail_error(host: np.ndarray, element_offset: int = 0, n_nodes: int | None = None):
+    """The exception an hx_fail_info record (3 int64 words, host) stands for, or None."""
     element = int(host[0])
     if element < 0:
-        return
+        return None
     gp = int(np.int32(host[1] & 0xFFFFFFFF))
     det = float(host[2:3].view(np.float64)[0])
-    raise DegenerateElementError(element_id=element_offset + element, gauss_point=gp, det=det)
+    if gp == FAIL_BAD_NODE:
+        return NodeIndexError(element_id=element_offset + element, node=int(det), n_nodes=n_nodes)
+    return DegenerateElementError(element_id=element_offset + element, gauss_point=gp, det=det)
+
+
+def raise_if_failed(fail: torch.Tensor, element_offset: int = 0, n_nodes: int | None = None) -> None:
+    """Synchronising read of an hx_fail_info record; raises NodeIndexError for the lowest element
+    with an out-of-range node id, else DegenerateElementError (element.py:237-244) for the lowest
+    failing element."""
+    if peek(fail[0:1])[0] < 0:
+        return
+    err = fail_error(fail.cpu().numpy(), element_offset, n_nodes)
+    if err is not None:
+        raise err
 
 
 def _mode_id(mode: str) -> int:
@@ -267,6 +279,9 @@ class DeviceCsc:
     dim: int
     col_lo: int = 0
     path: str = "mesh"
+    # events of asynchronous readers (e.g. a CscHostTransfer copy) that must complete before the
+    # buffers are overwritten -- set when the buffers belong to a reusable MeshPlan
+    readers: list | None = None
 
     @property
     def nnz(self) -> int:
@@ -408,6 +423,7 @@ class MeshPlan:
     capacity: int
     flags: int = 0
     nnz: int = -1  # known once the plan is verified (plan_assembly): emits then need no host sync
+    readers: list = None  # events of pending readers of row_buf / val_buf (see DeviceCsc.readers)
 
 
 def mesh_plan_async(conn: torch.Tensor, n_nodes: int, stream=None, order: str = "auto", ws_bytes: int | None = None,
@@ -465,18 +481,26 @@ def mesh_emit(plan: MeshPlan, ke: torch.Tensor, stream=None) -> DeviceCsc:
     overwritten by the next emit; otherwise one sync checks the status word and nnz and falls back
     to mesh_csc when the plan hit a limit."""
     _check_segment(plan.conn, ke)
+    if plan.readers is None:
+        plan.readers = []
+    s = torch.cuda.current_stream(ke.device) if stream is None else stream
+    for ev in plan.readers:  # a previous result still being read (host transfer): do not overwrite it
+        s.wait_event(ev)
+    plan.readers.clear()
     segs = N.segments([(plan.conn.data_ptr(), ke.data_ptr(), plan.conn.shape[0])])
     N.check(N.lib().hx_mesh_csc_emit(segs, 1, 0, plan.n_nodes, _ptr(plan.col_ptr), _ptr(plan.row_buf),
                                      _ptr(plan.val_buf), plan.capacity, _ptr(plan.ws), _ptr(plan.status),
                                      stream_handle(stream)), "hx_mesh_csc_emit")
     if plan.nnz >= 0:
-        return DeviceCsc(plan.col_ptr, plan.row_buf[:plan.nnz], plan.val_buf[:plan.nnz], plan.n_nodes, 0, "mesh")
+        return DeviceCsc(plan.col_ptr, plan.row_buf[:plan.nnz], plan.val_buf[:plan.nnz], plan.n_nodes, 0, "mesh",
+                         readers=plan.readers)
     st, nnz = peek(plan.status[0:1], plan.col_ptr[-1:], stream=stream)
     _status_error(st)
     if st & N.ST_FASTPATH_LIMITS or nnz > plan.capacity:
         order = "element" if plan.flags & N.CSC_ORDER_BY_ELEMENT else "column"
         return mesh_csc([(plan.conn, ke)], plan.n_nodes, stream=stream, order=order)
-    return DeviceCsc(plan.col_ptr, plan.row_buf[:nnz], plan.val_buf[:nnz], plan.n_nodes, 0, "mesh")
+    return DeviceCsc(plan.col_ptr, plan.row_buf[:nnz], plan.val_buf[:nnz], plan.n_nodes, 0, "mesh",
+                     readers=plan.readers)
 
 
 def rows_narrow(row_idx: torch.Tensor, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:

@@ -1,39 +1,57 @@
-"""Multi-GPU construction: element-range shards, column blocks, one all-to-all of element halos.
+"""Multi-GPU construction: element-range shards, nnz-balanced column blocks, one exchange of
+compact element records.
+
+The reference is single-process; the sharded build produces its LowerCscMatrix
+(assemble.py:51-62) cut into column blocks, bitwise equal to the single-GPU build.
 
 Rank r of G (one process per GPU, torch.distributed over NCCL):
 
 1. integrates its contiguous element range E_r = [n_el*r/G, n_el*(r+1)/G) -- KE + fused iK/jK,
    exactly the single-GPU kernel on a slice of the mesh;
-2. owns the lower-CSC column block C_r = [n_nodes*r/G, n_nodes*(r+1)/G) (a column block of the
-   lower triangle is a row block of K by symmetry).  Column nnz is <= 27 and near-uniform on
-   conforming hex meshes, so an equal node split is an equal nnz split;
-3. sends every owned element that has a node in another rank's block to that rank -- one
-   all-to-all of 320-byte records (36 KE values + 8 node ids), packed destination-major in
-   ascending element order by hx_halo_pack;
-4. assembles its block from the segments [received from lower ranks | own | received from
-   higher ranks], which are in ascending global element order, so every duplicate position is
-   summed in the single-GPU order: the concatenated blocks are bitwise equal to G = 1.
+2. owns the lower-CSC column block C_r = [b_r, b_r+1) (a column block of the lower triangle is a
+   row block of K by symmetry).  The bounds cut a global per-column nnz estimate at equal prefix
+   sums (``hx_column_weights`` on each rank's elements, one all-reduce of a 64K-bin histogram, the
+   same integer cut on every rank): columns are min(node) (assemble.py:86-93), so on a randomly
+   numbered mesh low ids own far more lower-triangle entries than high ids and an equal node split
+   is off by up to 1.8x;
+3. sends every owned element with a node in another rank's block to that rank as a compact record:
+   its 8 node ids + only the KE entries whose column the destination owns (entry (i, j) lands in
+   column min(g_i, g_j), owned by min(owner(g_i), owner(g_j))).  One all-gather carries the G x G
+   (records, values) count matrix and every rank's fail record; one all-to-all (NCCL) moves the
+   records -- or, with ``P2PExchange``, the pack kernel writes them straight into the destinations'
+   receive buffers (CUDA IPC peer memory over NVLink) and a one-word all-reduce orders the reads;
+4. unpacks the received records into 40-word segments and assembles its block from [received from
+   lower ranks | own | received from higher ranks], which are in ascending global element order,
+   so every duplicate position is summed in the single-GPU order: bitwise equal to G = 1.
 
-The global K is the concatenation of the blocks; global col_ptr = block col_ptr + exclusive
-scan of the block nnz (one all-gather of G int64).
+The global K is the concatenation of the blocks; global col_ptr = block col_ptr + exclusive scan of
+the block nnz (one all-gather of G int64).  ``block_digest`` gives position-keyed checksums whose sum
+over the ranks equals the single-GPU build's (the bench's parity check at N > 1).
 
-The collective is behind a small ``Exchange`` interface (torch.distributed for NCCL/gloo, a
-loopback for simulating G ranks in one process) and the per-rank compute behind ``Ops`` (the
-CUDA ops by default), so the host logic is tested with gloo on CPU and the CUDA path with the
-loopback on one GPU.
+The collectives are behind a small exchange interface (torch.distributed for NCCL/gloo; the
+loopback drivers simulate G ranks in one process) and the per-rank compute behind ``Ops`` (the CUDA
+ops by default), so the host logic is tested with gloo on CPU and the CUDA path with the loopback
+and multi-process runs on one GPU.
 """
 
 from __future__ import annotations
 
+import contextlib
+import ctypes
 from dataclasses import dataclass
 
 import numpy as np
 import torch
 
-__all__ = ["element_ranges", "column_bounds", "ShardedBuild", "TorchExchange", "LoopbackExchange", "CudaOps",
-           "run_loopback", "run_loopback_p2p", "P2PExchange", "RECORD_DOUBLES", "all_reduce", "barrier"]
+from .errors import NodeIndexError
 
-RECORD_DOUBLES = 40  # 36 packed KE values + 8 int32 node ids
+__all__ = ["element_ranges", "column_bounds", "balanced_bounds", "histogram_bins", "ShardedBuild", "TorchExchange",
+           "P2PExchange", "CudaOps", "run_loopback", "run_loopback_p2p", "RECORD_DOUBLES", "all_reduce", "barrier",
+           "digest_words", "concat_blocks", "csc_digest"]
+
+RECORD_DOUBLES = 40  # unpacked record: 36 packed KE values + 8 int32 node ids
+FAIL_WORDS = 3       # hx_fail_info as int64 words
+MAX_BINS = 1 << 16   # column histogram bins of the balanced bounds
 
 
 def element_ranges(n_el: int, world: int):
@@ -41,7 +59,67 @@ def element_ranges(n_el: int, world: int):
 
 
 def column_bounds(n_nodes: int, world: int) -> np.ndarray:
+    """Equal node split (the out-of-core build's blocks)."""
     return np.array([n_nodes * r // world for r in range(world + 1)], dtype=np.int64)
+
+
+def histogram_bins(n_nodes: int) -> int:
+    return int(max(1, min(MAX_BINS, n_nodes)))
+
+
+def balanced_bounds(hist: np.ndarray, n_nodes: int, world: int) -> np.ndarray:
+    """Column bounds at equal prefix sums of a per-bin weight histogram (bin b = nodes with
+    node * B // n_nodes == b, i.e. starting at ceil(b * n_nodes / B)).  Bound r is the first node
+    of the first bin whose exclusive prefix reaches r/G of the total; integer arithmetic only, so
+    every rank computes the same bounds from the same all-reduced histogram.  Every block keeps at
+    least one column when n_nodes >= world."""
+    hist = np.asarray(hist, dtype=np.int64)
+    B = hist.shape[0]
+    prefix = np.concatenate([[0], np.cumsum(hist)])  # prefix[b] = weight of bins < b
+    total = int(prefix[-1])
+    bounds = np.zeros(world + 1, dtype=np.int64)
+    bounds[world] = n_nodes
+    for r in range(1, world):
+        if total > 0:
+            b = int(np.searchsorted(prefix * world, r * total, side="left"))  # first b: prefix[b]*G >= r*total
+            b = min(b, B)
+            node = -(-b * n_nodes // B)
+        else:
+            node = n_nodes * r // world
+        bounds[r] = node
+    if n_nodes >= world:  # strictly increasing: no empty block
+        for r in range(1, world):
+            bounds[r] = min(max(bounds[r], bounds[r - 1] + 1), n_nodes - (world - r))
+    return bounds
+
+
+# ------------------------------------------------------------------------------------------
+# position-keyed digest (hx_digest restated for the host; test and bench checker)
+# ------------------------------------------------------------------------------------------
+_M64 = np.uint64(0xFFFFFFFFFFFFFFFF)
+
+
+def _mix(x: np.ndarray) -> np.ndarray:
+    with np.errstate(over="ignore"):
+        x = x + np.uint64(0x9E3779B97F4A7C15)
+        x = (x ^ (x >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        x = (x ^ (x >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        return x ^ (x >> np.uint64(31))
+
+
+def digest_words(words: np.ndarray, pos0: int = 0, add: int = 0) -> int:
+    """sum_i mix(mix(pos0 + i) ^ (word_i + add)) mod 2^64 over the 8-byte words of ``words``."""
+    w = np.ascontiguousarray(words).view(np.uint64)
+    pos = np.arange(pos0, pos0 + w.shape[0], dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        h = _mix(_mix(pos) ^ (w + np.uint64(add & 0xFFFFFFFFFFFFFFFF)))
+    return int(np.sum(h, dtype=np.uint64))
+
+
+def csc_digest(col_ptr, row_idx, vals) -> tuple:
+    """(col_ptr, row_idx, vals) digests of a whole lower CSC (host arrays)."""
+    return (digest_words(np.asarray(col_ptr, np.int64)), digest_words(np.asarray(row_idx, np.int64)),
+            digest_words(np.asarray(vals, np.float64)))
 
 
 # ------------------------------------------------------------------------------------------
@@ -79,45 +157,10 @@ def barrier(group=None, device_index=None) -> None:
 
 
 class TorchExchange:
-    """torch.distributed all-to-all: NCCL over NVLink on GPUs (device buffers), gloo on CPU (and
+    """torch.distributed collectives: NCCL over NVLink on GPUs (device buffers), gloo on CPU (and
     host-staged CUDA buffers when several ranks share one GPU for testing)."""
 
-    def __init__(self, group=None):
-        import torch.distributed as dist
-
-        self.dist = dist
-        self.group = group
-
-    def _a2a(self, recv, send, **kw):
-        if send.is_cuda and _host_staged(self.group):
-            r = torch.empty(recv.shape, dtype=recv.dtype)
-            self.dist.all_to_all_single(r, send.cpu(), group=self.group, **kw)
-            recv.copy_(r)
-        else:
-            self.dist.all_to_all_single(recv, send, group=self.group, **kw)
-        return recv
-
-    def counts(self, send_counts: torch.Tensor) -> torch.Tensor:
-        return self._a2a(torch.empty_like(send_counts), send_counts)
-
-    def records(self, send: torch.Tensor, send_splits, recv_splits) -> torch.Tensor:
-        recv = torch.empty((sum(recv_splits), RECORD_DOUBLES), dtype=send.dtype, device=send.device)
-        return self._a2a(recv, send, output_split_sizes=list(recv_splits), input_split_sizes=list(send_splits))
-
-    def allgather_int(self, value: int, device) -> list:
-        t = torch.tensor([value], dtype=torch.int64, device="cpu" if _host_staged(self.group) else device)
-        out = [torch.empty_like(t) for _ in range(self.dist.get_world_size(self.group))]
-        self.dist.all_gather(out, t, group=self.group)
-        return [int(x.item()) for x in out]
-
-
-class P2PExchange:
-    """The all-to-all done by the producer: every rank maps every other rank's receive buffer
-    (CUDA IPC through torch's storage sharing -- NVLink peer memory between GPUs, the same memory
-    between processes sharing a GPU) and hx_halo_send writes the records straight into them.  Only
-    the G x G count matrix goes through the process group (one all-gather); a stream-ordered
-    barrier (an NCCL all-reduce of one word; a host barrier under gloo) orders the receivers'
-    reads after every sender's kernel."""
+    p2p = False
 
     def __init__(self, group=None):
         import torch.distributed as dist
@@ -126,70 +169,153 @@ class P2PExchange:
         self.group = group
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
-        self.buf = None        # own receive buffer (records, 40 doubles each)
-        self.peers = None      # tensors mapping every rank's buffer (own included)
+
+    def allgather(self, t: torch.Tensor) -> np.ndarray:
+        """All-gather of a 1-D int64 tensor -> host (world, k) array (one host sync)."""
+        if t.is_cuda and _host_staged(self.group):
+            t = t.cpu()
+        out = [torch.empty_like(t) for _ in range(self.world)]
+        self.dist.all_gather(out, t, group=self.group)
+        return torch.stack(out).cpu().numpy()
+
+    def sum_(self, t: torch.Tensor) -> torch.Tensor:
+        return all_reduce(t, group=self.group)
+
+    def alltoall(self, send: torch.Tensor, send_splits, recv_splits) -> torch.Tensor:
+        recv = torch.empty(int(sum(recv_splits)), dtype=send.dtype, device=send.device)
+        kw = dict(output_split_sizes=[int(x) for x in recv_splits], input_split_sizes=[int(x) for x in send_splits])
+        if send.is_cuda and _host_staged(self.group):
+            r = torch.empty(recv.shape, dtype=recv.dtype)
+            self.dist.all_to_all_single(r, send.cpu(), group=self.group, **kw)
+            recv.copy_(r)
+        else:
+            self.dist.all_to_all_single(recv, send, group=self.group, **kw)
+        return recv
+
+
+class P2PExchange(TorchExchange):
+    """The all-to-all done by the producer: every rank maps every other rank's receive buffer and
+    hx_halo_pack writes the records straight into them.
+
+    Receive buffers are allocated by the library (``hx_ipc_alloc``: cudaMalloc + IPC handle); the
+    handles are all-gathered and opened with ``hx_ipc_open`` in THIS process's device context with
+    lazy peer access, so the pack kernel's stores reach another GPU's HBM over NVLink (and the same
+    GPU's memory when ranks share a device in tests).  Buffers grow (and every rank re-maps) only
+    when a rank needs more room.  Ordering: the count all-gather that precedes the pack is stream-
+    ordered after each rank's previous assembly, so no peer overwrites records still being read; a
+    one-word all-reduce after the pack orders the receivers' reads after every sender's kernel."""
+
+    p2p = True
+
+    def __init__(self, group=None, device=None):
+        super().__init__(group)
+        from . import _native as N
+
+        self.N = N
+        self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+        self.own = None        # (ptr, words) of this rank's receive buffer
+        self.peers = None      # raw pointers of every rank's buffer as seen from this process
+        self.opened = []
         self.ptrs = None       # device int64 array of the peer base pointers
 
-    def _ensure_capacity(self, need: int, device):
-        """Grow the receive buffer when needed; whenever any rank grows, all ranks re-map."""
-        grow = self.buf is None or self.buf.shape[0] < need
-        flag = torch.tensor([1 if grow else 0], dtype=torch.int64)
-        if self.dist.get_backend(self.group) != "gloo":
-            flag = flag.to(device)
+    def _on_device(self):
+        return torch.cuda.device(self.device) if self.device.type == "cuda" else contextlib.nullcontext()
+
+    def _sync(self):
+        if self.device.type == "cuda":
+            torch.cuda.synchronize(self.device)
+
+    def _release(self):
+        for p in self.opened:
+            self.N.lib().hx_ipc_close(ctypes.c_void_p(p))
+        self.opened = []
+        if self.own is not None:
+            self._sync()
+            self.N.lib().hx_ipc_free(ctypes.c_void_p(self.own[0]))
+            self.own = None
+
+    def close(self):
+        self._release()
+
+    def __del__(self):  # pragma: no cover - interpreter shutdown order
+        try:
+            self._release()
+        except Exception:
+            pass
+
+    def _ensure_capacity(self, need_words: int):
+        grow = self.own is None or self.own[1] < need_words
+        flag = torch.tensor([1 if grow else 0], dtype=torch.int64,
+                            device="cpu" if _host_staged(self.group) else self.device)
         self.dist.all_reduce(flag, op=self.dist.ReduceOp.MAX, group=self.group)
         if int(flag.item()) == 0:
             return
+        N = self.N
+        for p in self.opened:
+            N.check(N.lib().hx_ipc_close(ctypes.c_void_p(p)), "hx_ipc_close")
+        self.opened = []
         if grow:
-            self.buf = torch.empty((max(need + need // 4, 1024), RECORD_DOUBLES), dtype=torch.float64, device=device)
-        meta = self.buf.untyped_storage()._share_cuda_()
+            if self.own is not None:
+                self._sync()
+                N.check(N.lib().hx_ipc_free(ctypes.c_void_p(self.own[0])), "hx_ipc_free")
+                self.own = None
+            words = max(need_words + need_words // 4, 1024)
+            ptr = ctypes.c_void_p()
+            handle = ctypes.create_string_buffer(N.IPC_HANDLE_BYTES)
+            with self._on_device():
+                N.check(N.lib().hx_ipc_alloc(8 * words, ctypes.byref(ptr), handle), "hx_ipc_alloc")
+            self.own = (ptr.value, words, handle.raw)
         metas = [None] * self.world
-        self.dist.all_gather_object(metas, meta, group=self.group)
-        self.peers = []
-        for r, m in enumerate(metas):
-            if r == self.rank:
-                self.peers.append(self.buf)
-            else:
-                st = torch.UntypedStorage._new_shared_cuda(*m)
-                self.peers.append(torch.empty(0, dtype=torch.float64, device=device).set_(st))
-        self.ptrs = torch.tensor([p.data_ptr() for p in self.peers], dtype=torch.int64, device=device)
+        self.dist.all_gather_object(metas, self.own[2], group=self.group)
+        peers = []
+        with self._on_device():
+            for r, h in enumerate(metas):
+                if r == self.rank:
+                    peers.append(self.own[0])
+                    continue
+                p = ctypes.c_void_p()
+                N.check(N.lib().hx_ipc_open(ctypes.create_string_buffer(h, N.IPC_HANDLE_BYTES), ctypes.byref(p)),
+                        "hx_ipc_open")
+                self.opened.append(p.value)
+                peers.append(p.value)
+        self.peers = peers
+        self.ptrs = torch.tensor(peers, dtype=torch.int64, device=self.device)
 
-    def prepare(self, send_counts, device):
-        """-> (dest_ptrs, dest_offsets (device int64), recv_counts host list, receive view)"""
-        mine = torch.tensor(send_counts, dtype=torch.int64)
-        rows = [torch.empty_like(mine) for _ in range(self.world)]
-        if self.dist.get_backend(self.group) == "gloo":
-            self.dist.all_gather(rows, mine, group=self.group)
-        else:
-            dev_rows = [torch.empty(self.world, dtype=torch.int64, device=device) for _ in range(self.world)]
-            self.dist.all_gather(dev_rows, mine.to(device), group=self.group)
-            rows = [r.cpu() for r in dev_rows]
-        C = torch.stack(rows).numpy()  # C[s][d] records s -> d
-        recv_counts = [int(C[s][self.rank]) for s in range(self.world)]
-        self._ensure_capacity(int(sum(recv_counts)), device)
-        offsets = torch.tensor([int(C[:self.rank, d].sum()) for d in range(self.world)], dtype=torch.int64,
-                               device=device)
-        return self.ptrs, offsets, recv_counts, self.buf[:sum(recv_counts)]
+    def prepare(self, chunk: np.ndarray):
+        """chunk[s, d] = words source s sends to d -> (dest_ptrs, dest_offsets (device int64),
+        receive view (int64 words))."""
+        need = int(chunk[:, self.rank].sum())
+        self._ensure_capacity(need)
+        offsets = torch.tensor(p2p_offsets(chunk, self.rank), dtype=torch.int64, device=self.device)
+        recv = _words_view(self.own[0], need, self.device)
+        return self.ptrs, offsets, recv
 
-    def barrier(self, device):
-        if self.dist.get_backend(self.group) == "gloo":
-            torch.cuda.synchronize(device)
+    def fence(self):
+        """Stream-ordered barrier: the receivers read after every sender's pack kernel."""
+        if _host_staged(self.group):
+            torch.cuda.synchronize(self.device)
             self.dist.barrier(group=self.group)
         else:
-            t = torch.zeros(1, dtype=torch.int32, device=device)
-            self.dist.all_reduce(t, group=self.group)  # stream-ordered: after every rank's send kernel
+            t = torch.zeros(1, dtype=torch.int32, device=self.device)
+            self.dist.all_reduce(t, group=self.group)
 
-    def counts(self, send_counts):  # the ShardedBuild e2e helpers use the process group directly
-        raise NotImplementedError
 
-    def allgather_int(self, value: int, device) -> list:
-        t = torch.tensor([value], dtype=torch.int64)
-        out = [torch.empty_like(t) for _ in range(self.world)]
-        if self.dist.get_backend(self.group) == "gloo":
-            self.dist.all_gather(out, t, group=self.group)
-            return [int(x.item()) for x in out]
-        dev_out = [torch.empty(1, dtype=torch.int64, device=device) for _ in range(self.world)]
-        self.dist.all_gather(dev_out, t.to(device), group=self.group)
-        return [int(x.item()) for x in dev_out]
+def p2p_offsets(chunk: np.ndarray, rank: int) -> list:
+    """Where ``rank``'s chunk for each destination d starts in d's receive buffer (words): after
+    the chunks of every lower source -- the layout all_to_all_single produces."""
+    return [int(chunk[:rank, d].sum()) for d in range(chunk.shape[1])]
+
+
+def _words_view(ptr: int, words: int, device) -> torch.Tensor:
+    """An int64 tensor over raw device memory owned elsewhere (no copy, no ownership)."""
+    if words == 0:
+        return torch.empty(0, dtype=torch.int64, device=device)
+
+    class _Arr:
+        __cuda_array_interface__ = {"shape": (words,), "typestr": "<i8", "data": (ptr, False), "version": 3,
+                                    "strides": None}
+
+    return torch.as_tensor(_Arr(), device=device)
 
 
 # ------------------------------------------------------------------------------------------
@@ -199,11 +325,18 @@ class CudaOps:
     """The device kernels of libhexfem_b200.so."""
 
     def __init__(self, device=None, mode="exact"):
+        from . import _native as N
         from . import device as D
 
-        self.D = D
+        self.D, self.N = D, N
         self.device = D.require_device(device)
         self.mode = mode
+
+    def _p(self, t):
+        return self.D._ptr(t)
+
+    def _s(self):
+        return self.D.stream_handle()
 
     def upload(self, coords, conn, coeff):
         def up(a, dt):
@@ -212,49 +345,62 @@ class CudaOps:
         return self.D.DeviceMesh(up(coords, np.float64), up(conn, np.int32), up(coeff, np.float64))
 
     def integrate(self, dm):
-        ke, rows, cols, fail = self.D.integrate_mesh(dm, mode=self.mode)
-        return ke, rows, cols, fail
+        """-> (ke, rows, cols, fail record (3,) int64 device)"""
+        return self.D.integrate_mesh(dm, mode=self.mode)
 
-    def check_fail(self, fail, offset):
-        self.D.raise_if_failed(fail, offset)
-
-    def halo_count(self, dm, bounds_dev, world, rank):
-        """-> (per_dest (world,) int64 host list, workspace) -- hx_halo_count."""
-        from . import _native as N
-
-        n = dm.n_el
-        ws_bytes = N.lib().hx_halo_workspace_bytes(n, world)
-        ws = torch.empty(ws_bytes, dtype=torch.uint8, device=self.device)
-        per_dest = torch.empty(world, dtype=torch.int64, device=self.device)
-        N.check(N.lib().hx_halo_count(self.D._ptr(dm.conn), n, self.D._ptr(bounds_dev), world, rank,
-                                      self.D._ptr(per_dest), self.D._ptr(ws), ws_bytes, self.D.stream_handle()),
-                "hx_halo_count")
-        return per_dest.cpu().tolist(), ws
-
-    def halo(self, dm, ke, bounds_dev, world, rank):
-        """-> (records (S, 40) f64 destination-major send buffer, per_dest host list)"""
-        from . import _native as N
-
-        counts, ws = self.halo_count(dm, bounds_dev, world, rank)
-        records = torch.empty((max(sum(counts), 0), RECORD_DOUBLES), dtype=torch.float64, device=self.device)
-        N.check(N.lib().hx_halo_pack(self.D._ptr(dm.conn), self.D._ptr(ke), dm.n_el, self.D._ptr(bounds_dev), world,
-                                     rank, self.D._ptr(records), self.D._ptr(ws), self.D.stream_handle()),
-                "hx_halo_pack")
-        return records, counts
-
-    def halo_send(self, dm, ke, bounds_dev, world, rank, dest_ptrs, dest_offsets, ws):
-        """Fused pack-and-send: records straight into the destinations' receive buffers."""
-        from . import _native as N
-
-        N.check(N.lib().hx_halo_send(self.D._ptr(dm.conn), self.D._ptr(ke), dm.n_el, self.D._ptr(bounds_dev), world,
-                                     rank, self.D._ptr(dest_ptrs), self.D._ptr(dest_offsets), self.D._ptr(ws),
-                                     self.D.stream_handle()), "hx_halo_send")
+    def column_weights(self, dm, n_nodes: int, n_bins: int) -> torch.Tensor:
+        hist = torch.zeros(n_bins, dtype=torch.int64, device=self.device)
+        self.N.check(self.N.lib().hx_column_weights(self._p(dm.conn), dm.n_el, n_nodes, n_bins, self._p(hist),
+                                                    self._s()), "hx_column_weights")
+        return hist
 
     def bounds(self, bounds_np):
-        return torch.from_numpy(bounds_np).to(self.device)
+        return torch.from_numpy(np.ascontiguousarray(bounds_np, dtype=np.int64)).to(self.device)
+
+    def halo_count(self, dm, bounds_dev, world, rank):
+        """-> (per_dest (world, 2) int64 device: records, values per destination; workspace)"""
+        ws_bytes = self.N.lib().hx_halo_workspace_bytes(dm.n_el, world)
+        ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=self.device)
+        per_dest = torch.empty((world, 2), dtype=torch.int64, device=self.device)
+        self.N.check(self.N.lib().hx_halo_count(self._p(dm.conn), dm.n_el, self._p(bounds_dev), world, rank,
+                                                self._p(per_dest), self._p(ws), ws_bytes, self._s()), "hx_halo_count")
+        return per_dest, ws
+
+    def alloc_words(self, n: int) -> torch.Tensor:
+        return torch.empty(n, dtype=torch.int64, device=self.device)
+
+    def halo_pack(self, dm, ke, bounds_dev, world, rank, dest_ptrs, dest_offsets, ws):
+        """dest_ptrs: device int64 (world,) base addresses; dest_offsets: device int64 (world,) words."""
+        self.N.check(self.N.lib().hx_halo_pack(self._p(dm.conn), self._p(ke), dm.n_el, self._p(bounds_dev), world,
+                                               rank, self._p(dest_ptrs), self._p(dest_offsets), self._p(ws),
+                                               self._s()), "hx_halo_pack")
+
+    def pointers(self, bases, offsets):
+        return (torch.tensor([int(b) for b in bases], dtype=torch.int64, device=self.device),
+                torch.tensor([int(o) for o in offsets], dtype=torch.int64, device=self.device))
+
+    def halo_unpack(self, recv, src_desc: np.ndarray, bounds_dev, world, rank, n_rec):
+        records = torch.empty((n_rec, RECORD_DOUBLES), dtype=torch.float64, device=self.device)
+        if n_rec == 0:
+            return records
+        desc = torch.from_numpy(np.ascontiguousarray(src_desc, dtype=np.int64)).to(self.device)
+        ws_bytes = self.N.lib().hx_halo_unpack_workspace_bytes(n_rec)
+        ws = torch.empty(ws_bytes, dtype=torch.uint8, device=self.device)
+        self.N.check(self.N.lib().hx_halo_unpack(self._p(recv), self._p(desc), world, rank, self._p(bounds_dev), n_rec,
+                                                 self._p(records), self._p(ws), ws_bytes, self._s()),
+                     "hx_halo_unpack")
+        return records
 
     def assemble(self, segments, n_nodes, c_lo, c_hi):
         return self.D.mesh_csc(segments, n_nodes, c_lo, c_hi)
+
+    def digest(self, t: torch.Tensor, pos0: int, add: int = 0) -> torch.Tensor:
+        """Device u64 (as int64) accumulator of hx_digest over ``t``'s 8-byte words."""
+        out = torch.zeros(1, dtype=torch.int64, device=self.device)
+        self.N.check(self.N.lib().hx_digest(self._p(t), t.numel() * t.element_size() // 8, pos0,
+                                            ctypes.c_uint64(add & 0xFFFFFFFFFFFFFFFF), self._p(out), self._s()),
+                     "hx_digest")
+        return out
 
 
 def record_segment(records: torch.Tensor):
@@ -273,100 +419,168 @@ class ShardResult:
     nnz_offset: int = 0
 
 
+def _fail_error(meta: np.ndarray, e_starts, n_nodes):
+    """The exception every rank raises: the lowest element with a bad node id, else the lowest
+    degenerate element (global ids) over all ranks' fail records (hx_fail_info words)."""
+    from .device import fail_error
+
+    best = None
+    for r in range(meta.shape[0]):
+        err = fail_error(meta[r, :FAIL_WORDS], int(e_starts[r]), n_nodes)
+        if err is None:
+            continue
+        key = (not isinstance(err, NodeIndexError), err.element_id)
+        if best is None or key < best[0]:
+            best = (key, err)
+    return None if best is None else best[1]
+
+
 class ShardedBuild:
     """One rank's share of the global build (see module docstring)."""
 
-    def __init__(self, mesh, rank: int, world: int, mode: str = "exact", ops=None, exchange=None):
+    def __init__(self, mesh, rank: int, world: int, mode: str = "exact", ops=None, exchange=None, bounds=None):
         self.rank, self.world = rank, world
         self.ops = ops if ops is not None else CudaOps(mode=mode)
         self.exchange = exchange if exchange is not None else TorchExchange()
         self.n_el, self.n_nodes = mesh.n_el, mesh.n_nodes
-        self.e_lo, self.e_hi = element_ranges(mesh.n_el, world)[rank]
-        self.bounds_np = column_bounds(mesh.n_nodes, world)
-        self.c_lo, self.c_hi = int(self.bounds_np[rank]), int(self.bounds_np[rank + 1])
+        self.ranges = element_ranges(mesh.n_el, world)
+        self.e_lo, self.e_hi = self.ranges[rank]
         self.dm = self.ops.upload(mesh.coords, mesh.connectivity[self.e_lo:self.e_hi],
                                   mesh.coefficient[self.e_lo:self.e_hi])
+        if bounds is None:  # nnz-balanced: one all-reduce of the per-bin weights of every rank's elements
+            hist = self.ops.column_weights(self.dm, self.n_nodes, histogram_bins(self.n_nodes))
+            hist = self.exchange.sum_(hist)
+            bounds = balanced_bounds(hist.cpu().numpy(), self.n_nodes, world)
+        self.bounds_np = np.asarray(bounds, dtype=np.int64)
+        self.c_lo, self.c_hi = int(self.bounds_np[rank]), int(self.bounds_np[rank + 1])
         self.bounds = self.ops.bounds(self.bounds_np)
         self.last = None
         self.last_index = None
+        self.last_counts = None
 
     # -- phases (so a loopback driver can interleave G ranks in one process) --
     def phase_local(self):
+        """Integrate the owned elements and count the records per destination -> the row this
+        rank contributes to the metadata all-gather: fail record (3) + (records, values) x G."""
         ke, rows, cols, fail = self.ops.integrate(self.dm)
-        records, send_counts = self.ops.halo(self.dm, ke, self.bounds, self.world, self.rank)
-        self._pending = (ke, rows, cols, fail)
-        return records, send_counts
+        per_dest, ws = self.ops.halo_count(self.dm, self.bounds, self.world, self.rank)
+        self._pending = (ke, rows, cols, ws)
+        return torch.cat([fail.reshape(-1).to(per_dest.device), per_dest.reshape(-1)])
 
-    def phase_assemble(self, recv: torch.Tensor, recv_counts):
-        ke, rows, cols, fail = self._pending
+    def check_meta(self, meta: np.ndarray) -> np.ndarray:
+        """Raise the global failure on every rank; -> C (world, world, 2): C[s, d] = (records, values)."""
+        err = _fail_error(meta, [lo for lo, _ in self.ranges], self.n_nodes)
+        if err is not None:
+            self._pending = None
+            raise err
+        return meta[:, FAIL_WORDS:].reshape(self.world, self.world, 2)
+
+    def pack(self, dest_ptrs, dest_offsets):
+        ke, _, _, ws = self._pending
+        self.ops.halo_pack(self.dm, ke, self.bounds, self.world, self.rank, dest_ptrs, dest_offsets, ws)
+
+    def phase_assemble(self, recv: torch.Tensor, C: np.ndarray):
+        """recv: int64 words, the chunks of every source in ascending source order."""
+        ke, rows, cols, _ = self._pending
         self._pending = None
-        n_lower = int(sum(recv_counts[:self.rank]))
+        chunk = 4 * C[:, :, 0] + C[:, :, 1]
+        r = self.rank
+        desc = np.zeros((self.world, 3), dtype=np.int64)
+        desc[:, 0] = np.concatenate([[0], np.cumsum(chunk[:, r])[:-1]])
+        desc[:, 1:] = C[:, r, :]
+        n_rec = int(C[:, r, 0].sum())
+        records = self.ops.halo_unpack(recv, desc, self.bounds, self.world, r, n_rec)
+        n_lower = int(C[:r, r, 0].sum())
         segments = []
         if n_lower:
-            segments.append(record_segment(recv[:n_lower]))
+            segments.append(record_segment(records[:n_lower]))
         segments.append((self.dm.conn, ke))
-        if recv.shape[0] > n_lower:
-            segments.append(record_segment(recv[n_lower:]))
-        self.ops.check_fail(fail, self.e_lo)
+        if n_rec > n_lower:
+            segments.append(record_segment(records[n_lower:]))
         csc = self.ops.assemble(segments, self.n_nodes, self.c_lo, self.c_hi)
         self.last = ShardResult(csc.col_ptr, csc.row_idx, csc.vals, self.c_lo, self.c_hi)
         self.last_index = (ke, rows, cols)
+        self.last_counts = C
         return self.last
 
     def step(self):
-        if isinstance(self.exchange, P2PExchange):
-            return self.step_p2p()
-        records, send_counts = self.phase_local()
-        dev = records.device
-        recv_counts = self.exchange.counts(torch.tensor(send_counts, dtype=torch.int64, device=dev)).cpu().tolist()
-        recv = self.exchange.records(records, send_counts, recv_counts)
-        return self.phase_assemble(recv, recv_counts)
-
-    def step_p2p(self):
-        """Integrate, count, map the destinations, fused pack-and-send, barrier, assemble."""
-        dev = self.ops.device
-        ke, rows, cols, fail = self.ops.integrate(self.dm)
-        send_counts, ws = self.ops.halo_count(self.dm, self.bounds, self.world, self.rank)
-        ptrs, offsets, recv_counts, recv = self.exchange.prepare(send_counts, dev)
-        self.ops.halo_send(self.dm, ke, self.bounds, self.world, self.rank, ptrs, offsets, ws)
-        self.exchange.barrier(dev)
-        self._pending = (ke, rows, cols, fail)
-        return self.phase_assemble(recv, recv_counts)
+        meta = self.exchange.allgather(self.phase_local())
+        C = self.check_meta(meta)
+        chunk = 4 * C[:, :, 0] + C[:, :, 1]
+        r = self.rank
+        if self.exchange.p2p:
+            ptrs, offsets, recv = self.exchange.prepare(chunk)
+            self.pack(ptrs, offsets)
+            self.exchange.fence()
+        else:
+            send_splits = chunk[r, :]
+            send = self.ops.alloc_words(int(send_splits.sum()))
+            offs = np.concatenate([[0], np.cumsum(send_splits)[:-1]])
+            ptrs, offsets = self.ops.pointers([send.data_ptr()] * self.world, offs)
+            self.pack(ptrs, offsets)
+            recv = self.exchange.alltoall(send, send_splits, chunk[:, r])
+        return self.phase_assemble(recv, C)
 
     def global_nnz(self) -> int:
-        nnzs = self.exchange.allgather_int(int(self.last.row_idx.shape[0]), self.last.row_idx.device)
-        self.last.nnz_offset = int(sum(nnzs[:self.rank]))
-        return int(sum(nnzs))
+        nnz = torch.tensor([int(self.last.row_idx.shape[0])], dtype=torch.int64, device=self.last.row_idx.device)
+        nnzs = self.exchange.allgather(nnz)[:, 0]
+        self.last.nnz_offset = int(nnzs[:self.rank].sum())
+        return int(nnzs.sum())
+
+    def exchange_bytes(self) -> dict:
+        """Bytes of the last step's record exchange over all ranks (wire format: 8-byte words)."""
+        C = self.last_counts
+        off = ~np.eye(self.world, dtype=bool)
+        recs, vals = int(C[:, :, 0][off].sum()), int(C[:, :, 1][off].sum())
+        return {"records": recs, "values": vals, "bytes": 8 * (4 * recs + vals),
+                "bytes_per_element": 8 * (4 * recs + vals) / max(self.n_el, 1),
+                "records_per_element": recs / max(self.n_el, 1)}
+
+    def block_digest(self) -> torch.Tensor:
+        """(col_ptr, row_idx, vals) digests of this rank's block at their global positions (call
+        global_nnz first); summed over ranks they equal csc_digest of the whole matrix."""
+        res, ops = self.last, self.ops
+        ncols = self.c_hi - self.c_lo
+        d_cp = ops.digest(res.col_ptr[:ncols], self.c_lo, res.nnz_offset)
+        if self.rank == self.world - 1:
+            d_cp = d_cp + ops.digest(res.col_ptr[ncols:], self.n_nodes, res.nnz_offset)
+        return torch.cat([d_cp, ops.digest(res.row_idx, res.nnz_offset), ops.digest(res.vals, res.nnz_offset)])
 
     # -- benchmark helpers --
     def stage_times(self, repeats=3):
-        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        """Per-stage device times of step() (CUDA events; the exchange includes its host syncs)."""
         acc = {"ke_ms": 0.0, "halo_exchange_ms": 0.0, "assembly_ms": 0.0}
         for _ in range(repeats):
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
             ev[0].record()
             ke, rows, cols, fail = self.ops.integrate(self.dm)
             ev[1].record()
-            if isinstance(self.exchange, P2PExchange):
-                dev = self.ops.device
-                send_counts, ws = self.ops.halo_count(self.dm, self.bounds, self.world, self.rank)
-                ptrs, offsets, recv_counts, recv = self.exchange.prepare(send_counts, dev)
-                self.ops.halo_send(self.dm, ke, self.bounds, self.world, self.rank, ptrs, offsets, ws)
-                self.exchange.barrier(dev)
+            per_dest, ws = self.ops.halo_count(self.dm, self.bounds, self.world, self.rank)
+            self._pending = (ke, rows, cols, ws)
+            meta = self.exchange.allgather(torch.cat([fail.reshape(-1), per_dest.reshape(-1)]))
+            C = self.check_meta(meta)
+            chunk = 4 * C[:, :, 0] + C[:, :, 1]
+            if self.exchange.p2p:
+                ptrs, offsets, recv = self.exchange.prepare(chunk)
+                self.pack(ptrs, offsets)
+                self.exchange.fence()
             else:
-                records, send_counts = self.ops.halo(self.dm, ke, self.bounds, self.world, self.rank)
-                dev = records.device
-                recv_counts = self.exchange.counts(torch.tensor(send_counts, dtype=torch.int64,
-                                                                device=dev)).cpu().tolist()
-                recv = self.exchange.records(records, send_counts, recv_counts)
+                send_splits = chunk[self.rank, :]
+                send = self.ops.alloc_words(int(send_splits.sum()))
+                offs = np.concatenate([[0], np.cumsum(send_splits)[:-1]])
+                ptrs, offsets = self.ops.pointers([send.data_ptr()] * self.world, offs)
+                self.pack(ptrs, offsets)
+                recv = self.exchange.alltoall(send, send_splits, chunk[:, self.rank])
             ev[2].record()
-            self._pending = (ke, rows, cols, fail)
-            self.phase_assemble(recv, recv_counts)
+            self.phase_assemble(recv, C)
             ev[3].record()
             torch.cuda.synchronize()
             acc["ke_ms"] += ev[0].elapsed_time(ev[1]) / repeats
             acc["halo_exchange_ms"] += ev[1].elapsed_time(ev[2]) / repeats
             acc["assembly_ms"] += ev[2].elapsed_time(ev[3]) / repeats
-        acc["launches_per_step"] = 7 + 5  # single-GPU set + halo count/scan(2)/totals/pack
+        # integration + fail resolve, halo count (+2 CUB scans x 2 kernels + totals), pack, unpack
+        # (count + 2 scan kernels + expand), mesh assembly (adjacency, pattern, scan x2, emit, peek)
+        acc["launches_per_step"] = 2 + 6 + 1 + 4 + 6
         return acc
 
     def measure_e2e(self, steps, barrier):
@@ -427,61 +641,55 @@ class ShardedBuild:
 # ------------------------------------------------------------------------------------------
 # loopback: G virtual ranks in one process (tests the CUDA sharded path on one GPU)
 # ------------------------------------------------------------------------------------------
-class LoopbackExchange:
-    def allgather_int(self, value, device):
-        raise NotImplementedError("use run_loopback")
+def _loopback_ranks(mesh, world, ops_factory):
+    ops0 = ops_factory()
+    whole = ops0.upload(mesh.coords, mesh.connectivity, mesh.coefficient)
+    hist = ops0.column_weights(whole, mesh.n_nodes, histogram_bins(mesh.n_nodes))
+    bounds = balanced_bounds(hist.cpu().numpy(), mesh.n_nodes, world)
+    del whole
+    ranks = [ShardedBuild(mesh, r, world, ops=ops_factory(), exchange=None, bounds=bounds) for r in range(world)]
+    meta = np.stack([rk.phase_local().cpu().numpy() for rk in ranks])
+    C = ranks[0].check_meta(meta)
+    return ranks, C, 4 * C[:, :, 0] + C[:, :, 1]
+
+
+def _finish(ranks, recvs, C):
+    results = [rk.phase_assemble(recvs[r], C) for r, rk in enumerate(ranks)]
+    off = 0
+    for res in results:
+        res.nnz_offset = off
+        off += int(res.row_idx.shape[0])
+    return results
 
 
 def run_loopback(mesh, world: int, ops_factory):
-    """Run all G ranks' phases in one process; returns the list of ShardResult (rank order)."""
-    ranks = [ShardedBuild(mesh, r, world, ops=ops_factory(), exchange=LoopbackExchange()) for r in range(world)]
-    sends = [rk.phase_local() for rk in ranks]
-    results = []
+    """All-to-all layout: each rank packs into its own send buffer, the driver moves the chunks
+    like all_to_all_single; returns the ShardResults (rank order)."""
+    ranks, C, chunk = _loopback_ranks(mesh, world, ops_factory)
+    sends = []
     for r, rk in enumerate(ranks):
-        parts, recv_counts = [], []
-        for s, (records, counts) in enumerate(sends):
-            off = int(sum(counts[:r]))
-            parts.append(records[off:off + counts[r]])
-            recv_counts.append(int(counts[r]))
-        recv = torch.cat(parts) if parts else sends[r][0][:0]
-        results.append(rk.phase_assemble(recv, recv_counts))
-    off = 0
-    for res in results:
-        res.nnz_offset = off
-        off += int(res.row_idx.shape[0])
-    return results
+        send = rk.ops.alloc_words(int(chunk[r].sum()))
+        offs = np.concatenate([[0], np.cumsum(chunk[r])[:-1]])
+        rk.pack(*rk.ops.pointers([send.data_ptr()] * world, offs))
+        sends.append((send, offs))
+    recvs = []
+    for d in range(world):
+        parts = [sends[s][0][int(sends[s][1][d]):int(sends[s][1][d] + chunk[s, d])] for s in range(world)]
+        recvs.append(torch.cat(parts))
+    return _finish(ranks, recvs, C)
 
 
 def run_loopback_p2p(mesh, world: int, ops_factory):
-    """G virtual ranks in one process with the fused pack-and-send: each rank's hx_halo_send writes
-    into the other ranks' receive buffers (local memory here, peer memory across GPUs)."""
-    ranks = [ShardedBuild(mesh, r, world, ops=ops_factory(), exchange=LoopbackExchange()) for r in range(world)]
-    local = []
-    C = np.zeros((world, world), dtype=np.int64)
+    """Fused pack-and-send layout: every rank's pack kernel writes straight into the destinations'
+    receive buffers (local memory here, peer memory across GPUs)."""
+    ranks, C, chunk = _loopback_ranks(mesh, world, ops_factory)
+    ops = ranks[0].ops
+    recvs = [ops.alloc_words(max(int(chunk[:, d].sum()), 1)).fill_(-1) for d in range(world)]
     for r, rk in enumerate(ranks):
-        ke, rows, cols, fail = rk.ops.integrate(rk.dm)
-        counts, ws = rk.ops.halo_count(rk.dm, rk.bounds, world, r)
-        C[r] = counts
-        local.append((ke, rows, cols, fail, ws))
-    dev = ranks[0].ops.device
-    bufs = [torch.full((max(int(C[:, d].sum()), 1), RECORD_DOUBLES), float("nan"), dtype=torch.float64, device=dev)
-            for d in range(world)]
-    ptrs = torch.tensor([b.data_ptr() for b in bufs], dtype=torch.int64, device=dev)
-    for r, rk in enumerate(ranks):
-        offsets = torch.tensor([int(C[:r, d].sum()) for d in range(world)], dtype=torch.int64, device=dev)
-        ke, _, _, _, ws = local[r]
-        rk.ops.halo_send(rk.dm, ke, rk.bounds, world, r, ptrs, offsets, ws)
-    results = []
-    for r, rk in enumerate(ranks):
-        ke, rows, cols, fail, _ = local[r]
-        rk._pending = (ke, rows, cols, fail)
-        recv_counts = [int(C[s][r]) for s in range(world)]
-        results.append(rk.phase_assemble(bufs[r][:sum(recv_counts)], recv_counts))
-    off = 0
-    for res in results:
-        res.nnz_offset = off
-        off += int(res.row_idx.shape[0])
-    return results
+        offs = p2p_offsets(chunk, r)
+        rk.pack(*rk.ops.pointers([b.data_ptr() for b in recvs], offs))
+    recvs = [recvs[d][:int(chunk[:, d].sum())] for d in range(world)]
+    return _finish(ranks, recvs, C)
 
 
 def concat_blocks(results):

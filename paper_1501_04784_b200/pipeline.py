@@ -18,7 +18,7 @@ import torch
 
 from . import device as D
 from .assemble import LowerCscMatrix, csc_to_host
-from .errors import ConfigurationError
+from .errors import ConfigurationError, DegenerateElementError, MeshValidationError, NodeIndexError
 from .integrate import plan_batches, required_bytes
 
 __all__ = ["BuildReport", "DeviceBuild", "build_device", "run_build", "build_out_of_core", "device_bytes", "triplet_memory", "csc_memory",
@@ -159,10 +159,15 @@ def build_device(dm: D.DeviceMesh, mode: str = "exact", with_index: bool = True,
         main.wait_event(plan_done)
         csc = D.mesh_emit(plan, ke, stream=main)
     else:
-        csc = D.mesh_csc([(dm.conn, ke)], dm.n_nodes, stream=main, order=dm.assembly_order(), prep=prep)
+        try:
+            csc = D.mesh_csc([(dm.conn, ke)], dm.n_nodes, stream=main, order=dm.assembly_order(), prep=prep)
+        except MeshValidationError:
+            for f in fails:  # an out-of-range node id is reported as the element's NodeIndexError
+                D.raise_if_failed(f, n_nodes=dm.n_nodes)
+            raise
     if cached is None:  # a planned rebuild stays asynchronous: check the fail records later
         for f in fails:
-            D.raise_if_failed(f)
+            D.raise_if_failed(f, n_nodes=dm.n_nodes)
     return DeviceBuild(ke, rows if with_index else None, cols if with_index else None, csc, fails)
 
 
@@ -219,8 +224,12 @@ def build_out_of_core(mesh, n_blocks: int, mode: str = "exact", device=None, ret
             f = fail.cpu().numpy()
             if f[0] >= 0:
                 gid = int(ids[int(f[0])].item())
-                if worst is None or gid < worst[0]:
-                    worst = (gid, int(np.int32(f[1] & 0xFFFFFFFF)), float(f[2:3].view(np.float64)[0]))
+                err = D.fail_error(f, n_nodes=n_nodes)
+                err.element_id = gid
+                # the lowest bad-node element wins over every degenerate one (hx_fail_info)
+                key = (not isinstance(err, NodeIndexError), gid)
+                if worst is None or key < worst[0]:
+                    worst = (key, err)
                 continue
             csc = D.mesh_csc([(conn, ke)], n_nodes, lo, hi, order=order)
             ev[2].record()
@@ -238,9 +247,10 @@ def build_out_of_core(mesh, n_blocks: int, mode: str = "exact", device=None, ret
                 done[ids_h] = True
             del ids, conn, coeff, sub, ke, csc
         if worst is not None:
-            from .errors import DegenerateElementError
-
-            raise DegenerateElementError(element_id=worst[0], gauss_point=worst[1], det=worst[2])
+            err = worst[1]
+            if isinstance(err, NodeIndexError):
+                raise NodeIndexError(element_id=err.element_id, node=err.node, n_nodes=n_nodes)
+            raise DegenerateElementError(element_id=err.element_id, gauss_point=err.gauss_point, det=err.det)
         # columns of nodes no element references keep col_ptr flat
         np.maximum.accumulate(col_ptr, out=col_ptr)
     matrix = LowerCscMatrix(col_ptr=col_ptr, row_idx=np.concatenate(rows) if rows else np.empty(0, np.int64),
@@ -286,7 +296,7 @@ def run_build(mesh, budget_bytes: int, workers: int = 1, mode: str = "sequential
             fails.append(fail)
         ev[1].record()
         for f in fails:
-            D.raise_if_failed(f)
+            D.raise_if_failed(f, n_nodes=dm.n_nodes)
         csc = D.mesh_csc([(dm.conn, ke)], dm.n_nodes)
         ev[2].record()
         matrix: LowerCscMatrix = csc_to_host(csc)

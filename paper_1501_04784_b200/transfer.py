@@ -90,6 +90,8 @@ class CscHostTransfer:
             done = self.copy.record_event(torch.cuda.Event(enable_timing=self.trace is not None))
             for t in (rows32, csc.row_idx, csc.vals, csc.col_ptr):
                 t.record_stream(self.copy)  # keep the device blocks alive until the copies ran
+        if csc.readers is not None:  # plan-owned buffers: the next emit into them waits for these copies
+            csc.readers.append(done)
         dim, threads = csc.dim, self.threads
 
         trace, k = self.trace, self.k - 1

@@ -1,7 +1,7 @@
 """Generate the golden fixtures by running the REFERENCE package itself (build container only).
 
     PYTHONPATH=/root/reference/pkg/src:. PYTHONDONTWRITEBYTECODE=1 NUMBA_CACHE_DIR=/tmp/nc \
-        python tests/golden/make_golden.py [--big]
+        python tests/golden/make_golden.py [--big | --add C5]
 
 Writes
   tests/golden/small.npz     small arrays: dn table, element batches, meshes, CSC outputs, errors
@@ -150,6 +150,18 @@ def main(big: bool):
     (HERE / "digests.json").write_text(json.dumps(digests, indent=1) + "\n")
 
 
+def add_config(name: str):
+    """Append one BASELINE config's reference digests to digests.json (C5: 16.8M elements,
+    permuted numbering -- about 7 minutes and ~40 GB of RAM for the reference's lexsort)."""
+    path = HERE / "digests.json"
+    digests = json.loads(path.read_text())
+    digests["configs"][name] = digests_of(name, make_workload(name))
+    path.write_text(json.dumps(digests, indent=1) + "\n")
+
+
 if __name__ == "__main__":
     assert os.environ.get("PYTHONDONTWRITEBYTECODE"), "set PYTHONDONTWRITEBYTECODE=1 (reference is read-only)"
-    main(big="--big" in sys.argv)
+    if "--add" in sys.argv:
+        add_config(sys.argv[sys.argv.index("--add") + 1])
+    else:
+        main(big="--big" in sys.argv)

@@ -32,7 +32,7 @@ def test_library_loads_and_exports_every_declared_symbol():
 
 
 def test_abi_version():
-    assert N.lib().hx_abi_version() == 3
+    assert N.lib().hx_abi_version() == 4
 
 
 def test_compiled_dn_table_is_the_reference_table(golden):

@@ -8,6 +8,7 @@ infrastructure).  The concatenated column blocks must be bitwise equal to the si
 reference CSC -- the same bar the GPU loopback tests apply to the CUDA kernels.
 """
 
+import ctypes
 import os
 import socket
 import sys
@@ -20,45 +21,69 @@ import torch
 import torch.multiprocessing as mp
 
 ROOT = Path(__file__).resolve().parent.parent
-RECORD_DOUBLES = 40
+
+
+def _words_at(ptr: int, n: int) -> np.ndarray:
+    return np.ctypeslib.as_array((ctypes.c_int64 * max(n, 1)).from_address(ptr))[:n]
 
 
 class OracleOps:
-    """CPU stand-in for distributed.CudaOps with the same call contract (oracle arithmetic)."""
+    """CPU stand-in for distributed.CudaOps with the same call contract (oracle arithmetic and the
+    numpy restatement of the exchange kernels, oracle/halo.py)."""
 
     def upload(self, coords, conn, coeff):
-        return SimpleNamespace(coords=np.ascontiguousarray(coords), conn=torch.from_numpy(np.ascontiguousarray(conn)),
-                               coeff=np.ascontiguousarray(coeff))
+        conn = np.ascontiguousarray(conn)
+        return SimpleNamespace(coords=np.ascontiguousarray(coords), conn=torch.from_numpy(conn),
+                               coeff=np.ascontiguousarray(coeff), n_el=conn.shape[0])
 
     def integrate(self, dm):
         import oracle
 
         ke, rows, cols, first, _, _ = oracle.stiffness_mesh(dm.coords, dm.conn.numpy(), dm.coeff, threads=1)
-        return torch.from_numpy(ke), torch.from_numpy(rows), torch.from_numpy(cols), first
+        fail = torch.tensor([-1, -1, 0], dtype=torch.int64)
+        if first >= 0:
+            fail[0] = first
+            fail[1] = 0
+        return torch.from_numpy(ke), torch.from_numpy(rows), torch.from_numpy(cols), fail
 
-    def check_fail(self, fail, offset):
-        assert fail == -1
+    def column_weights(self, dm, n_nodes, n_bins):
+        from oracle import halo
+
+        return torch.from_numpy(halo.column_weights(dm.conn.numpy(), n_nodes, n_bins))
 
     def bounds(self, bounds_np):
         return bounds_np
 
-    def halo(self, dm, ke, bounds, world, rank):
-        """Restatement of hx_halo_count/hx_halo_pack: every local element, in ascending order, to
-        every other rank owning one of its nodes; destination-major record buffer."""
-        conn = dm.conn.numpy()
-        owner = np.searchsorted(bounds, conn, side="right") - 1  # (n, 8)
-        buckets = [[] for _ in range(world)]
-        for e in range(conn.shape[0]):
-            for d in sorted(set(owner[e].tolist()) - {rank}):
-                rec = np.empty(RECORD_DOUBLES)
-                rec[:36] = ke[e].numpy()
-                rec.view(np.int32)[72:80] = conn[e]
-                buckets[d].append(rec)
-        counts = [len(b) for b in buckets]
-        recs = [r for b in buckets for r in b]
-        records = torch.from_numpy(np.array(recs).reshape(-1, RECORD_DOUBLES)) if recs else \
-            torch.empty((0, RECORD_DOUBLES), dtype=torch.float64)
-        return records, counts
+    def halo_count(self, dm, bounds, world, rank):
+        from oracle import halo
+
+        return torch.from_numpy(halo.count(dm.conn.numpy(), bounds, world, rank)), None
+
+    def alloc_words(self, n):
+        return torch.empty(n, dtype=torch.int64)
+
+    def pointers(self, bases, offsets):
+        return [int(b) for b in bases], [int(o) for o in offsets]
+
+    def halo_pack(self, dm, ke, bounds, world, rank, ptrs, offsets, ws):
+        from oracle import halo
+
+        for d, chunk in enumerate(halo.pack(dm.conn.numpy(), ke.numpy(), bounds, world, rank)):
+            if chunk.size:
+                _words_at(ptrs[d] + 8 * offsets[d], chunk.size)[:] = chunk
+
+    def halo_unpack(self, recv, desc, bounds, world, rank, n_rec):
+        from oracle import halo
+
+        out = halo.unpack(recv.numpy(), desc, bounds, world, rank)
+        assert out.shape[0] == n_rec
+        return torch.from_numpy(out)
+
+    def digest(self, t, pos0, add=0):
+        from paper_1501_04784_b200.distributed import digest_words
+
+        v = digest_words(t.contiguous().numpy(), pos0, add)
+        return torch.tensor([np.uint64(v).astype(np.int64)], dtype=torch.int64)
 
     def assemble(self, segments, n_nodes, c_lo, c_hi):
         import oracle
@@ -97,8 +122,10 @@ def _worker(rank, world, port, kind, outdir):
         runner = ShardedBuild(_mesh(kind), rank, world, ops=OracleOps(), exchange=TorchExchange())
         res = runner.step()
         total = runner.global_nnz()
+        digest = runner.exchange.sum_(runner.block_digest())
         np.savez(Path(outdir) / f"rank{rank}.npz", col_ptr=res.col_ptr.numpy(), row_idx=res.row_idx.numpy(),
-                 vals=res.vals.numpy(), nnz_offset=res.nnz_offset, total=total)
+                 vals=res.vals.numpy(), nnz_offset=res.nnz_offset, total=total, digest=digest.numpy(),
+                 bounds=runner.bounds_np, xbytes=runner.exchange_bytes()["bytes"])
     finally:
         dist.destroy_process_group()
 
@@ -126,3 +153,9 @@ def test_gloo_sharded_build_bitwise_equal_to_reference(tmp_path, world, kind):
     assert all(int(b["total"]) == len(ri) for b in blocks)
     assert np.array_equal(col_ptr, cp) and np.array_equal(row_idx, ri)
     assert vals.tobytes() == vv.tobytes()
+    # every rank holds the same bounds, and the summed block digests are the whole matrix's
+    assert all(np.array_equal(b["bounds"], blocks[0]["bounds"]) for b in blocks)
+    from paper_1501_04784_b200.distributed import csc_digest
+
+    want = np.array(csc_digest(cp, ri, vv), dtype=np.uint64).astype(np.int64)
+    assert all(np.array_equal(b["digest"], want) for b in blocks)

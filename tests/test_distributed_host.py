@@ -1,0 +1,225 @@
+"""Host logic of the sharded build on CPU: nnz-balanced column bounds, the compact record format
+(oracle/halo.py restates hx_halo.cu), the exchange volume, the digest algebra and the P2P receive
+buffer mapping (with a fake native library, over gloo world_size 2)."""
+
+import ctypes
+import os
+import socket
+import sys
+from pathlib import Path
+from types import SimpleNamespace
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+from oracle import halo
+from paper_1501_04784_b200.distributed import (balanced_bounds, column_bounds, csc_digest, digest_words,
+                                               element_ranges, histogram_bins, p2p_offsets)
+from paper_1501_04784_b200.workloads import permuted_mesh, perturbed_mesh
+
+ROOT = Path(__file__).resolve().parent.parent
+
+
+def column_nnz(conn, n_nodes):
+    """Exact lower-CSC nnz per column (distinct (row, col) pairs, col = min)."""
+    conn = np.asarray(conn, dtype=np.int64)
+    r = np.maximum(conn[:, halo.PACK_I], conn[:, halo.PACK_J]).ravel()
+    c = np.minimum(conn[:, halo.PACK_I], conn[:, halo.PACK_J]).ravel()
+    key = np.unique(c * n_nodes + r)
+    return np.bincount(key // n_nodes, minlength=n_nodes)
+
+
+def block_imbalance(nnz_col, bounds):
+    per = np.array([nnz_col[bounds[r]:bounds[r + 1]].sum() for r in range(len(bounds) - 1)])
+    return per.max() / per.mean()
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_balanced_bounds_permuted_mesh(world):
+    """Permuted numbering: an equal node split is off by up to ~1.8x at G=8 (low ids own more
+    lower-triangle entries); the weight histogram brings max/mean block nnz to <= 1.05."""
+    mesh = permuted_mesh(perturbed_mesh(40, seed=1), seed=2)
+    nnz_col = column_nnz(mesh.connectivity, mesh.n_nodes)
+    hist = halo.column_weights(mesh.connectivity, mesh.n_nodes, histogram_bins(mesh.n_nodes))
+    b = balanced_bounds(hist, mesh.n_nodes, world)
+    assert b[0] == 0 and b[-1] == mesh.n_nodes and np.all(np.diff(b) > 0)
+    assert block_imbalance(nnz_col, b) <= 1.05
+    if world == 8:
+        assert block_imbalance(nnz_col, column_bounds(mesh.n_nodes, world)) > 1.5
+
+
+def test_balanced_bounds_structured_and_binned():
+    mesh = perturbed_mesh(30, seed=3)
+    nnz_col = column_nnz(mesh.connectivity, mesh.n_nodes)
+    for bins in (histogram_bins(mesh.n_nodes), 1000):  # per node, and binned (several nodes per bin)
+        hist = halo.column_weights(mesh.connectivity, mesh.n_nodes, bins)
+        b = balanced_bounds(hist, mesh.n_nodes, 8)
+        assert block_imbalance(nnz_col, b) <= 1.05
+
+
+def test_balanced_bounds_degenerate_inputs():
+    assert list(balanced_bounds(np.zeros(4, np.int64), 4, 4)) == [0, 1, 2, 3, 4]
+    b = balanced_bounds(np.array([100, 0, 0, 0, 0, 0, 0, 1]), 8, 4)  # all weight in bin 0
+    assert b[0] == 0 and b[-1] == 8 and np.all(np.diff(b) > 0)
+
+
+def test_column_weights_interior_is_exact_nnz():
+    """In the interior of a conforming hex mesh the 1/8-unit weights sum to 8 x the column nnz."""
+    from paper_1501_04784_b200.mesh import StructuredGridSpec, generate_cube_mesh
+
+    mesh = generate_cube_mesh(StructuredGridSpec(6, 6, 6))
+    nnz_col = column_nnz(mesh.connectivity, mesh.n_nodes)
+    w = halo.column_weights(mesh.connectivity, mesh.n_nodes, mesh.n_nodes)
+    ijk = np.stack(np.unravel_index(np.arange(mesh.n_nodes), (7, 7, 7)), axis=1)
+    interior = np.all((ijk >= 1) & (ijk <= 5), axis=1)
+    assert np.array_equal(w[interior], 8 * nnz_col[interior])
+
+
+@pytest.mark.parametrize("kind", ["structured", "permuted"])
+def test_halo_records_round_trip(kind):
+    """pack on every rank -> unpack on every receiver: each receiver gets, for every foreign element
+    touching its block, exactly the KE entries of its columns (ascending element order)."""
+    mesh = perturbed_mesh(7, seed=5)
+    if kind == "permuted":
+        mesh = permuted_mesh(mesh, seed=6)
+    world = 3
+    rng = np.random.default_rng(0)
+    ke = rng.standard_normal((mesh.n_el, 36))
+    hist = halo.column_weights(mesh.connectivity, mesh.n_nodes, histogram_bins(mesh.n_nodes))
+    bounds = balanced_bounds(hist, mesh.n_nodes, world)
+    ranges = element_ranges(mesh.n_el, world)
+    C = np.stack([halo.count(mesh.connectivity[lo:hi], bounds, world, r) for r, (lo, hi) in enumerate(ranges)])
+    chunks = [halo.pack(mesh.connectivity[lo:hi], ke[lo:hi], bounds, world, r) for r, (lo, hi) in enumerate(ranges)]
+    for s in range(world):
+        for d in range(world):
+            assert chunks[s][d].size == 4 * C[s, d, 0] + C[s, d, 1]
+    owner = halo.owners(mesh.connectivity, bounds)
+    for d in range(world):
+        recv = np.concatenate([chunks[s][d] for s in range(world)])
+        desc = np.zeros((world, 3), np.int64)
+        desc[:, 0] = np.concatenate([[0], np.cumsum([chunks[s][d].size for s in range(world)])[:-1]])
+        desc[:, 1:] = C[:, d, :]
+        rec = halo.unpack(recv, desc, bounds, world, d)
+        foreign = np.array([e for s, (lo, hi) in enumerate(ranges) if s != d for e in range(lo, hi)
+                            if (owner[e] == d).any()], dtype=np.int64)
+        assert rec.shape[0] == foreign.size
+        assert np.array_equal(rec.view(np.int32)[:, 72:80], mesh.connectivity[foreign])
+        m = halo.owned_mask(mesh.connectivity[foreign], bounds, d)
+        assert np.array_equal(rec[:, :36][m], ke[foreign][m]) and np.all(rec[:, :36][~m] == 0.0)
+
+
+def test_exchange_volume_permuted_g8():
+    """Compact records on a permuted mesh at G=8: <= 520 B per element crosses the network (40-word
+    element records would be ~4.6 records x 320 B = ~1,470 B/el)."""
+    mesh = permuted_mesh(perturbed_mesh(32, seed=0), seed=5)
+    world = 8
+    hist = halo.column_weights(mesh.connectivity, mesh.n_nodes, histogram_bins(mesh.n_nodes))
+    bounds = balanced_bounds(hist, mesh.n_nodes, world)
+    total = 0
+    records = 0
+    for r, (lo, hi) in enumerate(element_ranges(mesh.n_el, world)):
+        c = halo.count(mesh.connectivity[lo:hi], bounds, world, r)
+        total += 8 * int((4 * c[:, 0] + c[:, 1]).sum())
+        records += int(c[:, 0].sum())
+    assert records / mesh.n_el > 3.5
+    assert total / mesh.n_el <= 520
+
+
+def test_digest_is_additive_over_blocks():
+    rng = np.random.default_rng(1)
+    a = rng.integers(-2**62, 2**62, size=1000, dtype=np.int64)
+    whole = digest_words(a)
+    parts = (digest_words(a[:300], 0) + digest_words(a[300:], 300)) % 2**64
+    assert whole == parts
+    assert digest_words(a + 7) == digest_words(a, 0, 7)
+    b = a.copy()
+    b[500] ^= 1
+    assert digest_words(b) != whole
+    cp, ri, vv = np.array([0, 2, 3]), np.array([0, 1, 1]), np.array([1.0, -0.0, 2.0])
+    assert csc_digest(cp, ri, vv) != csc_digest(cp, ri, np.array([1.0, 0.0, 2.0]))  # sign of zero counts
+
+
+def test_p2p_offsets_match_all_to_all_layout():
+    chunk = np.array([[0, 5, 7], [3, 0, 2], [4, 1, 0]])
+    assert p2p_offsets(chunk, 0) == [0, 0, 0]
+    assert p2p_offsets(chunk, 1) == [0, 5, 7]
+    assert p2p_offsets(chunk, 2) == [3, 5, 9]
+
+
+class FakeIpcLib:
+    """hx_ipc_* stand-in: 'device memory' is host memory, a handle names the owning allocation."""
+
+    def __init__(self, rank):
+        self.rank, self.allocs, self.opened, self.closed, self.freed = rank, [], [], [], []
+        self.bufs = []
+
+    def hx_ipc_alloc(self, nbytes, ptr_ref, handle):
+        buf = ctypes.create_string_buffer(nbytes)
+        self.bufs.append(buf)
+        ptr_ref._obj.value = ctypes.addressof(buf)
+        tag = f"rank{self.rank}:{len(self.allocs)}".encode()
+        ctypes.memmove(handle, tag.ljust(64, b"\0"), 64)
+        self.allocs.append(tag)
+        return 0
+
+    def hx_ipc_open(self, handle, ptr_ref):
+        tag = handle.raw.rstrip(b"\0")
+        self.opened.append(tag)
+        ptr_ref._obj.value = 0x10000 + len(self.opened)
+        return 0
+
+    def hx_ipc_close(self, p):
+        self.closed.append(p.value)
+        return 0
+
+    def hx_ipc_free(self, p):
+        self.freed.append(p.value)
+        return 0
+
+
+def _p2p_worker(rank, world, port, outdir):
+    sys.path.insert(0, str(ROOT))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch.distributed as dist
+
+    from paper_1501_04784_b200 import distributed as X
+
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        fake = FakeIpcLib(rank)
+        ex = X.P2PExchange(device="cpu")
+        ex.N = SimpleNamespace(lib=lambda: fake, check=lambda rc, what: None, IPC_HANDLE_BYTES=64)
+        ex._ensure_capacity(100)            # first mapping: every rank allocates and opens the others
+        first = (list(fake.opened), list(ex.peers))
+        ex._ensure_capacity(50)             # fits everywhere: nothing happens
+        same = list(fake.opened)
+        ex._ensure_capacity(5000 if rank == 1 else 10)  # rank 1 grows -> every rank re-maps
+        np.save(Path(outdir) / f"p2p{rank}.npy", np.array(
+            [repr(first), repr(same), repr(list(fake.opened)), repr(fake.allocs), repr(fake.closed),
+             repr(list(ex.peers)), repr(ex.ptrs.tolist())], dtype=object), allow_pickle=True)
+    finally:
+        dist.destroy_process_group()
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def test_p2p_mapping_opens_peers_only_and_remaps_on_growth(tmp_path):
+    world = 2
+    mp.start_processes(_p2p_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True,
+                       start_method="spawn")
+    for r in range(world):
+        first, same, opened, allocs, closed, peers, ptrs = (eval(x) for x in np.load(tmp_path / f"p2p{r}.npy",
+                                                                                      allow_pickle=True))
+        other = 1 - r
+        assert first[0] == [f"rank{other}:0".encode()]          # only the peer's handle is opened
+        assert same == first[0]                                  # no re-map when nothing grows
+        # after rank 1 grew: rank 1 allocated again, everyone re-opened the (new) peer handle
+        assert opened[-1] == f"rank{other}:{1 if other == 1 else 0}".encode()
+        assert len(allocs) == (2 if r == 1 else 1)
+        assert len(closed) == 1                                  # the stale mapping was closed
+        assert peers == ptrs and len(peers) == world

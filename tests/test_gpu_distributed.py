@@ -57,3 +57,122 @@ def test_loopback_fused_send_bitwise(world, kind):
     cp, ri, vv = concat_blocks(run_loopback_p2p(mesh, world, lambda: CudaOps()))
     cp1, ri1, vv1 = single(mesh)
     assert bits_equal(cp, cp1) and bits_equal(ri, ri1) and bits_equal(vv, vv1)
+
+
+def _dev_mesh(mesh):
+    return D.DeviceMesh.from_host(mesh)
+
+
+@pytest.mark.parametrize("kind", ["structured", "permuted"])
+def test_column_weights_match_oracle(kind):
+    from oracle import halo
+    from paper_1501_04784_b200.distributed import histogram_bins
+
+    mesh = perturbed_mesh(11, seed=7)
+    if kind == "permuted":
+        mesh = permuted_mesh(mesh, seed=8)
+    ops = CudaOps()
+    dm = _dev_mesh(mesh)
+    for bins in (histogram_bins(mesh.n_nodes), 97, 20000 if mesh.n_nodes > 20000 else mesh.n_nodes):
+        got = ops.column_weights(dm, mesh.n_nodes, bins).cpu().numpy()
+        assert np.array_equal(got, halo.column_weights(mesh.connectivity, mesh.n_nodes, bins))
+
+
+def test_column_weights_global_atomics_path():
+    """> 16384 bins: the kernel accumulates in global memory instead of shared memory."""
+    from oracle import halo
+
+    mesh = permuted_mesh(perturbed_mesh(30, seed=1), seed=2)
+    ops = CudaOps()
+    got = ops.column_weights(_dev_mesh(mesh), mesh.n_nodes, 25000).cpu().numpy()
+    assert np.array_equal(got, halo.column_weights(mesh.connectivity, mesh.n_nodes, 25000))
+
+
+@pytest.mark.parametrize("world", [2, 3, 8])
+@pytest.mark.parametrize("kind", ["structured", "permuted"])
+def test_halo_pack_unpack_words_match_oracle(world, kind):
+    """hx_halo_count / hx_halo_pack / hx_halo_unpack word for word against oracle/halo.py."""
+    from oracle import halo
+    from paper_1501_04784_b200.distributed import balanced_bounds, element_ranges, histogram_bins
+
+    mesh = perturbed_mesh(9, seed=world)
+    if kind == "permuted":
+        mesh = permuted_mesh(mesh, seed=world + 3)
+    ops = CudaOps()
+    hist = halo.column_weights(mesh.connectivity, mesh.n_nodes, histogram_bins(mesh.n_nodes))
+    bounds = balanced_bounds(hist, mesh.n_nodes, world)
+    bdev = ops.bounds(bounds)
+    rng = np.random.default_rng(world)
+    ke = rng.standard_normal((mesh.n_el, 36))
+    ke[:, 3] = -0.0
+    for r, (lo, hi) in enumerate(element_ranges(mesh.n_el, world)):
+        dm = ops.upload(mesh.coords, mesh.connectivity[lo:hi], mesh.coefficient[lo:hi])
+        ke_d = torch.from_numpy(ke[lo:hi]).to(ops.device)
+        per_dest, ws = ops.halo_count(dm, bdev, world, r)
+        want = halo.count(mesh.connectivity[lo:hi], bounds, world, r)
+        assert np.array_equal(per_dest.cpu().numpy(), want)
+        chunks = 4 * want[:, 0] + want[:, 1]
+        send = ops.alloc_words(int(chunks.sum())).fill_(-7)
+        offs = np.concatenate([[0], np.cumsum(chunks)[:-1]])
+        ops.halo_pack(dm, ke_d, bdev, world, r, *ops.pointers([send.data_ptr()] * world, offs))
+        got = send.cpu().numpy()
+        for d, c in enumerate(halo.pack(mesh.connectivity[lo:hi], ke[lo:hi], bounds, world, r)):
+            assert np.array_equal(got[offs[d]:offs[d] + chunks[d]], c)
+        # this rank's chunks, unpacked by each receiver as if it were the only source
+        for d in range(world):
+            if d == r or chunks[d] == 0:
+                continue
+            desc = np.zeros((world, 3), np.int64)
+            desc[r] = (offs[d], want[d, 0], want[d, 1])
+            recs = ops.halo_unpack(send, desc, bdev, world, d, int(want[d, 0])).cpu().numpy()
+            ref = halo.unpack(got, desc, bounds, world, d)
+            assert recs.tobytes() == ref.tobytes()
+
+
+def test_digest_matches_host_restatement():
+    from paper_1501_04784_b200.distributed import digest_words
+
+    ops = CudaOps()
+    rng = np.random.default_rng(3)
+    a = rng.standard_normal(100_003)
+    t = torch.from_numpy(a).to(ops.device)
+    got = int(np.int64(ops.digest(t, 12345, 99).item()).astype(np.uint64))
+    assert got == digest_words(a, 12345, 99)
+
+
+@pytest.mark.parametrize("world", [2, 8])
+def test_block_digests_sum_to_single_gpu_digest(world):
+    from paper_1501_04784_b200.distributed import csc_digest
+
+    mesh = permuted_mesh(perturbed_mesh(10, seed=4), seed=6)
+    results = run_loopback(mesh, world, lambda: CudaOps())
+    cp, ri, vv = single(mesh)
+    want = csc_digest(cp, ri, vv)
+    # recompute block digests the way ShardedBuild.block_digest does
+    ops = CudaOps()
+    tot = np.zeros(3, dtype=np.uint64)
+    for r, res in enumerate(results):
+        ncols = res.col_hi - res.col_lo
+        d = [ops.digest(res.col_ptr[:ncols], res.col_lo, res.nnz_offset)]
+        if r == world - 1:
+            d[0] = d[0] + ops.digest(res.col_ptr[ncols:], mesh.n_nodes, res.nnz_offset)
+        d += [ops.digest(res.row_idx, res.nnz_offset), ops.digest(res.vals, res.nnz_offset)]
+        with np.errstate(over="ignore"):
+            tot += np.array([int(np.int64(x.item()).astype(np.uint64)) for x in d], dtype=np.uint64)
+    assert tuple(int(x) for x in tot) == want
+
+
+def test_loopback_bad_node_id_raises_node_index_error():
+    from paper_1501_04784_b200.errors import MeshValidationError, NodeIndexError
+
+    mesh = perturbed_mesh(6, seed=1)
+    conn = mesh.connectivity.copy()
+    conn[150, 3] = mesh.n_nodes + 5
+    conn[20, 1] = -1  # element 20 < 150: reported
+    from paper_1501_04784_b200.mesh import Mesh
+
+    bad = Mesh(coords=mesh.coords, connectivity=conn, coefficient=mesh.coefficient)
+    with pytest.raises(NodeIndexError) as ei:
+        run_loopback(bad, 3, lambda: CudaOps())
+    assert ei.value.element_id == 20 and ei.value.node == -1
+    assert isinstance(ei.value, MeshValidationError) and isinstance(ei.value, IndexError)

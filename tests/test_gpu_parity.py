@@ -781,3 +781,103 @@ def test_compact_host_transfer_empty_block():
     xfer.close()
     assert got.row_idx.shape == (0,) and got.vals.shape == (0,) and got.row_idx.dtype == np.int64
     assert np.array_equal(got.col_ptr, np.zeros(6, np.int64))
+
+
+@pytest.mark.parametrize("node", ["big", "negative"])
+def test_unfused_paths_bad_node_id_raise_node_index_error(node):
+    """Every integration entry point refuses out-of-range node ids without dereferencing them:
+    integrate_all (CudaBackend, the reference raises IndexError at staging, integrate.py:146-149),
+    build_device with element groups / overlap, run_build and the out-of-core blocks.  The lowest
+    such element wins over a degenerate one (the reference fails at staging, before computing)."""
+    from paper_1501_04784_b200 import NodeIndexError
+    from paper_1501_04784_b200.pipeline import build_out_of_core
+
+    mesh = perturbed_mesh(5, seed=3)
+    conn = mesh.connectivity.copy()
+    bad_id = mesh.n_nodes + 10**6 if node == "big" else -3
+    conn[77, 5] = bad_id
+    conn[90, 2] = mesh.n_nodes  # a later bad element
+    conn[10] = conn[10][[4, 5, 6, 7, 0, 1, 2, 3]]  # degenerate (flipped), lower id: still loses
+    bad = Mesh(mesh.coords, conn, mesh.coefficient)
+
+    def check(exc):
+        assert exc.element_id == 77 and exc.node == bad_id
+        assert isinstance(exc, IndexError) and isinstance(exc, MeshValidationError)
+
+    with CudaBackend() as be:
+        for plan in (one_group(bad), plan_batches(required_bytes(bad.n_el), required_bytes(40), bad.n_el)):
+            with pytest.raises(NodeIndexError) as ei:
+                integrate_all(bad, be, plan)
+            if plan.group_count == 1:
+                check(ei.value)
+            else:  # groups run in order: the group holding element 77 fails first
+                assert ei.value.element_id == 77
+    dm = D.DeviceMesh.from_host(bad)
+    for kw in ({"ranges": [(0, 60), (60, 125)]}, {"overlap": True}, {}):
+        with pytest.raises(NodeIndexError) as ei:
+            build_device(dm, **kw)
+        check(ei.value)
+    with pytest.raises(NodeIndexError) as ei:
+        run_build(bad, budget_bytes=10**12)
+    check(ei.value)
+    with pytest.raises(NodeIndexError) as ei:
+        build_out_of_core(bad, 3)
+    check(ei.value)
+
+
+def test_cuda_backend_sees_in_place_changes():
+    """integrate_all uploads the mesh per call: changing the caller's arrays in place between
+    calls (same objects, same ids) is always seen -- the reference backend is stateless."""
+    mesh = perturbed_mesh(4, seed=5)
+    coords = mesh.coords.copy()
+    coeff = mesh.coefficient.copy()
+    m = Mesh(coords, mesh.connectivity, coeff)
+    with CudaBackend() as be:
+        a = integrate_all(m, be, one_group(m)).values.copy()
+        coeff *= 2.0
+        coords[:] = coords * 1.5
+        b = integrate_all(m, be, one_group(m)).values
+    ke, _, _, first, _, _ = oracle.stiffness_mesh(coords, m.connectivity, coeff)
+    assert first == -1 and bits_equal(b, ke) and not bits_equal(a, b)
+
+
+def test_integrate_all_pipelined_groups_many_plans():
+    """Two groups in flight (pinned staging, one stream): every plan, both modes, bitwise."""
+    mesh = permuted_mesh(perturbed_mesh(9, seed=2), seed=4)
+    ke, _, _, _, _, _ = oracle.stiffness_mesh(mesh.coords, mesh.connectivity, mesh.coefficient)
+    seen = []
+    with CudaBackend() as be:
+        for groups in (1, 2, 3, 7, 64):
+            plan = plan_batches(groups * required_bytes(mesh.n_el // groups + 1), required_bytes(mesh.n_el // groups + 1),
+                                mesh.n_el)
+            for mode in ("sequential", "overlapped"):
+                seen.clear()
+                got = integrate_all(mesh, be, plan, mode=mode,
+                                    consumer=lambda r, v: seen.append((r, v.copy())))
+                assert bits_equal(got.values, ke)
+                assert [r for r, _ in seen] == list(plan.ranges)
+                assert all(bits_equal(v, ke[lo:hi]) for (lo, hi), v in seen)
+
+
+def test_host_transfer_of_planned_rebuilds_not_overwritten():
+    """A verified plan reuses its output buffers; the next emit waits for a pending host copy of
+    the previous result instead of overwriting it (DeviceCsc.readers)."""
+    from paper_1501_04784_b200.transfer import CscHostTransfer
+
+    mesh = perturbed_mesh(12, seed=6)
+    dm = D.DeviceMesh.from_host(mesh)
+    plan = D.plan_assembly(dm)
+    xfer = CscHostTransfer(mesh.n_nodes, plan.nnz, depth=2, threads=2)
+    futs, want = [], []
+    for k in range(4):
+        dm.coeff.mul_(2.0)  # exact: the host restatement scales by 2**(k+1)
+        b = build_device(dm, plan=plan)
+        futs.append(xfer.submit(b.csc))
+        ke, rows, cols, _, _, _ = oracle.stiffness_mesh(mesh.coords, mesh.connectivity,
+                                                        mesh.coefficient * 2.0 ** (k + 1))
+        want.append(oracle.triplet_to_csc(rows, cols, ke.reshape(-1), mesh.n_nodes)[2])
+        if k % 2 == 1:
+            for f, w in zip(futs, want):
+                assert bits_equal(f.result().vals, w)
+            futs, want = [], []
+    xfer.close()
