@@ -19,4 +19,5 @@ from .oracle import (  # noqa: F401
     stiffness_batch,
     stiffness_mesh,
     triplet_to_csc,
+    triplet_to_csc_columns,
 )

@@ -139,6 +139,32 @@ def triplet_to_csc(rows, cols, vals, dim):
     return col_ptr, row_idx, summed
 
 
+def triplet_to_csc_columns(rows, cols, vals, col_lo, col_hi):
+    """assemble.py:110-140 on a column window: the triplets whose column lies in [col_lo, col_hi)
+    (given in the reference's element-major order), the same stable lexsort by (col, row) and
+    add.reduceat; col_ptr covers only the window (starts at 0).  Equal to the window of the
+    full triplet_to_csc because the stable sort keeps every column's triplets in input order."""
+    rows = np.asarray(rows)
+    cols = np.asarray(cols)
+    vals = np.asarray(vals, dtype=np.float64)
+    n = col_hi - col_lo
+    if rows.size == 0:
+        return np.zeros(n + 1, dtype=np.int64), np.empty(0, dtype=np.int64), np.empty(0)
+    assert cols.min() >= col_lo and cols.max() < col_hi and (rows >= cols).all()
+    order = np.lexsort((rows, cols))
+    r = rows[order]
+    c = cols[order]
+    v = vals[order]
+    is_start = np.empty(r.shape[0], dtype=bool)
+    is_start[0] = True
+    is_start[1:] = (r[1:] != r[:-1]) | (c[1:] != c[:-1])
+    starts = np.flatnonzero(is_start)
+    summed = np.add.reduceat(v, starts)
+    col_ptr = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(np.bincount(c[starts] - col_lo, minlength=n), out=col_ptr[1:])
+    return col_ptr, r[starts].astype(np.int64), summed
+
+
 def pairwise_sum(a):
     """Pure-Python model of numpy's pairwise summation (numpy/_core/src/umath/loops_utils.h.src
     ``@TYPE@_pairwise_sum``), used to pin the rule the GPU numeric phase implements."""

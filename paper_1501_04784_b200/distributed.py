@@ -641,13 +641,23 @@ class ShardedBuild:
 # ------------------------------------------------------------------------------------------
 # loopback: G virtual ranks in one process (tests the CUDA sharded path on one GPU)
 # ------------------------------------------------------------------------------------------
+class LoopbackExchange:
+    """Placeholder exchange of the in-process drivers (they move the chunks themselves)."""
+
+    p2p = False
+
+    def __getattr__(self, name):
+        raise NotImplementedError(f"loopback ranks have no collective {name!r}: use run_loopback")
+
+
 def _loopback_ranks(mesh, world, ops_factory):
     ops0 = ops_factory()
     whole = ops0.upload(mesh.coords, mesh.connectivity, mesh.coefficient)
     hist = ops0.column_weights(whole, mesh.n_nodes, histogram_bins(mesh.n_nodes))
     bounds = balanced_bounds(hist.cpu().numpy(), mesh.n_nodes, world)
     del whole
-    ranks = [ShardedBuild(mesh, r, world, ops=ops_factory(), exchange=None, bounds=bounds) for r in range(world)]
+    ranks = [ShardedBuild(mesh, r, world, ops=ops_factory(), exchange=LoopbackExchange(), bounds=bounds)
+             for r in range(world)]
     meta = np.stack([rk.phase_local().cpu().numpy() for rk in ranks])
     C = ranks[0].check_meta(meta)
     return ranks, C, 4 * C[:, :, 0] + C[:, :, 1]

@@ -258,13 +258,64 @@ def build_out_of_core(mesh, n_blocks: int, mode: str = "exact", device=None, ret
     return matrix, values, {"time_integration_s": t_int, "time_assembly_s": t_asm, "blocks": n_blocks}
 
 
+# run_build uploads the connectivity in this many element ranges (meshes of at least
+# UPLOAD_RANGES_MIN_ELEMENTS elements), so the integration of range k overlaps the copy of range k+1
+UPLOAD_RANGES = 8
+UPLOAD_RANGES_MIN_ELEMENTS = 1 << 22
+
+
+def _host_tensor(a, dtype):
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=dtype))
+
+
+def upload_overlapped(mesh, dev, chunks: int, stream=None):
+    """Host mesh -> DeviceMesh on the copy stream: coordinates first, then the connectivity and
+    coefficients in ``chunks`` element ranges, one event per range.  Pinned host arrays (hostmem)
+    copy asynchronously, so the integration of range k can start while range k+1 is in flight;
+    pageable arrays are staged by the driver (the copy blocks the host).  Returns (dm, [(lo, hi,
+    event)]); the consumer stream must wait on each event before reading its range."""
+    from .transfer import copy_stream
+
+    main = torch.cuda.current_stream(dev) if stream is None else stream
+    n = mesh.n_el
+    coords_h, conn_h, coeff_h = (_host_tensor(mesh.coords, np.float64), _host_tensor(mesh.connectivity, np.int32),
+                                 _host_tensor(mesh.coefficient, np.float64))
+    dm = D.DeviceMesh(torch.empty(tuple(coords_h.shape), dtype=torch.float64, device=dev),
+                      torch.empty(tuple(conn_h.shape), dtype=torch.int32, device=dev),
+                      torch.empty(tuple(coeff_h.shape), dtype=torch.float64, device=dev))
+    copy = copy_stream(dev)
+    copy.wait_stream(main)  # the buffers' allocation (and anything the caller queued before)
+    parts = []
+    with torch.cuda.stream(copy):
+        dm.coords.copy_(coords_h, non_blocking=True)
+        k = max(1, min(chunks, n))
+        for i in range(k):
+            lo, hi = n * i // k, n * (i + 1) // k
+            dm.conn[lo:hi].copy_(conn_h[lo:hi], non_blocking=True)
+            dm.coeff[lo:hi].copy_(coeff_h[lo:hi], non_blocking=True)
+            parts.append((lo, hi, copy.record_event()))
+        if not parts:
+            parts.append((0, 0, copy.record_event()))
+    return dm, parts
+
+
 def run_build(mesh, budget_bytes: int, workers: int = 1, mode: str = "sequential", assembler: str = "direct",
               integration: str = "exact", device=None, device_budget_bytes: int | None = None):
-    """Integrate and assemble one mesh on the GPU; returns (LowerCscMatrix, BuildReport).
+    """cli.py:65-149 run_build on the GPU: integrate and assemble one host mesh, return the host
+    (LowerCscMatrix, BuildReport) with the reference's dtypes and report fields.
+
+    One call = mesh upload + KE (+ fused iK/jK and the assembly's node adjacency) + lower CSC +
+    transfer back.  The connectivity uploads in element ranges on the copy stream while the
+    integration kernel consumes the ranges already in HBM (asynchronous when the mesh is in pinned
+    memory, ``hostmem.pinned_mesh``); the CSC returns through ``transfer.fetch_csc`` (int32 rows over
+    PCIe, widened on the host cores chunk by chunk while the values are still in flight).  Stage
+    times come from CUDA events; the host clock brackets the whole call.
 
     ``device_budget_bytes``: HBM the build may use.  When the in-core footprint (device_bytes)
     exceeds it, the matrix is built in ceil(footprint / budget) column blocks (build_out_of_core).
     """
+    from .transfer import fetch_csc
+
     if assembler not in ("direct", "triplet"):
         raise ConfigurationError(f"assembler must be 'direct' or 'triplet', got {assembler!r}")
     if mode not in ("sequential", "overlapped"):
@@ -273,36 +324,50 @@ def run_build(mesh, budget_bytes: int, workers: int = 1, mode: str = "sequential
         raise ConfigurationError(f"worker count must be at least 1, got {workers}")
     plan = plan_batches(required_bytes(mesh.n_el), budget_bytes, mesh.n_el)
     dev = D.require_device(device)
-    need = device_bytes(mesh.n_el, mesh.n_nodes, with_index=assembler == "triplet")
+    with_index = assembler == "triplet"
+    need = device_bytes(mesh.n_el, mesh.n_nodes, with_index=with_index)
     if device_budget_bytes is not None and need > device_budget_bytes:
         return _run_build_blocks(mesh, plan, -(-need // device_budget_bytes), workers, mode, assembler, integration,
                                  dev)
     wall0 = time.perf_counter()
     with torch.cuda.device(dev):
-        dm = D.DeviceMesh.from_host(mesh, dev)
-        ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
-        ev[0].record()
+        main = torch.cuda.current_stream(dev)
         n = mesh.n_el
-        with_index = assembler == "triplet"
+        # upload ranges: enough to overlap the connectivity copy with the integration kernel
+        chunks = UPLOAD_RANGES if n >= UPLOAD_RANGES_MIN_ELEMENTS else 1
+        dm, parts = upload_overlapped(mesh, dev, chunks, stream=main)
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
         ke = torch.empty((n, 36), dtype=torch.float64, device=dev)
         rows = torch.empty(36 * n, dtype=torch.int32, device=dev) if with_index else None
         cols = torch.empty(36 * n, dtype=torch.int32, device=dev) if with_index else None
+        fuse = 0 < n and 8 * n < 2**31 - 1 and os.environ.get("HX_FUSED_ADJACENCY", "1") != "0"
+        prep = D.new_assembly_prep(dm) if fuse else None
+        main.wait_event(parts[0][2])  # the coordinates (and the first range)
+        ev[0].record(main)
         fails = []
-        for lo, hi in plan.ranges:
-            _, _, _, fail = D.integrate_mesh(dm, lo, hi, ke=ke[lo:hi],
-                                             rows=rows[36 * lo:36 * hi] if with_index else None,
-                                             cols=cols[36 * lo:36 * hi] if with_index else None,
-                                             with_index=with_index, mode=integration)
-            fails.append(fail)
-        ev[1].record()
+        for lo, hi, landed in parts:
+            main.wait_event(landed)
+            if hi > lo:
+                _, _, _, fail = D.integrate_mesh(dm, lo, hi, ke=ke[lo:hi],
+                                                 rows=rows[36 * lo:36 * hi] if with_index else None,
+                                                 cols=cols[36 * lo:36 * hi] if with_index else None,
+                                                 with_index=with_index, mode=integration, stream=main,
+                                                 adjacency=prep)
+                fails.append(fail)
+        ev[1].record(main)
+        try:
+            csc = D.mesh_csc([(dm.conn, ke)], dm.n_nodes, stream=main, order=dm.assembly_order(), prep=prep)
+        except MeshValidationError:
+            for f in fails:  # an out-of-range node id is the element's NodeIndexError
+                D.raise_if_failed(f, n_nodes=dm.n_nodes)
+            raise
         for f in fails:
             D.raise_if_failed(f, n_nodes=dm.n_nodes)
-        csc = D.mesh_csc([(dm.conn, ke)], dm.n_nodes)
-        ev[2].record()
-        matrix: LowerCscMatrix = csc_to_host(csc)
-        torch.cuda.synchronize(dev)
+        ev[2].record(main)
+        matrix: LowerCscMatrix = fetch_csc(csc, stream=main)
         time_integration = ev[0].elapsed_time(ev[1]) / 1e3
         time_assembly = ev[1].elapsed_time(ev[2]) / 1e3
+        del dm, ke, rows, cols, csc, prep
     time_total = time.perf_counter() - wall0
     nnz_triplet = 36 * mesh.n_el
     trip_mb = triplet_memory(nnz_triplet)

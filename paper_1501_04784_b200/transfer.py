@@ -26,7 +26,7 @@ from . import _native as N
 from . import device as D
 from .assemble import LowerCscMatrix
 
-__all__ = ["CscHostTransfer", "host_threads"]
+__all__ = ["CscHostTransfer", "host_threads", "fetch_csc"]
 
 
 def host_threads() -> int:
@@ -116,3 +116,54 @@ class CscHostTransfer:
             if s.pending is not None:
                 s.pending.result()
         self.pool.shutdown()
+
+
+_COPY_STREAMS: dict = {}
+
+
+def copy_stream(dev) -> torch.cuda.Stream:
+    """The device's host-transfer stream (one per device, shared by fetch_csc and uploads)."""
+    key = torch.device(dev).index
+    if key not in _COPY_STREAMS:
+        _COPY_STREAMS[key] = torch.cuda.Stream(device=dev)
+    return _COPY_STREAMS[key]
+
+
+def fetch_csc(csc: D.DeviceCsc, stream=None, threads: int | None = None, chunk: int = 1 << 25) -> LowerCscMatrix:
+    """Device lower CSC -> host LowerCscMatrix (reference dtypes) for one synchronous call.
+
+    Row indices cross as int32 (hx_rows_narrow) in chunks interleaved with the value chunks on the
+    copy stream; each row chunk is sign-extended to int64 by the host cores (hx_rows_widen) as soon
+    as it lands, while the next chunks are in flight, so only the last chunk's widening is exposed.
+    Outputs are pinned arrays from torch's caching host allocator (recycled when dropped)."""
+    dev = csc.row_idx.device
+    producer = torch.cuda.current_stream(dev) if stream is None else stream
+    copy = copy_stream(dev)
+    n = csc.nnz
+    threads = host_threads() if threads is None else int(threads)
+    col_ptr = torch.empty(csc.col_ptr.shape[0], dtype=torch.int64, pin_memory=True)
+    vals = torch.empty(n, dtype=torch.float64, pin_memory=True)
+    row_idx = torch.empty(n, dtype=torch.int64, pin_memory=True)
+    rows32 = torch.empty(max(n, 1), dtype=torch.int32, pin_memory=True)
+    narrow = D.rows_narrow(csc.row_idx, stream=producer) if n else None
+    copy.wait_event(producer.record_event())
+    landed = []
+    with torch.cuda.stream(copy):
+        col_ptr.copy_(csc.col_ptr, non_blocking=True)
+        for lo in range(0, n, chunk):
+            hi = min(n, lo + chunk)
+            rows32[lo:hi].copy_(narrow[lo:hi], non_blocking=True)
+            landed.append((lo, hi, copy.record_event()))
+            vals[lo:hi].copy_(csc.vals[lo:hi], non_blocking=True)
+        done = copy.record_event()
+        for t in (narrow, csc.row_idx, csc.vals, csc.col_ptr):
+            if t is not None:
+                t.record_stream(copy)
+    if csc.readers is not None:
+        csc.readers.append(done)
+    base32, base64 = rows32.data_ptr(), row_idx.data_ptr()
+    for lo, hi, ev in landed:
+        ev.synchronize()
+        N.check(N.lib().hx_rows_widen(base32 + 4 * lo, base64 + 8 * lo, hi - lo, threads), "hx_rows_widen")
+    done.synchronize()
+    return LowerCscMatrix(col_ptr=col_ptr.numpy(), row_idx=row_idx.numpy(), vals=vals.numpy(), dim=csc.dim)

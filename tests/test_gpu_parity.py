@@ -3,6 +3,8 @@
 Bar: bit-exact for indices and (exact mode) values.
 """
 
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -238,7 +240,7 @@ def test_mesh_assembly_random_values_random_numbering():
         assert bits_equal(m.col_ptr, cp) and bits_equal(m.row_idx, ri) and bits_equal(m.vals, vv)
 
 
-@pytest.mark.parametrize("config", ["C1", "C2", "P64", "C3"])
+@pytest.mark.parametrize("config", ["C1", "C2", "P64", "C3", "C5"])
 def test_full_pipeline_matches_reference_digests(digests, config):
     d = digests["configs"][config]
     if config == "P64":
@@ -557,35 +559,64 @@ def test_fast_path_row_limits_fall_back_bitwise(shared):
     assert bits_equal(m.col_ptr, cp) and bits_equal(m.row_idx, ri) and bits_equal(m.vals, vv)
 
 
-@pytest.mark.parametrize("config", ["C4", "C5"])
-def test_full_size_column_windows_bitwise(config):
-    """Full-size builds (C4: 64M elements in one GPU, C5: 16.8M permuted) checked bit for bit on
-    column windows: the oracle assembles exactly the elements incident to a window of columns
-    (KE in reference order, triplets of those columns, numpy lexsort + reduceat) and the GPU's
-    columns, rows, values and KE rows must match -- a size-independent parity check at the
-    BASELINE sizes the golden digests cannot reach."""
-    mesh = make_workload(config)
+_C4 = {}
+
+
+def _c4_block(bounds):
+    """One column block of the C4 check, run in a forked worker (numpy only, no CUDA): the
+    reference algorithm on the elements touching the block, compared with the GPU's block."""
+    c0, c1 = bounds
+    g = _C4
+    conn = g["conn"]
+    cand = np.flatnonzero((g["emin"] < c1) & (g["emax"] >= c0))
+    sub = conn[cand]
+    touch = cand[((sub >= c0) & (sub < c1)).any(axis=1)]  # ascending element ids
+    c = conn[touch]
+    r = np.maximum(c[:, oracle.PACK_ROWS], c[:, oracle.PACK_COLS]).reshape(-1)
+    k = np.minimum(c[:, oracle.PACK_ROWS], c[:, oracle.PACK_COLS]).reshape(-1)
+    keep = (k >= c0) & (k < c1)
+    cp, ri, vv = oracle.triplet_to_csc_columns(r[keep], k[keep], g["ke"][touch].reshape(-1)[keep], c0, c1)
+    gcp = g["col_ptr"][c0:c1 + 1]
+    a, z = int(gcp[0]), int(gcp[-1])
+    return (np.array_equal(gcp - a, cp), np.array_equal(g["row_idx"][a:z], ri),
+            np.array_equal(g["vals"][a:z].view(np.int64), vv.view(np.int64)))
+
+
+@pytest.mark.slow
+def test_c4_every_column_bitwise_against_oracle():
+    """C4 (400^3, 64M elements) checked whole: the oracle's KE for every element (C, all host
+    cores), iK/jK for every element, and every column of the lower CSC assembled by the reference
+    algorithm (numpy lexsort + add.reduceat) in 32 column blocks on forked host workers -- bitwise
+    against the single-GPU build (replaces round 1's three 4000-column windows)."""
+    import multiprocessing as mp
+
+    mesh = make_workload("C4")
     dm = D.DeviceMesh.from_host(mesh)
     b = build_device(dm)
-    n = mesh.n_nodes
-    col_ptr = b.csc.col_ptr
-    for lo in (0, n // 2 - 2000, n - 4000):
-        hi = lo + 4000
-        # elements with a node in [lo, hi), ascending (the reference's stable order within a column)
-        touch = np.flatnonzero(((mesh.connectivity >= lo) & (mesh.connectivity < hi)).any(axis=1))
-        conn = mesh.connectivity[touch]
-        ke, rows, cols, first, _, _ = oracle.stiffness_mesh(mesh.coords, conn, mesh.coefficient[touch])
-        assert first == -1
-        assert bits_equal(b.ke[torch.from_numpy(touch).cuda()].cpu().numpy(), ke)
-        keep = (cols >= lo) & (cols < hi)
-        cp, ri, vv = oracle.triplet_to_csc(rows[keep], cols[keep], ke.reshape(-1)[keep], n)
-        gcp = col_ptr[lo:hi + 1].cpu().numpy()
-        a, z = int(gcp[0]), int(gcp[-1])
-        assert bits_equal(gcp - a, cp[lo:hi + 1] - cp[lo])
-        assert bits_equal(b.csc.row_idx[a:z].cpu().numpy(), ri)
-        assert bits_equal(b.csc.vals[a:z].cpu().numpy(), vv)
+    torch.cuda.synchronize()
+    ke_o, _, _, first, _, _ = oracle.stiffness_mesh(mesh.coords, mesh.connectivity, mesh.coefficient,
+                                                    with_index=False)
+    assert first == -1
+    step = 1 << 23
+    for lo in range(0, mesh.n_el, step):  # KE and the fused iK/jK, element chunks
+        hi = min(lo + step, mesh.n_el)
+        assert np.array_equal(b.ke[lo:hi].cpu().numpy().view(np.int64), ke_o[lo:hi].view(np.int64))
+        r, k = oracle.connectivity_index_arrays(mesh.connectivity, lo, hi)
+        assert np.array_equal(b.rows[36 * lo:36 * hi].cpu().numpy(), r)
+        assert np.array_equal(b.cols[36 * lo:36 * hi].cpu().numpy(), k)
+    _C4.update(conn=mesh.connectivity, ke=ke_o, emin=mesh.connectivity.min(axis=1), emax=mesh.connectivity.max(axis=1),
+               col_ptr=b.csc.col_ptr.cpu().numpy(), row_idx=b.csc.row_idx.cpu().numpy(), vals=b.csc.vals.cpu().numpy())
+    assert int(_C4["col_ptr"][-1]) == b.csc.nnz == 898_402_401
     del b, dm
     torch.cuda.empty_cache()
+    n = mesh.n_nodes
+    blocks = [(n * i // 32, n * (i + 1) // 32) for i in range(32)]
+    try:
+        with mp.get_context("fork").Pool(min(16, os.cpu_count() or 1)) as pool:
+            results = pool.map(_c4_block, blocks)
+    finally:
+        _C4.clear()
+    assert all(all(r) for r in results), [i for i, r in enumerate(results) if not all(r)]
 
 
 def test_empty_and_single_element_meshes():
@@ -881,3 +912,29 @@ def test_host_transfer_of_planned_rebuilds_not_overwritten():
                 assert bits_equal(f.result().vals, w)
             futs, want = [], []
     xfer.close()
+
+
+@pytest.mark.parametrize("pinned", [False, True])
+@pytest.mark.parametrize("assembler", ["direct", "triplet"])
+def test_run_build_overlapped_upload_bitwise(monkeypatch, pinned, assembler):
+    """run_build's element-range upload (copy stream, one event per range, integration chasing the
+    copies) and fetch_csc's chunked int32 transfer + host widening: bitwise the oracle, pinned or
+    pageable host arrays, many ranges and many transfer chunks."""
+    from paper_1501_04784_b200 import pipeline, transfer
+    from paper_1501_04784_b200.hostmem import is_pinned, pinned_mesh
+
+    monkeypatch.setattr(pipeline, "UPLOAD_RANGES_MIN_ELEMENTS", 1)
+    monkeypatch.setattr(pipeline, "UPLOAD_RANGES", 7)
+    mesh = permuted_mesh(perturbed_mesh(13, seed=8), seed=9)
+    if pinned:
+        mesh = pinned_mesh(mesh)
+        assert is_pinned(mesh.connectivity)
+    ke, rows, cols, _, _, _ = oracle.stiffness_mesh(mesh.coords, mesh.connectivity, mesh.coefficient)
+    cp, ri, vv = oracle.triplet_to_csc(rows, cols, ke.reshape(-1), mesh.n_nodes)
+    orig = transfer.fetch_csc
+    monkeypatch.setattr(transfer, "fetch_csc", lambda csc, stream=None: orig(csc, stream=stream, chunk=1000))
+    for _ in range(2):
+        m, rep = run_build(mesh, budget_bytes=10**12, assembler=assembler)
+        assert m.col_ptr.dtype == np.int64 and m.row_idx.dtype == np.int64 and m.vals.dtype == np.float64
+        assert bits_equal(m.col_ptr, cp) and bits_equal(m.row_idx, ri) and bits_equal(m.vals, vv)
+        assert rep.nnz_csc == len(ri) and rep.time_total_s > 0

@@ -86,3 +86,22 @@ def test_oracle_matches_reference_digests(digests, config):
     col_ptr, row_idx, vals = oracle.triplet_to_csc(rows, cols, ke.reshape(-1), mesh.n_nodes)
     assert len(row_idx) == d["nnz"]
     assert sha(col_ptr) == d["col_ptr"] and sha(row_idx) == d["row_idx"] and sha(vals) == d["vals"]
+
+
+def test_column_window_restatement_equals_full_assembly(golden):
+    """oracle.triplet_to_csc_columns (the reference algorithm on a column window, used by the C4
+    every-column GPU check) == the window of the full triplet_to_csc, on the reference's outputs."""
+    for name in ("perm5", "m345"):
+        conn, ke = golden[f"{name}_conn"], golden[f"{name}_ke"]
+        cp, ri, vv = golden[f"{name}_col_ptr"], golden[f"{name}_row_idx"], golden[f"{name}_vals"]
+        n = cp.shape[0] - 1
+        for c0, c1 in ((0, n // 3), (n // 3, n // 2), (n // 2, n)):
+            touch = np.flatnonzero(((conn >= c0) & (conn < c1)).any(axis=1))
+            c = conn[touch]
+            r = np.maximum(c[:, oracle.PACK_ROWS], c[:, oracle.PACK_COLS]).reshape(-1)
+            k = np.minimum(c[:, oracle.PACK_ROWS], c[:, oracle.PACK_COLS]).reshape(-1)
+            keep = (k >= c0) & (k < c1)
+            a, b, v = oracle.triplet_to_csc_columns(r[keep], k[keep], ke[touch].reshape(-1)[keep], c0, c1)
+            assert np.array_equal(a, cp[c0:c1 + 1] - cp[c0])
+            assert np.array_equal(b, ri[cp[c0]:cp[c1]])
+            assert v.tobytes() == vv[cp[c0]:cp[c1]].tobytes()
