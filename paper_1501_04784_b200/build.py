@@ -19,7 +19,7 @@ OBJ = PKG / "_lib" / "obj"
 LIB = PKG / "_lib" / "libhexfem_b200.so"
 INCLUDE = PKG.parent / "include"
 
-SOURCES = ["hx_abi.cu", "hx_ke.cu", "hx_assemble.cu", "hx_triplet.cu", "hx_shard.cu", "hx_halo.cu", "hx_mmio.cu", "hx_transfer.cu"]
+SOURCES = ["hx_abi.cu", "hx_ke.cu", "hx_assemble.cu", "hx_triplet.cu", "hx_shard.cu", "hx_halo.cu", "hx_mmio.cu", "hx_transfer.cu", "hx_host.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
               "-Xptxas", "-warn-spills", f"-I{INCLUDE}"]

@@ -8,9 +8,6 @@
 // while the next build's transfers run.  12 bytes per entry instead of 16; values and col_ptr cross
 // unchanged.
 #include <algorithm>
-#include <atomic>
-#include <thread>
-#include <vector>
 
 #include "hx_common.cuh"
 
@@ -77,28 +74,4 @@ extern "C" int hx_rows_narrow(const int64_t *row_idx, int32_t *rows32, int64_t n
     return HX_OK;
 }
 
-extern "C" int hx_rows_widen(const int32_t *rows32, int64_t *row_idx, int64_t n, int32_t threads) {
-    if (n < 0 || (n > 0 && (rows32 == nullptr || row_idx == nullptr))) {
-        set_last_error("hx_rows_widen: bad arguments");
-        return HX_ERR_VALUE;
-    }
-    // chunks of 2^21 entries taken from a shared counter: a core that is busy elsewhere (the
-    // caller's stream synchronisation spins on one) delays only the chunks it holds
-    constexpr int64_t CHUNK = int64_t(1) << 21;
-    const int64_t chunks = (n + CHUNK - 1) / CHUNK;
-    const int nt = (int)std::max<int64_t>(1, std::min<int64_t>(threads > 0 ? threads : (int)std::thread::hardware_concurrency(),
-                                                              chunks));
-    std::atomic<int64_t> next{0};
-    auto work = [&]() {
-        for (int64_t c = next.fetch_add(1); c < chunks; c = next.fetch_add(1)) {
-            const int64_t lo = c * CHUNK, hi = std::min(n, lo + CHUNK);
-            for (int64_t i = lo; i < hi; ++i) row_idx[i] = rows32[i];
-        }
-    };
-    std::vector<std::thread> pool;
-    pool.reserve(nt - 1);
-    for (int t = 1; t < nt; ++t) pool.emplace_back(work);
-    work();
-    for (auto &th : pool) th.join();
-    return HX_OK;
-}
+

@@ -129,7 +129,8 @@ def copy_stream(dev) -> torch.cuda.Stream:
     return _COPY_STREAMS[key]
 
 
-def fetch_csc(csc: D.DeviceCsc, stream=None, threads: int | None = None, chunk: int = 1 << 25) -> LowerCscMatrix:
+def fetch_csc(csc: D.DeviceCsc, stream=None, threads: int | None = None, chunk: int = 1 << 25,
+              rows_first: bool | None = None) -> LowerCscMatrix:
     """Device lower CSC -> host LowerCscMatrix (reference dtypes) for one synchronous call.
 
     Row indices cross as int32 (hx_rows_narrow) in chunks interleaved with the value chunks on the
@@ -147,6 +148,8 @@ def fetch_csc(csc: D.DeviceCsc, stream=None, threads: int | None = None, chunk: 
     rows32 = torch.empty(max(n, 1), dtype=torch.int32, pin_memory=True)
     narrow = D.rows_narrow(csc.row_idx, stream=producer) if n else None
     copy.wait_event(producer.record_event())
+    if rows_first is None:
+        rows_first = os.environ.get("HX_FETCH_ROWS_FIRST", "0") == "1"
     landed = []
     with torch.cuda.stream(copy):
         col_ptr.copy_(csc.col_ptr, non_blocking=True)
@@ -154,7 +157,10 @@ def fetch_csc(csc: D.DeviceCsc, stream=None, threads: int | None = None, chunk: 
             hi = min(n, lo + chunk)
             rows32[lo:hi].copy_(narrow[lo:hi], non_blocking=True)
             landed.append((lo, hi, copy.record_event()))
-            vals[lo:hi].copy_(csc.vals[lo:hi], non_blocking=True)
+            if not rows_first:
+                vals[lo:hi].copy_(csc.vals[lo:hi], non_blocking=True)
+        if rows_first:
+            vals.copy_(csc.vals, non_blocking=True)
         done = copy.record_event()
         for t in (narrow, csc.row_idx, csc.vals, csc.col_ptr):
             if t is not None:

@@ -114,7 +114,7 @@ def test_halo_pack_unpack_words_match_oracle(world, kind):
         chunks = 4 * want[:, 0] + want[:, 1]
         send = ops.alloc_words(int(chunks.sum())).fill_(-7)
         offs = np.concatenate([[0], np.cumsum(chunks)[:-1]])
-        ops.halo_pack(dm, ke_d, bdev, world, r, *ops.pointers([send.data_ptr()] * world, offs))
+        ops.halo_pack(dm, ke_d, bdev, world, r, *ops.pointers([send.data_ptr()] * world, offs), ws)
         got = send.cpu().numpy()
         for d, c in enumerate(halo.pack(mesh.connectivity[lo:hi], ke[lo:hi], bounds, world, r)):
             assert np.array_equal(got[offs[d]:offs[d] + chunks[d]], c)
