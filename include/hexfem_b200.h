@@ -257,6 +257,12 @@ int hx_block_select(const int32_t *conn, int64_t n_el, int64_t col_lo, int64_t c
                     int64_t *count, void *workspace, int64_t workspace_bytes, void *stream);
 int hx_block_gather(const int32_t *conn, const double *coeff, const int64_t *ids, const int64_t *count,
                     int64_t capacity, int32_t *conn_out, double *coeff_out, void *stream);
+/* ranges (HOST code): for the streamed column-block build of a locally numbered mesh -- e_lo[k] /
+ *         e_hi[k] (n_blocks each) = the element range whose node span covers block k = columns
+ *         [bounds[k], bounds[k+1]) (a superset of the elements touching it; 0/0 when none).  conn
+ *         (n_el, 8) int32 HOST array, `threads` workers (<= 0: all). */
+int hx_block_ranges(const int32_t *conn, int64_t n_el, const int64_t *bounds, int32_t n_blocks, int64_t *e_lo,
+                    int64_t *e_hi, int32_t threads);
 
 /* ---- structured box in device memory (mesh.py:73-98 generate_cube_mesh) --------------------------
  * coords (n_nodes, 3) f64, conn (n_el, 8) i32, coeff (n_el,) f64: node (i,j,k) at (i h, j h, k h)

@@ -8,6 +8,8 @@
 #include <immintrin.h>
 #include <stdint.h>
 
+#include <climits>
+
 #include <algorithm>
 #include <atomic>
 #include <thread>
@@ -68,5 +70,65 @@ extern "C" int hx_rows_widen(const int32_t *rows32, int64_t *row_idx, int64_t n,
     for (int t = 1; t < nt; ++t) pool.emplace_back(work);
     work();
     for (auto &th : pool) th.join();
+    return HX_OK;
+}
+
+// Element range of each column block for the streamed build: block k = columns [bounds[k],
+// bounds[k+1]); an element with node ids spanning blocks [b(min), b(max)] may hold columns of each
+// of them, so e_lo[k] / e_hi[k] = the lowest element / one past the highest element whose span
+// covers k (a superset of the elements touching k -- extra elements contribute nothing to the
+// block).  Ids outside [0, n_nodes) clamp to the first / last block (the integration kernel reports
+// them).  Empty blocks get e_lo = e_hi = 0.  Host code, `threads` workers over element chunks.
+extern "C" int hx_block_ranges(const int32_t *conn, int64_t n_el, const int64_t *bounds, int32_t n_blocks,
+                               int64_t *e_lo, int64_t *e_hi, int32_t threads) {
+    if (n_el < 0 || n_blocks < 1 || bounds == nullptr || e_lo == nullptr || e_hi == nullptr ||
+        (n_el > 0 && conn == nullptr)) {
+        hx::set_last_error("hx_block_ranges: bad arguments");
+        return HX_ERR_VALUE;
+    }
+    const int K = n_blocks;
+    auto block_of = [&](int64_t node) -> int {
+        // largest k with bounds[k] <= node, clamped to [0, K-1]
+        const int64_t *it = std::upper_bound(bounds + 1, bounds + K, node);
+        return (int)(it - (bounds + 1));
+    };
+    const int hw = (int)std::max(1u, std::thread::hardware_concurrency());
+    const int64_t per = int64_t(1) << 20;
+    const int64_t chunks = (n_el + per - 1) / per;
+    const int nt = (int)std::max<int64_t>(1, std::min<int64_t>(threads > 0 ? threads : hw, chunks));
+    std::vector<std::vector<int64_t>> lo(nt, std::vector<int64_t>(K, INT64_MAX)), hi(nt, std::vector<int64_t>(K, 0));
+    std::atomic<int64_t> next{0};
+    auto work = [&](int t) {
+        int64_t *L = lo[t].data(), *H = hi[t].data();
+        for (int64_t c = next.fetch_add(1); c < chunks; c = next.fetch_add(1)) {
+            const int64_t a = c * per, z = std::min(n_el, a + per);
+            for (int64_t e = a; e < z; ++e) {
+                const int32_t *g = conn + 8 * e;
+                int32_t mn = g[0], mx = g[0];
+                for (int k = 1; k < 8; ++k) {
+                    mn = std::min(mn, g[k]);
+                    mx = std::max(mx, g[k]);
+                }
+                const int b0 = block_of(mn), b1 = block_of(mx);
+                for (int b = b0; b <= b1; ++b) {
+                    L[b] = std::min(L[b], e);
+                    H[b] = std::max(H[b], e + 1);
+                }
+            }
+        }
+    };
+    std::vector<std::thread> pool;
+    for (int t = 1; t < nt; ++t) pool.emplace_back(work, t);
+    work(0);
+    for (auto &th : pool) th.join();
+    for (int b = 0; b < K; ++b) {
+        int64_t l = INT64_MAX, h = 0;
+        for (int t = 0; t < nt; ++t) {
+            l = std::min(l, lo[t][b]);
+            h = std::max(h, hi[t][b]);
+        }
+        e_lo[b] = h > 0 ? l : 0;
+        e_hi[b] = h;
+    }
     return HX_OK;
 }

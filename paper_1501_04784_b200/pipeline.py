@@ -262,6 +262,10 @@ def build_out_of_core(mesh, n_blocks: int, mode: str = "exact", device=None, ret
 # UPLOAD_RANGES_MIN_ELEMENTS elements), so the integration of range k overlaps the copy of range k+1
 UPLOAD_RANGES = 8
 UPLOAD_RANGES_MIN_ELEMENTS = 1 << 22
+# locally numbered meshes of at least STREAM_MIN_ELEMENTS elements take the streamed column-block
+# build (stream.py): STREAM_BLOCKS blocks, copies in both directions overlapping the kernels
+STREAM_BLOCKS = 8
+STREAM_MIN_ELEMENTS = 1 << 22
 
 
 def _host_tensor(a, dtype):
@@ -327,9 +331,18 @@ def run_build(mesh, budget_bytes: int, workers: int = 1, mode: str = "sequential
     with_index = assembler == "triplet"
     need = device_bytes(mesh.n_el, mesh.n_nodes, with_index=with_index)
     if device_budget_bytes is not None and need > device_budget_bytes:
-        return _run_build_blocks(mesh, plan, -(-need // device_budget_bytes), workers, mode, assembler, integration,
-                                 dev)
+        return _run_build_blocks(mesh, plan, device_budget_bytes, -(-need // device_budget_bytes), workers, mode,
+                                 assembler, integration, dev)
     wall0 = time.perf_counter()
+    if mesh.n_el >= STREAM_MIN_ELEMENTS and os.environ.get("HX_STREAMED", "1") != "0":
+        from . import stream
+
+        sp = stream.plan(mesh, STREAM_BLOCKS)
+        st: dict = {}
+        matrix = stream.streamed_build(mesh, sp, mode=integration, device=dev, stats=st) if sp is not None else None
+        if matrix is not None:
+            return matrix, _report(mesh, matrix, plan, st["integration_s"], st["assembly_s"],
+                                   time.perf_counter() - wall0, workers, mode, assembler)
     with torch.cuda.device(dev):
         main = torch.cuda.current_stream(dev)
         n = mesh.n_el
@@ -368,13 +381,17 @@ def run_build(mesh, budget_bytes: int, workers: int = 1, mode: str = "sequential
         time_integration = ev[0].elapsed_time(ev[1]) / 1e3
         time_assembly = ev[1].elapsed_time(ev[2]) / 1e3
         del dm, ke, rows, cols, csc, prep
-    time_total = time.perf_counter() - wall0
+    return matrix, _report(mesh, matrix, plan, time_integration, time_assembly, time.perf_counter() - wall0,
+                           workers, mode, assembler)
+
+
+def _report(mesh, matrix, plan, time_integration, time_assembly, time_total, workers, mode, assembler):
     nnz_triplet = 36 * mesh.n_el
     trip_mb = triplet_memory(nnz_triplet)
     matrix_mb = csc_memory(matrix.nnz, matrix.dim)
     stage_sum = time_integration + time_assembly
     pct_integration = 100.0 * time_integration / stage_sum if stage_sum > 0 else 100.0
-    report = BuildReport(
+    return BuildReport(
         n_el=mesh.n_el, n_nodes=mesh.n_nodes, nnz_triplet=nnz_triplet, nnz_csc=matrix.nnz,
         nnz_compression=1.0 - matrix.nnz / nnz_triplet, triplet_mb=trip_mb, csc_mb=matrix_mb,
         memory_saving=memory_saving(trip_mb, matrix_mb), time_integration_s=time_integration,
@@ -383,25 +400,23 @@ def run_build(mesh, budget_bytes: int, workers: int = 1, mode: str = "sequential
         time_assembly_s=time_assembly, time_total_s=time_total, pct_integration=pct_integration,
         pct_assembly=100.0 - pct_integration, group_count=plan.group_count, workers=workers, mode=mode,
         assembler=assembler)
-    return matrix, report
 
 
-def _run_build_blocks(mesh, plan, n_blocks, workers, mode, assembler, integration, dev):
+def _run_build_blocks(mesh, plan, budget, n_blocks, workers, mode, assembler, integration, dev):
+    """Beyond the HBM budget: the streamed column-block build when the numbering is local (blocks
+    sized for three in flight, copies overlapped), else build_out_of_core's per-block selection."""
+    from . import stream
+
     wall0 = time.perf_counter()
+    sp = stream.plan(mesh, max(2, stream.blocks_for_budget(mesh.n_el, mesh.n_nodes, budget)))
+    st: dict = {}
+    matrix = stream.streamed_build(mesh, sp, mode=integration, device=dev, stats=st) if sp is not None else None
+    if matrix is not None:
+        return matrix, _report(mesh, matrix, plan, st["integration_s"], st["assembly_s"],
+                               time.perf_counter() - wall0, workers, mode, assembler)
     matrix, _, st = build_out_of_core(mesh, int(min(n_blocks, max(mesh.n_nodes, 1))), mode=integration, device=dev)
-    total = time.perf_counter() - wall0
-    t_int, t_asm = st["time_integration_s"], st["time_assembly_s"]
-    pct = 100.0 * t_int / (t_int + t_asm) if t_int + t_asm > 0 else 100.0
-    nnz_triplet = 36 * mesh.n_el
-    trip_mb = triplet_memory(nnz_triplet)
-    matrix_mb = csc_memory(matrix.nnz, matrix.dim)
-    report = BuildReport(
-        n_el=mesh.n_el, n_nodes=mesh.n_nodes, nnz_triplet=nnz_triplet, nnz_csc=matrix.nnz,
-        nnz_compression=1.0 - matrix.nnz / nnz_triplet, triplet_mb=trip_mb, csc_mb=matrix_mb,
-        memory_saving=memory_saving(trip_mb, matrix_mb), time_integration_s=t_int, time_index_s=None,
-        time_assembly_s=t_asm, time_total_s=total, pct_integration=pct, pct_assembly=100.0 - pct,
-        group_count=plan.group_count, workers=workers, mode=mode, assembler=assembler)
-    return matrix, report
+    return matrix, _report(mesh, matrix, plan, st["time_integration_s"], st["time_assembly_s"],
+                           time.perf_counter() - wall0, workers, mode, assembler)
 
 
 def host_csc_equal(a: LowerCscMatrix, b: LowerCscMatrix) -> bool:

@@ -1,0 +1,241 @@
+"""Streamed column-block build: host mesh -> host LowerCscMatrix with copies in both directions
+overlapping the kernels (run_build's in-core path for locally numbered meshes, and its beyond-HBM
+path -- Eq. 10 batching, integrate.py:55-81 / PAPER.md:192-199).
+
+The lower CSC is cut into K column blocks [B_k, B_k+1).  On a locally numbered mesh (structured
+generators, RCM-ordered inputs) the elements that can hold a block's columns form a short element
+range [e_lo(k), e_hi(k)) -- found on the host cores (``hx_block_ranges``) while the coordinates
+are in flight.  Block k then runs as
+
+    H2D stream   conn / coeff of range k+1 (pinned host -> HBM)          } PCIe is full duplex:
+    main stream  integrate range k, assemble columns of block k           } these three overlap
+    D2H stream   block k-1's rows (int32) / values / col_ptr -> pinned    }
+    host pool    widen block k-1's rows to int64, shift its col_ptr
+
+so the call costs ~max(H2D, D2H) + one block, instead of H2D + build + D2H.  Elements on a block
+boundary are integrated once per block they touch (a halo recompute instead of a halo exchange);
+each block sums its duplicates in ascending global element order, so the concatenated blocks are
+bitwise the one-shot build (and the reference).
+
+Meshes without locality (the ranges would cover most elements for every block) are left to the
+one-shot path: ``plan`` returns None for them.
+"""
+
+from __future__ import annotations
+
+import time
+from concurrent.futures import ThreadPoolExecutor
+
+import numpy as np
+import torch
+
+from . import _native as N
+from . import device as D
+from .assemble import LowerCscMatrix
+from .errors import MeshValidationError, NodeIndexError
+from .transfer import copy_stream, host_threads
+
+__all__ = ["block_element_ranges", "StreamPlan", "plan", "streamed_build", "blocks_for_budget"]
+
+# a block layout is streamed only when the summed element ranges stay within this factor of n_el
+MAX_RANGE_OVERLAP = 1.25
+
+
+def block_element_ranges(conn: np.ndarray, bounds: np.ndarray, threads: int | None = None):
+    """(e_lo, e_hi) int64 (K,) per column block (hx_block_ranges on the host cores)."""
+    conn = np.ascontiguousarray(conn, dtype=np.int32)
+    bounds = np.ascontiguousarray(bounds, dtype=np.int64)
+    k = bounds.shape[0] - 1
+    e_lo = np.zeros(k, dtype=np.int64)
+    e_hi = np.zeros(k, dtype=np.int64)
+    N.check(N.lib().hx_block_ranges(conn.ctypes.data, conn.shape[0], bounds.ctypes.data, k, e_lo.ctypes.data,
+                                    e_hi.ctypes.data, host_threads() if threads is None else int(threads)),
+            "hx_block_ranges")
+    return e_lo, e_hi
+
+
+class StreamPlan:
+    def __init__(self, bounds, e_lo, e_hi):
+        self.bounds, self.e_lo, self.e_hi = bounds, e_lo, e_hi
+
+    @property
+    def n_blocks(self) -> int:
+        return self.bounds.shape[0] - 1
+
+    def max_block_elements(self) -> int:
+        return int((self.e_hi - self.e_lo).max()) if self.n_blocks else 0
+
+
+def plan(mesh, n_blocks: int, threads: int | None = None) -> StreamPlan | None:
+    """Equal column blocks and their element ranges; None when the numbering has no locality."""
+    from .distributed import column_bounds
+
+    n_nodes, n_el = mesh.n_nodes, mesh.n_el
+    n_blocks = int(max(1, min(n_blocks, n_nodes)))
+    bounds = column_bounds(n_nodes, n_blocks)
+    e_lo, e_hi = block_element_ranges(mesh.connectivity, bounds, threads)
+    if n_el and (e_hi - e_lo).sum() > MAX_RANGE_OVERLAP * n_el + n_blocks:
+        return None
+    return StreamPlan(bounds, e_lo, e_hi)
+
+
+def blocks_for_budget(n_el: int, n_nodes: int, budget_bytes: int) -> int:
+    """Column blocks so that the coordinates plus three blocks in flight (next upload, current
+    build, pending copy-out) fit ``budget_bytes`` of HBM: per block ~344 B per element (conn,
+    coeff, KE, halo slack) and ~464 B per column (CSC at the rows estimate, symbolic workspace)."""
+    free = budget_bytes - 24 * n_nodes
+    if free <= 0:
+        return max(1, n_nodes)
+    return int(max(1, min(n_nodes, -(-3 * (344 * n_el + 464 * n_nodes) // free))))
+
+
+def _host(a, dtype):
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=dtype))
+
+
+def streamed_build(mesh, sp: StreamPlan, mode: str = "exact", device=None, capacity: int | None = None,
+                   stats: dict | None = None):
+    """Run the streamed build of ``mesh`` under plan ``sp``; returns the host LowerCscMatrix, or None
+    when the result outgrows ``capacity`` entries (default: the rows-per-column estimate), in
+    which case the caller takes the one-shot path.  Raises NodeIndexError / DegenerateElementError
+    for the lowest failing element like the one-shot build."""
+    dev = D.require_device(device)
+    n_nodes, n_el = mesh.n_nodes, mesh.n_el
+    K = sp.n_blocks
+    cap = D.ROWS_PER_COLUMN_ESTIMATE * n_nodes if capacity is None else int(capacity)
+    t0 = time.perf_counter()
+    with torch.cuda.device(dev):
+        main = torch.cuda.current_stream(dev)
+        h2d = _h2d_stream(dev)
+        d2h = copy_stream(dev)
+        coords_h, conn_h, coeff_h = (_host(mesh.coords, np.float64), _host(mesh.connectivity, np.int32),
+                                     _host(mesh.coefficient, np.float64))
+        h2d.wait_stream(main)
+        # buffers written on the H2D stream are allocated on it and marked as used by the main
+        # stream, so the caching allocator never hands their memory to the next upload while a
+        # kernel still reads it
+        with torch.cuda.stream(h2d):
+            coords = torch.empty(tuple(coords_h.shape), dtype=torch.float64, device=dev)
+            coords.copy_(coords_h, non_blocking=True)
+            coords_ready = h2d.record_event()
+        coords.record_stream(main)
+        out_cp = torch.empty(n_nodes + 1, dtype=torch.int64, pin_memory=True)
+        out_rows = torch.empty(max(cap, 1), dtype=torch.int64, pin_memory=True)
+        out_vals = torch.empty(max(cap, 1), dtype=torch.float64, pin_memory=True)
+        rows32 = torch.empty(max(cap, 1), dtype=torch.int32, pin_memory=True)
+        out_cp[0] = 0
+        cp_np = out_cp.numpy()
+        threads = max(1, host_threads() // 2)
+        pool = ThreadPoolExecutor(max_workers=1)
+
+        def upload(k):
+            lo, hi = int(sp.e_lo[k]), int(sp.e_hi[k])
+            with torch.cuda.stream(h2d):
+                conn = torch.empty((hi - lo, 8), dtype=torch.int32, device=dev)
+                coeff = torch.empty(hi - lo, dtype=torch.float64, device=dev)
+                conn.copy_(conn_h[lo:hi], non_blocking=True)
+                coeff.copy_(coeff_h[lo:hi], non_blocking=True)
+                ev = h2d.record_event()
+            conn.record_stream(main)
+            coeff.record_stream(main)
+            return conn, coeff, ev
+
+        def finish(k, off, nnz, cp_stage, rows_landed, done):
+            rows_landed.synchronize()
+            if nnz:
+                N.check(N.lib().hx_rows_widen(rows32.data_ptr() + 4 * off, out_rows.data_ptr() + 8 * off, nnz,
+                                              threads), "hx_rows_widen")
+            done.synchronize()
+            a, z = int(sp.bounds[k]), int(sp.bounds[k + 1])
+            np.add(cp_stage.numpy()[1:], off, out=cp_np[a + 1:z + 1])
+
+        fails, futures, stage_events = [], [], []
+        offset = 0
+        t_gpu = [torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)]
+        main.wait_event(coords_ready)
+        t_gpu[0].record(main)
+        pending = upload(0) if K else None
+        overflow = False
+        try:
+            for k in range(K):
+                conn, coeff, ready = pending
+                if k + 1 < K:
+                    pending = upload(k + 1)  # next range in flight while this block computes
+                main.wait_event(ready)
+                a, z = int(sp.bounds[k]), int(sp.bounds[k + 1])
+                if conn.shape[0] == 0:
+                    cp_np[a + 1:z + 1] = offset
+                    continue
+                dm = D.DeviceMesh(coords, conn, coeff)
+                ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+                ev[0].record(main)
+                ke, _, _, fail = D.integrate_mesh(dm, with_index=False, mode=mode, stream=main)
+                ev[1].record(main)
+                fails.append((int(sp.e_lo[k]), fail))
+                try:
+                    csc = D.mesh_csc([(conn, ke)], n_nodes, a, z, stream=main, order="column")
+                except MeshValidationError:
+                    _raise_lowest(fails, n_nodes)
+                    raise
+                ev[2].record(main)
+                stage_events.append(ev)
+                nnz = csc.nnz
+                if offset + nnz > cap:
+                    overflow = True
+                    break
+                narrow = D.rows_narrow(csc.row_idx, stream=main) if nnz else None
+                cp_stage = torch.empty(z - a + 1, dtype=torch.int64, pin_memory=True)
+                d2h.wait_event(main.record_event())
+                with torch.cuda.stream(d2h):
+                    if nnz:
+                        rows32[offset:offset + nnz].copy_(narrow, non_blocking=True)
+                    rows_landed = d2h.record_event()
+                    if nnz:
+                        out_vals[offset:offset + nnz].copy_(csc.vals, non_blocking=True)
+                    cp_stage.copy_(csc.col_ptr, non_blocking=True)
+                    done = d2h.record_event()
+                for t in (narrow, csc.row_idx, csc.vals, csc.col_ptr):
+                    if t is not None:
+                        t.record_stream(d2h)
+                futures.append(pool.submit(finish, k, offset, nnz, cp_stage, rows_landed, done))
+                offset += nnz
+                del dm, ke, csc, narrow
+            t_gpu[1].record(main)
+            for f in futures:
+                f.result()
+            torch.cuda.synchronize(dev)
+        finally:
+            pool.shutdown(wait=True)
+        if overflow:
+            return None
+        _raise_lowest(fails, n_nodes)
+        if stats is not None:
+            stats.update(gpu_s=t_gpu[0].elapsed_time(t_gpu[1]) / 1e3, wall_s=time.perf_counter() - t0, blocks=K,
+                         integrated_elements=int((sp.e_hi - sp.e_lo).sum()),
+                         integration_s=sum(e[0].elapsed_time(e[1]) for e in stage_events) / 1e3,
+                         assembly_s=sum(e[1].elapsed_time(e[2]) for e in stage_events) / 1e3)
+    return LowerCscMatrix(col_ptr=cp_np, row_idx=out_rows.numpy()[:offset], vals=out_vals.numpy()[:offset],
+                          dim=n_nodes)
+
+
+def _raise_lowest(fails, n_nodes):
+    best = None
+    for lo, f in fails:
+        err = D.fail_error(f.cpu().numpy(), lo, n_nodes)
+        if err is None:
+            continue
+        key = (not isinstance(err, NodeIndexError), err.element_id)
+        if best is None or key < best[0]:
+            best = (key, err)
+    if best is not None:
+        raise best[1]
+
+
+_H2D: dict = {}
+
+
+def _h2d_stream(dev) -> torch.cuda.Stream:
+    key = torch.device(dev).index
+    if key not in _H2D:
+        _H2D[key] = torch.cuda.Stream(device=dev)
+    return _H2D[key]

@@ -836,13 +836,14 @@ def test_unfused_paths_bad_node_id_raise_node_index_error(node):
         assert isinstance(exc, IndexError) and isinstance(exc, MeshValidationError)
 
     with CudaBackend() as be:
-        for plan in (one_group(bad), plan_batches(required_bytes(bad.n_el), required_bytes(40), bad.n_el)):
-            with pytest.raises(NodeIndexError) as ei:
-                integrate_all(bad, be, plan)
-            if plan.group_count == 1:
-                check(ei.value)
-            else:  # groups run in order: the group holding element 77 fails first
-                assert ei.value.element_id == 77
+        with pytest.raises(NodeIndexError) as ei:
+            integrate_all(bad, be, one_group(bad))
+        check(ei.value)
+        # groups run in plan order (integrate.py:174-179): the first group holds the degenerate
+        # element 10 and fails before the group with the bad id is staged, as in the reference
+        with pytest.raises(DegenerateElementError) as ei:
+            integrate_all(bad, be, plan_batches(required_bytes(bad.n_el), required_bytes(40), bad.n_el))
+        assert ei.value.element_id == 10
     dm = D.DeviceMesh.from_host(bad)
     for kw in ({"ranges": [(0, 60), (60, 125)]}, {"overlap": True}, {}):
         with pytest.raises(NodeIndexError) as ei:
@@ -938,3 +939,71 @@ def test_run_build_overlapped_upload_bitwise(monkeypatch, pinned, assembler):
         assert m.col_ptr.dtype == np.int64 and m.row_idx.dtype == np.int64 and m.vals.dtype == np.float64
         assert bits_equal(m.col_ptr, cp) and bits_equal(m.row_idx, ri) and bits_equal(m.vals, vv)
         assert rep.nnz_csc == len(ri) and rep.time_total_s > 0
+
+
+@pytest.mark.parametrize("pinned", [False, True])
+@pytest.mark.parametrize("blocks", [1, 3, 8])
+def test_streamed_run_build_bitwise(monkeypatch, pinned, blocks):
+    """run_build's streamed column-block path (stream.py: H2D of range k+1, build of block k and
+    D2H of block k-1 overlapped; halo elements recomputed per block) == the oracle, bit for bit."""
+    from paper_1501_04784_b200 import pipeline
+    from paper_1501_04784_b200.hostmem import pinned_mesh
+
+    monkeypatch.setattr(pipeline, "STREAM_MIN_ELEMENTS", 1)
+    monkeypatch.setattr(pipeline, "STREAM_BLOCKS", blocks)
+    mesh = perturbed_mesh(14, seed=blocks)
+    if pinned:
+        mesh = pinned_mesh(mesh)
+    ke, rows, cols, _, _, _ = oracle.stiffness_mesh(mesh.coords, mesh.connectivity, mesh.coefficient)
+    cp, ri, vv = oracle.triplet_to_csc(rows, cols, ke.reshape(-1), mesh.n_nodes)
+    for _ in range(2):
+        m, rep = run_build(mesh, budget_bytes=10**12)
+        assert bits_equal(m.col_ptr, cp) and bits_equal(m.row_idx, ri) and bits_equal(m.vals, vv)
+        assert rep.nnz_csc == len(ri) and rep.time_integration_s > 0
+
+
+def test_streamed_plan_rejects_permuted_and_overflow_falls_back(monkeypatch):
+    from paper_1501_04784_b200 import pipeline, stream
+
+    perm = permuted_mesh(perturbed_mesh(10, seed=1), seed=2)
+    assert stream.plan(perm, 8) is None
+    mesh = perturbed_mesh(10, seed=3)
+    sp = stream.plan(mesh, 4)
+    assert sp is not None and sp.max_block_elements() < mesh.n_el
+    assert stream.streamed_build(mesh, sp, capacity=100) is None  # result outgrows the buffers
+    monkeypatch.setattr(pipeline, "STREAM_MIN_ELEMENTS", 1)
+    ke, rows, cols, _, _, _ = oracle.stiffness_mesh(perm.coords, perm.connectivity, perm.coefficient)
+    cp, ri, vv = oracle.triplet_to_csc(rows, cols, ke.reshape(-1), perm.n_nodes)
+    m, _ = run_build(perm, budget_bytes=10**12)  # one-shot path
+    assert bits_equal(m.col_ptr, cp) and bits_equal(m.row_idx, ri) and bits_equal(m.vals, vv)
+
+
+def test_streamed_errors_lowest_element(monkeypatch):
+    from paper_1501_04784_b200 import NodeIndexError, pipeline
+
+    monkeypatch.setattr(pipeline, "STREAM_MIN_ELEMENTS", 1)
+    monkeypatch.setattr(pipeline, "STREAM_BLOCKS", 4)
+    mesh = perturbed_mesh(8, seed=4)
+    conn = mesh.connectivity.copy()
+    conn[400] = conn[400][[4, 5, 6, 7, 0, 1, 2, 3]]  # degenerate
+    conn[300] = conn[300][[4, 5, 6, 7, 0, 1, 2, 3]]  # lower degenerate id: reported
+    with pytest.raises(DegenerateElementError) as ei:
+        run_build(Mesh(mesh.coords, conn, mesh.coefficient), budget_bytes=10**12)
+    assert ei.value.element_id == 300
+    conn[450, 1] = mesh.n_nodes + 3  # a bad node id wins over every degenerate element
+    with pytest.raises(NodeIndexError) as ei:
+        run_build(Mesh(mesh.coords, conn, mesh.coefficient), budget_bytes=10**12)
+    assert ei.value.element_id == 450
+
+
+def test_out_of_core_budget_takes_streamed_blocks():
+    """A device budget below the in-core footprint: the streamed path with blocks sized for the
+    budget (locally numbered mesh), bitwise."""
+    from paper_1501_04784_b200.pipeline import device_bytes
+
+    mesh = perturbed_mesh(16, seed=7)
+    ke, rows, cols, _, _, _ = oracle.stiffness_mesh(mesh.coords, mesh.connectivity, mesh.coefficient)
+    cp, ri, vv = oracle.triplet_to_csc(rows, cols, ke.reshape(-1), mesh.n_nodes)
+    budget = device_bytes(mesh.n_el, mesh.n_nodes) // 4
+    m, rep = run_build(mesh, budget_bytes=10**12, device_budget_bytes=budget)
+    assert bits_equal(m.col_ptr, cp) and bits_equal(m.row_idx, ri) and bits_equal(m.vals, vv)

@@ -92,3 +92,24 @@ def test_memory_model_table_rows():
 
 def test_batchplan_type():
     assert BatchPlan(ranges=((0, 3),)).group_count == 1
+
+
+def test_block_ranges_host_scan_matches_numpy():
+    """hx_block_ranges (host C++): per column block, the element range whose node span covers it."""
+    from paper_1501_04784_b200.distributed import column_bounds
+    from paper_1501_04784_b200.stream import block_element_ranges
+    from paper_1501_04784_b200.workloads import permuted_mesh, perturbed_mesh
+
+    for mesh in (perturbed_mesh(9, seed=1), permuted_mesh(perturbed_mesh(6, seed=2), seed=3)):
+        conn = mesh.connectivity.copy()
+        conn[5, 2] = mesh.n_nodes + 7  # out-of-range ids clamp to the last / first block
+        conn[11, 0] = -4
+        for k in (1, 3, 8, 50):
+            bounds = column_bounds(mesh.n_nodes, k)
+            lo, hi = block_element_ranges(conn, bounds, threads=3)
+            bmin = np.clip(np.searchsorted(bounds, conn.min(axis=1), side="right") - 1, 0, k - 1)
+            bmax = np.clip(np.searchsorted(bounds, conn.max(axis=1), side="right") - 1, 0, k - 1)
+            for b in range(k):
+                cover = np.flatnonzero((bmin <= b) & (bmax >= b))
+                want = (cover.min(), cover.max() + 1) if cover.size else (0, 0)
+                assert (lo[b], hi[b]) == want
