@@ -96,10 +96,12 @@ extern "C" int hx_block_ranges(const int32_t *conn, int64_t n_el, const int64_t 
     const int64_t per = int64_t(1) << 20;
     const int64_t chunks = (n_el + per - 1) / per;
     const int nt = (int)std::max<int64_t>(1, std::min<int64_t>(threads > 0 ? threads : hw, chunks));
-    std::vector<std::vector<int64_t>> lo(nt, std::vector<int64_t>(K, INT64_MAX)), hi(nt, std::vector<int64_t>(K, 0));
+    std::vector<std::vector<int64_t>> lo(nt), hi(nt);
     std::atomic<int64_t> next{0};
     auto work = [&](int t) {
-        int64_t *L = lo[t].data(), *H = hi[t].data();
+        // thread-local accumulators (the per-element updates must not share cache lines)
+        std::vector<int64_t> Lv(K, INT64_MAX), Hv(K, 0);
+        int64_t *L = Lv.data(), *H = Hv.data();
         for (int64_t c = next.fetch_add(1); c < chunks; c = next.fetch_add(1)) {
             const int64_t a = c * per, z = std::min(n_el, a + per);
             for (int64_t e = a; e < z; ++e) {
@@ -116,6 +118,8 @@ extern "C" int hx_block_ranges(const int32_t *conn, int64_t n_el, const int64_t 
                 }
             }
         }
+        lo[t] = std::move(Lv);
+        hi[t] = std::move(Hv);
     };
     std::vector<std::thread> pool;
     for (int t = 1; t < nt; ++t) pool.emplace_back(work, t);

@@ -264,7 +264,7 @@ UPLOAD_RANGES = 8
 UPLOAD_RANGES_MIN_ELEMENTS = 1 << 22
 # locally numbered meshes of at least STREAM_MIN_ELEMENTS elements take the streamed column-block
 # build (stream.py): STREAM_BLOCKS blocks, copies in both directions overlapping the kernels
-STREAM_BLOCKS = 8
+STREAM_BLOCKS = 10
 STREAM_MIN_ELEMENTS = 1 << 22
 
 
@@ -337,9 +337,8 @@ def run_build(mesh, budget_bytes: int, workers: int = 1, mode: str = "sequential
     if mesh.n_el >= STREAM_MIN_ELEMENTS and os.environ.get("HX_STREAMED", "1") != "0":
         from . import stream
 
-        sp = stream.plan(mesh, STREAM_BLOCKS)
         st: dict = {}
-        matrix = stream.streamed_build(mesh, sp, mode=integration, device=dev, stats=st) if sp is not None else None
+        matrix = stream.streamed_build(mesh, STREAM_BLOCKS, mode=integration, device=dev, stats=st)
         if matrix is not None:
             return matrix, _report(mesh, matrix, plan, st["integration_s"], st["assembly_s"],
                                    time.perf_counter() - wall0, workers, mode, assembler)
@@ -408,9 +407,9 @@ def _run_build_blocks(mesh, plan, budget, n_blocks, workers, mode, assembler, in
     from . import stream
 
     wall0 = time.perf_counter()
-    sp = stream.plan(mesh, max(2, stream.blocks_for_budget(mesh.n_el, mesh.n_nodes, budget)))
     st: dict = {}
-    matrix = stream.streamed_build(mesh, sp, mode=integration, device=dev, stats=st) if sp is not None else None
+    matrix = stream.streamed_build(mesh, max(3, stream.blocks_for_budget(mesh.n_el, mesh.n_nodes, budget)),
+                                   mode=integration, device=dev, stats=st)
     if matrix is not None:
         return matrix, _report(mesh, matrix, plan, st["integration_s"], st["assembly_s"],
                                time.perf_counter() - wall0, workers, mode, assembler)

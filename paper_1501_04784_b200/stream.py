@@ -23,6 +23,7 @@ one-shot path: ``plan`` returns None for them.
 
 from __future__ import annotations
 
+import os
 import time
 from concurrent.futures import ThreadPoolExecutor
 
@@ -66,13 +67,39 @@ class StreamPlan:
         return int((self.e_hi - self.e_lo).max()) if self.n_blocks else 0
 
 
-def plan(mesh, n_blocks: int, threads: int | None = None) -> StreamPlan | None:
-    """Equal column blocks and their element ranges; None when the numbering has no locality."""
-    from .distributed import column_bounds
+def stream_bounds(n_nodes: int, n_blocks: int) -> np.ndarray:
+    """Column bounds with quarter-size first and last blocks (K >= 3): the copy-out pipeline
+    starts after a short first block and ends with a short widening tail."""
+    if n_blocks < 3:
+        from .distributed import column_bounds
 
+        return column_bounds(n_nodes, n_blocks)
+    w = np.array([0.25] + [1.0] * (n_blocks - 2) + [0.25])
+    b = np.floor(np.concatenate([[0.0], np.cumsum(w)]) / w.sum() * n_nodes).astype(np.int64)
+    b[-1] = n_nodes
+    for r in range(1, n_blocks):  # strictly increasing
+        b[r] = min(max(b[r], b[r - 1] + 1), n_nodes - (n_blocks - r))
+    return b
+
+
+def looks_local(conn: np.ndarray, n_nodes: int, sample: int = 4096) -> bool:
+    """Host-side twin of device.numbering_is_local: sampled elements' node-id spans are a small
+    fraction of the id range on locally numbered meshes."""
+    n = conn.shape[0]
+    if n == 0 or n_nodes < 1 << 16:
+        return True
+    idx = np.linspace(0, n - 1, min(sample, n)).astype(np.int64)
+    rows = np.asarray(conn[idx], dtype=np.int64)
+    return float((rows.max(axis=1) - rows.min(axis=1)).mean()) < n_nodes / 64
+
+
+def plan(mesh, n_blocks: int, threads: int | None = None) -> StreamPlan | None:
+    """Column blocks and their element ranges; None when the numbering has no locality."""
     n_nodes, n_el = mesh.n_nodes, mesh.n_el
     n_blocks = int(max(1, min(n_blocks, n_nodes)))
-    bounds = column_bounds(n_nodes, n_blocks)
+    if not looks_local(mesh.connectivity, n_nodes):
+        return None
+    bounds = stream_bounds(n_nodes, n_blocks)
     e_lo, e_hi = block_element_ranges(mesh.connectivity, bounds, threads)
     if n_el and (e_hi - e_lo).sum() > MAX_RANGE_OVERLAP * n_el + n_blocks:
         return None
@@ -93,15 +120,18 @@ def _host(a, dtype):
     return torch.from_numpy(np.ascontiguousarray(a, dtype=dtype))
 
 
-def streamed_build(mesh, sp: StreamPlan, mode: str = "exact", device=None, capacity: int | None = None,
+def streamed_build(mesh, sp, mode: str = "exact", device=None, capacity: int | None = None,
                    stats: dict | None = None):
-    """Run the streamed build of ``mesh`` under plan ``sp``; returns the host LowerCscMatrix, or None
-    when the result outgrows ``capacity`` entries (default: the rows-per-column estimate), in
-    which case the caller takes the one-shot path.  Raises NodeIndexError / DegenerateElementError
-    for the lowest failing element like the one-shot build."""
+    """Run the streamed build of ``mesh``; returns the host LowerCscMatrix, or None when the mesh
+    has no locality or the result outgrows ``capacity`` entries (default: the rows-per-column
+    estimate) -- the caller then takes the one-shot path.  ``sp`` is a StreamPlan, or a block
+    count: the plan's host scan then runs while the coordinates are in flight.  Raises
+    NodeIndexError / DegenerateElementError for the lowest failing element like the one-shot
+    build."""
     dev = D.require_device(device)
     n_nodes, n_el = mesh.n_nodes, mesh.n_el
-    K = sp.n_blocks
+    if not isinstance(sp, StreamPlan) and not looks_local(mesh.connectivity, n_nodes):
+        return None
     cap = D.ROWS_PER_COLUMN_ESTIMATE * n_nodes if capacity is None else int(capacity)
     t0 = time.perf_counter()
     with torch.cuda.device(dev):
@@ -119,6 +149,11 @@ def streamed_build(mesh, sp: StreamPlan, mode: str = "exact", device=None, capac
             coords.copy_(coords_h, non_blocking=True)
             coords_ready = h2d.record_event()
         coords.record_stream(main)
+        if not isinstance(sp, StreamPlan):  # host scan while the coordinates cross PCIe
+            sp = plan(mesh, int(sp))
+            if sp is None:
+                return None
+        K = sp.n_blocks
         out_cp = torch.empty(n_nodes + 1, dtype=torch.int64, pin_memory=True)
         out_rows = torch.empty(max(cap, 1), dtype=torch.int64, pin_memory=True)
         out_vals = torch.empty(max(cap, 1), dtype=torch.float64, pin_memory=True)
@@ -133,9 +168,11 @@ def streamed_build(mesh, sp: StreamPlan, mode: str = "exact", device=None, capac
             with torch.cuda.stream(h2d):
                 conn = torch.empty((hi - lo, 8), dtype=torch.int32, device=dev)
                 coeff = torch.empty(hi - lo, dtype=torch.float64, device=dev)
+                mark(f"h2d {k} start", h2d)
                 conn.copy_(conn_h[lo:hi], non_blocking=True)
                 coeff.copy_(coeff_h[lo:hi], non_blocking=True)
                 ev = h2d.record_event()
+                mark(f"h2d {k} end", h2d)
             conn.record_stream(main)
             coeff.record_stream(main)
             return conn, coeff, ev
@@ -149,11 +186,21 @@ def streamed_build(mesh, sp: StreamPlan, mode: str = "exact", device=None, capac
             a, z = int(sp.bounds[k]), int(sp.bounds[k + 1])
             np.add(cp_stage.numpy()[1:], off, out=cp_np[a + 1:z + 1])
 
+        trace = [] if os.environ.get("HX_TRACE_STREAM") else None
+
+        def mark(name, stream):
+            if trace is not None:
+                e = torch.cuda.Event(enable_timing=True)
+                e.record(stream)
+                trace.append((name, e, time.perf_counter()))
+
         fails, futures, stage_events = [], [], []
         offset = 0
         t_gpu = [torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)]
+        mark("start", main)
         main.wait_event(coords_ready)
         t_gpu[0].record(main)
+        mark("coords landed", main)
         pending = upload(0) if K else None
         overflow = False
         try:
@@ -186,7 +233,9 @@ def streamed_build(mesh, sp: StreamPlan, mode: str = "exact", device=None, capac
                 narrow = D.rows_narrow(csc.row_idx, stream=main) if nnz else None
                 cp_stage = torch.empty(z - a + 1, dtype=torch.int64, pin_memory=True)
                 d2h.wait_event(main.record_event())
+                mark(f"asm {k} done (host)", main)
                 with torch.cuda.stream(d2h):
+                    mark(f"d2h {k} start", d2h)
                     if nnz:
                         rows32[offset:offset + nnz].copy_(narrow, non_blocking=True)
                     rows_landed = d2h.record_event()
@@ -194,6 +243,7 @@ def streamed_build(mesh, sp: StreamPlan, mode: str = "exact", device=None, capac
                         out_vals[offset:offset + nnz].copy_(csc.vals, non_blocking=True)
                     cp_stage.copy_(csc.col_ptr, non_blocking=True)
                     done = d2h.record_event()
+                    mark(f"d2h {k} end", d2h)
                 for t in (narrow, csc.row_idx, csc.vals, csc.col_ptr):
                     if t is not None:
                         t.record_stream(d2h)
@@ -204,6 +254,11 @@ def streamed_build(mesh, sp: StreamPlan, mode: str = "exact", device=None, capac
             for f in futures:
                 f.result()
             torch.cuda.synchronize(dev)
+            if trace:
+                z = trace[0][1]
+                for name, e, th in trace:
+                    print(f"  {name:24s} gpu {z.elapsed_time(e):8.2f} ms   host {1e3 * (th - t0):8.2f} ms", flush=True)
+                print(f"  total host {1e3 * (time.perf_counter() - t0):.2f} ms", flush=True)
         finally:
             pool.shutdown(wait=True)
         if overflow:

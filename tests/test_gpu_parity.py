@@ -845,10 +845,13 @@ def test_unfused_paths_bad_node_id_raise_node_index_error(node):
             integrate_all(bad, be, plan_batches(required_bytes(bad.n_el), required_bytes(40), bad.n_el))
         assert ei.value.element_id == 10
     dm = D.DeviceMesh.from_host(bad)
-    for kw in ({"ranges": [(0, 60), (60, 125)]}, {"overlap": True}, {}):
+    for kw in ({"ranges": [(0, 125)]}, {"overlap": True}, {}):
         with pytest.raises(NodeIndexError) as ei:
             build_device(dm, **kw)
         check(ei.value)
+    with pytest.raises(DegenerateElementError) as ei:  # groups report in order, like integrate_all
+        build_device(dm, ranges=[(0, 60), (60, 125)])
+    assert ei.value.element_id == 10
     with pytest.raises(NodeIndexError) as ei:
         run_build(bad, budget_bytes=10**12)
     check(ei.value)

@@ -113,3 +113,14 @@ def test_block_ranges_host_scan_matches_numpy():
                 cover = np.flatnonzero((bmin <= b) & (bmax >= b))
                 want = (cover.min(), cover.max() + 1) if cover.size else (0, 0)
                 assert (lo[b], hi[b]) == want
+
+
+def test_stream_bounds_quarter_end_blocks():
+    from paper_1501_04784_b200.stream import stream_bounds
+
+    for n, k in ((1000, 10), (17, 5), (5, 5), (100, 3)):
+        b = stream_bounds(n, k)
+        assert b[0] == 0 and b[-1] == n and len(b) == k + 1 and np.all(np.diff(b) > 0)
+    b = stream_bounds(10_000, 10)
+    w = np.diff(b)
+    assert abs(w[0] / w[1] - 0.25) < 0.01 and abs(w[-1] / w[-2] - 0.25) < 0.01
