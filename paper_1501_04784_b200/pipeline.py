@@ -151,20 +151,20 @@ def build_device(dm: D.DeviceMesh, mode: str = "exact", with_index: bool = True,
                                          cols=cols[36 * lo:36 * hi] if with_index else None,
                                          with_index=with_index, mode=mode, stream=main, adjacency=prep)
         fails.append(fail)
-    if cached is not None:
-        if cached.conn is not dm.conn:
-            raise ConfigurationError("the assembly plan belongs to another mesh")
-        csc = D.mesh_emit(cached, ke, stream=main)
-    elif plan is not None:
-        main.wait_event(plan_done)
-        csc = D.mesh_emit(plan, ke, stream=main)
-    else:
-        try:
+    if cached is not None and cached.conn is not dm.conn:
+        raise ConfigurationError("the assembly plan belongs to another mesh")
+    try:
+        if cached is not None:
+            csc = D.mesh_emit(cached, ke, stream=main)
+        elif plan is not None:
+            main.wait_event(plan_done)
+            csc = D.mesh_emit(plan, ke, stream=main)
+        else:
             csc = D.mesh_csc([(dm.conn, ke)], dm.n_nodes, stream=main, order=dm.assembly_order(), prep=prep)
-        except MeshValidationError:
-            for f in fails:  # an out-of-range node id is reported as the element's NodeIndexError
-                D.raise_if_failed(f, n_nodes=dm.n_nodes)
-            raise
+    except MeshValidationError:
+        for f in fails:  # an out-of-range node id is reported as the element's NodeIndexError
+            D.raise_if_failed(f, n_nodes=dm.n_nodes)
+        raise
     if cached is None:  # a planned rebuild stays asynchronous: check the fail records later
         for f in fails:
             D.raise_if_failed(f, n_nodes=dm.n_nodes)
