@@ -154,6 +154,15 @@ int hx_integrate_mesh_adjacency(const double *coords, int64_t n_nodes, const int
 int hx_connectivity_index_arrays(const int32_t *conn, int64_t lo, int64_t hi, int32_t *rows,
                                  int32_t *cols, void *stream);
 
+/* assemble.py:65-83 map_local_to_global for dofxn >= 1, element-major over elements [lo, hi):
+ * rows/cols ((8 dofxn)(8 dofxn + 1)/2 * (hi-lo),) i32 -- local dof i = a * dofxn + k of node a is
+ * global dof conn[e][a] * dofxn + k (node-major blocks), pairs in np.tril_indices(8 dofxn) order,
+ * swapped to (max, min).  Assemble them with hx_triplet_csc_* (dim = n_nodes * dofxn).
+ * n_nodes * dofxn must fit int32; 1 <= dofxn <= HX_MAX_DOFXN. */
+#define HX_MAX_DOFXN 16
+int hx_dof_index_arrays(const int32_t *conn, int64_t lo, int64_t hi, int64_t n_nodes, int32_t dofxn,
+                        int32_t *rows, int32_t *cols, void *stream);
+
 /* ---- mesh-path assembly (node-adjacency symbolic + deterministic column numeric) ---------
  * Builds the lower-triangular CSC block for columns [col_lo, col_hi) of a mesh with
  * n_nodes nodes, from element segments in ascending global element order.

@@ -13,6 +13,7 @@ from .oracle import (  # noqa: F401
     PACK_ROWS,
     connectivity_index_arrays,
     dn_table,
+    dof_index_arrays,
     export_matrix_market_text,
     pairwise_sum,
     reduceat_model,

@@ -104,6 +104,18 @@ def connectivity_index_arrays(conn, lo=0, hi=None):
     return np.maximum(gr, gc).reshape(-1), np.minimum(gr, gc).reshape(-1)
 
 
+def dof_index_arrays(conn, dofxn, lo=0, hi=None):
+    """assemble.py:65-83 map_local_to_global applied to every element of [lo, hi), element-major:
+    dofs = node * dofxn + k (node-major blocks), pairs in np.tril_indices(8 dofxn) order, swapped to
+    (max, min); int32 like connectivity_index_arrays (assemble.py:86-93)."""
+    c = np.asarray(conn)[lo:hi].astype(np.int64)
+    ndof = 8 * dofxn
+    dofs = (c[:, :, None] * dofxn + np.arange(dofxn)[None, None, :]).reshape(c.shape[0], ndof)
+    li, lj = np.tril_indices(ndof)
+    gr, gc = dofs[:, li], dofs[:, lj]
+    return (np.maximum(gr, gc).reshape(-1).astype(np.int32), np.minimum(gr, gc).reshape(-1).astype(np.int32))
+
+
 class OracleValidationError(ValueError):
     """Raised where the reference raises MeshValidationError (assemble.py:143-149)."""
 

@@ -12,6 +12,8 @@ from .assemble import (
     LowerCscMatrix,
     TripletMatrix,
     assemble_direct,
+    assemble_dof,
+    dof_index_arrays,
     build_triplet,
     connectivity_index_arrays,
     map_local_to_global,

@@ -32,6 +32,7 @@ EXPORTED = (
     "hx_abi_version", "hx_last_error", "hx_dn_table", "hx_pack_tables", "hx_device_sm_count",
     "hx_selftest_division",
     "hx_stiffness_batch", "hx_integrate_mesh", "hx_integrate_mesh_adjacency", "hx_connectivity_index_arrays",
+    "hx_dof_index_arrays",
     "hx_mesh_csc_workspace_bytes", "hx_mesh_csc_symbolic", "hx_mesh_csc_build", "hx_mesh_csc_numeric",
     "hx_mesh_csc_emit",
     "hx_triplet_csc_workspace_bytes", "hx_triplet_csc_symbolic", "hx_triplet_csc_numeric",
@@ -89,6 +90,7 @@ def lib():
         "hx_integrate_mesh": ([P, I64, P, P, I64, I64, P, P, P, I32, P, P], ctypes.c_int),
         "hx_integrate_mesh_adjacency": ([P, I64, P, P, I64, I64, P, P, P, I32, P, P, I64, P, I32, P], ctypes.c_int),
         "hx_connectivity_index_arrays": ([P, I64, I64, P, P, P], ctypes.c_int),
+        "hx_dof_index_arrays": ([P, I64, I64, I64, I32, P, P, P], ctypes.c_int),
         "hx_mesh_csc_workspace_bytes": ([I64, I64], I64),
         "hx_mesh_csc_symbolic": ([P, I32, I64, I64, I64, P, P, I64, P, I64, P, I32, P], ctypes.c_int),
         "hx_mesh_csc_build": ([P, I32, I64, I64, I64, P, P, P, I64, P, I64, P, I32, P], ctypes.c_int),

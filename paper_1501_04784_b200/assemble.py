@@ -23,7 +23,8 @@ from .integrate import LocalValuesBatch
 
 __all__ = [
     "TripletMatrix", "LowerCscMatrix", "map_local_to_global", "connectivity_index_arrays", "build_triplet",
-    "triplet_to_csc", "DirectAssembler", "assemble_direct", "nnz_compression", "csc_to_host",
+    "triplet_to_csc", "DirectAssembler", "assemble_direct", "nnz_compression", "csc_to_host", "dof_index_arrays",
+    "assemble_dof",
 ]
 
 
@@ -82,6 +83,34 @@ def connectivity_index_arrays(mesh, lo: int = 0, hi: int | None = None):
         return np.empty(0, dtype=np.int32), np.empty(0, dtype=np.int32)
     rows, cols = D.connectivity_index_arrays(_device_conn(mesh), lo, hi)
     return rows.cpu().numpy(), cols.cpu().numpy()
+
+
+def dof_index_arrays(mesh, dofxn: int = 1, lo: int = 0, hi: int | None = None):
+    """map_local_to_global (assemble.py:65-83) of elements [lo, hi), element-major, on the GPU ->
+    (rows, cols) int32 ((8 dofxn)(8 dofxn + 1)/2 per element, node-major dof blocks); dofxn = 1
+    equals connectivity_index_arrays."""
+    if dofxn < 1:
+        raise ValueError(f"dofxn must be at least 1, got {dofxn}")
+    n_el = mesh.n_el
+    hi = n_el if hi is None else min(hi, n_el)
+    lo = max(0, lo)
+    if hi <= lo:
+        return np.empty(0, dtype=np.int32), np.empty(0, dtype=np.int32)
+    rows, cols = D.dof_index_arrays(_device_conn(mesh), mesh.n_nodes, dofxn, lo, hi)
+    return rows.cpu().numpy(), cols.cpu().numpy()
+
+
+def assemble_dof(mesh, values, dofxn: int) -> LowerCscMatrix:
+    """Lower K (dim n_nodes * dofxn) of per-element packed matrices values (n_el, P) f64, P =
+    (8 dofxn)(8 dofxn + 1)/2 in map_local_to_global order: build_triplet + triplet_to_csc
+    (assemble.py:96-140) on the GPU, numpy's summation rule."""
+    P = (8 * dofxn) * (8 * dofxn + 1) // 2
+    values = np.ascontiguousarray(values, dtype=np.float64)
+    if values.shape != (mesh.n_el, P):
+        raise ValueError(f"values must be ({mesh.n_el}, {P}), got {values.shape}")
+    conn = _device_conn(mesh)
+    csc = D.assemble_dof(conn, torch.from_numpy(values).to(conn.device), mesh.n_nodes, dofxn)
+    return csc_to_host(csc)
 
 
 def build_triplet(mesh, values: LocalValuesBatch, rows=None, cols=None) -> TripletMatrix:

@@ -733,6 +733,31 @@ __global__ void index_kernel(const int32_t *__restrict__ conn, int64_t lo, int64
     }
 }
 
+// map_local_to_global for dofxn >= 1 (assemble.py:65-83), element-major over a range: local dof
+// i = a * dofxn + k of node a is global dof g[a] * dofxn + k (node-major blocks); element e's
+// (8 dofxn)(8 dofxn + 1)/2 pairs follow np.tril_indices(8 dofxn) (row-major lower triangle,
+// li >= lj) and are swapped to (max, min).  dofxn = 1 is connectivity_index_arrays.
+__global__ void dof_index_kernel(const int32_t *__restrict__ conn, int64_t lo, int64_t n, int32_t dofxn,
+                                 int32_t *__restrict__ rows, int32_t *__restrict__ cols) {
+    const int64_t P = (int64_t)(8 * dofxn) * (8 * dofxn + 1) / 2;
+    const int64_t total = P * n;
+    for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < total;
+         w += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t k = w / P;
+        const int p = (int)(w - k * P);
+        // row li of the packed lower triangle: li (li + 1) / 2 <= p < (li + 1)(li + 2) / 2
+        int li = (int)((sqrt(8.0 * p + 1.0) - 1.0) * 0.5);
+        while (li * (li + 1) / 2 > p) --li;
+        while ((li + 1) * (li + 2) / 2 <= p) ++li;
+        const int lj = p - li * (li + 1) / 2;
+        const int32_t *c = conn + 8 * (lo + k);
+        const int32_t gi = __ldg(c + li / dofxn) * dofxn + li % dofxn;
+        const int32_t gj = __ldg(c + lj / dofxn) * dofxn + lj % dofxn;
+        rows[w] = max(gi, gj);
+        cols[w] = min(gi, gj);
+    }
+}
+
 constexpr size_t GP_SMEM = GP_WARPS * sizeof(GpWarpSmem);  // dynamic shared memory per block
 
 // Opt the integration kernels into dynamic shared memory beyond the default (once per device).
@@ -963,5 +988,26 @@ extern "C" int hx_connectivity_index_arrays(const int32_t *conn, int64_t lo, int
     const int64_t blocks = std::min<int64_t>(ceil_div(36 * n, threads), 148 * 16);
     index_kernel<<<(unsigned)blocks, threads, 0, (cudaStream_t)stream>>>(conn, lo, n, rows, cols);
     HX_CHECK_LAUNCH("index_kernel");
+    return HX_OK;
+}
+
+extern "C" int hx_dof_index_arrays(const int32_t *conn, int64_t lo, int64_t hi, int64_t n_nodes, int32_t dofxn,
+                                   int32_t *rows, int32_t *cols, void *stream) {
+    if (lo < 0 || hi < lo || dofxn < 1 || dofxn > HX_MAX_DOFXN || (hi > lo && (rows == nullptr || cols == nullptr))) {
+        set_last_error("hx_dof_index_arrays: bad arguments (dofxn must be in [1, %d])", HX_MAX_DOFXN);
+        return HX_ERR_VALUE;
+    }
+    if (n_nodes * (int64_t)dofxn > INT32_MAX) {
+        set_last_error("hx_dof_index_arrays: %lld nodes x %d dofs exceed the int32 index range",
+                       (long long)n_nodes, dofxn);
+        return HX_ERR_VALUE;
+    }
+    const int64_t n = hi - lo;
+    if (n == 0) return HX_OK;
+    const int64_t P = (int64_t)(8 * dofxn) * (8 * dofxn + 1) / 2;
+    const int threads = 256;
+    const int64_t blocks = std::min<int64_t>(ceil_div(P * n, threads), 148 * 16);
+    dof_index_kernel<<<(unsigned)blocks, threads, 0, (cudaStream_t)stream>>>(conn, lo, n, dofxn, rows, cols);
+    HX_CHECK_LAUNCH("dof_index_kernel");
     return HX_OK;
 }

@@ -20,7 +20,7 @@ from .errors import ConfigurationError, DegenerateElementError, MeshValidationEr
 
 __all__ = [
     "DeviceMesh", "DeviceCsc", "AssemblyPrep", "new_assembly_prep", "rows_narrow", "require_device", "stream_handle", "integrate_mesh", "stiffness_batch",
-    "connectivity_index_arrays", "raise_if_failed", "mesh_csc", "triplet_csc", "MeshPlan", "mesh_plan_async",
+    "connectivity_index_arrays", "dof_index_arrays", "assemble_dof", "raise_if_failed", "mesh_csc", "triplet_csc", "MeshPlan", "mesh_plan_async",
     "mesh_emit", "plan_assembly", "block_elements", "generate_cube_mesh",
 ]
 
@@ -267,6 +267,34 @@ def connectivity_index_arrays(conn: torch.Tensor, lo: int = 0, hi: int | None = 
     N.check(N.lib().hx_connectivity_index_arrays(_ptr(conn), lo, hi, _ptr(rows), _ptr(cols),
                                                  stream_handle(stream)), "hx_connectivity_index_arrays")
     return rows, cols
+
+
+def dof_index_arrays(conn: torch.Tensor, n_nodes: int, dofxn: int = 1, lo: int = 0, hi: int | None = None,
+                     stream=None):
+    """map_local_to_global (assemble.py:65-83) for every element of [lo, hi) on device ->
+    (rows, cols) int32 (P * (hi-lo),), P = (8 dofxn)(8 dofxn + 1)/2, element-major, each element's
+    pairs in np.tril_indices(8 dofxn) order; dofxn = 1 equals connectivity_index_arrays."""
+    hi = conn.shape[0] if hi is None else hi
+    _check_tensor(conn, torch.int32, (conn.shape[0], 8), "conn")
+    if dofxn < 1:
+        raise ValueError(f"dofxn must be at least 1, got {dofxn}")
+    P = (8 * dofxn) * (8 * dofxn + 1) // 2
+    n = hi - lo
+    rows = torch.empty(P * n, dtype=torch.int32, device=conn.device)
+    cols = torch.empty(P * n, dtype=torch.int32, device=conn.device)
+    N.check(N.lib().hx_dof_index_arrays(_ptr(conn), lo, hi, n_nodes, dofxn, _ptr(rows), _ptr(cols),
+                                        stream_handle(stream)), "hx_dof_index_arrays")
+    return rows, cols
+
+
+def assemble_dof(conn: torch.Tensor, values: torch.Tensor, n_nodes: int, dofxn: int, stream=None) -> "DeviceCsc":
+    """Lower CSC of a dofxn-per-node element matrix set: values (n_el, P) f64 in packed
+    np.tril_indices(8 dofxn) order -> K of dim n_nodes * dofxn, through the generic triplet path
+    (build_triplet + triplet_to_csc, assemble.py:96-140, numpy's summation rule for any run)."""
+    P = (8 * dofxn) * (8 * dofxn + 1) // 2
+    _check_tensor(values, torch.float64, (conn.shape[0], P), "values")
+    rows, cols = dof_index_arrays(conn, n_nodes, dofxn, stream=stream)
+    return triplet_csc(rows, cols, values.reshape(-1), n_nodes * dofxn, stream=stream)
 
 
 @dataclass

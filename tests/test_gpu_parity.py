@@ -1010,3 +1010,46 @@ def test_out_of_core_budget_takes_streamed_blocks():
     budget = device_bytes(mesh.n_el, mesh.n_nodes) // 4
     m, rep = run_build(mesh, budget_bytes=10**12, device_budget_bytes=budget)
     assert bits_equal(m.col_ptr, cp) and bits_equal(m.row_idx, ri) and bits_equal(m.vals, vv)
+
+
+@pytest.mark.parametrize("d", [1, 2, 3, 5])
+def test_dof_index_arrays_and_assembly_bitwise(d):
+    """dofxn > 1 (assemble.py:65-83): the index kernel vs the reference's
+    map_local_to_global (golden, d = 2, 3) and the oracle; the generic triplet assembly of the
+    block matrix vs the reference's triplet_to_csc (golden) / the oracle."""
+    from pathlib import Path
+
+    g = np.load(Path(__file__).parent / "golden" / "dof.npz")
+    n_nodes = int(g["n_nodes"])
+    conn = torch.from_numpy(g["conn"]).cuda()
+    rows, cols = D.dof_index_arrays(conn, n_nodes, d)
+    r_o, c_o = oracle.dof_index_arrays(g["conn"], d)
+    assert bits_equal(rows.cpu().numpy(), r_o) and bits_equal(cols.cpu().numpy(), c_o)
+    P = (8 * d) * (8 * d + 1) // 2
+    if f"d{d}_pairs" in g:
+        assert np.array_equal(rows.cpu().numpy(), g[f"d{d}_pairs"][:, 0])
+        vals = g[f"d{d}_vals"]
+    else:
+        vals = np.random.default_rng(d).standard_normal(g["conn"].shape[0] * P)
+    csc = D.assemble_dof(conn, torch.from_numpy(vals.reshape(-1, P)).cuda(), n_nodes, d)
+    col_ptr, row_idx, v = oracle.triplet_to_csc(r_o, c_o, vals, n_nodes * d)
+    assert bits_equal(csc.col_ptr.cpu().numpy(), col_ptr) and bits_equal(csc.row_idx.cpu().numpy(), row_idx)
+    assert bits_equal(csc.vals.cpu().numpy(), v)
+    if f"d{d}_pairs" in g:
+        assert bits_equal(csc.vals.cpu().numpy(), g[f"d{d}_csc_vals"])
+    # a larger permuted mesh, index arrays only, over a sub-range
+    mesh = make_workload("C1")
+    cd = torch.from_numpy(mesh.connectivity).cuda()
+    r2, c2 = D.dof_index_arrays(cd, mesh.n_nodes, d, lo=100, hi=2100)
+    r_o2, c_o2 = oracle.dof_index_arrays(mesh.connectivity, d, lo=100, hi=2100)
+    assert bits_equal(r2.cpu().numpy(), r_o2) and bits_equal(c2.cpu().numpy(), c_o2)
+
+
+def test_dof_index_arrays_rejects_bad_dofxn():
+    conn = torch.zeros((1, 8), dtype=torch.int32, device="cuda")
+    with pytest.raises(ValueError):
+        D.dof_index_arrays(conn, 1, 0)
+    with pytest.raises(ValueError):
+        D.dof_index_arrays(conn, 1, 17)
+    with pytest.raises(ValueError):
+        D.dof_index_arrays(conn, 2**30, 4)

@@ -1,5 +1,7 @@
 """Pin the CPU oracle against the reference's own outputs (golden vectors + digests)."""
 
+from pathlib import Path
+
 import numpy as np
 import pytest
 
@@ -105,3 +107,22 @@ def test_column_window_restatement_equals_full_assembly(golden):
             assert np.array_equal(a, cp[c0:c1 + 1] - cp[c0])
             assert np.array_equal(b, ri[cp[c0]:cp[c1]])
             assert v.tobytes() == vv[cp[c0]:cp[c1]].tobytes()
+
+
+@pytest.mark.parametrize("d", [2, 3])
+def test_dof_index_arrays_match_reference_mapping(d):
+    """oracle.dof_index_arrays == the reference's map_local_to_global, element by element
+    (tests/golden/dof.npz, made by tests/golden/make_golden_dof.py), and its triplet_to_csc."""
+    g = np.load(Path(__file__).parent / "golden" / "dof.npz")
+    rows, cols = oracle.dof_index_arrays(g["conn"], d)
+    assert np.array_equal(rows, g[f"d{d}_pairs"][:, 0]) and np.array_equal(cols, g[f"d{d}_pairs"][:, 1])
+    col_ptr, row_idx, vals = oracle.triplet_to_csc(rows, cols, g[f"d{d}_vals"], int(g["n_nodes"]) * d)
+    assert bits_equal(col_ptr, g[f"d{d}_col_ptr"]) and bits_equal(row_idx, g[f"d{d}_row_idx"])
+    assert bits_equal(vals, g[f"d{d}_csc_vals"])
+
+
+def test_dof_index_arrays_dofxn1_is_connectivity_index_arrays():
+    conn = make_workload("C1").connectivity[:500]
+    r1, c1 = oracle.dof_index_arrays(conn, 1)
+    r0, c0 = oracle.connectivity_index_arrays(conn)
+    assert bits_equal(r1, r0) and bits_equal(c1, c0)
