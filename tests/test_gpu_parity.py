@@ -970,7 +970,7 @@ def test_streamed_plan_rejects_permuted_and_overflow_falls_back(monkeypatch):
 
     perm = permuted_mesh(perturbed_mesh(10, seed=1), seed=2)
     assert stream.plan(perm, 8) is None
-    mesh = perturbed_mesh(10, seed=3)
+    mesh = perturbed_mesh(20, seed=3)  # 4 blocks: the halo layers stay within MAX_RANGE_OVERLAP
     sp = stream.plan(mesh, 4)
     assert sp is not None and sp.max_block_elements() < mesh.n_el
     assert stream.streamed_build(mesh, sp, capacity=100) is None  # result outgrows the buffers
