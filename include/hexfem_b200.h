@@ -78,6 +78,11 @@ extern "C" {
 #define HX_CSC_ADJACENCY_READY 2  /* hx_mesh_csc_build only: the workspace's node adjacency and the status
                                    * word were filled by hx_integrate_mesh_adjacency over every element
                                    * (one segment, columns [0, n_nodes)); the build skips its first pass */
+#define HX_CSC_FIXED_ADJACENCY 4  /* symbolic/build: record the node adjacency in fixed slots (element e puts
+                                   * e << 3 | a in slot a of its local node a; plain stores, no atomic
+                                   * counter) -- one segment, columns [0, n_nodes).  Two elements holding one
+                                   * node at the same local index raise HX_ST_SLOT_COLLISION: re-run
+                                   * without the flag */
 
 /* Integration modes. */
 #define HX_MODE_EXACT 0 /* reference operation order, no FMA: bitwise equal to the reference */
@@ -193,6 +198,24 @@ int hx_mesh_csc_emit(const hx_elem_segment *segs, int32_t n_segs, int64_t col_lo
 int hx_mesh_csc_numeric(const hx_elem_segment *segs, int32_t n_segs, int64_t col_lo,
                         int64_t col_hi, const int64_t *col_ptr, const int64_t *row_idx,
                         double *vals, const void *workspace, uint32_t *status, void *stream);
+
+/* ---- integration fused with the emit pass (the cold build's second phase) ----------------------
+ * hx_integrate_mesh (KE + iK/jK of every element, same outputs, fail record and bitwise results)
+ * and hx_mesh_csc_emit (row_idx / vals of every column) in ONE persistent launch: the warps take
+ * element quads and, as soon as every element a column tile touches has been integrated, the
+ * tile's emit -- its KE gathers then hit the L2 lines the integration just wrote, and the DRAM-bound
+ * emit work runs under the FP64-bound integration.  csc_workspace / col_ptr / csc_status: a plan of
+ * the same connectivity from hx_mesh_csc_symbolic (row_capacity 0, one segment, columns
+ * [0, n_nodes)); when its status word has a fast-path limit bit the launch only integrates and the
+ * caller re-assembles.  sched_ws: hx_integrate_emit_workspace_bytes(n_el) bytes (scheduling
+ * counters, reset by the call).  Entries beyond `capacity` are not written (re-run when
+ * col_ptr[n_nodes] > capacity). */
+int64_t hx_integrate_emit_workspace_bytes(int64_t n_el);
+int hx_integrate_emit(const double *coords, int64_t n_nodes, const int32_t *conn, const double *coeff, int64_t n_el,
+                      double *ke, int32_t *rows, int32_t *cols, int32_t mode, hx_fail_info *fail,
+                      const int64_t *col_ptr, int64_t *row_idx, double *vals, int64_t capacity,
+                      const void *csc_workspace, const uint32_t *csc_status, void *sched_ws, int64_t sched_bytes,
+                      void *stream);
 
 /* ---- generic triplet -> CSC (assemble.py:110-149) ----------------------------------------
  * symbolic: validates (status bits BAD_INDEX / UPPER), stable-sorts by (col,row), finds the

@@ -25,6 +25,7 @@ ST_FASTPATH_LIMITS = ST_DEG_OVERFLOW | ST_ROW_OVERFLOW | ST_REPEATED_NODE | ST_S
 MODE_EXACT, MODE_FAST = 0, 1
 CSC_ORDER_BY_ELEMENT = 1
 CSC_ADJACENCY_READY = 2
+CSC_FIXED_ADJACENCY = 4
 MAX_SEGMENTS = 4
 
 # Every symbol declared in include/hexfem_b200.h (checked by tests/test_abi_cpu.py).
@@ -34,7 +35,7 @@ EXPORTED = (
     "hx_stiffness_batch", "hx_integrate_mesh", "hx_integrate_mesh_adjacency", "hx_connectivity_index_arrays",
     "hx_dof_index_arrays",
     "hx_mesh_csc_workspace_bytes", "hx_mesh_csc_symbolic", "hx_mesh_csc_build", "hx_mesh_csc_numeric",
-    "hx_mesh_csc_emit",
+    "hx_mesh_csc_emit", "hx_integrate_emit_workspace_bytes", "hx_integrate_emit",
     "hx_triplet_csc_workspace_bytes", "hx_triplet_csc_symbolic", "hx_triplet_csc_numeric",
     "hx_column_weights", "hx_halo_workspace_bytes", "hx_halo_count", "hx_halo_pack",
     "hx_halo_unpack_workspace_bytes", "hx_halo_unpack", "hx_digest",
@@ -92,6 +93,8 @@ def lib():
         "hx_connectivity_index_arrays": ([P, I64, I64, P, P, P], ctypes.c_int),
         "hx_dof_index_arrays": ([P, I64, I64, I64, I32, P, P, P], ctypes.c_int),
         "hx_mesh_csc_workspace_bytes": ([I64, I64], I64),
+        "hx_integrate_emit_workspace_bytes": ([I64], I64),
+        "hx_integrate_emit": ([P, I64, P, P, I64, P, P, P, I32, P, P, P, P, I64, P, P, P, I64, P], ctypes.c_int),
         "hx_mesh_csc_symbolic": ([P, I32, I64, I64, I64, P, P, I64, P, I64, P, I32, P], ctypes.c_int),
         "hx_mesh_csc_build": ([P, I32, I64, I64, I64, P, P, P, I64, P, I64, P, I32, P], ctypes.c_int),
         "hx_mesh_csc_numeric": ([P, I32, I64, I64, P, P, P, P, P, P], ctypes.c_int),

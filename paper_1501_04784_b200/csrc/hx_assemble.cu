@@ -31,6 +31,7 @@
 #include <type_traits>
 
 #include "hx_common.cuh"
+#include "hx_ke_device.cuh"
 
 namespace hx {
 
@@ -91,6 +92,23 @@ __global__ void adjacency_kernel(SegTable T, int64_t n_total, int64_t n_nodes, i
             if (slot < MAXDEG) adj[8 * c + slot] = (int32_t)((e << 3) | a);
             else atomicOr(status, HX_ST_DEG_OVERFLOW);
         }
+    }
+}
+
+// 1'. fixed-slot adjacency (HX_CSC_FIXED_ADJACENCY; single dense segment, every column): element e
+// stores (e << 3 | a) into slot a of its local node a -- a plain store, no counter -- after the slots
+// were emptied to -1.  Two elements holding one node at the same local index collide; the pattern
+// pass counts the filled slots and the caller then re-runs with the atomic adjacency.
+__global__ void adjacency_fixed_kernel(const int32_t *__restrict__ conn, int64_t n_total, int64_t n_nodes,
+                                       int32_t *__restrict__ adj, uint32_t *__restrict__ status) {
+    for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < 8 * n_total;
+         w += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t v = __ldg(conn + w);
+        if (v < 0 || (int64_t)v >= n_nodes) {
+            atomicOr(status, HX_ST_BAD_INDEX);
+            continue;
+        }
+        adj[8 * (int64_t)v + (w & 7)] = (int32_t)w;  // w = (e << 3) | a
     }
 }
 
@@ -389,14 +407,18 @@ __device__ __forceinline__ void sort_count(K *L, int n, int &rows, bool &ok) {
 template <typename K, bool SINGLE, bool FIXED>
 __device__ __forceinline__ int column_pattern_sort(const SegTable &T, bool active, int64_t cl, int32_t c,
                                                    int32_t *__restrict__ deg_arr, int32_t *__restrict__ adj, K *L,
-                                                   int &cnt, int &deg, uint32_t *__restrict__ status) {
+                                                   int &cnt, int &deg, int32_t &last, uint32_t *__restrict__ status) {
     int m = 0;
     deg = 0;
+    last = -1;
     int32_t ent[8];
     cnt = 0;
     if (active) {
         deg = incident_sorted<FIXED>(cl, deg_arr, adj, ent, status);
         if (deg < 0) deg = 0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+            if (k < deg) last = max(last, ent[k] >> 3);
         if (deg > 0) {  // the emit pass reads the sorted incident list
             int4 *a4 = reinterpret_cast<int4 *>(adj + 8 * cl);
             a4[0] = make_int4(ent[0], ent[1], ent[2], ent[3]);
@@ -463,7 +485,8 @@ pattern_kernel(SegTable T, int64_t col_lo, int64_t ncols, int32_t *__restrict__ 
                int32_t *__restrict__ adj, int64_t *__restrict__ col_ptr, int2 *__restrict__ scratch,
                int64_t scratch_capacity, unsigned long long *__restrict__ scratch_top,
                int64_t *__restrict__ block_scratch, uint32_t *__restrict__ status,
-               const uint32_t *__restrict__ order, unsigned long long *__restrict__ slot_total) {
+               const uint32_t *__restrict__ order, unsigned long long *__restrict__ slot_total,
+               int32_t *__restrict__ tile_need) {
 #if HX_PATTERN_SORT
     __shared__ K sL[SORT_SLOTS * COL_BLOCK];  // this thread's contribution keys, [slot][thread]
 #else
@@ -482,7 +505,13 @@ pattern_kernel(SegTable T, int64_t col_lo, int64_t ncols, int32_t *__restrict__ 
 #if HX_PATTERN_SORT
     K *L = sL + t;
     int cnt = 0, deg = 0;
-    const int m = column_pattern_sort<K, SINGLE, FIXED>(T, cl < ncols, cl, c, deg_arr, adj, L, cnt, deg, status);
+    int32_t last = -1;
+    const int m =
+        column_pattern_sort<K, SINGLE, FIXED>(T, cl < ncols, cl, c, deg_arr, adj, L, cnt, deg, last, status);
+    {  // elements the tile's emit needs: every incident element < tile_need (the fused kernel waits for them)
+        const int need = __reduce_max_sync(0xffffffffu, last + 1);
+        if ((t & 31) == 0) atomicMax(tile_need + blockIdx.x, need);
+    }
 #else
     int32_t *H = sH + t;
     uint32_t *W = sW + t;
@@ -490,6 +519,7 @@ pattern_kernel(SegTable T, int64_t col_lo, int64_t ncols, int32_t *__restrict__ 
     int32_t ent[8];
     int deg = 0;
     const int m = column_pattern<K, SINGLE, true, FIXED>(T, cl < ncols, cl, c, deg_arr, adj, H, W, L, ent, deg, status);
+    if (t == 0) tile_need[blockIdx.x] = INT32_MAX;  // hash variant: no incident maximum, wait for every element
 #endif
     if (cl < ncols) col_ptr[cl] = m;
     if (FIXED) {
@@ -571,7 +601,9 @@ __device__ __forceinline__ uint64_t ke_policy() {
 #endif
     return p;
 }
+template <bool LOAD_CG>
 __device__ __forceinline__ double ke_load(const double *ptr, uint64_t pol) {
+    if (LOAD_CG) return __ldcg(ptr);
 #if HX_EMIT_KE_HINT == 1
     double v;
     asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(ptr), "l"(pol));
@@ -586,50 +618,82 @@ __device__ __forceinline__ double ke_load(const double *ptr, uint64_t pol) {
 #endif
 }
 
-template <bool ROWS, bool VALS, bool SINGLE>
-__global__ void __launch_bounds__(EMIT_BLOCK)
-emit_kernel(SegTable T, int64_t col_lo, int64_t ncols, const int32_t *__restrict__ deg_arr,
-            const int32_t *__restrict__ adj, const int64_t *__restrict__ col_ptr, const int2 *__restrict__ scratch,
-            const int64_t *__restrict__ block_scratch, int64_t *__restrict__ row_idx, double *__restrict__ vals,
-            int64_t capacity, const uint32_t *__restrict__ status, const uint32_t *__restrict__ order_flag,
-            const uint32_t *__restrict__ order) {
-    // the pattern pass hit a fast-path limit: its records are incomplete and the caller re-runs
-    if (*status & (HX_ST_DEG_OVERFLOW | HX_ST_ROW_OVERFLOW | HX_ST_REPEATED_NODE | HX_ST_SCRATCH_OVERFLOW |
-                   HX_ST_SLOT_COLLISION))
-        return;
+// Shared state of one emit tile (aliases the integration warp's staging in the fused kernel).
+struct EmitSmem {
+    int64_t s_start[COL_BLOCK];       // first output entry of each column of the tile
+    int32_t s_m[COL_BLOCK + 1];       // entries per column
+    int32_t s_cl[COL_BLOCK];          // column (block-local index) of each tile position
+    int32_t s_rs[COL_BLOCK + 1];      // first scratch record of each column (tile-relative)
+    int32_t s_deg[COL_BLOCK];
+    int32_t s_adj[COL_BLOCK * 8];     // the tile's sorted incident lists
+    uint8_t s_col[COL_BLOCK * MAXR];  // tile position of each off-diagonal record
+};
+
+// Arguments of the emit pass over one column range (the pattern pass's workspace + outputs).
+struct EmitArgs {
+    SegTable T;
+    int64_t col_lo, ncols;
+    const int32_t *deg_arr, *adj;
+    const int64_t *col_ptr;
+    const int2 *scratch;
+    const int64_t *block_scratch;
+    int64_t *row_idx;
+    double *vals;
+    int64_t capacity;
+    const uint32_t *order_flag, *order;
+};
+
+constexpr uint32_t HX_ST_EMIT_SKIP =
+    HX_ST_DEG_OVERFLOW | HX_ST_ROW_OVERFLOW | HX_ST_REPEATED_NODE | HX_ST_SCRATCH_OVERFLOW | HX_ST_SLOT_COLLISION;
+
+template <int NT>
+__device__ __forceinline__ void tile_sync() {
+    if (NT == 32) __syncwarp();
+    else __syncthreads();
+}
+
+// Emit tile `tile` (COL_BLOCK columns of the processing order) with NT threads (tid = 0..NT-1):
+// row_idx / vals of its columns.  LOAD_CG: KE gathers through L2 only (the fused kernel reads KE
+// rows that other SMs stored during the same launch).
+template <int NT, bool ROWS, bool VALS, bool SINGLE, bool LOAD_CG>
+__device__ __forceinline__ void emit_tile(EmitSmem &S, const EmitArgs &A, int64_t tile, int tid) {
+    const SegTable &T = A.T;
+    const int64_t col_lo = A.col_lo, ncols = A.ncols, capacity = A.capacity;
+    const int32_t *__restrict__ deg_arr = A.deg_arr;
+    const int32_t *__restrict__ adj = A.adj;
+    const int64_t *__restrict__ col_ptr = A.col_ptr;
+    const int2 *__restrict__ scratch = A.scratch;
+    const int64_t *__restrict__ block_scratch = A.block_scratch;
+    int64_t *__restrict__ row_idx = A.row_idx;
+    double *__restrict__ vals = A.vals;
+    const uint32_t *__restrict__ order_flag = A.order_flag;
+    const uint32_t *__restrict__ order = A.order;
     const bool ordered = *order_flag != 0u;
     const uint64_t pol = ke_policy();
-    __shared__ int64_t s_start[COL_BLOCK];       // first output entry of each column of the tile
-    __shared__ int32_t s_m[COL_BLOCK + 1];       // entries per column
-    __shared__ int32_t s_cl[COL_BLOCK];          // column (block-local index) of each tile position
-    __shared__ int32_t s_rs[COL_BLOCK + 1];      // first scratch record of each column (tile-relative)
-    __shared__ int32_t s_deg[COL_BLOCK];
-    __shared__ int32_t s_adj[COL_BLOCK * 8];     // the tile's sorted incident lists
-    __shared__ uint8_t s_col[COL_BLOCK * MAXR];  // tile position of each off-diagonal record
-    const int64_t first = (int64_t)blockIdx.x * COL_BLOCK;
+    const int64_t first = tile * COL_BLOCK;
     const int ncol = (int)(ncols - first < COL_BLOCK ? ncols - first : COL_BLOCK);
-    for (int u = threadIdx.x; u < ncol; u += EMIT_BLOCK) {
+    for (int u = tid; u < ncol; u += NT) {
         const int64_t cl = ordered ? (int64_t)__ldg(order + first + u) : first + u;
-        s_cl[u] = (int32_t)cl;
+        S.s_cl[u] = (int32_t)cl;
         const int64_t a = col_ptr[cl], b = col_ptr[cl + 1];
-        s_start[u] = a;
-        s_m[u] = (int)(b - a);
-        s_deg[u] = min(deg_arr[cl], MAXDEG);
+        S.s_start[u] = a;
+        S.s_m[u] = (int)(b - a);
+        S.s_deg[u] = min(deg_arr[cl], MAXDEG);
     }
-    __syncthreads();
+    tile_sync<NT>();
     if (VALS)
-        for (int i = threadIdx.x; i < ncol * 8; i += EMIT_BLOCK)
-            s_adj[i] = __ldg(adj + 8 * (int64_t)s_cl[i >> 3] + (i & 7));
+        for (int i = tid; i < ncol * 8; i += NT)
+            S.s_adj[i] = __ldg(adj + 8 * (int64_t)S.s_cl[i >> 3] + (i & 7));
     // scratch record offsets: column u has max(m_u - 1, 0) records (m_u = 0 for a node no element
     // references), laid out in tile order by the pattern pass -- warp 0 scans them
-    if (threadIdx.x < 32) {
+    if (tid < 32) {
         constexpr int PER = COL_BLOCK / 32;  // columns per lane, consecutive
-        const int l = threadIdx.x;
+        const int l = tid;
         int off[PER], sum = 0;
 #pragma unroll
         for (int i = 0; i < PER; ++i) {
             const int u = PER * l + i;
-            const int m = u < ncol ? s_m[u] : 0;
+            const int m = u < ncol ? S.s_m[u] : 0;
             off[i] = m > 0 ? m - 1 : 0;
             sum += off[i];
         }
@@ -642,25 +706,25 @@ emit_kernel(SegTable T, int64_t col_lo, int64_t ncols, const int32_t *__restrict
         int run = incl - sum;
 #pragma unroll
         for (int i = 0; i < PER; ++i) {
-            s_rs[PER * l + i] = run;
+            S.s_rs[PER * l + i] = run;
             run += off[i];
         }
-        if (l == 31) s_rs[COL_BLOCK] = incl;
+        if (l == 31) S.s_rs[COL_BLOCK] = incl;
     }
-    __syncthreads();
-    const int64_t sb = block_scratch[blockIdx.x];
-    const int n_off = s_rs[COL_BLOCK];
-    for (int u = threadIdx.x; u < ncol; u += EMIT_BLOCK)
-        for (int q = s_rs[u]; q < s_rs[u] + s_m[u] - 1; ++q) s_col[q] = (uint8_t)u;
-    __syncthreads();
+    tile_sync<NT>();
+    const int64_t sb = block_scratch[tile];
+    const int n_off = S.s_rs[COL_BLOCK];
+    for (int u = tid; u < ncol; u += NT)
+        for (int q = S.s_rs[u]; q < S.s_rs[u] + S.s_m[u] - 1; ++q) S.s_col[q] = (uint8_t)u;
+    tile_sync<NT>();
     // diagonals
-    for (int u = threadIdx.x; u < ncol; u += EMIT_BLOCK) {
-        const int64_t o = s_start[u];
-        if (s_m[u] == 0 || o >= capacity) continue;
-        if (ROWS) __stcs(reinterpret_cast<long long *>(row_idx) + o, (long long)(col_lo + s_cl[u]));
+    for (int u = tid; u < ncol; u += NT) {
+        const int64_t o = S.s_start[u];
+        if (S.s_m[u] == 0 || o >= capacity) continue;
+        if (ROWS) __stcs(reinterpret_cast<long long *>(row_idx) + o, (long long)(col_lo + S.s_cl[u]));
         if (!VALS) continue;
-        const int deg = s_deg[u];
-        const int32_t *ent = s_adj + 8 * u;
+        const int deg = S.s_deg[u];
+        const int32_t *ent = S.s_adj + 8 * u;
         double x[8];
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
@@ -668,7 +732,7 @@ emit_kernel(SegTable T, int64_t col_lo, int64_t ncols, const int32_t *__restrict
             if (k < deg) {
                 const int32_t en = ent[k];
                 const int a = en & 7;
-                x[k] = ke_load(ke_row<SINGLE>(T, en >> 3) + pack_index(a, a), pol);
+                x[k] = ke_load<LOAD_CG>(ke_row<SINGLE>(T, en >> 3) + pack_index(a, a), pol);
             }
         }
         double v = x[0];
@@ -681,11 +745,11 @@ emit_kernel(SegTable T, int64_t col_lo, int64_t ncols, const int32_t *__restrict
         }
         __stcs(vals + o, v);
     }
-    // off-diagonals: record q of tile position u is output entry s_start[u] + 1 + (q - s_rs[u]).
+    // off-diagonals: record q of tile position u is output entry S.s_start[u] + 1 + (q - S.s_rs[u]).
     // Two records per thread per iteration: their KE gathers are independent and overlap.
     auto offdiag_value = [&](int u, uint32_t w) -> double {
         const int n = (int)(w & 7u);
-        const int32_t *ent = s_adj + 8 * u;
+        const int32_t *ent = S.s_adj + 8 * u;
         double x[MAX_OFFDIAG_CONTRIB];
 #pragma unroll
         for (int r = 0; r < MAX_OFFDIAG_CONTRIB; ++r) {
@@ -694,7 +758,7 @@ emit_kernel(SegTable T, int64_t col_lo, int64_t ncols, const int32_t *__restrict
                 const uint32_t kb = (w >> (3 + 6 * r)) & 63u;
                 const int32_t en = ent[kb >> 3];
                 const int a = en & 7, b = (int)(kb & 7u);
-                x[r] = ke_load(ke_row<SINGLE>(T, en >> 3) + pack_index(max(a, b), min(a, b)), pol);
+                x[r] = ke_load<LOAD_CG>(ke_row<SINGLE>(T, en >> 3) + pack_index(max(a, b), min(a, b)), pol);
             }
         }
         double v = x[0];
@@ -711,16 +775,16 @@ emit_kernel(SegTable T, int64_t col_lo, int64_t ncols, const int32_t *__restrict
 #define HX_EMIT_UNROLL 4
 #endif
     constexpr int R = HX_EMIT_UNROLL;  // records in flight per thread: their loads/gathers overlap
-    for (int q0 = threadIdx.x; q0 < n_off; q0 += R * EMIT_BLOCK) {
+    for (int q0 = tid; q0 < n_off; q0 += R * NT) {
         int u[R];
         int64_t o[R];
         int2 rec[R];
 #pragma unroll
         for (int i = 0; i < R; ++i) {
-            const int q = q0 + i * EMIT_BLOCK;
+            const int q = q0 + i * NT;
             const bool has = q < n_off;
-            u[i] = has ? s_col[q] : 0;
-            o[i] = has ? s_start[u[i]] + 1 + (q - s_rs[u[i]]) : capacity;
+            u[i] = has ? S.s_col[q] : 0;
+            o[i] = has ? S.s_start[u[i]] + 1 + (q - S.s_rs[u[i]]) : capacity;
             rec[i] = has ? __ldcs(scratch + sb + q) : make_int2(0, 0);  // streamed once: evict first
         }
         if (ROWS) {
@@ -738,6 +802,119 @@ emit_kernel(SegTable T, int64_t col_lo, int64_t ncols, const int32_t *__restrict
     }
 }
 
+template <bool ROWS, bool VALS, bool SINGLE>
+__global__ void __launch_bounds__(EMIT_BLOCK)
+emit_kernel(EmitArgs A, const uint32_t *__restrict__ status) {
+    // the pattern pass hit a fast-path limit: its records are incomplete and the caller re-runs
+    if (*status & HX_ST_EMIT_SKIP) return;
+    __shared__ EmitSmem S;
+    emit_tile<EMIT_BLOCK, ROWS, VALS, SINGLE, false>(S, A, blockIdx.x, threadIdx.x);
+}
+
+// ---------------------------------------------------------------------------------------------
+// 7. Integration fused with the emit pass (hx_integrate_emit).  The integration kernel's persistent
+// warps (hx_ke_device.cuh) run the emit tiles between their element quads: after every quad a warp
+// bumps its chunk's completion counter and, when the next emit tile (processing order) has every
+// incident element integrated -- tile_need from the pattern pass against the chunk counters -- it
+// claims the tile and emits it from the KE rows still in L2.  Once the quads are exhausted the warps
+// drain the remaining tiles, waiting for their chunks.  Deadlock-free: a warp waits only after its
+// own quads are done, and every quad it waits for has been claimed by a warp that never waits
+// before finishing it.  Same arithmetic as the separate kernels, so the results are bitwise equal.
+constexpr int FUSED_CHUNK_QUADS = 32;  // one completion counter per 32 quads (128 elements)
+
+struct FusedSched {
+    unsigned *done;             // per chunk: quads integrated
+    unsigned *wm;               // chunks known complete (monotone hint)
+    unsigned *tile_head;        // next emit tile of the processing order
+    const int32_t *tile_need;   // per tile: elements that must be integrated first
+    int64_t n_quads, n_chunks, n_tiles, n_el;
+};
+
+struct EmitHook {
+    EmitSmem *S;
+    const EmitArgs *A;
+    FusedSched sc;
+    int lane;
+    bool emit;
+
+    // lane 0: are elements [0, need_el) integrated (their KE rows stored)?
+    __device__ __forceinline__ bool chunks_ready(int64_t need_el) {
+        need_el = need_el < sc.n_el ? need_el : sc.n_el;
+        const int64_t cneed = (need_el + 4 * FUSED_CHUNK_QUADS - 1) / (4 * FUSED_CHUNK_QUADS);
+        unsigned w = *(volatile unsigned *)sc.wm;
+        if (w >= cneed) return true;
+        const unsigned w0 = w;
+        while (w < cneed) {
+            const unsigned full = w == sc.n_chunks - 1 ? (unsigned)(sc.n_quads - (int64_t)w * FUSED_CHUNK_QUADS)
+                                                       : (unsigned)FUSED_CHUNK_QUADS;
+            if (*(volatile unsigned *)(sc.done + w) < full) break;
+            ++w;
+        }
+        if (w > w0) atomicMax(sc.wm, w);
+        return w >= cneed;
+    }
+    __device__ __forceinline__ void run_tile(int64_t t) {
+        __threadfence();  // the counted quads' KE stores before this tile's (L2) loads
+        __syncwarp();
+        emit_tile<32, true, true, true, true>(*S, *A, t, lane);
+        __syncwarp();  // the staging buffer is the integration's again
+    }
+    __device__ __forceinline__ void after_quad(int64_t q) {
+        __threadfence();  // this quad's KE / iK / jK stores before its completion count
+        __syncwarp();
+        if (lane == 0) atomicAdd(sc.done + q / FUSED_CHUNK_QUADS, 1u);
+        if (!emit) return;
+#pragma unroll 1
+        for (int it = 0; it < 2; ++it) {  // at most two ready tiles between quads
+            long long t = -1;
+            if (lane == 0) {
+                const unsigned h = *(volatile unsigned *)sc.tile_head;
+                if (h < sc.n_tiles && chunks_ready(__ldg(sc.tile_need + h)) && atomicCAS(sc.tile_head, h, h + 1) == h)
+                    t = h;
+            }
+            t = __shfl_sync(0xffffffffu, t, 0);
+            if (t < 0) return;
+            run_tile(t);
+        }
+    }
+    __device__ __forceinline__ void drain() {
+        if (!emit) return;
+#pragma unroll 1
+        while (true) {
+            unsigned h = 0;
+            if (lane == 0) h = atomicAdd(sc.tile_head, 1u);
+            h = __shfl_sync(0xffffffffu, h, 0);
+            if (h >= sc.n_tiles) return;
+            if (lane == 0) {
+                const int32_t need = __ldg(sc.tile_need + h);
+                while (!chunks_ready(need)) __nanosleep(256);
+            }
+            __syncwarp();
+            run_tile(h);
+        }
+    }
+};
+
+static_assert(sizeof(EmitSmem) <= sizeof(GpWarpSmem), "the emit tile aliases the warp's integration staging");
+constexpr size_t FUSED_SMEM = GP_WARPS * sizeof(GpWarpSmem);
+
+template <int MODE, bool WITH_INDEX>
+__global__ void __launch_bounds__(GP_BLOCK, HX_KE_MIN_BLOCKS)
+integrate_emit_kernel(const double *__restrict__ coords, int64_t n_nodes, const int32_t *__restrict__ conn,
+                      const double *__restrict__ coeff, int64_t n, double *__restrict__ ke_out,
+                      int32_t *__restrict__ rows_out, int32_t *__restrict__ cols_out,
+                      unsigned long long *__restrict__ fail_min, unsigned *__restrict__ quad_counter, EmitArgs A,
+                      FusedSched sc, const uint32_t *__restrict__ status) {
+    extern __shared__ __align__(16) unsigned char s_dyn[];
+    GpWarpSmem *s_warp = reinterpret_cast<GpWarpSmem *>(s_dyn);
+    __shared__ uint8_t s_pi[36], s_pj[36];
+    init_pack_smem(s_pi, s_pj);
+    __syncthreads();
+    GpWarpSmem &sm = s_warp[threadIdx.x >> 5];
+    EmitHook hook{reinterpret_cast<EmitSmem *>(&sm), &A, sc, (int)(threadIdx.x & 31), (*status & (HX_ST_EMIT_SKIP | HX_ST_BAD_INDEX)) == 0};
+    integrate_quads<MODE, WITH_INDEX, false, true>(sm, s_pi, s_pj, coords, n_nodes, conn, coeff, 0, n, ke_out, rows_out,
+                                                   cols_out, fail_min, quad_counter, AdjOut{nullptr, nullptr}, hook);
+}
 
 // Workspace layout (all offsets 256-B aligned):
 //   order_flag u32 | deg (ncols) i32 | adj (8*ncols) i32 | block_scratch (blocks) i64 |
@@ -750,6 +927,7 @@ struct MeshWs {
     uint32_t *order_flag;
     int32_t *deg, *adj;
     int64_t *block_scratch;
+    int32_t *tile_need;  // per tile: 1 + its highest incident element (0: none)
     unsigned long long *scratch_top, *slot_total;
     uint32_t *keys_in, *keys_out, *cols_in, *order;
     int2 *scratch;
@@ -780,6 +958,7 @@ static MeshWs mesh_ws_layout(void *base, int64_t ncols, int64_t workspace_bytes 
     const size_t o_deg = take(sizeof(int32_t) * nc);
     const size_t o_adj = take(sizeof(int32_t) * 8 * nc);
     const size_t o_bs = take(sizeof(int64_t) * std::max<int64_t>(1, ceil_div(ncols, COL_BLOCK)));
+    const size_t o_tn = take(sizeof(int32_t) * std::max<int64_t>(1, ceil_div(ncols, COL_BLOCK)));
     const size_t o_st = take(2 * sizeof(unsigned long long));  // scratch_top, slot_total
     const size_t o_ki = take(sizeof(uint32_t) * nc), o_ko = take(sizeof(uint32_t) * nc);
     const size_t o_ci = take(sizeof(uint32_t) * nc), o_or = take(sizeof(uint32_t) * nc);
@@ -796,6 +975,7 @@ static MeshWs mesh_ws_layout(void *base, int64_t ncols, int64_t workspace_bytes 
         w.deg = (int32_t *)(b + o_deg);
         w.adj = (int32_t *)(b + o_adj);
         w.block_scratch = (int64_t *)(b + o_bs);
+        w.tile_need = (int32_t *)(b + o_tn);
         w.scratch_top = (unsigned long long *)(b + o_st);
         w.slot_total = w.scratch_top + 1;
         w.keys_in = (uint32_t *)(b + o_ki);
@@ -870,6 +1050,34 @@ extern "C" int64_t hx_mesh_csc_workspace_bytes(int64_t n_el_total, int64_t n_col
     return (int64_t)mesh_ws_layout(nullptr, n_cols).total;
 }
 
+static EmitArgs emit_args(const SegTable &T, int64_t col_lo, int64_t ncols, const MeshWs &w, const int64_t *col_ptr,
+                          int64_t *row_idx, double *vals, int64_t capacity) {
+    EmitArgs A;
+    A.T = T;
+    A.col_lo = col_lo;
+    A.ncols = ncols;
+    A.deg_arr = w.deg;
+    A.adj = w.adj;
+    A.col_ptr = col_ptr;
+    A.scratch = w.scratch;
+    A.block_scratch = w.block_scratch;
+    A.row_idx = row_idx;
+    A.vals = vals;
+    A.capacity = capacity;
+    A.order_flag = w.order_flag;
+    A.order = w.order;
+    return A;
+}
+
+template <bool ROWS, bool VALS>
+static int launch_emit(const EmitArgs &A, const uint32_t *status, cudaStream_t s, const char *where) {
+    const unsigned tiles = (unsigned)ceil_div(A.ncols, COL_BLOCK);
+    if (!VALS || single_dense(A.T)) emit_kernel<ROWS, VALS, true><<<tiles, EMIT_BLOCK, 0, s>>>(A, status);
+    else emit_kernel<ROWS, VALS, false><<<tiles, EMIT_BLOCK, 0, s>>>(A, status);
+    HX_CHECK_LAUNCH(where);
+    return HX_OK;
+}
+
 static int mesh_csc_build(const hx_elem_segment *segs, int32_t n_segs, int64_t n_nodes, int64_t col_lo,
                           int64_t col_hi, int64_t *col_ptr, int64_t *row_idx, double *vals, int64_t row_capacity,
                           void *workspace, int64_t workspace_bytes, uint32_t *status, int32_t flags, void *stream) {
@@ -894,8 +1102,10 @@ static int mesh_csc_build(const hx_elem_segment *segs, int32_t n_segs, int64_t n
     const bool ordered = (flags & HX_CSC_ORDER_BY_ELEMENT) != 0 && ncols > 0 && n_total > 0;
     // adjacency (and its status bits) already recorded by hx_integrate_mesh_adjacency
     const bool adj_ready = (flags & HX_CSC_ADJACENCY_READY) != 0;
-    if (adj_ready && (n_segs != 1 || col_lo != 0 || col_hi != n_nodes || !single_conn(T))) {
-        set_last_error("hx_mesh_csc_build: HX_CSC_ADJACENCY_READY needs one segment and every column");
+    // fixed-slot adjacency: recorded by the integration kernel (adj_ready) or by adjacency_fixed_kernel
+    const bool fixed = adj_ready || (flags & HX_CSC_FIXED_ADJACENCY) != 0;
+    if (fixed && (n_segs != 1 || col_lo != 0 || col_hi != n_nodes || !single_conn(T))) {
+        set_last_error("hx_mesh_csc_build: a fixed-slot adjacency needs one segment and every column");
         return HX_ERR_VALUE;
     }
     if (!adj_ready) HX_TRY_CUDA(cudaMemsetAsync(status, 0, sizeof(uint32_t), s));
@@ -903,7 +1113,12 @@ static int mesh_csc_build(const hx_elem_segment *segs, int32_t n_segs, int64_t n
     if (ordered) HX_TRY_CUDA(cudaMemsetAsync(w.order_flag, 1, 1, s));  // little-endian u32 == 1
     if (ncols > 0) {
         if (!adj_ready) HX_TRY_CUDA(cudaMemsetAsync(w.deg, 0, sizeof(int32_t) * ncols, s));
-        if (n_total > 0 && !adj_ready) {
+        if (n_total > 0 && !adj_ready && fixed) {
+            HX_TRY_CUDA(cudaMemsetAsync(w.adj, 0xff, sizeof(int32_t) * 8 * ncols, s));
+            const unsigned grid = (unsigned)std::min<int64_t>(ceil_div(8 * n_total, 256), 148 * 64);
+            adjacency_fixed_kernel<<<grid, 256, 0, s>>>(T.conn[0], n_total, n_nodes, w.adj, status);
+            HX_CHECK_LAUNCH("adjacency_fixed_kernel");
+        } else if (n_total > 0 && !adj_ready) {
             const unsigned grid = (unsigned)std::min<int64_t>(ceil_div(8 * n_total, 256), 148 * 64);
             if (single_conn(T))
                 adjacency_kernel<true><<<grid, 256, 0, s>>>(T, n_total, n_nodes, col_lo, col_hi, w.deg, w.adj, status);
@@ -914,7 +1129,7 @@ static int mesh_csc_build(const hx_elem_segment *segs, int32_t n_segs, int64_t n
         const unsigned tiles = (unsigned)ceil_div(ncols, COL_BLOCK);
         if (ordered) {
             const unsigned g = (unsigned)std::min<int64_t>(ceil_div(ncols, 256), 148 * 32);
-            if (adj_ready)
+            if (fixed)
                 first_element_kernel<true><<<g, 256, 0, s>>>(ncols, w.deg, w.adj, (uint32_t)n_total, w.keys_in, w.cols_in);
             else
                 first_element_kernel<false><<<g, 256, 0, s>>>(ncols, w.deg, w.adj, (uint32_t)n_total, w.keys_in, w.cols_in);
@@ -927,14 +1142,15 @@ static int mesh_csc_build(const hx_elem_segment *segs, int32_t n_segs, int64_t n
         }
         const uint32_t *order = ordered ? w.order : nullptr;
         HX_TRY_CUDA(cudaMemsetAsync(w.scratch_top, 0, 2 * sizeof(unsigned long long), s));  // + slot_total
+        HX_TRY_CUDA(cudaMemsetAsync(w.tile_need, 0, sizeof(int32_t) * tiles, s));
         auto pattern = [&](auto key_tag, auto single_tag, auto fixed_tag) {
             using K = decltype(key_tag);
             pattern_kernel<K, decltype(single_tag)::value, decltype(fixed_tag)::value><<<tiles, COL_BLOCK, 0, s>>>(
                 T, col_lo, ncols, w.deg, w.adj, col_ptr, w.scratch, w.scratch_capacity, w.scratch_top, w.block_scratch,
-                status, order, w.slot_total);
+                status, order, w.slot_total, w.tile_need);
         };
         const bool packed = n_nodes <= (int64_t(1) << 26);
-        if (adj_ready) {  // one dense segment (checked above)
+        if (fixed) {  // one dense segment (checked above)
             if (packed) pattern(uint32_t{}, std::true_type{}, std::true_type{});
             else pattern(uint64_t{}, std::true_type{}, std::true_type{});
         } else if (single_conn(T)) {
@@ -945,7 +1161,7 @@ static int mesh_csc_build(const hx_elem_segment *segs, int32_t n_segs, int64_t n
             else pattern(uint64_t{}, std::false_type{}, std::false_type{});
         }
         HX_CHECK_LAUNCH("pattern_kernel");
-        if (adj_ready) {
+        if (fixed) {
             slot_check_kernel<<<1, 32, 0, s>>>(w.slot_total, n_total, status);
             HX_CHECK_LAUNCH("slot_check_kernel");
         }
@@ -953,20 +1169,13 @@ static int mesh_csc_build(const hx_elem_segment *segs, int32_t n_segs, int64_t n
         size_t cb2 = w.cub_bytes;
         HX_TRY_CUDA(cub::DeviceScan::ExclusiveSum(w.cub_tmp, cb2, col_ptr, col_ptr, (int)(ncols + 1), s));
         if (vals != nullptr) {
-            if (single_dense(T))
-                emit_kernel<true, true, true><<<tiles, EMIT_BLOCK, 0, s>>>(T, col_lo, ncols, w.deg, w.adj, col_ptr,
-                                                                    w.scratch, w.block_scratch, row_idx, vals,
-                                                                    row_capacity, status, w.order_flag, w.order);
-            else
-                emit_kernel<true, true, false><<<tiles, EMIT_BLOCK, 0, s>>>(T, col_lo, ncols, w.deg, w.adj, col_ptr,
-                                                                     w.scratch, w.block_scratch, row_idx, vals,
-                                                                     row_capacity, status, w.order_flag, w.order);
-            HX_CHECK_LAUNCH("emit_kernel");
+            const int rc2 = launch_emit<true, true>(emit_args(T, col_lo, ncols, w, col_ptr, row_idx, vals, row_capacity),
+                                                    status, s, "emit_kernel");
+            if (rc2) return rc2;
         } else if (row_capacity > 0) {
-            emit_kernel<true, false, true><<<tiles, EMIT_BLOCK, 0, s>>>(T, col_lo, ncols, w.deg, w.adj, col_ptr,
-                                                                      w.scratch, w.block_scratch, row_idx, nullptr,
-                                                                      row_capacity, status, w.order_flag, w.order);
-            HX_CHECK_LAUNCH("emit_kernel<rows>");
+            const int rc2 = launch_emit<true, false>(
+                emit_args(T, col_lo, ncols, w, col_ptr, row_idx, nullptr, row_capacity), status, s, "emit_kernel<rows>");
+            if (rc2) return rc2;
         }
     } else {
         HX_TRY_CUDA(cudaMemsetAsync(col_ptr, 0, sizeof(int64_t), s));
@@ -1009,13 +1218,9 @@ extern "C" int hx_mesh_csc_numeric(const hx_elem_segment *segs, int32_t n_segs, 
     MeshWs w = mesh_ws_layout(const_cast<void *>(workspace), ncols);
     cudaStream_t s = (cudaStream_t)stream;
     if (ncols > 0) {
-        if (single_dense(T))
-            emit_kernel<false, true, true><<<(unsigned)ceil_div(ncols, COL_BLOCK), EMIT_BLOCK, 0, s>>>(
-                T, col_lo, ncols, w.deg, w.adj, col_ptr, w.scratch, w.block_scratch, nullptr, vals, INT64_MAX, status, w.order_flag, w.order);
-        else
-            emit_kernel<false, true, false><<<(unsigned)ceil_div(ncols, COL_BLOCK), EMIT_BLOCK, 0, s>>>(
-                T, col_lo, ncols, w.deg, w.adj, col_ptr, w.scratch, w.block_scratch, nullptr, vals, INT64_MAX, status, w.order_flag, w.order);
-        HX_CHECK_LAUNCH("emit_kernel<numeric>");
+        const int rc2 = launch_emit<false, true>(
+            emit_args(T, col_lo, ncols, w, col_ptr, nullptr, vals, INT64_MAX), status, s, "emit_kernel<numeric>");
+        if (rc2) return rc2;
     }
     return HX_OK;
 }
@@ -1036,16 +1241,107 @@ extern "C" int hx_mesh_csc_emit(const hx_elem_segment *segs, int32_t n_segs, int
     MeshWs w = mesh_ws_layout(const_cast<void *>(workspace), ncols);
     cudaStream_t s = (cudaStream_t)stream;
     if (ncols > 0) {
-        const unsigned tiles = (unsigned)ceil_div(ncols, COL_BLOCK);
-        if (single_dense(T))
-            emit_kernel<true, true, true><<<tiles, EMIT_BLOCK, 0, s>>>(T, col_lo, ncols, w.deg, w.adj, col_ptr, w.scratch,
-                                                                w.block_scratch, row_idx, vals, capacity, status,
-                                                                w.order_flag, w.order);
-        else
-            emit_kernel<true, true, false><<<tiles, EMIT_BLOCK, 0, s>>>(T, col_lo, ncols, w.deg, w.adj, col_ptr, w.scratch,
-                                                                 w.block_scratch, row_idx, vals, capacity, status,
-                                                                w.order_flag, w.order);
-        HX_CHECK_LAUNCH("emit_kernel<emit>");
+        const int rc2 = launch_emit<true, true>(emit_args(T, col_lo, ncols, w, col_ptr, row_idx, vals, capacity),
+                                                status, s, "emit_kernel<emit>");
+        if (rc2) return rc2;
     }
     return HX_OK;
+}
+
+static int64_t fused_chunks(int64_t n_el) {
+    return std::max<int64_t>(1, ceil_div(ceil_div(n_el, GP_EL_PER_WARP), FUSED_CHUNK_QUADS));
+}
+
+extern "C" int64_t hx_integrate_emit_workspace_bytes(int64_t n_el) {
+    if (n_el < 0) return -1;
+    return 256 + (int64_t)sizeof(unsigned) * fused_chunks(n_el);
+}
+
+template <int MODE>
+static void configure_fused() {
+    static bool done[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 64 && done[MODE * 32 + dev % 32]) return;
+    cudaFuncSetAttribute(integrate_emit_kernel<MODE, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FUSED_SMEM);
+    cudaFuncSetAttribute(integrate_emit_kernel<MODE, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FUSED_SMEM);
+    if (dev < 64) done[MODE * 32 + dev % 32] = true;
+}
+
+template <int MODE>
+static int launch_fused(int64_t n_el, cudaStream_t s, const double *coords, int64_t n_nodes, const int32_t *conn,
+                        const double *coeff, double *ke, int32_t *rows, int32_t *cols, hx_fail_info *fail,
+                        const EmitArgs &A, const FusedSched &sc, const uint32_t *status) {
+    configure_fused<MODE>();
+    int dev = 0, sms = 148, per_sm = HX_KE_MIN_BLOCKS;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, integrate_emit_kernel<MODE, true>, GP_BLOCK, FUSED_SMEM);
+    const int64_t blocks = std::min<int64_t>(ceil_div(n_el, GP_EL_PER_BLOCK), (int64_t)sms * std::max(per_sm, 1));
+    unsigned *counter = reinterpret_cast<unsigned *>(&fail->reserved);
+    auto *fmin = reinterpret_cast<unsigned long long *>(fail);
+    if (rows != nullptr)
+        integrate_emit_kernel<MODE, true><<<(unsigned)blocks, GP_BLOCK, FUSED_SMEM, s>>>(
+            coords, n_nodes, conn, coeff, n_el, ke, rows, cols, fmin, counter, A, sc, status);
+    else
+        integrate_emit_kernel<MODE, false><<<(unsigned)blocks, GP_BLOCK, FUSED_SMEM, s>>>(
+            coords, n_nodes, conn, coeff, n_el, ke, rows, cols, fmin, counter, A, sc, status);
+    HX_CHECK_LAUNCH("integrate_emit_kernel");
+    return HX_OK;
+}
+
+extern "C" int hx_integrate_emit(const double *coords, int64_t n_nodes, const int32_t *conn, const double *coeff,
+                                 int64_t n_el, double *ke, int32_t *rows, int32_t *cols, int32_t mode,
+                                 hx_fail_info *fail, const int64_t *col_ptr, int64_t *row_idx, double *vals,
+                                 int64_t capacity, const void *csc_workspace, const uint32_t *csc_status,
+                                 void *sched_ws, int64_t sched_bytes, void *stream) {
+    if (n_el < 0 || n_nodes < 0 || n_nodes >= INT32_MAX || 8 * n_el >= (int64_t)INT32_MAX || fail == nullptr ||
+        (rows == nullptr) != (cols == nullptr) || col_ptr == nullptr || csc_workspace == nullptr ||
+        csc_status == nullptr || sched_ws == nullptr || capacity < 0 ||
+        (n_el > 0 && (ke == nullptr || conn == nullptr || coords == nullptr || coeff == nullptr)) ||
+        (capacity > 0 && (row_idx == nullptr || vals == nullptr))) {
+        set_last_error("hx_integrate_emit: bad arguments (n_el=%lld n_nodes=%lld)", (long long)n_el,
+                       (long long)n_nodes);
+        return HX_ERR_VALUE;
+    }
+    if (mode != HX_MODE_EXACT && mode != HX_MODE_FAST) {
+        set_last_error("hx_integrate_emit: unknown mode %d", mode);
+        return HX_ERR_CONFIG;
+    }
+    if (sched_bytes < hx_integrate_emit_workspace_bytes(n_el)) {
+        set_last_error("hx_integrate_emit: scheduling workspace %lld < %lld bytes", (long long)sched_bytes,
+                       (long long)hx_integrate_emit_workspace_bytes(n_el));
+        return HX_ERR_WORKSPACE;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    HX_TRY_CUDA(cudaMemsetAsync(fail, 0xff, sizeof(unsigned long long), s));
+    HX_TRY_CUDA(cudaMemsetAsync(&fail->reserved, 0, sizeof(int32_t), s));  // quad counter
+    HX_TRY_CUDA(cudaMemsetAsync(sched_ws, 0, (size_t)hx_integrate_emit_workspace_bytes(n_el), s));
+    if (n_el > 0) {
+        hx_elem_segment seg{};
+        seg.conn = conn;
+        seg.ke = ke;
+        seg.n_el = n_el;
+        SegTable T;
+        int64_t n_total = 0;
+        int rc = make_segtable(&seg, 1, T, n_total, true);
+        if (rc) return rc;
+        const MeshWs w = mesh_ws_layout(const_cast<void *>(csc_workspace), n_nodes);
+        const EmitArgs A = emit_args(T, 0, n_nodes, w, col_ptr, row_idx, vals, capacity);
+        FusedSched sc;
+        unsigned *base = (unsigned *)sched_ws;
+        sc.wm = base;
+        sc.tile_head = base + 1;
+        sc.done = base + 64;  // 256 B in
+        sc.tile_need = w.tile_need;
+        sc.n_quads = ceil_div(n_el, GP_EL_PER_WARP);
+        sc.n_chunks = fused_chunks(n_el);
+        sc.n_tiles = ceil_div(n_nodes, COL_BLOCK);
+        sc.n_el = n_el;
+        rc = mode == HX_MODE_EXACT
+                 ? launch_fused<HX_MODE_EXACT>(n_el, s, coords, n_nodes, conn, coeff, ke, rows, cols, fail, A, sc, csc_status)
+                 : launch_fused<HX_MODE_FAST>(n_el, s, coords, n_nodes, conn, coeff, ke, rows, cols, fail, A, sc, csc_status);
+        if (rc) return rc;
+    }
+    return integrate_fail_resolve(coords, n_nodes, conn, fail, s);
 }

@@ -74,6 +74,10 @@ int cuda_status(cudaError_t err, const char *where);
 // filled by the integration kernel in the fused build (hx_integrate_mesh_adjacency).
 int mesh_ws_adjacency(void *workspace, int64_t workspace_bytes, int64_t ncols, int32_t **deg, int32_t **adj);
 
+// Resolve an integration launch's fail key into the hx_fail_info record (hx_ke.cu).
+int integrate_fail_resolve(const double *coords, int64_t n_nodes, const int32_t *conn, hx_fail_info *fail,
+                           cudaStream_t s);
+
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 

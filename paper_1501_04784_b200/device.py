@@ -21,7 +21,7 @@ from .errors import ConfigurationError, DegenerateElementError, MeshValidationEr
 __all__ = [
     "DeviceMesh", "DeviceCsc", "AssemblyPrep", "new_assembly_prep", "rows_narrow", "require_device", "stream_handle", "integrate_mesh", "stiffness_batch",
     "connectivity_index_arrays", "dof_index_arrays", "assemble_dof", "raise_if_failed", "mesh_csc", "triplet_csc", "MeshPlan", "mesh_plan_async",
-    "mesh_emit", "plan_assembly", "block_elements", "generate_cube_mesh",
+    "mesh_emit", "integrate_emit", "plan_result", "plan_assembly", "block_elements", "generate_cube_mesh",
 ]
 
 _FAIL_WORDS = 3  # hx_fail_info = {int64 element, int32 gp, int32 pad, double det} = 24 bytes
@@ -455,9 +455,11 @@ class MeshPlan:
 
 
 def mesh_plan_async(conn: torch.Tensor, n_nodes: int, stream=None, order: str = "auto", ws_bytes: int | None = None,
-                    capacity: int | None = None) -> MeshPlan:
+                    capacity: int | None = None, fixed: bool = False) -> MeshPlan:
     """Launch the symbolic phase of a single-segment mesh assembly on ``stream`` (no host sync).
-    It reads only the connectivity, so it can run concurrently with the integration kernel."""
+    It reads only the connectivity, so it can run concurrently with the integration kernel.
+    ``fixed``: fixed-slot adjacency (HX_CSC_FIXED_ADJACENCY, no atomic counters); a mesh whose
+    elements hold a node at the same local index reports a slot collision (plan_result re-assembles)."""
     n = conn.shape[0]
     if conn.dtype != torch.int32 or tuple(conn.shape) != (n, 8) or not conn.is_contiguous():
         raise ValueError("conn must be a contiguous CUDA int32 (n, 8) tensor")
@@ -473,7 +475,7 @@ def mesh_plan_async(conn: torch.Tensor, n_nodes: int, stream=None, order: str = 
     row_buf = torch.empty(max(capacity, 1), dtype=torch.int64, device=dev)
     val_buf = torch.empty(max(capacity, 1), dtype=torch.float64, device=dev)
     segs = N.segments([(conn.data_ptr(), 0, n)])
-    flags = _order_flags(order, conn, n_nodes)
+    flags = _order_flags(order, conn, n_nodes) | (N.CSC_FIXED_ADJACENCY if fixed else 0)
     N.check(N.lib().hx_mesh_csc_symbolic(segs, 1, n_nodes, 0, n_nodes, _ptr(col_ptr), ctypes.c_void_p(0), 0,
                                          _ptr(ws), ws_bytes, _ptr(status), flags, stream_handle(stream)),
             "hx_mesh_csc_symbolic")
@@ -519,12 +521,51 @@ def mesh_emit(plan: MeshPlan, ke: torch.Tensor, stream=None) -> DeviceCsc:
     N.check(N.lib().hx_mesh_csc_emit(segs, 1, 0, plan.n_nodes, _ptr(plan.col_ptr), _ptr(plan.row_buf),
                                      _ptr(plan.val_buf), plan.capacity, _ptr(plan.ws), _ptr(plan.status),
                                      stream_handle(stream)), "hx_mesh_csc_emit")
+    return plan_result(plan, ke, stream=stream)
+
+
+def integrate_emit(dm: "DeviceMesh", plan: MeshPlan, ke: torch.Tensor, rows=None, cols=None, mode: str = "exact",
+                   stream=None) -> torch.Tensor:
+    """KE (+ iK/jK) of every element and the plan's emit pass in one launch (hx_integrate_emit): the
+    emit tiles run on the integration kernel's warps as soon as their elements are integrated.
+    Returns the fail record; the CSC is read with plan_result."""
+    n = dm.n_el
+    _check_tensor(ke, torch.float64, (n, 36), "ke")
+    if (rows is None) != (cols is None):
+        raise ValueError("rows and cols go together")
+    if rows is not None:
+        _check_tensor(rows, torch.int32, (36 * n,), "rows")
+        _check_tensor(cols, torch.int32, (36 * n,), "cols")
+    if plan.conn is not dm.conn:
+        raise ConfigurationError("the assembly plan belongs to another mesh")
+    dev = ke.device
+    if plan.readers is None:
+        plan.readers = []
+    s = torch.cuda.current_stream(dev) if stream is None else stream
+    for ev in plan.readers:  # a previous result still being read (host transfer): do not overwrite it
+        s.wait_event(ev)
+    plan.readers.clear()
+    fail = new_fail_record(dev)
+    sched_bytes = N.lib().hx_integrate_emit_workspace_bytes(n)
+    sched = torch.empty(sched_bytes, dtype=torch.uint8, device=dev)
+    N.check(N.lib().hx_integrate_emit(_ptr(dm.coords), dm.n_nodes, _ptr(dm.conn), _ptr(dm.coeff), n, _ptr(ke),
+                                      _ptr(rows), _ptr(cols), _mode_id(mode), _ptr(fail), _ptr(plan.col_ptr),
+                                      _ptr(plan.row_buf), _ptr(plan.val_buf), plan.capacity, _ptr(plan.ws),
+                                      _ptr(plan.status), _ptr(sched), sched_bytes, stream_handle(stream)),
+            "hx_integrate_emit")
+    return fail
+
+
+def plan_result(plan: MeshPlan, ke: torch.Tensor, stream=None) -> DeviceCsc:
+    """The CSC an emit into ``plan``'s buffers produced (mesh_emit / integrate_emit): a verified plan
+    returns without a host sync; otherwise one sync checks the status word and nnz and re-assembles
+    with mesh_csc when the plan hit a limit (or its fixed-slot adjacency collided)."""
     if plan.nnz >= 0:
         return DeviceCsc(plan.col_ptr, plan.row_buf[:plan.nnz], plan.val_buf[:plan.nnz], plan.n_nodes, 0, "mesh",
                          readers=plan.readers)
     st, nnz = peek(plan.status[0:1], plan.col_ptr[-1:], stream=stream)
     _status_error(st)
-    if st & N.ST_FASTPATH_LIMITS or nnz > plan.capacity:
+    if st & (N.ST_FASTPATH_LIMITS | N.ST_SLOT_COLLISION) or nnz > plan.capacity:
         order = "element" if plan.flags & N.CSC_ORDER_BY_ELEMENT else "column"
         return mesh_csc([(plan.conn, ke)], plan.n_nodes, stream=stream, order=order)
     return DeviceCsc(plan.col_ptr, plan.row_buf[:nnz], plan.val_buf[:nnz], plan.n_nodes, 0, "mesh",

@@ -138,10 +138,31 @@ def build_device(dm: D.DeviceMesh, mode: str = "exact", with_index: bool = True,
         side.wait_stream(main)  # inputs and the buffers below are ordered before the plan
         plan = D.mesh_plan_async(dm.conn, dm.n_nodes, stream=side, order=dm.assembly_order())
         plan_done = side.record_event()
-    # cold single-stream build: the integration kernel also records the node adjacency (the
-    # assembly's first pass), so the connectivity is read once and the atomics hide under FP64 work
     spans = sorted(ranges or [(0, n)])
     covers = spans[0][0] == 0 and spans[-1][1] == n and all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
+    # default build: symbolic phase first (fixed-slot adjacency, pattern, scan), then ONE launch that
+    # integrates every element and runs each column tile's emit as soon as its elements are done
+    # (hx_integrate_emit) -- the DRAM-bound emit hides under the FP64-bound integration and reads the
+    # KE rows back from L2.  A verified plan (warm rebuild) skips the symbolic phase.
+    fused_emit = (plan is None and (ranges is None or len(spans) == 1) and 0 < n and 8 * n < 2**31 - 1
+                  and os.environ.get("HX_FUSED_EMIT", "1") != "0")
+    if fused_emit:
+        if cached is not None and cached.conn is not dm.conn:
+            raise ConfigurationError("the assembly plan belongs to another mesh")
+        fplan = cached if cached is not None else D.mesh_plan_async(dm.conn, dm.n_nodes, stream=main,
+                                                                     order=dm.assembly_order(), fixed=True)
+        fail = D.integrate_emit(dm, fplan, ke, rows if with_index else None, cols if with_index else None,
+                                mode=mode, stream=main)
+        try:
+            csc = D.plan_result(fplan, ke, stream=main)
+        except MeshValidationError:  # an out-of-range node id is reported as the element's NodeIndexError
+            D.raise_if_failed(fail, n_nodes=dm.n_nodes)
+            raise
+        if cached is None:  # a planned rebuild stays asynchronous: check the fail record later
+            D.raise_if_failed(fail, n_nodes=dm.n_nodes)
+        return DeviceBuild(ke, rows if with_index else None, cols if with_index else None, csc, [fail])
+    # cold single-stream build: the integration kernel also records the node adjacency (the
+    # assembly's first pass), so the connectivity is read once and the atomics hide under FP64 work
     fuse = cached is None and plan is None and covers and 0 < n and 8 * n < 2**31 - 1
     prep = D.new_assembly_prep(dm) if fuse and os.environ.get("HX_FUSED_ADJACENCY", "1") != "0" else None
     fails = []

@@ -676,14 +676,16 @@ def _oracle_build(mesh):
     return ke, rows, cols, oracle.triplet_to_csc(rows, cols, ke.reshape(-1), mesh.n_nodes)
 
 
+@pytest.mark.parametrize("emit", ["0", "1"])
 @pytest.mark.parametrize("fused", ["0", "1"])
 @pytest.mark.parametrize("rotate", [0.0, 0.3, 1.0])
-def test_fused_adjacency_orientations_bitwise(monkeypatch, fused, rotate):
+def test_fused_adjacency_orientations_bitwise(monkeypatch, fused, rotate, emit):
     """The cold build records the node adjacency inside the integration kernel in fixed slots
     (slot = local node).  Elements re-oriented by a rotation of the reference cube put shared nodes
     at colliding local indices; the build detects the lost slots and re-runs the atomic adjacency
     pass.  Either way the results are bitwise the oracle's (also with the fusion switched off)."""
     monkeypatch.setenv("HX_FUSED_ADJACENCY", fused)
+    monkeypatch.setenv("HX_FUSED_EMIT", emit)
     rng = np.random.default_rng(77)
     mesh = perturbed_mesh(7, seed=5, distortion=0.15)
     conn = mesh.connectivity.copy()
@@ -1053,3 +1055,78 @@ def test_dof_index_arrays_rejects_bad_dofxn():
         D.dof_index_arrays(conn, 1, 17)
     with pytest.raises(ValueError):
         D.dof_index_arrays(conn, 2**30, 4)
+
+
+# ---- integration fused with the emit pass (hx_integrate_emit, the default build) --------------------
+def _fused_meshes():
+    rot = perturbed_mesh(9, seed=21, distortion=0.15)
+    conn = rot.connectivity.copy()
+    turn = np.random.default_rng(3).random(rot.n_el) < 0.5
+    conn[turn] = conn[turn][:, [1, 2, 3, 0, 5, 6, 7, 4]]  # colliding fixed slots -> re-assembly
+    return {"structured": perturbed_mesh(23, seed=20), "permuted": permuted_mesh(perturbed_mesh(19, seed=22), seed=23),
+            "rotated": Mesh(rot.coords, np.ascontiguousarray(conn), rot.coefficient),
+            "tiny": perturbed_mesh(1, seed=24)}
+
+
+@pytest.mark.parametrize("name", ["structured", "permuted", "rotated", "tiny"])
+@pytest.mark.parametrize("mode", ["exact", "fast"])
+def test_integrate_emit_equals_separate_kernels(monkeypatch, name, mode):
+    """One launch integrating every element and emitting every column tile once its elements are
+    done: KE, iK/jK and the CSC are bitwise those of the separate kernels (and the oracle in exact
+    mode), for local, permuted and colliding-slot meshes."""
+    mesh = _fused_meshes()[name]
+    dm = D.DeviceMesh.from_host(mesh)
+    monkeypatch.setenv("HX_FUSED_EMIT", "0")
+    ref = build_device(dm, mode=mode)
+    monkeypatch.setenv("HX_FUSED_EMIT", "1")
+    for _ in range(2):
+        b = build_device(dm, mode=mode)
+        torch.cuda.synchronize()
+        assert bits_equal(b.ke.cpu().numpy(), ref.ke.cpu().numpy())
+        assert bits_equal(b.rows.cpu().numpy(), ref.rows.cpu().numpy())
+        assert bits_equal(b.cols.cpu().numpy(), ref.cols.cpu().numpy())
+        for a, r in ((b.csc.col_ptr, ref.csc.col_ptr), (b.csc.row_idx, ref.csc.row_idx), (b.csc.vals, ref.csc.vals)):
+            assert bits_equal(a.cpu().numpy(), r.cpu().numpy())
+    if mode == "exact":
+        ke, rows, cols, (cp, ri, vv) = _oracle_build(mesh)
+        assert bits_equal(b.ke.cpu().numpy(), ke) and bits_equal(b.csc.vals.cpu().numpy(), vv)
+        assert bits_equal(b.csc.row_idx.cpu().numpy(), ri) and bits_equal(b.csc.col_ptr.cpu().numpy(), cp)
+
+
+def test_integrate_emit_low_capacity_and_plan_reuse():
+    """A plan whose output buffers are too small: the fused launch writes only the first entries and
+    plan_result re-assembles; a verified plan (warm rebuild) runs the fused launch without a sync."""
+    mesh = permuted_mesh(perturbed_mesh(12, seed=31), seed=32)
+    dm = D.DeviceMesh.from_host(mesh)
+    ke_o, _, _, (cp, ri, vv) = _oracle_build(mesh)
+    plan = D.mesh_plan_async(dm.conn, dm.n_nodes, capacity=100, fixed=True)
+    ke = torch.empty((dm.n_el, 36), dtype=torch.float64, device="cuda")
+    fail = D.integrate_emit(dm, plan, ke)
+    csc = D.plan_result(plan, ke)
+    D.raise_if_failed(fail)
+    assert bits_equal(ke.cpu().numpy(), ke_o)
+    assert bits_equal(csc.row_idx.cpu().numpy(), ri) and bits_equal(csc.vals.cpu().numpy(), vv)
+    vplan = D.plan_assembly(dm)
+    for _ in range(3):
+        b = build_device(dm, plan=vplan)
+        torch.cuda.synchronize()
+        D.raise_if_failed(b.fails[0])
+        assert bits_equal(b.csc.vals.cpu().numpy(), vv) and bits_equal(b.csc.row_idx.cpu().numpy(), ri)
+
+
+def test_integrate_emit_errors():
+    """Degenerate elements and bad node ids through the fused launch: the reference's exceptions for
+    the lowest failing element, nothing dereferenced out of range."""
+    mesh = perturbed_mesh(6, seed=41)
+    conn = mesh.connectivity.copy()
+    conn[100] = conn[100][[4, 5, 6, 7, 0, 1, 2, 3]]
+    conn[70] = conn[70][[4, 5, 6, 7, 0, 1, 2, 3]]
+    with pytest.raises(DegenerateElementError) as ei:
+        build_device(D.DeviceMesh.from_host(Mesh(mesh.coords, np.ascontiguousarray(conn), mesh.coefficient)))
+    assert ei.value.element_id == 70
+    conn[150, 3] = -5
+    from paper_1501_04784_b200 import NodeIndexError
+
+    with pytest.raises(NodeIndexError) as ei:
+        build_device(D.DeviceMesh.from_host(Mesh(mesh.coords, np.ascontiguousarray(conn), mesh.coefficient)))
+    assert ei.value.element_id == 150
