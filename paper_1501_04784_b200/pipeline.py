@@ -144,7 +144,7 @@ def build_device(dm: D.DeviceMesh, mode: str = "exact", with_index: bool = True,
     # integrates every element and runs each column tile's emit as soon as its elements are done
     # (hx_integrate_emit) -- the DRAM-bound emit hides under the FP64-bound integration and reads the
     # KE rows back from L2.  A verified plan (warm rebuild) skips the symbolic phase.
-    fused_emit = (plan is None and (ranges is None or len(spans) == 1) and 0 < n and 8 * n < 2**31 - 1
+    fused_emit = (plan is None and covers and len(spans) == 1 and 0 < n and 8 * n < 2**31 - 1
                   and os.environ.get("HX_FUSED_EMIT", "1") != "0")
     if fused_emit:
         if cached is not None and cached.conn is not dm.conn:
