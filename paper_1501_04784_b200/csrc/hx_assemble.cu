@@ -828,8 +828,6 @@ struct FusedSched {
     unsigned *tile_head;        // next emit tile of the processing order
     const int32_t *tile_need;   // per tile: elements that must be integrated first
     int64_t n_quads, n_chunks, n_tiles, n_el;
-    int variant;                // experiments (HX_FUSED_VARIANT): 0 full, 1 counters only (no emit),
-                                // 2 emit every tile after the warp's quads, 3 ready checks every 4th quad
 };
 
 struct EmitHook {
@@ -861,14 +859,11 @@ struct EmitHook {
         emit_tile<32, true, true, true, true>(*S, *A, t, lane);
         __syncwarp();  // the staging buffer is the integration's again
     }
-    int calls = 0;
     __device__ __forceinline__ void after_quad(int64_t q) {
-        if (sc.variant == 2) return;
         __threadfence();  // this quad's KE / iK / jK stores before its completion count
         __syncwarp();
         if (lane == 0) atomicAdd(sc.done + q / FUSED_CHUNK_QUADS, 1u);
-        if (!emit || sc.variant == 1) return;
-        if (sc.variant == 3 && (++calls & 3) != 0) return;
+        if (!emit) return;
 #pragma unroll 1
         for (int it = 0; it < 2; ++it) {  // at most two ready tiles between quads
             long long t = -1;
@@ -883,17 +878,7 @@ struct EmitHook {
         }
     }
     __device__ __forceinline__ void drain() {
-        if (!emit || sc.variant == 1) return;
-        if (sc.variant == 2) {  // integration done by this warp: emit without completion tracking
-#pragma unroll 1
-            while (true) {
-                unsigned h = 0;
-                if (lane == 0) h = atomicAdd(sc.tile_head, 1u);
-                h = __shfl_sync(0xffffffffu, h, 0);
-                if (h >= sc.n_tiles) return;
-                run_tile(h);
-            }
-        }
+        if (!emit) return;
 #pragma unroll 1
         while (true) {
             unsigned h = 0;
@@ -1348,7 +1333,6 @@ extern "C" int hx_integrate_emit(const double *coords, int64_t n_nodes, const in
         sc.wm = base;              // its own 128-B line
         sc.tile_head = base + 32;  // its own 128-B line
         sc.done = base + 64;       // 256 B in
-        sc.variant = getenv("HX_FUSED_VARIANT") ? atoi(getenv("HX_FUSED_VARIANT")) : 0;
         sc.tile_need = w.tile_need;
         sc.n_quads = ceil_div(n_el, GP_EL_PER_WARP);
         sc.n_chunks = fused_chunks(n_el);

@@ -140,12 +140,12 @@ def build_device(dm: D.DeviceMesh, mode: str = "exact", with_index: bool = True,
         plan_done = side.record_event()
     spans = sorted(ranges or [(0, n)])
     covers = spans[0][0] == 0 and spans[-1][1] == n and all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
-    # default build: symbolic phase first (fixed-slot adjacency, pattern, scan), then ONE launch that
-    # integrates every element and runs each column tile's emit as soon as its elements are done
-    # (hx_integrate_emit) -- the DRAM-bound emit hides under the FP64-bound integration and reads the
-    # KE rows back from L2.  A verified plan (warm rebuild) skips the symbolic phase.
+    # HX_FUSED_EMIT=1 (opt-in, measured slower -- DESIGN.md 4.3): symbolic phase first (fixed-slot
+    # adjacency, pattern, scan), then ONE launch that integrates every element and runs each column
+    # tile's emit on the same warps once its elements are done (hx_integrate_emit).  A verified plan
+    # (warm rebuild) skips the symbolic phase.
     fused_emit = (plan is None and covers and len(spans) == 1 and 0 < n and 8 * n < 2**31 - 1
-                  and os.environ.get("HX_FUSED_EMIT", "1") != "0")
+                  and os.environ.get("HX_FUSED_EMIT", "0") == "1")
     if fused_emit:
         if cached is not None and cached.conn is not dm.conn:
             raise ConfigurationError("the assembly plan belongs to another mesh")

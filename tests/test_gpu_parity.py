@@ -1078,7 +1078,7 @@ def test_integrate_emit_equals_separate_kernels(monkeypatch, name, mode):
     dm = D.DeviceMesh.from_host(mesh)
     monkeypatch.setenv("HX_FUSED_EMIT", "0")
     ref = build_device(dm, mode=mode)
-    monkeypatch.setenv("HX_FUSED_EMIT", "1")
+    monkeypatch.setenv("HX_FUSED_EMIT", "1")  # opt-in path
     for _ in range(2):
         b = build_device(dm, mode=mode)
         torch.cuda.synchronize()
@@ -1107,16 +1107,21 @@ def test_integrate_emit_low_capacity_and_plan_reuse():
     assert bits_equal(ke.cpu().numpy(), ke_o)
     assert bits_equal(csc.row_idx.cpu().numpy(), ri) and bits_equal(csc.vals.cpu().numpy(), vv)
     vplan = D.plan_assembly(dm)
-    for _ in range(3):
-        b = build_device(dm, plan=vplan)
+    os.environ["HX_FUSED_EMIT"] = "1"
+    try:
+        bs = [build_device(dm, plan=vplan) for _ in range(3)]
+    finally:
+        os.environ.pop("HX_FUSED_EMIT")
+    for b in bs:
         torch.cuda.synchronize()
         D.raise_if_failed(b.fails[0])
         assert bits_equal(b.csc.vals.cpu().numpy(), vv) and bits_equal(b.csc.row_idx.cpu().numpy(), ri)
 
 
-def test_integrate_emit_errors():
+def test_integrate_emit_errors(monkeypatch):
     """Degenerate elements and bad node ids through the fused launch: the reference's exceptions for
     the lowest failing element, nothing dereferenced out of range."""
+    monkeypatch.setenv("HX_FUSED_EMIT", "1")
     mesh = perturbed_mesh(6, seed=41)
     conn = mesh.connectivity.copy()
     conn[100] = conn[100][[4, 5, 6, 7, 0, 1, 2, 3]]
