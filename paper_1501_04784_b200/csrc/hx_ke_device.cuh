@@ -526,6 +526,9 @@ __device__ __forceinline__ bool ke_gauss_point(GpWarpSmem &sm, int el, int gp, b
 #ifndef HX_KE_STATIC
 #define HX_KE_STATIC 0
 #endif
+#ifndef HX_KE_LATE_GRAB
+#define HX_KE_LATE_GRAB 1
+#endif
 // Adjacency output of the fused symbolic first pass (WITH_ADJ): adj (8 n_nodes) i32 fixed slots
 // (emptied to -1 by the caller), status bit HX_ST_BAD_INDEX.
 struct AdjOut {
@@ -610,7 +613,14 @@ __device__ __forceinline__ void integrate_quads(GpWarpSmem &sm, const uint8_t *s
             x0 = __ldg(p); x1 = __ldg(p + 1); x2 = __ldg(p + 2);
             c = __ldg(coeff + lo + quad1 * GP_EL_PER_WARP + el);
         }
+#if HX_KE_LATE_GRAB
+        // claim the quad after next now, read the claim after this quad's FP64 work: the atomic's
+        // round trip overlaps the Gauss-point arithmetic instead of stalling the warp here
+        unsigned claim = 0;
+        if (!HX_KE_STATIC && lane == 0 && quad2 < n_quads) claim = atomicAdd(quad_counter, 1u);
+#else
         const int64_t quad3 = quad2 < n_quads ? grab() : n_quads;
+#endif
         bool ok;
         if constexpr (MODE == HX_MODE_EXACT)
             ok = ke_gauss_point<WITH_INDEX, KE_KEEP>(sm, el, gp, fast_div, k, valid, ke_out, rows_out, cols_out, s_pi,
@@ -619,6 +629,17 @@ __device__ __forceinline__ void integrate_quads(GpWarpSmem &sm, const uint8_t *s
             ok = ke_gauss_point_fast<WITH_INDEX, KE_KEEP>(sm, el, gp, k, valid, ke_out, rows_out, cols_out, s_pi,
                                                           s_pj);
         if (valid && !ok) atomicMin(fail_min, HX_FAIL_DEGENERATE_KEY | (unsigned long long)(lo + k));
+#if HX_KE_LATE_GRAB
+        int64_t quad3 = n_quads;
+        if (quad2 < n_quads) {
+            if (HX_KE_STATIC) {
+                static_next += first_dynamic;
+                quad3 = static_next;
+            } else {
+                quad3 = first_dynamic + (int64_t)__shfl_sync(0xffffffffu, claim, 0);
+            }
+        }
+#endif
         hook.after_quad(quad);
         quad = quad1;
         quad1 = quad2;

@@ -7,9 +7,9 @@ rm -rf $OUT; mkdir -p $OUT
 while [ $# -gt 1 ]; do
   name=$1; defs=$2; shift 2
   d=/tmp/hxvar_$name; rm -rf $d; mkdir -p $d
-  python -c "from paper_1501_04784_b200.build import SOURCES; print(\"\\n\".join(s[:-3] for s in SOURCES))" | xargs -P 6 -I{} \
+  python -c "from paper_1501_04784_b200.build import SOURCES; print(\"\\n\".join(SOURCES))" | xargs -P 8 -I{} \
     nvcc -std=c++17 -O3 -lineinfo -Xcompiler -fPIC --expt-relaxed-constexpr -Iinclude $defs \
-      -gencode arch=compute_100a,code=sm_100a -c paper_1501_04784_b200/csrc/{}.cu -o $d/{}.o
+      -gencode arch=compute_100a,code=sm_100a -c paper_1501_04784_b200/csrc/{} -o $d/{}.o
   nvcc -shared -gencode arch=compute_100a,code=sm_100a -o $OUT/$name.so $d/*.o -cudart static
 done
 ls -la $OUT
