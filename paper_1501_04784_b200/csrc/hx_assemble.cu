@@ -148,20 +148,6 @@ __device__ __forceinline__ void sort8(int32_t (&v)[8]) {
     cswap(v[3], v[4]);
 }
 
-// Sorted-unique insert into a per-thread list R[0..m) laid out [slot][BLOCK] in smem
-// (thread-fastest: conflict-free for any per-thread slot).  Returns false on overflow.
-template <int BLOCK>
-__device__ __forceinline__ bool insert_row(int32_t *R, int &m, int32_t v) {
-    int pos = 0;
-    while (pos < m && R[pos * BLOCK] < v) ++pos;
-    if (pos < m && R[pos * BLOCK] == v) return true;
-    if (m == MAXR) return false;
-    for (int q = m; q > pos; --q) R[q * BLOCK] = R[(q - 1) * BLOCK];
-    R[pos * BLOCK] = v;
-    ++m;
-    return true;
-}
-
 // Incident elements of column cl, sorted by element id (= the stable triplet order).
 // Returns deg, or -1 with a status bit when the column is outside the fast path.
 // FIXED: the adjacency was recorded by the integration kernel in fixed slots -- element e stores
@@ -182,7 +168,6 @@ __device__ __forceinline__ int incident_sorted(int64_t cl, int32_t *__restrict__
             ent[k] = v[k] >= 0 ? v[k] : INT32_MAX;
             deg += v[k] >= 0;
         }
-        deg_arr[cl] = deg;
     } else {
         deg = __ldg(deg_arr + cl);
         if (deg > MAXDEG) return -1;  // flagged by the adjacency pass
@@ -200,7 +185,6 @@ __device__ __forceinline__ int incident_sorted(int64_t cl, int32_t *__restrict__
     return deg;
 }
 
-constexpr int32_t HASH_EMPTY = INT32_MAX;
 constexpr int MAX_OFFDIAG_CONTRIB = 4;     // hex meshes: an edge is shared by at most 4 elements
 #ifndef HX_COL_BLOCK
 #define HX_COL_BLOCK 64
@@ -231,113 +215,13 @@ __device__ __forceinline__ void bitonic_sort(K (&v)[N]) {
             }
 }
 
-// Sort the first n (<= N) keys of the per-thread list L[q * COL_BLOCK] in place (padding sorts last).
-template <int N, typename K>
-__device__ __forceinline__ void sort_list(K *L, int n) {
-    K v[N];
-#pragma unroll
-    for (int q = 0; q < N; ++q) v[q] = q < n ? L[q * COL_BLOCK] : (K)~(K)0;
-    bitonic_sort<N, K>(v);
-#pragma unroll
-    for (int q = 0; q < N; ++q)
-        if (q < n) L[q * COL_BLOCK] = v[q];
-}
-
-__device__ __forceinline__ uint32_t hash_slot(int32_t v) { return ((uint32_t)v * 0x9E3779B1u) >> 27; }
-
-// Pattern of one column (the calling thread's): sorted incident list (written back to the adjacency
-// when WRITE_ADJ), distinct rows r > c in the hash set H with contribution words W[slot], then the
-// occupied keys compacted into L as (row << 5 | slot) and sorted.  Returns m = 1 + rows (0 for an
-// empty column or one outside the fast path, with a status bit).  H, W, L: this thread's slices of
-// the [slot][thread] shared arrays.
-template <typename K, bool SINGLE, bool WRITE_ADJ, bool FIXED>
-__device__ __forceinline__ int column_pattern(const SegTable &T, bool active, int64_t cl, int32_t c,
-                                              int32_t *__restrict__ deg_arr, int32_t *__restrict__ adj,
-                                              int32_t *H, uint32_t *W, K *L, int32_t (&ent)[8], int &deg,
-                                              uint32_t *__restrict__ status) {
-    int m = 0;
-    deg = 0;
-    if (active) {
-        deg = incident_sorted<FIXED>(cl, deg_arr, adj, ent, status);
-        if (deg < 0) deg = 0;
-#pragma unroll
-        for (int k = 0; k < 8; ++k)
-            if (WRITE_ADJ && k < deg) adj[8 * cl + k] = ent[k];
-    }
-    if (deg > 0) {
-#pragma unroll
-        for (int q = 0; q < MAXR; ++q) H[q * COL_BLOCK] = HASH_EMPTY;  // W[slot] is written on first insert
-        // all incident connectivity rows in flight at once (memory-level parallelism)
-        int32_t g[8][8];
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            if (k < deg) {
-                const int4 *c4 = reinterpret_cast<const int4 *>(conn_row<SINGLE>(T, ent[k] >> 3));
-                const int4 lo = __ldg(c4), hi = __ldg(c4 + 1);
-                g[k][0] = lo.x; g[k][1] = lo.y; g[k][2] = lo.z; g[k][3] = lo.w;
-                g[k][4] = hi.x; g[k][5] = hi.y; g[k][6] = hi.z; g[k][7] = hi.w;
-            } else {
-#pragma unroll
-                for (int b = 0; b < 8; ++b) g[k][b] = INT32_MIN;  // never a row (< c)
-            }
-        }
-        bool ok = true;
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-#pragma unroll
-            for (int b = 0; b < 8; ++b) {
-                const int32_t v = g[k][b];
-                if (v <= c) continue;  // the diagonal (v == c) is implicit
-                uint32_t h = hash_slot(v);
-                int32_t cur = H[h * COL_BLOCK];
-#pragma unroll 1
-                for (int probe = 1; cur != v && cur != HASH_EMPTY && probe < MAXR; ++probe) {
-                    h = (h + 1) & (MAXR - 1);
-                    cur = H[h * COL_BLOCK];
-                }
-                if (cur != v && cur != HASH_EMPTY) {
-                    ok = false;  // more than MAXR distinct rows
-                    continue;
-                }
-                H[h * COL_BLOCK] = v;
-                const uint32_t w = cur == HASH_EMPTY ? 0u : W[h * COL_BLOCK];
-                const uint32_t n = w & 7u;
-                if (n == MAX_OFFDIAG_CONTRIB) ok = false;
-                else W[h * COL_BLOCK] = (w + 1u) | ((uint32_t)(k << 3 | b) << (3 + 6 * n));
-            }
-        }
-        if (!ok) {
-            atomicOr(status, HX_ST_ROW_OVERFLOW);
-        } else {
-            int cnt = 0;
-#pragma unroll
-            for (int q = 0; q < MAXR; ++q) {
-                const int32_t key = H[q * COL_BLOCK];
-                if (key != HASH_EMPTY) {
-                    L[cnt * COL_BLOCK] = ((K)key << 5) | (K)q;
-                    ++cnt;
-                }
-            }
-            // one network per warp: a warp with any column above 16 rows sorts all with 32 keys
-            // (a divergent warp would otherwise run both networks)
-            if (!__any_sync(__activemask(), cnt > 16)) sort_list<16, K>(L, cnt);
-            else sort_list<32, K>(L, cnt);
-            m = 1 + cnt;
-        }
-    }
-    return m;
-}
-
-// Sort-based pattern of one column (HX_PATTERN_SORT, the default): every contribution (k, b) of an
+// Sort-based pattern of one column: every contribution (k, b) of an
 // incident element k whose node v = g[k][b] lies below the diagonal becomes one key
 // (v << 6 | k << 3 | b), appended branch-free to the thread's list L; a 16/32/64-key register
 // network (warp-uniform choice) sorts them, so equal rows form runs whose contributions are already
-// in element order.  Replaces the hash set: no data-dependent probe loops (the hash variant spent
-// half its instructions and most of its divergence there).  Returns m = 1 + distinct rows (0 for an
+// in element order.  (Replaced a 32-slot hash set in round 1: its data-dependent probe loops were
+// half its instructions and most of its divergence.)  Returns m = 1 + distinct rows (0 for an
 // empty column or one outside the fast path) and cnt = keys left sorted in L.
-#ifndef HX_PATTERN_SORT
-#define HX_PATTERN_SORT 1
-#endif
 constexpr int SORT_SLOTS = 64;  // <= 8 elements x 7 other nodes = 56 contributions per column
 
 // Batcher's odd-even merge sort on N register-resident keys, ascending (N = 16/32/64: 63/191/543
@@ -406,8 +290,9 @@ __device__ __forceinline__ void sort_count(K *L, int n, int &rows, bool &ok) {
 
 template <typename K, bool SINGLE, bool FIXED>
 __device__ __forceinline__ int column_pattern_sort(const SegTable &T, bool active, int64_t cl, int32_t c,
-                                                   int32_t *__restrict__ deg_arr, int32_t *__restrict__ adj, K *L,
-                                                   int &cnt, int &deg, int32_t &last, uint32_t *__restrict__ status) {
+                                                   int32_t *__restrict__ deg_arr, const int32_t *__restrict__ adj,
+                                                   int32_t *__restrict__ ent_out, K *L, int &cnt, int &deg,
+                                                   int32_t &last, uint32_t *__restrict__ status) {
     int m = 0;
     deg = 0;
     last = -1;
@@ -419,8 +304,8 @@ __device__ __forceinline__ int column_pattern_sort(const SegTable &T, bool activ
 #pragma unroll
         for (int k = 0; k < 8; ++k)
             if (k < deg) last = max(last, ent[k] >> 3);
-        if (deg > 0) {  // the emit pass reads the sorted incident list
-            int4 *a4 = reinterpret_cast<int4 *>(adj + 8 * cl);
+        if (deg > 0) {  // the emit pass reads the sorted incident list (processing order)
+            int4 *a4 = reinterpret_cast<int4 *>(ent_out);
             a4[0] = make_int4(ent[0], ent[1], ent[2], ent[3]);
             a4[1] = make_int4(ent[4], ent[5], ent[6], ent[7]);
         }
@@ -465,17 +350,15 @@ __device__ __forceinline__ int column_pattern_sort(const SegTable &T, bool activ
     return m;
 }
 
-// 2. Pattern pass: one thread per column, COL_BLOCK columns per block.
-//   - incident elements sorted by id and written back to the adjacency (the emit pass reads them
-//     in order);
-//   - distinct rows > c in a 32-slot open-addressing hash set (smem, [slot][thread] layout); every
-//     slot carries its contribution word: count (3 bits) + up to 4 (incident k, local node b) pairs
-//     appended in ascending element order;
-//   - occupied slots compacted in place to keys (row << 5 | slot) -- 32-bit when n_nodes <= 2^26,
-//     else 64-bit -- and sorted by a 16- or 32-key register network;
+// 2. Pattern pass: one thread per column, COL_BLOCK columns per block (column_pattern_sort):
+//   - incident elements sorted by id, written with the column's degree by processing position
+//     (over the adjacency in column order; separate arrays for element-ordered builds, so the emit
+//     pass reads them contiguously instead of gathering them column by column);
+//   - contribution keys (row << 6 | k << 3 | b) sorted by a 16/32/64-key register network;
 //   - m = 1 + distinct rows -> col_ptr[cl] (the exclusive scan turns counts into offsets);
-//   - sorted off-diagonal records (row, word) -> a compact scratch region reserved per block with
-//     one atomic (every block records where its records start).
+//   - runs of equal rows -> off-diagonal records (row, contribution word) in a compact scratch
+//     region reserved per block with one atomic (every block records where its records start);
+//   - tile_need[block] = 1 + the highest incident element of the tile (the fused kernel's wait).
 #ifndef HX_PATTERN_MIN_BLOCKS
 #define HX_PATTERN_MIN_BLOCKS 10  // 96 registers: 10 x 64-thread tiles per SM (measured best of 1, 10, 12)
 #endif
@@ -486,15 +369,8 @@ pattern_kernel(SegTable T, int64_t col_lo, int64_t ncols, int32_t *__restrict__ 
                int64_t scratch_capacity, unsigned long long *__restrict__ scratch_top,
                int64_t *__restrict__ block_scratch, uint32_t *__restrict__ status,
                const uint32_t *__restrict__ order, unsigned long long *__restrict__ slot_total,
-               int32_t *__restrict__ tile_need) {
-#if HX_PATTERN_SORT
+               int32_t *__restrict__ tile_need, int32_t *__restrict__ tadj, int32_t *__restrict__ tdeg) {
     __shared__ K sL[SORT_SLOTS * COL_BLOCK];  // this thread's contribution keys, [slot][thread]
-#else
-    __shared__ int32_t sH[MAXR * COL_BLOCK];   // hash keys
-    __shared__ uint32_t sW[MAXR * COL_BLOCK];  // contribution words, by hash slot
-    // compacted / sorted keys (row << 5 | slot): 32-bit keys reuse the hash-key array in place
-    __shared__ K sL[sizeof(K) == 4 ? 1 : MAXR * COL_BLOCK];
-#endif
     __shared__ unsigned long long s_base;
     using BlockScan = cub::BlockScan<int32_t, COL_BLOCK>;
     __shared__ typename BlockScan::TempStorage scan_tmp;
@@ -502,25 +378,18 @@ pattern_kernel(SegTable T, int64_t col_lo, int64_t ncols, int32_t *__restrict__ 
     const int64_t idx = (int64_t)blockIdx.x * COL_BLOCK + t;  // position in the processing order
     const int64_t cl = order != nullptr && idx < ncols ? (int64_t)__ldg(order + idx) : idx;
     const int32_t c = (int32_t)(col_lo + cl);
-#if HX_PATTERN_SORT
     K *L = sL + t;
     int cnt = 0, deg = 0;
     int32_t last = -1;
-    const int m =
-        column_pattern_sort<K, SINGLE, FIXED>(T, cl < ncols, cl, c, deg_arr, adj, L, cnt, deg, last, status);
+    // sorted incident lists and degrees in processing order (in place over adj / deg in column order)
+    int32_t *ent_out = (order != nullptr ? tadj : adj) + 8 * idx;
+    const int m = column_pattern_sort<K, SINGLE, FIXED>(T, cl < ncols, cl, c, deg_arr, adj, ent_out, L, cnt, deg, last,
+                                                        status);
+    if (cl < ncols) (order != nullptr ? tdeg : deg_arr)[idx] = deg;
     {  // elements the tile's emit needs: every incident element < tile_need (the fused kernel waits for them)
         const int need = __reduce_max_sync(0xffffffffu, last + 1);
         if ((t & 31) == 0) atomicMax(tile_need + blockIdx.x, need);
     }
-#else
-    int32_t *H = sH + t;
-    uint32_t *W = sW + t;
-    K *L = sizeof(K) == 4 ? reinterpret_cast<K *>(sH) + t : sL + t;
-    int32_t ent[8];
-    int deg = 0;
-    const int m = column_pattern<K, SINGLE, true, FIXED>(T, cl < ncols, cl, c, deg_arr, adj, H, W, L, ent, deg, status);
-    if (t == 0) tile_need[blockIdx.x] = INT32_MAX;  // hash variant: no incident maximum, wait for every element
-#endif
     if (cl < ncols) col_ptr[cl] = m;
     if (FIXED) {
         const unsigned filled = __reduce_add_sync(0xffffffffu, (unsigned)deg);
@@ -541,7 +410,6 @@ pattern_kernel(SegTable T, int64_t col_lo, int64_t ncols, int32_t *__restrict__ 
         if (off > 0) atomicOr(status, HX_ST_SCRATCH_OVERFLOW);
         return;
     }
-#if HX_PATTERN_SORT
     // runs of equal rows -> records (row, count | (k, b) pairs in element order)
     int2 *out = scratch + sb - 1;  // record j of this column at out[j + 1]; j = -1 before the first
     int j = -1, shift = 3;
@@ -560,13 +428,6 @@ pattern_kernel(SegTable T, int64_t col_lo, int64_t ncols, int32_t *__restrict__ 
         prev = v;
     }
     if (j >= 0) out[j + 1] = make_int2((int)prev, (int)word);
-#else
-#pragma unroll 1
-    for (int j = 0; j < off; ++j) {
-        const K key = L[j * COL_BLOCK];
-        scratch[sb + j] = make_int2((int)(key >> 5), (int)W[(int)(key & 31) * COL_BLOCK]);
-    }
-#endif
 }
 
 // Fixed-slot adjacency check: every (element, local node) pair must have landed in its own slot.
@@ -633,7 +494,8 @@ struct EmitSmem {
 struct EmitArgs {
     SegTable T;
     int64_t col_lo, ncols;
-    const int32_t *deg_arr, *adj;
+    const int32_t *deg_arr, *adj;    // column order (in-place lists of the pattern pass)
+    const int32_t *tdeg, *tadj;      // processing order (element-ordered builds)
     const int64_t *col_ptr;
     const int2 *scratch;
     const int64_t *block_scratch;
@@ -669,6 +531,9 @@ __device__ __forceinline__ void emit_tile(EmitSmem &S, const EmitArgs &A, int64_
     const uint32_t *__restrict__ order_flag = A.order_flag;
     const uint32_t *__restrict__ order = A.order;
     const bool ordered = *order_flag != 0u;
+    // the pattern pass wrote the sorted incident lists / degrees by processing position
+    const int32_t *__restrict__ deg_list = ordered ? A.tdeg : deg_arr;
+    const int32_t *__restrict__ adj_list = ordered ? A.tadj : adj;
     const uint64_t pol = ke_policy();
     const int64_t first = tile * COL_BLOCK;
     const int ncol = (int)(ncols - first < COL_BLOCK ? ncols - first : COL_BLOCK);
@@ -678,12 +543,12 @@ __device__ __forceinline__ void emit_tile(EmitSmem &S, const EmitArgs &A, int64_
         const int64_t a = col_ptr[cl], b = col_ptr[cl + 1];
         S.s_start[u] = a;
         S.s_m[u] = (int)(b - a);
-        S.s_deg[u] = min(deg_arr[cl], MAXDEG);
+        S.s_deg[u] = min(deg_list[first + u], MAXDEG);
     }
     tile_sync<NT>();
     if (VALS)
         for (int i = tid; i < ncol * 8; i += NT)
-            S.s_adj[i] = __ldg(adj + 8 * (int64_t)S.s_cl[i >> 3] + (i & 7));
+            S.s_adj[i] = __ldg(adj_list + 8 * first + i);  // contiguous: lists are in processing order
     // scratch record offsets: column u has max(m_u - 1, 0) records (m_u = 0 for a node no element
     // references), laid out in tile order by the pattern pass -- warp 0 scans them
     if (tid < 32) {
@@ -928,6 +793,7 @@ struct MeshWs {
     int32_t *deg, *adj;
     int64_t *block_scratch;
     int32_t *tile_need;  // per tile: 1 + its highest incident element (0: none)
+    int32_t *tadj, *tdeg;  // element order only: sorted incident lists / degrees by processing position
     unsigned long long *scratch_top, *slot_total;
     uint32_t *keys_in, *keys_out, *cols_in, *order;
     int2 *scratch;
@@ -959,6 +825,7 @@ static MeshWs mesh_ws_layout(void *base, int64_t ncols, int64_t workspace_bytes 
     const size_t o_adj = take(sizeof(int32_t) * 8 * nc);
     const size_t o_bs = take(sizeof(int64_t) * std::max<int64_t>(1, ceil_div(ncols, COL_BLOCK)));
     const size_t o_tn = take(sizeof(int32_t) * std::max<int64_t>(1, ceil_div(ncols, COL_BLOCK)));
+    const size_t o_ta = take(sizeof(int32_t) * 8 * nc), o_td = take(sizeof(int32_t) * nc);
     const size_t o_st = take(2 * sizeof(unsigned long long));  // scratch_top, slot_total
     const size_t o_ki = take(sizeof(uint32_t) * nc), o_ko = take(sizeof(uint32_t) * nc);
     const size_t o_ci = take(sizeof(uint32_t) * nc), o_or = take(sizeof(uint32_t) * nc);
@@ -976,6 +843,8 @@ static MeshWs mesh_ws_layout(void *base, int64_t ncols, int64_t workspace_bytes 
         w.adj = (int32_t *)(b + o_adj);
         w.block_scratch = (int64_t *)(b + o_bs);
         w.tile_need = (int32_t *)(b + o_tn);
+        w.tadj = (int32_t *)(b + o_ta);
+        w.tdeg = (int32_t *)(b + o_td);
         w.scratch_top = (unsigned long long *)(b + o_st);
         w.slot_total = w.scratch_top + 1;
         w.keys_in = (uint32_t *)(b + o_ki);
@@ -1058,6 +927,8 @@ static EmitArgs emit_args(const SegTable &T, int64_t col_lo, int64_t ncols, cons
     A.ncols = ncols;
     A.deg_arr = w.deg;
     A.adj = w.adj;
+    A.tdeg = w.tdeg;
+    A.tadj = w.tadj;
     A.col_ptr = col_ptr;
     A.scratch = w.scratch;
     A.block_scratch = w.block_scratch;
@@ -1147,7 +1018,7 @@ static int mesh_csc_build(const hx_elem_segment *segs, int32_t n_segs, int64_t n
             using K = decltype(key_tag);
             pattern_kernel<K, decltype(single_tag)::value, decltype(fixed_tag)::value><<<tiles, COL_BLOCK, 0, s>>>(
                 T, col_lo, ncols, w.deg, w.adj, col_ptr, w.scratch, w.scratch_capacity, w.scratch_top, w.block_scratch,
-                status, order, w.slot_total, w.tile_need);
+                status, order, w.slot_total, w.tile_need, w.tadj, w.tdeg);
         };
         const bool packed = n_nodes <= (int64_t(1) << 26);
         if (fixed) {  // one dense segment (checked above)
