@@ -1007,9 +1007,13 @@ static int mesh_csc_build(const hx_elem_segment *segs, int32_t n_segs, int64_t n
             HX_CHECK_LAUNCH("first_element_kernel");
             int end_bit = 1;
             while (end_bit < 32 && ((uint64_t)n_total >> end_bit) != 0) ++end_bit;
+            // the order only needs element locality: sort on the top 16 bits of the first element (2
+            // radix passes instead of up to 4); the stable sort keeps column order inside a bucket of
+            // n_el / 2^16 consecutive elements
+            const int begin_bit = std::max(0, end_bit - 16);
             size_t cb = w.cub_bytes;
             HX_TRY_CUDA(cub::DeviceRadixSort::SortPairs(w.cub_tmp, cb, w.keys_in, w.keys_out, w.cols_in, w.order,
-                                                        (int)ncols, 0, end_bit, s));
+                                                        (int)ncols, begin_bit, end_bit, s));
         }
         const uint32_t *order = ordered ? w.order : nullptr;
         HX_TRY_CUDA(cudaMemsetAsync(w.scratch_top, 0, 2 * sizeof(unsigned long long), s));  // + slot_total
