@@ -203,9 +203,9 @@ __global__ void halo_totals_kernel(const int64_t *__restrict__ rec_offsets, cons
 __global__ void __launch_bounds__(HALO_TILE)
 halo_pack_kernel(const int32_t *__restrict__ conn, const double *__restrict__ ke, int64_t n_el,
                  const int64_t *__restrict__ bounds, int world, int self, int64_t n_tiles,
-                 const int64_t *__restrict__ rec_offsets, const int64_t *__restrict__ val_offsets,
-                 const int64_t *__restrict__ totals, int64_t *const *__restrict__ dest_ptrs,
-                 const int64_t *__restrict__ dest_offsets) {
+                 const int64_t *__restrict__ rec_counts, const int64_t *__restrict__ rec_offsets,
+                 const int64_t *__restrict__ val_offsets, const int64_t *__restrict__ totals,
+                 int64_t *const *__restrict__ dest_ptrs, const int64_t *__restrict__ dest_offsets) {
     __shared__ int s_wrec[HALO_WARPS], s_wval[HALO_WARPS];
     __shared__ uint16_t s_list[HALO_WARPS][32 * 36];  // (lane << 8) | p of the warp's values, in order
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
@@ -216,7 +216,8 @@ halo_pack_kernel(const int32_t *__restrict__ conn, const double *__restrict__ ke
     element_owners(conn, e, n_el, bounds, world, g, o);
     const unsigned long long *ke_bits = reinterpret_cast<const unsigned long long *>(ke);
     for (int d = 0; d < world; ++d) {
-        if (d == self) continue;
+        // nothing of this tile goes to d (block-uniform, from the count pass): skip the scan and syncs
+        if (d == self || rec_counts[(int64_t)d * n_tiles + blockIdx.x] == 0) continue;
         const int k = owned_count(o, d);
         const unsigned ballot = __ballot_sync(0xffffffffu, k > 0);
         int incl = k;  // inclusive warp scan of k
@@ -307,38 +308,59 @@ halo_unpack_count_kernel(const int64_t *__restrict__ recv, const int64_t *__rest
     }
 }
 
+// 8 lanes per record (4 records per warp and step): lane a of a record owns node a (owner lookup) and
+// the packed entries p = a, a + 8, ... (p < 36); the record's owned-entry mask is OR-reduced across
+// its 8 lanes, so each lane knows where its entries sit in the compact value list.  Stores are 8
+// consecutive doubles per record and instruction (the thread-per-record form wrote 40 scattered
+// words per thread: 4x slower at C5, G = 8).
 __global__ void __launch_bounds__(256)
 halo_unpack_kernel(const int64_t *__restrict__ recv, const int64_t *__restrict__ src_desc, int world, int self,
                    const int64_t *__restrict__ bounds, int64_t n_rec, const int64_t *__restrict__ voff,
                    double *__restrict__ records) {
     __shared__ SrcTable tb;
     load_src_table(tb, src_desc, world);
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_rec; i += (int64_t)gridDim.x * blockDim.x) {
-        const int s = src_of(tb, i, world);
-        const int64_t *chunk = recv + tb.off[s];
-        const int64_t *ids = chunk + 4 * (i - tb.rec_start[s]);
-        const int64_t *vals = chunk + 4 * tb.nrec[s] + (voff[i] - tb.val_start[s]);
-        int32_t g[8];
+    const int lane = threadIdx.x & 31, sub = lane & 7, grp = lane >> 3;
+    const int64_t stride = ((int64_t)gridDim.x * blockDim.x) >> 3;  // records per grid step
+    // warp-uniform loop (shuffles below): the warp's 4 records are base .. base + 3
+    for (int64_t base = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 4; base < n_rec; base += stride) {
+        const int64_t i = base + grp;
+        const bool active = i < n_rec;
+        int s = 0;
+        int64_t chunk_off = 0, rec_start = 0, val_start = 0, nrec = 0;
+        if (active) {
+            s = src_of(tb, i, world);
+            chunk_off = tb.off[s];
+            rec_start = tb.rec_start[s];
+            val_start = tb.val_start[s];
+            nrec = tb.nrec[s];
+        }
+        const int64_t *chunk = recv + chunk_off;
+        const int32_t *g = reinterpret_cast<const int32_t *>(chunk + 4 * (i - rec_start));
+        const int32_t node = active ? __ldg(g + sub) : 0;
+        const int own_node = active ? halo_owner(node, bounds, world) : -1;
         int o[8];
 #pragma unroll
-        for (int w = 0; w < 4; ++w) {
-            const int64_t x = ids[w];
-            g[2 * w] = (int32_t)(x & 0xffffffff);
-            g[2 * w + 1] = (int32_t)(x >> 32);
+        for (int a = 0; a < 8; ++a) o[a] = __shfl_sync(0xffffffffu, own_node, 8 * grp + a);
+        unsigned long long mine = 0;
+#pragma unroll
+        for (int m = 0; m < 5; ++m) {
+            const int p = sub + 8 * m;
+            if (p < 36 && min(o[pack_i(p)], o[pack_j(p)]) == self) mine |= 1ull << p;
         }
 #pragma unroll
-        for (int a = 0; a < 8; ++a) o[a] = halo_owner(g[a], bounds, world);
+        for (int sh = 1; sh < 8; sh <<= 1) mine |= __shfl_xor_sync(0xffffffffu, mine, sh);
+        if (!active) continue;
+        const int64_t *vals = chunk + 4 * nrec + (voff[i] - val_start);
         double *out = records + 40 * i;
-        int q = 0;
 #pragma unroll
-        for (int p = 0; p < 36; ++p) {
-            const bool own = min(o[pack_i(p)], o[pack_j(p)]) == self;
-            out[p] = own ? __longlong_as_double(vals[q]) : 0.0;
-            q += own;
+        for (int m = 0; m < 5; ++m) {
+            const int p = sub + 8 * m;
+            if (p < 36) {
+                const bool own = (mine >> p) & 1ull;
+                out[p] = own ? __longlong_as_double(__ldg(vals + __popcll(mine & ((1ull << p) - 1ull)))) : 0.0;
+            }
         }
-        long long *out_ids = reinterpret_cast<long long *>(out + 36);
-#pragma unroll
-        for (int w = 0; w < 4; ++w) out_ids[w] = ids[w];
+        if (sub < 4) reinterpret_cast<long long *>(out + 36)[sub] = __ldg(reinterpret_cast<const long long *>(g) + sub);
     }
 }
 
@@ -438,8 +460,8 @@ extern "C" int hx_halo_pack(const int32_t *conn, const double *ke, int64_t n_el,
     HaloWs w = halo_ws_layout(const_cast<void *>(workspace), n_el, world);
     const int64_t n_tiles = ceil_div(n_el, HALO_TILE);
     halo_pack_kernel<<<(unsigned)n_tiles, HALO_TILE, 0, (cudaStream_t)stream>>>(
-        conn, ke, n_el, col_bounds, world, self, n_tiles, w.rec_offsets, w.val_offsets, w.totals, dest_ptrs,
-        dest_offsets);
+        conn, ke, n_el, col_bounds, world, self, n_tiles, w.rec_counts, w.rec_offsets, w.val_offsets, w.totals,
+        dest_ptrs, dest_offsets);
     HX_CHECK_LAUNCH("halo_pack_kernel");
     return HX_OK;
 }

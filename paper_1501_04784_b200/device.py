@@ -371,7 +371,8 @@ def _order_flags(order, conn, n_nodes) -> int:
 
 
 def mesh_csc(parts, n_nodes: int, col_lo: int = 0, col_hi: int | None = None, stream=None,
-             row_capacity: int | None = None, order: str = "auto", prep: AssemblyPrep | None = None) -> DeviceCsc:
+             row_capacity: int | None = None, order: str = "auto", prep: AssemblyPrep | None = None,
+             nnz_hint: int | None = None) -> DeviceCsc:
     """Assemble columns [col_lo, col_hi) of the lower CSC from element segments.
 
     ``parts`` is a list of (conn (n,8) i32, ke (n,36) f64) CUDA tensor views in ascending global
@@ -380,7 +381,9 @@ def mesh_csc(parts, n_nodes: int, col_lo: int = 0, col_hi: int | None = None, st
     generic triplet path with identical results.  ``order`` picks the column processing order
     (results are identical; "auto" uses element order for numberings without locality).  ``prep``:
     the workspace whose adjacency the integration kernel already recorded (one segment, every
-    column) -- the first attempt skips the adjacency pass; retries rebuild it.
+    column) -- the first attempt skips the adjacency pass; retries rebuild it.  ``nnz_hint``: expected
+    nnz of the block (e.g. the previous step's); sizes the output buffers and the pattern scratch so
+    blocks with more rows per column than average (the low columns of a permuted mesh) need no retry.
     """
     col_hi = n_nodes if col_hi is None else col_hi
     if not 1 <= len(parts) <= N.MAX_SEGMENTS:
@@ -406,6 +409,11 @@ def mesh_csc(parts, n_nodes: int, col_lo: int = 0, col_hi: int | None = None, st
     col_ptr = torch.empty(ncols + 1, dtype=torch.int64, device=dev)
     sh = stream_handle(stream)
     capacity = ROWS_PER_COLUMN_ESTIMATE * ncols if row_capacity is None else row_capacity
+    if nnz_hint is not None and prep is None:
+        capacity = max(capacity, int(nnz_hint))
+        extra = int(nnz_hint) - ncols - 15 * ncols  # off-diagonal records beyond the default scratch
+        if extra > 0:
+            ws_bytes += 8 * extra
     while True:
         if not flags & N.CSC_ADJACENCY_READY:
             ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)

@@ -391,8 +391,12 @@ class CudaOps:
                      "hx_halo_unpack")
         return records
 
-    def assemble(self, segments, n_nodes, c_lo, c_hi):
-        return self.D.mesh_csc(segments, n_nodes, c_lo, c_hi)
+    def assemble(self, segments, n_nodes, c_lo, c_hi, nnz_hint=None, order="auto"):
+        return self.D.mesh_csc(segments, n_nodes, c_lo, c_hi, nnz_hint=nnz_hint, order=order)
+
+    def column_order(self, dm, n_nodes) -> str:
+        """Column processing order of this rank's assemblies, decided once (one small reduction)."""
+        return "column" if self.D.numbering_is_local(dm.conn, n_nodes) else "element"
 
     def digest(self, t: torch.Tensor, pos0: int, add: int = 0) -> torch.Tensor:
         """Device u64 (as int64) accumulator of hx_digest over ``t``'s 8-byte words."""
@@ -447,12 +451,23 @@ class ShardedBuild:
         self.e_lo, self.e_hi = self.ranges[rank]
         self.dm = self.ops.upload(mesh.coords, mesh.connectivity[self.e_lo:self.e_hi],
                                   mesh.coefficient[self.e_lo:self.e_hi])
+        hist = None
         if bounds is None:  # nnz-balanced: one all-reduce of the per-bin weights of every rank's elements
             hist = self.ops.column_weights(self.dm, self.n_nodes, histogram_bins(self.n_nodes))
             hist = self.exchange.sum_(hist)
             bounds = balanced_bounds(hist.cpu().numpy(), self.n_nodes, world)
         self.bounds_np = np.asarray(bounds, dtype=np.int64)
         self.c_lo, self.c_hi = int(self.bounds_np[rank]), int(self.bounds_np[rank + 1])
+        # the block's nnz: estimated from the column-weight histogram (units of 1/8 entry) until the
+        # first step measured it; sizes the assembly's buffers so no step re-runs its pattern pass
+        self.nnz_hint = None
+        if hist is not None:
+            h = hist.cpu().numpy() if isinstance(hist, torch.Tensor) else np.asarray(hist)
+            nb = h.shape[0]
+            b_lo, b_hi = self.c_lo * nb // max(self.n_nodes, 1), max(self.c_hi - 1, 0) * nb // max(self.n_nodes, 1)
+            self.nnz_hint = int(1.1 * h[b_lo:b_hi + 1].sum() / 8) + (self.c_hi - self.c_lo)
+        order_fn = getattr(self.ops, "column_order", None)
+        self.order = order_fn(self.dm, self.n_nodes) if order_fn is not None else "auto"
         self.bounds = self.ops.bounds(self.bounds_np)
         self.last = None
         self.last_index = None
@@ -497,7 +512,8 @@ class ShardedBuild:
         segments.append((self.dm.conn, ke))
         if n_rec > n_lower:
             segments.append(record_segment(records[n_lower:]))
-        csc = self.ops.assemble(segments, self.n_nodes, self.c_lo, self.c_hi)
+        csc = self.ops.assemble(segments, self.n_nodes, self.c_lo, self.c_hi, nnz_hint=self.nnz_hint, order=self.order)
+        self.nnz_hint = int(csc.row_idx.shape[0])  # exact from now on (same mesh every step)
         self.last = ShardResult(csc.col_ptr, csc.row_idx, csc.vals, self.c_lo, self.c_hi)
         self.last_index = (ke, rows, cols)
         self.last_counts = C

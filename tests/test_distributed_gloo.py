@@ -85,7 +85,7 @@ class OracleOps:
         v = digest_words(t.contiguous().numpy(), pos0, add)
         return torch.tensor([np.uint64(v).astype(np.int64)], dtype=torch.int64)
 
-    def assemble(self, segments, n_nodes, c_lo, c_hi):
+    def assemble(self, segments, n_nodes, c_lo, c_hi, nnz_hint=None, order="auto"):
         import oracle
 
         rows, cols, vals = [], [], []
