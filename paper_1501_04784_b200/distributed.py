@@ -46,6 +46,7 @@ import torch
 from .errors import NodeIndexError
 
 __all__ = ["element_ranges", "column_bounds", "balanced_bounds", "histogram_bins", "ShardedBuild", "TorchExchange",
+           "small_h2d",
            "P2PExchange", "CudaOps", "run_loopback", "run_loopback_p2p", "RECORD_DOUBLES", "all_reduce", "barrier",
            "digest_words", "concat_blocks", "csc_digest"]
 
@@ -286,7 +287,8 @@ class P2PExchange(TorchExchange):
         receive view (int64 words))."""
         need = int(chunk[:, self.rank].sum())
         self._ensure_capacity(need)
-        offsets = torch.tensor(p2p_offsets(chunk, self.rank), dtype=torch.int64, device=self.device)
+        self._staging = getattr(self, "_staging", [])
+        offsets = small_h2d(p2p_offsets(chunk, self.rank), self.device, self._staging)
         recv = _words_view(self.own[0], need, self.device)
         return self.ptrs, offsets, recv
 
@@ -318,6 +320,18 @@ def _words_view(ptr: int, words: int, device) -> torch.Tensor:
     return torch.as_tensor(_Arr(), device=device)
 
 
+def small_h2d(values, device, keep: list | None = None) -> torch.Tensor:
+    """A small int64 array on ``device`` without a host sync: staged in pinned memory and copied
+    asynchronously (a pageable tensor.to(device) waits for the stream, idling the GPU while the host
+    prepares the next launches).  ``keep`` holds the pinned staging tensor until the copy is done
+    (the caller's next stream synchronisation)."""
+    h = torch.tensor(np.ascontiguousarray(values, dtype=np.int64).reshape(-1), dtype=torch.int64).pin_memory()
+    if keep is not None:
+        keep.append(h)
+        del keep[:-8]
+    return h.to(device, non_blocking=True)
+
+
 # ------------------------------------------------------------------------------------------
 # per-rank compute (CUDA)
 # ------------------------------------------------------------------------------------------
@@ -331,6 +345,7 @@ class CudaOps:
         self.D, self.N = D, N
         self.device = D.require_device(device)
         self.mode = mode
+        self._staging = []  # pinned sources of in-flight small copies (small_h2d)
 
     def _p(self, t):
         return self.D._ptr(t)
@@ -376,14 +391,14 @@ class CudaOps:
                                                self._s()), "hx_halo_pack")
 
     def pointers(self, bases, offsets):
-        return (torch.tensor([int(b) for b in bases], dtype=torch.int64, device=self.device),
-                torch.tensor([int(o) for o in offsets], dtype=torch.int64, device=self.device))
+        return (small_h2d([int(b) for b in bases], self.device, self._staging),
+                small_h2d([int(o) for o in offsets], self.device, self._staging))
 
     def halo_unpack(self, recv, src_desc: np.ndarray, bounds_dev, world, rank, n_rec):
         records = torch.empty((n_rec, RECORD_DOUBLES), dtype=torch.float64, device=self.device)
         if n_rec == 0:
             return records
-        desc = torch.from_numpy(np.ascontiguousarray(src_desc, dtype=np.int64)).to(self.device)
+        desc = small_h2d(src_desc, self.device, self._staging).reshape(-1, 3)
         ws_bytes = self.N.lib().hx_halo_unpack_workspace_bytes(n_rec)
         ws = torch.empty(ws_bytes, dtype=torch.uint8, device=self.device)
         self.N.check(self.N.lib().hx_halo_unpack(self._p(recv), self._p(desc), world, rank, self._p(bounds_dev), n_rec,
