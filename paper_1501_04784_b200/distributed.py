@@ -183,7 +183,11 @@ class TorchExchange:
         return all_reduce(t, group=self.group)
 
     def alltoall(self, send: torch.Tensor, send_splits, recv_splits) -> torch.Tensor:
-        recv = torch.empty(int(sum(recv_splits)), dtype=send.dtype, device=send.device)
+        n = int(sum(recv_splits))
+        buf = getattr(self, "_recv", None)  # reused across steps (stream-ordered)
+        if buf is None or buf.dtype != send.dtype or buf.device != send.device or buf.numel() < n:
+            self._recv = buf = torch.empty(max(int(n * 1.05), 1), dtype=send.dtype, device=send.device)
+        recv = buf[:n]
         kw = dict(output_split_sizes=[int(x) for x in recv_splits], input_split_sizes=[int(x) for x in send_splits])
         if send.is_cuda and _host_staged(self.group):
             r = torch.empty(recv.shape, dtype=recv.dtype)
@@ -346,6 +350,18 @@ class CudaOps:
         self.device = D.require_device(device)
         self.mode = mode
         self._staging = []  # pinned sources of in-flight small copies (small_h2d)
+        self._bufs = {}     # step-to-step scratch (records, workspaces): reused, grown on demand
+
+    def scratch(self, name: str, n: int, dtype) -> torch.Tensor:
+        """A reusable device buffer of >= n elements (stream-ordered reuse across steps): the large
+        per-step buffers are not re-allocated, so the caching allocator never has to free and
+        re-map gigabytes between steps (which synchronises the device)."""
+        b = self._bufs.get(name)
+        if b is None or b.dtype != dtype or b.numel() < n:
+            self._bufs.pop(name, None)
+            b = torch.empty(max(int(n * 1.05), 1), dtype=dtype, device=self.device)
+            self._bufs[name] = b
+        return b[:n]
 
     def _p(self, t):
         return self.D._ptr(t)
@@ -375,14 +391,15 @@ class CudaOps:
     def halo_count(self, dm, bounds_dev, world, rank):
         """-> (per_dest (world, 2) int64 device: records, values per destination; workspace)"""
         ws_bytes = self.N.lib().hx_halo_workspace_bytes(dm.n_el, world)
-        ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=self.device)
+        ws = self.scratch("halo_ws", max(ws_bytes, 1), torch.uint8)
         per_dest = torch.empty((world, 2), dtype=torch.int64, device=self.device)
         self.N.check(self.N.lib().hx_halo_count(self._p(dm.conn), dm.n_el, self._p(bounds_dev), world, rank,
                                                 self._p(per_dest), self._p(ws), ws_bytes, self._s()), "hx_halo_count")
         return per_dest, ws
 
     def alloc_words(self, n: int) -> torch.Tensor:
-        return torch.empty(n, dtype=torch.int64, device=self.device)
+        """The step's send buffer (reused across steps)."""
+        return self.scratch("send", n, torch.int64)
 
     def halo_pack(self, dm, ke, bounds_dev, world, rank, dest_ptrs, dest_offsets, ws):
         """dest_ptrs: device int64 (world,) base addresses; dest_offsets: device int64 (world,) words."""
@@ -395,12 +412,12 @@ class CudaOps:
                 small_h2d([int(o) for o in offsets], self.device, self._staging))
 
     def halo_unpack(self, recv, src_desc: np.ndarray, bounds_dev, world, rank, n_rec):
-        records = torch.empty((n_rec, RECORD_DOUBLES), dtype=torch.float64, device=self.device)
+        records = self.scratch("records", n_rec * RECORD_DOUBLES, torch.float64).view(n_rec, RECORD_DOUBLES)
         if n_rec == 0:
             return records
         desc = small_h2d(src_desc, self.device, self._staging).reshape(-1, 3)
         ws_bytes = self.N.lib().hx_halo_unpack_workspace_bytes(n_rec)
-        ws = torch.empty(ws_bytes, dtype=torch.uint8, device=self.device)
+        ws = self.scratch("unpack_ws", ws_bytes, torch.uint8)
         self.N.check(self.N.lib().hx_halo_unpack(self._p(recv), self._p(desc), world, rank, self._p(bounds_dev), n_rec,
                                                  self._p(records), self._p(ws), ws_bytes, self._s()),
                      "hx_halo_unpack")
@@ -725,7 +742,8 @@ def run_loopback_p2p(mesh, world: int, ops_factory):
     receive buffers (local memory here, peer memory across GPUs)."""
     ranks, C, chunk = _loopback_ranks(mesh, world, ops_factory)
     ops = ranks[0].ops
-    recvs = [ops.alloc_words(max(int(chunk[:, d].sum()), 1)).fill_(-1) for d in range(world)]
+    recvs = [torch.full((max(int(chunk[:, d].sum()), 1),), -1, dtype=torch.int64, device=ops.device)
+             for d in range(world)]
     for r, rk in enumerate(ranks):
         offs = p2p_offsets(chunk, r)
         rk.pack(*rk.ops.pointers([b.data_ptr() for b in recvs], offs))
