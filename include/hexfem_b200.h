@@ -256,6 +256,11 @@ int hx_triplet_csc_numeric(const double *vals, int64_t n, int64_t dim, const int
  *        a position-keyed checksum whose sum over the ranks' blocks equals that of the whole array. */
 int hx_column_weights(const int32_t *conn, int64_t n_el, int64_t n_nodes, int64_t n_bins, uint64_t *hist,
                       void *stream);
+/* touch: hist[b] += 8 per element with a node in bin b (each distinct bin of the element once) -- the
+ *        per-element work of a column block (received records, adjacency), blended with the nnz
+ *        weights so randomly numbered meshes balance records as well as nnz.  Caller-zeroed. */
+int hx_column_touch(const int32_t *conn, int64_t n_el, int64_t n_nodes, int64_t n_bins, uint64_t *hist,
+                    void *stream);
 int64_t hx_halo_workspace_bytes(int64_t n_el, int32_t world);
 int hx_halo_count(const int32_t *conn, int64_t n_el, const int64_t *col_bounds, int32_t world, int32_t self,
                   int64_t *per_dest, void *workspace, int64_t workspace_bytes, void *stream);

@@ -42,6 +42,17 @@ def column_weights(conn: np.ndarray, n_nodes: int, n_bins: int) -> np.ndarray:
     return np.bincount(b.ravel(), weights=w.ravel(), minlength=n_bins).astype(np.int64)
 
 
+def column_touch(conn: np.ndarray, n_nodes: int, n_bins: int) -> np.ndarray:
+    """hx_column_touch restated: 8 per (element, distinct bin of its nodes)."""
+    conn = np.asarray(conn, dtype=np.int64)
+    b = conn * n_bins // n_nodes
+    hist = np.zeros(n_bins, dtype=np.int64)
+    for e in range(b.shape[0]):
+        for x in set(b[e].tolist()):
+            hist[x] += 8
+    return hist
+
+
 def count(conn, bounds, world, self_rank) -> np.ndarray:
     """(world, 2) int64: records, values per destination (0 for self)."""
     out = np.zeros((world, 2), dtype=np.int64)

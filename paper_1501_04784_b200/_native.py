@@ -37,7 +37,7 @@ EXPORTED = (
     "hx_mesh_csc_workspace_bytes", "hx_mesh_csc_symbolic", "hx_mesh_csc_build", "hx_mesh_csc_numeric",
     "hx_mesh_csc_emit", "hx_integrate_emit_workspace_bytes", "hx_integrate_emit",
     "hx_triplet_csc_workspace_bytes", "hx_triplet_csc_symbolic", "hx_triplet_csc_numeric",
-    "hx_column_weights", "hx_halo_workspace_bytes", "hx_halo_count", "hx_halo_pack",
+    "hx_column_weights", "hx_column_touch", "hx_halo_workspace_bytes", "hx_halo_count", "hx_halo_pack",
     "hx_halo_unpack_workspace_bytes", "hx_halo_unpack", "hx_digest",
     "hx_ipc_alloc", "hx_ipc_open", "hx_ipc_close", "hx_ipc_free",
     "hx_block_select_workspace_bytes", "hx_block_select", "hx_block_gather", "hx_block_ranges",
@@ -103,6 +103,7 @@ def lib():
         "hx_triplet_csc_symbolic": ([P, P, I64, I64, P, P, P, I64, P, P], ctypes.c_int),
         "hx_triplet_csc_numeric": ([P, I64, I64, P, P, P, P], ctypes.c_int),
         "hx_column_weights": ([P, I64, I64, I64, P, P], ctypes.c_int),
+        "hx_column_touch": ([P, I64, I64, I64, P, P], ctypes.c_int),
         "hx_halo_workspace_bytes": ([I64, I32], I64),
         "hx_halo_count": ([P, I64, P, I32, I32, P, P, I64, P], ctypes.c_int),
         "hx_halo_pack": ([P, P, I64, P, I32, I32, P, P, P, P], ctypes.c_int),

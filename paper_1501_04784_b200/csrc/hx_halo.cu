@@ -104,6 +104,30 @@ column_weights_kernel(const int32_t *__restrict__ conn, int64_t n_el, int64_t n_
     }
 }
 
+// ---- per-bin element touches: the records / adjacency work a column block costs ---------------
+// hist[b] += 8 for every element with at least one node in bin b (distinct bins of an element).  A
+// block's received records and the elements its assembly walks scale with the elements touching it,
+// not with its nnz: on a randomly numbered mesh the high-id blocks that an nnz-balanced cut makes
+// wide receive twice the records of the low-id ones.
+__global__ void __launch_bounds__(256)
+column_touch_kernel(const int32_t *__restrict__ conn, int64_t n_el, int64_t n_nodes, int64_t n_bins,
+                    unsigned long long *__restrict__ hist) {
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n_el; e += (int64_t)gridDim.x * blockDim.x) {
+        int32_t g[8];
+        halo_load(conn, e, g);
+        int64_t b[8];
+#pragma unroll
+        for (int a = 0; a < 8; ++a) b[a] = (g[a] < 0 || g[a] >= n_nodes) ? -1 : (int64_t)g[a] * n_bins / n_nodes;
+#pragma unroll
+        for (int a = 0; a < 8; ++a) {
+            bool first = b[a] >= 0;
+#pragma unroll
+            for (int q = 0; q < a; ++q) first = first && b[q] != b[a];
+            if (first) atomicAdd(&hist[b[a]], 8ull);
+        }
+    }
+}
+
 // ---- count / pack ------------------------------------------------------------------------------
 struct HaloWs {
     int64_t *rec_counts, *val_counts, *rec_offsets, *val_offsets, *totals;  // totals: (world, 2)
@@ -402,6 +426,20 @@ extern "C" int hx_column_weights(const int32_t *conn, int64_t n_el, int64_t n_no
     column_weights_kernel<<<(unsigned)blocks, 256, smem, (cudaStream_t)stream>>>(
         conn, n_el, n_nodes, n_bins, reinterpret_cast<unsigned long long *>(hist), use_smem);
     HX_CHECK_LAUNCH("column_weights_kernel");
+    return HX_OK;
+}
+
+extern "C" int hx_column_touch(const int32_t *conn, int64_t n_el, int64_t n_nodes, int64_t n_bins, uint64_t *hist,
+                               void *stream) {
+    if (n_el < 0 || n_nodes < 1 || n_bins < 1 || n_bins > n_nodes || hist == nullptr || (n_el > 0 && conn == nullptr)) {
+        set_last_error("hx_column_touch: bad arguments");
+        return HX_ERR_VALUE;
+    }
+    if (n_el == 0) return HX_OK;
+    const int64_t blocks = std::min<int64_t>(ceil_div(n_el, 256), 148 * 16);
+    column_touch_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(
+        conn, n_el, n_nodes, n_bins, reinterpret_cast<unsigned long long *>(hist));
+    HX_CHECK_LAUNCH("column_touch_kernel");
     return HX_OK;
 }
 

@@ -46,7 +46,7 @@ import torch
 from .errors import NodeIndexError
 
 __all__ = ["element_ranges", "column_bounds", "balanced_bounds", "histogram_bins", "ShardedBuild", "TorchExchange",
-           "small_h2d",
+           "small_h2d", "block_cost_histograms", "touch_weight",
            "P2PExchange", "CudaOps", "run_loopback", "run_loopback_p2p", "RECORD_DOUBLES", "all_reduce", "barrier",
            "digest_words", "concat_blocks", "csc_digest"]
 
@@ -385,6 +385,12 @@ class CudaOps:
                                                     self._s()), "hx_column_weights")
         return hist
 
+    def column_touch(self, dm, n_nodes: int, n_bins: int) -> torch.Tensor:
+        hist = torch.zeros(n_bins, dtype=torch.int64, device=self.device)
+        self.N.check(self.N.lib().hx_column_touch(self._p(dm.conn), dm.n_el, n_nodes, n_bins, self._p(hist),
+                                                  self._s()), "hx_column_touch")
+        return hist
+
     def bounds(self, bounds_np):
         return torch.from_numpy(np.ascontiguousarray(bounds_np, dtype=np.int64)).to(self.device)
 
@@ -471,6 +477,32 @@ def _fail_error(meta: np.ndarray, e_starts, n_nodes):
     return None if best is None else best[1]
 
 
+def touch_weight() -> float:
+    """Weight of the element-touch histogram against the nnz weights in the block cost
+    (HX_BALANCE_TOUCH; measured on C5 at G = 8)."""
+    import os
+
+    return float(os.environ.get("HX_BALANCE_TOUCH", "1.0"))
+
+
+def block_cost_histograms(ops, exchange, dm, n_nodes):
+    """(nnz histogram, cost histogram) summed over the ranks (one all-reduce of both): cost = nnz
+    weights + touch_weight() x element touches, so the cut balances the assembly's per-entry AND
+    per-element work (an nnz-only cut gives the wide high-id blocks of a permuted mesh 2.3x the
+    records of the low-id ones)."""
+    bins = histogram_bins(n_nodes)
+    nnz = ops.column_weights(dm, n_nodes, bins)
+    lam = touch_weight()
+    touch_fn = getattr(ops, "column_touch", None)
+    if lam == 0.0 or touch_fn is None:
+        nnz = exchange.sum_(nnz)
+        h = nnz.cpu().numpy()
+        return h, h
+    both = exchange.sum_(torch.cat([nnz, touch_fn(dm, n_nodes, bins).to(nnz.device)]))
+    h = both.cpu().numpy()
+    return h[:bins], h[:bins] + lam * h[bins:]
+
+
 class ShardedBuild:
     """One rank's share of the global build (see module docstring)."""
 
@@ -484,10 +516,9 @@ class ShardedBuild:
         self.dm = self.ops.upload(mesh.coords, mesh.connectivity[self.e_lo:self.e_hi],
                                   mesh.coefficient[self.e_lo:self.e_hi])
         hist = None
-        if bounds is None:  # nnz-balanced: one all-reduce of the per-bin weights of every rank's elements
-            hist = self.ops.column_weights(self.dm, self.n_nodes, histogram_bins(self.n_nodes))
-            hist = self.exchange.sum_(hist)
-            bounds = balanced_bounds(hist.cpu().numpy(), self.n_nodes, world)
+        if bounds is None:
+            hist, cost = block_cost_histograms(self.ops, self.exchange, self.dm, self.n_nodes)
+            bounds = balanced_bounds(cost, self.n_nodes, world)
         self.bounds_np = np.asarray(bounds, dtype=np.int64)
         self.c_lo, self.c_hi = int(self.bounds_np[rank]), int(self.bounds_np[rank + 1])
         # the block's nnz: estimated from the column-weight histogram (units of 1/8 entry) until the
@@ -689,6 +720,14 @@ class ShardedBuild:
 # ------------------------------------------------------------------------------------------
 # loopback: G virtual ranks in one process (tests the CUDA sharded path on one GPU)
 # ------------------------------------------------------------------------------------------
+class _LocalSum:
+    """The single-process stand-in of the histogram all-reduce."""
+
+    @staticmethod
+    def sum_(t):
+        return t
+
+
 class LoopbackExchange:
     """Placeholder exchange of the in-process drivers (they move the chunks themselves)."""
 
@@ -701,8 +740,8 @@ class LoopbackExchange:
 def _loopback_ranks(mesh, world, ops_factory):
     ops0 = ops_factory()
     whole = ops0.upload(mesh.coords, mesh.connectivity, mesh.coefficient)
-    hist = ops0.column_weights(whole, mesh.n_nodes, histogram_bins(mesh.n_nodes))
-    bounds = balanced_bounds(hist.cpu().numpy(), mesh.n_nodes, world)
+    _, cost = block_cost_histograms(ops0, _LocalSum(), whole, mesh.n_nodes)
+    bounds = balanced_bounds(cost, mesh.n_nodes, world)
     del whole
     ranks = [ShardedBuild(mesh, r, world, ops=ops_factory(), exchange=LoopbackExchange(), bounds=bounds)
              for r in range(world)]

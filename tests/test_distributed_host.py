@@ -223,3 +223,16 @@ def test_p2p_mapping_opens_peers_only_and_remaps_on_growth(tmp_path):
         assert len(allocs) == (2 if r == 1 else 1)
         assert len(closed) == 1                                  # the stale mapping was closed
         assert peers == ptrs and len(peers) == world
+
+
+def test_column_touch_oracle_counts_elements_per_block():
+    """The touch histogram summed over a block's bins bounds the elements touching the block (equal
+    when each element's nodes in the block share one bin) and equals 8 n_el x distinct bins."""
+    from oracle import halo
+
+    mesh = permuted_mesh(perturbed_mesh(6, seed=1), seed=2)
+    h = halo.column_touch(mesh.connectivity, mesh.n_nodes, mesh.n_nodes)  # one bin per node
+    distinct = sum(len(set(row.tolist())) for row in mesh.connectivity)
+    assert h.sum() == 8 * distinct == 8 * 8 * mesh.n_el
+    h1 = halo.column_touch(mesh.connectivity, mesh.n_nodes, 1)
+    assert h1.tolist() == [8 * mesh.n_el]

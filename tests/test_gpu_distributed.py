@@ -7,6 +7,7 @@ import torch
 
 from common import bits_equal, golden_mesh
 from paper_1501_04784_b200 import device as D
+from paper_1501_04784_b200 import distributed as X
 from paper_1501_04784_b200.distributed import CudaOps, concat_blocks, run_loopback, run_loopback_p2p
 from paper_1501_04784_b200.pipeline import build_device
 from paper_1501_04784_b200.workloads import make_workload, permuted_mesh, perturbed_mesh
@@ -176,3 +177,16 @@ def test_loopback_bad_node_id_raises_node_index_error():
         run_loopback(bad, 3, lambda: CudaOps())
     assert ei.value.element_id == 20 and ei.value.node == -1
     assert isinstance(ei.value, MeshValidationError) and isinstance(ei.value, IndexError)
+
+
+@pytest.mark.parametrize("kind", ["structured", "permuted"])
+def test_column_touch_matches_oracle(kind):
+    """hx_column_touch: 8 per (element, distinct histogram bin of its nodes) -- the oracle restatement."""
+    from oracle import halo
+
+    mesh = perturbed_mesh(10, seed=3) if kind == "structured" else permuted_mesh(perturbed_mesh(10, seed=3), seed=4)
+    ops = X.CudaOps()
+    dm = ops.upload(mesh.coords, mesh.connectivity, mesh.coefficient)
+    for bins in (1, 7, 300, mesh.n_nodes):
+        got = ops.column_touch(dm, mesh.n_nodes, bins).cpu().numpy()
+        assert np.array_equal(got, halo.column_touch(mesh.connectivity, mesh.n_nodes, bins))

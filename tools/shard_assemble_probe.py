@@ -53,24 +53,21 @@ def timed(name, fn):
     return out
 
 
-for rep in range(3):
+def wrap(obj, name):
+    fn = getattr(obj, name)
+
+    def w(*a, **k):
+        return timed(name, lambda: fn(*a, **k))
+    setattr(obj, name, w)
+
+
+for name in ("integrate", "halo_count", "halo_unpack", "assemble"):
+    wrap(rk.ops, name)
+for rep in range(5):
     print(f"rep {rep}")
     timed("phase_local", rk.phase_local)
-    desc = np.zeros((world, 3), dtype=np.int64)
-    desc[:, 0] = np.concatenate([[0], np.cumsum(chunk[:, r])[:-1]])
-    desc[:, 1:] = C[:, r, :]
-    n_rec = int(C[:, r, 0].sum())
-    records = timed("halo_unpack", lambda: rk.ops.halo_unpack(recv, desc, rk.bounds, world, r, n_rec))
-    ke = rk._pending[0]
-    n_lower = int(C[:r, r, 0].sum())
-    segs = []
-    if n_lower:
-        segs.append(X.record_segment(records[:n_lower]))
-    segs.append((rk.dm.conn, ke))
-    if n_rec > n_lower:
-        segs.append(X.record_segment(records[n_lower:]))
-    csc = timed("mesh_csc", lambda: rk.ops.assemble(segs, rk.n_nodes, rk.c_lo, rk.c_hi, nnz_hint=rk.nnz_hint,
-                                                   order=rk.order))
-    rk.nnz_hint = int(csc.row_idx.shape[0])
-    print(f"  order {rk.order} nnz {rk.nnz_hint} records {n_rec} own {rk.dm.n_el}")
-    rk._pending = None
+    send = rk.ops.alloc_words(int(chunk[r].sum()))
+    offs = np.concatenate([[0], np.cumsum(chunk[r])[:-1]])
+    timed("pack", lambda: rk.pack(*rk.ops.pointers([send.data_ptr()] * world, offs)))
+    timed("phase_assemble", lambda: rk.phase_assemble(recv, C))
+    print(f"  mem allocated {torch.cuda.memory_allocated() / 1e9:.2f} GB reserved {torch.cuda.memory_reserved() / 1e9:.2f} GB")

@@ -26,9 +26,9 @@ mesh = make_workload(wl)
 for world in [int(g) for g in (args[1:] or ["2", "4", "8"])]:
     ops0 = X.CudaOps()
     whole = ops0.upload(mesh.coords, mesh.connectivity, mesh.coefficient)
-    hist = ops0.column_weights(whole, mesh.n_nodes, X.histogram_bins(mesh.n_nodes))
-    bounds = X.balanced_bounds(hist.cpu().numpy(), mesh.n_nodes, world)
-    del whole, hist
+    _, cost = X.block_cost_histograms(ops0, X._LocalSum(), whole, mesh.n_nodes)
+    bounds = X.balanced_bounds(cost, mesh.n_nodes, world)
+    del whole
     # one loopback pass: every rank's received words (kept on the host), the count matrix
     recv_host, C = [], None
     ranks = [X.ShardedBuild(mesh, r, world, ops=X.CudaOps(), exchange=X.LoopbackExchange(), bounds=bounds)
@@ -79,3 +79,6 @@ for world in [int(g) for g in (args[1:] or ["2", "4", "8"])]:
           f"{max(t[0] for t in rows):.2f}, pack max {max(t[1] for t in rows):.2f}, unpack+assemble max "
           f"{max(t[2] for t in rows):.2f}; -> {mesh.n_el / ms / 1e6:.2f} G el/s without collectives; exchange "
           f"{xb / 1e9:.3f} GB ({xb / mesh.n_el:.1f} B/el, {xb_recs / mesh.n_el:.2f} records/el)", flush=True)
+    print("   per rank (integrate+count, pack, unpack+assemble) ms:",
+          " ".join(f"[{a:.2f} {b:.2f} {c:.2f}]" for a, b, c in rows), flush=True)
+    print("   records received per rank:", [int(C[:, d, 0].sum() - C[d, d, 0]) for d in range(world)], flush=True)
