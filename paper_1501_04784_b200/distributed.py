@@ -482,7 +482,7 @@ def touch_weight() -> float:
     (HX_BALANCE_TOUCH; measured on C5 at G = 8)."""
     import os
 
-    return float(os.environ.get("HX_BALANCE_TOUCH", "1.0"))
+    return float(os.environ.get("HX_BALANCE_TOUCH", "4.0"))
 
 
 def block_cost_histograms(ops, exchange, dm, n_nodes):
