@@ -190,7 +190,14 @@ halo_count_kernel(const int32_t *__restrict__ conn, int64_t n_el, const int64_t 
     int o[8];
     element_owners(conn, e, n_el, bounds, world, g, o);
     for (int d = 0; d < world; ++d) {
-        const int k = d == self ? 0 : owned_count(o, d);
+        if (d == self) continue;
+        // an element sends to d iff one of its nodes is owned by d (its diagonal entry): skip the
+        // destinations no element of this warp touches (most of them on locally numbered meshes)
+        bool touches = false;
+#pragma unroll
+        for (int a = 0; a < 8; ++a) touches |= o[a] == d;
+        if (!__any_sync(0xffffffffu, touches)) continue;
+        const int k = owned_count(o, d);
         const unsigned ballot = __ballot_sync(0xffffffffu, k > 0);
         int ks = k;
 #pragma unroll
@@ -242,7 +249,10 @@ halo_pack_kernel(const int32_t *__restrict__ conn, const double *__restrict__ ke
     for (int d = 0; d < world; ++d) {
         // nothing of this tile goes to d (block-uniform, from the count pass): skip the scan and syncs
         if (d == self || rec_counts[(int64_t)d * n_tiles + blockIdx.x] == 0) continue;
-        const int k = owned_count(o, d);
+        bool touches = false;
+#pragma unroll
+        for (int a = 0; a < 8; ++a) touches |= o[a] == d;
+        const int k = __any_sync(0xffffffffu, touches) ? owned_count(o, d) : 0;
         const unsigned ballot = __ballot_sync(0xffffffffu, k > 0);
         int incl = k;  // inclusive warp scan of k
 #pragma unroll
