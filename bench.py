@@ -167,6 +167,20 @@ def reference_step(sample, threads):
     return time.perf_counter() - t0, len(row_idx)
 
 
+def host_info(threads) -> dict:
+    """Host facts BASELINE.md asks for next to a CPU number: RAM, cores used, and the numba thread
+    count the reference would run with (the port's C kernel uses the same pthreads count)."""
+    ram = None
+    try:
+        import psutil
+
+        ram = round(psutil.virtual_memory().total / 2**30, 1)
+    except Exception:
+        pass
+    return {"host_ram_gib": ram, "numba_num_threads": int(os.environ.get("NUMBA_NUM_THREADS", threads)),
+            "logical_cpus": os.cpu_count()}
+
+
 def cpu_baseline(mesh, side, layers, repeats=2):
     threads = os.cpu_count() or 1
     sample = cpu_sample_mesh(mesh, side, layers)
@@ -176,7 +190,7 @@ def cpu_baseline(mesh, side, layers, repeats=2):
             "sample": f"first {layers} z-layers of the workload mesh ({sample.n_el} elements, {sample.n_nodes} nodes); "
                       f"reference triplet-path algorithm: numpy gather + C/pthreads KE (no FMA, bitwise = reference) + "
                       f"numpy index arrays + numpy lexsort/reduceat; best of {repeats}",
-            "seconds": best}
+            "seconds": best, **host_info(threads)}
 
 
 def run_reference(args):
@@ -201,7 +215,8 @@ def run_reference(args):
         "config": {"workload": f"{args.workload.upper()}: {WORKLOADS[args.workload.upper()]['desc']}",
                    "sample_elements": sample.n_el, "parallelism": f"host threads ({threads})"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": f"first {args.cpu_sample_layers} z-layers ({sample.n_el} elements) per step"},
+                         "sample": f"first {args.cpu_sample_layers} z-layers ({sample.n_el} elements) per step",
+                         **host_info(threads)},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
