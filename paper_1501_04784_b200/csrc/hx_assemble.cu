@@ -267,81 +267,25 @@ __device__ __forceinline__ void oddeven_merge_sort(K (&v)[N]) {
     }
 }
 
-// Finish a column (warp-uniform N; every lane of the warp calls it, empty columns with cnt = 0):
-// sort its cnt (<= N) contribution keys in registers, count the distinct rows (key >> 6) and check
-// that no row has more than MAX_OFFDIAG_CONTRIB contributions (sorted: a run of 5 has v[q] and
-// v[q - 4] in the same row), reserve the warp's off-diagonal records with one atomic (warp scan of
-// the per-column counts) and write them straight from the registers: runs of equal rows -> (row,
-// count | (k, b) pairs in element order).  Returns m (0: empty or outside the fast path).
+// Sort the first n (<= N) contribution keys of L in place and, while they are in registers, count
+// the distinct rows (key >> 6) and check that no row has more than MAX_OFFDIAG_CONTRIB
+// contributions (sorted: a run of 5 has v[q] and v[q - 4] in the same row).
 template <int N, typename K>
-__device__ __forceinline__ int finish_column(K *L, int cnt, int m, int2 *__restrict__ scratch,
-                                             int64_t scratch_capacity, unsigned long long *__restrict__ scratch_top,
-                                             int64_t *__restrict__ warp_base, uint32_t *__restrict__ status) {
-    const int lane = threadIdx.x & 31;
+__device__ __forceinline__ void sort_count(K *L, int n, int &rows, bool &ok) {
     K v[N];
 #pragma unroll
-    for (int q = 0; q < N; ++q) v[q] = q < cnt ? L[q * COL_BLOCK] : (K)~(K)0;
+    for (int q = 0; q < N; ++q) v[q] = q < n ? L[q * COL_BLOCK] : (K)~(K)0;
     if (HX_PATTERN_NET) oddeven_merge_sort<N, K>(v);
     else bitonic_sort<N, K>(v);
-    int rows = 0;
-    bool ok = true;
+    rows = 0;
+    ok = true;
 #pragma unroll
     for (int q = 0; q < N; ++q) {
+        if (q < n) L[q * COL_BLOCK] = v[q];
         const K r = v[q] >> 6;
-        rows += q < cnt && (q == 0 || r != (v[q > 0 ? q - 1 : 0] >> 6));
-        if (q >= MAX_OFFDIAG_CONTRIB) ok &= !(q < cnt && r == (v[q >= MAX_OFFDIAG_CONTRIB ? q - MAX_OFFDIAG_CONTRIB : 0] >> 6));
+        rows += q < n && (q == 0 || r != (v[q > 0 ? q - 1 : 0] >> 6));
+        if (q >= MAX_OFFDIAG_CONTRIB) ok &= !(q < n && r == (v[q >= MAX_OFFDIAG_CONTRIB ? q - MAX_OFFDIAG_CONTRIB : 0] >> 6));
     }
-    if (m > 0 && (!ok || rows > MAXR)) {
-        atomicOr(status, HX_ST_ROW_OVERFLOW);
-        m = 0;
-    }
-    // 64 keys do not stay in registers across the scan (spills): that rare path re-reads them
-    constexpr bool REG = N <= 32;
-    if (!REG) {
-#pragma unroll
-        for (int q = 0; q < N; ++q)
-            if (q < cnt) L[q * COL_BLOCK] = v[q];
-    }
-    if (m > 0) m += rows;
-    const int off = m > 0 ? m - 1 : 0;
-    int incl = off;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-        const int x = __shfl_up_sync(0xffffffffu, incl, d);
-        if (lane >= d) incl += x;
-    }
-    const int total = __shfl_sync(0xffffffffu, incl, 31);
-    unsigned long long base = 0;
-    if (lane == 0) {
-        base = atomicAdd(scratch_top, (unsigned long long)total);
-        *warp_base = (int64_t)base;
-    }
-    base = __shfl_sync(0xffffffffu, base, 0);
-    if ((int64_t)base + total > scratch_capacity) {
-        if (off > 0) atomicOr(status, HX_ST_SCRATCH_OVERFLOW);
-        return m;
-    }
-    if (off == 0) return m;
-    int2 *out = scratch + (int64_t)base + (incl - off) - 1;  // record j at out[j + 1]
-    int j = -1, shift = 3;
-    K prev = ~(K)0;
-    uint32_t word = 0;
-#pragma unroll
-    for (int q = 0; q < N; ++q) {
-        if (q < cnt) {
-            const K key = REG ? v[q] : L[q * COL_BLOCK];
-            const K r = key >> 6;
-            const uint32_t kb = (uint32_t)key & 63u;
-            const bool head = r != prev;
-            if (head && j >= 0) out[j + 1] = make_int2((int)prev, (int)word);
-            j += head;
-            word = head ? (1u | (kb << 3)) : ((word + 1u) | (kb << shift));
-            shift = head ? 9 : shift + 6;
-            prev = r;
-        }
-    }
-    if (j >= 0) out[j + 1] = make_int2((int)prev, (int)word);
-    return m;
 }
 
 template <typename K, bool SINGLE, bool FIXED>
@@ -389,7 +333,19 @@ __device__ __forceinline__ int column_pattern_sort(const SegTable &T, bool activ
                 L[cnt * COL_BLOCK] = ((K)(uint32_t)v << 6) | (K)(k * 8 + b);  // kept only when v > c
                 cnt += (int)((uint32_t)(c - v) >> 31);
             }
-        m = 1;  // the diagonal; finish_column adds the distinct rows below it
+        const unsigned am = __activemask();
+        // distinct rows; a row with more than MAX_OFFDIAG_CONTRIB contributions leaves the fast path
+        int rows = 0;
+        bool ok = true;
+        if (!__any_sync(am, cnt > 16)) sort_count<16, K>(L, cnt, rows, ok);
+        else if (!__any_sync(am, cnt > 32)) sort_count<32, K>(L, cnt, rows, ok);
+        else sort_count<64, K>(L, cnt, rows, ok);
+        if (!ok || rows > MAXR) {
+            atomicOr(status, HX_ST_ROW_OVERFLOW);
+            cnt = 0;
+        } else {
+            m = 1 + rows;
+        }
     }
     return m;
 }
@@ -415,6 +371,9 @@ pattern_kernel(SegTable T, int64_t col_lo, int64_t ncols, int32_t *__restrict__ 
                const uint32_t *__restrict__ order, unsigned long long *__restrict__ slot_total,
                int32_t *__restrict__ tile_need, int32_t *__restrict__ tadj, int32_t *__restrict__ tdeg) {
     __shared__ K sL[SORT_SLOTS * COL_BLOCK];  // this thread's contribution keys, [slot][thread]
+    __shared__ unsigned long long s_base;
+    using BlockScan = cub::BlockScan<int32_t, COL_BLOCK>;
+    __shared__ typename BlockScan::TempStorage scan_tmp;
     const int t = threadIdx.x;
     const int64_t idx = (int64_t)blockIdx.x * COL_BLOCK + t;  // position in the processing order
     const int64_t cl = order != nullptr && idx < ncols ? (int64_t)__ldg(order + idx) : idx;
@@ -424,27 +383,51 @@ pattern_kernel(SegTable T, int64_t col_lo, int64_t ncols, int32_t *__restrict__ 
     int32_t last = -1;
     // sorted incident lists and degrees in processing order (in place over adj / deg in column order)
     int32_t *ent_out = (order != nullptr ? tadj : adj) + 8 * idx;
-    int m = column_pattern_sort<K, SINGLE, FIXED>(T, cl < ncols, cl, c, deg_arr, adj, ent_out, L, cnt, deg, last,
-                                                  status);
+    const int m = column_pattern_sort<K, SINGLE, FIXED>(T, cl < ncols, cl, c, deg_arr, adj, ent_out, L, cnt, deg, last,
+                                                        status);
     if (cl < ncols) (order != nullptr ? tdeg : deg_arr)[idx] = deg;
     {  // elements the tile's emit needs: every incident element < tile_need (the fused kernel waits for them)
         const int need = __reduce_max_sync(0xffffffffu, last + 1);
         if ((t & 31) == 0) atomicMax(tile_need + blockIdx.x, need);
     }
+    if (cl < ncols) col_ptr[cl] = m;
     if (FIXED) {
         const unsigned filled = __reduce_add_sync(0xffffffffu, (unsigned)deg);
         if ((t & 31) == 0 && filled) atomicAdd(slot_total, (unsigned long long)filled);
     }
-    // sort + count + records, warp-uniform network size; the warp's records go to one scratch
-    // region (block_scratch[tile * WARPS + warp] = its first record)
-    int64_t *wb = block_scratch + (int64_t)blockIdx.x * (COL_BLOCK / 32) + (t >> 5);
-    if (!__any_sync(0xffffffffu, cnt > 16))
-        m = finish_column<16, K>(L, cnt, m, scratch, scratch_capacity, scratch_top, wb, status);
-    else if (!__any_sync(0xffffffffu, cnt > 32))
-        m = finish_column<32, K>(L, cnt, m, scratch, scratch_capacity, scratch_top, wb, status);
-    else
-        m = finish_column<64, K>(L, cnt, m, scratch, scratch_capacity, scratch_top, wb, status);
-    if (cl < ncols) col_ptr[cl] = m;
+
+    // compact scratch: this block's off-diagonal records
+    int excl, total;
+    const int off = m > 0 ? m - 1 : 0;
+    BlockScan(scan_tmp).ExclusiveSum(off, excl, total);
+    if (t == 0) {
+        s_base = atomicAdd(scratch_top, (unsigned long long)total);
+        block_scratch[blockIdx.x] = (int64_t)s_base;
+    }
+    __syncthreads();
+    const int64_t sb = (int64_t)s_base + excl;
+    if (sb + off > scratch_capacity) {
+        if (off > 0) atomicOr(status, HX_ST_SCRATCH_OVERFLOW);
+        return;
+    }
+    // runs of equal rows -> records (row, count | (k, b) pairs in element order)
+    int2 *out = scratch + sb - 1;  // record j of this column at out[j + 1]; j = -1 before the first
+    int j = -1, shift = 3;
+    K prev = ~(K)0;
+    uint32_t word = 0;
+#pragma unroll 1
+    for (int q = 0; q < cnt; ++q) {
+        const K key = L[q * COL_BLOCK];
+        const K v = key >> 6;
+        const uint32_t kb = (uint32_t)key & 63u;
+        const bool head = v != prev;
+        if (head && j >= 0) out[j + 1] = make_int2((int)prev, (int)word);
+        j += head;
+        word = head ? (1u | (kb << 3)) : ((word + 1u) | (kb << shift));
+        shift = head ? 9 : shift + 6;
+        prev = v;
+    }
+    if (j >= 0) out[j + 1] = make_int2((int)prev, (int)word);
 }
 
 // Fixed-slot adjacency check: every (element, local node) pair must have landed in its own slot.
@@ -505,7 +488,6 @@ struct EmitSmem {
     int32_t s_deg[COL_BLOCK];
     int32_t s_adj[COL_BLOCK * 8];     // the tile's sorted incident lists
     uint8_t s_col[COL_BLOCK * MAXR];  // tile position of each off-diagonal record
-    int64_t s_wadj[COL_BLOCK / 32];   // per pattern warp: scratch address of its first record - its s_rs
 };
 
 // Arguments of the emit pass over one column range (the pattern pass's workspace + outputs).
@@ -595,9 +577,7 @@ __device__ __forceinline__ void emit_tile(EmitSmem &S, const EmitArgs &A, int64_
         if (l == 31) S.s_rs[COL_BLOCK] = incl;
     }
     tile_sync<NT>();
-    // the pattern pass stored each warp's records (its 32 columns, in order) from block_scratch[tile *
-    // WARPS + w]: record q of tile column u lives at s_wadj[u / 32] + q
-    if (tid < COL_BLOCK / 32) S.s_wadj[tid] = block_scratch[tile * (COL_BLOCK / 32) + tid] - S.s_rs[32 * tid];
+    const int64_t sb = block_scratch[tile];
     const int n_off = S.s_rs[COL_BLOCK];
     for (int u = tid; u < ncol; u += NT)
         for (int q = S.s_rs[u]; q < S.s_rs[u] + S.s_m[u] - 1; ++q) S.s_col[q] = (uint8_t)u;
@@ -670,7 +650,7 @@ __device__ __forceinline__ void emit_tile(EmitSmem &S, const EmitArgs &A, int64_
             const bool has = q < n_off;
             u[i] = has ? S.s_col[q] : 0;
             o[i] = has ? S.s_start[u[i]] + 1 + (q - S.s_rs[u[i]]) : capacity;
-            rec[i] = has ? __ldcs(scratch + S.s_wadj[u[i] >> 5] + q) : make_int2(0, 0);  // streamed once
+            rec[i] = has ? __ldcs(scratch + sb + q) : make_int2(0, 0);  // streamed once: evict first
         }
         if (ROWS) {
 #pragma unroll
@@ -843,7 +823,7 @@ static MeshWs mesh_ws_layout(void *base, int64_t ncols, int64_t workspace_bytes 
     const size_t o_flag = take(sizeof(uint32_t));
     const size_t o_deg = take(sizeof(int32_t) * nc);
     const size_t o_adj = take(sizeof(int32_t) * 8 * nc);
-    const size_t o_bs = take(sizeof(int64_t) * (COL_BLOCK / 32) * std::max<int64_t>(1, ceil_div(ncols, COL_BLOCK)));
+    const size_t o_bs = take(sizeof(int64_t) * std::max<int64_t>(1, ceil_div(ncols, COL_BLOCK)));
     const size_t o_tn = take(sizeof(int32_t) * std::max<int64_t>(1, ceil_div(ncols, COL_BLOCK)));
     const size_t o_ta = take(sizeof(int32_t) * 8 * nc), o_td = take(sizeof(int32_t) * nc);
     const size_t o_st = take(2 * sizeof(unsigned long long));  // scratch_top, slot_total
