@@ -563,13 +563,20 @@ def measure_e2e(args, mesh, nnz):
     ms = (time.perf_counter() - t0) * 1e3 / steps
     del matrix
     st = np.array(stages).mean(axis=0)
+    from paper_1501_04784_b200.pipeline import LAST_RUN_STATS
+
+    if "d2h_bytes" in LAST_RUN_STATS:  # what the streamed call actually moved (row codec: ~2 B per row)
+        d2h = int(LAST_RUN_STATS["d2h_bytes"])
+    coded = LAST_RUN_STATS.get("row_codec_blocks", 0)
     return {"value": mesh.n_el / (ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
             "ms_per_step": ms, "steps": steps,
             "api": "pipeline.run_build(mesh in pinned host memory) -> (LowerCscMatrix host arrays, BuildReport): "
                    "the reference's cli.py:65-149 entry point, one synchronous call per step",
             "report_stage_ms": {"integration_incl_upload_overlap": 1e3 * st[0], "assembly": 1e3 * st[1],
                                 "total_call": 1e3 * st[2]},
-            "row_transfer": "int32 over PCIe, widened to int64 on the host cores chunk by chunk",
+            "row_transfer": ("delta-encoded (hx_rows_encode: Stream-VByte groups of row deltas, u8 per-column "
+                             "counts instead of col_ptr), decoded to int64 on the host cores (hx_rows_decode)"
+                             if coded else "int32 over PCIe, widened to int64 on the host cores chunk by chunk"),
             "warmup_call_ms": [round(x, 1) for x in first_ms]}
 
 
@@ -647,11 +654,13 @@ def measure_e2e_pipelined(args, mesh, nnz):
     drain()
     ms = (time.perf_counter() - t0) * 1e3 / steps
     if compact:
+        d2h = xfer.bytes_per_transfer(nnz)  # the codec's actual bytes once a transfer ran
         xfer.close()
     return {"value": mesh.n_el / (ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
             "ms_per_step": ms, "steps": steps,
-            "pipelined": "step i's D2H (+ host widening) overlaps step i+1's H2D + build",
-            "row_transfer": "int32 over PCIe, widened to int64 on the host" if compact else "int64",
+            "pipelined": "step i's D2H (+ host decode) overlaps step i+1's H2D + build",
+            "row_transfer": (("delta-encoded rows (hx_rows_encode / hx_rows_decode)" if xfer.codec else
+                              "int32 over PCIe, widened to int64 on the host") if compact else "int64"),
             "api": "DeviceMesh(pinned host -> HBM) + build_device + transfer.CscHostTransfer -> host LowerCscMatrix"
                    if compact else "DeviceMesh(pinned host -> HBM) + build_device + CSC -> pinned host"}
 

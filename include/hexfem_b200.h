@@ -326,6 +326,24 @@ typedef struct hx_peek_args {
 int hx_peek(const hx_peek_args *args, int64_t *host_dst, void *stream);
 int hx_rows_widen(const int32_t *rows32, int64_t *row_idx, int64_t n, int32_t threads);
 
+/* Row-index codec of the device -> host transfer (the PCIe bytes bound the end-to-end build).
+ * encode (device): each column's ascending rows as deltas from the column id / previous row, in
+ *   Stream-VByte groups of 4 (one control byte of 2-bit byte lengths, then the deltas' little-endian
+ *   bytes; a partial last group padded with 1-byte zeros), columns concatenated.  counts (ncols) u8
+ *   = rows per column (col_ptr differences), lens (ncols) u8 = bytes per column, bytes = the stream
+ *   (capacity bytes; 5 * nnz + 17 * ncols always suffices); *total (device int64) = stream bytes, or
+ *   -1 when a column has more than 36 rows (send the rows uncompressed instead).  Workspace:
+ *   hx_rows_encode_workspace_bytes(ncols).
+ * decode (HOST): rows_out (int64, sum(counts) entries) and col_ptr_out (ncols entries: row_base +
+ *   the rows of columns 0..j) from counts / lens / bytes; all host cores (threads <= 0) or the given
+ *   count; bytes must be readable for 16 bytes past nbytes.  SSSE3 + SSE4.1. */
+int64_t hx_rows_encode_workspace_bytes(int64_t ncols);
+int hx_rows_encode(const int64_t *col_ptr, const int64_t *row_idx, int64_t ncols, int64_t col_lo, uint8_t *counts,
+                   uint8_t *lens, uint8_t *bytes, int64_t capacity, int64_t *total, void *workspace,
+                   int64_t workspace_bytes, void *stream);
+int hx_rows_decode(const uint8_t *counts, const uint8_t *lens, const uint8_t *bytes, int64_t nbytes, int64_t ncols,
+                   int64_t col_lo, int64_t row_base, int64_t *col_ptr_out, int64_t *rows_out, int32_t threads);
+
 /* ---- Matrix Market export (sparseio.py:73-87), host code -----------------------------------------
  * Host arrays of a lower CSC -> "%%MatrixMarket matrix coordinate real symmetric" file, 1-based,
  * column-major, "%.17g" values: byte-identical to the reference's writer, formatted by `threads`

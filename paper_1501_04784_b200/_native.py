@@ -42,6 +42,7 @@ EXPORTED = (
     "hx_ipc_alloc", "hx_ipc_open", "hx_ipc_close", "hx_ipc_free",
     "hx_block_select_workspace_bytes", "hx_block_select", "hx_block_gather", "hx_block_ranges",
     "hx_mm_write", "hx_mm_read", "hx_generate_cube_mesh", "hx_rows_narrow", "hx_rows_widen", "hx_peek",
+    "hx_rows_encode_workspace_bytes", "hx_rows_encode", "hx_rows_decode",
 )
 
 
@@ -117,6 +118,9 @@ def lib():
         "hx_mm_write": ([P, P, P, I64, ctypes.c_char_p, I32], ctypes.c_int),
         "hx_rows_narrow": ([P, P, I64, P], ctypes.c_int),
         "hx_rows_widen": ([P, P, I64, I32], ctypes.c_int),
+        "hx_rows_encode_workspace_bytes": ([I64], I64),
+        "hx_rows_encode": ([P, P, I64, I64, P, P, P, I64, P, P, I64, P], ctypes.c_int),
+        "hx_rows_decode": ([P, P, P, I64, I64, I64, I64, P, P, I32], ctypes.c_int),
         "hx_peek": ([P, P, P], ctypes.c_int),
         "hx_mm_read": ([ctypes.c_char_p, P, P, P, P, P, P], ctypes.c_int),
         "hx_generate_cube_mesh": ([I64, I64, I64, ctypes.c_double, ctypes.c_double, P, P, P, P], ctypes.c_int),

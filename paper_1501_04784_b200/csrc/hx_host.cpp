@@ -43,6 +43,139 @@ __attribute__((target("avx512f"))) void widen_avx512(const int32_t *src, int64_t
     _mm_sfence();
 }
 
+// ---- row-index codec, host half (hx_rows_encode's format, hx_transfer.cu) ------------------------
+struct CodecTables {
+    alignas(16) uint8_t shuf[256][16];
+    uint8_t len[256];
+    CodecTables() {
+        for (int c = 0; c < 256; ++c) {
+            int off = 0;
+            for (int k = 0; k < 4; ++k) {
+                const int nb = ((c >> (2 * k)) & 3) + 1;
+                for (int q = 0; q < 4; ++q) shuf[c][4 * k + q] = q < nb ? (uint8_t)(off + q) : 0x80;
+                off += nb;
+            }
+            len[c] = (uint8_t)off;
+        }
+    }
+};
+const CodecTables &codec_tables() {
+    static const CodecTables t;
+    return t;
+}
+
+// Columns [j0, j1) of a block: rows_out / bytes at this range's first row / byte.  Every group but
+// the range's very last one is decoded 4 rows at a time (the 0..3 rows past a column's end are
+// rewritten by the next column); the range's last group is written exactly (no race with the next
+// range).  Returns the bytes consumed.
+__attribute__((target("ssse3,sse4.1"))) int64_t decode_columns(const uint8_t *counts, const uint8_t *bytes,
+                                                                 int64_t j0, int64_t j1, int64_t col_lo,
+                                                                 int64_t *rows_out) {
+    const CodecTables &T = codec_tables();
+    const uint8_t *p = bytes;
+    int64_t *out = rows_out;
+    int64_t j_end = j1 - 1;  // the range's last non-empty column writes its final group exactly
+    while (j_end > j0 && counts[j_end] == 0) --j_end;
+    for (int64_t j = j0; j < j1; ++j) {
+        const int m = counts[j];
+        const int groups = (m + 3) >> 2;
+        const uint8_t *ctrl = p;
+        const uint8_t *data = p + groups;
+        __m128i base = _mm_set1_epi32((int)(uint32_t)(col_lo + j));
+        for (int g = 0; g < groups; ++g) {
+            const uint8_t c = ctrl[g];
+            __m128i v = _mm_shuffle_epi8(_mm_loadu_si128(reinterpret_cast<const __m128i *>(data)),
+                                         _mm_load_si128(reinterpret_cast<const __m128i *>(T.shuf[c])));
+            v = _mm_add_epi32(v, _mm_slli_si128(v, 4));
+            v = _mm_add_epi32(v, _mm_slli_si128(v, 8));
+            v = _mm_add_epi32(v, base);
+            const bool tail = j == j_end && g == groups - 1;
+            if (!tail) {
+                _mm_storeu_si128(reinterpret_cast<__m128i *>(out + 4 * g), _mm_cvtepu32_epi64(v));
+                _mm_storeu_si128(reinterpret_cast<__m128i *>(out + 4 * g + 2), _mm_cvtepu32_epi64(_mm_srli_si128(v, 8)));
+            } else {
+                alignas(16) uint32_t x[4];
+                _mm_store_si128(reinterpret_cast<__m128i *>(x), v);
+                for (int k = 0; k < m - 4 * g; ++k) out[4 * g + k] = (int64_t)x[k];
+            }
+            base = _mm_shuffle_epi32(v, 0xFF);
+            data += T.len[c];
+        }
+        out += m;
+        p = data;
+    }
+    return p - bytes;
+}
+
+}  // namespace
+
+// Decode hx_rows_encode's stream into int64 rows (the reference's row_idx dtype) and col_ptr ends
+// (col_ptr_out[j] = row_base + rows of columns 0..j), all host cores: each worker takes a range of
+// columns, whose first row / byte come from a first parallel pass over the counts and lengths.
+extern "C" int hx_rows_decode(const uint8_t *counts, const uint8_t *lens, const uint8_t *bytes, int64_t nbytes,
+                              int64_t ncols, int64_t col_lo, int64_t row_base, int64_t *col_ptr_out,
+                              int64_t *rows_out, int32_t threads) {
+    if (ncols < 0 || nbytes < 0 || (ncols > 0 && (counts == nullptr || lens == nullptr || col_ptr_out == nullptr)) ||
+        (nbytes > 0 && (bytes == nullptr || rows_out == nullptr))) {
+        hx::set_last_error("hx_rows_decode: bad arguments");
+        return HX_ERR_VALUE;
+    }
+    if (ncols == 0) return HX_OK;
+    if (!__builtin_cpu_supports("ssse3") || !__builtin_cpu_supports("sse4.1")) {
+        hx::set_last_error("hx_rows_decode: the host CPU lacks SSSE3 / SSE4.1");
+        return HX_ERR_CONFIG;
+    }
+    const int hw = (int)std::max(1u, std::thread::hardware_concurrency());
+    constexpr int64_t MIN_COLS = int64_t(1) << 15;
+    const int nt = (int)std::max<int64_t>(1, std::min<int64_t>(threads > 0 ? threads : hw, ncols / MIN_COLS + 1));
+    std::vector<int64_t> jb(nt + 1), rows_before(nt + 1, 0), bytes_before(nt + 1, 0);
+    for (int t = 0; t <= nt; ++t) jb[t] = ncols * t / nt;
+    auto run = [&](auto &&fn) {
+        std::vector<std::thread> pool;
+        pool.reserve(nt - 1);
+        for (int t = 1; t < nt; ++t) pool.emplace_back(fn, t);
+        fn(0);
+        for (auto &th : pool) th.join();
+    };
+    run([&](int t) {  // per range: rows and bytes
+        int64_t r = 0, b = 0;
+        for (int64_t j = jb[t]; j < jb[t + 1]; ++j) {
+            r += counts[j];
+            b += lens[j];
+        }
+        rows_before[t + 1] = r;
+        bytes_before[t + 1] = b;
+    });
+    for (int t = 0; t < nt; ++t) {
+        rows_before[t + 1] += rows_before[t];
+        bytes_before[t + 1] += bytes_before[t];
+    }
+    if (bytes_before[nt] != nbytes) {
+        hx::set_last_error("hx_rows_decode: the stream holds %lld bytes, the lengths say %lld", (long long)nbytes,
+                           (long long)bytes_before[nt]);
+        return HX_ERR_VALUE;
+    }
+    std::atomic<int> bad{0};
+    run([&](int t) {
+        const int64_t j0 = jb[t], j1 = jb[t + 1];
+        if (j0 == j1) return;
+        const int64_t used = decode_columns(counts, bytes + bytes_before[t], j0, j1, col_lo, rows_out + rows_before[t]);
+        if (used != bytes_before[t + 1] - bytes_before[t]) bad.store(1);
+        int64_t acc = row_base + rows_before[t];
+        for (int64_t j = j0; j < j1; ++j) {
+            acc += counts[j];
+            col_ptr_out[j] = acc;
+        }
+    });
+    if (bad.load()) {
+        hx::set_last_error("hx_rows_decode: corrupt stream (byte lengths do not match the control bytes)");
+        return HX_ERR_VALUE;
+    }
+    return HX_OK;
+}
+
+namespace {
+
 }  // namespace
 
 extern "C" int hx_rows_widen(const int32_t *rows32, int64_t *row_idx, int64_t n, int32_t threads) {

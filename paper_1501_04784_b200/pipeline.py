@@ -285,6 +285,8 @@ UPLOAD_RANGES = 8
 UPLOAD_RANGES_MIN_ELEMENTS = 1 << 22
 # locally numbered meshes of at least STREAM_MIN_ELEMENTS elements take the streamed column-block
 # build (stream.py): STREAM_BLOCKS blocks, copies in both directions overlapping the kernels
+# transfer statistics of the last streamed run_build (d2h_bytes, row codec use, stage times)
+LAST_RUN_STATS: dict = {}
 STREAM_BLOCKS = 10
 STREAM_MIN_ELEMENTS = 1 << 22
 
@@ -360,6 +362,8 @@ def run_build(mesh, budget_bytes: int, workers: int = 1, mode: str = "sequential
 
         st: dict = {}
         matrix = stream.streamed_build(mesh, STREAM_BLOCKS, mode=integration, device=dev, stats=st)
+        LAST_RUN_STATS.clear()
+        LAST_RUN_STATS.update(st)
         if matrix is not None:
             return matrix, _report(mesh, matrix, plan, st["integration_s"], st["assembly_s"],
                                    time.perf_counter() - wall0, workers, mode, assembler)

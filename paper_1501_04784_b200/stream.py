@@ -34,7 +34,7 @@ from . import _native as N
 from . import device as D
 from .assemble import LowerCscMatrix
 from .errors import MeshValidationError, NodeIndexError
-from .transfer import copy_stream, host_threads
+from .transfer import RowEncoder, copy_stream, decode_rows, host_threads, row_codec_enabled
 
 __all__ = ["block_element_ranges", "StreamPlan", "plan", "streamed_build", "blocks_for_budget"]
 
@@ -157,6 +157,14 @@ def streamed_build(mesh, sp, mode: str = "exact", device=None, capacity: int | N
         out_cp = torch.empty(n_nodes + 1, dtype=torch.int64, pin_memory=True)
         out_rows = torch.empty(max(cap, 1), dtype=torch.int64, pin_memory=True)
         out_vals = torch.empty(max(cap, 1), dtype=torch.float64, pin_memory=True)
+        codec = row_codec_enabled()
+        if codec:  # delta-encoded rows (~2 bytes per row on local meshes) + per-column counts / lengths
+            encs = [RowEncoder(dev), RowEncoder(dev)]  # alternate: block k encodes while k-1 copies out
+            enc_done = [None, None]
+            counts_h = torch.empty(max(n_nodes, 1), dtype=torch.uint8, pin_memory=True)
+            lens_h = torch.empty(max(n_nodes, 1), dtype=torch.uint8, pin_memory=True)
+            bytes_h = torch.empty(3 * max(cap, 1) + 64, dtype=torch.uint8, pin_memory=True)
+            boff = 0
         rows32 = torch.empty(max(cap, 1), dtype=torch.int32, pin_memory=True)
         out_cp[0] = 0
         cp_np = out_cp.numpy()
@@ -177,6 +185,12 @@ def streamed_build(mesh, sp, mode: str = "exact", device=None, capacity: int | N
             coeff.record_stream(main)
             return conn, coeff, ev
 
+        def finish_codec(k, off, nnz, b0, nbytes, done):
+            done.synchronize()
+            a, z = int(sp.bounds[k]), int(sp.bounds[k + 1])
+            decode_rows(counts_h.numpy()[a:z], lens_h.numpy()[a:z], bytes_h.numpy()[b0:], nbytes, a, off,
+                        cp_np[a + 1:z + 1], out_rows.numpy()[off:off + nnz], threads)
+
         def finish(k, off, nnz, cp_stage, rows_landed, done):
             rows_landed.synchronize()
             if nnz:
@@ -196,6 +210,7 @@ def streamed_build(mesh, sp, mode: str = "exact", device=None, capacity: int | N
 
         fails, futures, stage_events = [], [], []
         offset = 0
+        d2h_bytes, coded_blocks = 0, 0
         t_gpu = [torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)]
         mark("start", main)
         main.wait_event(coords_ready)
@@ -230,6 +245,33 @@ def streamed_build(mesh, sp, mode: str = "exact", device=None, capacity: int | N
                 if offset + nnz > cap:
                     overflow = True
                     break
+                if codec:
+                    if enc_done[k & 1] is not None:  # block k-2's copies out of these buffers are done
+                        main.wait_event(enc_done[k & 1])
+                    counts_d, lens_d, bytes_d, total_d = encs[k & 1].encode(csc.col_ptr, csc.row_idx, a, stream=main)
+                    nbytes = D.peek(total_d, stream=main)[0]
+                    if 0 <= nbytes and boff + nbytes + 16 <= bytes_h.numel():
+                        d2h.wait_event(main.record_event())
+                        with torch.cuda.stream(d2h):
+                            mark(f"d2h {k} start", d2h)
+                            counts_h[a:z].copy_(counts_d, non_blocking=True)
+                            lens_h[a:z].copy_(lens_d, non_blocking=True)
+                            if nbytes:
+                                bytes_h[boff:boff + nbytes].copy_(bytes_d[:nbytes], non_blocking=True)
+                            if nnz:
+                                out_vals[offset:offset + nnz].copy_(csc.vals, non_blocking=True)
+                            done = d2h.record_event()
+                            mark(f"d2h {k} end", d2h)
+                        enc_done[k & 1] = done
+                        for t in (counts_d, lens_d, bytes_d, csc.vals):
+                            t.record_stream(d2h)
+                        futures.append(pool.submit(finish_codec, k, offset, nnz, boff, nbytes, done))
+                        d2h_bytes += 2 * (z - a) + nbytes + 8 * nnz
+                        coded_blocks += 1
+                        boff += nbytes
+                        offset += nnz
+                        del dm, ke, csc
+                        continue
                 narrow = D.rows_narrow(csc.row_idx, stream=main) if nnz else None
                 cp_stage = torch.empty(z - a + 1, dtype=torch.int64, pin_memory=True)
                 d2h.wait_event(main.record_event())
@@ -248,6 +290,7 @@ def streamed_build(mesh, sp, mode: str = "exact", device=None, capacity: int | N
                     if t is not None:
                         t.record_stream(d2h)
                 futures.append(pool.submit(finish, k, offset, nnz, cp_stage, rows_landed, done))
+                d2h_bytes += 8 * (z - a + 1) + 12 * nnz
                 offset += nnz
                 del dm, ke, csc, narrow
             t_gpu[1].record(main)
@@ -268,7 +311,9 @@ def streamed_build(mesh, sp, mode: str = "exact", device=None, capacity: int | N
             stats.update(gpu_s=t_gpu[0].elapsed_time(t_gpu[1]) / 1e3, wall_s=time.perf_counter() - t0, blocks=K,
                          integrated_elements=int((sp.e_hi - sp.e_lo).sum()),
                          integration_s=sum(e[0].elapsed_time(e[1]) for e in stage_events) / 1e3,
-                         assembly_s=sum(e[1].elapsed_time(e[2]) for e in stage_events) / 1e3)
+                         assembly_s=sum(e[1].elapsed_time(e[2]) for e in stage_events) / 1e3,
+                         d2h_bytes=d2h_bytes, h2d_bytes=coords_h.numel() * 8 + conn_h.numel() * 4 + coeff_h.numel() * 8,
+                         row_codec_blocks=coded_blocks)
     return LowerCscMatrix(col_ptr=cp_np, row_idx=out_rows.numpy()[:offset], vals=out_vals.numpy()[:offset],
                           dim=n_nodes)
 

@@ -26,7 +26,57 @@ from . import _native as N
 from . import device as D
 from .assemble import LowerCscMatrix
 
-__all__ = ["CscHostTransfer", "host_threads", "fetch_csc"]
+__all__ = ["CscHostTransfer", "host_threads", "fetch_csc", "RowEncoder", "decode_rows", "row_codec_enabled"]
+
+
+def row_codec_enabled() -> bool:
+    """Row indices cross PCIe delta-encoded (hx_rows_encode / hx_rows_decode) unless HX_ROW_CODEC=0
+    (then as int32, widened on the host)."""
+    return os.environ.get("HX_ROW_CODEC", "1") != "0"
+
+
+class RowEncoder:
+    """Device half of the row-index codec with reusable buffers: encode(col_ptr, row_idx, col_lo)
+    launches hx_rows_encode on ``stream`` and returns (counts u8, lens u8, stream bytes u8, total
+    int64 (1,)) device tensors; total is -1 when a column is outside the codec."""
+
+    def __init__(self, device=None):
+        self.dev = D.require_device(device)
+        self._bufs = {}
+
+    def _buf(self, name, n, dtype):
+        b = self._bufs.get(name)
+        if b is None or b.numel() < n:
+            b = self._bufs[name] = torch.empty(max(int(n * 1.05), 16), dtype=dtype, device=self.dev)
+        return b[:n]
+
+    def encode(self, col_ptr: torch.Tensor, row_idx: torch.Tensor, col_lo: int, stream=None):
+        ncols = col_ptr.shape[0] - 1
+        nnz = row_idx.shape[0]
+        counts = self._buf("counts", max(ncols, 1), torch.uint8)
+        lens = self._buf("lens", max(ncols, 1), torch.uint8)
+        cap = 5 * nnz + 17 * ncols
+        data = self._buf("bytes", max(cap, 1), torch.uint8)
+        total = self._buf("total", 1, torch.int64)
+        ws_bytes = N.lib().hx_rows_encode_workspace_bytes(ncols)
+        ws = self._buf("ws", max(ws_bytes, 1), torch.uint8)
+        N.check(N.lib().hx_rows_encode(D._ptr(col_ptr), D._ptr(row_idx), ncols, col_lo, D._ptr(counts), D._ptr(lens),
+                                       D._ptr(data), cap, D._ptr(total), D._ptr(ws), ws_bytes,
+                                       D.stream_handle(stream)), "hx_rows_encode")
+        return counts[:ncols], lens[:ncols], data, total
+
+
+def decode_rows(counts: np.ndarray, lens: np.ndarray, data: np.ndarray, nbytes: int, col_lo: int, row_base: int,
+                col_ptr_out: np.ndarray, rows_out: np.ndarray, threads: int) -> None:
+    """Host half (hx_rows_decode): int64 rows into rows_out and col_ptr ends (row_base + running
+    count) into col_ptr_out; ``data`` must hold 16 readable bytes past nbytes."""
+    ncols = counts.shape[0]
+    if ncols == 0:
+        return
+    N.check(N.lib().hx_rows_decode(counts.ctypes.data, lens.ctypes.data, data.ctypes.data, int(nbytes), ncols,
+                                   int(col_lo), int(row_base), col_ptr_out.ctypes.data,
+                                   rows_out.ctypes.data if rows_out.size else 0, int(threads)),
+            "hx_rows_decode")
 
 
 def host_threads() -> int:
@@ -38,10 +88,15 @@ def host_threads() -> int:
 
 
 class _Slot:
-    def __init__(self, n_cols: int, nnz: int):
+    def __init__(self, n_cols: int, nnz: int, codec: bool = False, device=None):
         self.col_ptr = torch.empty(n_cols + 1, dtype=torch.int64, pin_memory=True)
         self.vals = torch.empty(max(nnz, 1), dtype=torch.float64, pin_memory=True)
         self.rows32 = torch.empty(max(nnz, 1), dtype=torch.int32, pin_memory=True)
+        if codec:  # delta-encoded rows: per-column counts / lengths + the byte stream (16 B read slack)
+            self.enc = RowEncoder(device)
+            self.counts = torch.empty(max(n_cols, 1), dtype=torch.uint8, pin_memory=True)
+            self.lens = torch.empty(max(n_cols, 1), dtype=torch.uint8, pin_memory=True)
+            self.bytes = torch.empty(3 * max(nnz, 1) + 64, dtype=torch.uint8, pin_memory=True)
         self.row_idx = np.empty(max(nnz, 1), dtype=np.int64)
         self.row_idx.fill(0)  # fault the pages in now, not inside a timed transfer
         self.pending: Future | None = None
@@ -59,14 +114,19 @@ class CscHostTransfer:
         if threads is None:  # half the cores: the widening shares host memory bandwidth with the DMA
             threads = int(os.environ.get("HX_WIDEN_THREADS", "0")) or max(1, host_threads() // 2)
         self.threads = int(threads)
-        self.slots = [_Slot(self.n_cols, self.capacity) for _ in range(depth)]
+        self.codec = row_codec_enabled()
+        self.slots = [_Slot(self.n_cols, self.capacity, self.codec, self.dev) for _ in range(depth)]
+        self.last_bytes = None  # PCIe bytes of the last transfer
         self.copy = torch.cuda.Stream(device=self.dev)
         self.pool = ThreadPoolExecutor(max_workers=depth)
         self.k = 0
         self.trace = [] if os.environ.get("HX_TRACE_TRANSFER") else None
 
     def bytes_per_transfer(self, nnz: int) -> int:
-        """PCIe bytes of one transfer: col_ptr int64 + row indices int32 + values float64."""
+        """PCIe bytes of one transfer: the last transfer's when known (codec: counts + lengths + the
+        row stream + values), else col_ptr int64 + row indices int32 + values float64."""
+        if self.last_bytes is not None:
+            return self.last_bytes
         return 8 * (self.n_cols + 1) + 12 * nnz
 
     def submit(self, csc: D.DeviceCsc, stream=None) -> Future:
@@ -78,6 +138,10 @@ class CscHostTransfer:
         if slot.pending is not None:  # its previous result must be finished (widened) first
             slot.pending.result()
         producer = torch.cuda.current_stream(self.dev) if stream is None else stream
+        if self.codec:
+            fut = self._submit_codec(slot, csc, producer)
+            if fut is not None:
+                return fut
         rows32 = D.rows_narrow(csc.row_idx, stream=producer)
         ready = producer.record_event()
         self.copy.wait_event(ready)
@@ -108,6 +172,47 @@ class CscHostTransfer:
             return LowerCscMatrix(col_ptr=slot.col_ptr.numpy(), row_idx=slot.row_idx[:nnz],
                                   vals=slot.vals.numpy()[:nnz], dim=dim)
 
+        self.last_bytes = 8 * (self.n_cols + 1) + 12 * nnz
+        slot.pending = self.pool.submit(finish)
+        return slot.pending
+
+    def _submit_codec(self, slot, csc, producer):
+        """Delta-encoded rows (hx_rows_encode on the producer stream, one status read for the stream
+        length); None when a column is outside the codec or the stream outgrows the slot."""
+        nnz, n_cols = csc.nnz, self.n_cols
+        counts_d, lens_d, bytes_d, total_d = slot.enc.encode(csc.col_ptr, csc.row_idx, csc.col_lo, stream=producer)
+        nbytes = D.peek(total_d, stream=producer)[0]
+        if nbytes < 0 or nbytes + 16 > slot.bytes.numel():
+            return None
+        self.copy.wait_event(producer.record_event())
+        with torch.cuda.stream(self.copy):
+            started = self.copy.record_event(torch.cuda.Event(enable_timing=self.trace is not None))
+            slot.counts[:n_cols].copy_(counts_d, non_blocking=True)
+            slot.lens[:n_cols].copy_(lens_d, non_blocking=True)
+            if nbytes:
+                slot.bytes[:nbytes].copy_(bytes_d[:nbytes], non_blocking=True)
+            slot.vals[:nnz].copy_(csc.vals, non_blocking=True)
+            done = self.copy.record_event(torch.cuda.Event(enable_timing=self.trace is not None))
+            for t in (counts_d, lens_d, bytes_d, csc.vals):
+                t.record_stream(self.copy)
+        if csc.readers is not None:
+            csc.readers.append(done)
+        dim, threads, trace, k = csc.dim, self.threads, self.trace, self.k - 1
+        col_lo = csc.col_lo
+
+        def finish() -> LowerCscMatrix:
+            done.synchronize()
+            t0 = time.perf_counter()
+            slot.col_ptr[0] = 0
+            decode_rows(slot.counts.numpy()[:n_cols], slot.lens.numpy()[:n_cols], slot.bytes.numpy(), nbytes, col_lo,
+                        0, slot.col_ptr.numpy()[1:], slot.row_idx[:nnz], threads)
+            t1 = time.perf_counter()
+            if trace is not None:
+                trace.append((k, started.elapsed_time(done), (t1 - t0) * 1e3))
+            return LowerCscMatrix(col_ptr=slot.col_ptr.numpy(), row_idx=slot.row_idx[:nnz],
+                                  vals=slot.vals.numpy()[:nnz], dim=dim)
+
+        self.last_bytes = 2 * n_cols + nbytes + 8 * nnz
         slot.pending = self.pool.submit(finish)
         return slot.pending
 

@@ -86,3 +86,86 @@ def test_rows_widen_host_threads():
         N.check(N.lib().hx_rows_widen(a.ctypes.data, b.ctypes.data, a.size, threads), "widen")
         assert np.array_equal(b, a.astype(np.int64))
     N.check(N.lib().hx_rows_widen(None, None, 0, 0), "widen empty")
+
+
+# ---- row-index codec (hx_rows_encode / hx_rows_decode): the format's executable spec -------------
+def encode_rows_ref(col_ptr, rows, col_lo):
+    """Per column: deltas d_0 = r_0 - c, d_i = r_i - r_(i-1), padded with zeros to a multiple of 4;
+    per group of 4 one control byte (2 bits per delta: byte length - 1), all control bytes first,
+    then the deltas' little-endian bytes.  Returns (counts u8, lens u8, stream bytes)."""
+    import numpy as np
+
+    counts, lens, out = [], [], bytearray()
+    for j in range(len(col_ptr) - 1):
+        r = [int(x) for x in rows[col_ptr[j]:col_ptr[j + 1]]]
+        prev, deltas = col_lo + j, []
+        for x in r:
+            deltas.append(x - prev)
+            prev = x
+        deltas += [0] * ((4 - len(deltas) % 4) % 4)
+        ctrl, data = bytearray(), bytearray()
+        for g in range(len(deltas) // 4):
+            c = 0
+            for k in range(4):
+                d = deltas[4 * g + k]
+                nb = 1 if d < 1 << 8 else 2 if d < 1 << 16 else 3 if d < 1 << 24 else 4
+                c |= (nb - 1) << (2 * k)
+                data += d.to_bytes(nb, "little")
+            ctrl.append(c)
+        counts.append(len(r))
+        lens.append(len(ctrl) + len(data))
+        out += ctrl + data
+    return np.array(counts, np.uint8), np.array(lens, np.uint8), np.frombuffer(bytes(out), np.uint8)
+
+
+def _codec_case(seed, ncols, col_lo):
+    import numpy as np
+
+    rng = np.random.default_rng(seed)
+    counts = rng.integers(0, 34, ncols)
+    counts[rng.random(ncols) < 0.1] = 0
+    cp = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+    rows = []
+    for j, m in enumerate(counts):
+        c = col_lo + j
+        if m == 0:
+            continue
+        gaps = rng.choice([1, 2, 399, 401, 160_801, 2**20 + 3, 2**27], size=m - 1)
+        col = np.concatenate([[c], c + np.cumsum(gaps)])
+        rows.append(np.minimum(col, 2**31 - 1 - (m - 1 - np.arange(m))))  # stay below 2^31, ascending
+    rows = np.concatenate(rows).astype(np.int64) if rows else np.empty(0, np.int64)
+    return cp, rows
+
+
+@pytest.mark.parametrize("seed,ncols,col_lo,threads", [(1, 1, 0, 1), (2, 7, 5, 1), (3, 5000, 1234, 4),
+                                                        (4, 70000, 10, 0), (5, 3, 2**30, 2)])
+def test_row_codec_host_decoder_matches_format(seed, ncols, col_lo, threads):
+    """hx_rows_decode (host C++, SSSE3) inverts the reference encoding of the format, any thread
+    count, empty / single-row columns and deltas up to 2^27; col_ptr ends are offset by row_base."""
+    import numpy as np
+
+    from paper_1501_04784_b200.transfer import decode_rows
+
+    cp, rows = _codec_case(seed, ncols, col_lo)
+    counts, lens, data = encode_rows_ref(cp, rows, col_lo)
+    buf = np.zeros(data.size + 16, np.uint8)
+    buf[:data.size] = data
+    out = np.full(rows.size + 4, -7, np.int64)
+    ends = np.zeros(ncols, np.int64)
+    decode_rows(counts, lens, buf, data.size, col_lo, 1000, ends, out, threads)
+    assert np.array_equal(out[:rows.size], rows) and np.all(out[rows.size:] == -7)
+    assert np.array_equal(ends, 1000 + cp[1:])
+
+
+def test_row_codec_rejects_inconsistent_stream():
+    import numpy as np
+
+    from paper_1501_04784_b200.errors import ConfigurationError
+    from paper_1501_04784_b200.transfer import decode_rows
+
+    cp, rows = _codec_case(9, 100, 0)
+    counts, lens, data = encode_rows_ref(cp, rows, 0)
+    buf = np.zeros(data.size + 16, np.uint8)
+    buf[:data.size] = data
+    with pytest.raises((ValueError, ConfigurationError)):
+        decode_rows(counts, lens, buf, data.size - 1, 0, 0, np.zeros(100, np.int64), np.zeros(rows.size + 4, np.int64), 1)

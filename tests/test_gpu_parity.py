@@ -1135,3 +1135,50 @@ def test_integrate_emit_errors(monkeypatch):
     with pytest.raises(NodeIndexError) as ei:
         build_device(D.DeviceMesh.from_host(Mesh(mesh.coords, np.ascontiguousarray(conn), mesh.coefficient)))
     assert ei.value.element_id == 150
+
+
+@pytest.mark.parametrize("name", ["structured", "permuted"])
+def test_row_codec_device_encoder_matches_format(name):
+    """hx_rows_encode produces exactly the format's reference bytes (tests/test_abi_cpu.py), and the
+    host decoder restores row_idx / col_ptr of a real build bit for bit, also on a column block."""
+    from test_abi_cpu import encode_rows_ref
+
+    from paper_1501_04784_b200.transfer import RowEncoder, decode_rows
+
+    mesh = perturbed_mesh(12, seed=61) if name == "structured" else permuted_mesh(perturbed_mesh(12, seed=61), seed=62)
+    b = build_device(D.DeviceMesh.from_host(mesh))
+    cp, ri = b.csc.col_ptr.cpu().numpy(), b.csc.row_idx.cpu().numpy()
+    enc = RowEncoder()
+    for lo, hi in ((0, mesh.n_nodes), (100, 1500)):
+        sub_cp = torch.from_numpy(cp[lo:hi + 1] - cp[lo]).cuda()
+        sub_ri = torch.from_numpy(ri[cp[lo]:cp[hi]]).cuda()
+        counts, lens, data, total = enc.encode(sub_cp, sub_ri, lo)
+        nbytes = int(total.item())
+        c_ref, l_ref, d_ref = encode_rows_ref(cp[lo:hi + 1] - cp[lo], ri[cp[lo]:cp[hi]], lo)
+        assert np.array_equal(counts.cpu().numpy(), c_ref) and np.array_equal(lens.cpu().numpy(), l_ref)
+        assert nbytes == d_ref.size and np.array_equal(data[:nbytes].cpu().numpy(), d_ref)
+        buf = np.zeros(nbytes + 16, np.uint8)
+        buf[:nbytes] = d_ref
+        out = np.empty(cp[hi] - cp[lo] + 4, np.int64)
+        ends = np.empty(hi - lo, np.int64)
+        decode_rows(c_ref, l_ref, buf, nbytes, lo, 0, ends, out, 3)
+        assert np.array_equal(out[:cp[hi] - cp[lo]], ri[cp[lo]:cp[hi]]) and np.array_equal(ends, cp[lo + 1:hi + 1] - cp[lo])
+
+
+@pytest.mark.parametrize("codec", ["0", "1"])
+def test_host_transfer_codec_round_trip(monkeypatch, codec):
+    """CscHostTransfer with and without the row codec: the host LowerCscMatrix equals the device CSC
+    (and the oracle), several submissions through the pipelined slots."""
+    from paper_1501_04784_b200.transfer import CscHostTransfer
+
+    monkeypatch.setenv("HX_ROW_CODEC", codec)
+    mesh = permuted_mesh(perturbed_mesh(14, seed=71), seed=72)
+    dm = D.DeviceMesh.from_host(mesh)
+    _, _, _, (cp, ri, vv) = _oracle_build(mesh)
+    xfer = CscHostTransfer(mesh.n_nodes, len(ri), depth=2)
+    futs = [xfer.submit(build_device(dm).csc) for _ in range(3)]
+    for f in futs[-2:]:
+        m = f.result()
+        assert bits_equal(m.col_ptr, cp) and bits_equal(m.row_idx, ri) and bits_equal(m.vals, vv)
+    assert (xfer.bytes_per_transfer(len(ri)) < 8 * (mesh.n_nodes + 1) + 12 * len(ri)) == (codec == "1")
+    xfer.close()
