@@ -64,18 +64,17 @@ const CodecTables &codec_tables() {
     return t;
 }
 
-// Columns [j0, j1) of a block: rows_out / bytes at this range's first row / byte.  Every group but
-// the range's very last one is decoded 4 rows at a time (the 0..3 rows past a column's end are
-// rewritten by the next column); the range's last group is written exactly (no race with the next
-// range).  Returns the bytes consumed.
+// Columns [j0, j1) of a block: rows_out / bytes at this range's first row / byte, rows_end = one
+// past the range's last row.  A group is stored 4 rows at once (the 0..3 rows past a column's end
+// are rewritten by the next column) unless those 4 would pass rows_end -- then exactly (no write
+// outside the range: no race with the next range, no overrun of the array).  Returns the bytes
+// consumed.
 __attribute__((target("ssse3,sse4.1"))) int64_t decode_columns(const uint8_t *counts, const uint8_t *bytes,
                                                                  int64_t j0, int64_t j1, int64_t col_lo,
-                                                                 int64_t *rows_out) {
+                                                                 int64_t *rows_out, const int64_t *rows_end) {
     const CodecTables &T = codec_tables();
     const uint8_t *p = bytes;
     int64_t *out = rows_out;
-    int64_t j_end = j1 - 1;  // the range's last non-empty column writes its final group exactly
-    while (j_end > j0 && counts[j_end] == 0) --j_end;
     for (int64_t j = j0; j < j1; ++j) {
         const int m = counts[j];
         const int groups = (m + 3) >> 2;
@@ -89,14 +88,14 @@ __attribute__((target("ssse3,sse4.1"))) int64_t decode_columns(const uint8_t *co
             v = _mm_add_epi32(v, _mm_slli_si128(v, 4));
             v = _mm_add_epi32(v, _mm_slli_si128(v, 8));
             v = _mm_add_epi32(v, base);
-            const bool tail = j == j_end && g == groups - 1;
+            const bool tail = out + 4 * g + 4 > rows_end;
             if (!tail) {
                 _mm_storeu_si128(reinterpret_cast<__m128i *>(out + 4 * g), _mm_cvtepu32_epi64(v));
                 _mm_storeu_si128(reinterpret_cast<__m128i *>(out + 4 * g + 2), _mm_cvtepu32_epi64(_mm_srli_si128(v, 8)));
             } else {
                 alignas(16) uint32_t x[4];
                 _mm_store_si128(reinterpret_cast<__m128i *>(x), v);
-                for (int k = 0; k < m - 4 * g; ++k) out[4 * g + k] = (int64_t)x[k];
+                for (int k = 0; k < 4 && 4 * g + k < m; ++k) out[4 * g + k] = (int64_t)x[k];
             }
             base = _mm_shuffle_epi32(v, 0xFF);
             data += T.len[c];
@@ -159,7 +158,8 @@ extern "C" int hx_rows_decode(const uint8_t *counts, const uint8_t *lens, const 
     run([&](int t) {
         const int64_t j0 = jb[t], j1 = jb[t + 1];
         if (j0 == j1) return;
-        const int64_t used = decode_columns(counts, bytes + bytes_before[t], j0, j1, col_lo, rows_out + rows_before[t]);
+        const int64_t used = decode_columns(counts, bytes + bytes_before[t], j0, j1, col_lo, rows_out + rows_before[t],
+                                            rows_out + rows_before[t + 1]);
         if (used != bytes_before[t + 1] - bytes_before[t]) bad.store(1);
         int64_t acc = row_base + rows_before[t];
         for (int64_t j = j0; j < j1; ++j) {
