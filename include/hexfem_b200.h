@@ -300,6 +300,11 @@ int hx_block_gather(const int32_t *conn, const double *coeff, const int64_t *ids
  *         (n_el, 8) int32 HOST array, `threads` workers (<= 0: all). */
 int hx_block_ranges(const int32_t *conn, int64_t n_el, const int64_t *bounds, int32_t n_blocks, int64_t *e_lo,
                     int64_t *e_hi, int32_t threads);
+/* as hx_block_ranges, plus node_lo / node_hi (n_blocks each): a node range [node_lo, node_hi) that
+ * holds every node the elements [e_lo[k], e_hi[k]) reference (bounded per chunk of 2^20 elements;
+ * the streamed build uploads the coordinates as prefixes ahead of each block).  HOST code. */
+int hx_block_ranges_nodes(const int32_t *conn, int64_t n_el, const int64_t *bounds, int32_t n_blocks, int64_t *e_lo,
+                          int64_t *e_hi, int64_t *node_lo, int64_t *node_hi, int32_t threads);
 
 /* ---- structured box in device memory (mesh.py:73-98 generate_cube_mesh) --------------------------
  * coords (n_nodes, 3) f64, conn (n_el, 8) i32, coeff (n_el,) f64: node (i,j,k) at (i h, j h, k h)

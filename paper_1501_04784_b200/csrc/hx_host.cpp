@@ -212,10 +212,20 @@ extern "C" int hx_rows_widen(const int32_t *rows32, int64_t *row_idx, int64_t n,
 // covers k (a superset of the elements touching k -- extra elements contribute nothing to the
 // block).  Ids outside [0, n_nodes) clamp to the first / last block (the integration kernel reports
 // them).  Empty blocks get e_lo = e_hi = 0.  Host code, `threads` workers over element chunks.
+extern "C" int hx_block_ranges_nodes(const int32_t *conn, int64_t n_el, const int64_t *bounds, int32_t n_blocks,
+                                     int64_t *e_lo, int64_t *e_hi, int64_t *node_lo, int64_t *node_hi,
+                                     int32_t threads);
+
 extern "C" int hx_block_ranges(const int32_t *conn, int64_t n_el, const int64_t *bounds, int32_t n_blocks,
                                int64_t *e_lo, int64_t *e_hi, int32_t threads) {
+    return hx_block_ranges_nodes(conn, n_el, bounds, n_blocks, e_lo, e_hi, nullptr, nullptr, threads);
+}
+
+extern "C" int hx_block_ranges_nodes(const int32_t *conn, int64_t n_el, const int64_t *bounds, int32_t n_blocks,
+                                     int64_t *e_lo, int64_t *e_hi, int64_t *node_lo, int64_t *node_hi,
+                                     int32_t threads) {
     if (n_el < 0 || n_blocks < 1 || bounds == nullptr || e_lo == nullptr || e_hi == nullptr ||
-        (n_el > 0 && conn == nullptr)) {
+        (n_el > 0 && conn == nullptr) || ((node_lo == nullptr) != (node_hi == nullptr))) {
         hx::set_last_error("hx_block_ranges: bad arguments");
         return HX_ERR_VALUE;
     }
@@ -229,7 +239,13 @@ extern "C" int hx_block_ranges(const int32_t *conn, int64_t n_el, const int64_t 
     const int64_t per = int64_t(1) << 20;
     const int64_t chunks = (n_el + per - 1) / per;
     const int nt = (int)std::max<int64_t>(1, std::min<int64_t>(threads > 0 ? threads : hw, chunks));
-    std::vector<std::vector<int64_t>> lo(nt), hi(nt);
+    struct Acc {
+        std::vector<int64_t> L, H;
+    };
+    std::vector<Acc> acc(nt);
+    // per element chunk: its smallest / largest node (the node range of a block's element range is
+    // bounded by the chunks it overlaps -- a superset of what the block gathers)
+    std::vector<int64_t> cmin(chunks, INT64_MAX), cmax(chunks, INT64_MIN);
     std::atomic<int64_t> next{0};
     auto work = [&](int t) {
         // thread-local accumulators (the per-element updates must not share cache lines)
@@ -237,6 +253,11 @@ extern "C" int hx_block_ranges(const int32_t *conn, int64_t n_el, const int64_t 
         int64_t *L = Lv.data(), *H = Hv.data();
         for (int64_t c = next.fetch_add(1); c < chunks; c = next.fetch_add(1)) {
             const int64_t a = c * per, z = std::min(n_el, a + per);
+            // consecutive elements of a locally numbered mesh stay in one block span: cache the last
+            // element's block bounds and binary-search only when a node leaves them
+            int b0 = 0, b1 = 0;
+            int64_t lo0 = INT64_MAX, hi0 = INT64_MIN, lo1 = INT64_MAX, hi1 = INT64_MIN;
+            int32_t chunk_min = INT32_MAX, chunk_max = INT32_MIN;
             for (int64_t e = a; e < z; ++e) {
                 const int32_t *g = conn + 8 * e;
                 int32_t mn = g[0], mx = g[0];
@@ -244,15 +265,27 @@ extern "C" int hx_block_ranges(const int32_t *conn, int64_t n_el, const int64_t 
                     mn = std::min(mn, g[k]);
                     mx = std::max(mx, g[k]);
                 }
-                const int b0 = block_of(mn), b1 = block_of(mx);
+                chunk_min = std::min(chunk_min, mn);
+                chunk_max = std::max(chunk_max, mx);
+                if (mn < lo0 || mn >= hi0) {
+                    b0 = block_of(mn);
+                    lo0 = b0 == 0 ? INT64_MIN : bounds[b0];
+                    hi0 = b0 == K - 1 ? INT64_MAX : bounds[b0 + 1];
+                }
+                if (mx < lo1 || mx >= hi1) {
+                    b1 = block_of(mx);
+                    lo1 = b1 == 0 ? INT64_MIN : bounds[b1];
+                    hi1 = b1 == K - 1 ? INT64_MAX : bounds[b1 + 1];
+                }
                 for (int b = b0; b <= b1; ++b) {
-                    L[b] = std::min(L[b], e);
-                    H[b] = std::max(H[b], e + 1);
+                    if (L[b] == INT64_MAX) L[b] = e;  // elements of a chunk come in ascending order
+                    H[b] = e + 1;
                 }
             }
+            cmin[c] = chunk_min;
+            cmax[c] = chunk_max;
         }
-        lo[t] = std::move(Lv);
-        hi[t] = std::move(Hv);
+        acc[t] = Acc{std::move(Lv), std::move(Hv)};
     };
     std::vector<std::thread> pool;
     for (int t = 1; t < nt; ++t) pool.emplace_back(work, t);
@@ -261,11 +294,20 @@ extern "C" int hx_block_ranges(const int32_t *conn, int64_t n_el, const int64_t 
     for (int b = 0; b < K; ++b) {
         int64_t l = INT64_MAX, h = 0;
         for (int t = 0; t < nt; ++t) {
-            l = std::min(l, lo[t][b]);
-            h = std::max(h, hi[t][b]);
+            l = std::min(l, acc[t].L[b]);
+            h = std::max(h, acc[t].H[b]);
         }
         e_lo[b] = h > 0 ? l : 0;
         e_hi[b] = h;
+        if (node_lo != nullptr) {  // nodes the block's element range may gather: [node_lo, node_hi)
+            int64_t nl = INT64_MAX, nh = INT64_MIN;
+            for (int64_t c = h > 0 ? e_lo[b] / per : 0; h > 0 && c <= (h - 1) / per; ++c) {
+                nl = std::min(nl, cmin[c]);
+                nh = std::max(nh, cmax[c]);
+            }
+            node_lo[b] = h > 0 ? std::max<int64_t>(nl, 0) : 0;
+            node_hi[b] = h > 0 ? nh + 1 : 0;
+        }
     }
     return HX_OK;
 }

@@ -47,17 +47,19 @@ def block_element_ranges(conn: np.ndarray, bounds: np.ndarray, threads: int | No
     conn = np.ascontiguousarray(conn, dtype=np.int32)
     bounds = np.ascontiguousarray(bounds, dtype=np.int64)
     k = bounds.shape[0] - 1
-    e_lo = np.zeros(k, dtype=np.int64)
-    e_hi = np.zeros(k, dtype=np.int64)
-    N.check(N.lib().hx_block_ranges(conn.ctypes.data, conn.shape[0], bounds.ctypes.data, k, e_lo.ctypes.data,
-                                    e_hi.ctypes.data, host_threads() if threads is None else int(threads)),
-            "hx_block_ranges")
-    return e_lo, e_hi
+    e_lo, e_hi, n_lo, n_hi = (np.zeros(k, dtype=np.int64) for _ in range(4))
+    N.check(N.lib().hx_block_ranges_nodes(conn.ctypes.data, conn.shape[0], bounds.ctypes.data, k, e_lo.ctypes.data,
+                                          e_hi.ctypes.data, n_lo.ctypes.data, n_hi.ctypes.data,
+                                          host_threads() if threads is None else int(threads)),
+            "hx_block_ranges_nodes")
+    return e_lo, e_hi, n_lo, n_hi
 
 
 class StreamPlan:
-    def __init__(self, bounds, e_lo, e_hi):
+    def __init__(self, bounds, e_lo, e_hi, node_hi=None):
         self.bounds, self.e_lo, self.e_hi = bounds, e_lo, e_hi
+        # coordinates block k's element range may gather lie below node_hi[k] (prefix uploads)
+        self.node_hi = node_hi
 
     @property
     def n_blocks(self) -> int:
@@ -100,10 +102,10 @@ def plan(mesh, n_blocks: int, threads: int | None = None) -> StreamPlan | None:
     if not looks_local(mesh.connectivity, n_nodes):
         return None
     bounds = stream_bounds(n_nodes, n_blocks)
-    e_lo, e_hi = block_element_ranges(mesh.connectivity, bounds, threads)
+    e_lo, e_hi, _, n_hi = block_element_ranges(mesh.connectivity, bounds, threads)
     if n_el and (e_hi - e_lo).sum() > MAX_RANGE_OVERLAP * n_el + n_blocks:
         return None
-    return StreamPlan(bounds, e_lo, e_hi)
+    return StreamPlan(bounds, e_lo, e_hi, np.maximum.accumulate(np.minimum(n_hi, n_nodes)))
 
 
 def blocks_for_budget(n_el: int, n_nodes: int, budget_bytes: int) -> int:
@@ -146,14 +148,16 @@ def streamed_build(mesh, sp, mode: str = "exact", device=None, capacity: int | N
         # kernel still reads it
         with torch.cuda.stream(h2d):
             coords = torch.empty(tuple(coords_h.shape), dtype=torch.float64, device=dev)
-            coords.copy_(coords_h, non_blocking=True)
-            coords_ready = h2d.record_event()
         coords.record_stream(main)
-        if not isinstance(sp, StreamPlan):  # host scan while the coordinates cross PCIe
+        if not isinstance(sp, StreamPlan):  # host scan (element and node ranges of the blocks)
             sp = plan(mesh, int(sp))
             if sp is None:
                 return None
         K = sp.n_blocks
+        # the coordinates go up as prefixes just ahead of the blocks that gather them (block 0 starts
+        # after its slice instead of after the whole array)
+        node_hi = sp.node_hi if sp.node_hi is not None else np.full(K, n_nodes, dtype=np.int64)
+        coords_up = [0]
         out_cp = torch.empty(n_nodes + 1, dtype=torch.int64, pin_memory=True)
         out_rows = torch.empty(max(cap, 1), dtype=torch.int64, pin_memory=True)
         out_vals = torch.empty(max(cap, 1), dtype=torch.float64, pin_memory=True)
@@ -168,7 +172,10 @@ def streamed_build(mesh, sp, mode: str = "exact", device=None, capacity: int | N
         rows32 = torch.empty(max(cap, 1), dtype=torch.int32, pin_memory=True)
         out_cp[0] = 0
         cp_np = out_cp.numpy()
-        threads = max(1, host_threads() // 2)
+        # host workers of the row decode / widening: half the cores while copies stream in (they share
+        # host memory bandwidth with the DMA), HX_DECODE_THREADS to override
+        threads = int(os.environ.get("HX_DECODE_THREADS", "0")) or max(1, host_threads() // 2)
+        tail_threads = max(threads, host_threads())  # the last blocks' decode has the host to itself
         pool = ThreadPoolExecutor(max_workers=1)
 
         def upload(k):
@@ -177,6 +184,10 @@ def streamed_build(mesh, sp, mode: str = "exact", device=None, capacity: int | N
                 conn = torch.empty((hi - lo, 8), dtype=torch.int32, device=dev)
                 coeff = torch.empty(hi - lo, dtype=torch.float64, device=dev)
                 mark(f"h2d {k} start", h2d)
+                top = int(min(max(node_hi[k], coords_up[0]), n_nodes)) if k < K - 1 else n_nodes
+                if top > coords_up[0]:
+                    coords[coords_up[0]:top].copy_(coords_h[coords_up[0]:top], non_blocking=True)
+                    coords_up[0] = top
                 conn.copy_(conn_h[lo:hi], non_blocking=True)
                 coeff.copy_(coeff_h[lo:hi], non_blocking=True)
                 ev = h2d.record_event()
@@ -189,7 +200,7 @@ def streamed_build(mesh, sp, mode: str = "exact", device=None, capacity: int | N
             done.synchronize()
             a, z = int(sp.bounds[k]), int(sp.bounds[k + 1])
             decode_rows(counts_h.numpy()[a:z], lens_h.numpy()[a:z], bytes_h.numpy()[b0:], nbytes, a, off,
-                        cp_np[a + 1:z + 1], out_rows.numpy()[off:off + nnz], threads)
+                        cp_np[a + 1:z + 1], out_rows.numpy()[off:off + nnz], tail_threads if k >= K - 2 else threads)
 
         def finish(k, off, nnz, cp_stage, rows_landed, done):
             rows_landed.synchronize()
@@ -213,9 +224,7 @@ def streamed_build(mesh, sp, mode: str = "exact", device=None, capacity: int | N
         d2h_bytes, coded_blocks = 0, 0
         t_gpu = [torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)]
         mark("start", main)
-        main.wait_event(coords_ready)
         t_gpu[0].record(main)
-        mark("coords landed", main)
         pending = upload(0) if K else None
         overflow = False
         try:

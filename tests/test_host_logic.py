@@ -106,13 +106,16 @@ def test_block_ranges_host_scan_matches_numpy():
         conn[11, 0] = -4
         for k in (1, 3, 8, 50):
             bounds = column_bounds(mesh.n_nodes, k)
-            lo, hi = block_element_ranges(conn, bounds, threads=3)
+            lo, hi, n_lo, n_hi = block_element_ranges(conn, bounds, threads=3)
             bmin = np.clip(np.searchsorted(bounds, conn.min(axis=1), side="right") - 1, 0, k - 1)
             bmax = np.clip(np.searchsorted(bounds, conn.max(axis=1), side="right") - 1, 0, k - 1)
             for b in range(k):
                 cover = np.flatnonzero((bmin <= b) & (bmax >= b))
                 want = (cover.min(), cover.max() + 1) if cover.size else (0, 0)
                 assert (lo[b], hi[b]) == want
+                if hi[b] > lo[b]:  # the node range covers every node the element range gathers
+                    sub = conn[lo[b]:hi[b]]
+                    assert n_lo[b] <= max(sub.min(), 0) and n_hi[b] >= sub.max() + 1
 
 
 def test_stream_bounds_quarter_end_blocks():
