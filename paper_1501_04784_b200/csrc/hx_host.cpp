@@ -64,23 +64,45 @@ const CodecTables &codec_tables() {
     return t;
 }
 
-// Columns [j0, j1) of a block: rows_out / bytes at this range's first row / byte, rows_end = one
-// past the range's last row.  A group is stored 4 rows at once (the 0..3 rows past a column's end
-// are rewritten by the next column) unless those 4 would pass rows_end -- then exactly (no write
-// outside the range: no race with the next range, no overrun of the array).  Returns the bytes
-// consumed.
+// Columns [j0, j1) of a block: rows_out / bytes at this range's first row / byte.  Groups decode 4
+// rows at a time into a cache-resident staging buffer (the 0..3 rows past a column's end are
+// rewritten by the next column), which is flushed to rows_out with non-temporal stores: the int64
+// rows are the host's largest write, and regular stores would first read every destination line
+// (read-for-ownership), doubling the memory traffic the decode shares with the incoming DMA.
+// Returns the bytes consumed.
+__attribute__((target("sse2"))) void stream_out(int64_t *dst, const int64_t *src, int64_t n) {
+    if (n > 0 && (reinterpret_cast<uintptr_t>(dst) & 15)) {
+        _mm_stream_si64(reinterpret_cast<long long *>(dst), src[0]);
+        ++dst;
+        ++src;
+        --n;
+    }
+    for (; n >= 2; n -= 2, dst += 2, src += 2)
+        _mm_stream_si128(reinterpret_cast<__m128i *>(dst), _mm_loadu_si128(reinterpret_cast<const __m128i *>(src)));
+    if (n > 0) _mm_stream_si64(reinterpret_cast<long long *>(dst), src[0]);
+}
+
 __attribute__((target("ssse3,sse4.1"))) int64_t decode_columns(const uint8_t *counts, const uint8_t *bytes,
                                                                  int64_t j0, int64_t j1, int64_t col_lo,
-                                                                 int64_t *rows_out, const int64_t *rows_end) {
+                                                                 int64_t *rows_out) {
     const CodecTables &T = codec_tables();
+    constexpr int STAGE = 2048;
+    alignas(64) int64_t stage[STAGE + 8];
+    int pos = 0;
     const uint8_t *p = bytes;
     int64_t *out = rows_out;
     for (int64_t j = j0; j < j1; ++j) {
         const int m = counts[j];
+        if (pos + m + 4 > STAGE) {
+            stream_out(out, stage, pos);
+            out += pos;
+            pos = 0;
+        }
         const int groups = (m + 3) >> 2;
         const uint8_t *ctrl = p;
         const uint8_t *data = p + groups;
         __m128i base = _mm_set1_epi32((int)(uint32_t)(col_lo + j));
+        int64_t *st = stage + pos;
         for (int g = 0; g < groups; ++g) {
             const uint8_t c = ctrl[g];
             __m128i v = _mm_shuffle_epi8(_mm_loadu_si128(reinterpret_cast<const __m128i *>(data)),
@@ -88,21 +110,16 @@ __attribute__((target("ssse3,sse4.1"))) int64_t decode_columns(const uint8_t *co
             v = _mm_add_epi32(v, _mm_slli_si128(v, 4));
             v = _mm_add_epi32(v, _mm_slli_si128(v, 8));
             v = _mm_add_epi32(v, base);
-            const bool tail = out + 4 * g + 4 > rows_end;
-            if (!tail) {
-                _mm_storeu_si128(reinterpret_cast<__m128i *>(out + 4 * g), _mm_cvtepu32_epi64(v));
-                _mm_storeu_si128(reinterpret_cast<__m128i *>(out + 4 * g + 2), _mm_cvtepu32_epi64(_mm_srli_si128(v, 8)));
-            } else {
-                alignas(16) uint32_t x[4];
-                _mm_store_si128(reinterpret_cast<__m128i *>(x), v);
-                for (int k = 0; k < 4 && 4 * g + k < m; ++k) out[4 * g + k] = (int64_t)x[k];
-            }
+            _mm_storeu_si128(reinterpret_cast<__m128i *>(st + 4 * g), _mm_cvtepu32_epi64(v));
+            _mm_storeu_si128(reinterpret_cast<__m128i *>(st + 4 * g + 2), _mm_cvtepu32_epi64(_mm_srli_si128(v, 8)));
             base = _mm_shuffle_epi32(v, 0xFF);
             data += T.len[c];
         }
-        out += m;
+        pos += m;
         p = data;
     }
+    stream_out(out, stage, pos);
+    _mm_sfence();
     return p - bytes;
 }
 
@@ -158,8 +175,7 @@ extern "C" int hx_rows_decode(const uint8_t *counts, const uint8_t *lens, const 
     run([&](int t) {
         const int64_t j0 = jb[t], j1 = jb[t + 1];
         if (j0 == j1) return;
-        const int64_t used = decode_columns(counts, bytes + bytes_before[t], j0, j1, col_lo, rows_out + rows_before[t],
-                                            rows_out + rows_before[t + 1]);
+        const int64_t used = decode_columns(counts, bytes + bytes_before[t], j0, j1, col_lo, rows_out + rows_before[t]);
         if (used != bytes_before[t + 1] - bytes_before[t]) bad.store(1);
         int64_t acc = row_base + rows_before[t];
         for (int64_t j = j0; j < j1; ++j) {

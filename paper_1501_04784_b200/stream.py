@@ -154,6 +154,7 @@ def streamed_build(mesh, sp, mode: str = "exact", device=None, capacity: int | N
             if sp is None:
                 return None
         K = sp.n_blocks
+        t_plan = time.perf_counter()
         # the coordinates go up as prefixes just ahead of the blocks that gather them (block 0 starts
         # after its slice instead of after the whole array)
         node_hi = sp.node_hi if sp.node_hi is not None else np.full(K, n_nodes, dtype=np.int64)
@@ -198,9 +199,13 @@ def streamed_build(mesh, sp, mode: str = "exact", device=None, capacity: int | N
 
         def finish_codec(k, off, nnz, b0, nbytes, done):
             done.synchronize()
+            td = time.perf_counter()
             a, z = int(sp.bounds[k]), int(sp.bounds[k + 1])
             decode_rows(counts_h.numpy()[a:z], lens_h.numpy()[a:z], bytes_h.numpy()[b0:], nbytes, a, off,
                         cp_np[a + 1:z + 1], out_rows.numpy()[off:off + nnz], tail_threads if k >= K - 2 else threads)
+            if trace is not None:
+                trace.append((f"decode {k} {nnz / 1e6:.0f}M rows {1e3 * (time.perf_counter() - td):.1f} ms", None,
+                              time.perf_counter()))
 
         def finish(k, off, nnz, cp_stage, rows_landed, done):
             rows_landed.synchronize()
@@ -224,6 +229,9 @@ def streamed_build(mesh, sp, mode: str = "exact", device=None, capacity: int | N
         d2h_bytes, coded_blocks = 0, 0
         t_gpu = [torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)]
         mark("start", main)
+        if trace is not None:
+            print(f"  plan done at host {1e3 * (t_plan - t0):.2f} ms, buffers at {1e3 * (time.perf_counter() - t0):.2f} ms",
+                  flush=True)
         t_gpu[0].record(main)
         pending = upload(0) if K else None
         overflow = False
@@ -309,7 +317,8 @@ def streamed_build(mesh, sp, mode: str = "exact", device=None, capacity: int | N
             if trace:
                 z = trace[0][1]
                 for name, e, th in trace:
-                    print(f"  {name:24s} gpu {z.elapsed_time(e):8.2f} ms   host {1e3 * (th - t0):8.2f} ms", flush=True)
+                    g = f"{z.elapsed_time(e):8.2f}" if e is not None else "       -"
+                    print(f"  {name:24s} gpu {g} ms   host {1e3 * (th - t0):8.2f} ms", flush=True)
                 print(f"  total host {1e3 * (time.perf_counter() - t0):.2f} ms", flush=True)
         finally:
             pool.shutdown(wait=True)
