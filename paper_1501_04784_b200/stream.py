@@ -197,8 +197,8 @@ def streamed_build(mesh, sp, mode: str = "exact", device=None, capacity: int | N
             coeff.record_stream(main)
             return conn, coeff, ev
 
-        def finish_codec(k, off, nnz, b0, nbytes, done):
-            done.synchronize()
+        def finish_codec(k, off, nnz, b0, nbytes, rows_ready, done):
+            rows_ready.synchronize()  # decode while the block's values are still crossing
             td = time.perf_counter()
             a, z = int(sp.bounds[k]), int(sp.bounds[k + 1])
             decode_rows(counts_h.numpy()[a:z], lens_h.numpy()[a:z], bytes_h.numpy()[b0:], nbytes, a, off,
@@ -206,6 +206,7 @@ def streamed_build(mesh, sp, mode: str = "exact", device=None, capacity: int | N
             if trace is not None:
                 trace.append((f"decode {k} {nnz / 1e6:.0f}M rows {1e3 * (time.perf_counter() - td):.1f} ms", None,
                               time.perf_counter()))
+            done.synchronize()
 
         def finish(k, off, nnz, cp_stage, rows_landed, done):
             rows_landed.synchronize()
@@ -275,6 +276,7 @@ def streamed_build(mesh, sp, mode: str = "exact", device=None, capacity: int | N
                             lens_h[a:z].copy_(lens_d, non_blocking=True)
                             if nbytes:
                                 bytes_h[boff:boff + nbytes].copy_(bytes_d[:nbytes], non_blocking=True)
+                            rows_ready = d2h.record_event()
                             if nnz:
                                 out_vals[offset:offset + nnz].copy_(csc.vals, non_blocking=True)
                             done = d2h.record_event()
@@ -282,7 +284,7 @@ def streamed_build(mesh, sp, mode: str = "exact", device=None, capacity: int | N
                         enc_done[k & 1] = done
                         for t in (counts_d, lens_d, bytes_d, csc.vals):
                             t.record_stream(d2h)
-                        futures.append(pool.submit(finish_codec, k, offset, nnz, boff, nbytes, done))
+                        futures.append(pool.submit(finish_codec, k, offset, nnz, boff, nbytes, rows_ready, done))
                         d2h_bytes += 2 * (z - a) + nbytes + 8 * nnz
                         coded_blocks += 1
                         boff += nbytes

@@ -191,6 +191,7 @@ class CscHostTransfer:
             slot.lens[:n_cols].copy_(lens_d, non_blocking=True)
             if nbytes:
                 slot.bytes[:nbytes].copy_(bytes_d[:nbytes], non_blocking=True)
+            rows_ready = self.copy.record_event()
             slot.vals[:nnz].copy_(csc.vals, non_blocking=True)
             done = self.copy.record_event(torch.cuda.Event(enable_timing=self.trace is not None))
             for t in (counts_d, lens_d, bytes_d, csc.vals):
@@ -201,12 +202,13 @@ class CscHostTransfer:
         col_lo = csc.col_lo
 
         def finish() -> LowerCscMatrix:
-            done.synchronize()
+            rows_ready.synchronize()  # decode while the values are still crossing
             t0 = time.perf_counter()
             slot.col_ptr[0] = 0
             decode_rows(slot.counts.numpy()[:n_cols], slot.lens.numpy()[:n_cols], slot.bytes.numpy(), nbytes, col_lo,
                         0, slot.col_ptr.numpy()[1:], slot.row_idx[:nnz], threads)
             t1 = time.perf_counter()
+            done.synchronize()
             if trace is not None:
                 trace.append((k, started.elapsed_time(done), (t1 - t0) * 1e3))
             return LowerCscMatrix(col_ptr=slot.col_ptr.numpy(), row_idx=slot.row_idx[:nnz],
