@@ -43,7 +43,7 @@ from dataclasses import dataclass
 import numpy as np
 import torch
 
-from .errors import NodeIndexError
+from .errors import MeshValidationError, NodeIndexError
 
 __all__ = ["element_ranges", "column_bounds", "balanced_bounds", "histogram_bins", "ShardedBuild", "TorchExchange",
            "small_h2d", "block_cost_histograms", "touch_weight",
@@ -178,6 +178,24 @@ class TorchExchange:
         out = [torch.empty_like(t) for _ in range(self.world)]
         self.dist.all_gather(out, t, group=self.group)
         return torch.stack(out).cpu().numpy()
+
+    def allgather_async(self, t: torch.Tensor):
+        """All-gather of a 1-D int64 tensor whose host copy is read later: returns a callable giving
+        the (world, k) host array (it waits only for the collective, not for work enqueued after it
+        on the stream -- the host prepares the next launches while the GPU keeps computing)."""
+        if not t.is_cuda or _host_staged(self.group):
+            out = self.allgather(t)
+            return lambda: out
+        out = [torch.empty_like(t) for _ in range(self.world)]
+        self.dist.all_gather(out, t, group=self.group)
+        host = torch.empty((self.world, t.numel()), dtype=t.dtype, pin_memory=True)
+        host.copy_(torch.stack(out), non_blocking=True)
+        ev = torch.cuda.current_stream(t.device).record_event()
+
+        def result():
+            ev.synchronize()
+            return host.numpy()
+        return result
 
     def sum_(self, t: torch.Tensor) -> torch.Tensor:
         return all_reduce(t, group=self.group)
@@ -539,7 +557,8 @@ class ShardedBuild:
     # -- phases (so a loopback driver can interleave G ranks in one process) --
     def phase_local(self):
         """Integrate the owned elements and count the records per destination -> the row this
-        rank contributes to the metadata all-gather: fail record (3) + (records, values) x G."""
+        rank contributes to the metadata all-gather: fail record (3) + (records, values) x G
+        (the in-process drivers' single-gather form of step)."""
         ke, rows, cols, fail = self.ops.integrate(self.dm)
         per_dest, ws = self.ops.halo_count(self.dm, self.bounds, self.world, self.rank)
         self._pending = (ke, rows, cols, ws)
@@ -582,9 +601,48 @@ class ShardedBuild:
         self.last_counts = C
         return self.last
 
+    def phase_count(self) -> torch.Tensor:
+        """Records / values this rank sends each destination (connectivity only, no KE)."""
+        per_dest, ws = self.ops.halo_count(self.dm, self.bounds, self.world, self.rank)
+        self._count_ws = ws
+        return per_dest.reshape(-1)
+
+    def phase_integrate(self) -> torch.Tensor:
+        ke, rows, cols, fail = self.ops.integrate(self.dm)
+        self._pending = (ke, rows, cols, self._count_ws)
+        return fail.reshape(-1)
+
     def step(self):
+        """One sharded build.  The count all-gather needs only the connectivity, so it runs before
+        the integration kernel and the host reads it while the GPU integrates; the fail records
+        (one more small all-gather) are checked with the assembly's status read at the end, every
+        rank raising the same error for the lowest failing element."""
+        async_gather = getattr(self.exchange, "allgather_async", None)
+        if async_gather is None:  # in-process drivers / CPU stand-ins: the one-gather form
+            return self._step_gathered()
+        counts = async_gather(self.phase_count())
+        fails = async_gather(self.phase_integrate())
+        C = counts().reshape(self.world, self.world, 2)
+        err = None
+        try:
+            res = self._exchange_assemble(C)
+        except MeshValidationError as e:  # out-of-range node ids: reported as the element's error below
+            err, res = e, None
+        meta_fail = fails()
+        fe = _fail_error(meta_fail, [lo for lo, _ in self.ranges], self.n_nodes)
+        if fe is not None:
+            self._pending = None
+            raise fe
+        if err is not None:
+            raise err
+        return res
+
+    def _step_gathered(self):
         meta = self.exchange.allgather(self.phase_local())
         C = self.check_meta(meta)
+        return self._exchange_assemble(C)
+
+    def _exchange_assemble(self, C):
         chunk = 4 * C[:, :, 0] + C[:, :, 1]
         r = self.rank
         if self.exchange.p2p:

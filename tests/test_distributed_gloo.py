@@ -159,3 +159,42 @@ def test_gloo_sharded_build_bitwise_equal_to_reference(tmp_path, world, kind):
 
     want = np.array(csc_digest(cp, ri, vv), dtype=np.uint64).astype(np.int64)
     assert all(np.array_equal(b["digest"], want) for b in blocks)
+
+
+def _fail_worker(rank, world, port, outdir):
+    sys.path.insert(0, str(ROOT))
+    sys.path.insert(0, str(ROOT / "tests"))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch.distributed as dist
+
+    from paper_1501_04784_b200.distributed import ShardedBuild, TorchExchange
+    from paper_1501_04784_b200.errors import DegenerateElementError
+    from paper_1501_04784_b200.mesh import Mesh
+
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        mesh = _mesh("structured")
+        conn = mesh.connectivity.copy()
+        conn[[90, 110]] = conn[[90, 110]][:, [4, 5, 6, 7, 0, 1, 2, 3]]  # inverted: degenerate, in the last range
+        runner = ShardedBuild(Mesh(mesh.coords, np.ascontiguousarray(conn), mesh.coefficient), rank, world,
+                              ops=OracleOps(), exchange=TorchExchange())
+        try:
+            runner.step()
+            got = -1
+        except DegenerateElementError as e:
+            got = e.element_id
+        # every rank raised, so every rank reaches this collective (no rank left waiting in the step)
+        dist.barrier()
+        np.save(Path(outdir) / f"fail{rank}.npy", np.array([got]))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_sharded_build_raises_the_same_error_on_every_rank(tmp_path):
+    """A degenerate element in one rank's range: every rank raises DegenerateElementError for the
+    lowest failing global element (element.py:237-244) and none is left inside a collective."""
+    world = 2
+    mp.start_processes(_fail_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True,
+                       start_method="spawn")
+    got = [int(np.load(tmp_path / f"fail{r}.npy")[0]) for r in range(world)]
+    assert got == [90, 90]
