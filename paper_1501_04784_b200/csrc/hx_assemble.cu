@@ -185,6 +185,10 @@ __device__ __forceinline__ int incident_sorted(int64_t cl, int32_t *__restrict__
     return deg;
 }
 
+#ifndef HX_RECORDS_UNROLL
+#define HX_RECORDS_UNROLL 1
+#endif
+constexpr int RECORDS_UNROLL = HX_RECORDS_UNROLL;  // the pattern pass's record loop
 constexpr int MAX_OFFDIAG_CONTRIB = 4;     // hex meshes: an edge is shared by at most 4 elements
 #ifndef HX_COL_BLOCK
 #define HX_COL_BLOCK 64
@@ -415,7 +419,7 @@ pattern_kernel(SegTable T, int64_t col_lo, int64_t ncols, int32_t *__restrict__ 
     int j = -1, shift = 3;
     K prev = ~(K)0;
     uint32_t word = 0;
-#pragma unroll 1
+#pragma unroll RECORDS_UNROLL
     for (int q = 0; q < cnt; ++q) {
         const K key = L[q * COL_BLOCK];
         const K v = key >> 6;
