@@ -186,7 +186,7 @@ __device__ __forceinline__ int incident_sorted(int64_t cl, int32_t *__restrict__
 }
 
 #ifndef HX_RECORDS_UNROLL
-#define HX_RECORDS_UNROLL 1
+#define HX_RECORDS_UNROLL 4
 #endif
 constexpr int RECORDS_UNROLL = HX_RECORDS_UNROLL;  // the pattern pass's record loop
 constexpr int MAX_OFFDIAG_CONTRIB = 4;     // hex meshes: an edge is shared by at most 4 elements
