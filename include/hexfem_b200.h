@@ -78,13 +78,6 @@ extern "C" {
 #define HX_CSC_ADJACENCY_READY 2  /* hx_mesh_csc_build only: the workspace's node adjacency and the status
                                    * word were filled by hx_integrate_mesh_adjacency over every element
                                    * (one segment, columns [0, n_nodes)); the build skips its first pass */
-#define HX_CSC_ADJACENCY_BLOCK 8  /* hx_mesh_csc_build: the workspace's slots for columns [col_lo, col_hi) hold
-                                   * the elements of segment (flags >> 8) & 3 recorded by
-                                   * hx_integrate_mesh_block_adjacency (entries tagged HX_ADJ_OWN, element
-                                   * index relative to that segment); the build records the other segments'
-                                   * fixed slots itself and checks the slot count (the sharded build's own
-                                   * elements + received records) */
-#define HX_ADJ_OWN 0x40000000     /* tag of a segment-relative adjacency entry */
 #define HX_CSC_FIXED_ADJACENCY 4  /* symbolic/build: record the node adjacency in fixed slots (element e puts
                                    * e << 3 | a in slot a of its local node a; plain stores, no atomic
                                    * counter) -- one segment, columns [0, n_nodes).  Two elements holding one
@@ -161,17 +154,6 @@ int hx_integrate_mesh_adjacency(const double *coords, int64_t n_nodes, const int
                                 const double *coeff, int64_t lo, int64_t hi, double *ke, int32_t *rows,
                                 int32_t *cols, int32_t mode, hx_fail_info *fail, void *csc_workspace,
                                 int64_t workspace_bytes, uint32_t *csc_status, int32_t reset, void *stream);
-
-/* hx_integrate_mesh of elements [0, n_el) fused with the fixed-slot adjacency of the assembly of
- * columns [col_lo, col_hi) only: element e with local node a in the range stores (e << 3 | a) |
- * HX_ADJ_OWN in slot a of that column and counts the stored slots; the call empties the slots,
- * zeroes the status word and the counters first.  Follow with hx_mesh_csc_build(segments, ...,
- * HX_CSC_ADJACENCY_BLOCK | (index of this segment << 8)) on the same workspace and status.
- * 8 * (total elements of the build) must stay below 2^30. */
-int hx_integrate_mesh_block_adjacency(const double *coords, int64_t n_nodes, const int32_t *conn,
-                                      const double *coeff, int64_t n_el, double *ke, int32_t *rows, int32_t *cols,
-                                      int32_t mode, hx_fail_info *fail, void *csc_workspace, int64_t workspace_bytes,
-                                      uint32_t *csc_status, int64_t col_lo, int64_t col_hi, void *stream);
 
 /* assemble.py:86-93 alone: rows/cols (36*(hi-lo),) i32 for elements [lo, hi). */
 int hx_connectivity_index_arrays(const int32_t *conn, int64_t lo, int64_t hi, int32_t *rows,

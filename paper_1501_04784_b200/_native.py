@@ -26,14 +26,13 @@ MODE_EXACT, MODE_FAST = 0, 1
 CSC_ORDER_BY_ELEMENT = 1
 CSC_ADJACENCY_READY = 2
 CSC_FIXED_ADJACENCY = 4
-CSC_ADJACENCY_BLOCK = 8
 MAX_SEGMENTS = 4
 
 # Every symbol declared in include/hexfem_b200.h (checked by tests/test_abi_cpu.py).
 EXPORTED = (
     "hx_abi_version", "hx_last_error", "hx_dn_table", "hx_pack_tables", "hx_device_sm_count",
     "hx_selftest_division",
-    "hx_stiffness_batch", "hx_integrate_mesh", "hx_integrate_mesh_adjacency", "hx_integrate_mesh_block_adjacency", "hx_connectivity_index_arrays",
+    "hx_stiffness_batch", "hx_integrate_mesh", "hx_integrate_mesh_adjacency", "hx_connectivity_index_arrays",
     "hx_dof_index_arrays",
     "hx_mesh_csc_workspace_bytes", "hx_mesh_csc_symbolic", "hx_mesh_csc_build", "hx_mesh_csc_numeric",
     "hx_mesh_csc_emit", "hx_integrate_emit_workspace_bytes", "hx_integrate_emit",
@@ -92,8 +91,6 @@ def lib():
         "hx_stiffness_batch": ([P, P, I64, P, I32, P, P], ctypes.c_int),
         "hx_integrate_mesh": ([P, I64, P, P, I64, I64, P, P, P, I32, P, P], ctypes.c_int),
         "hx_integrate_mesh_adjacency": ([P, I64, P, P, I64, I64, P, P, P, I32, P, P, I64, P, I32, P], ctypes.c_int),
-        "hx_integrate_mesh_block_adjacency": ([P, I64, P, P, I64, P, P, P, I32, P, P, I64, P, I64, I64, P],
-                                              ctypes.c_int),
         "hx_connectivity_index_arrays": ([P, I64, I64, P, P, P], ctypes.c_int),
         "hx_dof_index_arrays": ([P, I64, I64, I64, I32, P, P, P], ctypes.c_int),
         "hx_mesh_csc_workspace_bytes": ([I64, I64], I64),

@@ -112,37 +112,6 @@ __global__ void adjacency_fixed_kernel(const int32_t *__restrict__ conn, int64_t
     }
 }
 
-// 1''. block build (HX_CSC_ADJACENCY_BLOCK): fixed slots of every segment but `skip` (whose slots the
-// integration kernel recorded) for the nodes in [col_lo, col_hi), combined element index, counted.
-__global__ void adjacency_block_kernel(SegTable T, int64_t n_total, int skip, int64_t n_nodes, int64_t col_lo,
-                                       int64_t col_hi, int32_t *__restrict__ adj,
-                                       unsigned long long *__restrict__ stored, uint32_t *__restrict__ status) {
-    unsigned long long mine = 0;
-    for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < 8 * n_total;
-         w += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t e = w >> 3;
-        const int sg = seg_of(T, e);
-        if (sg == skip) continue;
-        const int a = (int)(w & 7);
-        const int32_t v = __ldg(T.conn[sg] + T.conn_stride[sg] * (e - T.start[sg]) + a);
-        if (v < 0 || (int64_t)v >= n_nodes) {
-            atomicOr(status, HX_ST_BAD_INDEX);
-            continue;
-        }
-        if (v >= col_lo && v < col_hi) {
-            adj[8 * ((int64_t)v - col_lo) + a] = (int32_t)w;  // w = (e << 3) | a
-            ++mine;
-        }
-    }
-    if (mine) atomicAdd(stored, mine);
-}
-
-// A fixed-slot adjacency entry as a combined element entry: entries the integration kernel recorded
-// for one segment of a block build carry HX_ADJ_OWN and a segment-relative element index.
-__device__ __forceinline__ int32_t slot_entry(int32_t v, int32_t own_base) {
-    return (v >= 0 && (v & HX_ADJ_OWN)) ? (v & ~HX_ADJ_OWN) + (own_base << 3) : v;
-}
-
 // Column processing order for non-local numberings (HX_CSC_ORDER_BY_ELEMENT): key = the column's
 // lowest incident element (its adjacency slots), value = the column; sorting the pairs makes
 // consecutive pattern/emit threads work on nearby elements (connectivity rows and KE values stay in
@@ -150,13 +119,12 @@ __device__ __forceinline__ int32_t slot_entry(int32_t v, int32_t own_base) {
 // FIXED: fixed-slot adjacency (slot = local node, empty = -1; see incident_sorted).
 template <bool FIXED>
 __global__ void first_element_kernel(int64_t ncols, const int32_t *__restrict__ deg, const int32_t *__restrict__ adj,
-                                     uint32_t empty_key, uint32_t *__restrict__ keys, uint32_t *__restrict__ cols,
-                                     int32_t own_base) {
+                                     uint32_t empty_key, uint32_t *__restrict__ keys, uint32_t *__restrict__ cols) {
     for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < ncols; c += (int64_t)gridDim.x * blockDim.x) {
         const int d = FIXED ? MAXDEG : min(__ldg(deg + c), MAXDEG);
         uint32_t k = empty_key;
         for (int j = 0; j < d; ++j) {
-            const int32_t v = FIXED ? slot_entry(__ldg(adj + 8 * c + j), own_base) : __ldg(adj + 8 * c + j);
+            const int32_t v = __ldg(adj + 8 * c + j);
             if (!FIXED || v >= 0) k = min(k, (uint32_t)(v >> 3));
         }
         keys[c] = k;
@@ -189,14 +157,12 @@ __device__ __forceinline__ void sort8(int32_t (&v)[8]) {
 template <bool FIXED>
 __device__ __forceinline__ int incident_sorted(int64_t cl, int32_t *__restrict__ deg_arr,
                                                const int32_t *__restrict__ adj, int32_t (&ent)[8],
-                                               uint32_t *__restrict__ status, int32_t own_base = 0) {
+                                               uint32_t *__restrict__ status) {
     int deg = 0;
     if (FIXED) {
         const int4 *a4 = reinterpret_cast<const int4 *>(adj + 8 * cl);
         const int4 lo = a4[0], hi = a4[1];
-        const int32_t v[8] = {slot_entry(lo.x, own_base), slot_entry(lo.y, own_base), slot_entry(lo.z, own_base),
-                              slot_entry(lo.w, own_base), slot_entry(hi.x, own_base), slot_entry(hi.y, own_base),
-                              slot_entry(hi.z, own_base), slot_entry(hi.w, own_base)};
+        const int32_t v[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
             ent[k] = v[k] >= 0 ? v[k] : INT32_MAX;
@@ -330,14 +296,14 @@ template <typename K, bool SINGLE, bool FIXED>
 __device__ __forceinline__ int column_pattern_sort(const SegTable &T, bool active, int64_t cl, int32_t c,
                                                    int32_t *__restrict__ deg_arr, const int32_t *__restrict__ adj,
                                                    int32_t *__restrict__ ent_out, K *L, int &cnt, int &deg,
-                                                   int32_t &last, uint32_t *__restrict__ status, int32_t own_base) {
+                                                   int32_t &last, uint32_t *__restrict__ status) {
     int m = 0;
     deg = 0;
     last = -1;
     int32_t ent[8];
     cnt = 0;
     if (active) {
-        deg = incident_sorted<FIXED>(cl, deg_arr, adj, ent, status, own_base);
+        deg = incident_sorted<FIXED>(cl, deg_arr, adj, ent, status);
         if (deg < 0) deg = 0;
 #pragma unroll
         for (int k = 0; k < 8; ++k)
@@ -407,8 +373,7 @@ pattern_kernel(SegTable T, int64_t col_lo, int64_t ncols, int32_t *__restrict__ 
                int64_t scratch_capacity, unsigned long long *__restrict__ scratch_top,
                int64_t *__restrict__ block_scratch, uint32_t *__restrict__ status,
                const uint32_t *__restrict__ order, unsigned long long *__restrict__ slot_total,
-               int32_t *__restrict__ tile_need, int32_t *__restrict__ tadj, int32_t *__restrict__ tdeg,
-               int32_t own_base) {
+               int32_t *__restrict__ tile_need, int32_t *__restrict__ tadj, int32_t *__restrict__ tdeg) {
     __shared__ K sL[SORT_SLOTS * COL_BLOCK];  // this thread's contribution keys, [slot][thread]
     __shared__ unsigned long long s_base;
     using BlockScan = cub::BlockScan<int32_t, COL_BLOCK>;
@@ -423,7 +388,7 @@ pattern_kernel(SegTable T, int64_t col_lo, int64_t ncols, int32_t *__restrict__ 
     // sorted incident lists and degrees in processing order (in place over adj / deg in column order)
     int32_t *ent_out = (order != nullptr ? tadj : adj) + 8 * idx;
     const int m = column_pattern_sort<K, SINGLE, FIXED>(T, cl < ncols, cl, c, deg_arr, adj, ent_out, L, cnt, deg, last,
-                                                        status, own_base);
+                                                        status);
     if (cl < ncols) (order != nullptr ? tdeg : deg_arr)[idx] = deg;
     {  // elements the tile's emit needs: every incident element < tile_need (the fused kernel waits for them)
         const int need = __reduce_max_sync(0xffffffffu, last + 1);
@@ -470,11 +435,10 @@ pattern_kernel(SegTable T, int64_t col_lo, int64_t ncols, int32_t *__restrict__ 
 }
 
 // Fixed-slot adjacency check: every (element, local node) pair must have landed in its own slot.
-// expected: the writers' count (block build) or null = 8 slots per element (every column).
 __global__ void slot_check_kernel(const unsigned long long *__restrict__ slot_total, int64_t n_total,
-                                  const unsigned long long *__restrict__ expected, uint32_t *__restrict__ status) {
-    const unsigned long long want = expected != nullptr ? *expected : 8ull * (unsigned long long)n_total;
-    if (threadIdx.x == 0 && blockIdx.x == 0 && *slot_total != want) atomicOr(status, HX_ST_SLOT_COLLISION);
+                                  uint32_t *__restrict__ status) {
+    if (threadIdx.x == 0 && blockIdx.x == 0 && *slot_total != 8ull * (unsigned long long)n_total)
+        atomicOr(status, HX_ST_SLOT_COLLISION);
 }
 
 // 6. Emit pass: block b re-walks the output entries of the same COL_BLOCK columns (coalesced
@@ -834,7 +798,7 @@ struct MeshWs {
     int64_t *block_scratch;
     int32_t *tile_need;  // per tile: 1 + its highest incident element (0: none)
     int32_t *tadj, *tdeg;  // element order only: sorted incident lists / degrees by processing position
-    unsigned long long *scratch_top, *slot_total, *slot_expected;
+    unsigned long long *scratch_top, *slot_total;
     uint32_t *keys_in, *keys_out, *cols_in, *order;
     int2 *scratch;
     int64_t scratch_capacity;
@@ -866,7 +830,7 @@ static MeshWs mesh_ws_layout(void *base, int64_t ncols, int64_t workspace_bytes 
     const size_t o_bs = take(sizeof(int64_t) * std::max<int64_t>(1, ceil_div(ncols, COL_BLOCK)));
     const size_t o_tn = take(sizeof(int32_t) * std::max<int64_t>(1, ceil_div(ncols, COL_BLOCK)));
     const size_t o_ta = take(sizeof(int32_t) * 8 * nc), o_td = take(sizeof(int32_t) * nc);
-    const size_t o_st = take(3 * sizeof(unsigned long long));  // scratch_top, slot_total, slot_expected
+    const size_t o_st = take(2 * sizeof(unsigned long long));  // scratch_top, slot_total
     const size_t o_ki = take(sizeof(uint32_t) * nc), o_ko = take(sizeof(uint32_t) * nc);
     const size_t o_ci = take(sizeof(uint32_t) * nc), o_or = take(sizeof(uint32_t) * nc);
     w.cub_bytes = cub_temp_bytes(ncols);
@@ -887,7 +851,6 @@ static MeshWs mesh_ws_layout(void *base, int64_t ncols, int64_t workspace_bytes 
         w.tdeg = (int32_t *)(b + o_td);
         w.scratch_top = (unsigned long long *)(b + o_st);
         w.slot_total = w.scratch_top + 1;
-        w.slot_expected = w.scratch_top + 2;
         w.keys_in = (uint32_t *)(b + o_ki);
         w.keys_out = (uint32_t *)(b + o_ko);
         w.cols_in = (uint32_t *)(b + o_ci);
@@ -934,18 +897,6 @@ static int make_segtable(const hx_elem_segment *segs, int32_t n_segs, SegTable &
     return HX_OK;
 }
 
-
-int mesh_ws_block(void *workspace, int64_t workspace_bytes, int64_t ncols, int32_t **adj,
-                  unsigned long long **stored) {
-    const MeshWs w = mesh_ws_layout(workspace, ncols, workspace_bytes);
-    if (workspace == nullptr || workspace_bytes < (int64_t)w.total) {
-        set_last_error("mesh csc workspace %lld < %lld bytes", (long long)workspace_bytes, (long long)w.total);
-        return HX_ERR_WORKSPACE;
-    }
-    *adj = w.adj;
-    *stored = w.slot_expected;
-    return HX_OK;
-}
 
 int mesh_ws_adjacency(void *workspace, int64_t workspace_bytes, int64_t ncols, int32_t **deg, int32_t **adj) {
     const MeshWs w = mesh_ws_layout(workspace, ncols, workspace_bytes);
@@ -1026,33 +977,18 @@ static int mesh_csc_build(const hx_elem_segment *segs, int32_t n_segs, int64_t n
     const bool ordered = (flags & HX_CSC_ORDER_BY_ELEMENT) != 0 && ncols > 0 && n_total > 0;
     // adjacency (and its status bits) already recorded by hx_integrate_mesh_adjacency
     const bool adj_ready = (flags & HX_CSC_ADJACENCY_READY) != 0;
-    // block build: one segment's slots for [col_lo, col_hi) recorded by the integration kernel
-    const bool block = (flags & HX_CSC_ADJACENCY_BLOCK) != 0;
-    const int own_seg = (flags >> 8) & 3;
-    // fixed-slot adjacency: recorded by the integration kernel (adj_ready / block) or by
-    // adjacency_fixed_kernel / adjacency_block_kernel
-    const bool fixed = adj_ready || block || (flags & HX_CSC_FIXED_ADJACENCY) != 0;
-    if (fixed && !block && (n_segs != 1 || col_lo != 0 || col_hi != n_nodes || !single_conn(T))) {
+    // fixed-slot adjacency: recorded by the integration kernel (adj_ready) or by adjacency_fixed_kernel
+    const bool fixed = adj_ready || (flags & HX_CSC_FIXED_ADJACENCY) != 0;
+    if (fixed && (n_segs != 1 || col_lo != 0 || col_hi != n_nodes || !single_conn(T))) {
         set_last_error("hx_mesh_csc_build: a fixed-slot adjacency needs one segment and every column");
         return HX_ERR_VALUE;
     }
-    if (block && (own_seg >= n_segs || adj_ready || 8 * n_total >= (int64_t(1) << 30))) {
-        set_last_error("hx_mesh_csc_build: HX_CSC_ADJACENCY_BLOCK needs the recorded segment's index and < 2^27 "
-                       "elements");
-        return HX_ERR_VALUE;
-    }
-    const int32_t own_base = block ? (int32_t)T.start[own_seg] : 0;
-    if (!adj_ready && !block) HX_TRY_CUDA(cudaMemsetAsync(status, 0, sizeof(uint32_t), s));
+    if (!adj_ready) HX_TRY_CUDA(cudaMemsetAsync(status, 0, sizeof(uint32_t), s));
     HX_TRY_CUDA(cudaMemsetAsync(w.order_flag, 0, sizeof(uint32_t), s));
     if (ordered) HX_TRY_CUDA(cudaMemsetAsync(w.order_flag, 1, 1, s));  // little-endian u32 == 1
     if (ncols > 0) {
-        if (!adj_ready && !block) HX_TRY_CUDA(cudaMemsetAsync(w.deg, 0, sizeof(int32_t) * ncols, s));
-        if (block && n_total > 0) {  // the other segments' slots (received records)
-            const unsigned grid = (unsigned)std::min<int64_t>(ceil_div(8 * n_total, 256), 148 * 64);
-            adjacency_block_kernel<<<grid, 256, 0, s>>>(T, n_total, own_seg, n_nodes, col_lo, col_hi, w.adj,
-                                                        w.slot_expected, status);
-            HX_CHECK_LAUNCH("adjacency_block_kernel");
-        } else if (n_total > 0 && !adj_ready && fixed) {
+        if (!adj_ready) HX_TRY_CUDA(cudaMemsetAsync(w.deg, 0, sizeof(int32_t) * ncols, s));
+        if (n_total > 0 && !adj_ready && fixed) {
             HX_TRY_CUDA(cudaMemsetAsync(w.adj, 0xff, sizeof(int32_t) * 8 * ncols, s));
             const unsigned grid = (unsigned)std::min<int64_t>(ceil_div(8 * n_total, 256), 148 * 64);
             adjacency_fixed_kernel<<<grid, 256, 0, s>>>(T.conn[0], n_total, n_nodes, w.adj, status);
@@ -1069,11 +1005,9 @@ static int mesh_csc_build(const hx_elem_segment *segs, int32_t n_segs, int64_t n
         if (ordered) {
             const unsigned g = (unsigned)std::min<int64_t>(ceil_div(ncols, 256), 148 * 32);
             if (fixed)
-                first_element_kernel<true><<<g, 256, 0, s>>>(ncols, w.deg, w.adj, (uint32_t)n_total, w.keys_in, w.cols_in,
-                                                             own_base);
+                first_element_kernel<true><<<g, 256, 0, s>>>(ncols, w.deg, w.adj, (uint32_t)n_total, w.keys_in, w.cols_in);
             else
-                first_element_kernel<false><<<g, 256, 0, s>>>(ncols, w.deg, w.adj, (uint32_t)n_total, w.keys_in,
-                                                              w.cols_in, 0);
+                first_element_kernel<false><<<g, 256, 0, s>>>(ncols, w.deg, w.adj, (uint32_t)n_total, w.keys_in, w.cols_in);
             HX_CHECK_LAUNCH("first_element_kernel");
             int end_bit = 1;
             while (end_bit < 32 && ((uint64_t)n_total >> end_bit) != 0) ++end_bit;
@@ -1092,13 +1026,10 @@ static int mesh_csc_build(const hx_elem_segment *segs, int32_t n_segs, int64_t n
             using K = decltype(key_tag);
             pattern_kernel<K, decltype(single_tag)::value, decltype(fixed_tag)::value><<<tiles, COL_BLOCK, 0, s>>>(
                 T, col_lo, ncols, w.deg, w.adj, col_ptr, w.scratch, w.scratch_capacity, w.scratch_top, w.block_scratch,
-                status, order, w.slot_total, w.tile_need, w.tadj, w.tdeg, own_base);
+                status, order, w.slot_total, w.tile_need, w.tadj, w.tdeg);
         };
         const bool packed = n_nodes <= (int64_t(1) << 26);
-        if (fixed && block) {
-            if (packed) pattern(uint32_t{}, std::false_type{}, std::true_type{});
-            else pattern(uint64_t{}, std::false_type{}, std::true_type{});
-        } else if (fixed) {  // one dense segment (checked above)
+        if (fixed) {  // one dense segment (checked above)
             if (packed) pattern(uint32_t{}, std::true_type{}, std::true_type{});
             else pattern(uint64_t{}, std::true_type{}, std::true_type{});
         } else if (single_conn(T)) {
@@ -1110,7 +1041,7 @@ static int mesh_csc_build(const hx_elem_segment *segs, int32_t n_segs, int64_t n
         }
         HX_CHECK_LAUNCH("pattern_kernel");
         if (fixed) {
-            slot_check_kernel<<<1, 32, 0, s>>>(w.slot_total, n_total, block ? w.slot_expected : nullptr, status);
+            slot_check_kernel<<<1, 32, 0, s>>>(w.slot_total, n_total, status);
             HX_CHECK_LAUNCH("slot_check_kernel");
         }
         HX_TRY_CUDA(cudaMemsetAsync(col_ptr + ncols, 0, sizeof(int64_t), s));

@@ -73,9 +73,6 @@ int cuda_status(cudaError_t err, const char *where);
 // Adjacency section (deg (ncols) i32, adj (8 ncols) i32) of a mesh-CSC workspace (hx_assemble.cu),
 // filled by the integration kernel in the fused build (hx_integrate_mesh_adjacency).
 int mesh_ws_adjacency(void *workspace, int64_t workspace_bytes, int64_t ncols, int32_t **deg, int32_t **adj);
-// ... and the slot counter of a block build (HX_CSC_ADJACENCY_BLOCK): the slots the writers stored.
-int mesh_ws_block(void *workspace, int64_t workspace_bytes, int64_t ncols, int32_t **adj,
-                  unsigned long long **stored);
 
 // Resolve an integration launch's fail key into the hx_fail_info record (hx_ke.cu).
 int integrate_fail_resolve(const double *coords, int64_t n_nodes, const int32_t *conn, hx_fail_info *fail,

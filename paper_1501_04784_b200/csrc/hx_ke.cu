@@ -373,33 +373,6 @@ extern "C" int hx_integrate_mesh_adjacency(const double *coords, int64_t n_nodes
     return integrate_mesh_impl(coords, n_nodes, conn, coeff, lo, hi, ke, rows, cols, mode, fail, adj, s);
 }
 
-extern "C" int hx_integrate_mesh_block_adjacency(const double *coords, int64_t n_nodes, const int32_t *conn,
-                                                 const double *coeff, int64_t n_el, double *ke, int32_t *rows,
-                                                 int32_t *cols, int32_t mode, hx_fail_info *fail, void *csc_workspace,
-                                                 int64_t workspace_bytes, uint32_t *csc_status, int64_t col_lo,
-                                                 int64_t col_hi, void *stream) {
-    int rc = HX_OK;
-    if (!integrate_args_ok(0, n_el, ke, rows, cols, fail, mode, rc)) return rc;
-    if (csc_status == nullptr || n_nodes < 0 || n_nodes >= INT32_MAX || 8 * n_el >= (int64_t(1) << 30) ||
-        col_lo < 0 || col_hi < col_lo || col_hi > n_nodes) {
-        set_last_error("hx_integrate_mesh_block_adjacency: bad arguments (n_nodes=%lld n_el=%lld cols=[%lld, %lld))",
-                       (long long)n_nodes, (long long)n_el, (long long)col_lo, (long long)col_hi);
-        return HX_ERR_VALUE;
-    }
-    AdjOut adj{nullptr, csc_status};
-    adj.col_lo = col_lo;
-    adj.col_hi = col_hi;
-    adj.tag = HX_ADJ_OWN;
-    const int64_t ncols = col_hi - col_lo;
-    rc = mesh_ws_block(csc_workspace, workspace_bytes, ncols, &adj.adj, &adj.stored);
-    if (rc) return rc;
-    cudaStream_t s = (cudaStream_t)stream;
-    HX_TRY_CUDA(cudaMemsetAsync(csc_status, 0, sizeof(uint32_t), s));
-    HX_TRY_CUDA(cudaMemsetAsync(adj.stored, 0, sizeof(unsigned long long), s));
-    if (ncols > 0) HX_TRY_CUDA(cudaMemsetAsync(adj.adj, 0xff, sizeof(int32_t) * 8 * ncols, s));
-    return integrate_mesh_impl(coords, n_nodes, conn, coeff, 0, n_el, ke, rows, cols, mode, fail, adj, s);
-}
-
 extern "C" int hx_stiffness_batch(const double *coords, const double *coeff, int64_t n, double *out,
                                   int32_t mode, hx_fail_info *fail, void *stream) {
     if (n < 0 || (n > 0 && out == nullptr) || fail == nullptr) {

@@ -534,9 +534,6 @@ __device__ __forceinline__ bool ke_gauss_point(GpWarpSmem &sm, int el, int gp, b
 struct AdjOut {
     int32_t *adj;
     uint32_t *status;
-    int64_t col_lo = 0, col_hi = INT64_MAX;  // slots only for nodes in [col_lo, col_hi), indexed node - col_lo
-    int32_t tag = 0;                         // OR-ed into the entries (HX_ADJ_OWN: segment-relative index)
-    unsigned long long *stored = nullptr;    // counts the stored slots (the block build's slot check)
 };
 
 // The persistent warp loop of the integration kernel: element quads from a global counter, each
@@ -601,13 +598,8 @@ __device__ __forceinline__ void integrate_quads(GpWarpSmem &sm, const uint8_t *s
         if (valid && (node < 0 || node >= n_nodes)) {
             atomicMin(fail_min, (unsigned long long)(lo + k));  // bad-node key: below every degenerate key
             if (WITH_ADJ) atomicOr(adj_out.status, HX_ST_BAD_INDEX);
-        } else if (WITH_ADJ && valid && node >= adj_out.col_lo && node < adj_out.col_hi) {
-            adj_out.adj[8 * ((int64_t)node - adj_out.col_lo) + gp] = (int32_t)(((lo + k) << 3) | gp) | adj_out.tag;
-        }
-        if (WITH_ADJ && adj_out.stored != nullptr) {
-            const unsigned in_block = __ballot_sync(0xffffffffu, valid && node >= adj_out.col_lo &&
-                                                                     node < adj_out.col_hi);
-            if (lane == 0 && in_block) atomicAdd(adj_out.stored, (unsigned long long)__popc(in_block));
+        } else if (WITH_ADJ && valid) {
+            adj_out.adj[8 * (int64_t)node + gp] = (int32_t)(((lo + k) << 3) | gp);
         }
         __syncwarp();
         publish_node<MODE>(sm, el, gp, node, x0, x1, x2, c);

@@ -21,7 +21,7 @@ from .errors import ConfigurationError, DegenerateElementError, MeshValidationEr
 __all__ = [
     "DeviceMesh", "DeviceCsc", "AssemblyPrep", "new_assembly_prep", "rows_narrow", "require_device", "stream_handle", "integrate_mesh", "stiffness_batch",
     "connectivity_index_arrays", "dof_index_arrays", "assemble_dof", "raise_if_failed", "mesh_csc", "triplet_csc", "MeshPlan", "mesh_plan_async",
-    "new_block_prep", "mesh_emit", "integrate_emit", "plan_result", "plan_assembly", "block_elements", "generate_cube_mesh",
+    "mesh_emit", "integrate_emit", "plan_result", "plan_assembly", "block_elements", "generate_cube_mesh",
 ]
 
 _FAIL_WORDS = 3  # hx_fail_info = {int64 element, int32 gp, int32 pad, double det} = 24 bytes
@@ -210,16 +210,6 @@ def integrate_mesh(dm: DeviceMesh, lo: int = 0, hi: int | None = None, *, ke=Non
         N.check(N.lib().hx_integrate_mesh(_ptr(dm.coords), dm.n_nodes, _ptr(dm.conn), _ptr(dm.coeff), lo, hi,
                                           _ptr(ke), _ptr(rows), _ptr(cols), _mode_id(mode), _ptr(fail),
                                           stream_handle(stream)), "hx_integrate_mesh")
-    elif adjacency.block is not None:  # a column block of a sharded build: this segment's slots
-        if lo != 0 or hi != n:
-            raise ConfigurationError("a block adjacency records the whole segment")
-        c_lo, c_hi = adjacency.block
-        N.check(N.lib().hx_integrate_mesh_block_adjacency(
-            _ptr(dm.coords), dm.n_nodes, _ptr(dm.conn), _ptr(dm.coeff), n, _ptr(ke), _ptr(rows), _ptr(cols),
-            _mode_id(mode), _ptr(fail), _ptr(adjacency.ws), adjacency.ws.numel(), _ptr(adjacency.status), c_lo, c_hi,
-            stream_handle(stream)), "hx_integrate_mesh_block_adjacency")
-        adjacency.conn = dm.conn
-        adjacency.started = True
     else:
         if adjacency.conn is not dm.conn:
             raise ConfigurationError("the assembly workspace belongs to another mesh")
@@ -240,20 +230,6 @@ class AssemblyPrep:
     ws: torch.Tensor
     status: torch.Tensor
     started: bool = False
-    block: tuple | None = None  # (col_lo, col_hi): a block build's segment recorded by the integration
-
-
-def new_block_prep(n_nodes: int, col_lo: int, col_hi: int, nnz_hint: int | None = None, device=None) -> AssemblyPrep:
-    """Workspace of a column block's assembly whose fixed slots the integration kernel of one element
-    segment fills (hx_integrate_mesh_block_adjacency); mesh_csc(parts, ..., prep=, own_seg=) records
-    the other segments' slots.  Reusable step after step (the integration call resets it)."""
-    dev = require_device(device)
-    ncols = col_hi - col_lo
-    ws_bytes = N.lib().hx_mesh_csc_workspace_bytes(0, ncols)
-    if nnz_hint is not None and int(nnz_hint) - 16 * ncols > 0:  # scratch beyond the default 15 per column
-        ws_bytes += 8 * (int(nnz_hint) - 16 * ncols)
-    return AssemblyPrep(None, torch.empty(ws_bytes, dtype=torch.uint8, device=dev),
-                        torch.zeros(1, dtype=torch.int32, device=dev), block=(int(col_lo), int(col_hi)))
 
 
 def new_assembly_prep(dm: DeviceMesh) -> AssemblyPrep:
@@ -396,7 +372,7 @@ def _order_flags(order, conn, n_nodes) -> int:
 
 def mesh_csc(parts, n_nodes: int, col_lo: int = 0, col_hi: int | None = None, stream=None,
              row_capacity: int | None = None, order: str = "auto", prep: AssemblyPrep | None = None,
-             nnz_hint: int | None = None, own_seg: int | None = None) -> DeviceCsc:
+             nnz_hint: int | None = None) -> DeviceCsc:
     """Assemble columns [col_lo, col_hi) of the lower CSC from element segments.
 
     ``parts`` is a list of (conn (n,8) i32, ke (n,36) f64) CUDA tensor views in ascending global
@@ -423,34 +399,23 @@ def mesh_csc(parts, n_nodes: int, col_lo: int = 0, col_hi: int | None = None, st
     ws_bytes = N.lib().hx_mesh_csc_workspace_bytes(n_total, ncols)
     if ws_bytes < 0:
         raise ValueError("bad mesh size")
-    ready_flags = 0
-    if prep is not None and prep.block is not None:  # a block build: one segment's slots recorded
-        if (not prep.started or own_seg is None or not 0 <= own_seg < len(parts)
-                or parts[own_seg][0] is not prep.conn or prep.block != (col_lo, col_hi)):
-            raise ConfigurationError("block assembly prep must match the recorded segment and column range")
-        status, ws, ws_bytes = prep.status, prep.ws, prep.ws.numel()
-        ready_flags = N.CSC_ADJACENCY_BLOCK | (own_seg << 8)
-        flags |= ready_flags
-    elif prep is not None:
+    if prep is not None:
         if not prep.started or len(parts) != 1 or parts[0][0] is not prep.conn or col_lo != 0 or col_hi != n_nodes:
             raise ConfigurationError("assembly prep must cover the whole single-segment mesh it was made for")
         status, ws, ws_bytes = prep.status, prep.ws, prep.ws.numel()
-        ready_flags = N.CSC_ADJACENCY_READY
-        flags |= ready_flags
+        flags |= N.CSC_ADJACENCY_READY
     else:
         status = torch.zeros(1, dtype=torch.int32, device=dev)
     col_ptr = torch.empty(ncols + 1, dtype=torch.int64, device=dev)
     sh = stream_handle(stream)
     capacity = ROWS_PER_COLUMN_ESTIMATE * ncols if row_capacity is None else row_capacity
-    if nnz_hint is not None and (prep is None or prep.block is not None):
+    if nnz_hint is not None and prep is None:
         capacity = max(capacity, int(nnz_hint))
         extra = int(nnz_hint) - ncols - 15 * ncols  # off-diagonal records beyond the default scratch
         if extra > 0:
             ws_bytes += 8 * extra
-    if ready_flags == N.CSC_ADJACENCY_BLOCK | ((own_seg or 0) << 8):
-        ws_bytes = ws.numel()  # the block prep was sized for the hint already
     while True:
-        if not flags & (N.CSC_ADJACENCY_READY | N.CSC_ADJACENCY_BLOCK):
+        if not flags & N.CSC_ADJACENCY_READY:
             ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
         row_buf = torch.empty(max(capacity, 1), dtype=torch.int64, device=dev)
         val_buf = torch.empty(max(capacity, 1), dtype=torch.float64, device=dev)
@@ -459,9 +424,7 @@ def mesh_csc(parts, n_nodes: int, col_lo: int = 0, col_hi: int | None = None, st
                 "hx_mesh_csc_build")
         st, nnz = peek(status[0:1], col_ptr[-1:], stream=stream)  # one sync: status + nnz
         _status_error(st)
-        if flags & (N.CSC_ADJACENCY_READY | N.CSC_ADJACENCY_BLOCK):  # a retry recomputes the adjacency
-            flags &= ~(N.CSC_ADJACENCY_READY | N.CSC_ADJACENCY_BLOCK | (3 << 8))  # in a fresh workspace
-            status = torch.zeros(1, dtype=torch.int32, device=dev)
+        flags &= ~N.CSC_ADJACENCY_READY  # a retry recomputes the adjacency in a fresh workspace
         if st & N.ST_SLOT_COLLISION:
             continue  # fixed-slot adjacency lost an entry (inconsistent element orientation)
         if st & N.ST_SCRATCH and not st & (N.ST_FASTPATH_LIMITS & ~N.ST_SCRATCH):

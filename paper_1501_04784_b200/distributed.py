@@ -393,15 +393,9 @@ class CudaOps:
 
         return self.D.DeviceMesh(up(coords, np.float64), up(conn, np.int32), up(coeff, np.float64))
 
-    supports_block_prep = True
-
-    def integrate(self, dm, prep=None):
-        """-> (ke, rows, cols, fail record (3,) int64 device); ``prep`` (new_block_prep): the kernel
-        also records this rank's column-block slots of the assembly."""
-        return self.D.integrate_mesh(dm, mode=self.mode, adjacency=prep)
-
-    def block_prep(self, n_nodes, c_lo, c_hi, nnz_hint):
-        return self.D.new_block_prep(n_nodes, c_lo, c_hi, nnz_hint, device=self.device)
+    def integrate(self, dm):
+        """-> (ke, rows, cols, fail record (3,) int64 device)"""
+        return self.D.integrate_mesh(dm, mode=self.mode)
 
     def column_weights(self, dm, n_nodes: int, n_bins: int) -> torch.Tensor:
         hist = torch.zeros(n_bins, dtype=torch.int64, device=self.device)
@@ -453,9 +447,8 @@ class CudaOps:
                      "hx_halo_unpack")
         return records
 
-    def assemble(self, segments, n_nodes, c_lo, c_hi, nnz_hint=None, order="auto", prep=None, own_seg=None):
-        return self.D.mesh_csc(segments, n_nodes, c_lo, c_hi, nnz_hint=nnz_hint, order=order, prep=prep,
-                               own_seg=own_seg)
+    def assemble(self, segments, n_nodes, c_lo, c_hi, nnz_hint=None, order="auto"):
+        return self.D.mesh_csc(segments, n_nodes, c_lo, c_hi, nnz_hint=nnz_hint, order=order)
 
     def column_order(self, dm, n_nodes) -> str:
         """Column processing order of this rank's assemblies, decided once (one small reduction)."""
@@ -556,33 +549,17 @@ class ShardedBuild:
             self.nnz_hint = int(1.1 * h[b_lo:b_hi + 1].sum() / 8) + (self.c_hi - self.c_lo)
         order_fn = getattr(self.ops, "column_order", None)
         self.order = order_fn(self.dm, self.n_nodes) if order_fn is not None else "auto"
-        # the integration kernel records this block's slots for the own elements (HX_CSC_ADJACENCY_BLOCK);
-        # HX_SHARD_FUSED_ADJ=0 leaves the whole adjacency to the assembly's atomic pass
-        import os
-
-        self._prep = None
-        self._use_prep = (getattr(self.ops, "supports_block_prep", False)
-                          and os.environ.get("HX_SHARD_FUSED_ADJ", "1") != "0"
-                          and 8 * mesh.n_el < (1 << 30) and self.dm.n_el > 0)
         self.bounds = self.ops.bounds(self.bounds_np)
         self.last = None
         self.last_index = None
         self.last_counts = None
-
-    def _integrate(self):
-        if not self._use_prep:
-            return self.ops.integrate(self.dm)
-        if self._prep is None or (self.nnz_hint or 0) > self._prep_hint:  # sized for the block's nnz
-            self._prep = self.ops.block_prep(self.n_nodes, self.c_lo, self.c_hi, self.nnz_hint)
-            self._prep_hint = self.nnz_hint or 0
-        return self.ops.integrate(self.dm, prep=self._prep)
 
     # -- phases (so a loopback driver can interleave G ranks in one process) --
     def phase_local(self):
         """Integrate the owned elements and count the records per destination -> the row this
         rank contributes to the metadata all-gather: fail record (3) + (records, values) x G
         (the in-process drivers' single-gather form of step)."""
-        ke, rows, cols, fail = self._integrate()
+        ke, rows, cols, fail = self.ops.integrate(self.dm)
         per_dest, ws = self.ops.halo_count(self.dm, self.bounds, self.world, self.rank)
         self._pending = (ke, rows, cols, ws)
         return torch.cat([fail.reshape(-1).to(per_dest.device), per_dest.reshape(-1)])
@@ -617,12 +594,7 @@ class ShardedBuild:
         segments.append((self.dm.conn, ke))
         if n_rec > n_lower:
             segments.append(record_segment(records[n_lower:]))
-        if self._use_prep:
-            csc = self.ops.assemble(segments, self.n_nodes, self.c_lo, self.c_hi, nnz_hint=self.nnz_hint,
-                                    order=self.order, prep=self._prep, own_seg=1 if n_lower else 0)
-        else:
-            csc = self.ops.assemble(segments, self.n_nodes, self.c_lo, self.c_hi, nnz_hint=self.nnz_hint,
-                                    order=self.order)
+        csc = self.ops.assemble(segments, self.n_nodes, self.c_lo, self.c_hi, nnz_hint=self.nnz_hint, order=self.order)
         self.nnz_hint = int(csc.row_idx.shape[0])  # exact from now on (same mesh every step)
         self.last = ShardResult(csc.col_ptr, csc.row_idx, csc.vals, self.c_lo, self.c_hi)
         self.last_index = (ke, rows, cols)
@@ -636,7 +608,7 @@ class ShardedBuild:
         return per_dest.reshape(-1)
 
     def phase_integrate(self) -> torch.Tensor:
-        ke, rows, cols, fail = self._integrate()
+        ke, rows, cols, fail = self.ops.integrate(self.dm)
         self._pending = (ke, rows, cols, self._count_ws)
         return fail.reshape(-1)
 
