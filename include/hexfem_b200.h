@@ -112,6 +112,12 @@ typedef struct hx_elem_segment {
     int64_t n_el;
     int64_t conn_stride; /* in int32 units, multiple of 4; 0 means dense (8)                 */
     int64_t ke_stride;   /* in doubles; 0 means dense (36)                                   */
+    /* compact KE (received halo records, hx_halo_index): when ke_offset != NULL, element e holds
+     * only the packed entries set in ke_mask[e] (bit p = entry p), stored in ascending p at
+     * ke + ke_offset[e]; the assembly reads only entries of the columns it owns, which are exactly
+     * those.  NULL: dense rows as above. */
+    const int64_t *ke_offset;
+    const uint64_t *ke_mask;
 } hx_elem_segment;
 
 /* ---- introspection (host only, no GPU needed) ------------------------------------------ */
@@ -271,6 +277,13 @@ int64_t hx_halo_unpack_workspace_bytes(int64_t n_rec);
 int hx_halo_unpack(const int64_t *recv, const int64_t *src_desc, int32_t world, int32_t self,
                    const int64_t *col_bounds, int64_t n_rec, double *records, void *workspace,
                    int64_t workspace_bytes, void *stream);
+/* index: the received records as compact element segments without moving their values: conn
+ *        (n_rec, 8) i32 <- the ids, ke_offset (n_rec) i64 <- word index in recv of the record's first
+ *        value, ke_mask (n_rec) u64 <- the packed entries this rank owns (see hx_elem_segment).
+ *        Workspace: hx_halo_unpack_workspace_bytes(n_rec). */
+int hx_halo_index(const int64_t *recv, const int64_t *src_desc, int32_t world, int32_t self,
+                  const int64_t *col_bounds, int64_t n_rec, int32_t *conn, int64_t *ke_offset, uint64_t *ke_mask,
+                  void *workspace, int64_t workspace_bytes, void *stream);
 int hx_digest(const void *data, int64_t n_words, int64_t pos0, uint64_t add, uint64_t *out, void *stream);
 
 /* CUDA IPC receive buffers of the fused pack-and-send exchange (the one allocating entry point: an

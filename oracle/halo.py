@@ -80,6 +80,24 @@ def pack(conn, ke, bounds, world, self_rank) -> list:
     return chunks
 
 
+def index(recv: np.ndarray, desc: np.ndarray, bounds, world, self_rank):
+    """hx_halo_index restated: (conn (n, 8) int32, ke_offset (n,) int64 = word of each record's first
+    value in recv, ke_mask (n,) uint64 = its owned packed entries)."""
+    conns, offs, masks = [], [], []
+    for s in range(world):
+        off, nr, nv = (int(x) for x in desc[s])
+        if nr == 0:
+            continue
+        conn = np.ascontiguousarray(recv[off:off + 4 * nr]).view(np.int32).reshape(nr, 8)
+        m = owned_mask(conn, bounds, self_rank)
+        conns.append(conn)
+        offs.append(off + 4 * nr + np.concatenate([[0], np.cumsum(m.sum(axis=1))[:-1]]).astype(np.int64))
+        masks.append((m.astype(np.uint64) << np.arange(36, dtype=np.uint64)).sum(axis=1).astype(np.uint64))
+    if not conns:
+        return np.empty((0, 8), np.int32), np.empty(0, np.int64), np.empty(0, np.uint64)
+    return np.concatenate(conns), np.concatenate(offs), np.concatenate(masks)
+
+
 def unpack(recv: np.ndarray, desc: np.ndarray, bounds, world, self_rank) -> np.ndarray:
     """recv int64 words, desc (world, 3) = (offset, records, values) per source -> (n, 40) f64 records."""
     out = []

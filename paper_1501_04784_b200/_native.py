@@ -38,7 +38,7 @@ EXPORTED = (
     "hx_mesh_csc_emit", "hx_integrate_emit_workspace_bytes", "hx_integrate_emit",
     "hx_triplet_csc_workspace_bytes", "hx_triplet_csc_symbolic", "hx_triplet_csc_numeric",
     "hx_column_weights", "hx_column_touch", "hx_halo_workspace_bytes", "hx_halo_count", "hx_halo_pack",
-    "hx_halo_unpack_workspace_bytes", "hx_halo_unpack", "hx_digest",
+    "hx_halo_unpack_workspace_bytes", "hx_halo_unpack", "hx_halo_index", "hx_digest",
     "hx_ipc_alloc", "hx_ipc_open", "hx_ipc_close", "hx_ipc_free",
     "hx_block_select_workspace_bytes", "hx_block_select", "hx_block_gather", "hx_block_ranges", "hx_block_ranges_nodes",
     "hx_mm_write", "hx_mm_read", "hx_generate_cube_mesh", "hx_rows_narrow", "hx_rows_widen", "hx_peek",
@@ -61,7 +61,8 @@ class HxFailInfo(ctypes.Structure):
 
 class HxElemSegment(ctypes.Structure):
     _fields_ = [("conn", ctypes.c_void_p), ("ke", ctypes.c_void_p), ("n_el", ctypes.c_int64),
-                ("conn_stride", ctypes.c_int64), ("ke_stride", ctypes.c_int64)]
+                ("conn_stride", ctypes.c_int64), ("ke_stride", ctypes.c_int64),
+                ("ke_offset", ctypes.c_void_p), ("ke_mask", ctypes.c_void_p)]
 
 
 _lib = None
@@ -110,6 +111,7 @@ def lib():
         "hx_halo_pack": ([P, P, I64, P, I32, I32, P, P, P, P], ctypes.c_int),
         "hx_halo_unpack_workspace_bytes": ([I64], I64),
         "hx_halo_unpack": ([P, P, I32, I32, P, I64, P, P, I64, P], ctypes.c_int),
+        "hx_halo_index": ([P, P, I32, I32, P, I64, P, P, P, P, I64, P], ctypes.c_int),
         "hx_digest": ([P, I64, I64, ctypes.c_uint64, P, P], ctypes.c_int),
         "hx_ipc_alloc": ([I64, ctypes.POINTER(ctypes.c_void_p), P], ctypes.c_int),
         "hx_ipc_open": ([P, ctypes.POINTER(ctypes.c_void_p)], ctypes.c_int),
@@ -151,7 +153,8 @@ def check(rc: int, what: str) -> None:
 
 
 def segments(parts) -> ctypes.Array:
-    """Build an hx_elem_segment[] from (conn_ptr, ke_ptr, n_el[, conn_stride, ke_stride]) tuples."""
+    """Build an hx_elem_segment[] from (conn_ptr, ke_ptr, n_el[, conn_stride, ke_stride[, ke_offset_ptr,
+    ke_mask_ptr]]) tuples."""
     arr = (HxElemSegment * len(parts))()
     for i, part in enumerate(parts):
         conn, ke, n = part[:3]
@@ -160,4 +163,6 @@ def segments(parts) -> ctypes.Array:
         arr[i].n_el = n
         arr[i].conn_stride = part[3] if len(part) > 3 else 0
         arr[i].ke_stride = part[4] if len(part) > 4 else 0
+        arr[i].ke_offset = part[5] if len(part) > 5 else None
+        arr[i].ke_mask = part[6] if len(part) > 6 else None
     return arr

@@ -44,6 +44,8 @@ struct SegTable {
     const double *ke[MAX_SEGS];
     int64_t conn_stride[MAX_SEGS];  // int32 units
     int64_t ke_stride[MAX_SEGS];    // doubles
+    const int64_t *koff[MAX_SEGS];  // compact segments: first value of each element (null: dense rows)
+    const uint64_t *kmask[MAX_SEGS];
     int64_t start[MAX_SEGS + 1];  // combined element index where segment s starts
     int n;
 };
@@ -453,6 +455,21 @@ __device__ __forceinline__ const double *ke_row(const SegTable &T, int64_t e) {
     return T.ke[sg] + T.ke_stride[sg] * (e - T.start[sg]);
 }
 
+// Address of packed entry p of element e: a dense row, or a compact (received) element's p-th set
+// entry -- ke + ke_offset[e] + (owned entries below p).
+template <bool SINGLE>
+__device__ __forceinline__ const double *ke_entry(const SegTable &T, int64_t e, int p) {
+    if (SINGLE) return T.ke[0] + 36 * e + p;
+    const int sg = seg_of(T, e);
+    const int64_t le = e - T.start[sg];
+    if (T.koff[sg] != nullptr) {
+        const uint64_t m = __ldg(reinterpret_cast<const unsigned long long *>(T.kmask[sg]) + le);
+        return T.ke[sg] + __ldg(reinterpret_cast<const long long *>(T.koff[sg]) + le) +
+               __popcll(m & ((1ull << p) - 1ull));
+    }
+    return T.ke[sg] + T.ke_stride[sg] * le + p;
+}
+
 // KE gathers of the emit pass.  Each KE row is read by the columns of its element's 8 nodes, up to
 // one node layer apart; HX_EMIT_KE_HINT 1 marks those loads L2 evict_last (the streamed scratch
 // loads and CSC stores are evict-first) so the rows survive until their last column.
@@ -601,7 +618,7 @@ __device__ __forceinline__ void emit_tile(EmitSmem &S, const EmitArgs &A, int64_
             if (k < deg) {
                 const int32_t en = ent[k];
                 const int a = en & 7;
-                x[k] = ke_load<LOAD_CG>(ke_row<SINGLE>(T, en >> 3) + pack_index(a, a), pol);
+                x[k] = ke_load<LOAD_CG>(ke_entry<SINGLE>(T, en >> 3, pack_index(a, a)), pol);
             }
         }
         double v = x[0];
@@ -627,7 +644,7 @@ __device__ __forceinline__ void emit_tile(EmitSmem &S, const EmitArgs &A, int64_
                 const uint32_t kb = (w >> (3 + 6 * r)) & 63u;
                 const int32_t en = ent[kb >> 3];
                 const int a = en & 7, b = (int)(kb & 7u);
-                x[r] = ke_load<LOAD_CG>(ke_row<SINGLE>(T, en >> 3) + pack_index(max(a, b), min(a, b)), pol);
+                x[r] = ke_load<LOAD_CG>(ke_entry<SINGLE>(T, en >> 3, pack_index(max(a, b), min(a, b))), pol);
             }
         }
         double v = x[0];
@@ -878,6 +895,12 @@ static int make_segtable(const hx_elem_segment *segs, int32_t n_segs, SegTable &
         }
         T.conn[s] = segs[s].conn;
         T.ke[s] = segs[s].ke;
+        T.koff[s] = segs[s].ke_offset;
+        T.kmask[s] = segs[s].ke_mask;
+        if ((T.koff[s] == nullptr) != (T.kmask[s] == nullptr)) {
+            set_last_error("mesh csc: segment %d sets only one of ke_offset / ke_mask", s);
+            return HX_ERR_VALUE;
+        }
         T.conn_stride[s] = segs[s].conn_stride ? segs[s].conn_stride : 8;
         T.ke_stride[s] = segs[s].ke_stride ? segs[s].ke_stride : 36;
         if (T.conn_stride[s] < 8 || T.conn_stride[s] % 4 != 0 || T.ke_stride[s] < 36) {
@@ -909,7 +932,9 @@ int mesh_ws_adjacency(void *workspace, int64_t workspace_bytes, int64_t ncols, i
     return HX_OK;
 }
 
-static bool single_dense(const SegTable &T) { return T.n == 1 && T.ke_stride[0] == 36 && T.conn_stride[0] == 8; }
+static bool single_dense(const SegTable &T) {
+    return T.n == 1 && T.ke_stride[0] == 36 && T.conn_stride[0] == 8 && T.koff[0] == nullptr;
+}
 static bool single_conn(const SegTable &T) { return T.n == 1 && T.conn_stride[0] == 8; }
 
 

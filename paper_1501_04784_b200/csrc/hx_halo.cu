@@ -398,6 +398,37 @@ halo_unpack_kernel(const int64_t *__restrict__ recv, const int64_t *__restrict__
     }
 }
 
+// Received records as compact element segments (hx_halo_index): thread per record -- its 8 ids as
+// the segment's connectivity row, the word index of its first value in recv, its owned-entry mask.
+__global__ void __launch_bounds__(256)
+halo_index_kernel(const int64_t *__restrict__ recv, const int64_t *__restrict__ src_desc, int world, int self,
+                  const int64_t *__restrict__ bounds, int64_t n_rec, const int64_t *__restrict__ voff,
+                  int32_t *__restrict__ conn, int64_t *__restrict__ ke_offset, uint64_t *__restrict__ ke_mask) {
+    __shared__ SrcTable tb;
+    load_src_table(tb, src_desc, world);
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_rec; i += (int64_t)gridDim.x * blockDim.x) {
+        const int s = src_of(tb, i, world);
+        const int64_t *ids = recv + tb.off[s] + 4 * (i - tb.rec_start[s]);
+        // 8-byte loads: a source chunk starts at any word (its value count can be odd)
+        const int64_t w0 = ids[0], w1 = ids[1], w2 = ids[2], w3 = ids[3];
+        const int32_t g[8] = {(int32_t)(w0 & 0xffffffff), (int32_t)(w0 >> 32), (int32_t)(w1 & 0xffffffff),
+                              (int32_t)(w1 >> 32), (int32_t)(w2 & 0xffffffff), (int32_t)(w2 >> 32),
+                              (int32_t)(w3 & 0xffffffff), (int32_t)(w3 >> 32)};
+        int o[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) o[q] = halo_owner(g[q], bounds, world);
+        uint64_t m = 0;
+#pragma unroll
+        for (int p = 0; p < 36; ++p)
+            if (min(o[pack_i(p)], o[pack_j(p)]) == self) m |= 1ull << p;
+        int4 *c4 = reinterpret_cast<int4 *>(conn + 8 * i);
+        c4[0] = make_int4(g[0], g[1], g[2], g[3]);
+        c4[1] = make_int4(g[4], g[5], g[6], g[7]);
+        ke_offset[i] = tb.off[s] + 4 * tb.nrec[s] + (voff[i] - tb.val_start[s]);
+        ke_mask[i] = m;
+    }
+}
+
 // ---- digest ----------------------------------------------------------------------------------------
 __host__ __device__ __forceinline__ uint64_t digest_mix(uint64_t x) {
     x += 0x9e3779b97f4a7c15ull;
@@ -545,6 +576,35 @@ extern "C" int hx_halo_unpack(const int64_t *recv, const int64_t *src_desc, int3
     HX_TRY_CUDA(cub::DeviceScan::ExclusiveSum(cub_tmp, cb, kbuf, voff, (int)n_rec, s));
     halo_unpack_kernel<<<blocks, 256, 0, s>>>(recv, src_desc, world, self, col_bounds, n_rec, voff, records);
     HX_CHECK_LAUNCH("halo_unpack_kernel");
+    return HX_OK;
+}
+
+extern "C" int hx_halo_index(const int64_t *recv, const int64_t *src_desc, int32_t world, int32_t self,
+                             const int64_t *col_bounds, int64_t n_rec, int32_t *conn, int64_t *ke_offset,
+                             uint64_t *ke_mask, void *workspace, int64_t workspace_bytes, void *stream) {
+    if (world < 1 || world > HALO_MAX_WORLD || self < 0 || self >= world || n_rec < 0 || src_desc == nullptr ||
+        col_bounds == nullptr ||
+        (n_rec > 0 && (recv == nullptr || conn == nullptr || ke_offset == nullptr || ke_mask == nullptr))) {
+        set_last_error("hx_halo_index: bad arguments");
+        return HX_ERR_VALUE;
+    }
+    if (n_rec == 0) return HX_OK;
+    const int64_t need = hx_halo_unpack_workspace_bytes(n_rec);
+    if (need < 0 || workspace == nullptr || workspace_bytes < need) {
+        set_last_error("hx_halo_index: workspace too small");
+        return HX_ERR_WORKSPACE;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    int64_t *kbuf = (int64_t *)workspace, *voff = kbuf + n_rec;
+    void *cub_tmp = (char *)workspace + align_up(16 * (size_t)n_rec, 256);
+    size_t cb = (size_t)workspace_bytes - align_up(16 * (size_t)n_rec, 256);
+    const unsigned blocks = (unsigned)std::min<int64_t>(ceil_div(n_rec, 256), 148 * 8);
+    halo_unpack_count_kernel<<<blocks, 256, 0, s>>>(recv, src_desc, world, self, col_bounds, n_rec, kbuf);
+    HX_CHECK_LAUNCH("halo_unpack_count_kernel");
+    HX_TRY_CUDA(cub::DeviceScan::ExclusiveSum(cub_tmp, cb, kbuf, voff, (int)n_rec, s));
+    halo_index_kernel<<<blocks, 256, 0, s>>>(recv, src_desc, world, self, col_bounds, n_rec, voff, conn, ke_offset,
+                                             ke_mask);
+    HX_CHECK_LAUNCH("halo_index_kernel");
     return HX_OK;
 }
 

@@ -19,7 +19,7 @@ from . import _native as N
 from .errors import ConfigurationError, DegenerateElementError, MeshValidationError, NativeLibraryError, NodeIndexError
 
 __all__ = [
-    "DeviceMesh", "DeviceCsc", "AssemblyPrep", "new_assembly_prep", "rows_narrow", "require_device", "stream_handle", "integrate_mesh", "stiffness_batch",
+    "DeviceMesh", "DeviceCsc", "CompactSegment", "AssemblyPrep", "new_assembly_prep", "rows_narrow", "require_device", "stream_handle", "integrate_mesh", "stiffness_batch",
     "connectivity_index_arrays", "dof_index_arrays", "assemble_dof", "raise_if_failed", "mesh_csc", "triplet_csc", "MeshPlan", "mesh_plan_async",
     "mesh_emit", "integrate_emit", "plan_result", "plan_assembly", "block_elements", "generate_cube_mesh",
 ]
@@ -298,6 +298,25 @@ def assemble_dof(conn: torch.Tensor, values: torch.Tensor, n_nodes: int, dofxn: 
 
 
 @dataclass
+class CompactSegment:
+    """An element segment whose KE rows are compact (received halo records, hx_halo_index): element
+    e's owned packed entries (bit p of kmask[e]) at values[koff[e] + rank of p] -- see
+    hx_elem_segment.ke_offset / ke_mask.  conn (n, 8) int32, koff / kmask (n,) int64."""
+
+    conn: torch.Tensor
+    values: torch.Tensor
+    koff: torch.Tensor
+    kmask: torch.Tensor
+
+    def slice(self, a: int, b: int) -> "CompactSegment":
+        return CompactSegment(self.conn[a:b], self.values, self.koff[a:b], self.kmask[a:b])
+
+    @property
+    def n_el(self) -> int:
+        return self.conn.shape[0]
+
+
+@dataclass
 class DeviceCsc:
     """Lower-triangular CSC block in HBM: col_ptr (ncols+1) i64, row_idx (nnz) i64, vals (nnz) f64."""
 
@@ -388,14 +407,27 @@ def mesh_csc(parts, n_nodes: int, col_lo: int = 0, col_hi: int | None = None, st
     col_hi = n_nodes if col_hi is None else col_hi
     if not 1 <= len(parts) <= N.MAX_SEGMENTS:
         raise ValueError(f"1..{N.MAX_SEGMENTS} element segments required")
-    dev = parts[0][0].device
-    for conn, ke in parts:
-        _check_segment(conn, ke)
-    n_total = sum(int(c.shape[0]) for c, _ in parts)
+    def seg_conn(p):
+        return p.conn if isinstance(p, CompactSegment) else p[0]
+
+    dev = seg_conn(parts[0]).device
+    descs = []
+    for p in parts:
+        if isinstance(p, CompactSegment):
+            n = p.conn.shape[0]
+            if (p.conn.dtype != torch.int32 or tuple(p.conn.shape) != (n, 8) or p.conn.stride(1) != 1
+                    or p.koff.shape[0] != n or p.kmask.shape[0] != n or p.values.dtype != torch.float64):
+                raise ValueError("compact segment: conn (n, 8) int32, koff / kmask (n,), float64 values")
+            descs.append((p.conn.data_ptr(), p.values.data_ptr(), n, _row_stride(p.conn, 8), 0, p.koff.data_ptr(),
+                          p.kmask.data_ptr()))
+        else:
+            c, k = p
+            _check_segment(c, k)
+            descs.append((c.data_ptr(), k.data_ptr(), int(c.shape[0]), _row_stride(c, 8), _row_stride(k, 36)))
+    n_total = sum(int(d[2]) for d in descs)
     ncols = col_hi - col_lo
-    segs = N.segments([(c.data_ptr(), k.data_ptr(), int(c.shape[0]), _row_stride(c, 8), _row_stride(k, 36))
-                       for c, k in parts])
-    flags = _order_flags(order, parts[0][0], n_nodes)
+    segs = N.segments(descs)
+    flags = _order_flags(order, seg_conn(parts[0]), n_nodes)
     ws_bytes = N.lib().hx_mesh_csc_workspace_bytes(n_total, ncols)
     if ws_bytes < 0:
         raise ValueError("bad mesh size")
@@ -614,8 +646,17 @@ def block_elements(dm: DeviceMesh, col_lo: int, col_hi: int, ids=None, ws=None, 
     return ids[:m], conn, coeff
 
 
+def _dense_rows(seg: CompactSegment) -> torch.Tensor:
+    """(n, 36) float64 rows of a compact segment (entries it does not hold are 0)."""
+    bits = (seg.kmask[:, None] >> torch.arange(36, device=seg.kmask.device)) & 1
+    idx = seg.koff[:, None] + torch.cumsum(bits, dim=1) - 1
+    return torch.where(bits.bool(), seg.values[idx.clamp(min=0)], torch.zeros((), dtype=torch.float64,
+                                                                              device=seg.values.device))
+
+
 def _mesh_csc_generic(parts, n_nodes, col_lo, col_hi, stream) -> DeviceCsc:
     rows_l, cols_l, vals_l = [], [], []
+    parts = [(p.conn, _dense_rows(p)) if isinstance(p, CompactSegment) else p for p in parts]
     for conn, ke in parts:
         r, c = connectivity_index_arrays(conn.contiguous(), stream=stream)
         rows_l.append(r)

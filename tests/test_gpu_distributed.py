@@ -128,6 +128,14 @@ def test_halo_pack_unpack_words_match_oracle(world, kind):
             recs = ops.halo_unpack(send, desc, bdev, world, d, int(want[d, 0])).cpu().numpy()
             ref = halo.unpack(got, desc, bounds, world, d)
             assert recs.tobytes() == ref.tobytes()
+            seg = ops.halo_index(send, desc, bdev, world, d, int(want[d, 0]))
+            c_ref, o_ref, m_ref = halo.index(got, desc, bounds, world, d)
+            assert np.array_equal(seg.conn.cpu().numpy(), c_ref) and np.array_equal(seg.koff.cpu().numpy(), o_ref)
+            assert np.array_equal(seg.kmask.cpu().numpy().view(np.uint64), m_ref)
+            # the compact view holds exactly the unpacked records' KE rows
+            from paper_1501_04784_b200.device import _dense_rows
+
+            assert _dense_rows(seg).cpu().numpy().tobytes() == ref[:, :36].tobytes()
 
 
 def test_digest_matches_host_restatement():
@@ -190,3 +198,48 @@ def test_column_touch_matches_oracle(kind):
     for bins in (1, 7, 300, mesh.n_nodes):
         got = ops.column_touch(dm, mesh.n_nodes, bins).cpu().numpy()
         assert np.array_equal(got, halo.column_touch(mesh.connectivity, mesh.n_nodes, bins))
+
+
+def test_compact_segments_assemble_like_dense_records():
+    """mesh_csc over compact received segments (ke_offset / ke_mask) equals the same assembly over
+    unpacked 40-word records, bitwise -- the fast path and the generic fallback (forced by a node of
+    valence > 8)."""
+    from oracle import halo
+    from paper_1501_04784_b200.distributed import balanced_bounds, element_ranges, histogram_bins, record_segment
+
+    for mesh in (permuted_mesh(perturbed_mesh(10, seed=5), seed=6), _valence9_mesh()):
+        world = 3
+        ops = CudaOps()
+        hist = halo.column_weights(mesh.connectivity, mesh.n_nodes, histogram_bins(mesh.n_nodes))
+        bounds = balanced_bounds(hist, mesh.n_nodes, world)
+        bdev = ops.bounds(bounds)
+        ke = np.random.default_rng(1).standard_normal((mesh.n_el, 36))
+        lo, hi = element_ranges(mesh.n_el, world)[0]
+        dm = ops.upload(mesh.coords, mesh.connectivity[lo:hi], mesh.coefficient[lo:hi])
+        per_dest, ws = ops.halo_count(dm, bdev, world, 0)
+        want = halo.count(mesh.connectivity[lo:hi], bounds, world, 0)
+        chunks = 4 * want[:, 0] + want[:, 1]
+        send = ops.alloc_words(int(chunks.sum()))
+        offs = np.concatenate([[0], np.cumsum(chunks)[:-1]])
+        ops.halo_pack(dm, torch.from_numpy(ke[lo:hi]).cuda(), bdev, world, 0,
+                      *ops.pointers([send.data_ptr()] * world, offs), ws)
+        d = 2
+        desc = np.zeros((world, 3), np.int64)
+        desc[0] = (offs[d], want[d, 0], want[d, 1])
+        n = int(want[d, 0])
+        recs = ops.halo_unpack(send, desc, bdev, world, d, n).clone()
+        seg = ops.halo_index(send, desc, bdev, world, d, n)
+        c_lo, c_hi = int(bounds[d]), int(bounds[d + 1])
+        a = D.mesh_csc([record_segment(recs)], mesh.n_nodes, c_lo, c_hi)
+        b = D.mesh_csc([seg], mesh.n_nodes, c_lo, c_hi)
+        for x, y in ((a.col_ptr, b.col_ptr), (a.row_idx, b.row_idx), (a.vals, b.vals)):
+            assert x.cpu().numpy().tobytes() == y.cpu().numpy().tobytes()
+
+
+def _valence9_mesh():
+    """A perturbed mesh whose element 0 is duplicated: its nodes get valence 9 (generic path)."""
+    from paper_1501_04784_b200.mesh import Mesh
+
+    m = perturbed_mesh(6, seed=8)
+    conn = np.concatenate([m.connectivity, m.connectivity[:1]])
+    return Mesh(m.coords, conn, np.concatenate([m.coefficient, m.coefficient[:1]]))
