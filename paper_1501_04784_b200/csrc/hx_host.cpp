@@ -23,6 +23,120 @@ void set_last_error(const char *fmt, ...);
 
 namespace {
 
+// min and max of an element's 8 node ids (one 256-bit load on AVX2 hosts)
+__attribute__((target("avx2"))) inline void minmax8_avx2(const int32_t *g, int32_t &mn, int32_t &mx) {
+    const __m256i v = _mm256_loadu_si256(reinterpret_cast<const __m256i *>(g));
+    __m128i lo = _mm_min_epi32(_mm256_castsi256_si128(v), _mm256_extracti128_si256(v, 1));
+    __m128i hi = _mm_max_epi32(_mm256_castsi256_si128(v), _mm256_extracti128_si256(v, 1));
+    lo = _mm_min_epi32(lo, _mm_shuffle_epi32(lo, 0x4E));
+    hi = _mm_max_epi32(hi, _mm_shuffle_epi32(hi, 0x4E));
+    lo = _mm_min_epi32(lo, _mm_shuffle_epi32(lo, 0xB1));
+    hi = _mm_max_epi32(hi, _mm_shuffle_epi32(hi, 0xB1));
+    mn = _mm_cvtsi128_si32(lo);
+    mx = _mm_cvtsi128_si32(hi);
+}
+
+inline void minmax8_scalar(const int32_t *g, int32_t &mn, int32_t &mx) {
+    mn = mx = g[0];
+    for (int k = 1; k < 8; ++k) {
+        mn = std::min(mn, g[k]);
+        mx = std::max(mx, g[k]);
+    }
+}
+
+// Elements [a, z) of the block-range scan: per block the first / one-past-last element whose node
+// span covers it (L / H), and the chunk's node range.  The same body twice: AVX2 min / max of the 8
+// ids, and scalar.
+__attribute__((target("avx2"))) void scan_chunk_avx2(const int32_t *conn, int64_t a, int64_t z,
+                                                     const int64_t *bounds, int K, int64_t *L, int64_t *H,
+                                                     int32_t &chunk_min, int32_t &chunk_max) {
+    auto block_of = [&](int64_t node) -> int {
+        const int64_t *it = std::upper_bound(bounds + 1, bounds + K, node);
+        return (int)(it - (bounds + 1));
+    };
+    // consecutive elements of a locally numbered mesh stay in one block span: cache the last
+    // element's block bounds and binary-search only when a node leaves them
+    int b0 = 0, b1 = 0;
+    int64_t lo0 = INT64_MAX, hi0 = INT64_MIN, lo1 = INT64_MAX, hi1 = INT64_MIN;
+    // runs of consecutive elements with the same block span update L / H once per run
+    int rb0 = -1, rb1 = -1;
+    int64_t run_start = a;
+    auto close_run = [&](int64_t run_end) {
+        for (int b = rb0; b <= rb1 && rb0 >= 0; ++b) {
+            if (L[b] == INT64_MAX) L[b] = run_start;  // elements of a chunk come in ascending order
+            H[b] = run_end;
+        }
+    };
+    for (int64_t e = a; e < z; ++e) {
+        int32_t mn, mx;
+        minmax8_avx2(conn + 8 * e, mn, mx);
+        chunk_min = std::min(chunk_min, mn);
+        chunk_max = std::max(chunk_max, mx);
+        if (mn < lo0 || mn >= hi0) {
+            b0 = block_of(mn);
+            lo0 = b0 == 0 ? INT64_MIN : bounds[b0];
+            hi0 = b0 == K - 1 ? INT64_MAX : bounds[b0 + 1];
+        }
+        if (mx < lo1 || mx >= hi1) {
+            b1 = block_of(mx);
+            lo1 = b1 == 0 ? INT64_MIN : bounds[b1];
+            hi1 = b1 == K - 1 ? INT64_MAX : bounds[b1 + 1];
+        }
+        if (b0 != rb0 || b1 != rb1) {
+            close_run(e);
+            rb0 = b0;
+            rb1 = b1;
+            run_start = e;
+        }
+    }
+    close_run(z);
+}
+
+void scan_chunk_scalar(const int32_t *conn, int64_t a, int64_t z, const int64_t *bounds, int K, int64_t *L,
+                       int64_t *H, int32_t &chunk_min, int32_t &chunk_max) {
+    auto block_of = [&](int64_t node) -> int {
+        const int64_t *it = std::upper_bound(bounds + 1, bounds + K, node);
+        return (int)(it - (bounds + 1));
+    };
+    // consecutive elements of a locally numbered mesh stay in one block span: cache the last
+    // element's block bounds and binary-search only when a node leaves them
+    int b0 = 0, b1 = 0;
+    int64_t lo0 = INT64_MAX, hi0 = INT64_MIN, lo1 = INT64_MAX, hi1 = INT64_MIN;
+    // runs of consecutive elements with the same block span update L / H once per run
+    int rb0 = -1, rb1 = -1;
+    int64_t run_start = a;
+    auto close_run = [&](int64_t run_end) {
+        for (int b = rb0; b <= rb1 && rb0 >= 0; ++b) {
+            if (L[b] == INT64_MAX) L[b] = run_start;  // elements of a chunk come in ascending order
+            H[b] = run_end;
+        }
+    };
+    for (int64_t e = a; e < z; ++e) {
+        int32_t mn, mx;
+        minmax8_scalar(conn + 8 * e, mn, mx);
+        chunk_min = std::min(chunk_min, mn);
+        chunk_max = std::max(chunk_max, mx);
+        if (mn < lo0 || mn >= hi0) {
+            b0 = block_of(mn);
+            lo0 = b0 == 0 ? INT64_MIN : bounds[b0];
+            hi0 = b0 == K - 1 ? INT64_MAX : bounds[b0 + 1];
+        }
+        if (mx < lo1 || mx >= hi1) {
+            b1 = block_of(mx);
+            lo1 = b1 == 0 ? INT64_MIN : bounds[b1];
+            hi1 = b1 == K - 1 ? INT64_MAX : bounds[b1 + 1];
+        }
+        if (b0 != rb0 || b1 != rb1) {
+            close_run(e);
+            rb0 = b0;
+            rb1 = b1;
+            run_start = e;
+        }
+    }
+    close_run(z);
+}
+
+
 void widen_scalar(const int32_t *src, int64_t *dst, int64_t n) {
     for (int64_t i = 0; i < n; ++i) dst[i] = src[i];
 }
@@ -252,6 +366,7 @@ extern "C" int hx_block_ranges_nodes(const int32_t *conn, int64_t n_el, const in
         return (int)(it - (bounds + 1));
     };
     const int hw = (int)std::max(1u, std::thread::hardware_concurrency());
+    static const bool avx2 = __builtin_cpu_supports("avx2");
     const int64_t per = int64_t(1) << 20;
     const int64_t chunks = (n_el + per - 1) / per;
     const int nt = (int)std::max<int64_t>(1, std::min<int64_t>(threads > 0 ? threads : hw, chunks));
@@ -269,35 +384,9 @@ extern "C" int hx_block_ranges_nodes(const int32_t *conn, int64_t n_el, const in
         int64_t *L = Lv.data(), *H = Hv.data();
         for (int64_t c = next.fetch_add(1); c < chunks; c = next.fetch_add(1)) {
             const int64_t a = c * per, z = std::min(n_el, a + per);
-            // consecutive elements of a locally numbered mesh stay in one block span: cache the last
-            // element's block bounds and binary-search only when a node leaves them
-            int b0 = 0, b1 = 0;
-            int64_t lo0 = INT64_MAX, hi0 = INT64_MIN, lo1 = INT64_MAX, hi1 = INT64_MIN;
             int32_t chunk_min = INT32_MAX, chunk_max = INT32_MIN;
-            for (int64_t e = a; e < z; ++e) {
-                const int32_t *g = conn + 8 * e;
-                int32_t mn = g[0], mx = g[0];
-                for (int k = 1; k < 8; ++k) {
-                    mn = std::min(mn, g[k]);
-                    mx = std::max(mx, g[k]);
-                }
-                chunk_min = std::min(chunk_min, mn);
-                chunk_max = std::max(chunk_max, mx);
-                if (mn < lo0 || mn >= hi0) {
-                    b0 = block_of(mn);
-                    lo0 = b0 == 0 ? INT64_MIN : bounds[b0];
-                    hi0 = b0 == K - 1 ? INT64_MAX : bounds[b0 + 1];
-                }
-                if (mx < lo1 || mx >= hi1) {
-                    b1 = block_of(mx);
-                    lo1 = b1 == 0 ? INT64_MIN : bounds[b1];
-                    hi1 = b1 == K - 1 ? INT64_MAX : bounds[b1 + 1];
-                }
-                for (int b = b0; b <= b1; ++b) {
-                    if (L[b] == INT64_MAX) L[b] = e;  // elements of a chunk come in ascending order
-                    H[b] = e + 1;
-                }
-            }
+            if (avx2) scan_chunk_avx2(conn, a, z, bounds, K, L, H, chunk_min, chunk_max);
+            else scan_chunk_scalar(conn, a, z, bounds, K, L, H, chunk_min, chunk_max);
             cmin[c] = chunk_min;
             cmax[c] = chunk_max;
         }
