@@ -316,6 +316,15 @@ int hx_block_ranges(const int32_t *conn, int64_t n_el, const int64_t *bounds, in
 /* as hx_block_ranges, plus node_lo / node_hi (n_blocks each): a node range [node_lo, node_hi) that
  * holds every node the elements [e_lo[k], e_hi[k]) reference (bounded per chunk of 2^20 elements;
  * the streamed build uploads the coordinates as prefixes ahead of each block).  HOST code. */
+/* a predicted plan from every step-th element (the streamed run_build's fast start), checked on the
+ * device by hx_block_verify: element e0 + i (i < n, conn = the block's uploaded range) must lie in the
+ * predicted range of every block its node span covers and reference only nodes below node_top;
+ * failures set *flag (1: range, 2: coordinates) and the caller rebuilds with the exact scan. */
+int hx_block_ranges_sampled(const int32_t *conn, int64_t n_el, const int64_t *bounds, int32_t n_blocks, int64_t step,
+                            int64_t *e_lo, int64_t *e_hi, int64_t *node_hi, int32_t threads);
+int hx_block_verify(const int32_t *conn, int64_t n, int64_t e0, int64_t n_nodes, const int64_t *bounds,
+                    int32_t n_blocks, const int64_t *e_lo, const int64_t *e_hi, int64_t node_top, uint32_t *flag,
+                    void *stream);
 int hx_block_ranges_nodes(const int32_t *conn, int64_t n_el, const int64_t *bounds, int32_t n_blocks, int64_t *e_lo,
                           int64_t *e_hi, int64_t *node_lo, int64_t *node_hi, int32_t threads);
 

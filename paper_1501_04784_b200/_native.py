@@ -40,7 +40,7 @@ EXPORTED = (
     "hx_column_weights", "hx_column_touch", "hx_halo_workspace_bytes", "hx_halo_count", "hx_halo_pack",
     "hx_halo_unpack_workspace_bytes", "hx_halo_unpack", "hx_halo_index", "hx_digest",
     "hx_ipc_alloc", "hx_ipc_open", "hx_ipc_close", "hx_ipc_free",
-    "hx_block_select_workspace_bytes", "hx_block_select", "hx_block_gather", "hx_block_ranges", "hx_block_ranges_nodes",
+    "hx_block_select_workspace_bytes", "hx_block_select", "hx_block_gather", "hx_block_ranges", "hx_block_ranges_nodes", "hx_block_ranges_sampled", "hx_block_verify",
     "hx_mm_write", "hx_mm_read", "hx_generate_cube_mesh", "hx_rows_narrow", "hx_rows_widen", "hx_peek",
     "hx_rows_encode_workspace_bytes", "hx_rows_encode", "hx_rows_decode",
 )
@@ -131,6 +131,8 @@ def lib():
         "hx_block_gather": ([P, P, P, P, I64, P, P, P], ctypes.c_int),
         "hx_block_ranges": ([P, I64, P, I32, P, P, I32], ctypes.c_int),
         "hx_block_ranges_nodes": ([P, I64, P, I32, P, P, P, P, I32], ctypes.c_int),
+        "hx_block_ranges_sampled": ([P, I64, P, I32, I64, P, P, P, I32], ctypes.c_int),
+        "hx_block_verify": ([P, I64, I64, I64, P, I32, P, P, I64, P, P], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)

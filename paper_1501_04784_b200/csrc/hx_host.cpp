@@ -416,3 +416,74 @@ extern "C" int hx_block_ranges_nodes(const int32_t *conn, int64_t n_el, const in
     }
     return HX_OK;
 }
+
+// A streaming plan from every step-th element (the streamed run_build's fast start: ~1/step of the
+// connectivity read instead of all of it).  Block k's predicted element range extends one sample
+// before its first touching sample and two after its last; its coordinate prefix covers those
+// samples' nodes.  A prediction, not a superset: hx_block_verify checks every element on the device
+// and the caller falls back to hx_block_ranges_nodes when it fails.  HOST code.
+extern "C" int hx_block_ranges_sampled(const int32_t *conn, int64_t n_el, const int64_t *bounds, int32_t n_blocks,
+                                       int64_t step, int64_t *e_lo, int64_t *e_hi, int64_t *node_hi,
+                                       int32_t threads) {
+    if (n_el < 0 || n_blocks < 1 || step < 1 || bounds == nullptr || e_lo == nullptr || e_hi == nullptr ||
+        node_hi == nullptr || (n_el > 0 && conn == nullptr)) {
+        hx::set_last_error("hx_block_ranges_sampled: bad arguments");
+        return HX_ERR_VALUE;
+    }
+    const int K = n_blocks;
+    const int64_t ns = n_el > 0 ? (n_el - 1) / step + 1 : 0;  // samples 0, step, 2 step, ..., and n_el - 1
+    std::vector<int32_t> smax(ns + 1, INT32_MIN);
+    // each sample is one cache line (and usually one page walk) away from the last: latency-bound, so
+    // the samples are split over threads, each with its own first / last sample per block
+    const int hw = (int)std::max(1u, std::thread::hardware_concurrency());
+    const int T = (int)std::max<int64_t>(1, std::min<int64_t>({threads > 0 ? threads : hw, hw, (ns + 1) / 4096 + 1}));
+    std::vector<int64_t> first((size_t)T * K, -1), last((size_t)T * K, -1);
+    auto work = [&](int t) {
+        const int64_t i_lo = (ns + 1) * t / T, i_hi = (ns + 1) * (t + 1) / T;
+        int64_t *f = first.data() + (size_t)t * K, *l = last.data() + (size_t)t * K;
+        for (int64_t i = i_lo; i < i_hi && n_el > 0; ++i) {
+            const int64_t e = std::min(i * step, n_el - 1);
+            const int32_t *g = conn + 8 * e;
+            int32_t mn = g[0], mx = g[0];
+            for (int k = 1; k < 8; ++k) {
+                mn = std::min(mn, g[k]);
+                mx = std::max(mx, g[k]);
+            }
+            smax[i] = mx;
+            const int b0 = (int)(std::upper_bound(bounds + 1, bounds + K, (int64_t)mn) - (bounds + 1));
+            const int b1 = (int)(std::upper_bound(bounds + 1, bounds + K, (int64_t)mx) - (bounds + 1));
+            for (int b = b0; b <= b1; ++b) {
+                if (f[b] < 0) f[b] = i;
+                l[b] = i;
+            }
+        }
+    };
+    if (T == 1) {
+        work(0);
+    } else {
+        std::vector<std::thread> pool;
+        for (int t = 0; t < T; ++t) pool.emplace_back(work, t);
+        for (auto &th : pool) th.join();
+    }
+    for (int b = 0; b < K; ++b) {
+        int64_t fb = -1, lb = -1;
+        for (int t = 0; t < T; ++t) {  // threads hold ascending sample ranges
+            const int64_t f = first[(size_t)t * K + b], l = last[(size_t)t * K + b];
+            if (f >= 0 && fb < 0) fb = f;
+            if (l >= 0) lb = l;
+        }
+        if (fb < 0) {
+            e_lo[b] = e_hi[b] = node_hi[b] = 0;
+            continue;
+        }
+        const int64_t i0 = std::max<int64_t>(fb - 1, 0), i1 = std::min<int64_t>(lb + 2, ns);
+        e_lo[b] = std::min(i0 * step, n_el);
+        e_hi[b] = std::min((i1 + 1) * step, n_el);
+        // nodes up to the sample after the range (elements between the last two samples lie below it
+        // on a locally numbered mesh; hx_block_verify checks the rest)
+        int32_t top = INT32_MIN;
+        for (int64_t i = i0; i <= std::min(i1 + 1, ns); ++i) top = std::max(top, smax[i]);
+        node_hi[b] = (int64_t)top + 1;
+    }
+    return HX_OK;
+}

@@ -42,6 +42,33 @@ __global__ void block_gather_kernel(const int32_t *__restrict__ conn, const doub
     }
 }
 
+// Check of a sampled streaming plan (hx_block_ranges_sampled) on the device: every element of block
+// k's uploaded range (global ids e0 + i) must lie inside the predicted element range of every column
+// block its node span covers, and its nodes below the block's coordinate prefix -- else *flag != 0 and
+// the caller rebuilds with the exact host scan.  bounds (K + 1), e_lo / e_hi (K) device int64.
+__global__ void block_verify_kernel(const int32_t *__restrict__ conn, int64_t n, int64_t e0, int64_t n_nodes,
+                                    const int64_t *__restrict__ bounds, int K, const int64_t *__restrict__ e_lo,
+                                    const int64_t *__restrict__ e_hi, int64_t node_top,
+                                    unsigned *__restrict__ flag) {
+    unsigned bad = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int4 *c4 = reinterpret_cast<const int4 *>(conn + 8 * i);
+        const int4 lo = __ldg(c4), hi = __ldg(c4 + 1);
+        const int mn = min(min(min(lo.x, lo.y), min(lo.z, lo.w)), min(min(hi.x, hi.y), min(hi.z, hi.w)));
+        const int mx = max(max(max(lo.x, lo.y), max(lo.z, lo.w)), max(max(hi.x, hi.y), max(hi.z, hi.w)));
+        if ((int64_t)mx >= node_top && (int64_t)mx < n_nodes) bad |= 2u;  // a coordinate not uploaded yet
+        int b0 = 0, b1 = 0;  // blocks of mn / mx, clamped like hx_block_ranges
+        for (int b = 1; b < K; ++b) {
+            b0 += (int64_t)mn >= __ldg(bounds + b);
+            b1 += (int64_t)mx >= __ldg(bounds + b);
+        }
+        const int64_t e = e0 + i;
+        for (int b = b0; b <= b1; ++b)
+            if (e < __ldg(e_lo + b) || e >= __ldg(e_hi + b)) bad |= 1u;
+    }
+    if (bad) atomicOr(flag, bad);
+}
+
 }  // namespace hx
 
 using namespace hx;
@@ -136,5 +163,21 @@ extern "C" int hx_generate_cube_mesh(int64_t nx, int64_t ny, int64_t nz, double 
     cube_elements_kernel<<<(unsigned)std::min<int64_t>(ceil_div(n_el, 256), 148 * 32), 256, 0, s>>>(nx, ny, n_el, c0,
                                                                                                   conn, coeff);
     HX_CHECK_LAUNCH("cube_elements_kernel");
+    return HX_OK;
+}
+
+extern "C" int hx_block_verify(const int32_t *conn, int64_t n, int64_t e0, int64_t n_nodes, const int64_t *bounds,
+                               int32_t n_blocks, const int64_t *e_lo, const int64_t *e_hi, int64_t node_top,
+                               uint32_t *flag, void *stream) {
+    if (n < 0 || n_blocks < 1 || bounds == nullptr || e_lo == nullptr || e_hi == nullptr || flag == nullptr ||
+        (n > 0 && conn == nullptr)) {
+        set_last_error("hx_block_verify: bad arguments");
+        return HX_ERR_VALUE;
+    }
+    if (n == 0) return HX_OK;
+    const unsigned blocks = (unsigned)std::min<int64_t>(ceil_div(n, 256), 148 * 8);
+    block_verify_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(conn, n, e0, n_nodes, bounds, n_blocks, e_lo, e_hi,
+                                                                  node_top, flag);
+    HX_CHECK_LAUNCH("block_verify_kernel");
     return HX_OK;
 }

@@ -108,6 +108,40 @@ def plan(mesh, n_blocks: int, threads: int | None = None) -> StreamPlan | None:
     return StreamPlan(bounds, e_lo, e_hi, np.maximum.accumulate(np.minimum(n_hi, n_nodes)))
 
 
+SAMPLE_STEP = 256  # the sampled plan reads every 256th element's connectivity row
+
+
+def sampled_plan(mesh, n_blocks: int, step: int | None = None, threads: int | None = None) -> StreamPlan | None:
+    """A predicted plan from every step-th element (hx_block_ranges_sampled): ~1/step of the host
+    scan's reads.  The streamed build checks it on the device (hx_block_verify) and rebuilds with
+    the exact plan when an element falls outside it.  None when it does not cover every element or
+    the numbering has no locality."""
+    n_nodes, n_el = mesh.n_nodes, mesh.n_el
+    n_blocks = int(max(1, min(n_blocks, n_nodes)))
+    if n_el == 0 or not looks_local(mesh.connectivity, n_nodes):
+        return None
+    if step is None:  # a few steps of slack per block stay a small fraction of the block
+        step = int(max(1, min(SAMPLE_STEP, n_el // (64 * n_blocks))))
+    bounds = stream_bounds(n_nodes, n_blocks)
+    conn = np.ascontiguousarray(mesh.connectivity, dtype=np.int32)
+    e_lo, e_hi, n_hi = (np.zeros(n_blocks, dtype=np.int64) for _ in range(3))
+    N.check(N.lib().hx_block_ranges_sampled(conn.ctypes.data, n_el, bounds.ctypes.data, n_blocks, int(step),
+                                            e_lo.ctypes.data, e_hi.ctypes.data, n_hi.ctypes.data,
+                                            host_threads() if threads is None else int(threads)),
+            "hx_block_ranges_sampled")
+    spans = sorted((int(a), int(b)) for a, b in zip(e_lo, e_hi) if b > a)
+    reach = 0
+    for a, b in spans:  # every element must be uploaded (and so checked) by some block
+        if a > reach:
+            return None
+        reach = max(reach, b)
+    if reach < n_el or (e_hi - e_lo).sum() > MAX_RANGE_OVERLAP * n_el + n_blocks:
+        return None
+    sp = StreamPlan(bounds, e_lo, e_hi, np.maximum.accumulate(np.minimum(n_hi, n_nodes)))
+    sp.verify = True
+    return sp
+
+
 def blocks_for_budget(n_el: int, n_nodes: int, budget_bytes: int) -> int:
     """Column blocks so that the coordinates plus three blocks in flight (next upload, current
     build, pending copy-out) fit ``budget_bytes`` of HBM: per block ~344 B per element (conn,
@@ -149,8 +183,11 @@ def streamed_build(mesh, sp, mode: str = "exact", device=None, capacity: int | N
         with torch.cuda.stream(h2d):
             coords = torch.empty(tuple(coords_h.shape), dtype=torch.float64, device=dev)
         coords.record_stream(main)
-        if not isinstance(sp, StreamPlan):  # host scan (element and node ranges of the blocks)
-            sp = plan(mesh, int(sp))
+        if not isinstance(sp, StreamPlan):  # element and node ranges of the blocks
+            k_req = int(sp)
+            sp = sampled_plan(mesh, k_req) if os.environ.get("HX_SAMPLED_PLAN", "1") != "0" else None
+            if sp is None:
+                sp = plan(mesh, k_req)  # the exact host scan
             if sp is None:
                 return None
         K = sp.n_blocks
@@ -159,6 +196,13 @@ def streamed_build(mesh, sp, mode: str = "exact", device=None, capacity: int | N
         # after its slice instead of after the whole array)
         node_hi = sp.node_hi if sp.node_hi is not None else np.full(K, n_nodes, dtype=np.int64)
         coords_up = [0]
+        tops = [n_nodes] * K  # coordinate prefix uploaded when block k computes
+        verify = getattr(sp, "verify", False)
+        if verify:  # the predicted plan is checked element by element on the device
+            vflag = torch.zeros(1, dtype=torch.int32, device=dev)
+            v_bounds = torch.from_numpy(np.ascontiguousarray(sp.bounds, dtype=np.int64)).to(dev)
+            v_lo = torch.from_numpy(np.ascontiguousarray(sp.e_lo, dtype=np.int64)).to(dev)
+            v_hi = torch.from_numpy(np.ascontiguousarray(sp.e_hi, dtype=np.int64)).to(dev)
         out_cp = torch.empty(n_nodes + 1, dtype=torch.int64, pin_memory=True)
         out_rows = torch.empty(max(cap, 1), dtype=torch.int64, pin_memory=True)
         out_vals = torch.empty(max(cap, 1), dtype=torch.float64, pin_memory=True)
@@ -189,6 +233,7 @@ def streamed_build(mesh, sp, mode: str = "exact", device=None, capacity: int | N
                 if top > coords_up[0]:
                     coords[coords_up[0]:top].copy_(coords_h[coords_up[0]:top], non_blocking=True)
                     coords_up[0] = top
+                tops[k] = coords_up[0]
                 conn.copy_(conn_h[lo:hi], non_blocking=True)
                 coeff.copy_(coeff_h[lo:hi], non_blocking=True)
                 ev = h2d.record_event()
@@ -243,6 +288,10 @@ def streamed_build(mesh, sp, mode: str = "exact", device=None, capacity: int | N
                     pending = upload(k + 1)  # next range in flight while this block computes
                 main.wait_event(ready)
                 a, z = int(sp.bounds[k]), int(sp.bounds[k + 1])
+                if verify and conn.shape[0]:
+                    N.check(N.lib().hx_block_verify(D._ptr(conn), conn.shape[0], int(sp.e_lo[k]), n_nodes,
+                                                    D._ptr(v_bounds), K, D._ptr(v_lo), D._ptr(v_hi), tops[k],
+                                                    D._ptr(vflag), D.stream_handle(main)), "hx_block_verify")
                 if conn.shape[0] == 0:
                     cp_np[a + 1:z + 1] = offset
                     continue
@@ -326,6 +375,13 @@ def streamed_build(mesh, sp, mode: str = "exact", device=None, capacity: int | N
             pool.shutdown(wait=True)
         if overflow:
             return None
+        if verify and D.peek(vflag, stream=main)[0] != 0:  # the prediction missed an element: exact plan
+            exact = plan(mesh, K)
+            if exact is None:
+                return None
+            if stats is not None:
+                stats["sampled_plan_fallback"] = True
+            return streamed_build(mesh, exact, mode=mode, device=device, capacity=capacity, stats=stats)
         _raise_lowest(fails, n_nodes)
         if stats is not None:
             stats.update(gpu_s=t_gpu[0].elapsed_time(t_gpu[1]) / 1e3, wall_s=time.perf_counter() - t0, blocks=K,

@@ -965,6 +965,7 @@ def test_streamed_run_build_bitwise(monkeypatch, pinned, blocks):
         m, rep = run_build(mesh, budget_bytes=10**12)
         assert bits_equal(m.col_ptr, cp) and bits_equal(m.row_idx, ri) and bits_equal(m.vals, vv)
         assert rep.nnz_csc == len(ri) and rep.time_integration_s > 0
+        assert not pipeline.LAST_RUN_STATS.get("sampled_plan_fallback")  # the sampled plan held
 
 
 def test_streamed_plan_rejects_permuted_and_overflow_falls_back(monkeypatch):
@@ -980,6 +981,39 @@ def test_streamed_plan_rejects_permuted_and_overflow_falls_back(monkeypatch):
     ke, rows, cols, _, _, _ = oracle.stiffness_mesh(perm.coords, perm.connectivity, perm.coefficient)
     cp, ri, vv = oracle.triplet_to_csc(rows, cols, ke.reshape(-1), perm.n_nodes)
     m, _ = run_build(perm, budget_bytes=10**12)  # one-shot path
+    assert bits_equal(m.col_ptr, cp) and bits_equal(m.row_idx, ri) and bits_equal(m.vals, vv)
+
+
+@pytest.mark.parametrize("miss", ["node_hi", "e_hi"])
+def test_sampled_plan_device_check_falls_back_to_exact_plan(miss):
+    """The sampled plan (every 64th element) is checked element by element on the device
+    (hx_block_verify); a plan that misses an element's block or coordinates is detected and the
+    build reruns with the exact host-scan plan -- bitwise either way."""
+    import copy
+
+    from paper_1501_04784_b200 import stream
+
+    mesh = perturbed_mesh(20, seed=5)
+    ke, rows, cols, _, _, _ = oracle.stiffness_mesh(mesh.coords, mesh.connectivity, mesh.coefficient)
+    cp, ri, vv = oracle.triplet_to_csc(rows, cols, ke.reshape(-1), mesh.n_nodes)
+    sp = stream.sampled_plan(mesh, 4)
+    assert sp is not None and sp.verify
+    stats = {}
+    m = stream.streamed_build(mesh, sp, stats=stats)
+    assert not stats.get("sampled_plan_fallback")
+    assert bits_equal(m.col_ptr, cp) and bits_equal(m.row_idx, ri) and bits_equal(m.vals, vv)
+    bad = copy.copy(stream.plan(mesh, 4))
+    bad.verify = True
+    if miss == "node_hi":  # block 0's halo elements gather coordinates above the uploaded prefix
+        bad.node_hi = bad.node_hi.copy()
+        bad.node_hi[0] = bad.bounds[1]
+    else:  # the last element of block 0's range is uploaded only by block 1
+        bad.e_hi = bad.e_hi.copy()
+        bad.e_hi[0] -= 1
+        assert bad.e_lo[1] <= bad.e_hi[0]
+    stats = {}
+    m = stream.streamed_build(mesh, bad, stats=stats)
+    assert stats.get("sampled_plan_fallback")
     assert bits_equal(m.col_ptr, cp) and bits_equal(m.row_idx, ri) and bits_equal(m.vals, vv)
 
 

@@ -118,6 +118,24 @@ def test_block_ranges_host_scan_matches_numpy():
                     assert n_lo[b] <= max(sub.min(), 0) and n_hi[b] >= sub.max() + 1
 
 
+def test_sampled_plan_covers_the_exact_plan_on_local_meshes():
+    """hx_block_ranges_sampled (every step-th element): on locally numbered meshes the predicted
+    element and node ranges contain the exact scan's; a numbering without locality gets None."""
+    from paper_1501_04784_b200.stream import plan, sampled_plan
+    from paper_1501_04784_b200.workloads import permuted_mesh, perturbed_mesh
+
+    for n, k in ((12, 3), (20, 4), (9, 1)):
+        mesh = perturbed_mesh(n, seed=n)
+        ex, sm = plan(mesh, k), sampled_plan(mesh, k, step=16)
+        assert sm is not None and sm.verify and np.array_equal(sm.bounds, ex.bounds)
+        assert np.all(sm.e_lo <= ex.e_lo) and np.all(sm.e_hi >= ex.e_hi)
+        assert np.all(sm.node_hi <= mesh.n_nodes)
+        for b in range(k):  # the coordinate prefix covers every node the exact range gathers
+            assert sm.node_hi[b] >= mesh.connectivity[ex.e_lo[b]:ex.e_hi[b]].max() + 1
+        assert sm.e_lo.min() == 0 and sm.e_hi.max() == mesh.n_el
+    assert sampled_plan(permuted_mesh(perturbed_mesh(10, seed=1), seed=2), 8) is None
+
+
 def test_stream_bounds_quarter_end_blocks():
     from paper_1501_04784_b200.stream import stream_bounds
 
