@@ -22,6 +22,7 @@
 // distinct rows per column <= HX_MAX_COL_ROWS, no repeated node in an element.  With valence <= 8
 // every duplicate run has <= 8 terms, where numpy's pairwise sum degenerates to the sequential sum
 // implemented here.
+#include <cub/block/block_radix_sort.cuh>
 #include <cub/block/block_scan.cuh>
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
@@ -134,6 +135,62 @@ __global__ void first_element_kernel(int64_t ncols, const int32_t *__restrict__ 
     }
 }
 
+// Strip processing order for banded numberings (lexicographic structured meshes, RCM-like orders):
+// an element's nodes lie up to one band B (~ one node layer) apart, so in column order a KE row's
+// first and last columns are B columns -- a whole element layer of KE -- apart, more than the L2
+// keeps.  Cutting every band-row into strips of W columns and walking strip by strip (row after row
+// inside a strip) brings the two columns W apart.  band_kernel estimates B (median node span of 1024
+// sampled elements) and switches the order on (*order_flag = 2) only when the band holds at least
+// four strips (C4: B = 161k columns, 46 MB of KE per band-row; C3's 41k-column band stays in L2
+// and keeps column order); band_order_kernel writes position -> column.  Any order gives the same CSC.
+constexpr int BAND_SAMPLES = 1024;
+__global__ void __launch_bounds__(256) band_kernel(const int32_t *__restrict__ conn, int64_t n_el, int64_t ncols,
+                                                   int64_t strip, uint32_t *__restrict__ order_flag,
+                                                   int64_t *__restrict__ band) {
+    using Sort = cub::BlockRadixSort<int32_t, 256, BAND_SAMPLES / 256>;
+    __shared__ typename Sort::TempStorage tmp;
+    __shared__ int32_t s_med;
+    int32_t span[BAND_SAMPLES / 256];
+#pragma unroll
+    for (int i = 0; i < BAND_SAMPLES / 256; ++i) {
+        const int64_t e = (int64_t)(threadIdx.x * (BAND_SAMPLES / 256) + i) * n_el / BAND_SAMPLES;
+        const int4 a = __ldg(reinterpret_cast<const int4 *>(conn + 8 * e));
+        const int4 b = __ldg(reinterpret_cast<const int4 *>(conn + 8 * e) + 1);
+        const int32_t mn = min(min(min(a.x, a.y), min(a.z, a.w)), min(min(b.x, b.y), min(b.z, b.w)));
+        const int32_t mx = max(max(max(a.x, a.y), max(a.z, a.w)), max(max(b.x, b.y), max(b.z, b.w)));
+        span[i] = mx - mn;
+    }
+    Sort(tmp).Sort(span);  // blocked arrangement: thread t holds ranks 4t .. 4t + 3
+    if (threadIdx.x == BAND_SAMPLES / 2 / (BAND_SAMPLES / 256)) s_med = span[0];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const int64_t B = (int64_t)s_med;
+        band[0] = B;
+        band[1] = strip;
+        if (B >= 4 * strip && 2 * B <= ncols) *order_flag = 2u;
+    }
+}
+
+// Column at processing position i of the strip order (band[0] = B, band[1] = strip width; columns < 2^31).
+__device__ __forceinline__ int64_t band_col(int64_t i64, int64_t ncols, const int64_t *__restrict__ band) {
+    const uint32_t B = (uint32_t)__ldg(band), strip = (uint32_t)__ldg(band + 1), i = (uint32_t)i64;
+    const uint32_t rows = (uint32_t)ncols / B;
+    if (i >= rows * B) return i64;  // the partial last band-row keeps column order at the end
+    const uint32_t s = i / (rows * strip), rel = i - s * rows * strip;
+    const uint32_t w = min(strip, B - s * strip);
+    const uint32_t z = rel / w;
+    return (int64_t)(z * B + s * strip + (rel - z * w));
+}
+
+// The strip order as an order array (position -> column), read like the element order.  Computing
+// band_col inline in the pattern pass instead measured 1.9 ms slower at C4 (7.8 vs 5.9 ms).
+__global__ void band_order_kernel(int64_t ncols, const uint32_t *__restrict__ order_flag,
+                                  const int64_t *__restrict__ band, uint32_t *__restrict__ order) {
+    if (*order_flag != 2u) return;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < ncols; i += (int64_t)gridDim.x * blockDim.x)
+        order[i] = (uint32_t)band_col(i, ncols, band);
+}
+
 // Sorting network for 8 keys (19 compare-exchanges), padded with INT_MAX.
 __device__ __forceinline__ void cswap(int32_t &a, int32_t &b) {
     const int32_t lo = min(a, b), hi = max(a, b);
@@ -197,6 +254,9 @@ constexpr int MAX_OFFDIAG_CONTRIB = 4;     // hex meshes: an edge is shared by a
 #endif
 #ifndef HX_EMIT_BLOCK
 #define HX_EMIT_BLOCK 128
+#endif
+#ifndef HX_BAND_STRIP_DEFAULT
+#define HX_BAND_STRIP_DEFAULT 16384  // measured best of 4K..64K at C4 (profiles/r02/band_order_sweep.txt)
 #endif
 constexpr int COL_BLOCK = HX_COL_BLOCK;    // columns per tile (pattern: one thread per column)
 constexpr int EMIT_BLOCK = HX_EMIT_BLOCK;  // emit: threads per tile
@@ -375,14 +435,18 @@ pattern_kernel(SegTable T, int64_t col_lo, int64_t ncols, int32_t *__restrict__ 
                int64_t scratch_capacity, unsigned long long *__restrict__ scratch_top,
                int64_t *__restrict__ block_scratch, uint32_t *__restrict__ status,
                const uint32_t *__restrict__ order, unsigned long long *__restrict__ slot_total,
-               int32_t *__restrict__ tile_need, int32_t *__restrict__ tadj, int32_t *__restrict__ tdeg) {
+               int32_t *__restrict__ tile_need, int32_t *__restrict__ tadj, int32_t *__restrict__ tdeg,
+               const uint32_t *__restrict__ order_flag) {
     __shared__ K sL[SORT_SLOTS * COL_BLOCK];  // this thread's contribution keys, [slot][thread]
     __shared__ unsigned long long s_base;
     using BlockScan = cub::BlockScan<int32_t, COL_BLOCK>;
     __shared__ typename BlockScan::TempStorage scan_tmp;
     const int t = threadIdx.x;
     const int64_t idx = (int64_t)blockIdx.x * COL_BLOCK + t;  // position in the processing order
-    const int64_t cl = order != nullptr && idx < ncols ? (int64_t)__ldg(order + idx) : idx;
+    // 0: column order; 1: element order; 2: strip order of a banded numbering (both: the order array)
+    const uint32_t flag = order != nullptr ? __ldg(order_flag) : 0u;
+    if (flag == 0u) order = nullptr;
+    const int64_t cl = flag == 0u || idx >= ncols ? idx : (int64_t)__ldg(order + idx);
     const int32_t c = (int32_t)(col_lo + cl);
     K *L = sL + t;
     int cnt = 0, deg = 0;
@@ -816,6 +880,7 @@ struct MeshWs {
     int32_t *tile_need;  // per tile: 1 + its highest incident element (0: none)
     int32_t *tadj, *tdeg;  // element order only: sorted incident lists / degrees by processing position
     unsigned long long *scratch_top, *slot_total;
+    int64_t *band;  // band_kernel: B and the strip width
     uint32_t *keys_in, *keys_out, *cols_in, *order;
     int2 *scratch;
     int64_t scratch_capacity;
@@ -847,7 +912,7 @@ static MeshWs mesh_ws_layout(void *base, int64_t ncols, int64_t workspace_bytes 
     const size_t o_bs = take(sizeof(int64_t) * std::max<int64_t>(1, ceil_div(ncols, COL_BLOCK)));
     const size_t o_tn = take(sizeof(int32_t) * std::max<int64_t>(1, ceil_div(ncols, COL_BLOCK)));
     const size_t o_ta = take(sizeof(int32_t) * 8 * nc), o_td = take(sizeof(int32_t) * nc);
-    const size_t o_st = take(2 * sizeof(unsigned long long));  // scratch_top, slot_total
+    const size_t o_st = take(4 * sizeof(unsigned long long));  // scratch_top, slot_total, band[2]
     const size_t o_ki = take(sizeof(uint32_t) * nc), o_ko = take(sizeof(uint32_t) * nc);
     const size_t o_ci = take(sizeof(uint32_t) * nc), o_or = take(sizeof(uint32_t) * nc);
     w.cub_bytes = cub_temp_bytes(ncols);
@@ -868,6 +933,7 @@ static MeshWs mesh_ws_layout(void *base, int64_t ncols, int64_t workspace_bytes 
         w.tdeg = (int32_t *)(b + o_td);
         w.scratch_top = (unsigned long long *)(b + o_st);
         w.slot_total = w.scratch_top + 1;
+        w.band = reinterpret_cast<int64_t *>(w.scratch_top + 2);
         w.keys_in = (uint32_t *)(b + o_ki);
         w.keys_out = (uint32_t *)(b + o_ko);
         w.cols_in = (uint32_t *)(b + o_ci);
@@ -930,6 +996,16 @@ int mesh_ws_adjacency(void *workspace, int64_t workspace_bytes, int64_t ncols, i
     *deg = w.deg;
     *adj = w.adj;
     return HX_OK;
+}
+
+// Strip width of the band order in columns (a multiple of the tile); HX_BAND_STRIP=0 turns it off.
+static int64_t band_strip() {
+    static const int64_t w = [] {
+        const char *v = getenv("HX_BAND_STRIP");
+        const int64_t x = v ? atoll(v) : HX_BAND_STRIP_DEFAULT;
+        return x <= 0 ? (int64_t)0 : std::max<int64_t>(COL_BLOCK, x / COL_BLOCK * COL_BLOCK);
+    }();
+    return w;
 }
 
 static bool single_dense(const SegTable &T) {
@@ -1044,14 +1120,24 @@ static int mesh_csc_build(const hx_elem_segment *segs, int32_t n_segs, int64_t n
             HX_TRY_CUDA(cub::DeviceRadixSort::SortPairs(w.cub_tmp, cb, w.keys_in, w.keys_out, w.cols_in, w.order,
                                                         (int)ncols, begin_bit, end_bit, s));
         }
-        const uint32_t *order = ordered ? w.order : nullptr;
+        // banded numberings: strip order (decided on the device, see band_kernel)
+        const int64_t strip = band_strip();
+        const bool banded = !ordered && strip > 0 && single_conn(T) && n_total >= BAND_SAMPLES && ncols >= 8 * strip;
+        if (banded) {
+            band_kernel<<<1, 256, 0, s>>>(T.conn[0], n_total, ncols, strip, w.order_flag, w.band);
+            HX_CHECK_LAUNCH("band_kernel");
+            band_order_kernel<<<(unsigned)std::min<int64_t>(ceil_div(ncols, 256), 148 * 16), 256, 0, s>>>(
+                ncols, w.order_flag, w.band, w.order);
+            HX_CHECK_LAUNCH("band_order_kernel");
+        }
+        const uint32_t *order = ordered || banded ? w.order : nullptr;
         HX_TRY_CUDA(cudaMemsetAsync(w.scratch_top, 0, 2 * sizeof(unsigned long long), s));  // + slot_total
         HX_TRY_CUDA(cudaMemsetAsync(w.tile_need, 0, sizeof(int32_t) * tiles, s));
         auto pattern = [&](auto key_tag, auto single_tag, auto fixed_tag) {
             using K = decltype(key_tag);
             pattern_kernel<K, decltype(single_tag)::value, decltype(fixed_tag)::value><<<tiles, COL_BLOCK, 0, s>>>(
                 T, col_lo, ncols, w.deg, w.adj, col_ptr, w.scratch, w.scratch_capacity, w.scratch_top, w.block_scratch,
-                status, order, w.slot_total, w.tile_need, w.tadj, w.tdeg);
+                status, order, w.slot_total, w.tile_need, w.tadj, w.tdeg, w.order_flag);
         };
         const bool packed = n_nodes <= (int64_t(1) << 26);
         if (fixed) {  // one dense segment (checked above)

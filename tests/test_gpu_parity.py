@@ -1216,3 +1216,37 @@ def test_host_transfer_codec_round_trip(monkeypatch, codec):
         assert bits_equal(m.col_ptr, cp) and bits_equal(m.row_idx, ri) and bits_equal(m.vals, vv)
     assert (xfer.bytes_per_transfer(len(ri)) < 8 * (mesh.n_nodes + 1) + 12 * len(ri)) == (codec == "1")
     xfer.close()
+
+
+_BAND_SCRIPT = r"""
+import sys
+sys.path[:0] = [{root!r}, {root!r} + '/tests']
+import oracle
+from common import bits_equal
+from paper_1501_04784_b200 import device as D
+from paper_1501_04784_b200.pipeline import build_device, run_build
+from paper_1501_04784_b200.workloads import perturbed_mesh
+mesh = perturbed_mesh(24, seed=11)  # band 651 columns: ten 64-column strips
+ke, rows, cols, _, _, _ = oracle.stiffness_mesh(mesh.coords, mesh.connectivity, mesh.coefficient)
+cp, ri, vv = oracle.triplet_to_csc(rows, cols, ke.reshape(-1), mesh.n_nodes)
+csc = build_device(D.DeviceMesh.from_host(mesh)).csc
+assert bits_equal(csc.col_ptr.cpu().numpy(), cp) and bits_equal(csc.row_idx.cpu().numpy(), ri)
+assert bits_equal(csc.vals.cpu().numpy(), vv)
+m, _ = run_build(mesh, budget_bytes=10**12)
+assert bits_equal(m.col_ptr, cp) and bits_equal(m.row_idx, ri) and bits_equal(m.vals, vv)
+print("band ok")
+"""
+
+
+def test_band_strip_order_bitwise():
+    """The strip processing order of banded numberings (band_kernel / band_order_kernel, on by
+    default when the band holds four strips) forced onto a small mesh with 64-column strips: the
+    CSC is bitwise the oracle's (HX_BAND_STRIP is read once per process, hence the subprocess)."""
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = str(Path(__file__).resolve().parent.parent)
+    out = subprocess.run([sys.executable, "-c", _BAND_SCRIPT.format(root=root)], capture_output=True, text=True,
+                         env={**os.environ, "HX_BAND_STRIP": "64"}, timeout=600)
+    assert out.returncode == 0 and "band ok" in out.stdout, out.stderr[-2000:]
