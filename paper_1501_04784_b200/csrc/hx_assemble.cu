@@ -120,9 +120,22 @@ __global__ void adjacency_fixed_kernel(const int32_t *__restrict__ conn, int64_t
 // consecutive pattern/emit threads work on nearby elements (connectivity rows and KE values stay in
 // L1/L2 instead of being gathered from random elements).
 // FIXED: fixed-slot adjacency (slot = local node, empty = -1; see incident_sorted).
+// Element numberings are banded too (a node's elements lie up to one element layer apart): with a
+// band (band[0] = B elements, band[1] = strip width, B = 0: none) the key is the first element's
+// position in the strip order of the elements (strip_pos, the inverse of band_col), so the columns
+// that share a KE row are processed one strip -- not one element layer -- apart.
+__device__ __forceinline__ uint32_t strip_pos(uint32_t e, uint32_t n, uint32_t B, uint32_t W) {
+    const uint32_t rows = n / B;
+    if (e >= rows * B) return e;
+    const uint32_t z = e / B, r = e - z * B, s = r / W, w = min(W, B - s * W);
+    return s * rows * W + z * w + (r - s * W);
+}
+
 template <bool FIXED>
 __global__ void first_element_kernel(int64_t ncols, const int32_t *__restrict__ deg, const int32_t *__restrict__ adj,
-                                     uint32_t empty_key, uint32_t *__restrict__ keys, uint32_t *__restrict__ cols) {
+                                     uint32_t empty_key, uint32_t *__restrict__ keys, uint32_t *__restrict__ cols,
+                                     const int64_t *__restrict__ band) {
+    const uint32_t B = (uint32_t)__ldg(band), W = (uint32_t)__ldg(band + 1);
     for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < ncols; c += (int64_t)gridDim.x * blockDim.x) {
         const int d = FIXED ? MAXDEG : min(__ldg(deg + c), MAXDEG);
         uint32_t k = empty_key;
@@ -130,8 +143,42 @@ __global__ void first_element_kernel(int64_t ncols, const int32_t *__restrict__ 
             const int32_t v = __ldg(adj + 8 * c + j);
             if (!FIXED || v >= 0) k = min(k, (uint32_t)(v >> 3));
         }
-        keys[c] = k;
+        keys[c] = B != 0u && k != empty_key ? strip_pos(k, empty_key, B, W) : k;
         cols[c] = (uint32_t)c;
+    }
+}
+
+// Element band: median span (last - first incident element) of 1024 sampled columns; kept only when
+// it holds at least four strips (band[0] = 0 otherwise).
+template <bool FIXED>
+__global__ void __launch_bounds__(256) element_band_kernel(int64_t ncols, const int32_t *__restrict__ deg,
+                                                           const int32_t *__restrict__ adj, int64_t n_el,
+                                                           int64_t strip, int64_t *__restrict__ band) {
+    using Sort = cub::BlockRadixSort<int32_t, 256, 4>;
+    __shared__ typename Sort::TempStorage tmp;
+    __shared__ int32_t s_med;
+    int32_t span[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int64_t c = (int64_t)(threadIdx.x * 4 + i) * ncols / 1024;
+        const int d = FIXED ? MAXDEG : min(__ldg(deg + c), MAXDEG);
+        int32_t lo = INT32_MAX, hi = -1;
+        for (int j = 0; j < d; ++j) {
+            const int32_t v = __ldg(adj + 8 * c + j);
+            if (!FIXED || v >= 0) {
+                lo = min(lo, v >> 3);
+                hi = max(hi, v >> 3);
+            }
+        }
+        span[i] = hi >= 0 ? hi - lo : 0;
+    }
+    Sort(tmp).Sort(span);
+    if (threadIdx.x == 128) s_med = span[0];  // rank 512 of 1024
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const int64_t B = (int64_t)s_med;
+        band[0] = B >= 4 * strip && 2 * B <= n_el ? B : 0;
+        band[1] = strip;
     }
 }
 
@@ -1105,10 +1152,20 @@ static int mesh_csc_build(const hx_elem_segment *segs, int32_t n_segs, int64_t n
         const unsigned tiles = (unsigned)ceil_div(ncols, COL_BLOCK);
         if (ordered) {
             const unsigned g = (unsigned)std::min<int64_t>(ceil_div(ncols, 256), 148 * 32);
+            const int64_t strip = band_strip();
+            if (strip > 0 && ncols >= 1024 && n_total >= 8 * strip) {
+                if (fixed) element_band_kernel<true><<<1, 256, 0, s>>>(ncols, w.deg, w.adj, n_total, strip, w.band);
+                else element_band_kernel<false><<<1, 256, 0, s>>>(ncols, w.deg, w.adj, n_total, strip, w.band);
+                HX_CHECK_LAUNCH("element_band_kernel");
+            } else {
+                HX_TRY_CUDA(cudaMemsetAsync(w.band, 0, 2 * sizeof(int64_t), s));
+            }
             if (fixed)
-                first_element_kernel<true><<<g, 256, 0, s>>>(ncols, w.deg, w.adj, (uint32_t)n_total, w.keys_in, w.cols_in);
+                first_element_kernel<true><<<g, 256, 0, s>>>(ncols, w.deg, w.adj, (uint32_t)n_total, w.keys_in, w.cols_in,
+                                                             w.band);
             else
-                first_element_kernel<false><<<g, 256, 0, s>>>(ncols, w.deg, w.adj, (uint32_t)n_total, w.keys_in, w.cols_in);
+                first_element_kernel<false><<<g, 256, 0, s>>>(ncols, w.deg, w.adj, (uint32_t)n_total, w.keys_in,
+                                                              w.cols_in, w.band);
             HX_CHECK_LAUNCH("first_element_kernel");
             int end_bit = 1;
             while (end_bit < 32 && ((uint64_t)n_total >> end_bit) != 0) ++end_bit;
