@@ -585,7 +585,7 @@ __device__ __forceinline__ const double *ke_entry(const SegTable &T, int64_t e, 
 // one node layer apart; HX_EMIT_KE_HINT 1 marks those loads L2 evict_last (the streamed scratch
 // loads and CSC stores are evict-first) so the rows survive until their last column.
 #ifndef HX_EMIT_KE_HINT
-#define HX_EMIT_KE_HINT 0
+#define HX_EMIT_KE_HINT 1  // evict_last: -0.2..-0.45 ms at C4 with the strip order (profiles/r02/emit_variants.txt)
 #endif
 __device__ __forceinline__ uint64_t ke_policy() {
     uint64_t p = 0;
@@ -799,13 +799,13 @@ __device__ __forceinline__ void emit_tile(EmitSmem &S, const EmitArgs &A, int64_
     }
 }
 
-template <bool ROWS, bool VALS, bool SINGLE>
-__global__ void __launch_bounds__(EMIT_BLOCK)
+template <int NT, bool ROWS, bool VALS, bool SINGLE>
+__global__ void __launch_bounds__(NT)
 emit_kernel(EmitArgs A, const uint32_t *__restrict__ status) {
     // the pattern pass hit a fast-path limit: its records are incomplete and the caller re-runs
     if (*status & HX_ST_EMIT_SKIP) return;
     __shared__ EmitSmem S;
-    emit_tile<EMIT_BLOCK, ROWS, VALS, SINGLE, false>(S, A, blockIdx.x, threadIdx.x);
+    emit_tile<NT, ROWS, VALS, SINGLE, false>(S, A, blockIdx.x, threadIdx.x);
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -1092,11 +1092,17 @@ static EmitArgs emit_args(const SegTable &T, int64_t col_lo, int64_t ncols, cons
     return A;
 }
 
+// wide: element-ordered builds (randomly numbered meshes) run 256 threads per tile -- their KE gathers
+// and scattered CSC writes want more loads in flight (C5 -0.35 ms; column / strip order: +0.5 ms at C4).
 template <bool ROWS, bool VALS>
-static int launch_emit(const EmitArgs &A, const uint32_t *status, cudaStream_t s, const char *where) {
+static int launch_emit(const EmitArgs &A, const uint32_t *status, cudaStream_t s, const char *where,
+                       bool wide = false) {
     const unsigned tiles = (unsigned)ceil_div(A.ncols, COL_BLOCK);
-    if (!VALS || single_dense(A.T)) emit_kernel<ROWS, VALS, true><<<tiles, EMIT_BLOCK, 0, s>>>(A, status);
-    else emit_kernel<ROWS, VALS, false><<<tiles, EMIT_BLOCK, 0, s>>>(A, status);
+    const bool single = !VALS || single_dense(A.T);
+    if (wide && single) emit_kernel<2 * EMIT_BLOCK, ROWS, VALS, true><<<tiles, 2 * EMIT_BLOCK, 0, s>>>(A, status);
+    else if (wide) emit_kernel<2 * EMIT_BLOCK, ROWS, VALS, false><<<tiles, 2 * EMIT_BLOCK, 0, s>>>(A, status);
+    else if (single) emit_kernel<EMIT_BLOCK, ROWS, VALS, true><<<tiles, EMIT_BLOCK, 0, s>>>(A, status);
+    else emit_kernel<EMIT_BLOCK, ROWS, VALS, false><<<tiles, EMIT_BLOCK, 0, s>>>(A, status);
     HX_CHECK_LAUNCH(where);
     return HX_OK;
 }
@@ -1217,7 +1223,7 @@ static int mesh_csc_build(const hx_elem_segment *segs, int32_t n_segs, int64_t n
         HX_TRY_CUDA(cub::DeviceScan::ExclusiveSum(w.cub_tmp, cb2, col_ptr, col_ptr, (int)(ncols + 1), s));
         if (vals != nullptr) {
             const int rc2 = launch_emit<true, true>(emit_args(T, col_lo, ncols, w, col_ptr, row_idx, vals, row_capacity),
-                                                    status, s, "emit_kernel");
+                                                    status, s, "emit_kernel", ordered);
             if (rc2) return rc2;
         } else if (row_capacity > 0) {
             const int rc2 = launch_emit<true, false>(
