@@ -1225,7 +1225,7 @@ import oracle
 from common import bits_equal
 from paper_1501_04784_b200 import device as D
 from paper_1501_04784_b200.pipeline import build_device, run_build
-from paper_1501_04784_b200.workloads import perturbed_mesh
+from paper_1501_04784_b200.workloads import permuted_mesh, perturbed_mesh
 mesh = perturbed_mesh(24, seed=11)  # band 651 columns: ten 64-column strips
 ke, rows, cols, _, _, _ = oracle.stiffness_mesh(mesh.coords, mesh.connectivity, mesh.coefficient)
 cp, ri, vv = oracle.triplet_to_csc(rows, cols, ke.reshape(-1), mesh.n_nodes)
@@ -1234,14 +1234,22 @@ assert bits_equal(csc.col_ptr.cpu().numpy(), cp) and bits_equal(csc.row_idx.cpu(
 assert bits_equal(csc.vals.cpu().numpy(), vv)
 m, _ = run_build(mesh, budget_bytes=10**12)
 assert bits_equal(m.col_ptr, cp) and bits_equal(m.row_idx, ri) and bits_equal(m.vals, vv)
+# permuted node ids: element order, first-element keys in the strip order of the element band (~601)
+perm = permuted_mesh(mesh, seed=12)
+ke, rows, cols, _, _, _ = oracle.stiffness_mesh(perm.coords, perm.connectivity, perm.coefficient)
+cp, ri, vv = oracle.triplet_to_csc(rows, cols, ke.reshape(-1), perm.n_nodes)
+csc = build_device(D.DeviceMesh.from_host(perm)).csc
+assert bits_equal(csc.col_ptr.cpu().numpy(), cp) and bits_equal(csc.row_idx.cpu().numpy(), ri)
+assert bits_equal(csc.vals.cpu().numpy(), vv)
 print("band ok")
 """
 
 
 def test_band_strip_order_bitwise():
-    """The strip processing order of banded numberings (band_kernel / band_order_kernel, on by
-    default when the band holds four strips) forced onto a small mesh with 64-column strips: the
-    CSC is bitwise the oracle's (HX_BAND_STRIP is read once per process, hence the subprocess)."""
+    """The strip processing orders (band_kernel / band_order_kernel for banded node numberings,
+    element_band_kernel's strip keys for element-ordered builds; on by default when the band holds
+    four strips) forced onto small meshes with 64-wide strips: the CSC is bitwise the oracle's
+    (HX_BAND_STRIP is read once per process, hence the subprocess)."""
     import subprocess
     import sys
     from pathlib import Path
