@@ -287,7 +287,13 @@ UPLOAD_RANGES_MIN_ELEMENTS = 1 << 22
 # build (stream.py): STREAM_BLOCKS blocks, copies in both directions overlapping the kernels
 # transfer statistics of the last streamed run_build (d2h_bytes, row codec use, stage times)
 LAST_RUN_STATS: dict = {}
-STREAM_BLOCKS = 10
+STREAM_BLOCKS: int | None = None  # None: 10 blocks, 20 from 32M elements (C4: 231 vs 238 ms per call,
+                                  # profiles/r02/e2e_knobs_c4.txt)
+
+
+def stream_blocks(n_el: int) -> int:
+    return int(STREAM_BLOCKS) if STREAM_BLOCKS is not None else (20 if n_el >= 1 << 25 else 10)
+
 STREAM_MIN_ELEMENTS = 1 << 22
 
 
@@ -361,7 +367,7 @@ def run_build(mesh, budget_bytes: int, workers: int = 1, mode: str = "sequential
         from . import stream
 
         st: dict = {}
-        matrix = stream.streamed_build(mesh, STREAM_BLOCKS, mode=integration, device=dev, stats=st)
+        matrix = stream.streamed_build(mesh, stream_blocks(mesh.n_el), mode=integration, device=dev, stats=st)
         LAST_RUN_STATS.clear()
         LAST_RUN_STATS.update(st)
         if matrix is not None:
