@@ -526,6 +526,11 @@ __device__ __forceinline__ bool ke_gauss_point(GpWarpSmem &sm, int el, int gp, b
 #ifndef HX_KE_STATIC
 #define HX_KE_STATIC 0
 #endif
+// HX_KE_CLAIM: quads per counter claim (ptxas turns the lane-0 atomicAdd into a warp-aggregated
+// atomic whose result SHFL follows the ATOM directly, so every claim stalls its warp for a round trip).
+#ifndef HX_KE_CLAIM
+#define HX_KE_CLAIM 16  // 8-64 measured equal, 3.5% faster than 1 at C4 and C5 (profiles/r02/ke_claim_batch.txt)
+#endif
 #ifndef HX_KE_LATE_GRAB
 #define HX_KE_LATE_GRAB 1
 #endif
@@ -560,15 +565,24 @@ __device__ __forceinline__ void integrate_quads(GpWarpSmem &sm, const uint8_t *s
     const int64_t n_quads = (n + GP_EL_PER_WARP - 1) / GP_EL_PER_WARP;
     const int64_t first_dynamic = (int64_t)gridDim.x * GP_WARPS;
     int64_t static_next = (int64_t)blockIdx.x * GP_WARPS + warp;
+    int64_t spare = 0;  // the rest of the last claim: quads spare .. spare + spare_n - 1
+    int spare_n = 0;
     auto grab = [&]() -> int64_t {
         if (HX_KE_STATIC) {
             (void)quad_counter;
             static_next += first_dynamic;
             return static_next;
         }
+        if (spare_n > 0) {
+            --spare_n;
+            return spare++;
+        }
         unsigned q = 0;
-        if (lane == 0) q = atomicAdd(quad_counter, 1u);
-        return first_dynamic + (int64_t)__shfl_sync(0xffffffffu, q, 0);
+        if (lane == 0) q = atomicAdd(quad_counter, (unsigned)HX_KE_CLAIM);
+        const int64_t base = first_dynamic + (int64_t)__shfl_sync(0xffffffffu, q, 0);
+        spare = base + 1;
+        spare_n = HX_KE_CLAIM - 1;
+        return base;
     };
     auto node_id = [&](int64_t q) -> int32_t {
         const int64_t k = q * GP_EL_PER_WARP + el;
@@ -617,7 +631,8 @@ __device__ __forceinline__ void integrate_quads(GpWarpSmem &sm, const uint8_t *s
         // claim the quad after next now, read the claim after this quad's FP64 work: the atomic's
         // round trip overlaps the Gauss-point arithmetic instead of stalling the warp here
         unsigned claim = 0;
-        if (!HX_KE_STATIC && lane == 0 && quad2 < n_quads) claim = atomicAdd(quad_counter, 1u);
+        const bool claiming = !HX_KE_STATIC && quad2 < n_quads && spare_n == 0;
+        if (claiming && lane == 0) claim = atomicAdd(quad_counter, (unsigned)HX_KE_CLAIM);
 #else
         const int64_t quad3 = quad2 < n_quads ? grab() : n_quads;
 #endif
@@ -635,8 +650,13 @@ __device__ __forceinline__ void integrate_quads(GpWarpSmem &sm, const uint8_t *s
             if (HX_KE_STATIC) {
                 static_next += first_dynamic;
                 quad3 = static_next;
-            } else {
+            } else if (claiming) {
                 quad3 = first_dynamic + (int64_t)__shfl_sync(0xffffffffu, claim, 0);
+                spare = quad3 + 1;
+                spare_n = HX_KE_CLAIM - 1;
+            } else {
+                --spare_n;
+                quad3 = spare++;
             }
         }
 #endif
