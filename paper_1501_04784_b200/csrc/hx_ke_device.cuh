@@ -128,6 +128,16 @@ constexpr int GP_EL_PER_WARP = 4;
 // <= 12 distinct (el, m) words of one warp-wide load in distinct bank pairs.
 constexpr int P_M_STRIDE = 25;
 constexpr int P_EL_STRIDE = 76;
+// HX_KE_LANE_PRODUCTS (exact mode): the warp stages the raw coordinates X[el][k][a] instead of the
+// 72 products, and every Gauss-point lane forms its own dN x products (the same roundings: M x with
+// M the lane's magnitude, signs folded into the add/sub).  The integration kernel is bound by the
+// LSU data pipe (ncu: 95% of its wavefronts, shared memory 77%): a lane's 72 product loads cost 24
+// wavefronts per element, its 24 coordinates 3 (element-wide broadcast, 16-byte pairs), for +504
+// DMUL per element.  Element stride 26 doubles keeps the 4 elements' pairs in distinct banks.
+#ifndef HX_KE_LANE_PRODUCTS
+#define HX_KE_LANE_PRODUCTS 1
+#endif
+constexpr int X_EL_STRIDE = 26;
 // Contribution buffer t[el][j][g]: g contiguous (the reducing lane reads 8 doubles with 4 x 16-B
 // loads), j stride 10 and element stride 88 make both the stores and the loads conflict-free.
 constexpr int T_J_STRIDE = 10;
@@ -241,6 +251,15 @@ __device__ __forceinline__ double mag_select(int k) {
 template <int MODE>
 __device__ __forceinline__ void publish_node(GpWarpSmem &sm, int el, int a, int32_t node, double x0, double x1,
                                              double x2, double c) {
+    if (MODE == HX_MODE_EXACT && HX_KE_LANE_PRODUCTS) {
+        double *X = sm.P + el * X_EL_STRIDE + a;
+        X[0] = x0;
+        X[8] = x1;
+        X[16] = x2;
+        sm.conn[el * 8 + a] = node;
+        if (a == 0) sm.coeff[el] = c;
+        return;
+    }
     double *P = sm.P + el * P_EL_STRIDE + 3 * a;
     if (MODE == HX_MODE_EXACT) {
 #pragma unroll
@@ -402,14 +421,43 @@ __device__ __forceinline__ bool ke_gauss_point(GpWarpSmem &sm, int el, int gp, b
                                                int32_t *__restrict__ rows_out, int32_t *__restrict__ cols_out,
                                                const uint8_t *s_pi, const uint8_t *s_pj) {
     const int ir = (gp >> 2) & 1, is = (gp >> 1) & 1, it = gp & 1;
-    const double *P = sm.P + el * P_EL_STRIDE;
-    // J = dn @ x (element.py:262-269), accumulated from 0.0 over a = 0..7.  dN_r,a at this point
-    // has magnitude index (s_a == s_gp) + (t_a == t_gp), and cyclically for s and t.
+    // This lane's dN magnitudes per direction, indexed by the node's other two natural coordinates
+    // (dN_r,a = sign * Mr[2 s_a + t_a], cyclically for s and t).
+    double Mr[4], Ms[4], Mt[4];
+#pragma unroll
+    for (int u = 0; u < 2; ++u)
+#pragma unroll
+        for (int v = 0; v < 2; ++v) {
+            Mr[2 * u + v] = mag_select((u == is) + (v == it));  // (s_a, t_a)
+            Ms[2 * u + v] = mag_select((u == ir) + (v == it));  // (r_a, t_a)
+            Mt[2 * u + v] = mag_select((u == ir) + (v == is));  // (r_a, s_a)
+        }
+    // J = dn @ x (element.py:262-269), accumulated from 0.0 over a = 0..7.
     double j[3][3];
 #pragma unroll
     for (int d = 0; d < 3; ++d)
 #pragma unroll
         for (int k = 0; k < 3; ++k) j[d][k] = 0.0;
+#if HX_KE_LANE_PRODUCTS
+    const double *X = sm.P + el * X_EL_STRIDE;
+#pragma unroll
+    for (int a2 = 0; a2 < 8; a2 += 2)
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            const double2 xv = *reinterpret_cast<const double2 *>(X + 8 * k + a2);
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int a = a2 + h;
+                const double x = h ? xv.y : xv.x;
+                j[0][k] = acc_signed(j[0][k], nat_r(a), dmul(Mr[2 * bit_s(a) + bit_t(a)], x));
+                j[1][k] = acc_signed(j[1][k], nat_s(a), dmul(Ms[2 * bit_r(a) + bit_t(a)], x));
+                j[2][k] = acc_signed(j[2][k], nat_t(a), dmul(Mt[2 * bit_r(a) + bit_s(a)], x));
+            }
+        }
+#else
+    // dN_r,a at this point has magnitude index (s_a == s_gp) + (t_a == t_gp), and cyclically for s
+    // and t: the published products P[m][a][k] = M_m x[a][k].
+    const double *P = sm.P + el * P_EL_STRIDE;
 #pragma unroll
     for (int a = 0; a < 8; ++a) {
         const int mr = (bit_s(a) == is) + (bit_t(a) == it);
@@ -422,6 +470,7 @@ __device__ __forceinline__ bool ke_gauss_point(GpWarpSmem &sm, int el, int gp, b
             j[2][k] = acc_signed(j[2][k], nat_t(a), P[mt * P_M_STRIDE + 3 * a + k]);
         }
     }
+#endif
     // cofactors, det (element.py:271-275)
     const double c00 = dsub(dmul(j[1][1], j[2][2]), dmul(j[1][2], j[2][1]));
     const double c01 = dsub(dmul(j[1][2], j[2][0]), dmul(j[1][0], j[2][2]));
@@ -449,16 +498,6 @@ __device__ __forceinline__ bool ke_gauss_point(GpWarpSmem &sm, int el, int gp, b
         for (int i = 0; i < 9; ++i) inv[i / 3][i % 3] = __ddiv_rn(num[i], det);
     }
     // B = J^-1 dn (element.py:286-290): (i_r0 dn0a + i_r1 dn1a) + i_r2 dn2a with dn = sign * M.
-    // This lane's magnitudes per direction, indexed by the node's other two natural coordinates.
-    double Mr[4], Ms[4], Mt[4];
-#pragma unroll
-    for (int u = 0; u < 2; ++u)
-#pragma unroll
-        for (int v = 0; v < 2; ++v) {
-            Mr[2 * u + v] = mag_select((u == is) + (v == it));  // (s_a, t_a)
-            Ms[2 * u + v] = mag_select((u == ir) + (v == it));  // (r_a, t_a)
-            Mt[2 * u + v] = mag_select((u == ir) + (v == is));  // (r_a, s_a)
-        }
     double B[3][8];
 #pragma unroll
     for (int r = 0; r < 3; ++r) {
