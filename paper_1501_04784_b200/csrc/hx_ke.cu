@@ -79,9 +79,9 @@ stiffness_batch_kernel(const double *__restrict__ coords, const double *__restri
     __syncwarp();
     bool ok;
     if constexpr (MODE == HX_MODE_EXACT)
-        ok = ke_gauss_point<false>(sm, el, gp, fast_div, e, valid, out, nullptr, nullptr, nullptr, nullptr);
+        ok = ke_gauss_point<false>(sm, el, gp, fast_div, e, valid, out, nullptr, nullptr, 0u);
     else
-        ok = ke_gauss_point_fast<false>(sm, el, gp, e, valid, out, nullptr, nullptr, nullptr, nullptr);
+        ok = ke_gauss_point_fast<false>(sm, el, gp, e, valid, out, nullptr, nullptr, 0u);
     if (valid && !ok) atomicMin(fail_min, HX_FAIL_DEGENERATE_KEY | (unsigned long long)e);
 }
 

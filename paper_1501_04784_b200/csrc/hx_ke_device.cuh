@@ -133,11 +133,12 @@ constexpr int P_EL_STRIDE = 76;
 // M the lane's magnitude, signs folded into the add/sub).  The integration kernel is bound by the
 // LSU data pipe (ncu: 95% of its wavefronts, shared memory 77%): a lane's 72 product loads cost 24
 // wavefronts per element, its 24 coordinates 3 (element-wide broadcast, 16-byte pairs), for +504
-// DMUL per element.  Element stride 26 doubles keeps the 4 elements' pairs in distinct banks.
+// DMUL per element.  Element stride 24 doubles (= 8 mod 16): the two elements of a half-warp hit
+// distinct banks for both the 8-byte stores and the 16-byte pair loads.
 #ifndef HX_KE_LANE_PRODUCTS
 #define HX_KE_LANE_PRODUCTS 1
 #endif
-constexpr int X_EL_STRIDE = 26;
+constexpr int X_EL_STRIDE = 24;
 // Contribution buffer t[el][j][g]: g contiguous (the reducing lane reads 8 doubles with 4 x 16-B
 // loads), j stride 10 and element stride 88 make both the stores and the loads conflict-free.
 constexpr int T_J_STRIDE = 10;
@@ -202,7 +203,7 @@ template <int MODE, bool WITH_INDEX, bool KE_KEEP = false>
 __device__ __forceinline__ void reduce_store_all(const GpWarpSmem &sm, const double *tb, int el, int gp,
                                                  int64_t out_el, bool valid, double *__restrict__ ke_out,
                                                  int32_t *__restrict__ rows_out, int32_t *__restrict__ cols_out,
-                                                 const uint8_t *s_pi, const uint8_t *s_pj) {
+                                                 uint32_t pcode) {
     double acc[5];
 #pragma unroll
     for (int c = 0; c < 5; ++c) {
@@ -232,7 +233,8 @@ __device__ __forceinline__ void reduce_store_all(const GpWarpSmem &sm, const dou
             if (c < 4 || gp < 4) {
                 st_ke<KE_KEEP>(ke_out + out_el * 36 + p, acc[c]);
                 if (WITH_INDEX) {
-                    const int32_t gi = sm.conn[el * 8 + s_pi[p]], gj = sm.conn[el * 8 + s_pj[p]];
+                    const int pi = (pcode >> (6 * c)) & 7u, pj = (pcode >> (6 * c + 3)) & 7u;
+                    const int32_t gi = sm.conn[el * 8 + pi], gj = sm.conn[el * 8 + pj];
                     st_out(rows_out + out_el * 36 + p, max(gi, gj));
                     st_out(cols_out + out_el * 36 + p, min(gi, gj));
                 }
@@ -283,7 +285,7 @@ template <int MODE, bool WITH_INDEX>
 __device__ __forceinline__ void reduce_store(const GpWarpSmem &sm, const double *tb, int el, int gp, int c,
                                              int64_t out_el, bool valid, double *__restrict__ ke_out,
                                              int32_t *__restrict__ rows_out, int32_t *__restrict__ cols_out,
-                                             const uint8_t *s_pi, const uint8_t *s_pj) {
+                                             uint32_t pcode) {
     const int p = 8 * c + gp;  // this lane reduces packed entry p of its element
     if (p >= 36) return;
     const double2 *src = reinterpret_cast<const double2 *>(tb + gp * T_J_STRIDE);
@@ -304,7 +306,8 @@ __device__ __forceinline__ void reduce_store(const GpWarpSmem &sm, const double 
     if (valid) {
         ke_out[out_el * 36 + p] = acc;
         if (WITH_INDEX) {
-            const int32_t gi = sm.conn[el * 8 + s_pi[p]], gj = sm.conn[el * 8 + s_pj[p]];
+            const int pi = (pcode >> (6 * c)) & 7u, pj = (pcode >> (6 * c + 3)) & 7u;
+            const int32_t gi = sm.conn[el * 8 + pi], gj = sm.conn[el * 8 + pj];
             rows_out[out_el * 36 + p] = max(gi, gj);
             cols_out[out_el * 36 + p] = min(gi, gj);
         }
@@ -320,8 +323,7 @@ __device__ __forceinline__ void reduce_store(const GpWarpSmem &sm, const double 
 template <bool WITH_INDEX, bool KE_KEEP = false>
 __device__ __forceinline__ bool ke_gauss_point_fast(GpWarpSmem &sm, int el, int gp, int64_t out_el, bool valid,
                                                     double *__restrict__ ke_out, int32_t *__restrict__ rows_out,
-                                                    int32_t *__restrict__ cols_out, const uint8_t *s_pi,
-                                                    const uint8_t *s_pj) {
+                                                    int32_t *__restrict__ cols_out, uint32_t pcode) {
     const int ir = (gp >> 2) & 1, is = (gp >> 1) & 1, it = gp & 1;
     const double *X = sm.P + el * P_EL_STRIDE;
     double Mr[4], Ms[4], Mt[4];
@@ -389,8 +391,7 @@ __device__ __forceinline__ bool ke_gauss_point_fast(GpWarpSmem &sm, int el, int 
             tf[p * T_J_STRIDE + gp] = fma(dn(0, i), H[0][q], fma(dn(1, i), H[1][q], dn(2, i) * H[2][q]));
         }
         __syncwarp();
-        reduce_store_all<HX_MODE_FAST, WITH_INDEX, KE_KEEP>(sm, tf, el, gp, out_el, valid, ke_out, rows_out, cols_out, s_pi,
-                                                  s_pj);
+        reduce_store_all<HX_MODE_FAST, WITH_INDEX, KE_KEEP>(sm, tf, el, gp, out_el, valid, ke_out, rows_out, cols_out, pcode);
     }
     return ok;
 #endif
@@ -406,8 +407,7 @@ __device__ __forceinline__ bool ke_gauss_point_fast(GpWarpSmem &sm, int el, int 
             }
         }
         __syncwarp();
-        reduce_store<HX_MODE_FAST, WITH_INDEX>(sm, tb, el, gp, c, out_el, valid, ke_out, rows_out, cols_out, s_pi,
-                                              s_pj);
+        reduce_store<HX_MODE_FAST, WITH_INDEX>(sm, tb, el, gp, c, out_el, valid, ke_out, rows_out, cols_out, pcode);
         __syncwarp();
     }
     return ok;
@@ -419,7 +419,7 @@ template <bool WITH_INDEX, bool KE_KEEP = false>
 __device__ __forceinline__ bool ke_gauss_point(GpWarpSmem &sm, int el, int gp, bool fast_div,
                                                int64_t out_el, bool valid, double *__restrict__ ke_out,
                                                int32_t *__restrict__ rows_out, int32_t *__restrict__ cols_out,
-                                               const uint8_t *s_pi, const uint8_t *s_pj) {
+                                               uint32_t pcode) {
     const int ir = (gp >> 2) & 1, is = (gp >> 1) & 1, it = gp & 1;
     // This lane's dN magnitudes per direction, indexed by the node's other two natural coordinates
     // (dN_r,a = sign * Mr[2 s_a + t_a], cyclically for s and t).
@@ -528,8 +528,7 @@ __device__ __forceinline__ bool ke_gauss_point(GpWarpSmem &sm, int el, int gp, b
             tf[p * T_J_STRIDE + gp] = dmul(scale, s);
         }
         __syncwarp();
-        reduce_store_all<HX_MODE_EXACT, WITH_INDEX, KE_KEEP>(sm, tf, el, gp, out_el, valid, ke_out, rows_out, cols_out,
-                                                   s_pi, s_pj);
+        reduce_store_all<HX_MODE_EXACT, WITH_INDEX, KE_KEEP>(sm, tf, el, gp, out_el, valid, ke_out, rows_out, cols_out, pcode);
     }
     return ok;
 #endif
@@ -547,8 +546,7 @@ __device__ __forceinline__ bool ke_gauss_point(GpWarpSmem &sm, int el, int gp, b
             }
         }
         __syncwarp();
-        reduce_store<HX_MODE_EXACT, WITH_INDEX>(sm, tb, el, gp, c, out_el, valid, ke_out, rows_out, cols_out, s_pi,
-                                               s_pj);
+        reduce_store<HX_MODE_EXACT, WITH_INDEX>(sm, tb, el, gp, c, out_el, valid, ke_out, rows_out, cols_out, pcode);
         __syncwarp();
     }
     return ok;
@@ -601,6 +599,11 @@ __device__ __forceinline__ void integrate_quads(GpWarpSmem &sm, const uint8_t *s
                                                 unsigned *__restrict__ quad_counter, AdjOut adj_out, Hook &hook) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int el = lane >> 3, gp = lane & 7;
+    // the (i, j) local nodes of this lane's packed entries p = gp + 8c, 3 + 3 bits per c, in a register
+    uint32_t pcode = 0;
+#pragma unroll
+    for (int c = 0; c < 5; ++c)
+        if (8 * c + gp < 36) pcode |= (uint32_t)(s_pi[8 * c + gp] | (s_pj[8 * c + gp] << 3)) << (6 * c);
     const int64_t n_quads = (n + GP_EL_PER_WARP - 1) / GP_EL_PER_WARP;
     const int64_t first_dynamic = (int64_t)gridDim.x * GP_WARPS;
     int64_t static_next = (int64_t)blockIdx.x * GP_WARPS + warp;
@@ -677,11 +680,9 @@ __device__ __forceinline__ void integrate_quads(GpWarpSmem &sm, const uint8_t *s
 #endif
         bool ok;
         if constexpr (MODE == HX_MODE_EXACT)
-            ok = ke_gauss_point<WITH_INDEX, KE_KEEP>(sm, el, gp, fast_div, k, valid, ke_out, rows_out, cols_out, s_pi,
-                                                     s_pj);
+            ok = ke_gauss_point<WITH_INDEX, KE_KEEP>(sm, el, gp, fast_div, k, valid, ke_out, rows_out, cols_out, pcode);
         else
-            ok = ke_gauss_point_fast<WITH_INDEX, KE_KEEP>(sm, el, gp, k, valid, ke_out, rows_out, cols_out, s_pi,
-                                                          s_pj);
+            ok = ke_gauss_point_fast<WITH_INDEX, KE_KEEP>(sm, el, gp, k, valid, ke_out, rows_out, cols_out, pcode);
         if (valid && !ok) atomicMin(fail_min, HX_FAIL_DEGENERATE_KEY | (unsigned long long)(lo + k));
 #if HX_KE_LATE_GRAB
         int64_t quad3 = n_quads;
