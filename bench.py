@@ -33,10 +33,11 @@ METRIC = "hex8 elements/s (KE+index+CSR assembly), % HBM roofline, 1/2/4/8 GPUs"
 UNIT = "elements/s"
 # algorithmic bytes: each API array touched once
 KE_KERNEL = "integrate_mesh_kernel"  # KE + fused iK/jK
-# FP64 instructions per element of the exact-mode kernel (ncu smsp__sass_thread_inst_executed_op_
-# {dadd,dmul,dfma}, profiles/r01_ncu_full_c3.txt) and the FP64 pipe peak measured by
-# tools/fp64_peak.cu (profiles/r01_fp64_microbench.txt): the kernel's second ceiling.
-FP64_INSTR_PER_EL = {"exact": 4000.0, "fast": 2676.0}
+# FP64 thread instructions per element (ncu source-page opmix, tools/ncu_opmix.py): exact mode DMUL
+# 2264 + DADD 1912 + DFMA 328 since the Gauss-point lanes form their own dN x products
+# (profiles/r02/ke_lane_products.txt; 4032 before), fast mode profiles/r01_ncu_full_c3.txt; the FP64
+# pipe peak measured by tools/fp64_peak.cu (profiles/r01_fp64_microbench.txt): the kernel's second ceiling.
+FP64_INSTR_PER_EL = {"exact": 4504.0, "fast": 2676.0}
 FP64_PEAK_T_INSTR = 18.3
 KE_INDEX_BYTES_PER_EL = 32 + 8 + 288 + 288  # conn + coeff + KE f64 + iK/jK i32 (+ 24 B/node coords)
 ADJ_SLOT_BYTES_PER_NODE = 32  # 8 int32 adjacency slots per node, written by the fused integration kernel
@@ -444,8 +445,9 @@ def run_ours(args):
                                        "peak_t_instr_s": FP64_PEAK_T_INSTR,
                                        "frac": FP64_INSTR_PER_EL[args.mode] * n_el_total / world
                                        / (kernel["ke_ms"] / 1e3) / 1e12 / FP64_PEAK_T_INSTR},
-                         "note": "exact mode (reference operation order, bitwise) is FP64-pipe bound: ~4.0k FP64 "
-                                 "instr/element caps it at ~4.6 G el/s = 45% of the HBM roofline; see DESIGN.md"},
+                         "note": "exact mode (reference operation order, bitwise) is bound by the FP64 pipe and the "
+                                 "LSU data pipe together: ~4.5k FP64 instr/element cap it at ~4.1 G el/s = 42% "
+                                 "of the HBM roofline; see DESIGN.md"},
             "pipeline_roofline": {"achieved": pipeline_gbs, "peak": peak * world, "unit": "GB/s",
                                   "frac": pipeline_gbs / (peak * world),
                                   "frac_of_spec_8000": pipeline_gbs / (8000.0 * world),

@@ -113,8 +113,11 @@ __device__ __forceinline__ void init_pack_smem(uint8_t *pi, uint8_t *pj) {
     }
 }
 
+// __launch_bounds__ minimum blocks: 15 gives ptxas a 136-register budget; it still allocates 128,
+// so 16 one-warp blocks stay resident, but schedules better than under the exact 128 cap of 16:
+// C4 KE kernel 21.1 -> 20.4 ms (13: 20.9, 14: 20.6; profiles/r02/ke_min_blocks.txt).
 #ifndef HX_KE_MIN_BLOCKS
-#define HX_KE_MIN_BLOCKS 16
+#define HX_KE_MIN_BLOCKS 15
 #endif
 #ifndef HX_KE_BLOCK
 #define HX_KE_BLOCK 32
