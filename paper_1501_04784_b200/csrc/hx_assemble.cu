@@ -618,7 +618,8 @@ struct EmitSmem {
     int32_t s_cl[COL_BLOCK];          // column (block-local index) of each tile position
     int32_t s_rs[COL_BLOCK + 1];      // first scratch record of each column (tile-relative)
     int32_t s_deg[COL_BLOCK];
-    int32_t s_adj[COL_BLOCK * 8];     // the tile's sorted incident lists
+    int32_t s_adj[COL_BLOCK * 9];     // the tile's sorted incident lists, stride 9 (the diagonal pass reads
+                                      // one list per lane: conflict-free)
     uint8_t s_col[COL_BLOCK * MAXR];  // tile position of each off-diagonal record
 };
 
@@ -680,7 +681,7 @@ __device__ __forceinline__ void emit_tile(EmitSmem &S, const EmitArgs &A, int64_
     tile_sync<NT>();
     if (VALS)
         for (int i = tid; i < ncol * 8; i += NT)
-            S.s_adj[i] = __ldg(adj_list + 8 * first + i);  // contiguous: lists are in processing order
+            S.s_adj[(i >> 3) * 9 + (i & 7)] = __ldg(adj_list + 8 * first + i);  // contiguous: lists are in processing order
     // scratch record offsets: column u has max(m_u - 1, 0) records (m_u = 0 for a node no element
     // references), laid out in tile order by the pattern pass -- warp 0 scans them
     if (tid < 32) {
@@ -721,7 +722,7 @@ __device__ __forceinline__ void emit_tile(EmitSmem &S, const EmitArgs &A, int64_
         if (ROWS) __stcs(reinterpret_cast<long long *>(row_idx) + o, (long long)(col_lo + S.s_cl[u]));
         if (!VALS) continue;
         const int deg = S.s_deg[u];
-        const int32_t *ent = S.s_adj + 8 * u;
+        const int32_t *ent = S.s_adj + 9 * u;
         double x[8];
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
@@ -746,7 +747,7 @@ __device__ __forceinline__ void emit_tile(EmitSmem &S, const EmitArgs &A, int64_
     // Two records per thread per iteration: their KE gathers are independent and overlap.
     auto offdiag_value = [&](int u, uint32_t w) -> double {
         const int n = (int)(w & 7u);
-        const int32_t *ent = S.s_adj + 8 * u;
+        const int32_t *ent = S.s_adj + 9 * u;
         double x[MAX_OFFDIAG_CONTRIB];
 #pragma unroll
         for (int r = 0; r < MAX_OFFDIAG_CONTRIB; ++r) {
