@@ -1258,3 +1258,19 @@ def test_band_strip_order_bitwise():
     out = subprocess.run([sys.executable, "-c", _BAND_SCRIPT.format(root=root)], capture_output=True, text=True,
                          env={**os.environ, "HX_BAND_STRIP": "64"}, timeout=600)
     assert out.returncode == 0 and "band ok" in out.stdout, out.stderr[-2000:]
+
+
+@pytest.mark.parametrize("lo,hi", [(0, 1), (5, 8), (0, 63), (1, 66), (0, 9471), (3, 9476), (7, 10000), (0, 13824)])
+def test_persistent_integration_ranges_bitwise(lo, hi):
+    """The persistent integration kernel's quad scheduling (static first quads, then 16-quad claims
+    from the counter) on ranges around the quad, claim and first-wave boundaries (148 SMs x 16
+    warps x 4 elements = 9472): KE and iK/jK bitwise the oracle's for exactly the range."""
+    mesh = perturbed_mesh(24, seed=9)  # 13824 elements
+    ke_ref, rows_ref, cols_ref, _, _, _ = oracle.stiffness_mesh(mesh.coords, mesh.connectivity, mesh.coefficient)
+    dm = D.DeviceMesh.from_host(mesh)
+    ke, rows, cols, fail = D.integrate_mesh(dm, lo, hi)
+    torch.cuda.synchronize()
+    D.raise_if_failed(fail)
+    assert bits_equal(ke.cpu().numpy(), ke_ref[lo:hi])
+    assert np.array_equal(rows.cpu().numpy(), rows_ref[36 * lo:36 * hi])
+    assert np.array_equal(cols.cpu().numpy(), cols_ref[36 * lo:36 * hi])
