@@ -56,7 +56,7 @@ def parse():
     p.add_argument("--e2e-rows", choices=["i32", "i64"], default="i32",
                    help="row indices over PCIe: int32 widened on the host (default) or int64")
     p.add_argument("--no-cpu-baseline", action="store_true")
-    p.add_argument("--cpu-sample-layers", type=int, default=6)
+    p.add_argument("--cpu-sample-layers", type=int, default=16)  # ~5-6 s per sample pass at C4 (16 threads)
     return p.parse_args()
 
 
