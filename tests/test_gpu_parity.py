@@ -619,6 +619,27 @@ def test_c4_every_column_bitwise_against_oracle():
     assert all(all(r) for r in results), [i for i, r in enumerate(results) if not all(r)]
 
 
+def test_c4_streamed_run_build_bitwise_to_device_build():
+    """The e2e entry point at full size: run_build on C4 from pinned host memory (20 streamed column
+    blocks, sampled block plan checked on the device, delta-encoded row transfer decoded on the host)
+    returns exactly the single-GPU device build's CSC (which the test above pins to the oracle)."""
+    from paper_1501_04784_b200 import pipeline
+    from paper_1501_04784_b200.hostmem import pinned_mesh
+
+    mesh = make_workload("C4")
+    dm = D.DeviceMesh.from_host(mesh)
+    b = build_device(dm)
+    torch.cuda.synchronize()
+    cp, ri, vv = b.csc.col_ptr.cpu().numpy(), b.csc.row_idx.cpu().numpy(), b.csc.vals.cpu().numpy()
+    del b, dm
+    torch.cuda.empty_cache()
+    m, rep = run_build(pinned_mesh(mesh), budget_bytes=10**13)
+    st = pipeline.LAST_RUN_STATS
+    assert st.get("blocks", 0) >= 10 and st.get("row_codec_blocks", 0) > 0 and not st.get("sampled_plan_fallback")
+    assert np.array_equal(m.col_ptr, cp) and np.array_equal(m.row_idx, ri)
+    assert np.array_equal(m.vals.view(np.int64), vv.view(np.int64))
+
+
 def test_empty_and_single_element_meshes():
     """Edge sizes the reference accepts: zero elements (test_assemble.py:212-222 empty-triplet rule,
     stiffness_batch -> (0, 36), assemble_direct -> all-zero col_ptr; run_build rejects it through
