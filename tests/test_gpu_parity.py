@@ -635,7 +635,10 @@ def test_c4_streamed_run_build_bitwise_to_device_build():
     torch.cuda.empty_cache()
     m, rep = run_build(pinned_mesh(mesh), budget_bytes=10**13)
     st = pipeline.LAST_RUN_STATS
-    assert st.get("blocks", 0) >= 10 and st.get("row_codec_blocks", 0) > 0 and not st.get("sampled_plan_fallback")
+    from paper_1501_04784_b200.transfer import row_codec_enabled
+
+    assert st.get("blocks", 0) >= 10 and not st.get("sampled_plan_fallback")
+    assert (st.get("row_codec_blocks", 0) > 0) == row_codec_enabled()  # HX_ROW_CODEC=0: int32 rows
     assert np.array_equal(m.col_ptr, cp) and np.array_equal(m.row_idx, ri)
     assert np.array_equal(m.vals.view(np.int64), vv.view(np.int64))
 
