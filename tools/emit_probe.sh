@@ -1,0 +1,9 @@
+#!/bin/bash
+# ncu launch list of the emit kernel for the default library and each variant (C4 cold build)
+for lib in default paper_1501_04784_b200/_lib/variants/*.so; do
+  if [ "$lib" = default ]; then unset HEXFEM_B200_LIB; else export HEXFEM_B200_LIB=$lib; fi
+  n=$(basename $lib .so)
+  timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
+    -k regex:emit_kernel -c 2 --csv --log-file gpurun_out/ep_$n.csv python tools/profile_step.py C4 > /dev/null 2>&1
+  echo "== $n"; python tools/launches.py gpurun_out/ep_$n.csv | grep emit
+done
