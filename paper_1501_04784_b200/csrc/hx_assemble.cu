@@ -343,6 +343,17 @@ constexpr int SORT_SLOTS = 64;  // <= 8 elements x 7 other nodes = 56 contributi
 #ifndef HX_PATTERN_NET
 #define HX_PATTERN_NET 1
 #endif
+// Network tiers of the pattern pass (warp-uniform: the smallest tier that holds every lane's keys).
+// Interior columns of hex meshes hold exactly 28 keys, so the default tiers are 28 (the 32-key
+// odd-even network pruned to 28 wires: 162 instead of 191 compare-exchanges -- valid because the
+// pruned wires would hold +inf), 32 and 64; a 16-key tier costs instruction-cache room for the few
+// warps of boundary columns (C4 pattern 5.90 -> 5.78 ms, C5 unchanged; profiles/r02/pattern_net28_probe.txt).
+#ifndef HX_PATTERN_NET16
+#define HX_PATTERN_NET16 0
+#endif
+#ifndef HX_PATTERN_NET28
+#define HX_PATTERN_NET28 1
+#endif
 template <int N>
 struct OddEvenPairs {  // comparator list of the network, built at compile time
     static constexpr int count() {
@@ -450,7 +461,8 @@ __device__ __forceinline__ int column_pattern_sort(const SegTable &T, bool activ
         // distinct rows; a row with more than MAX_OFFDIAG_CONTRIB contributions leaves the fast path
         int rows = 0;
         bool ok = true;
-        if (!__any_sync(am, cnt > 16)) sort_count<16, K>(L, cnt, rows, ok);
+        if (HX_PATTERN_NET16 && !__any_sync(am, cnt > 16)) sort_count<16, K>(L, cnt, rows, ok);
+        else if (HX_PATTERN_NET28 && !__any_sync(am, cnt > 28)) sort_count<28, K>(L, cnt, rows, ok);
         else if (!__any_sync(am, cnt > 32)) sort_count<32, K>(L, cnt, rows, ok);
         else sort_count<64, K>(L, cnt, rows, ok);
         if (!ok || rows > MAXR) {
