@@ -234,8 +234,22 @@ __device__ __forceinline__ int64_t band_col(int64_t i64, int64_t ncols, const in
 __global__ void band_order_kernel(int64_t ncols, const uint32_t *__restrict__ order_flag,
                                   const int64_t *__restrict__ band, uint32_t *__restrict__ order) {
     if (*order_flag != 2u) return;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < ncols; i += (int64_t)gridDim.x * blockDim.x)
-        order[i] = (uint32_t)band_col(i, ncols, band);
+    // four positions per thread, one 16-byte store: inside a strip row consecutive positions map to
+    // consecutive columns, so the map is evaluated at the ends only (order is 256-byte aligned)
+    const int64_t n4 = ncols / 4;
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n4; q += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = 4 * q;
+        const uint32_t c0 = (uint32_t)band_col(i, ncols, band), c3 = (uint32_t)band_col(i + 3, ncols, band);
+        uint4 v;
+        if (c3 == c0 + 3u) {
+            v = make_uint4(c0, c0 + 1u, c0 + 2u, c3);
+        } else {
+            v = make_uint4(c0, (uint32_t)band_col(i + 1, ncols, band), (uint32_t)band_col(i + 2, ncols, band), c3);
+        }
+        reinterpret_cast<uint4 *>(order)[q] = v;
+    }
+    if (blockIdx.x == 0 && threadIdx.x < (unsigned)(ncols - 4 * n4))
+        order[4 * n4 + threadIdx.x] = (uint32_t)band_col(4 * n4 + threadIdx.x, ncols, band);
 }
 
 // Sorting network for 8 keys (19 compare-exchanges), padded with INT_MAX.
@@ -1202,7 +1216,7 @@ static int mesh_csc_build(const hx_elem_segment *segs, int32_t n_segs, int64_t n
         if (banded) {
             band_kernel<<<1, 256, 0, s>>>(T.conn[0], n_total, ncols, strip, w.order_flag, w.band);
             HX_CHECK_LAUNCH("band_kernel");
-            band_order_kernel<<<(unsigned)std::min<int64_t>(ceil_div(ncols, 256), 148 * 16), 256, 0, s>>>(
+            band_order_kernel<<<(unsigned)std::min<int64_t>(ceil_div(ceil_div(ncols, 4), 256), 148 * 16), 256, 0, s>>>(
                 ncols, w.order_flag, w.band, w.order);
             HX_CHECK_LAUNCH("band_order_kernel");
         }
