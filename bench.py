@@ -456,6 +456,10 @@ def run_ours(args):
             "ke_fast_mode": ({"kernel_ms": kernel["ke_fast_mode_ms"],
                               "achieved_gbs": ke_bytes_rank / (kernel["ke_fast_mode_ms"] / 1e3) / 1e9,
                               "frac": ke_bytes_rank / (kernel["ke_fast_mode_ms"] / 1e3) / 1e9 / peak,
+                              "fp64_pipe": {"instr_per_el": FP64_INSTR_PER_EL["fast"],
+                                            "frac": n_el_total / world * FP64_INSTR_PER_EL["fast"]
+                                            / (kernel["ke_fast_mode_ms"] / 1e3) / 1e12 / FP64_PEAK_T_INSTR},
+                              "bound": "LSU data pipe (~93%: the staged 8-way Gauss-point reduction); DESIGN.md 4.1",
                               "contract": "|dKE| <= 1e-12 max|KE row| (not bitwise); see DESIGN.md"}
                              if "ke_fast_mode_ms" in kernel else None),
             "gpu_launches": kernel["launches_per_step"] * args.steps,
