@@ -1298,3 +1298,30 @@ def test_persistent_integration_ranges_bitwise(lo, hi):
     assert bits_equal(ke.cpu().numpy(), ke_ref[lo:hi])
     assert np.array_equal(rows.cpu().numpy(), rows_ref[36 * lo:36 * hi])
     assert np.array_equal(cols.cpu().numpy(), cols_ref[36 * lo:36 * hi])
+
+
+@pytest.mark.parametrize("layout", ["reversed", "anisotropic"])
+def test_streamed_run_build_element_layouts(monkeypatch, layout):
+    """run_build's streamed path (sampled block plan checked on the device) on locally numbered meshes
+    whose element order runs backwards or whose box is far from a cube: bitwise the oracle's, and the
+    sampled plan holds (no fallback to the exact scan)."""
+    from paper_1501_04784_b200 import pipeline
+    from paper_1501_04784_b200.mesh import Mesh
+
+    monkeypatch.setattr(pipeline, "STREAM_MIN_ELEMENTS", 1)
+    monkeypatch.setattr(pipeline, "STREAM_BLOCKS", 4)
+    if layout == "reversed":
+        base = perturbed_mesh(22, seed=31)
+        mesh = Mesh(base.coords, np.ascontiguousarray(base.connectivity[::-1]), np.ascontiguousarray(base.coefficient[::-1]))
+    else:
+        from paper_1501_04784_b200.mesh import StructuredGridSpec, generate_cube_mesh
+
+        g = generate_cube_mesh(StructuredGridSpec(70, 9, 40))
+        rng = np.random.default_rng(32)
+        mesh = Mesh(g.coords + rng.uniform(-0.1, 0.1, g.coords.shape), g.connectivity,
+                    rng.uniform(0.5, 2.0, g.n_el))
+    ke, rows, cols, _, _, _ = oracle.stiffness_mesh(mesh.coords, mesh.connectivity, mesh.coefficient)
+    cp, ri, vv = oracle.triplet_to_csc(rows, cols, ke.reshape(-1), mesh.n_nodes)
+    m, _ = run_build(mesh, budget_bytes=10**12)
+    assert bits_equal(m.col_ptr, cp) and bits_equal(m.row_idx, ri) and bits_equal(m.vals, vv)
+    assert pipeline.LAST_RUN_STATS.get("blocks") == 4 and not pipeline.LAST_RUN_STATS.get("sampled_plan_fallback")
